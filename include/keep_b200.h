@@ -1,0 +1,199 @@
+/*
+ * keep_b200.h -- C ABI of the B200-native KEEP per-layer memory prefill.
+ *
+ * The drop-in boundary for the reference's hot path.
+ * Plain C types only (no torch, no C++ in the signatures); every entry point
+ * returns an int status (KEEP_OK or one of the error codes below, mirroring the
+ * reference's exception taxonomy, errors.hpp:8-26) and keep_last_error()
+ * returns the thread-local message of the last failure.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/proj):
+ *   keep_model_init            Model::init                  include/keep/model.hpp:54-73
+ *   keep_memory_put            CacheManager::put            include/keep/cache_manager.hpp:69-99
+ *   keep_memory_compute        EpisodeRuntime::compute_and_put (segment_prefill /
+ *                              joint full_prefill)          include/keep/harness.hpp:512-532
+ *   keep_load_memory           CacheManager::load           include/keep/cache_manager.hpp:103-130
+ *                              (paper: load_memory(memory_id, layer_id))
+ *   keep_memory_has_current    CacheManager::has_current    include/keep/cache_manager.hpp:151-159
+ *   keep_invalidate            CacheManager::invalidate     include/keep/cache_manager.hpp:163-184
+ *   keep_prefill_begin         PrefillCursor::PrefillCursor include/keep/prefill.hpp:174-217
+ *   keep_prefill_layer         PrefillCursor::step          include/keep/prefill.hpp:224-322
+ *                              (paper: prefill_layer(input, layer_id, kv))
+ *   keep_prefill_finish        PrefillCursor::finish        include/keep/prefill.hpp:324-337
+ *   keep_importance_evaluation converge                     include/keep/recompute.hpp:130-138
+ *                              (paper: importance_evaluation(...))
+ *   keep_plan_keep             plan_keep                    include/keep/recompute.hpp:140-180
+ *   keep_ratio_schedule        ratio_schedule               include/keep/recompute.hpp:33-70
+ *   keep_layer_budget          layer_budget                 include/keep/recompute.hpp:73-77
+ *   keep_logits                Model::logits                include/keep/model.hpp:76-85
+ *
+ * Threading: a context is single-threaded and stateful like the cursor and
+ * the cache manager it replaces; distinct contexts may be
+ * used from distinct threads.  All device work runs on the context's own
+ * CUDA streams; calls return after the work they report has completed.
+ *
+ * Numerics (keep_config.numerics):
+ *   KEEP_NUMERICS_PARITY  fp32 storage, fp64 accumulation in ascending k for
+ *                         every projection (tensor.hpp:31-41) and fp64
+ *                         attention / softmax / summaries: selections are
+ *                         bit-exact with the reference.
+ *   KEEP_NUMERICS_FAST    bf16 operands on the sm_100a tensor cores (tcgen05)
+ *                         with fp32 accumulation, fp32 residual stream, bf16
+ *                         merged KV, fp32 probabilities with fp64 summary
+ *                         reduction.  Selections agree with the reference
+ *                         except at near-ties; see DESIGN.md.
+ */
+#ifndef KEEP_B200_H
+#define KEEP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+enum {
+    KEEP_OK = 0,
+    KEEP_ERR_CONFIG = 1,     /* ConfigError    */
+    KEEP_ERR_INPUT = 2,      /* InputError     */
+    KEEP_ERR_PLAN = 3,       /* PlanError      */
+    KEEP_ERR_CACHE_MISS = 4, /* CacheMissError */
+    KEEP_ERR_TRACE = 5,      /* TraceError     */
+    KEEP_ERR_CUDA = 6,       /* CUDA / NCCL / out of memory */
+};
+
+enum { KEEP_NUMERICS_PARITY = 0, KEEP_NUMERICS_FAST = 1 };
+
+/* Memory owner (OwnerRef, memory_store.hpp:61-88): a dynamic segment owns
+ * per-segment blocks, a static group owns one joint block per layer. */
+enum { KEEP_OWNER_SEGMENT = 0, KEEP_OWNER_GROUP = 1 };
+/* Tiers: device HBM (fast) or pinned host DRAM (slow). */
+enum { KEEP_TIER_DEVICE = 0, KEEP_TIER_HOST = 1 };
+
+typedef struct {
+    int32_t num_layers, num_heads, model_dim, mlp_dim, vocab_size;
+    int32_t numerics;    /* KEEP_NUMERICS_* */
+    uint64_t seed;       /* ModelConfig::seed */
+    int32_t device;      /* CUDA ordinal */
+    int32_t world_size;  /* KV-head shards (1 = single GPU) */
+    int32_t rank;
+    int32_t reserved;
+} keep_config;
+
+typedef struct {
+    int32_t kind; /* KEEP_OWNER_* */
+    uint32_t id;
+} keep_owner;
+
+typedef struct {
+    int32_t num_segments;
+    int32_t num_units;            /* 0 => one dynamic unit per segment, owner s<position> */
+    const int32_t* seg_len;       /* [S] tokens per segment, >= 1 */
+    const int32_t* tokens;        /* [sum seg_len] concatenated in layout order */
+    const int32_t* unit_begin;    /* [num_units] first segment position of the unit */
+    const int32_t* unit_end;      /* [num_units] one past the last */
+    const keep_owner* unit_owner; /* [num_units] owner of the unit's cached KV */
+} keep_layout;
+
+/* Borrowed view of one (owner, layer) KV block: keys then values, each
+ * [tokens x d] row-major; element type fp32 (PARITY) or bf16 (FAST).  Device
+ * pointers, valid until the block is replaced or invalidated. */
+typedef struct {
+    void* keys;
+    void* values;
+    int64_t tokens;
+    int32_t tier;        /* tier the block was found in before the load */
+    int32_t elem_bytes;  /* 4 or 2 */
+    double load_ms;      /* measured H2D time of a slow-tier load (0 for fast hits) */
+} keep_kv_view;
+
+typedef struct {
+    uint64_t bytes_loaded_slow;
+    uint64_t cache_misses;
+    uint64_t tokens_invalidated;
+    uint64_t blocks;
+    uint64_t device_bytes;
+    uint64_t host_bytes;
+} keep_memory_stats;
+
+/* Per-run outputs of keep_plan_keep.  Any pointer may be NULL. */
+typedef struct {
+    uint8_t* plan;          /* [L*S] plan[l*S+i] = segment position i recomputed at layer l */
+    int32_t* orders;        /* [L*S] relevant_order of the walk after layer l */
+    int32_t* order_len;     /* [L] walk length, -1 when the layer kept every live segment */
+    int32_t* hops;          /* [L] ImportanceState::hop of that walk */
+    double* summaries;      /* [L*(S+S*S)] per layer qts then sts (prefill.hpp:76-80) */
+    float* final_hidden;    /* [T*d] (prefill.hpp:324-337) */
+    double* last_logits;    /* [V] Model::logits of the last row (model.hpp:76-85) */
+    int64_t* rows_per_layer;/* [L] N_act(l): recomputed rows (active segments + query) */
+    double* layer_ms;       /* [L] device time per layer (CUDA events) */
+    double ttft_ms;         /* device time begin -> last-row logits */
+} keep_plan_result;
+
+const char* keep_last_error(void);
+const char* keep_version(void);
+
+int keep_ctx_create(const keep_config* cfg, void** ctx_out);
+int keep_ctx_destroy(void* ctx);
+int keep_ctx_synchronize(void* ctx);
+
+/* Reference-identical counter-based weights generated on the device. */
+int keep_model_init(void* ctx);
+/* Copy the weights back in the reference layout (fp32; oracle/keep_oracle.h). */
+int keep_model_export(void* ctx, float* host_weights, uint64_t count);
+
+/* ---- memory tier: the load_memory surface ------------------------------ */
+int keep_memory_put(void* ctx, keep_owner owner, uint64_t version, int32_t layer,
+                    int64_t tokens, const float* keys, const float* values, int32_t tier);
+/* Canonical KV refresh on the GPU for every layer: one standalone prefill per
+ * segment (owner kind SEGMENT, n_members must be 1) or one joint prefill over
+ * the members (kind GROUP).  The result is stored under (owner, version). */
+int keep_memory_compute(void* ctx, keep_owner owner, uint64_t version, int32_t n_members,
+                        const int32_t* member_len, const int32_t* tokens, int32_t tier);
+/* Batched refresh of many owners in one set of launches (same semantics). */
+int keep_memory_compute_batch(void* ctx, int32_t n_owners, const keep_owner* owners,
+                              const uint64_t* versions, const int32_t* owner_members,
+                              const int32_t* member_len, const int32_t* tokens, int32_t tier);
+int keep_load_memory(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* out);
+int keep_memory_has_current(void* ctx, keep_owner owner, uint64_t version, int32_t* out);
+int keep_invalidate(void* ctx, keep_owner owner, uint64_t new_version, uint64_t tokens);
+int keep_memory_stats_get(void* ctx, keep_memory_stats* out);
+/* Copy one block back to the host as fp32 (tests). */
+int keep_memory_read(void* ctx, keep_owner owner, int32_t layer, float* keys, float* values);
+
+/* ---- prefill cursor: prefill_layer ------------------------------------- */
+int keep_prefill_begin(void* ctx, const keep_layout* layout, const int32_t* query,
+                       int32_t query_len);
+/* One layer.  active[S] host mask; summary_out (S+S*S doubles) may be NULL. */
+int keep_prefill_layer(void* ctx, const uint8_t* active, double* summary_out);
+/* final_hidden [T*d] fp32; kv_out per layer keys[T*d] then values[T*d] as
+ * fp32 (converted from bf16 in FAST).  Either may be NULL. */
+int keep_prefill_finish(void* ctx, float* final_hidden, float* kv_out);
+
+/* ---- selection ----------------------------------------------------------- */
+int keep_importance_evaluation(void* ctx, int32_t S, const double* qts, const double* sts,
+                               int64_t budget, const uint8_t* candidates, int32_t* order_out,
+                               int32_t* n_out, int32_t* hops_out);
+int keep_ratio_schedule(int32_t num_layers, double r_avg, double* r_out);
+int64_t keep_layer_budget(double ratio, int64_t num_segments);
+
+/* ---- the whole KEEP per-layer loop (plan_keep) on the device ------------ */
+int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query,
+                   int32_t query_len, const double* schedule, int32_t multihop,
+                   keep_plan_result* out);
+
+int keep_logits(void* ctx, const float* row, double* out);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KEEP_B200_H */

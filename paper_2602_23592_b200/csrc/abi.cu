@@ -1,0 +1,1079 @@
+// abi.cu -- the C ABI (include/keep_b200.h) and the host-side engine:
+// model weights, the two-tier memory store (load_memory), the prefill cursor
+// (prefill_layer), the device selector (importance_evaluation) and the
+// plan_keep per-layer loop.  C++ host code; all arithmetic runs in the sm_100a
+// kernels -- there is no CPU compute path.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "engine.hpp"
+
+using namespace keep_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return KEEP_OK;
+    } catch (const KeepError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host out of memory";
+        return KEEP_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return KEEP_ERR_CUDA;
+    }
+}
+
+Context* C(void* p) {
+    if (!p) raise(KEEP_ERR_CONFIG, "null context");
+    auto* c = static_cast<Context*>(p);
+    KEEP_CUDA(cudaSetDevice(c->cfg.device));
+    return c;
+}
+
+uint16_t f2bf(float x) {  // round-to-nearest-even (finite inputs)
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+float bf2f(uint16_t b) {
+    uint32_t u = uint32_t(b) << 16;
+    float x;
+    std::memcpy(&x, &u, 4);
+    return x;
+}
+
+// ------------------------------------------------------------------ buffers --
+}  // namespace
+
+namespace keep_b200 {
+
+void DevBuf::release() {
+    if (p) {
+        if (host) cudaFreeHost(p);
+        else cudaFree(p);
+    }
+    p = nullptr;
+    bytes = 0;
+}
+
+void DevBuf::ensure(size_t nbytes) {
+    if (nbytes <= bytes && p && !host) return;
+    release();
+    if (nbytes == 0) nbytes = 16;
+    if (cudaMalloc(&p, nbytes) != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        raise(KEEP_ERR_CUDA, "device out of memory allocating " + std::to_string(nbytes) + " bytes");
+    }
+    bytes = nbytes;
+    host = false;
+}
+
+void DevBuf::alloc(size_t nbytes, bool pinned_host) {
+    release();
+    if (nbytes == 0) nbytes = 16;
+    cudaError_t e = pinned_host ? cudaHostAlloc(&p, nbytes, cudaHostAllocDefault) : cudaMalloc(&p, nbytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        raise(KEEP_ERR_CUDA, std::string(pinned_host ? "pinned host" : "device") +
+                                 " allocation failed: " + std::to_string(nbytes) + " bytes");
+    }
+    bytes = nbytes;
+    host = pinned_host;
+}
+
+}  // namespace keep_b200
+
+namespace {
+
+template <typename T>
+void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
+    b.ensure(sizeof(T) * std::max<size_t>(v.size(), 1));
+    if (!v.empty()) KEEP_CUDA(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+}
+
+void check_cfg(const keep_config& c) {  // ModelConfig::validate, model.hpp:28-38
+    if (c.num_layers < 1) raise(KEEP_ERR_CONFIG, "num_layers must be positive");
+    if (c.num_heads < 1) raise(KEEP_ERR_CONFIG, "num_heads must be positive");
+    if (c.model_dim < 1) raise(KEEP_ERR_CONFIG, "model_dim must be positive");
+    if (c.mlp_dim < 1) raise(KEEP_ERR_CONFIG, "mlp_dim must be positive");
+    if (c.vocab_size < 1) raise(KEEP_ERR_CONFIG, "vocab_size must be positive");
+    if (c.model_dim % c.num_heads != 0) raise(KEEP_ERR_CONFIG, "model_dim not divisible by num_heads");
+    if (c.numerics != KEEP_NUMERICS_PARITY && c.numerics != KEEP_NUMERICS_FAST)
+        raise(KEEP_ERR_CONFIG, "unknown numerics mode");
+    if (c.model_dim % 4 != 0) raise(KEEP_ERR_CONFIG, "model_dim must be a multiple of 4");
+    if (c.model_dim / c.num_heads > 128) raise(KEEP_ERR_CONFIG, "head_dim > 128 not supported");
+    if (c.numerics == KEEP_NUMERICS_FAST && (c.model_dim % 64 != 0 || c.mlp_dim % 64 != 0))
+        raise(KEEP_ERR_CONFIG, "FAST numerics needs model_dim and mlp_dim multiples of 64");
+    if (c.world_size != 1) raise(KEEP_ERR_CONFIG, "head sharding: use one context per rank (world_size 1)");
+}
+
+// ------------------------------------------------------------ memory store --
+uint8_t* layer_keys(const Context& c, const Payload& p, int l) {
+    const int64_t sheet = p.arena->rows * c.d * c.elem;
+    return static_cast<uint8_t*>(p.arena->buf.p) + (int64_t(l) * 2) * sheet + p.row0 * c.d * c.elem;
+}
+uint8_t* layer_values(const Context& c, const Payload& p, int l) {
+    return layer_keys(c, p, l) + p.arena->rows * c.d * c.elem;
+}
+
+std::shared_ptr<Arena> make_arena(Context& c, int64_t rows, int tier) {
+    auto a = std::make_shared<Arena>();
+    a->rows = rows;
+    a->tier = tier;
+    a->buf.alloc(size_t(c.L) * 2 * rows * c.d * c.elem, tier == KEEP_TIER_HOST);
+    return a;
+}
+
+bool block_current(const Context& c, const OwnerKey& k, int layer, const Payload** out) {
+    auto it = c.store.find(k);
+    if (it == c.store.end()) return false;
+    auto cv = c.current_version.find(k);
+    if (cv == c.current_version.end()) return false;
+    if (layer < 0 || layer >= c.L) return false;
+    if (!it->second.present[layer] || it->second.layer_version[layer] != cv->second) return false;
+    if (out) *out = &it->second;
+    return true;
+}
+
+std::string owner_str(const OwnerKey& k) {
+    return (k.kind == KEEP_OWNER_SEGMENT ? "s" : "g") + std::to_string(k.id);
+}
+
+// ----------------------------------------------------------- weight access --
+void model_alloc_init(Context& c) {
+    const int L = c.L, d = c.d, f = c.f, V = c.V;
+    const double std_ = 1.0 / std::sqrt(double(d));  // model.hpp:56
+    cudaStream_t st = c.s_main;
+    c.embed.ensure(sizeof(float) * size_t(V) * d);
+    c.unembed.ensure(sizeof(float) * size_t(d) * V);
+    launch_init_tensor(c.cfg.seed, "embed", V, d, std_, c.embed.p, d, 0, false, st);
+    launch_init_tensor(c.cfg.seed, "unembed", d, V, std_, c.unembed.p, V, 0, false, st);
+    c.w.clear();
+    for (int i = 0; i < L * 4; ++i) c.w.emplace_back(new DevBuf());
+    char name[64];
+    for (int l = 0; l < L; ++l) {
+        auto nm = [&](const char* part) {
+            std::snprintf(name, sizeof name, "layer%d.%s", l, part);
+            return name;
+        };
+        if (!c.fast) {
+            c.w[l * 4 + W_QKV]->ensure(sizeof(float) * size_t(d) * 3 * d);
+            c.w[l * 4 + W_O]->ensure(sizeof(float) * size_t(d) * d);
+            c.w[l * 4 + W_IN]->ensure(sizeof(float) * size_t(d) * f);
+            c.w[l * 4 + W_OUT]->ensure(sizeof(float) * size_t(f) * d);
+            launch_init_tensor(c.cfg.seed, nm("wq"), d, d, std_, c.wslot(l, W_QKV), 3 * d, 0, false, st);
+            launch_init_tensor(c.cfg.seed, nm("wk"), d, d, std_, c.wslot(l, W_QKV), 3 * d, d, false, st);
+            launch_init_tensor(c.cfg.seed, nm("wv"), d, d, std_, c.wslot(l, W_QKV), 3 * d, 2 * d, false, st);
+            launch_init_tensor(c.cfg.seed, nm("wo"), d, d, std_, c.wslot(l, W_O), d, 0, false, st);
+            launch_init_tensor(c.cfg.seed, nm("mlp_in"), d, f, std_, c.wslot(l, W_IN), f, 0, false, st);
+            launch_init_tensor(c.cfg.seed, nm("mlp_out"), f, d, std_, c.wslot(l, W_OUT), d, 0, false, st);
+        } else {
+            const size_t b = sizeof(__nv_bfloat16);
+            c.w[l * 4 + W_QKV]->ensure(b * size_t(3 * d) * d);
+            c.w[l * 4 + W_O]->ensure(b * size_t(d) * d);
+            c.w[l * 4 + W_IN]->ensure(b * size_t(f) * d);
+            c.w[l * 4 + W_OUT]->ensure(b * size_t(d) * f);
+            launch_init_tensor(c.cfg.seed, nm("wq"), d, d, std_, c.wslot(l, W_QKV), d, 0, true, st);
+            launch_init_tensor(c.cfg.seed, nm("wk"), d, d, std_, c.wslot(l, W_QKV), d, d, true, st);
+            launch_init_tensor(c.cfg.seed, nm("wv"), d, d, std_, c.wslot(l, W_QKV), d, 2 * d, true, st);
+            launch_init_tensor(c.cfg.seed, nm("wo"), d, d, std_, c.wslot(l, W_O), d, 0, true, st);
+            launch_init_tensor(c.cfg.seed, nm("mlp_in"), d, f, std_, c.wslot(l, W_IN), d, 0, true, st);
+            launch_init_tensor(c.cfg.seed, nm("mlp_out"), f, d, std_, c.wslot(l, W_OUT), f, 0, true, st);
+        }
+    }
+    KEEP_CUDA(cudaStreamSynchronize(st));
+    c.weights_ready = true;
+}
+
+void need_weights(const Context& c) {
+    if (!c.weights_ready) raise(KEEP_ERR_CONFIG, "keep_model_init has not been called");
+}
+
+// ----------------------------------------------------------------- passes --
+// Segment-aligned key splits so that every (row, destination segment) bin is
+// produced by exactly one CTA (deterministic, no atomics).
+void plan_splits(Context& c, Pass& p) {
+    const int tiles = int(ceil_div(p.n, 16));
+    int nsplit = 1;
+    if (!p.block_diag) {
+        const int target = 4 * kNumSMs;
+        nsplit = int(std::min<int64_t>(ceil_div(target, tiles), std::max(1, p.T / 128)));
+        // bound the fp64 partial-context scratch to ~512 MB
+        const int64_t per_split = int64_t(p.n) * c.d * 8;
+        nsplit = int(std::max<int64_t>(1, std::min<int64_t>(nsplit, (512ll << 20) / std::max<int64_t>(per_split, 1))));
+    }
+    std::vector<int32_t> lo, hi;
+    if (nsplit == 1) {
+        lo.push_back(0);
+        hi.push_back(p.T);
+    } else {
+        // candidate cut points: segment starts and the query start
+        std::vector<int32_t> cuts;
+        for (int i = 0; i < p.S; ++i) cuts.push_back(p.seg_start[i]);
+        cuts.push_back(p.Tm);
+        int32_t prev = 0;
+        lo.push_back(0);
+        for (int k = 1; k < nsplit; ++k) {
+            const int64_t want = int64_t(k) * p.T / nsplit;
+            auto it = std::lower_bound(cuts.begin(), cuts.end(), int32_t(want));
+            if (it == cuts.end()) break;
+            if (*it <= prev) continue;
+            hi.push_back(*it);
+            lo.push_back(*it);
+            prev = *it;
+        }
+        hi.push_back(p.T);
+    }
+    upload(p.split_lo, lo, c.s_main);
+    upload(p.split_hi, hi, c.s_main);
+    const int ns = int(lo.size());
+    p.m_part.ensure(sizeof(double) * size_t(ns) * p.n * c.H);
+    p.l_part.ensure(sizeof(double) * size_t(ns) * p.n * c.H);
+    p.m_fin.ensure(sizeof(double) * size_t(p.n) * c.H);
+    p.l_fin.ensure(sizeof(double) * size_t(p.n) * c.H);
+    if (ns > 1) p.o_part.ensure(sizeof(double) * size_t(ns) * p.n * c.d);
+    p.split_count = ns;
+}
+
+void ensure_layer_scratch(Context& c, Pass& p) {
+    const size_t n = size_t(std::max(p.n, 1));
+    if (!c.fast) {
+        p.q.ensure(sizeof(float) * n * c.d);
+        p.ctx.ensure(sizeof(float) * n * c.d);
+        p.h.ensure(sizeof(float) * n * c.f);
+    } else {
+        p.q.ensure(2 * n * c.d);
+        p.ctxb.ensure(2 * n * c.d);
+        p.hb.ensure(2 * n * c.f);
+    }
+    if (p.with_summary) p.rowbin.ensure((c.fast ? 4 : 8) * n * std::max(p.S, 1));
+}
+
+// One transformer layer over the compact rows of a pass
+// (PrefillCursor::step body, prefill.hpp:245-304 minus the cached copy).
+void run_layer(Context& c, Pass& p, int l) {
+    const int n = p.n, d = c.d, f = c.f;
+    cudaStream_t st = c.s_main;
+    if (n == 0) return;
+    ensure_layer_scratch(c, p);
+    plan_splits(c, p);
+    const int32_t* rows = p.d_rows.as<int32_t>();
+    AttnArgs a{};
+    a.n = n;
+    a.T = p.T;
+    a.H = c.H;
+    a.dh = c.dh;
+    a.d = d;
+    a.k = p.kdst[l];
+    a.v = p.vdst[l];
+    a.rows = rows;
+    a.row_seg = p.d_row_seg.as<int32_t>();
+    a.key_lo = p.block_diag ? p.d_key_lo.as<int32_t>() : nullptr;
+    a.with_bins = p.with_summary;
+    a.S = p.S;
+    a.nsplit = p.split_count;
+    a.split_lo = p.split_lo.as<int32_t>();
+    a.split_hi = p.split_hi.as<int32_t>();
+    a.rows_per_tile = 16;
+    a.m_part = p.m_part.as<double>();
+    a.l_part = p.l_part.as<double>();
+    a.m_fin = p.m_fin.as<double>();
+    a.l_fin = p.l_fin.as<double>();
+    a.o_part = p.o_part.as<double>();
+    a.rowbin = p.rowbin.p;
+
+    if (!c.fast) {
+        EpiArgs e{EPI_QKV, d, p.q.as<float>(), d, p.kdst[l], p.vdst[l], rows, nullptr};
+        launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * d, n, 3 * d, d, e, st);
+        a.q = p.q.p;
+        a.ctx = p.ctx.as<float>();
+        launch_attention_parity(a, st);
+        EpiArgs eo{EPI_RESID, d, p.x.as<float>(), d, nullptr, nullptr, nullptr, nullptr};
+        launch_gemm_f64acc(p.ctx.as<float>(), d, static_cast<const float*>(c.wslot(l, W_O)), d, n, d, d, eo, st);
+        EpiArgs ei{EPI_RELU, d, p.h.as<float>(), f, nullptr, nullptr, nullptr, nullptr};
+        launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_IN)), f, n, f, d, ei, st);
+        launch_gemm_f64acc(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, n, d, f, eo, st);
+    } else {
+        auto* xb = p.xb.as<__nv_bfloat16>();
+        EpiArgs e{EPI_QKV, d, nullptr, d, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
+        launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_QKV)), d, n, 3 * d, d, e, st);
+        a.q = p.q.p;
+        a.ctx_bf16 = p.ctxb.as<__nv_bfloat16>();
+        launch_attention_fast(a, st);
+        EpiArgs eo{EPI_RESID, d, p.x.as<float>(), d, nullptr, nullptr, nullptr, xb};
+        launch_gemm_bf16(p.ctxb.as<__nv_bfloat16>(), d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_O)), d, n, d, d, eo, st);
+        EpiArgs ei{EPI_RELU, d, nullptr, f, nullptr, nullptr, nullptr, p.hb.as<__nv_bfloat16>()};
+        launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_IN)), d, n, f, d, ei, st);
+        launch_gemm_bf16(p.hb.as<__nv_bfloat16>(), f, static_cast<const __nv_bfloat16*>(c.wslot(l, W_OUT)), f, n, d, f, eo, st);
+    }
+    if (p.with_summary) {
+        // compact row range per segment (rows of a segment are contiguous)
+        std::vector<int32_t> cb(p.S, 0), ce(p.S, 0);
+        int qb = n, qe = n;
+        for (int i = 0; i < n;) {
+            const int sg = p.row_seg[p.rows_h[i]];
+            int j = i;
+            while (j < n && p.row_seg[p.rows_h[j]] == sg) ++j;
+            if (sg >= 0) {
+                cb[sg] = i;
+                ce[sg] = j;
+            } else {
+                qb = i;
+                qe = j;
+            }
+            i = j;
+        }
+        upload(p.seg_cbeg, cb, st);
+        upload(p.seg_cend, ce, st);
+        p.summ.ensure(sizeof(double) * (size_t(p.S) + size_t(p.S) * p.S));
+        if (!c.fast)
+            launch_summary_reduce<double>(p.rowbin.as<double>(), p.S, p.seg_cbeg.as<int32_t>(), p.seg_cend.as<int32_t>(),
+                                          p.d_seg_len.as<int32_t>(), qb, qe, p.qlen, p.summ.as<double>(), st);
+        else
+            launch_summary_reduce<float>(p.rowbin.as<float>(), p.S, p.seg_cbeg.as<int32_t>(), p.seg_cend.as<int32_t>(),
+                                         p.d_seg_len.as<int32_t>(), qb, qe, p.qlen, p.summ.as<double>(), st);
+    }
+}
+
+// Replace the compact row set (rows only shrink): gather the residual rows.
+void set_rows(Context& c, Pass& p, const std::vector<int32_t>& rows_new, bool first) {
+    cudaStream_t st = c.s_main;
+    const int n_new = int(rows_new.size());
+    if (!first) {
+        if (rows_new == p.rows_h) return;
+        std::vector<int32_t> idx(n_new);
+        size_t j = 0;
+        for (int i = 0; i < n_new; ++i) {
+            while (j < p.rows_h.size() && p.rows_h[j] != rows_new[i]) ++j;
+            if (j == p.rows_h.size()) raise(KEEP_ERR_PLAN, "internal: row set grew");
+            idx[i] = int32_t(j);
+        }
+        upload(p.d_idx, idx, st);
+        p.x_alt.ensure(sizeof(float) * size_t(std::max(n_new, 1)) * c.d);
+        launch_gather_rows(p.x.as<float>(), p.d_idx.as<int32_t>(), n_new, c.d, p.x_alt.as<float>(),
+                           c.fast ? p.xb.as<__nv_bfloat16>() : nullptr, st);
+        std::swap(p.x.p, p.x_alt.p);
+        std::swap(p.x.bytes, p.x_alt.bytes);
+    }
+    p.rows_h = rows_new;
+    p.n = n_new;
+    upload(p.d_rows, p.rows_h, st);
+}
+
+// Build a pass over a token sequence.  seg_len partitions the memory rows;
+// query rows follow.
+void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const int32_t* tokens,
+               const int32_t* query, int qlen) {
+    p.S = int(seg_len.size());
+    p.seg_len = seg_len;
+    p.seg_start.assign(p.S, 0);
+    int pos = 0;
+    for (int i = 0; i < p.S; ++i) {
+        p.seg_start[i] = pos;
+        pos += seg_len[i];
+    }
+    p.Tm = pos;
+    p.qlen = qlen;
+    p.T = pos + qlen;
+    p.row_seg.assign(p.T, -1);
+    for (int i = 0; i < p.S; ++i)
+        for (int t = 0; t < seg_len[i]; ++t) p.row_seg[p.seg_start[i] + t] = i;
+    std::vector<int32_t> toks(p.T);
+    std::copy(tokens, tokens + p.Tm, toks.begin());
+    for (int k = 0; k < qlen; ++k) toks[p.Tm + k] = query[k];
+    for (int32_t t : toks)
+        if (t < 0 || t >= c.V) raise(KEEP_ERR_INPUT, "token " + std::to_string(t) + " out of vocab range");
+    cudaStream_t st = c.s_main;
+    upload(p.d_tokens, toks, st);
+    upload(p.d_row_seg, p.row_seg, st);
+    upload(p.d_seg_len, p.seg_len, st);
+    std::vector<int32_t> all(p.T);
+    std::iota(all.begin(), all.end(), 0);
+    p.x.ensure(sizeof(float) * size_t(std::max(p.T, 1)) * c.d);
+    if (c.fast) p.xb.ensure(2 * size_t(std::max(p.T, 1)) * c.d);
+    set_rows(c, p, all, true);
+    launch_embed(c.embed.as<float>(), p.d_tokens.as<int32_t>(), p.d_rows.as<int32_t>(), p.T, c.d,
+                 p.x.as<float>(), st);
+    if (c.fast) launch_to_bf16(p.x.as<float>(), int64_t(p.T) * c.d, p.xb.as<__nv_bfloat16>(), st);
+    p.prev.assign(p.S, 1);
+    p.dropped.assign(p.S, 0);
+    p.layer = 0;
+}
+
+// ------------------------------------------------------------------ cursor --
+void cursor_layer(Context& c, const uint8_t* active, bool keep_summary) {
+    Pass& p = *c.pf;
+    const int S = p.S, l = p.layer;
+    if (l >= c.L) raise(KEEP_ERR_PLAN, "stepped past last layer");  // prefill.hpp:227
+    for (int i = 0; i < S; ++i)
+        if (active[i] && !p.prev[i]) raise(KEEP_ERR_PLAN, "plan is not monotone across layers");
+    // cached rows of this layer (prefill.hpp:255-263, 340-350): resolve first
+    std::vector<void*> ks, vs;
+    std::vector<int32_t> dr, nr;
+    int maxr = 0;
+    for (int i = 0; i < S; ++i) {
+        if (active[i]) continue;
+        const Payload* pl = nullptr;
+        const OwnerKey& ok = c.seg_owner[i];
+        if (!block_current(c, ok, l, &pl)) {
+            c.stats.cache_misses++;
+            raise(KEEP_ERR_CACHE_MISS, "missing cached KV for segment " + std::to_string(i) + " (owner " +
+                                           owner_str(ok) + ") layer " + std::to_string(l));
+        }
+        if (pl->arena->tier != KEEP_TIER_DEVICE)
+            raise(KEEP_ERR_CACHE_MISS, "owner " + owner_str(ok) + " is host-resident: load it first");
+        if (c.seg_owner_row[i] + p.seg_len[i] > pl->tokens)
+            raise(KEEP_ERR_INPUT, "cached block of " + owner_str(ok) + " is shorter than its members");
+        ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * c.d * c.elem);
+        vs.push_back(layer_values(c, *pl, l) + c.seg_owner_row[i] * c.d * c.elem);
+        dr.push_back(p.seg_start[i]);
+        nr.push_back(p.seg_len[i]);
+        maxr = std::max(maxr, p.seg_len[i]);
+    }
+    // newly dropped rows leave the compact set for good (prefill.hpp:233-239)
+    std::vector<int32_t> rows_new;
+    rows_new.reserve(p.n);
+    for (int32_t r : p.rows_h) {
+        const int sg = p.row_seg[r];
+        if (sg < 0 || active[sg]) rows_new.push_back(r);
+    }
+    for (int i = 0; i < S; ++i)
+        if (!active[i]) p.dropped[i] = 1;
+    set_rows(c, p, rows_new, false);
+    cudaStream_t st = c.s_main;
+    if (!ks.empty()) {
+        upload(c.d_ksrc, ks, st);
+        upload(c.d_vsrc, vs, st);
+        upload(c.d_cdst, dr, st);
+        upload(c.d_cn, nr, st);
+        launch_copy_cached(c.d_ksrc.as<const void*>(), c.d_vsrc.as<const void*>(), c.d_cdst.as<int32_t>(),
+                           c.d_cn.as<int32_t>(), int(ks.size()), int64_t(c.d) * c.elem, p.kdst[l], p.vdst[l],
+                           maxr, st);
+    }
+    p.with_summary = true;
+    run_layer(c, p, l);
+    if (p.n == 0) {  // no computed rows: the summary is all zero
+        p.summ.ensure(sizeof(double) * (size_t(S) + size_t(S) * S));
+        KEEP_CUDA(cudaMemsetAsync(p.summ.p, 0, sizeof(double) * (size_t(S) + size_t(S) * S), st));
+    }
+    (void)keep_summary;
+    std::copy(active, active + S, p.prev.begin());
+    p.layer++;
+}
+
+void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int qlen) {
+    need_weights(c);
+    if (!lay || lay->num_segments < 1) raise(KEEP_ERR_INPUT, "layout is empty");  // prefill.hpp:177
+    if (qlen < 0) raise(KEEP_ERR_INPUT, "negative query length");
+    const int S = lay->num_segments;
+    std::vector<int32_t> sl(lay->seg_len, lay->seg_len + S);
+    for (int x : sl)
+        if (x < 1) raise(KEEP_ERR_INPUT, "empty segment in layout");
+    // owners of the cached KV of each segment (units = static groups or segments)
+    c.seg_owner.assign(S, OwnerKey{KEEP_OWNER_SEGMENT, 0});
+    c.seg_owner_row.assign(S, 0);
+    if (lay->num_units == 0) {
+        for (int i = 0; i < S; ++i) c.seg_owner[i] = OwnerKey{KEEP_OWNER_SEGMENT, uint32_t(i)};
+    } else {
+        std::vector<int> covered(S, 0);
+        for (int u = 0; u < lay->num_units; ++u) {
+            const int b = lay->unit_begin[u], e = lay->unit_end[u];
+            if (b < 0 || e > S || b >= e) raise(KEEP_ERR_INPUT, "bad unit range");
+            int64_t off = 0;
+            for (int i = b; i < e; ++i) {
+                c.seg_owner[i] = OwnerKey{lay->unit_owner[u].kind, lay->unit_owner[u].id};
+                c.seg_owner_row[i] = off;
+                off += sl[i];
+                covered[i]++;
+            }
+        }
+        for (int i = 0; i < S; ++i)
+            if (covered[i] != 1) raise(KEEP_ERR_INPUT, "units must partition the layout");
+    }
+    c.pf.reset(new Pass());
+    Pass& p = *c.pf;
+    pass_init(c, p, sl, lay->tokens, query, qlen);
+    const size_t sheet = size_t(p.T) * c.d * c.elem;
+    c.kv.ensure(std::max<size_t>(size_t(c.L) * 2 * sheet, 16));
+    p.kdst.resize(c.L);
+    p.vdst.resize(c.L);
+    for (int l = 0; l < c.L; ++l) {
+        p.kdst[l] = static_cast<uint8_t*>(c.kv.p) + size_t(l) * 2 * sheet;
+        p.vdst[l] = static_cast<uint8_t*>(c.kv.p) + (size_t(l) * 2 + 1) * sheet;
+    }
+}
+
+// Row T-1 of the final hidden state (device pointer or nullptr if dropped).
+const float* last_row_ptr(const Context& c, const Pass& p) {
+    if (p.n > 0 && p.rows_h.back() == p.T - 1) return p.x.as<float>() + int64_t(p.n - 1) * c.d;
+    return nullptr;
+}
+
+void cursor_finish(Context& c, float* final_hidden, float* kv_out) {
+    Pass& p = *c.pf;
+    if (p.layer != c.L) raise(KEEP_ERR_PLAN, "cursor finished before the last layer");
+    KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+    const int d = c.d;
+    if (final_hidden) {
+        std::memset(final_hidden, 0, sizeof(float) * size_t(p.T) * d);
+        std::vector<float> xc(size_t(p.n) * d);
+        if (p.n) KEEP_CUDA(cudaMemcpy(xc.data(), p.x.p, sizeof(float) * xc.size(), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < p.n; ++i)
+            std::memcpy(final_hidden + size_t(p.rows_h[i]) * d, xc.data() + size_t(i) * d, sizeof(float) * d);
+    }
+    if (kv_out) {
+        const size_t nel = size_t(c.L) * 2 * p.T * d;
+        if (!c.fast) {
+            KEEP_CUDA(cudaMemcpy(kv_out, c.kv.p, sizeof(float) * nel, cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<uint16_t> tmp(nel);
+            KEEP_CUDA(cudaMemcpy(tmp.data(), c.kv.p, 2 * nel, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < nel; ++i) kv_out[i] = bf2f(tmp[i]);
+        }
+    }
+}
+
+// --------------------------------------------------- canonical KV refresh --
+// compute_and_put (harness.hpp:512-532) for a batch of owners: one pass over
+// all their rows with block-diagonal attention (each owner is its own causal
+// context: segment_prefill for a segment, joint full_prefill for a group).
+void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, const uint64_t* versions,
+                          const int32_t* owner_members, const int32_t* member_len, const int32_t* tokens,
+                          int tier) {
+    need_weights(c);
+    if (n_owners < 1) return;
+    if (tier != KEEP_TIER_DEVICE && tier != KEEP_TIER_HOST) raise(KEEP_ERR_CONFIG, "unknown tier");
+    std::vector<int32_t> seglen;  // one "segment" per owner (the owner's rows)
+    std::vector<int64_t> row0(n_owners);
+    int mi = 0;
+    int64_t rows = 0;
+    for (int o = 0; o < n_owners; ++o) {
+        if (owner_members[o] < 1) raise(KEEP_ERR_INPUT, "owner without members");
+        if (owners[o].kind == KEEP_OWNER_SEGMENT && owner_members[o] != 1)
+            raise(KEEP_ERR_INPUT, "a segment owner has exactly one member");
+        int32_t tot = 0;
+        for (int k = 0; k < owner_members[o]; ++k, ++mi) {
+            if (member_len[mi] < 1) raise(KEEP_ERR_INPUT, "segment is empty");
+            tot += member_len[mi];
+        }
+        row0[o] = rows;
+        rows += tot;
+        seglen.push_back(tot);
+    }
+    if (rows > INT32_MAX / 2) raise(KEEP_ERR_CONFIG, "refresh batch too large");
+    Pass p;
+    p.block_diag = true;
+    p.with_summary = false;
+    pass_init(c, p, seglen, tokens, nullptr, 0);
+    p.key_lo_h.resize(p.T);
+    for (int o = 0; o < n_owners; ++o)
+        for (int t = 0; t < seglen[o]; ++t) p.key_lo_h[row0[o] + t] = int32_t(row0[o]);
+    upload(p.d_key_lo, p.key_lo_h, c.s_main);
+    auto dev = make_arena(c, rows, KEEP_TIER_DEVICE);
+    const size_t sheet = size_t(rows) * c.d * c.elem;
+    p.kdst.resize(c.L);
+    p.vdst.resize(c.L);
+    for (int l = 0; l < c.L; ++l) {
+        p.kdst[l] = static_cast<uint8_t*>(dev->buf.p) + size_t(l) * 2 * sheet;
+        p.vdst[l] = static_cast<uint8_t*>(dev->buf.p) + (size_t(l) * 2 + 1) * sheet;
+    }
+    for (int l = 0; l < c.L; ++l) run_layer(c, p, l);
+    std::shared_ptr<Arena> arena = dev;
+    if (tier == KEEP_TIER_HOST) {
+        arena = make_arena(c, rows, KEEP_TIER_HOST);
+        KEEP_CUDA(cudaMemcpyAsync(arena->buf.p, dev->buf.p, size_t(c.L) * 2 * sheet, cudaMemcpyDeviceToHost, c.s_main));
+    }
+    KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+    for (int o = 0; o < n_owners; ++o) {
+        const OwnerKey k{owners[o].kind, owners[o].id};
+        auto& cur = c.current_version[k];
+        cur = std::max(cur, versions[o]);
+        Payload pl;
+        pl.arena = arena;
+        pl.row0 = row0[o];
+        pl.tokens = seglen[o];
+        pl.layer_version.assign(c.L, versions[o]);
+        pl.present.assign(c.L, 1);
+        c.store[k] = std::move(pl);
+    }
+}
+
+}  // namespace
+
+// =================================================================== C ABI ==
+extern "C" {
+
+const char* keep_last_error(void) { return g_err.c_str(); }
+const char* keep_version(void) { return "keep_b200 0.1 (sm_100a)"; }
+
+int keep_ctx_create(const keep_config* cfg, void** out) {
+    return guard([&] {
+        if (!cfg || !out) raise(KEEP_ERR_CONFIG, "null argument");
+        check_cfg(*cfg);
+        int ndev = 0;
+        KEEP_CUDA(cudaGetDeviceCount(&ndev));
+        if (cfg->device < 0 || cfg->device >= ndev) raise(KEEP_ERR_CONFIG, "no such CUDA device");
+        KEEP_CUDA(cudaSetDevice(cfg->device));
+        cudaDeviceProp prop{};
+        KEEP_CUDA(cudaGetDeviceProperties(&prop, cfg->device));
+        if (prop.major != 10) raise(KEEP_ERR_CONFIG, "keep_b200 requires an sm_100 (B200) device");
+        auto* c = new Context();
+        c->cfg = *cfg;
+        c->L = cfg->num_layers;
+        c->H = cfg->num_heads;
+        c->d = cfg->model_dim;
+        c->dh = c->d / c->H;
+        c->f = cfg->mlp_dim;
+        c->V = cfg->vocab_size;
+        c->fast = cfg->numerics == KEEP_NUMERICS_FAST;
+        c->elem = c->fast ? 2 : 4;
+        KEEP_CUDA(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
+        KEEP_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
+        KEEP_CUDA(cudaStreamCreateWithFlags(&c->s_sel, cudaStreamNonBlocking));
+        KEEP_CUDA(cudaEventCreate(&c->ev_a));
+        KEEP_CUDA(cudaEventCreate(&c->ev_b));
+        *out = c;
+    });
+}
+
+int keep_ctx_destroy(void* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        Context* c = C(ctx);
+        cudaDeviceSynchronize();
+        c->pf.reset();
+        c->store.clear();
+        cudaStreamDestroy(c->s_main);
+        cudaStreamDestroy(c->s_copy);
+        cudaStreamDestroy(c->s_sel);
+        cudaEventDestroy(c->ev_a);
+        cudaEventDestroy(c->ev_b);
+        delete c;
+    });
+}
+
+int keep_ctx_synchronize(void* ctx) {
+    return guard([&] { KEEP_CUDA(cudaStreamSynchronize(C(ctx)->s_main)); });
+}
+
+int keep_model_init(void* ctx) {
+    return guard([&] { model_alloc_init(*C(ctx)); });
+}
+
+int keep_model_export(void* ctx, float* hw, uint64_t count) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        const int64_t d = c.d, f = c.f, V = c.V;
+        const uint64_t need = 2ull * V * d + uint64_t(c.L) * (4ull * d * d + 2ull * d * f);
+        if (count < need) raise(KEEP_ERR_INPUT, "export buffer too small");
+        const double std_ = 1.0 / std::sqrt(double(d));
+        DevBuf tmp;
+        tmp.ensure(sizeof(float) * size_t(std::max(V * d, std::max(d * f, d * d))));
+        float* o = hw;
+        auto one = [&](const char* name, int64_t r, int64_t cols) {
+            launch_init_tensor(c.cfg.seed, name, r, cols, std_, tmp.p, cols, 0, false, c.s_main);
+            KEEP_CUDA(cudaMemcpyAsync(o, tmp.p, sizeof(float) * r * cols, cudaMemcpyDeviceToHost, c.s_main));
+            KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+            o += r * cols;
+        };
+        one("embed", V, d);
+        one("unembed", d, V);
+        char nm[64];
+        const char* parts[6] = {"wq", "wk", "wv", "wo", "mlp_in", "mlp_out"};
+        for (int l = 0; l < c.L; ++l)
+            for (int k = 0; k < 6; ++k) {
+                std::snprintf(nm, sizeof nm, "layer%d.%s", l, parts[k]);
+                one(nm, k == 5 ? f : d, k == 4 ? f : d);
+            }
+    });
+}
+
+int keep_memory_put(void* ctx, keep_owner owner, uint64_t version, int32_t layer, int64_t tokens,
+                    const float* keys, const float* values, int32_t tier) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        if (layer < 0 || layer >= c.L) raise(KEEP_ERR_INPUT, "layer out of range");
+        if (tokens < 1) raise(KEEP_ERR_INPUT, "empty block");
+        if (tier != KEEP_TIER_DEVICE && tier != KEEP_TIER_HOST) raise(KEEP_ERR_CONFIG, "unknown tier");
+        const OwnerKey k{owner.kind, owner.id};
+        auto& cur = c.current_version[k];
+        cur = std::max(cur, version);  // cache_manager.hpp:80-81
+        auto it = c.store.find(k);
+        if (it == c.store.end() || it->second.tokens != tokens || it->second.arena->tier != tier ||
+            it->second.arena.use_count() > 1) {
+            Payload pl;
+            if (it != c.store.end() && it->second.tokens == tokens && it->second.arena->tier == tier) {
+                // keep the other layers of a shared arena by copying them out
+                pl.arena = make_arena(c, tokens, tier);
+                pl.tokens = tokens;
+                pl.layer_version = it->second.layer_version;
+                pl.present = it->second.present;
+                const size_t blk = size_t(tokens) * c.d * c.elem;
+                for (int l = 0; l < c.L; ++l) {
+                    if (!pl.present[l]) continue;
+                    KEEP_CUDA(cudaMemcpy(layer_keys(c, pl, l), layer_keys(c, it->second, l), blk, cudaMemcpyDefault));
+                    KEEP_CUDA(cudaMemcpy(layer_values(c, pl, l), layer_values(c, it->second, l), blk, cudaMemcpyDefault));
+                }
+            } else {
+                pl.arena = make_arena(c, tokens, tier);
+                pl.tokens = tokens;
+                pl.layer_version.assign(c.L, 0);
+                pl.present.assign(c.L, 0);
+            }
+            c.store[k] = std::move(pl);
+        }
+        Payload& pl = c.store[k];
+        const size_t nel = size_t(tokens) * c.d;
+        if (!c.fast) {
+            KEEP_CUDA(cudaMemcpy(layer_keys(c, pl, layer), keys, 4 * nel, cudaMemcpyDefault));
+            KEEP_CUDA(cudaMemcpy(layer_values(c, pl, layer), values, 4 * nel, cudaMemcpyDefault));
+        } else {
+            std::vector<uint16_t> tk(nel), tv(nel);
+            for (size_t i = 0; i < nel; ++i) {
+                tk[i] = f2bf(keys[i]);
+                tv[i] = f2bf(values[i]);
+            }
+            KEEP_CUDA(cudaMemcpy(layer_keys(c, pl, layer), tk.data(), 2 * nel, cudaMemcpyDefault));
+            KEEP_CUDA(cudaMemcpy(layer_values(c, pl, layer), tv.data(), 2 * nel, cudaMemcpyDefault));
+        }
+        pl.layer_version[layer] = version;
+        pl.present[layer] = 1;
+    });
+}
+
+int keep_memory_compute(void* ctx, keep_owner owner, uint64_t version, int32_t n_members,
+                        const int32_t* member_len, const int32_t* tokens, int32_t tier) {
+    return guard([&] {
+        memory_compute_batch(*C(ctx), 1, &owner, &version, &n_members, member_len, tokens, tier);
+    });
+}
+
+int keep_memory_compute_batch(void* ctx, int32_t n_owners, const keep_owner* owners, const uint64_t* versions,
+                              const int32_t* owner_members, const int32_t* member_len, const int32_t* tokens,
+                              int32_t tier) {
+    return guard([&] {
+        memory_compute_batch(*C(ctx), n_owners, owners, versions, owner_members, member_len, tokens, tier);
+    });
+}
+
+int keep_load_memory(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* out) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        const OwnerKey k{owner.kind, owner.id};
+        const Payload* pl = nullptr;
+        if (!block_current(c, k, layer, &pl)) {  // cache_manager.hpp:104-116
+            c.stats.cache_misses++;
+            const bool absent = c.store.find(k) == c.store.end();
+            raise(KEEP_ERR_CACHE_MISS, std::string(absent ? "no block for " : "stale block for ") + owner_str(k) +
+                                           " layer " + std::to_string(layer));
+        }
+        Payload& P = c.store[k];
+        out->tokens = P.tokens;
+        out->elem_bytes = c.elem;
+        out->tier = P.arena->tier;
+        out->load_ms = 0.0;
+        if (P.arena->tier == KEEP_TIER_HOST) {
+            // slow tier: copy the block to HBM and promote the owner (117-127)
+            const size_t blk = size_t(P.tokens) * c.d * c.elem;
+            auto dev = make_arena(c, P.tokens, KEEP_TIER_DEVICE);
+            Payload np;
+            np.arena = dev;
+            np.tokens = P.tokens;
+            np.layer_version = P.layer_version;
+            np.present = P.present;
+            KEEP_CUDA(cudaEventRecord(c.ev_a, c.s_copy));
+            for (int l = 0; l < c.L; ++l) {
+                if (!np.present[l]) continue;
+                KEEP_CUDA(cudaMemcpyAsync(layer_keys(c, np, l), layer_keys(c, P, l), blk, cudaMemcpyHostToDevice, c.s_copy));
+                KEEP_CUDA(cudaMemcpyAsync(layer_values(c, np, l), layer_values(c, P, l), blk, cudaMemcpyHostToDevice, c.s_copy));
+                c.stats.bytes_loaded_slow += 2 * blk;
+            }
+            KEEP_CUDA(cudaEventRecord(c.ev_b, c.s_copy));
+            KEEP_CUDA(cudaEventSynchronize(c.ev_b));
+            float ms = 0.f;
+            KEEP_CUDA(cudaEventElapsedTime(&ms, c.ev_a, c.ev_b));
+            out->load_ms = ms;
+            c.store[k] = std::move(np);
+        }
+        const Payload& Q = c.store[k];
+        out->keys = layer_keys(c, Q, layer);
+        out->values = layer_values(c, Q, layer);
+    });
+}
+
+int keep_memory_has_current(void* ctx, keep_owner owner, uint64_t version, int32_t* out) {
+    return guard([&] {  // cache_manager.hpp:151-159
+        Context& c = *C(ctx);
+        const OwnerKey k{owner.kind, owner.id};
+        *out = 0;
+        auto cv = c.current_version.find(k);
+        if (cv != c.current_version.end() && cv->second > version) return;
+        auto it = c.store.find(k);
+        if (it == c.store.end()) return;
+        for (int l = 0; l < c.L; ++l)
+            if (!it->second.present[l] || it->second.layer_version[l] != version) return;
+        *out = 1;
+    });
+}
+
+int keep_invalidate(void* ctx, keep_owner owner, uint64_t new_version, uint64_t tokens) {
+    return guard([&] {  // cache_manager.hpp:163-184
+        Context& c = *C(ctx);
+        const OwnerKey k{owner.kind, owner.id};
+        auto it = c.store.find(k);
+        if (it != c.store.end()) {
+            c.store.erase(it);
+            c.stats.tokens_invalidated += tokens;
+        }
+        auto& cur = c.current_version[k];
+        cur = std::max(cur, new_version);
+    });
+}
+
+int keep_memory_stats_get(void* ctx, keep_memory_stats* out) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        keep_memory_stats s = c.stats;
+        s.blocks = 0;
+        s.device_bytes = s.host_bytes = 0;
+        std::vector<const Arena*> seen;
+        for (const auto& [k, p] : c.store) {
+            for (int l = 0; l < c.L; ++l) s.blocks += p.present[l];
+            const Arena* a = p.arena.get();
+            if (std::find(seen.begin(), seen.end(), a) != seen.end()) continue;
+            seen.push_back(a);
+            (a->tier == KEEP_TIER_HOST ? s.host_bytes : s.device_bytes) += a->buf.bytes;
+        }
+        *out = s;
+    });
+}
+
+int keep_memory_read(void* ctx, keep_owner owner, int32_t layer, float* keys, float* values) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        const Payload* pl = nullptr;
+        if (!block_current(c, OwnerKey{owner.kind, owner.id}, layer, &pl))
+            raise(KEEP_ERR_CACHE_MISS, "no current block");
+        const size_t nel = size_t(pl->tokens) * c.d;
+        if (!c.fast) {
+            KEEP_CUDA(cudaMemcpy(keys, layer_keys(c, *pl, layer), 4 * nel, cudaMemcpyDefault));
+            KEEP_CUDA(cudaMemcpy(values, layer_values(c, *pl, layer), 4 * nel, cudaMemcpyDefault));
+        } else {
+            std::vector<uint16_t> t(nel);
+            KEEP_CUDA(cudaMemcpy(t.data(), layer_keys(c, *pl, layer), 2 * nel, cudaMemcpyDefault));
+            for (size_t i = 0; i < nel; ++i) keys[i] = bf2f(t[i]);
+            KEEP_CUDA(cudaMemcpy(t.data(), layer_values(c, *pl, layer), 2 * nel, cudaMemcpyDefault));
+            for (size_t i = 0; i < nel; ++i) values[i] = bf2f(t[i]);
+        }
+    });
+}
+
+int keep_prefill_begin(void* ctx, const keep_layout* layout, const int32_t* query, int32_t qlen) {
+    return guard([&] { cursor_begin(*C(ctx), layout, query, qlen); });
+}
+
+int keep_prefill_layer(void* ctx, const uint8_t* active, double* summary_out) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        if (!c.pf) raise(KEEP_ERR_PLAN, "no prefill in progress");
+        cursor_layer(c, active, summary_out != nullptr);
+        if (summary_out) {
+            const size_t ns = size_t(c.pf->S) + size_t(c.pf->S) * c.pf->S;
+            KEEP_CUDA(cudaMemcpyAsync(summary_out, c.pf->summ.p, sizeof(double) * ns, cudaMemcpyDeviceToHost, c.s_main));
+        }
+        KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+    });
+}
+
+int keep_prefill_finish(void* ctx, float* final_hidden, float* kv_out) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        if (!c.pf) raise(KEEP_ERR_PLAN, "no prefill in progress");
+        cursor_finish(c, final_hidden, kv_out);
+    });
+}
+
+int keep_importance_evaluation(void* ctx, int32_t S, const double* qts, const double* sts, int64_t budget,
+                               const uint8_t* candidates, int32_t* order_out, int32_t* n_out, int32_t* hops_out) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        if (S < 0) raise(KEEP_ERR_INPUT, "negative segment count");
+        DevBuf dq, ds, dc;
+        cudaStream_t st = c.s_sel;
+        dq.ensure(sizeof(double) * std::max(S, 1));
+        ds.ensure(sizeof(double) * std::max<size_t>(size_t(S) * S, 1));
+        KEEP_CUDA(cudaMemcpyAsync(dq.p, qts, sizeof(double) * S, cudaMemcpyHostToDevice, st));
+        KEEP_CUDA(cudaMemcpyAsync(ds.p, sts, sizeof(double) * size_t(S) * S, cudaMemcpyHostToDevice, st));
+        if (candidates) {
+            dc.ensure(std::max(S, 1));
+            KEEP_CUDA(cudaMemcpyAsync(dc.p, candidates, S, cudaMemcpyHostToDevice, st));
+        }
+        c.sel_order.ensure(sizeof(int32_t) * (std::max(S, 1) + 2));
+        int32_t* o = c.sel_order.as<int32_t>();
+        launch_select(S, dq.as<double>(), ds.as<double>(), budget, candidates ? dc.as<uint8_t>() : nullptr, o + 2,
+                      o, o + 1, st);
+        std::vector<int32_t> h(S + 2);
+        KEEP_CUDA(cudaMemcpyAsync(h.data(), o, sizeof(int32_t) * (S + 2), cudaMemcpyDeviceToHost, st));
+        KEEP_CUDA(cudaStreamSynchronize(st));
+        *n_out = h[0];
+        *hops_out = h[1];
+        std::copy(h.begin() + 2, h.begin() + 2 + h[0], order_out);
+    });
+}
+
+int keep_ratio_schedule(int32_t L, double r_avg, double* r) {
+    return guard([&] {  // recompute.hpp:33-70
+        if (L < 1) raise(KEEP_ERR_CONFIG, "num_layers must be >= 1");
+        if (L == 1) {
+            r[0] = 1.0;
+            return;
+        }
+        if (r_avg < 1.0 / L - 1e-9 || r_avg > 1.0 + 1e-9) raise(KEEP_ERR_CONFIG, "infeasible r_avg " + std::to_string(r_avg));
+        double lo = 0.0, hi = 1.0;
+        for (int it = 0; it < 200; ++it) {
+            const double g = 0.5 * (lo + hi);
+            double sum = 0.0, term = 1.0;
+            for (int l = 0; l < L; ++l) {
+                sum += term;
+                term *= g;
+            }
+            if (sum / L < r_avg) lo = g;
+            else hi = g;
+        }
+        const double g = 0.5 * (lo + hi);
+        double term = 1.0;
+        for (int l = 0; l < L; ++l) {
+            r[l] = term;
+            term *= g;
+        }
+        r[0] = 1.0;
+    });
+}
+
+int64_t keep_layer_budget(double ratio, int64_t S) {  // recompute.hpp:73-77
+    int64_t b = int64_t(std::ceil(ratio * double(S) - 1e-9));
+    b = std::min(b, S);
+    return std::max<int64_t>(1, b);
+}
+
+int keep_logits(void* ctx, const float* row, double* out) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        need_weights(c);
+        DevBuf dr;
+        dr.ensure(sizeof(float) * c.d);
+        c.logits.ensure(sizeof(double) * c.V);
+        KEEP_CUDA(cudaMemcpyAsync(dr.p, row, sizeof(float) * c.d, cudaMemcpyHostToDevice, c.s_main));
+        launch_logits(dr.as<float>(), c.unembed.as<float>(), c.d, c.V, c.logits.as<double>(), c.s_main);
+        KEEP_CUDA(cudaMemcpyAsync(out, c.logits.p, sizeof(double) * c.V, cudaMemcpyDeviceToHost, c.s_main));
+        KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+    });
+}
+
+// plan_keep (recompute.hpp:140-180) with every layer, the selection and the
+// last-row logits on the device.  The host only decides keep-all vs walk from
+// the budget and applies the returned order (one small D2H per layer).
+int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, int32_t qlen,
+                   const double* sched, int32_t multihop, keep_plan_result* out) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        cudaStream_t st = c.s_main;
+        std::vector<cudaEvent_t> evs(c.L + 1);
+        for (auto& e : evs) KEEP_CUDA(cudaEventCreate(&e));
+        struct EvGuard {
+            std::vector<cudaEvent_t>& v;
+            ~EvGuard() {
+                for (auto e : v) cudaEventDestroy(e);
+            }
+        } evg{evs};
+        KEEP_CUDA(cudaEventRecord(evs[0], st));
+        cursor_begin(c, layout, query, qlen);
+        Pass& p = *c.pf;
+        const int S = p.S, L = c.L;
+        std::vector<uint8_t> active(S, 1);
+        c.sel_order.ensure(sizeof(int32_t) * (S + 2));
+        c.sel_cand.ensure(std::max(S, 1));
+        std::vector<int32_t> hbuf(S + 2);
+        for (int l = 0; l < L; ++l) {
+            if (out && out->plan) std::copy(active.begin(), active.end(), out->plan + size_t(l) * S);
+            if (out && out->order_len) out->order_len[l] = -1;
+            if (out && out->hops) out->hops[l] = 0;
+            cursor_layer(c, active.data(), true);
+            if (out && out->rows_per_layer) out->rows_per_layer[l] = p.n;
+            if (out && out->summaries)
+                KEEP_CUDA(cudaMemcpyAsync(out->summaries + size_t(l) * (S + size_t(S) * S), p.summ.p,
+                                          sizeof(double) * (S + size_t(S) * S), cudaMemcpyDeviceToHost, st));
+            KEEP_CUDA(cudaEventRecord(evs[l + 1], st));
+            if (l + 1 >= L) break;
+            const int64_t budget = keep_layer_budget(sched[l + 1], S);
+            int64_t live = 0;
+            for (uint8_t a : active) live += a;
+            if (budget >= live) continue;  // recompute everything still live
+            std::vector<uint8_t> next(S, 0);
+            if (multihop) {
+                KEEP_CUDA(cudaMemcpyAsync(c.sel_cand.p, active.data(), S, cudaMemcpyHostToDevice, st));
+                int32_t* o = c.sel_order.as<int32_t>();
+                launch_select(S, p.summ.as<double>(), p.summ.as<double>() + S, budget, c.sel_cand.as<uint8_t>(), o + 2, o,
+                              o + 1, st);
+                KEEP_CUDA(cudaMemcpyAsync(hbuf.data(), o, sizeof(int32_t) * (S + 2), cudaMemcpyDeviceToHost, st));
+                KEEP_CUDA(cudaStreamSynchronize(st));
+                for (int k = 0; k < hbuf[0]; ++k) next[hbuf[2 + k]] = 1;
+                if (out && out->orders) std::copy(hbuf.begin() + 2, hbuf.begin() + 2 + hbuf[0], out->orders + size_t(l) * S);
+                if (out && out->order_len) out->order_len[l] = hbuf[0];
+                if (out && out->hops) out->hops[l] = hbuf[1];
+            } else {  // single-hop ablation (recompute.hpp:166-176)
+                std::vector<double> qts(S);
+                KEEP_CUDA(cudaMemcpyAsync(qts.data(), p.summ.p, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+                KEEP_CUDA(cudaStreamSynchronize(st));
+                std::vector<int> ord;
+                for (int i = 0; i < S; ++i)
+                    if (active[i]) ord.push_back(i);
+                std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return qts[a] > qts[b]; });
+                for (size_t i = 0; i < size_t(budget) && i < ord.size(); ++i) next[ord[i]] = 1;
+            }
+            active = std::move(next);
+        }
+        // last-row logits (model.hpp:76-85) close the TTFT
+        c.logits.ensure(sizeof(double) * c.V);
+        const float* lr = last_row_ptr(c, p);
+        DevBuf zero;
+        if (!lr) {
+            zero.ensure(sizeof(float) * c.d);
+            KEEP_CUDA(cudaMemsetAsync(zero.p, 0, sizeof(float) * c.d, st));
+            lr = zero.as<float>();
+        }
+        launch_logits(lr, c.unembed.as<float>(), c.d, c.V, c.logits.as<double>(), st);
+        KEEP_CUDA(cudaEventRecord(c.ev_b, st));
+        if (out && out->last_logits)
+            KEEP_CUDA(cudaMemcpyAsync(out->last_logits, c.logits.p, sizeof(double) * c.V, cudaMemcpyDeviceToHost, st));
+        KEEP_CUDA(cudaStreamSynchronize(st));
+        if (out) {
+            float ms = 0.f;
+            KEEP_CUDA(cudaEventElapsedTime(&ms, evs[0], c.ev_b));
+            out->ttft_ms = ms;
+            if (out->layer_ms)
+                for (int l = 0; l < L; ++l) {
+                    float m = 0.f;
+                    KEEP_CUDA(cudaEventElapsedTime(&m, evs[l], evs[l + 1]));
+                    out->layer_ms[l] = m;
+                }
+            if (out->final_hidden) cursor_finish(c, out->final_hidden, nullptr);
+        }
+    });
+}
+
+}  // extern "C"

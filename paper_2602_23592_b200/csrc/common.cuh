@@ -1,0 +1,43 @@
+// common.cuh -- shared definitions for the KEEP B200 library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "keep_b200.h"
+
+namespace keep_b200 {
+
+// Error taxonomy of the reference (errors.hpp:8-26) plus device failures.
+struct KeepError : std::runtime_error {
+    int code;
+    KeepError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+inline void raise(int code, const std::string& msg) { throw KeepError(code, msg); }
+
+#define KEEP_CUDA(expr)                                                                  \
+    do {                                                                                 \
+        cudaError_t e_ = (expr);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            ::keep_b200::raise(KEEP_ERR_CUDA, std::string(#expr) + ": " +               \
+                                                  cudaGetErrorString(e_));               \
+    } while (0)
+
+#define KEEP_LAUNCH_CHECK() KEEP_CUDA(cudaGetLastError())
+
+constexpr int kNumSMs = 148;
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------- layouts --
+// Device weight layouts (one context holds exactly one of them):
+//  PARITY: fp32 row-major [K x N] exactly as the reference Mat (x . W),
+//          with the three projections fused column-wise: wqkv [d x 3d].
+//  FAST:   bf16 transposed [N x K] (K-major rows = the tcgen05 B operand),
+//          wqkv_t [3d x d], wo_t [d x d], win_t [f x d], wout_t [d x f].
+enum WeightSlot { W_QKV = 0, W_O = 1, W_IN = 2, W_OUT = 3 };
+
+}  // namespace keep_b200

@@ -1,0 +1,107 @@
+// engine.hpp -- the B200 KEEP prefill engine behind the C ABI (internal).
+#pragma once
+
+#include <map>
+#include <memory>
+#include <vector>
+
+#include "kernels.hpp"
+
+namespace keep_b200 {
+
+// FAST-mode projection GEMM on the tcgen05 tensor cores:
+// C[M x N] = A[M x K] (bf16 row-major) . Bt[N x K]^T (bf16, K-major rows).
+void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb,
+                      int M, int N, int K, const EpiArgs& epi, cudaStream_t st);
+
+// Device buffer with RAII.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    bool host = false;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release();
+    void ensure(size_t nbytes);              // device, grow-only
+    void alloc(size_t nbytes, bool pinned_host);
+    template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+// A KV arena: per layer, keys [rows x d] then values [rows x d].  Owner
+// payloads are row ranges of an arena (a batch of canonical refreshes writes
+// its merged KV straight into the arena -- no staging copy).
+struct Arena {
+    DevBuf buf;
+    int64_t rows = 0;
+    int tier = KEEP_TIER_DEVICE;
+    int refs = 0;
+};
+
+struct OwnerKey {
+    int kind;
+    uint32_t id;
+    bool operator<(const OwnerKey& o) const { return kind != o.kind ? kind < o.kind : id < o.id; }
+};
+
+struct Payload {
+    std::shared_ptr<Arena> arena;
+    int64_t row0 = 0, tokens = 0;
+    std::vector<uint64_t> layer_version;  // per layer; 0 = absent
+    std::vector<uint8_t> present;
+};
+
+// One prefill over a row space [0, T): the selective cursor (memory rows +
+// query) or a batched canonical refresh (block-diagonal attention).
+struct Pass {
+    int T = 0, Tm = 0, qlen = 0, S = 0;
+    bool with_summary = true;
+    bool block_diag = false;
+    std::vector<int32_t> seg_start, seg_len, row_seg;  // host copies
+    std::vector<int32_t> key_lo_h;
+    DevBuf d_tokens, d_row_seg, d_key_lo, d_seg_len;
+    // compact state
+    std::vector<int32_t> rows_h;  // compact -> global row, ascending
+    int n = 0;
+    DevBuf d_rows, d_rows_tmp, d_idx;
+    DevBuf x, x_alt, xb, q, ctx, ctxb, h, hb;
+    // attention scratch
+    DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi;
+    int split_count = 1;
+    DevBuf seg_cbeg, seg_cend, summ;
+    // merged KV destination per layer (device)
+    std::vector<void*> kdst, vdst;
+    std::vector<uint8_t> prev, dropped;
+    int layer = 0;
+};
+
+struct Context {
+    keep_config cfg{};
+    int L = 0, H = 0, d = 0, dh = 0, f = 0, V = 0;
+    bool fast = false;
+    int elem = 4;  // merged-KV element bytes
+    cudaStream_t s_main = nullptr, s_copy = nullptr, s_sel = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    bool weights_ready = false;
+    DevBuf embed, unembed;
+    std::vector<std::unique_ptr<DevBuf>> w;  // L*4 slots
+    // memory tier
+    std::map<OwnerKey, Payload> store;
+    std::map<OwnerKey, uint64_t> current_version;
+    keep_memory_stats stats{};
+    // cursor
+    std::unique_ptr<Pass> pf;
+    DevBuf kv;  // merged KV of the cursor [L][2][T][d]
+    std::vector<void*> seg_ksrc_h, seg_vsrc_h;
+    DevBuf d_ksrc, d_vsrc, d_cdst, d_cn;
+    std::vector<OwnerKey> seg_owner;      // owner of each layout segment
+    std::vector<int64_t> seg_owner_row;   // row offset of the segment in the owner block
+    // selector scratch
+    DevBuf sel_order, sel_n, sel_cand;
+    DevBuf logits;
+
+    void* wslot(int l, int slot) const { return w[l * 4 + slot]->p; }
+};
+
+}  // namespace keep_b200

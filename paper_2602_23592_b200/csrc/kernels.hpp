@@ -1,0 +1,103 @@
+// kernels.hpp -- host-side launchers of the sm_100a kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace keep_b200 {
+
+// K0: counter-based weights (model.hpp:54-73, 88-94; prng.hpp:16-61).
+// Element (i, j) of a named [rows x cols] tensor is the e = i*cols+j-th normal
+// of Rng::stream(seed, name).  Written either fp32 row-major into a wider
+// matrix (dst[i*ld + col_off + j]) or bf16 transposed (dst[(col_off+j)*ld + i]).
+uint64_t fnv1a64_host(const char* s);
+void launch_init_tensor(uint64_t seed, const char* name, int64_t rows, int64_t cols, double std_,
+                        void* dst, int64_t ld, int64_t col_off, bool bf16_transposed,
+                        cudaStream_t st);
+
+// K1: x[i] = embed[tokens[rows[i]]] (prefill.hpp:201-211).
+void launch_embed(const float* embed, const int32_t* tokens, const int32_t* rows, int64_t n, int d,
+                  float* x, cudaStream_t st);
+
+// Row gather: dst[i] = src[idx[i]] (fp32 rows of width d); optional bf16 copy.
+void launch_gather_rows(const float* src, const int32_t* idx, int64_t n, int d, float* dst,
+                        __nv_bfloat16* dst_bf16, cudaStream_t st);
+void launch_to_bf16(const float* src, int64_t n, __nv_bfloat16* dst, cudaStream_t st);
+
+// K4: merged-KV assembly from cached blocks (prefill.hpp:255-263, 340-350).
+// For entry e: copy rows [dst_row[e], dst_row[e]+nrows[e]) of K and V from
+// the block pointers ksrc[e] / vsrc[e].
+void launch_copy_cached(const void* const* ksrc, const void* const* vsrc, const int32_t* dst_row,
+                        const int32_t* nrows, int n_entries, int64_t row_bytes, void* kdst,
+                        void* vdst, int max_rows, cudaStream_t st);
+
+// K6: rowbins -> summary (prefill.hpp:281-288, 306-315).
+// rowbin[i][j]: probability mass (head mean) of compact row i on segment j.
+// seg_cbeg/seg_cend: compact row range of each segment (empty if inactive);
+// query rows are [q_cbeg, q_cend).  Writes qts[S] and sts[S*S] (fp64).
+template <typename TB>
+void launch_summary_reduce(const TB* rowbin, int S, const int32_t* seg_cbeg, const int32_t* seg_cend,
+                           const int32_t* seg_len, int q_cbeg, int q_cend, int qlen, double* summ,
+                           cudaStream_t st);
+
+// K7: converge on the device (recompute.hpp:86-138).
+void launch_select(int S, const double* qts, const double* sts, int64_t budget,
+                   const uint8_t* candidates, int32_t* order, int32_t* n_out, int32_t* hops_out,
+                   cudaStream_t st);
+
+// K11: Model::logits of one fp32 row, fp64 accumulation in ascending i
+// (model.hpp:76-85).
+void launch_logits(const float* row, const float* unembed, int d, int V, double* out,
+                   cudaStream_t st);
+
+// ------------------------------------------------------------ parity GEMM --
+// C = A[M x K] . B[K x N] with fp32 operands and fp64 accumulation in
+// ascending k (bit-exact with vec_mat, tensor.hpp:31-41).
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_RELU = 2, EPI_STORE = 3 };
+struct EpiArgs {
+    int kind;
+    int d;                 // model dim (QKV split)
+    float* out;            // STORE / RELU: [M x N]; QKV: q [M x d]; RESID: x [M x N] (+=)
+    int64_t ldo;
+    void* kdst;            // QKV: merged keys [T x d] (row = rows[i])
+    void* vdst;
+    const int32_t* rows;   // QKV scatter rows
+    __nv_bfloat16* out_bf16;  // optional bf16 mirror of the written value (FAST)
+};
+void launch_gemm_f64acc(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
+                        const EpiArgs& epi, cudaStream_t st);
+
+// ------------------------------------------------------- attention family --
+// Causal attention of compact rows against the merged KV of one layer, with
+// normalised probabilities binned per (row, destination segment).
+struct AttnArgs {
+    int n;          // compact rows
+    int T;          // keys
+    int H, dh, d;
+    const void* q;  // [n x d] compact queries (fp32 PARITY / bf16 FAST)
+    const void* k;  // [T x d] merged keys
+    const void* v;  // [T x d] merged values
+    const int32_t* rows;     // [n] global row of compact row i
+    const int32_t* row_seg;  // [T] segment of key row (-1 = query)
+    const int32_t* key_lo;   // [T] first visible key of a row (nullptr = 0: causal prefix);
+                             // block-diagonal contexts for canonical refresh
+    bool with_bins;
+    int S;
+    // split plan (segment-aligned key splits, computed by the host)
+    int nsplit;
+    const int32_t* split_lo;  // [nsplit] first key of split
+    const int32_t* split_hi;  // [nsplit] one past last key
+    int rows_per_tile;
+    // scratch / outputs
+    double* m_part;  // [nsplit x n x H]
+    double* l_part;
+    double* m_fin;   // [n x H]
+    double* l_fin;
+    double* o_part;  // [nsplit x n x d] (only when nsplit > 1)
+    float* ctx;      // [n x d] fp32 output (PARITY)
+    __nv_bfloat16* ctx_bf16;  // [n x d] (FAST)
+    void* rowbin;    // [n x S] fp64 (PARITY) / fp32 (FAST)
+};
+void launch_attention_parity(const AttnArgs& a, cudaStream_t st);
+void launch_attention_fast(const AttnArgs& a, cudaStream_t st);
+
+}  // namespace keep_b200

@@ -1,0 +1,432 @@
+// kernels_common.cu -- K0 init, K1 embed, row gathers, K4 merged-KV assembly,
+// K6 summary reduce, K7 selector, K11 logits.  All HBM- or latency-bound
+// integer/fp64 work: coalesced 16-byte accesses, grids sized in SM multiples.
+#include "kernels.hpp"
+
+#include <cfloat>
+
+namespace keep_b200 {
+
+// ======================================================================= K0 ==
+uint64_t fnv1a64_host(const char* s) {  // prng.hpp:23-30
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (; *s; ++s) {
+        h ^= static_cast<unsigned char>(*s);
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+__device__ __forceinline__ uint64_t sm64_mix(uint64_t z) {  // prng.hpp:17-20
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+// Normal #e of the stream whose pre-warm-up state is s0: draws 12e..12e+11,
+// draw n seeing state s0 + (n+3)*gamma (two warm-up draws, prng.hpp:34-38),
+// summed in order in fp64 (Irwin-Hall, prng.hpp:57-61).
+__device__ __forceinline__ float normal_at(uint64_t s0, uint64_t e, double std_) {
+    const uint64_t g = 0x9e3779b97f4a7c15ULL;
+    uint64_t st = s0 + (12ull * e + 3ull) * g;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        acc += static_cast<double>(sm64_mix(st) >> 11) * 0x1.0p-53;
+        st += g;
+    }
+    return static_cast<float>((acc - 6.0) * std_);
+}
+
+// Output-order traversal so the (possibly transposed) stores coalesce; the
+// counter-based stream lets every element be drawn independently.
+__global__ void init_tensor_kernel(uint64_t s0, int64_t rows, int64_t cols, double std_, void* dst,
+                                   int64_t ld, int64_t col_off, int transposed) {
+    const int64_t n = rows * cols;
+    for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < n;
+         o += int64_t(gridDim.x) * blockDim.x) {
+        if (!transposed) {
+            const int64_t i = o / cols, j = o % cols;
+            static_cast<float*>(dst)[i * ld + col_off + j] = normal_at(s0, uint64_t(o), std_);
+        } else {
+            const int64_t j = o / rows, i = o % rows;  // dst row j (output), col i (input)
+            static_cast<__nv_bfloat16*>(dst)[(col_off + j) * ld + i] =
+                __float2bfloat16_rn(normal_at(s0, uint64_t(i * cols + j), std_));
+        }
+    }
+}
+
+void launch_init_tensor(uint64_t seed, const char* name, int64_t rows, int64_t cols, double std_,
+                        void* dst, int64_t ld, int64_t col_off, bool bf16_transposed,
+                        cudaStream_t st) {
+    const uint64_t s0 = seed ^ fnv1a64_host(name);
+    const int64_t n = rows * cols;
+    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), kNumSMs * 16));
+    init_tensor_kernel<<<grid, 256, 0, st>>>(s0, rows, cols, std_, dst, ld, col_off,
+                                             bf16_transposed ? 1 : 0);
+    KEEP_LAUNCH_CHECK();
+}
+
+// ======================================================================= K1 ==
+__global__ void embed_kernel(const float* __restrict__ embed, const int32_t* __restrict__ tokens,
+                             const int32_t* __restrict__ rows, int64_t n, int d,
+                             float* __restrict__ x) {
+    const int vec = d / 4;
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        const float4* src = reinterpret_cast<const float4*>(embed + int64_t(tokens[rows[r]]) * d);
+        float4* dst = reinterpret_cast<float4*>(x + r * d);
+        for (int c = threadIdx.x; c < vec; c += blockDim.x) dst[c] = src[c];
+    }
+}
+
+void launch_embed(const float* embed, const int32_t* tokens, const int32_t* rows, int64_t n, int d,
+                  float* x, cudaStream_t st) {
+    if (n == 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>(n, kNumSMs * 8));
+    embed_kernel<<<grid, 256, 0, st>>>(embed, tokens, rows, n, d, x);
+    KEEP_LAUNCH_CHECK();
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ src, const int32_t* __restrict__ idx,
+                                   int64_t n, int d, float* __restrict__ dst,
+                                   __nv_bfloat16* __restrict__ dstb) {
+    const int vec = d / 4;
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        const float4* s = reinterpret_cast<const float4*>(src + int64_t(idx[r]) * d);
+        float4* o = reinterpret_cast<float4*>(dst + r * d);
+        for (int c = threadIdx.x; c < vec; c += blockDim.x) {
+            const float4 v = s[c];
+            o[c] = v;
+            if (dstb) {
+                __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(dstb + r * d + 4 * c);
+                ob[0] = __floats2bfloat162_rn(v.x, v.y);
+                ob[1] = __floats2bfloat162_rn(v.z, v.w);
+            }
+        }
+    }
+}
+
+void launch_gather_rows(const float* src, const int32_t* idx, int64_t n, int d, float* dst,
+                        __nv_bfloat16* dst_bf16, cudaStream_t st) {
+    if (n == 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>(n, kNumSMs * 8));
+    gather_rows_kernel<<<grid, 256, 0, st>>>(src, idx, n, d, dst, dst_bf16);
+    KEEP_LAUNCH_CHECK();
+}
+
+__global__ void to_bf16_kernel(const float* __restrict__ src, int64_t n4, __nv_bfloat16* __restrict__ dst) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n4; i += int64_t(gridDim.x) * blockDim.x) {
+        const float4 v = reinterpret_cast<const float4*>(src)[i];
+        __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(dst + 4 * i);
+        o[0] = __floats2bfloat162_rn(v.x, v.y);
+        o[1] = __floats2bfloat162_rn(v.z, v.w);
+    }
+}
+
+void launch_to_bf16(const float* src, int64_t n, __nv_bfloat16* dst, cudaStream_t st) {
+    if (n == 0) return;
+    const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n / 4, 256), kNumSMs * 8));
+    to_bf16_kernel<<<grid, 256, 0, st>>>(src, n / 4, dst);
+    KEEP_LAUNCH_CHECK();
+}
+
+// ======================================================================= K4 ==
+// One CTA per (entry, 16-row chunk); 16-byte vector copies of K and V rows.
+__global__ void copy_cached_kernel(const void* const* __restrict__ ksrc,
+                                   const void* const* __restrict__ vsrc,
+                                   const int32_t* __restrict__ dst_row, const int32_t* __restrict__ nrows,
+                                   int64_t row_bytes, uint8_t* __restrict__ kdst,
+                                   uint8_t* __restrict__ vdst) {
+    const int e = blockIdx.x;
+    const int r0 = blockIdx.y * 16;
+    const int nr = nrows[e];
+    if (r0 >= nr) return;
+    const int r1 = min(nr, r0 + 16);
+    const int64_t vec = row_bytes / 16;
+    const uint4* ks = static_cast<const uint4*>(ksrc[e]);
+    const uint4* vs = static_cast<const uint4*>(vsrc[e]);
+    uint4* kd = reinterpret_cast<uint4*>(kdst + int64_t(dst_row[e]) * row_bytes);
+    uint4* vd = reinterpret_cast<uint4*>(vdst + int64_t(dst_row[e]) * row_bytes);
+    const int64_t total = int64_t(r1 - r0) * vec, base = int64_t(r0) * vec;
+    for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
+        kd[base + i] = ks[base + i];
+        vd[base + i] = vs[base + i];
+    }
+}
+
+void launch_copy_cached(const void* const* ksrc, const void* const* vsrc, const int32_t* dst_row,
+                        const int32_t* nrows, int n_entries, int64_t row_bytes, void* kdst,
+                        void* vdst, int max_rows, cudaStream_t st) {
+    if (n_entries == 0) return;
+    dim3 grid(n_entries, static_cast<unsigned>(ceil_div(max_rows, 16)));
+    copy_cached_kernel<<<grid, 256, 0, st>>>(ksrc, vsrc, dst_row, nrows, row_bytes,
+                                             static_cast<uint8_t*>(kdst), static_cast<uint8_t*>(vdst));
+    KEEP_LAUNCH_CHECK();
+}
+
+// ======================================================================= K6 ==
+// sts[src][dst] = (sum over compact rows of src, in row order, of
+// rowbin[row][dst]) / seg_len[src] for dst < src; qts[dst] likewise over the
+// query rows / qlen (prefill.hpp:281-288, 306-315).  Inactive sources and the
+// upper triangle are zero.
+template <typename TB>
+__global__ void summary_reduce_kernel(const TB* __restrict__ rowbin, int S,
+                                      const int32_t* __restrict__ seg_cbeg,
+                                      const int32_t* __restrict__ seg_cend,
+                                      const int32_t* __restrict__ seg_len, int q_cbeg, int q_cend,
+                                      int qlen, double* __restrict__ summ) {
+    const int src = blockIdx.y - 1;  // -1 = the query row block
+    double* out = src < 0 ? summ : summ + S + int64_t(src) * S;
+    int cb, ce;
+    double denom;
+    if (src < 0) {
+        cb = q_cbeg;
+        ce = q_cend;
+        denom = double(qlen);
+    } else {
+        cb = seg_cbeg[src];
+        ce = seg_cend[src];
+        denom = double(seg_len[src]);
+    }
+    for (int dst = blockIdx.x * blockDim.x + threadIdx.x; dst < S; dst += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        const bool live = (src < 0) ? (qlen > 0) : (dst < src);
+        if (live)
+            for (int r = cb; r < ce; ++r) acc += double(rowbin[int64_t(r) * S + dst]);
+        out[dst] = live ? acc / denom : 0.0;
+    }
+}
+
+template <typename TB>
+void launch_summary_reduce(const TB* rowbin, int S, const int32_t* seg_cbeg, const int32_t* seg_cend,
+                           const int32_t* seg_len, int q_cbeg, int q_cend, int qlen, double* summ,
+                           cudaStream_t st) {
+    dim3 grid(static_cast<unsigned>(ceil_div(S, 256)), S + 1);
+    summary_reduce_kernel<TB><<<grid, 256, 0, st>>>(rowbin, S, seg_cbeg, seg_cend, seg_len, q_cbeg,
+                                                    q_cend, qlen, summ);
+    KEEP_LAUNCH_CHECK();
+}
+template void launch_summary_reduce<double>(const double*, int, const int32_t*, const int32_t*,
+                                            const int32_t*, int, int, int, double*, cudaStream_t);
+template void launch_summary_reduce<float>(const float*, int, const int32_t*, const int32_t*,
+                                           const int32_t*, int, int, int, double*, cudaStream_t);
+
+// ======================================================================= K7 ==
+// converge (recompute.hpp:86-138) as one persistent CTA.  Column sums of the
+// relevant set are kept incrementally (O(S) per hop instead of O(S*|R|));
+// because the reference re-sums in ascending position, each hop arbitrates
+// exactly: a forward error bound on the incremental sums yields the set of
+// positions that could be the reference's pick, and when that set is not a
+// single clear winner those positions are re-summed in the reference's order
+// and compared with the reference's rule (strict >, lowest position, > 0).
+constexpr int kSelThreads = 1024;
+
+struct SelRed {
+    double v;
+    int i;
+};
+
+__device__ __forceinline__ SelRed sel_better(SelRed a, SelRed b) {
+    // larger value wins; equal values -> lower index
+    if (b.i < 0) return a;
+    if (a.i < 0) return b;
+    if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+    return a;
+}
+
+__device__ SelRed block_argmax(SelRed x, SelRed* scratch) {
+    for (int o = 16; o > 0; o >>= 1) {
+        SelRed y{__shfl_xor_sync(0xffffffffu, x.v, o), __shfl_xor_sync(0xffffffffu, x.i, o)};
+        x = sel_better(x, y);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) scratch[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        x = (l < int(blockDim.x >> 5)) ? scratch[l] : SelRed{0.0, -1};
+        for (int o = 16; o > 0; o >>= 1) {
+            SelRed y{__shfl_xor_sync(0xffffffffu, x.v, o), __shfl_xor_sync(0xffffffffu, x.i, o)};
+            x = sel_better(x, y);
+        }
+        if (l == 0) scratch[32] = x;
+    }
+    __syncthreads();
+    return scratch[32];
+}
+
+__device__ int block_sum_int(int x, int* scratch) {
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) scratch[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        x = (l < int(blockDim.x >> 5)) ? scratch[l] : 0;
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (l == 0) scratch[32] = x;
+    }
+    __syncthreads();
+    return scratch[32];
+}
+
+// State per position lives in shared memory (colsum fp64, colabs fp32
+// upper bound, ascending relevant list); the allowed set is a per-thread
+// bitmask (position tid + k*1024 -> bit k).
+constexpr int kSelMaxS = 14 * kSelThreads;
+
+__global__ void __launch_bounds__(kSelThreads, 1)
+select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ sts, int64_t budget,
+              const uint8_t* __restrict__ cand, int32_t* __restrict__ order, int32_t* n_out,
+              int32_t* hops_out) {
+    extern __shared__ __align__(16) uint8_t sraw[];
+    double* colsum = reinterpret_cast<double*>(sraw);               // [S]
+    float* colabs = reinterpret_cast<float*>(colsum + S);           // [S]
+    int32_t* sorted_r = reinterpret_cast<int32_t*>(colabs + S);     // [S] ascending relevant set
+    __shared__ SelRed red[33];
+    __shared__ int ired[33];
+    __shared__ int s_win;
+
+    const int items = int(ceil_div(S, kSelThreads));
+    uint32_t allowed = 0;
+    for (int k = 0; k < items; ++k) {
+        const int i = threadIdx.x + k * kSelThreads;
+        if (i < S && (cand == nullptr || cand[i] != 0)) allowed |= 1u << k;
+        if (i < S) {
+            colsum[i] = 0.0;
+            colabs[i] = 0.f;
+        }
+    }
+    __syncthreads();
+    const double u = 0x1.0p-53;
+    int n = 0, hop = 0;
+    // score and error radius of position i (scores of the reference: qts
+    // before the first pick, mean over the relevant set afterwards)
+    auto score_of = [&](int i, double& sc, double& err) {
+        if (n == 0) {
+            sc = qts[i];
+            err = 0.0;
+        } else {
+            sc = colsum[i] / double(n);
+            // colabs is rounded to fp32: inflate by 2^-20 to keep it an upper bound
+            err = (2.0 * (n + 2)) * u * (double(colabs[i]) * (1.0 + 0x1.0p-20) / double(n)) + 4.0 * u * fabs(sc);
+        }
+    };
+    while (int64_t(n) < budget && hop < S) {
+        SelRed best{0.0, -1};
+        for (int k = 0; k < items; ++k) {
+            if (!(allowed >> k & 1u)) continue;
+            const int i = threadIdx.x + k * kSelThreads;
+            double sc, err;
+            score_of(i, sc, err);
+            // lower bound of the reference score; only positions that can be > 0
+            if (sc + err > 0.0) best = sel_better(best, SelRed{sc - err, i});
+        }
+        const SelRed lo = block_argmax(best, red);
+        ++hop;
+        if (lo.i < 0) break;  // nothing can be strictly positive: stalled hop
+        // possible winners: upper bound reaches the best lower bound
+        int mine = 0, first = INT32_MAX;
+        for (int k = 0; k < items; ++k) {
+            if (!(allowed >> k & 1u)) continue;
+            const int i = threadIdx.x + k * kSelThreads;
+            double sc, err;
+            score_of(i, sc, err);
+            if (sc + err > 0.0 && sc + err >= lo.v) {
+                ++mine;
+                first = min(first, i);
+            }
+        }
+        const int cnt = block_sum_int(mine, ired);
+        if (cnt == 1 && lo.v > 0.0) {
+            if (mine) s_win = first;
+        } else {
+            // exact arbitration: the reference's ascending-position sums
+            SelRed ex{0.0, -1};
+            for (int k = 0; k < items; ++k) {
+                if (!(allowed >> k & 1u)) continue;
+                const int i = threadIdx.x + k * kSelThreads;
+                double sc, err;
+                score_of(i, sc, err);
+                if (!(sc + err > 0.0 && sc + err >= lo.v)) continue;
+                double v;
+                if (n == 0) {
+                    v = qts[i];
+                } else {
+                    double acc = 0.0;
+                    for (int m = 0; m < n; ++m) acc += sts[int64_t(sorted_r[m]) * S + i];
+                    v = acc / double(n);
+                }
+                if (v > 0.0) ex = sel_better(ex, SelRed{v, i});
+            }
+            const SelRed w = block_argmax(ex, red);
+            if (threadIdx.x == 0) s_win = w.i;
+        }
+        __syncthreads();
+        const int win = s_win;
+        __syncthreads();
+        if (win < 0) break;  // the stalled hop still counts (recompute.hpp:124)
+        if (threadIdx.x == 0) order[n] = win;
+        // insert into the ascending list: count smaller entries, shift the tail
+        int cntlt = 0;
+        for (int m = threadIdx.x; m < n; m += kSelThreads) cntlt += sorted_r[m] < win;
+        const int pos = block_sum_int(cntlt, ired);
+        const int tail = n - pos;
+        for (int c = int(ceil_div(tail, kSelThreads)) - 1; c >= 0; --c) {
+            const int off = c * kSelThreads + int(threadIdx.x);
+            const bool ok = off < tail;
+            const int v = ok ? sorted_r[pos + off] : 0;
+            __syncthreads();
+            if (ok) sorted_r[pos + off + 1] = v;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) sorted_r[pos] = win;
+        ++n;
+        // fold the new member's row into the column sums (insertion order)
+        const double* row = sts + int64_t(win) * S;
+        for (int k = 0; k < items; ++k) {
+            const int i = threadIdx.x + k * kSelThreads;
+            if (i == win) allowed &= ~(1u << k);
+            if (!(allowed >> k & 1u)) continue;
+            const double t = row[i];
+            colsum[i] += t;
+            colabs[i] = __fadd_ru(colabs[i], __double2float_ru(fabs(t)));
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *n_out = n;
+        *hops_out = hop;
+    }
+}
+
+void launch_select(int S, const double* qts, const double* sts, int64_t budget,
+                   const uint8_t* candidates, int32_t* order, int32_t* n_out, int32_t* hops_out,
+                   cudaStream_t st) {
+    if (S > kSelMaxS) raise(KEEP_ERR_CONFIG, "selector supports at most 14336 segments");
+    const size_t smem = size_t(std::max(S, 1)) * (8 + 4 + 4) + 16;
+    if (smem > 48 * 1024)
+        KEEP_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    select_kernel<<<1, kSelThreads, smem, st>>>(S, qts, sts, budget, candidates, order, n_out, hops_out);
+    KEEP_LAUNCH_CHECK();
+}
+
+// ====================================================================== K11 ==
+__global__ void logits_kernel(const float* __restrict__ row, const float* __restrict__ unembed, int d,
+                              int V, double* __restrict__ out) {
+    extern __shared__ float srow[];
+    for (int i = threadIdx.x; i < d; i += blockDim.x) srow[i] = row[i];
+    __syncthreads();
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= V) return;
+    double acc = 0.0;
+    for (int i = 0; i < d; ++i) acc = fma(double(srow[i]), double(unembed[int64_t(i) * V + j]), acc);
+    out[j] = acc;
+}
+
+void launch_logits(const float* row, const float* unembed, int d, int V, double* out, cudaStream_t st) {
+    logits_kernel<<<static_cast<unsigned>(ceil_div(V, 128)), 128, sizeof(float) * d, st>>>(row, unembed, d, V, out);
+    KEEP_LAUNCH_CHECK();
+}
+
+}  // namespace keep_b200
