@@ -144,17 +144,20 @@ attn_stats_kernel(AttnArgs a, ACC scale) {
             if (c + 16 * kk < nk && key <= t && key >= klo) cm = max(cm, s[kk]);
         }
         cm = red16_max(cm);
-        if (cm == neg_inf<ACC>()) continue;  // no visible key for this row in the chunk
+        // every lane of the warp must reach the shuffles: no early continue
+        const bool any = cm != neg_inf<ACC>();  // a visible key for this row in the chunk
         const ACC mn = max(m, cm);
         ACC part = ACC(0);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
             const int key = k0 + c + 16 * kk;
-            if (c + 16 * kk < nk && key <= t && key >= klo) part += ex(s[kk] - mn);
+            if (any && c + 16 * kk < nk && key <= t && key >= klo) part += ex(s[kk] - mn);
         }
         part = red16_sum(part);
-        l = (m == neg_inf<ACC>() ? ACC(0) : l * ex(m - mn)) + part;
-        m = mn;
+        if (any) {
+            l = (m == neg_inf<ACC>() ? ACC(0) : l * ex(m - mn)) + part;
+            m = mn;
+        }
     }
     if (c == 0 && r < tl.nrows) {
         const int64_t o = (int64_t(sp) * a.n + tl.i0 + r) * a.H + h;

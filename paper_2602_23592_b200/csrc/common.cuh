@@ -5,6 +5,8 @@
 #include <cuda_bf16.h>
 #include <cstdint>
 #include <stdexcept>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "keep_b200.h"
@@ -26,7 +28,14 @@ inline void raise(int code, const std::string& msg) { throw KeepError(code, msg)
                                                   cudaGetErrorString(e_));               \
     } while (0)
 
-#define KEEP_LAUNCH_CHECK() KEEP_CUDA(cudaGetLastError())
+// KEEP_SYNC_DEBUG=1: synchronise and trace after every launch (bring-up aid)
+bool sync_debug();
+void trace_launch(const char* file, int line);
+#define KEEP_LAUNCH_CHECK()                                                \
+    do {                                                                   \
+        KEEP_CUDA(cudaGetLastError());                                     \
+        if (::keep_b200::sync_debug()) ::keep_b200::trace_launch(__FILE__, __LINE__); \
+    } while (0)
 
 constexpr int kNumSMs = 148;
 

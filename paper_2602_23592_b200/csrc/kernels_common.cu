@@ -7,6 +7,22 @@
 
 namespace keep_b200 {
 
+bool sync_debug() {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_SYNC_DEBUG");
+        return e && *e == '1';
+    }();
+    return on;
+}
+
+void trace_launch(const char* file, int line) {
+    std::fprintf(stderr, "[keep] launch %s:%d ...", file, line);
+    std::fflush(stderr);
+    const cudaError_t e = cudaDeviceSynchronize();
+    std::fprintf(stderr, " %s\n", cudaGetErrorString(e));
+    std::fflush(stderr);
+}
+
 // ======================================================================= K0 ==
 uint64_t fnv1a64_host(const char* s) {  // prng.hpp:23-30
     uint64_t h = 0xcbf29ce484222325ULL;

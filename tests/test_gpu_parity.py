@@ -154,11 +154,15 @@ def test_selective_prefill_plans(ko, golden, ctx_cache):
         assert rel(got["kv"], ref["kv"]) <= HIDDEN_RTOL, name
         assert np.max(np.abs(got["sts"] - ref["sts"])) <= SUMMARY_ATOL, name
         assert np.max(np.abs(got["qts"] - ref["qts"])) <= SUMMARY_ATOL, name
-        # merged KV takes the cached rows verbatim (test_prefill.cpp:273-287)
-        inactive = np.repeat(plan == 0, p.seg_len, axis=1)
+        # merged KV takes the (device) cached rows verbatim (test_prefill.cpp:273-287)
+        starts = np.concatenate([[0], np.cumsum(p.seg_len)])
         for l in range(L):
-            rows = np.nonzero(inactive[l])[0]
-            assert np.array_equal(got["kv"][l, :, rows], cached[l][:, rows]) if len(rows) else True
+            for i in range(S):
+                if plan[l, i]:
+                    continue
+                k, v = ctx.memory_read(kb.SEGMENT, i, l, int(p.seg_len[i]))
+                assert np.array_equal(got["kv"][l][0][starts[i]:starts[i + 1]], k), (name, l, i)
+                assert np.array_equal(got["kv"][l][1][starts[i]:starts[i + 1]], v), (name, l, i)
 
 
 def test_errors(ko, golden, ctx_cache):
