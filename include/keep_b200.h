@@ -189,6 +189,11 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query,
 
 int keep_logits(void* ctx, const float* row, double* out);
 
+/* ---- test hook (not part of the reference surface) ----------------------
+ * C[M x N] (fp32, device) = A[M x K] . Bt[N x K]^T with bf16 device operands
+ * on the tcgen05 GEMM; force_bn 0 = automatic tile, 64 or 256 = forced. */
+int keep_debug_gemm_bf16(const void* A, const void* Bt, float* C, int M, int N, int K, int force_bn);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

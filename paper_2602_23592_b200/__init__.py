@@ -123,6 +123,7 @@ def load_library() -> C.CDLL:
         "keep_plan_keep": (C.c_int, [vp, C.POINTER(keep_layout), i32p, i32, dp, i32,
                                      C.POINTER(keep_plan_result)]),
         "keep_logits": (C.c_int, [vp, fp, dp]),
+        "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -1,76 +1,395 @@
-// gemm_tc.cu -- FAST-mode projection GEMM (bf16 operands, fp32 accumulation).
-// Interim SIMT implementation; replaced by the tcgen05/TMA kernel.
+// gemm_tc.cu -- FAST-mode projection GEMM on the 5th-generation tensor cores.
+//
+//   C[M x N] = A[M x K] . Bt[N x K]^T      bf16 operands, fp32 accumulation
+//
+// A = compact activations (row-major, K-major), Bt = transposed weights
+// (K-major rows).  One persistent CTA per SM, warp-specialised:
+//   warp 0      TMA producer   (one elected lane; cp.async.bulk.tensor into a
+//                               STAGES-deep ring of 128B-swizzled tiles)
+//   warp 1      MMA issuer     (one lane; tcgen05.mma.cta_group::1.kind::f16,
+//                               128 x BN x 16 per instruction, accumulators in
+//                               TMEM, double buffered so the epilogue of tile
+//                               i overlaps the main loop of tile i+1)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue       (tcgen05.ld 32x32b -> registers -> fused op)
+// Fused epilogues: QKV split with K/V rows scattered into
+// the merged KV cache at their global row (gathered recompute), fp32 residual
+// add with a bf16 mirror for the next GEMM, ReLU to bf16, plain fp32 store.
+// Tiles are rasterised in bands of GM m-blocks so a band of A and a window of
+// weight columns stay L2-resident (126 MB) while 148 CTAs sweep them.
+#include <cuda.h>
+
 #include "engine.hpp"
 
 namespace keep_b200 {
 
 namespace {
-constexpr int BM = 64, BN = 64, BK = 32;
 
-__global__ void __launch_bounds__(256)
-gemm_bf16_simt(const __nv_bfloat16* __restrict__ A, int64_t lda, const __nv_bfloat16* __restrict__ Bt,
-               int64_t ldb, int M, int N, int K, EpiArgs epi) {
-    __shared__ float As[BK][BM + 1];
-    __shared__ float Bs[BK][BN + 1];
-    const int t = threadIdx.x, ty = t / 16, tx = t % 16;
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-    float acc[4][4] = {};
-    for (int k0 = 0; k0 < K; k0 += BK) {
-        for (int e = t; e < BM * BK; e += 256) {
-            const int r = e / BK, k = e % BK;
-            As[k][r] = (m0 + r < M && k0 + k < K) ? __bfloat162float(A[int64_t(m0 + r) * lda + k0 + k]) : 0.f;
-            Bs[k][r] = (n0 + r < N && k0 + k < K) ? __bfloat162float(Bt[int64_t(n0 + r) * ldb + k0 + k]) : 0.f;
-        }
-        __syncthreads();
-        for (int k = 0; k < BK; ++k) {
-            float a[4], b[4];
-            for (int r = 0; r < 4; ++r) a[r] = As[k][ty + 16 * r];
-            for (int c = 0; c < 4; ++c) b[c] = Bs[k][tx + 16 * c];
-            for (int r = 0; r < 4; ++r)
-                for (int c = 0; c < 4; ++c) acc[r][c] = fmaf(a[r], b[c], acc[r][c]);
-        }
-        __syncthreads();
-    }
-    for (int r = 0; r < 4; ++r) {
-        const int m = m0 + ty + 16 * r;
-        if (m >= M) continue;
-        for (int c = 0; c < 4; ++c) {
-            const int n = n0 + tx + 16 * c;
-            if (n >= N) continue;
-            const float v = acc[r][c];
-            const int d = epi.d;
-            switch (epi.kind) {
-                case EPI_QKV:
-                    if (n < d) epi.out_bf16[int64_t(m) * d + n] = __float2bfloat16_rn(v);
-                    else if (n < 2 * d)
-                        static_cast<__nv_bfloat16*>(epi.kdst)[int64_t(epi.rows[m]) * d + n - d] = __float2bfloat16_rn(v);
-                    else
-                        static_cast<__nv_bfloat16*>(epi.vdst)[int64_t(epi.rows[m]) * d + n - 2 * d] = __float2bfloat16_rn(v);
-                    break;
-                case EPI_RESID: {
-                    float* o = epi.out + int64_t(m) * epi.ldo + n;
-                    const float x = *o + v;
-                    *o = x;
-                    epi.out_bf16[int64_t(m) * epi.ldo + n] = __float2bfloat16_rn(x);
-                    break;
-                }
-                case EPI_RELU:
-                    epi.out_bf16[int64_t(m) * epi.ldo + n] = __float2bfloat16_rn(v < 0.f ? 0.f : v);
-                    break;
-                default:
-                    break;
+constexpr int BM = 128, BK = 64, UMMA_K = 16, GM = 16;
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major operand staged by TMA with 128B
+// swizzle (8-row x 128-byte atoms, atoms 1024 B apart along M/N).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);          // start address
+    d |= uint64_t(1) << 16;                         // leading byte offset (unused for SW128 K-major)
+    d |= uint64_t(1024 >> 4) << 32;                 // stride byte offset: 8 rows * 128 B
+    d |= uint64_t(1) << 46;                         // descriptor version (sm_100)
+    d |= uint64_t(2) << 61;                         // layout: SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major.
+__host__ __device__ constexpr uint32_t instr_desc(int M, int N) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Store 32 consecutive values of one row starting at column n.
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
+    uint4* o = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        o[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                          pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+}
+
+__device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int m, int n, float (&v)[32]) {
+    switch (e.kind) {
+        case EPI_QKV: {
+            const int d = e.d;
+            if (n < d) {
+                store_bf16x32(e.out_bf16 + int64_t(m) * d + n, v);
+            } else if (n < 2 * d) {
+                store_bf16x32(static_cast<__nv_bfloat16*>(e.kdst) + int64_t(e.rows[m]) * d + (n - d), v);
+            } else {
+                store_bf16x32(static_cast<__nv_bfloat16*>(e.vdst) + int64_t(e.rows[m]) * d + (n - 2 * d), v);
             }
+            break;
+        }
+        case EPI_RESID: {
+            float4* x = reinterpret_cast<float4*>(e.out + int64_t(m) * e.ldo + n);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                float4 t = x[q];
+                t.x += v[4 * q + 0];
+                t.y += v[4 * q + 1];
+                t.z += v[4 * q + 2];
+                t.w += v[4 * q + 3];
+                x[q] = t;
+                v[4 * q + 0] = t.x;
+                v[4 * q + 1] = t.y;
+                v[4 * q + 2] = t.z;
+                v[4 * q + 3] = t.w;
+            }
+            if (e.out_bf16) store_bf16x32(e.out_bf16 + int64_t(m) * e.ldo + n, v);
+            break;
+        }
+        case EPI_RELU: {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) v[q] = v[q] < 0.f ? 0.f : v[q];
+            store_bf16x32(e.out_bf16 + int64_t(m) * e.ldo + n, v);
+            break;
+        }
+        default: {
+            float4* o = reinterpret_cast<float4*>(e.out + int64_t(m) * e.ldo + n);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
     }
 }
-}  // namespace
 
-void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N,
-                      int K, const EpiArgs& epi, cudaStream_t st) {
-    if (M == 0 || N == 0) return;
-    dim3 grid(static_cast<unsigned>(ceil_div(N, BN)), static_cast<unsigned>(ceil_div(M, BM)));
-    gemm_bf16_simt<<<grid, 256, 0, st>>>(A, lda, Bt, ldb, M, N, K, epi);
+template <int BN>
+struct Cfg {
+    static constexpr int STAGES = BN == 256 ? 4 : 8;
+    static constexpr uint32_t A_BYTES = BM * BK * 2;
+    static constexpr uint32_t B_BYTES = BN * BK * 2;
+    static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
+    const int band = t / (GM * tiles_n);
+    const int m0 = band * GM;
+    const int gm = min(GM, tiles_m - m0);
+    const int r = t - band * GM * tiles_n;
+    mb = m0 + r % gm;
+    nb = r / gm;
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+               EpiArgs epi) {
+    using CF = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE_BYTES);
+    uint64_t* empty = full + CF::STAGES;
+    uint64_t* tfull = empty + CF::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_m = int(ceil_div(M, BM)), tiles_n = int(ceil_div(N, BN));
+    const int ntiles = tiles_m * tiles_n, kblocks = K / BK;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        for (int s = 0; s < CF::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(CF::TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int mb, nb;
+                tile_coords(t, tiles_m, tiles_n, mb, nb);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * CF::STAGE_BYTES;
+                    mbar_expect_tx(&full[stage], CF::STAGE_BYTES);
+                    tma_load_2d(sa, &tmA, &full[stage], kb * BK, mb * BM);
+                    tma_load_2d(sa + CF::A_BYTES, &tmB, &full[stage], kb * BK, nb * BN);
+                    if (++stage == CF::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            constexpr uint32_t idesc = instr_desc(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], aphase ^ 1);  // epilogue drained this accumulator
+                fence_after();
+                const uint32_t tmem_d = tmem_base + uint32_t(acc * BN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
+                    const uint64_t ad = smem_desc(sa), bd = smem_desc(sa + CF::A_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / UMMA_K; ++k) {
+                        // advance 16 bf16 = 32 bytes along K inside the swizzle atom
+                        umma(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+                    if (++stage == CF::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+            }
+        }
+    } else if (warp >= 4) {  // ---------------- epilogue warps
+        const int q = warp & 3;  // TMEM lanes 32q..32q+31
+        int it = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+            int mb, nb;
+            tile_coords(t, tiles_m, tiles_n, mb, nb);
+            const int acc = it & 1;
+            mbar_wait(&tfull[acc], (it >> 1) & 1);
+            fence_after();
+            const int m = mb * BM + q * 32 + lane;
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t r[32];
+                tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + ch * 32), r);
+                const int n = nb * BN + ch * 32;
+                if (m < M && n < N) {
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                    epilogue_chunk(epi, m, n, v);
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CF::TMEM_COLS)
+                     : "memory");
+    }
+}
+
+// ------------------------------------------------------------ tensor maps --
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            raise(KEEP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeFn>(p);
+    }();
+    return fn;
+}
+
+// 2-D bf16 tensor [rows x cols] (row stride ld elements), box BK x box_rows,
+// 128-byte swizzle; out-of-bounds rows read as zero.
+CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    CUtensorMap tm;
+    const cuuint64_t gdim[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    const cuuint64_t gstride[1] = {cuuint64_t(ld * 2)};
+    const cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(KEEP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return tm;
+}
+
+template <int BN>
+void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
+               const EpiArgs& epi, cudaStream_t st) {
+    using CF = Cfg<BN>;
+    static bool attr = false;
+    if (!attr) {
+        KEEP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM)));
+        attr = true;
+    }
+    const CUtensorMap ta = make_map(A, M, K, lda, BM);
+    const CUtensorMap tb = make_map(Bt, N, K, ldb, BN);
+    const int ntiles = int(ceil_div(M, BM) * ceil_div(N, BN));
+    const int grid = std::min(ntiles, kNumSMs);
+    gemm_tc_kernel<BN><<<grid, kThreads, CF::SMEM, st>>>(ta, tb, M, N, K, epi);
     KEEP_LAUNCH_CHECK();
 }
 
+}  // namespace
+
+void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
+                      const EpiArgs& epi, cudaStream_t st) {
+    if (M == 0 || N == 0) return;
+    if (K % BK != 0 || N % 32 != 0) raise(KEEP_ERR_CONFIG, "tcgen05 GEMM needs K % 64 == 0 and N % 32 == 0");
+    // few row blocks: narrow N tiles so enough CTAs stream the weights
+    if (ceil_div(M, BM) * ceil_div(N, 256) >= kNumSMs || N % 256 != 0)
+        launch_bn<256>(A, lda, Bt, ldb, M, N, K, epi, st);
+    else
+        launch_bn<64>(A, lda, Bt, ldb, M, N, K, epi, st);
+}
+
 }  // namespace keep_b200
+
+// Test hook: plain fp32-output GEMM on device pointers (C = A . Bt^T).
+extern "C" int keep_debug_gemm_bf16(const void* A, const void* Bt, float* Cout,
+                                                                           int M, int N, int K, int force_bn) {
+    try {
+        keep_b200::EpiArgs e{keep_b200::EPI_STORE, 0, Cout, N, nullptr, nullptr, nullptr, nullptr};
+        auto a = static_cast<const __nv_bfloat16*>(A);
+        auto b = static_cast<const __nv_bfloat16*>(Bt);
+        if (force_bn == 256) keep_b200::launch_bn<256>(a, K, b, K, M, N, K, e, 0);
+        else if (force_bn == 64) keep_b200::launch_bn<64>(a, K, b, K, M, N, K, e, 0);
+        else keep_b200::launch_gemm_bf16(a, K, b, K, M, N, K, e, 0);
+        return cudaDeviceSynchronize() == cudaSuccess ? 0 : KEEP_ERR_CUDA;
+    } catch (const keep_b200::KeepError& e) {
+        return e.code;
+    }
+}
