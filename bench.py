@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""KEEP per-layer memory prefill benchmark (TTFT + recomputed tokens/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full KEEP prefill (plan_keep: every layer's scoring, multi-hop
+selection, gathered recompute, merged-KV assembly, plus the first-token
+logits) over a 16K-token synthetic memory on Qwen2.5-14B dimensions
+(BASELINE.json configs[2], SURVEY.md 8 "C3").  Prints one JSON line.
+
+  value  recomputed tokens/s = sum_l N_act(l) / TTFT, device-timed (CUDA
+         events) with the memory KV resident in HBM.
+  e2e    the same metric through the C ABI call with host buffers (token
+         ids H2D, logits/plan D2H inside the timed region), host wall clock.
+The CPU baseline is the reference's own path (oracle/_ref, the unmodified
+headers; else the plain-C restatement) timed on a bounded one-layer sample of
+the same configuration on one host core and extrapolated op-for-op to the
+workload (the reference is single-threaded; a full C3 run takes days).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: model dims, memory size in segments (8-12 tokens each), ratio
+    "c1": dict(L=4, H=4, d=32, mlp=64, V=128, S=16, r_avg=0.5, desc="reference CPU default (example-config.json)"),
+    "c2": dict(L=28, H=28, d=3584, mlp=18944, V=152064, S=410, r_avg=0.15,
+               desc="Qwen2.5-7B dims, 4K-token memory, r_avg 0.15"),
+    "c3": dict(L=48, H=40, d=5120, mlp=13824, V=152064, S=1638, r_avg=0.5,
+               desc="Qwen2.5-14B dims, 16K-token memory, r_avg 0.5 (reference default, harness.hpp:57)"),
+}
+METRIC = "memory-prefill TTFT (ms) and recomputed tokens/s, 16K-token memory, 1/2/4/8 B200"
+UNIT = "recomputed tokens/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:6], float(parts[6])))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
+        sm = [r[0] for r in rows]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in rows), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(r[3] for r in rows)}
+
+
+def workload(cfg, seed):
+    import paper_2602_23592_b200 as kb
+    from paper_2602_23592_b200.synth import group_units, make_instance_layout
+    inst = make_instance_layout(seed, cfg["S"], cfg["V"])
+    # static/dynamic memory layout: half the memory in static groups of 8
+    # segments (joint KV), half dynamic per-segment owners
+    units = group_units(cfg["S"], 8, 0.5)
+    return kb.Layout(inst.seg_len, inst.tokens, units), inst.query
+
+
+def attention_pairs(layout, qlen, plan):
+    """sum over computed rows of visible keys (t + 1), per layer."""
+    seg_len = np.asarray(layout.seg_len, np.int64)
+    starts = np.concatenate([[0], np.cumsum(seg_len)])
+    Tm = int(starts[-1])
+    out = []
+    for l in range(plan.shape[0]):
+        act = plan[l].astype(bool)
+        b, e = starts[:-1][act], starts[1:][act]
+        s = float(np.sum((e * (e + 1) - b * (b + 1)) // 2))  # sum_{t=b}^{e-1} (t+1)
+        s += float(sum(Tm + k + 1 for k in range(qlen)))
+        out.append(s)
+    return np.array(out)
+
+
+# ------------------------------------------------------------------ CPU arm --
+_W_CACHE = {}
+
+
+def cpu_sample(cfg, seed=7, sample_segments=2, reps=1):
+    """Time the reference path (PrefillCursor::step + converge via plan_keep)
+    for ONE layer at the workload's full width on a small layout; return the
+    measured fp64-accumulate MAC rate and what was sampled."""
+    from oracle.oracle import Oracle, available, Problem
+    kind = "reference" if available("kr") else "port"
+    orc = Oracle("kr" if kind == "reference" else "ko")
+    L1, H, d, mlp = 1, cfg["H"], cfg["d"], cfg["mlp"]
+    V = 1024  # vocabulary only feeds the embedding gather in a step
+    rng = np.random.default_rng(seed)
+    std = 1.0 / np.sqrt(d)
+    n_w = orc.weight_count(L1, H, d, mlp, V)
+    key = (n_w, seed)
+    if key not in _W_CACHE:
+        _W_CACHE[key] = (rng.standard_normal(n_w, dtype=np.float32) * np.float32(std)).astype(np.float32)
+    w = _W_CACHE[key]
+    from paper_2602_23592_b200.synth import make_instance_layout
+    inst = make_instance_layout(seed, sample_segments, V)
+    p = Problem(L1, H, d, mlp, V, seed, inst.seg_len, inst.tokens, inst.query)
+    T = p.T
+    cached = np.zeros((L1, 2, p.Tm, d), np.float32)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        orc.plan_keep(p, w, np.ones(1), cached=cached)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    macs = T * (4.0 * d * d + 2.0 * d * mlp) + 2.0 * d * T * (T + 1) / 2.0
+    return {"kind": kind, "seconds": best, "macs": macs, "rate": macs / best, "rows": T,
+            "sample": f"one layer at full width (d={d}, H={H}, mlp={mlp}) over {T} rows "
+                      f"({sample_segments} segments + {len(inst.query)}-token query), V reduced to {V}; "
+                      f"{kind} path, 1 host core, extrapolated op-for-op to the workload"}
+
+
+def cpu_extrapolate(sample, cfg, rows_per_layer, pairs_per_layer):
+    d, mlp = cfg["d"], cfg["mlp"]
+    macs = float(np.sum(rows_per_layer)) * (4.0 * d * d + 2.0 * d * mlp) + 2.0 * d * float(np.sum(pairs_per_layer))
+    ttft_s = macs / sample["rate"]
+    return {"ttft_s": ttft_s, "tokens_per_s": float(np.sum(rows_per_layer)) / ttft_s}
+
+
+def budget_plan(cfg, layout, r):
+    """Plan sizes if every budget were realised (reference arm's workload
+    model; the realised walk can only be shorter)."""
+    import paper_2602_23592_b200 as kb
+    S = layout.S
+    plan = np.zeros((cfg["L"], S), np.uint8)
+    for l in range(cfg["L"]):
+        b = S if l == 0 else min(S, kb.layer_budget(r[l], S))
+        plan[l, :b] = 1
+    return plan
+
+
+def run_reference(args, cfg):
+    import paper_2602_23592_b200 as kb
+    layout, query = workload(cfg, args.seed)
+    r = kb.ratio_schedule(cfg["L"], cfg["r_avg"])
+    plan = budget_plan(cfg, layout, r)
+    seg_len = np.asarray(layout.seg_len)
+    rows = plan.astype(np.int64) @ seg_len + len(query)
+    pairs = attention_pairs(layout, len(query), plan)
+    for _ in range(args.warmup):
+        cpu_sample(cfg, reps=1)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s = cpu_sample(cfg, reps=1)
+        vals.append(cpu_extrapolate(s, cfg, rows, pairs))
+    wall = time.perf_counter() - t0
+    v = float(np.median([x["tokens_per_s"] for x in vals]))
+    ttft = float(np.median([x["ttft_s"] for x in vals])) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32-store/f64-acc",
+            "data": "synthetic", "ttft_ms": ttft,
+            "config": {"workload": args.config, "desc": cfg["desc"], "S": layout.S,
+                       "T": int(seg_len.sum()) + len(query), "plan_model": "budgets fully realised"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": s["kind"], "sample": s["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm --
+def run_ours(args, cfg, rank, world, dist):
+    import torch
+
+    import paper_2602_23592_b200 as kb
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    numerics = kb.FAST if args.numerics == "fast" else kb.PARITY
+    L, H, d, mlp, V = cfg["L"], cfg["H"], cfg["d"], cfg["mlp"], cfg["V"]
+    layout, query = workload(cfg, args.seed)
+    r = kb.ratio_schedule(L, cfg["r_avg"])
+    t0 = time.perf_counter()
+    ctx = kb.Context(L, H, d, mlp, V, args.seed + rank * 0, numerics, device=dev)
+    ctx.model_init()
+    t_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    ctx.memory_compute_layout(layout, version=1)
+    t_mem = time.perf_counter() - t0
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        ctx.plan_keep(layout, query, r, final_hidden=False)
+    ctx.profile_read(reset=True)
+    ctx.profile_enable(True)
+    barrier()
+    steps = []
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            steps.append(ctx.plan_keep(layout, query, r, final_hidden=False))
+    barrier()
+    ctx.profile_enable(False)
+    prof = ctx.profile_read(reset=True)
+    ttft = np.array([s["ttft_ms"] for s in steps])
+    tokens = float(np.sum(steps[-1]["rows_per_layer"]))
+    total_ms = float(np.sum(ttft))
+    if dist is not None:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * tokens * args.steps / (total_ms / 1e3)
+
+    # e2e: the C-ABI call with host buffers, host wall clock
+    e2e_s = []
+    for _ in range(max(1, args.steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = ctx.plan_keep(layout, query, r, final_hidden=False)
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_val = world * tokens / float(np.mean(e2e_s))
+    h2d = 4 * (len(layout.tokens) + len(query) + layout.S + 3 * len(layout.units) + L)
+    d2h = 8 * V + L * layout.S * (1 + 4) + 4 * 2 * L + 8 * 2 * L
+
+    pk, src = peaks()
+    gemm_phases = ["qkv", "wo", "mlp_in", "mlp_out"]
+    g_ms = sum(prof[p]["ms"] for p in gemm_phases)
+    g_fl = sum(prof[p]["flops"] for p in gemm_phases)
+    g_by = sum(prof[p]["bytes"] for p in gemm_phases)
+    g_n = sum(prof[p]["launches"] for p in gemm_phases)
+    a_ms, a_fl = prof["attn"]["ms"], prof["attn"]["flops"]
+    phase_ms = {k: round(v["ms"] / args.steps, 3) for k, v in prof.items() if v["ms"] > 0}
+    if g_ms >= a_ms:
+        tensor_peak = pk["bf16_tflops_sustained"] if numerics == kb.FAST else 37.0
+        achieved = g_fl / (g_ms / 1e3) / 1e12
+        roof = {"kernel": "gemm_tc_kernel (tcgen05 bf16, fused epilogues)" if numerics == kb.FAST else "gemm_f64acc",
+                "bound": "tensor", "achieved": achieved, "peak": tensor_peak, "unit": "TFLOP/s",
+                "frac": achieved / tensor_peak, "traffic": None, "peak_source": src + " (bf16 sustained)",
+                "per_launch_ms": g_ms / max(g_n, 1), "hbm_gbs_achieved": g_by / (g_ms / 1e3) / 1e9}
+    else:
+        achieved = a_fl / (a_ms / 1e3) / 1e12
+        roof = {"kernel": "attention+summary (K5)", "bound": "tensor", "achieved": achieved,
+                "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops_sustained"],
+                "traffic": None, "peak_source": src}
+    launches = int(sum(v["kernels"] for v in prof.values())) // max(args.steps, 1)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        s = cpu_sample(cfg)
+        plan = steps[-1]["plan"]
+        ex = cpu_extrapolate(s, cfg, steps[-1]["rows_per_layer"], attention_pairs(layout, len(query), plan))
+        cpu = {"value": ex["tokens_per_s"], "unit": UNIT, "cores": 1, "kind": s["kind"], "sample": s["sample"],
+               "ttft_ms_extrapolated": ex["ttft_s"] * 1e3, "sample_seconds": s["seconds"]}
+
+    if rank == 0:
+        plan = steps[-1]["plan"]
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": "bf16" if numerics == kb.FAST else "f32-store/f64-acc", "data": "synthetic",
+            "ttft_ms": float(np.median(ttft)), "ttft_ms_min": float(np.min(ttft)),
+            "config": {"workload": args.config, "desc": cfg["desc"], "L": L, "H": H, "d": d, "mlp": mlp, "V": V,
+                       "S": layout.S, "T": int(np.sum(layout.seg_len)) + len(query),
+                       "units": {"static_groups_of_8": sum(1 for u in layout.units if u[2] == 1),
+                                 "dynamic_segments": sum(1 for u in layout.units if u[2] == 0)},
+                       "r_avg": cfg["r_avg"], "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs larger than L2 (26.8 GB bf16 weights + 16 GB merged KV per step)",
+                       "memory_kv": "HBM-resident canonical KV (static groups joint, dynamic per segment)"},
+            "recomputed_tokens_per_step": tokens,
+            "plan_segments_per_layer": [int(x) for x in plan.sum(1)],
+            "rows_per_layer": [int(x) for x in steps[-1]["rows_per_layer"]],
+            "hops_per_layer": [int(x) for x in steps[-1]["hops"]],
+            "phase_ms_per_step": phase_ms,
+            "setup_s": {"model_init": t_init, "canonical_kv_refresh": t_mem},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ttft_ms": float(np.mean(e2e_s)) * 1e3},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--numerics", choices=["fast", "parity"], default="fast")
+    ap.add_argument("--r-avg", type=float, default=None)
+    ap.add_argument("--seed", type=int, default=20250807)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.r_avg is not None:
+        cfg["r_avg"] = args.r_avg
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, cfg)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    run_ours(args, cfg, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

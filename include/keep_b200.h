@@ -189,6 +189,32 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query,
 
 int keep_logits(void* ctx, const float* row, double* out);
 
+/* ---- per-phase device timing (CUDA events on the launching streams) ----- */
+enum {
+    KEEP_PROF_QKV = 0,      /* gathered QKV GEMM + K/V scatter (K3)          */
+    KEEP_PROF_ATTN = 1,     /* attention + segment binning (K5)              */
+    KEEP_PROF_WO = 2,       /* Wo GEMM + residual (K8)                       */
+    KEEP_PROF_MLP_IN = 3,   /* MLP in + ReLU (K9a)                           */
+    KEEP_PROF_MLP_OUT = 4,  /* MLP out + residual (K9b)                      */
+    KEEP_PROF_SUMMARY = 5,  /* row bins -> segment summary (K6)              */
+    KEEP_PROF_SELECT = 6,   /* multi-hop selector (K7)                       */
+    KEEP_PROF_CACHED = 7,   /* merged-KV assembly from cached blocks (K4)    */
+    KEEP_PROF_COMPACT = 8,  /* active-row compaction (K2)                    */
+    KEEP_PROF_EMBED = 9,    /* embedding gather (K1)                         */
+    KEEP_PROF_LOGITS = 10,  /* last-row logits (K11)                         */
+    KEEP_PROF_LOADER = 11,  /* host->HBM layer loads (K10)                   */
+    KEEP_PROF_COUNT = 16
+};
+typedef struct {
+    double ms[16];          /* summed device time                          */
+    double flops[16];       /* algorithmic FLOPs                           */
+    double bytes[16];       /* algorithmic HBM bytes                       */
+    int64_t launches[16];   /* timed regions (one per phase per layer)     */
+    int64_t kernels[16];    /* kernel launches inside them                 */
+} keep_profile;
+int keep_profile_enable(void* ctx, int32_t on);
+int keep_profile_read(void* ctx, keep_profile* out, int32_t reset);
+
 /* ---- test hook (not part of the reference surface) ----------------------
  * C[M x N] (fp32, device) = A[M x K] . Bt[N x K]^T with bf16 device operands
  * on the tcgen05 GEMM; force_bn 0 = automatic tile, 64 or 256 = forced. */

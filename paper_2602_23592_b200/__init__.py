@@ -72,6 +72,15 @@ class keep_memory_stats(C.Structure):
                 ("device_bytes", C.c_uint64), ("host_bytes", C.c_uint64)]
 
 
+class keep_profile(C.Structure):
+    _fields_ = [("ms", C.c_double * 16), ("flops", C.c_double * 16), ("bytes", C.c_double * 16),
+                ("launches", C.c_int64 * 16), ("kernels", C.c_int64 * 16)]
+
+
+PROFILE_PHASES = ["qkv", "attn", "wo", "mlp_in", "mlp_out", "summary", "select", "cached_kv", "compact",
+                  "embed", "logits", "loader"]
+
+
 class keep_plan_result(C.Structure):
     _fields_ = [("plan", C.POINTER(C.c_uint8)), ("orders", C.POINTER(C.c_int32)),
                 ("order_len", C.POINTER(C.c_int32)), ("hops", C.POINTER(C.c_int32)),
@@ -124,6 +133,8 @@ def load_library() -> C.CDLL:
                                      C.POINTER(keep_plan_result)]),
         "keep_logits": (C.c_int, [vp, fp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+        "keep_profile_enable": (C.c_int, [vp, i32]),
+        "keep_profile_read": (C.c_int, [vp, C.POINTER(keep_profile), i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -243,6 +254,17 @@ class Context:
         out = np.empty(self.V, np.float64)
         _check(self.lib.keep_logits(self._h, _p(row, C.c_float), _p(out, C.c_double)))
         return out
+
+    # -- per-phase device timing --------------------------------------------
+    def profile_enable(self, on=True):
+        _check(self.lib.keep_profile_enable(self._h, int(bool(on))))
+
+    def profile_read(self, reset=True) -> dict:
+        pr = keep_profile()
+        _check(self.lib.keep_profile_read(self._h, C.byref(pr), int(bool(reset))))
+        return {name: {"ms": pr.ms[i], "flops": pr.flops[i], "bytes": pr.bytes[i],
+                       "launches": int(pr.launches[i]), "kernels": int(pr.kernels[i])}
+                for i, name in enumerate(PROFILE_PHASES)}
 
     # -- memory tier (load_memory) ----------------------------------------
     def memory_put(self, kind, oid, version, layer, keys, values, tier=TIER_DEVICE):

@@ -95,6 +95,55 @@ void DevBuf::alloc(size_t nbytes, bool pinned_host) {
     host = pinned_host;
 }
 
+cudaEvent_t Profiler::get() {
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    KEEP_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void Profiler::collect() {
+    for (auto& r : pending) {
+        KEEP_CUDA(cudaEventSynchronize(r.b));
+        float ms = 0.f;
+        KEEP_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+        acc.ms[r.cat] += ms;
+        acc.flops[r.cat] += r.flops;
+        acc.bytes[r.cat] += r.bytes;
+        acc.launches[r.cat] += 1;
+        acc.kernels[r.cat] += r.kernels;
+        pool.push_back(r.a);
+        pool.push_back(r.b);
+    }
+    pending.clear();
+}
+
+Profiler::~Profiler() {
+    for (auto& r : pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+}
+
+ProfScope::ProfScope(Profiler& prof, int c, cudaStream_t s, double fl, double by, int nk)
+    : p(prof.on ? &prof : nullptr), cat(c), st(s), flops(fl), bytes(by), kernels(nk) {
+    if (!p) return;
+    a = p->get();
+    KEEP_CUDA(cudaEventRecord(a, st));
+}
+
+ProfScope::~ProfScope() {
+    if (!p) return;
+    cudaEvent_t b = p->get();
+    if (cudaEventRecord(b, st) != cudaSuccess) return;
+    p->pending.push_back(Profiler::Rec{cat, a, b, flops, bytes, kernels});
+}
+
 }  // namespace keep_b200
 
 namespace {
@@ -263,9 +312,19 @@ void ensure_layer_scratch(Context& c, Pass& p) {
     if (p.with_summary) p.rowbin.ensure((c.fast ? 4 : 8) * n * std::max(p.S, 1));
 }
 
+// Algorithmic attention work of a layer: sum over computed rows of visible keys.
+double visible_pairs(const Pass& p) {
+    double s = 0.0;
+    for (int32_t r : p.rows_h) s += double(r + 1 - (p.block_diag ? p.key_lo_h[r] : 0));
+    return s;
+}
+
 // One transformer layer over the compact rows of a pass
 // (PrefillCursor::step body, prefill.hpp:245-304 minus the cached copy).
-void run_layer(Context& c, Pass& p, int l) {
+// after_summary runs once the layer's segment summary is complete (the
+// selector for layer l+1 overlaps this layer's Wo + MLP; SPEC D2).
+template <class AfterSummary>
+void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
     const int n = p.n, d = c.d, f = c.f;
     cudaStream_t st = c.s_main;
     if (n == 0) return;
@@ -296,31 +355,44 @@ void run_layer(Context& c, Pass& p, int l) {
     a.o_part = p.o_part.as<double>();
     a.rowbin = p.rowbin.p;
 
+    const double wb = c.fast ? 2.0 : 4.0;  // weight / activation element bytes
+    const double gq = 2.0 * n * 3.0 * d * d, go = 2.0 * n * double(d) * d, gi = 2.0 * n * double(d) * f;
+    const double bq = wb * (3.0 * d * d + n * double(d)) + c.elem * 3.0 * n * d;
+    const double bo = wb * (double(d) * d + n * double(d)) + 8.0 * n * d;
+    const double bi = wb * (double(d) * f + n * double(d) + n * double(f));
+    const double bout = wb * (double(d) * f + n * double(f)) + 8.0 * n * d;
+    const double pairs = visible_pairs(p);
+    // algorithmic attention: QK^T and PV over visible keys; K+V of the layer read once
+    const double fa = 4.0 * d * pairs, ba = double(c.elem) * (2.0 * p.T * d + 2.0 * n * d);
+
     if (!c.fast) {
-        EpiArgs e{EPI_QKV, d, p.q.as<float>(), d, p.kdst[l], p.vdst[l], rows, nullptr};
-        launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * d, n, 3 * d, d, e, st);
+        {
+            ProfScope ps(c.prof, KEEP_PROF_QKV, st, gq, bq);
+            EpiArgs e{EPI_QKV, d, p.q.as<float>(), d, p.kdst[l], p.vdst[l], rows, nullptr};
+            launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * d, n, 3 * d, d, e, st);
+        }
         a.q = p.q.p;
         a.ctx = p.ctx.as<float>();
-        launch_attention_parity(a, st);
-        EpiArgs eo{EPI_RESID, d, p.x.as<float>(), d, nullptr, nullptr, nullptr, nullptr};
-        launch_gemm_f64acc(p.ctx.as<float>(), d, static_cast<const float*>(c.wslot(l, W_O)), d, n, d, d, eo, st);
-        EpiArgs ei{EPI_RELU, d, p.h.as<float>(), f, nullptr, nullptr, nullptr, nullptr};
-        launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_IN)), f, n, f, d, ei, st);
-        launch_gemm_f64acc(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, n, d, f, eo, st);
+        {
+            ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, 5);
+            launch_attention_parity(a, st);
+        }
     } else {
         auto* xb = p.xb.as<__nv_bfloat16>();
-        EpiArgs e{EPI_QKV, d, nullptr, d, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
-        launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_QKV)), d, n, 3 * d, d, e, st);
+        {
+            ProfScope ps(c.prof, KEEP_PROF_QKV, st, gq, bq);
+            EpiArgs e{EPI_QKV, d, nullptr, d, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
+            launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_QKV)), d, n, 3 * d, d, e, st);
+        }
         a.q = p.q.p;
         a.ctx_bf16 = p.ctxb.as<__nv_bfloat16>();
-        launch_attention_fast(a, st);
-        EpiArgs eo{EPI_RESID, d, p.x.as<float>(), d, nullptr, nullptr, nullptr, xb};
-        launch_gemm_bf16(p.ctxb.as<__nv_bfloat16>(), d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_O)), d, n, d, d, eo, st);
-        EpiArgs ei{EPI_RELU, d, nullptr, f, nullptr, nullptr, nullptr, p.hb.as<__nv_bfloat16>()};
-        launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_IN)), d, n, f, d, ei, st);
-        launch_gemm_bf16(p.hb.as<__nv_bfloat16>(), f, static_cast<const __nv_bfloat16*>(c.wslot(l, W_OUT)), f, n, d, f, eo, st);
+        {
+            ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, 5);
+            launch_attention_fast(a, st);
+        }
     }
     if (p.with_summary) {
+        ProfScope ps(c.prof, KEEP_PROF_SUMMARY, st, 0.0, (c.fast ? 4.0 : 8.0) * n * double(p.S) + 8.0 * p.S * double(p.S));
         // compact row range per segment (rows of a segment are contiguous)
         std::vector<int32_t> cb(p.S, 0), ce(p.S, 0);
         int qb = n, qe = n;
@@ -347,6 +419,46 @@ void run_layer(Context& c, Pass& p, int l) {
             launch_summary_reduce<float>(p.rowbin.as<float>(), p.S, p.seg_cbeg.as<int32_t>(), p.seg_cend.as<int32_t>(),
                                          p.d_seg_len.as<int32_t>(), qb, qe, p.qlen, p.summ.as<double>(), st);
     }
+    after_summary();
+    if (!c.fast) {
+        EpiArgs eo{EPI_RESID, d, p.x.as<float>(), d, nullptr, nullptr, nullptr, nullptr};
+        {
+            ProfScope ps(c.prof, KEEP_PROF_WO, st, go, bo);
+            launch_gemm_f64acc(p.ctx.as<float>(), d, static_cast<const float*>(c.wslot(l, W_O)), d, n, d, d, eo, st);
+        }
+        {
+            ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
+            EpiArgs ei{EPI_RELU, d, p.h.as<float>(), f, nullptr, nullptr, nullptr, nullptr};
+            launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_IN)), f, n, f, d, ei, st);
+        }
+        {
+            ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
+            launch_gemm_f64acc(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, n, d, f, eo, st);
+        }
+    } else {
+        auto* xb = p.xb.as<__nv_bfloat16>();
+        const int mc = c.gemm_ctas;
+        EpiArgs eo{EPI_RESID, d, p.x.as<float>(), d, nullptr, nullptr, nullptr, xb};
+        {
+            ProfScope ps(c.prof, KEEP_PROF_WO, st, go, bo);
+            launch_gemm_bf16(p.ctxb.as<__nv_bfloat16>(), d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_O)), d, n, d, d, eo,
+                             st, mc);
+        }
+        {
+            ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
+            EpiArgs ei{EPI_RELU, d, nullptr, f, nullptr, nullptr, nullptr, p.hb.as<__nv_bfloat16>()};
+            launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_IN)), d, n, f, d, ei, st, mc);
+        }
+        {
+            ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
+            launch_gemm_bf16(p.hb.as<__nv_bfloat16>(), f, static_cast<const __nv_bfloat16*>(c.wslot(l, W_OUT)), f, n, d, f, eo,
+                             st, mc);
+        }
+    }
+}
+
+void run_layer(Context& c, Pass& p, int l) {
+    run_layer(c, p, l, [] {});
 }
 
 // Replace the compact row set (rows only shrink): gather the residual rows.
@@ -363,6 +475,7 @@ void set_rows(Context& c, Pass& p, const std::vector<int32_t>& rows_new, bool fi
             idx[i] = int32_t(j);
         }
         upload(p.d_idx, idx, st);
+        ProfScope ps(c.prof, KEEP_PROF_COMPACT, st, 0.0, double(n_new) * c.d * (8.0 + (c.fast ? 2.0 : 0.0)));
         p.x_alt.ensure(sizeof(float) * size_t(std::max(n_new, 1)) * c.d);
         launch_gather_rows(p.x.as<float>(), p.d_idx.as<int32_t>(), n_new, c.d, p.x_alt.as<float>(),
                            c.fast ? p.xb.as<__nv_bfloat16>() : nullptr, st);
@@ -406,6 +519,7 @@ void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const i
     p.x.ensure(sizeof(float) * size_t(std::max(p.T, 1)) * c.d);
     if (c.fast) p.xb.ensure(2 * size_t(std::max(p.T, 1)) * c.d);
     set_rows(c, p, all, true);
+    ProfScope ps(c.prof, KEEP_PROF_EMBED, st, 0.0, double(p.T) * c.d * (8.0 + (c.fast ? 2.0 : 0.0)), c.fast ? 2 : 1);
     launch_embed(c.embed.as<float>(), p.d_tokens.as<int32_t>(), p.d_rows.as<int32_t>(), p.T, c.d,
                  p.x.as<float>(), st);
     if (c.fast) launch_to_bf16(p.x.as<float>(), int64_t(p.T) * c.d, p.xb.as<__nv_bfloat16>(), st);
@@ -415,7 +529,8 @@ void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const i
 }
 
 // ------------------------------------------------------------------ cursor --
-void cursor_layer(Context& c, const uint8_t* active, bool keep_summary) {
+template <class AfterSummary>
+void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summary) {
     Pass& p = *c.pf;
     const int S = p.S, l = p.layer;
     if (l >= c.L) raise(KEEP_ERR_PLAN, "stepped past last layer");  // prefill.hpp:227
@@ -456,6 +571,9 @@ void cursor_layer(Context& c, const uint8_t* active, bool keep_summary) {
     set_rows(c, p, rows_new, false);
     cudaStream_t st = c.s_main;
     if (!ks.empty()) {
+        double rows_copied = 0.0;
+        for (int32_t r : nr) rows_copied += r;
+        ProfScope ps(c.prof, KEEP_PROF_CACHED, st, 0.0, rows_copied * c.d * c.elem * 4.0);
         upload(c.d_ksrc, ks, st);
         upload(c.d_vsrc, vs, st);
         upload(c.d_cdst, dr, st);
@@ -465,14 +583,19 @@ void cursor_layer(Context& c, const uint8_t* active, bool keep_summary) {
                            maxr, st);
     }
     p.with_summary = true;
-    run_layer(c, p, l);
     if (p.n == 0) {  // no computed rows: the summary is all zero
         p.summ.ensure(sizeof(double) * (size_t(S) + size_t(S) * S));
         KEEP_CUDA(cudaMemsetAsync(p.summ.p, 0, sizeof(double) * (size_t(S) + size_t(S) * S), st));
+        after_summary();
+    } else {
+        run_layer(c, p, l, after_summary);
     }
-    (void)keep_summary;
     std::copy(active, active + S, p.prev.begin());
     p.layer++;
+}
+
+void cursor_layer(Context& c, const uint8_t* active) {
+    cursor_layer(c, active, [] {});
 }
 
 void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int qlen) {
@@ -890,7 +1013,7 @@ int keep_prefill_layer(void* ctx, const uint8_t* active, double* summary_out) {
     return guard([&] {
         Context& c = *C(ctx);
         if (!c.pf) raise(KEEP_ERR_PLAN, "no prefill in progress");
-        cursor_layer(c, active, summary_out != nullptr);
+        cursor_layer(c, active);
         if (summary_out) {
             const size_t ns = size_t(c.pf->S) + size_t(c.pf->S) * c.pf->S;
             KEEP_CUDA(cudaMemcpyAsync(summary_out, c.pf->summ.p, sizeof(double) * ns, cudaMemcpyDeviceToHost, c.s_main));
@@ -970,6 +1093,21 @@ int64_t keep_layer_budget(double ratio, int64_t S) {  // recompute.hpp:73-77
     return std::max<int64_t>(1, b);
 }
 
+int keep_profile_enable(void* ctx, int32_t on) {
+    return guard([&] { C(ctx)->prof.on = on != 0; });
+}
+
+int keep_profile_read(void* ctx, keep_profile* out, int32_t reset) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+        KEEP_CUDA(cudaStreamSynchronize(c.s_sel));
+        c.prof.collect();
+        *out = c.prof.acc;
+        if (reset) c.prof.acc = keep_profile{};
+    });
+}
+
 int keep_logits(void* ctx, const float* row, double* out) {
     return guard([&] {
         Context& c = *C(ctx);
@@ -1007,32 +1145,63 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
         std::vector<uint8_t> active(S, 1);
         c.sel_order.ensure(sizeof(int32_t) * (S + 2));
         c.sel_cand.ensure(std::max(S, 1));
-        std::vector<int32_t> hbuf(S + 2);
+        int32_t* hbuf = nullptr;  // pinned: the async D2H of the walk must not stage
+        KEEP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hbuf), sizeof(int32_t) * (S + 2), cudaHostAllocDefault));
+        struct HostFree {
+            int32_t* p;
+            ~HostFree() { cudaFreeHost(p); }
+        } hf{hbuf};
+        cudaEvent_t ev_sum, ev_sel;
+        KEEP_CUDA(cudaEventCreateWithFlags(&ev_sum, cudaEventDisableTiming));
+        KEEP_CUDA(cudaEventCreateWithFlags(&ev_sel, cudaEventDisableTiming));
+        struct EvFree {
+            cudaEvent_t a, b;
+            ~EvFree() {
+                cudaEventDestroy(a);
+                cudaEventDestroy(b);
+            }
+        } ef{ev_sum, ev_sel};
         for (int l = 0; l < L; ++l) {
             if (out && out->plan) std::copy(active.begin(), active.end(), out->plan + size_t(l) * S);
             if (out && out->order_len) out->order_len[l] = -1;
             if (out && out->hops) out->hops[l] = 0;
-            cursor_layer(c, active.data(), true);
+            int64_t budget = 0, live = 0;
+            if (l + 1 < L) {
+                budget = keep_layer_budget(sched[l + 1], S);
+                for (uint8_t x : active) live += x;
+            }
+            const bool walk = l + 1 < L && budget < live && multihop;
+            // the walk for layer l+1 runs on the selector stream as soon as the
+            // summary of layer l exists, overlapping this layer's Wo + MLP
+            auto launch_walk = [&] {
+                if (!walk) return;
+                KEEP_CUDA(cudaMemcpyAsync(c.sel_cand.p, active.data(), S, cudaMemcpyHostToDevice, c.s_sel));
+                KEEP_CUDA(cudaEventRecord(ev_sum, st));
+                KEEP_CUDA(cudaStreamWaitEvent(c.s_sel, ev_sum, 0));
+                int32_t* o = c.sel_order.as<int32_t>();
+                {
+                    ProfScope ps(c.prof, KEEP_PROF_SELECT, c.s_sel, 0.0, 8.0 * double(S) * S);
+                    launch_select(S, p.summ.as<double>(), p.summ.as<double>() + S, budget, c.sel_cand.as<uint8_t>(), o + 2,
+                                  o, o + 1, c.s_sel);
+                }
+                KEEP_CUDA(cudaMemcpyAsync(hbuf, o, sizeof(int32_t) * (S + 2), cudaMemcpyDeviceToHost, c.s_sel));
+                KEEP_CUDA(cudaEventRecord(ev_sel, c.s_sel));
+            };
+            c.gemm_ctas = walk ? kNumSMs - 1 : kNumSMs;
+            cursor_layer(c, active.data(), launch_walk);
+            c.gemm_ctas = kNumSMs;
             if (out && out->rows_per_layer) out->rows_per_layer[l] = p.n;
             if (out && out->summaries)
                 KEEP_CUDA(cudaMemcpyAsync(out->summaries + size_t(l) * (S + size_t(S) * S), p.summ.p,
                                           sizeof(double) * (S + size_t(S) * S), cudaMemcpyDeviceToHost, st));
             KEEP_CUDA(cudaEventRecord(evs[l + 1], st));
             if (l + 1 >= L) break;
-            const int64_t budget = keep_layer_budget(sched[l + 1], S);
-            int64_t live = 0;
-            for (uint8_t a : active) live += a;
             if (budget >= live) continue;  // recompute everything still live
             std::vector<uint8_t> next(S, 0);
             if (multihop) {
-                KEEP_CUDA(cudaMemcpyAsync(c.sel_cand.p, active.data(), S, cudaMemcpyHostToDevice, st));
-                int32_t* o = c.sel_order.as<int32_t>();
-                launch_select(S, p.summ.as<double>(), p.summ.as<double>() + S, budget, c.sel_cand.as<uint8_t>(), o + 2, o,
-                              o + 1, st);
-                KEEP_CUDA(cudaMemcpyAsync(hbuf.data(), o, sizeof(int32_t) * (S + 2), cudaMemcpyDeviceToHost, st));
-                KEEP_CUDA(cudaStreamSynchronize(st));
+                KEEP_CUDA(cudaEventSynchronize(ev_sel));
                 for (int k = 0; k < hbuf[0]; ++k) next[hbuf[2 + k]] = 1;
-                if (out && out->orders) std::copy(hbuf.begin() + 2, hbuf.begin() + 2 + hbuf[0], out->orders + size_t(l) * S);
+                if (out && out->orders) std::copy(hbuf + 2, hbuf + 2 + hbuf[0], out->orders + size_t(l) * S);
                 if (out && out->order_len) out->order_len[l] = hbuf[0];
                 if (out && out->hops) out->hops[l] = hbuf[1];
             } else {  // single-hop ablation (recompute.hpp:166-176)
@@ -1056,7 +1225,10 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
             KEEP_CUDA(cudaMemsetAsync(zero.p, 0, sizeof(float) * c.d, st));
             lr = zero.as<float>();
         }
-        launch_logits(lr, c.unembed.as<float>(), c.d, c.V, c.logits.as<double>(), st);
+        {
+            ProfScope ps(c.prof, KEEP_PROF_LOGITS, st, 2.0 * c.d * double(c.V), 4.0 * c.d * double(c.V));
+            launch_logits(lr, c.unembed.as<float>(), c.d, c.V, c.logits.as<double>(), st);
+        }
         KEEP_CUDA(cudaEventRecord(c.ev_b, st));
         if (out && out->last_logits)
             KEEP_CUDA(cudaMemcpyAsync(out->last_logits, c.logits.p, sizeof(double) * c.V, cudaMemcpyDeviceToHost, st));

@@ -11,8 +11,39 @@ namespace keep_b200 {
 
 // FAST-mode projection GEMM on the tcgen05 tensor cores:
 // C[M x N] = A[M x K] (bf16 row-major) . Bt[N x K]^T (bf16, K-major rows).
+// max_ctas < 148 leaves SMs free for a concurrently running selector.
 void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb,
-                      int M, int N, int K, const EpiArgs& epi, cudaStream_t st);
+                      int M, int N, int K, const EpiArgs& epi, cudaStream_t st, int max_ctas = kNumSMs);
+
+// Per-phase CUDA-event timing (keep_profile_*).
+struct Profiler {
+    bool on = false;
+    struct Rec {
+        int cat;
+        cudaEvent_t a, b;
+        double flops, bytes;
+        int kernels;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    keep_profile acc{};
+    cudaEvent_t get();
+    void collect();  // synchronises the recorded events
+    ~Profiler();
+};
+
+struct Context;
+// RAII region: events on `st` around the launches of one phase.
+struct ProfScope {
+    Profiler* p;
+    int cat;
+    cudaStream_t st;
+    double flops, bytes;
+    int kernels;
+    cudaEvent_t a = nullptr;
+    ProfScope(Profiler& prof, int c, cudaStream_t s, double fl, double by, int nk = 1);
+    ~ProfScope();
+};
 
 // Device buffer with RAII.
 struct DevBuf {
@@ -100,6 +131,8 @@ struct Context {
     // selector scratch
     DevBuf sel_order, sel_n, sel_cand;
     DevBuf logits;
+    Profiler prof;
+    int gemm_ctas = kNumSMs;  // 147 while the selector overlaps the MLP
 
     void* wslot(int l, int slot) const { return w[l * 4 + slot]->p; }
 };

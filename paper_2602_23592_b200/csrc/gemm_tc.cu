@@ -348,7 +348,7 @@ CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, in
 
 template <int BN>
 void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
-               const EpiArgs& epi, cudaStream_t st) {
+               const EpiArgs& epi, cudaStream_t st, int max_ctas = kNumSMs) {
     using CF = Cfg<BN>;
     static bool attr = false;
     if (!attr) {
@@ -358,7 +358,7 @@ void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int
     const CUtensorMap ta = make_map(A, M, K, lda, BM);
     const CUtensorMap tb = make_map(Bt, N, K, ldb, BN);
     const int ntiles = int(ceil_div(M, BM) * ceil_div(N, BN));
-    const int grid = std::min(ntiles, kNumSMs);
+    const int grid = std::min(ntiles, std::max(1, std::min(max_ctas, kNumSMs)));
     gemm_tc_kernel<BN><<<grid, kThreads, CF::SMEM, st>>>(ta, tb, M, N, K, epi);
     KEEP_LAUNCH_CHECK();
 }
@@ -366,14 +366,14 @@ void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int
 }  // namespace
 
 void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
-                      const EpiArgs& epi, cudaStream_t st) {
+                      const EpiArgs& epi, cudaStream_t st, int max_ctas) {
     if (M == 0 || N == 0) return;
     if (K % BK != 0 || N % 32 != 0) raise(KEEP_ERR_CONFIG, "tcgen05 GEMM needs K % 64 == 0 and N % 32 == 0");
     // few row blocks: narrow N tiles so enough CTAs stream the weights
     if (ceil_div(M, BM) * ceil_div(N, 256) >= kNumSMs || N % 256 != 0)
-        launch_bn<256>(A, lda, Bt, ldb, M, N, K, epi, st);
+        launch_bn<256>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas);
     else
-        launch_bn<64>(A, lda, Bt, ldb, M, N, K, epi, st);
+        launch_bn<64>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas);
 }
 
 }  // namespace keep_b200
