@@ -255,11 +255,40 @@ void need_weights(const Context& c) {
 // ----------------------------------------------------------------- passes --
 // Segment-aligned key splits so that every (row, destination segment) bin is
 // produced by exactly one CTA (deterministic, no atomics).
+// KEEP_ATTN_SIMT=1 forces the CUDA-core attention in FAST mode (A/B checks).
+bool use_tc_attention(const Context& c) {
+    static const bool simt = [] {
+        const char* e = std::getenv("KEEP_ATTN_SIMT");
+        return e && *e == '1';
+    }();
+    return c.fast && c.dh == 128 && !simt;
+}
+
 void plan_splits(Context& c, Pass& p) {
-    const int tiles = int(ceil_div(p.n, 16));
+    const bool tc = use_tc_attention(c);
+    const int tiles = int(ceil_div(p.n, tc ? 128 : 16));
     int nsplit = 1;
+    if (tc && !p.block_diag) {
+        // stats / context: unaligned splits, ~2 waves of (tile, head, split) CTAs
+        const int na = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * kNumSMs, int64_t(tiles) * c.H),
+                                                                  ceil_div(p.T, 1024))));
+        std::vector<int32_t> lo, hi;
+        const int64_t step = ceil_div(ceil_div(p.T, na), 128) * 128;
+        for (int64_t k = 0; k < p.T; k += step) {
+            lo.push_back(int32_t(k));
+            hi.push_back(int32_t(std::min<int64_t>(p.T, k + step)));
+        }
+        upload(p.split_lo_a, lo, c.s_main);
+        upload(p.split_hi_a, hi, c.s_main);
+        p.split_count_a = int(lo.size());
+    } else {
+        std::vector<int32_t> lo{0}, hi{p.T};
+        upload(p.split_lo_a, lo, c.s_main);
+        upload(p.split_hi_a, hi, c.s_main);
+        p.split_count_a = 1;
+    }
     if (!p.block_diag) {
-        const int target = 4 * kNumSMs;
+        const int target = tc ? 2 * kNumSMs : 4 * kNumSMs;
         nsplit = int(std::min<int64_t>(ceil_div(target, tiles), std::max(1, p.T / 128)));
         // bound the fp64 partial-context scratch to ~512 MB
         const int64_t per_split = int64_t(p.n) * c.d * 8;
@@ -290,11 +319,13 @@ void plan_splits(Context& c, Pass& p) {
     upload(p.split_lo, lo, c.s_main);
     upload(p.split_hi, hi, c.s_main);
     const int ns = int(lo.size());
-    p.m_part.ensure(sizeof(double) * size_t(ns) * p.n * c.H);
-    p.l_part.ensure(sizeof(double) * size_t(ns) * p.n * c.H);
+    const int nm = std::max(ns, p.split_count_a);
+    p.m_part.ensure(sizeof(double) * size_t(nm) * p.n * c.H);
+    p.l_part.ensure(sizeof(double) * size_t(nm) * p.n * c.H);
     p.m_fin.ensure(sizeof(double) * size_t(p.n) * c.H);
     p.l_fin.ensure(sizeof(double) * size_t(p.n) * c.H);
-    if (ns > 1) p.o_part.ensure(sizeof(double) * size_t(ns) * p.n * c.d);
+    if (ns > 1 && !tc) p.o_part.ensure(sizeof(double) * size_t(ns) * p.n * c.d);
+    if (tc && p.split_count_a > 1) p.o_part.ensure(sizeof(float) * size_t(p.split_count_a) * p.n * c.d);
     p.split_count = ns;
 }
 
@@ -309,7 +340,7 @@ void ensure_layer_scratch(Context& c, Pass& p) {
         p.ctxb.ensure(2 * n * c.d);
         p.hb.ensure(2 * n * c.f);
     }
-    if (p.with_summary) p.rowbin.ensure((c.fast ? 4 : 8) * n * std::max(p.S, 1));
+    if (p.with_summary && !use_tc_attention(c)) p.rowbin.ensure((c.fast ? 4 : 8) * n * std::max(p.S, 1));
 }
 
 // Algorithmic attention work of a layer: sum over computed rows of visible keys.
@@ -386,12 +417,48 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
         }
         a.q = p.q.p;
         a.ctx_bf16 = p.ctxb.as<__nv_bfloat16>();
-        {
+        if (use_tc_attention(c)) {
+            ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, p.split_count_a > 1 ? 6 : 5);
+            p.vt.ensure(2 * size_t(d) * size_t(ceil_div(p.T, 64) * 64));
+            AttnTcLaunch t{};
+            t.n = n;
+            t.T = p.T;
+            t.H = c.H;
+            t.d = d;
+            t.S = p.S;
+            t.q = p.q.p;
+            t.k = p.kdst[l];
+            t.v = p.vdst[l];
+            t.vt = p.vt.as<__nv_bfloat16>();
+            t.rows = rows;
+            t.row_seg = p.d_row_seg.as<int32_t>();
+            t.key_lo = a.key_lo;
+            t.with_bins = p.with_summary;
+            t.nsplit_a = p.split_count_a;
+            t.split_lo_a = p.split_lo_a.as<int32_t>();
+            t.split_hi_a = p.split_hi_a.as<int32_t>();
+            t.m_part = p.m_part.as<float>();
+            t.l_part = p.l_part.as<float>();
+            t.m_fin = p.m_fin.as<float>();
+            t.inv_l = p.l_fin.as<float>();
+            t.o_part = p.o_part.as<float>();
+            t.ctx = p.ctxb.as<__nv_bfloat16>();
+            if (p.with_summary) {
+                const size_t ns = size_t(p.S) + size_t(p.S) * p.S;
+                p.summ_raw.ensure(sizeof(double) * ns);
+                p.summ.ensure(sizeof(double) * ns);
+                t.summ_raw = p.summ_raw.as<double>();
+                t.summ = p.summ.as<double>();
+            }
+            t.seg_len = p.d_seg_len.as<int32_t>();
+            t.qlen = p.qlen;
+            launch_attention_tc(t, st);
+        } else {
             ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, 5);
             launch_attention_fast(a, st);
         }
     }
-    if (p.with_summary) {
+    if (p.with_summary && !use_tc_attention(c)) {  // (the tensor-core path bins inside attention)
         ProfScope ps(c.prof, KEEP_PROF_SUMMARY, st, 0.0, (c.fast ? 4.0 : 8.0) * n * double(p.S) + 8.0 * p.S * double(p.S));
         // compact row range per segment (rows of a segment are contiguous)
         std::vector<int32_t> cb(p.S, 0), ce(p.S, 0);
@@ -627,8 +694,12 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
         for (int i = 0; i < S; ++i)
             if (covered[i] != 1) raise(KEEP_ERR_INPUT, "units must partition the layout");
     }
-    c.pf.reset(new Pass());
+    // the workspace persists across prefills: buffers only grow (no per-step
+    // cudaMalloc / cudaFree on the TTFT path)
+    if (!c.pf) c.pf.reset(new Pass());
     Pass& p = *c.pf;
+    p.block_diag = false;
+    p.key_lo_h.clear();
     pass_init(c, p, sl, lay->tokens, query, qlen);
     const size_t sheet = size_t(p.T) * c.d * c.elem;
     c.kv.ensure(std::max<size_t>(size_t(c.L) * 2 * sheet, 16));
@@ -698,7 +769,8 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
         seglen.push_back(tot);
     }
     if (rows > INT32_MAX / 2) raise(KEEP_ERR_CONFIG, "refresh batch too large");
-    Pass p;
+    if (!c.refresh) c.refresh.reset(new Pass());
+    Pass& p = *c.refresh;
     p.block_diag = true;
     p.with_summary = false;
     pass_init(c, p, seglen, tokens, nullptr, 0);

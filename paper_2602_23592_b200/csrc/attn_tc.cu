@@ -1,0 +1,548 @@
+// attn_tc.cu -- K5 on the tcgen05 tensor cores (FAST numerics, head_dim 128).
+//
+// The segment summary needs NORMALISED probabilities (prefill.hpp:138-152),
+// so attention runs as two warp-specialised passes over 128-row x 128-key
+// tiles, grid (row tiles, heads, key splits).  Both compute S = Q K^T with
+// tcgen05.mma into TMEM (double buffered: the MMA of chunk i+1 overlaps the
+// softmax of chunk i):
+//
+//   STATS  per-row running max / sum of exp2 (log2 domain) -> partials per
+//          split, combined in split order.
+//   CTX    p = exp2(s - m) / l, written as bf16 into a 128B-swizzled smem tile;
+//          O += P . V with a second tcgen05.mma (V^T staged K-major); O read
+//          back with tcgen05.ld.  The same fp32 p feed the segment summary
+//          (prefill.hpp:266-288): each row thread sums its keys per
+//          destination segment in key order (segment boundaries are the same
+//          for every row of the chunk, so the branches are warp-uniform), the
+//          tile's rows are reduced per source segment through shared memory,
+//          and one fp64 atomic per (source, destination) pair per tile and
+//          head lands in the raw summary (mass on query keys and on the row's
+//          own segment is dropped, prefill.hpp:283-287).
+//
+// Warp roles (256 threads): warp 0 TMA producer, warp 1 MMA issuer, warp 2
+// TMEM allocator, warps 4-7 softmax / summary / epilogue (thread = row = TMEM
+// lane).
+#include "engine.hpp"
+#include "tc_common.cuh"
+
+#include <cfloat>
+
+namespace keep_b200 {
+
+using namespace tc;
+
+namespace {
+
+constexpr int TM = 128;  // rows per tile
+constexpr int TK = 128;  // keys per chunk
+constexpr int DH = 128;  // head dim (two 64-wide swizzle atoms)
+constexpr int NTHR = 256;
+constexpr uint32_t TILE_BYTES = TM * DH * 2;  // 32 KB: [128 x 128] bf16 as 2 boxes of 64 columns
+constexpr uint32_t BOX_BYTES = TILE_BYTES / 2;
+constexpr uint32_t IDESC = instr_desc(128, 128);
+constexpr int PART_STRIDE = 33;               // partial bins: 32 segments per pass (+1 pad)
+
+enum { MODE_STATS = 0, MODE_CTX = 1 };
+
+struct TcArgs {
+    int n, T, H, d, S;
+    int nsplit;
+    const int32_t* split_lo;
+    const int32_t* split_hi;
+    const int32_t* rows;
+    const int32_t* row_seg;
+    const int32_t* key_lo;  // nullable (block-diagonal refresh)
+    float scale_log2;       // log2(e) / sqrt(dh)
+    float inv_heads;
+    float* m_part;          // [nsplit][n][H] log2-domain max
+    float* l_part;          // [nsplit][n][H]
+    const float* m_fin;     // [n][H]
+    const float* inv_l;     // [n][H] 1 / sum
+    float* o_part;          // [nsplit][n][d] (nsplit > 1)
+    __nv_bfloat16* ctx;     // [n][d]
+    double* qts_raw;        // [S]      (nullptr: no summary)
+    double* sts_raw;        // [S x S]
+};
+
+template <int MODE>
+struct Layout {
+    static constexpr int ST = MODE == MODE_STATS ? 4 : 2;  // pipeline stages
+    static constexpr uint32_t STAGE = MODE == MODE_STATS ? TILE_BYTES : 2 * TILE_BYTES;  // K (+ V^T)
+    static constexpr uint32_t Q_OFF = 0;
+    static constexpr uint32_t STAGE_OFF = TILE_BYTES;
+    static constexpr uint32_t P_OFF = STAGE_OFF + ST * STAGE;             // CTX: one P tile
+    static constexpr uint32_t PART_OFF = P_OFF + TILE_BYTES;              // CTX: partial bins [128][33] f32
+    static constexpr uint32_t SEG_OFF = PART_OFF + TM * PART_STRIDE * 4;  // CTX: chunk segments [128] i32
+    static constexpr uint32_t GRP_OFF = SEG_OFF + TK * 4;                 // CTX: row groups [130] i32
+    static constexpr uint32_t MSK_OFF = GRP_OFF + (TM + 2) * 4;           // CTX: boundary mask [4] u32
+    static constexpr uint32_t BAR_OFF = MODE == MODE_CTX ? ((MSK_OFF + 16 + 7) & ~7u) : P_OFF;
+    static constexpr size_t SMEM = size_t(BAR_OFF) + 256 + 1024;
+    static constexpr uint32_t TMEM_COLS = MODE == MODE_CTX ? 512 : 256;
+};
+
+// P tile 16-byte chunk (row r, keys 8*chunk16 .. +8) in the 128B-swizzled
+// K-major layout TMA would produce: box = chunk16 / 8, slot = chunk16 % 8.
+__device__ __forceinline__ uint32_t p_chunk_off(int r, int chunk16) {
+    const int box = chunk16 >> 3, c = chunk16 & 7;
+    return uint32_t(box) * BOX_BYTES + uint32_t(r >> 3) * 1024u + uint32_t(r & 7) * 128u +
+           (uint32_t(c ^ (r & 7)) << 4);
+}
+
+__device__ __forceinline__ uint64_t desc_k(uint32_t tile, int ks) {
+    // k-step ks of 16 elements across the two 64-wide boxes of a tile
+    return smem_desc(tile + uint32_t(ks >> 2) * BOX_BYTES + uint32_t(ks & 3) * 32u);
+}
+
+__device__ __forceinline__ void named_sync_softmax() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+template <int MODE>
+__global__ void __launch_bounds__(NTHR, 1)
+attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+               const __grid_constant__ CUtensorMap tmVt, TcArgs a) {
+    using LY = Layout<MODE>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + LY::BAR_OFF);
+    uint64_t* full = bar;            // [ST]
+    uint64_t* empty = bar + 4;       // [ST]
+    uint64_t* s_full = bar + 8;      // [2]
+    uint64_t* s_empty = bar + 10;    // [2]
+    uint64_t* p_full = bar + 12;
+    uint64_t* p_empty = bar + 13;
+    uint64_t* q_full = bar + 14;
+    uint64_t* o_full = bar + 15;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = blockIdx.x * TM;
+    const int nrows = min(TM, a.n - i0);
+    const int head = blockIdx.y, sp = blockIdx.z;
+    const int tmax = a.rows[i0 + nrows - 1];
+    const int tklo = a.key_lo ? a.key_lo[a.rows[i0]] : 0;
+    const int lo = max(a.split_lo[sp], tklo);
+    const int hi = min(a.split_hi[sp], tmax + 1);
+    // chunk base rounded down to 8 keys: a TMA box may only start on a
+    // 16-byte boundary of the innermost dimension (the V^T loads index keys
+    // there); keys below lo are masked
+    const int kbase = lo & ~7;
+    const int niter = hi > lo ? int(ceil_div(hi - kbase, TK)) : 0;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_map(&tmQ);
+        prefetch_map(&tmK);
+        if (MODE == MODE_CTX) prefetch_map(&tmVt);
+        for (int s = 0; s < LY::ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&s_full[b], 1);
+            mbar_init(&s_empty[b], 4);
+        }
+        mbar_init(p_full, 4);
+        mbar_init(p_empty, 1);
+        mbar_init(q_full, 1);
+        mbar_init(o_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc(tmem_slot, LY::TMEM_COLS);
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tm_s0 = tmem, tm_o = tmem + 256;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ TMA
+        if (lane == 0 && niter > 0) {
+            mbar_expect_tx(q_full, TILE_BYTES);
+            tma_load_2d(sm + LY::Q_OFF, &tmQ, q_full, head * DH, i0);
+            tma_load_2d(sm + LY::Q_OFF + BOX_BYTES, &tmQ, q_full, head * DH + 64, i0);
+            for (int it = 0; it < niter; ++it) {
+                const int s = it % LY::ST;
+                mbar_wait(&empty[s], ((it / LY::ST) & 1) ^ 1);
+                uint8_t* st = sm + LY::STAGE_OFF + s * LY::STAGE;
+                const int k0 = kbase + it * TK;
+                mbar_expect_tx(&full[s], LY::STAGE);
+                tma_load_2d(st, &tmK, &full[s], head * DH, k0);
+                tma_load_2d(st + BOX_BYTES, &tmK, &full[s], head * DH + 64, k0);
+                if (MODE == MODE_CTX) {
+                    tma_load_2d(st + TILE_BYTES, &tmVt, &full[s], k0, head * DH);
+                    tma_load_2d(st + TILE_BYTES + BOX_BYTES, &tmVt, &full[s], k0 + 64, head * DH);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA
+        if (lane == 0 && niter > 0) {
+            mbar_wait(q_full, 0);
+            auto pv = [&](int j) {  // O += P_j . V_j  (CTX only)
+                mbar_wait(p_full, j & 1);
+                fence_after();
+                const uint32_t pt = smem_u32(sm + LY::P_OFF);
+                const uint32_t vt = smem_u32(sm + LY::STAGE_OFF + (j % LY::ST) * LY::STAGE + TILE_BYTES);
+#pragma unroll
+                for (int ks = 0; ks < TK / 16; ++ks)
+                    umma(tm_o, desc_k(pt, ks), desc_k(vt, ks), IDESC, (j | ks) ? 1u : 0u);
+                umma_commit(p_empty);
+                umma_commit(&empty[j % LY::ST]);
+            };
+            const uint32_t qt = smem_u32(sm + LY::Q_OFF);
+            for (int it = 0; it < niter; ++it) {
+                const int s = it % LY::ST, b = it & 1;
+                mbar_wait(&full[s], (it / LY::ST) & 1);
+                mbar_wait(&s_empty[b], ((it >> 1) & 1) ^ 1);
+                fence_after();
+                const uint32_t kt = smem_u32(sm + LY::STAGE_OFF + s * LY::STAGE);
+#pragma unroll
+                for (int ks = 0; ks < DH / 16; ++ks)
+                    umma(tm_s0 + uint32_t(b * TK), desc_k(qt, ks), desc_k(kt, ks), IDESC, ks ? 1u : 0u);
+                umma_commit(&s_full[b]);
+                if (MODE == MODE_STATS) umma_commit(&empty[s]);
+                if (MODE == MODE_CTX && it > 0) pv(it - 1);
+            }
+            if (MODE == MODE_CTX) {
+                pv(niter - 1);
+                umma_commit(o_full);
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------ softmax / summary / epilogue
+        const int q = warp & 3;
+        const int tid = threadIdx.x - 128;
+        const int r = q * 32 + lane;  // tile row == TMEM lane
+        const bool rvalid = r < nrows;
+        const int row = i0 + r;
+        const int t = rvalid ? a.rows[row] : -1;
+        const int klo = max(lo, rvalid && a.key_lo ? a.key_lo[t] : 0);  // first visible key
+        const uint32_t lane_base = uint32_t(q * 32) << 16;
+        float m_run = -FLT_MAX, l_run = 0.f;  // STATS
+        float m_row = 0.f, il_row = 0.f;      // CTX
+        const bool summary = MODE == MODE_CTX && a.sts_raw != nullptr;
+        float* part = reinterpret_cast<float*>(sm + LY::PART_OFF);
+        int32_t* seg_s = reinterpret_cast<int32_t*>(sm + LY::SEG_OFF);
+        int32_t* grp = reinterpret_cast<int32_t*>(sm + LY::GRP_OFF);  // [0]=count, then group row starts
+        uint32_t* bmask = reinterpret_cast<uint32_t*>(sm + LY::MSK_OFF);
+        int src = -1;  // this row's source segment (-1: query row)
+        if (MODE == MODE_CTX) {
+            if (rvalid) {
+                m_row = a.m_fin[int64_t(row) * a.H + head];
+                il_row = a.inv_l[int64_t(row) * a.H + head];
+                src = a.row_seg[t];
+            }
+            if (summary) {
+                // row groups of equal source segment (rows of a segment are contiguous)
+                const int prev = (r > 0 && rvalid) ? a.row_seg[a.rows[row - 1]] : INT32_MIN;
+                const bool start = rvalid && (r == 0 || prev != src);
+                const uint32_t bal = __ballot_sync(0xffffffffu, start);
+                if (lane == 0) bmask[q] = bal;
+                named_sync_softmax();
+                if (tid == 0) {
+                    int ng = 0;
+                    for (int w = 0; w < 4; ++w)
+                        for (uint32_t m = bmask[w]; m; m &= m - 1) grp[1 + ng++] = w * 32 + __ffs(m) - 1;
+                    grp[1 + ng] = nrows;
+                    grp[0] = ng;
+                }
+                named_sync_softmax();
+            }
+        }
+        for (int it = 0; it < niter; ++it) {
+            const int b = it & 1;
+            const int k0 = kbase + it * TK;
+            mbar_wait(&s_full[b], (it >> 1) & 1);
+            fence_after();
+            uint32_t sv[4][32];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tmem_ld32(tm_s0 + lane_base + uint32_t(b * TK + c * 32), sv[c]);
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[b]);
+            // keys of this chunk visible to this row: [kv0, kv1)
+            const int kv0 = klo - k0, kv1 = min(hi, t + 1) - k0;
+            if (MODE == MODE_STATS) {
+                float cm = -FLT_MAX;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int k = c * 32 + j;
+                        const float v = (k >= kv0 && k < kv1) ? __uint_as_float(sv[c][j]) * a.scale_log2 : -FLT_MAX;
+                        sv[c][j] = __float_as_uint(v);
+                        cm = fmaxf(cm, v);
+                    }
+                if (cm > -FLT_MAX) {
+                    const float mn = fmaxf(m_run, cm);
+                    float part_sum = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) part_sum += exp2f(__uint_as_float(sv[c][j]) - mn);
+                    l_run = (m_run > -FLT_MAX ? l_run * exp2f(m_run - mn) : 0.f) + part_sum;
+                    m_run = mn;
+                }
+            } else {
+                // normalised probabilities (fp32, kept in sv for the summary)
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int k = c * 32 + j;
+                        const float p = (k >= kv0 && k < kv1)
+                                            ? exp2f(fmaf(__uint_as_float(sv[c][j]), a.scale_log2, -m_row)) * il_row
+                                            : 0.f;
+                        sv[c][j] = __float_as_uint(p);
+                    }
+                mbar_wait(p_empty, (it & 1) ^ 1);
+                uint8_t* pt = sm + LY::P_OFF;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        const uint32_t* v = &sv[c][g * 8];
+                        const uint4 w4 = make_uint4(pack_bf16(__uint_as_float(v[0]), __uint_as_float(v[1])),
+                                                    pack_bf16(__uint_as_float(v[2]), __uint_as_float(v[3])),
+                                                    pack_bf16(__uint_as_float(v[4]), __uint_as_float(v[5])),
+                                                    pack_bf16(__uint_as_float(v[6]), __uint_as_float(v[7])));
+                        *reinterpret_cast<uint4*>(pt + p_chunk_off(r, c * 4 + g)) = w4;
+                    }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full);
+
+                if (summary) {
+                    // destination segment of each key; boundary bit k = key k closes a
+                    // memory segment inside this chunk
+                    named_sync_softmax();  // previous chunk's reduction is done with seg_s / part
+                    const int keyk = k0 + tid;
+                    const int sk = (keyk < hi && keyk >= lo) ? a.row_seg[keyk] : -1;
+                    seg_s[tid] = sk;
+                    named_sync_softmax();
+                    const int sn = tid + 1 < TK ? seg_s[tid + 1] : -2;
+                    const uint32_t bb = __ballot_sync(0xffffffffu, sk >= 0 && sn != sk);
+                    if (lane == 0) bmask[q] = bb;
+                    named_sync_softmax();
+                    int nseg = 0, f = -1;
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const uint32_t m = bmask[w];
+                        nseg += __popc(m);
+                        if (f < 0 && m) f = w * 32 + __ffs(m) - 1;
+                    }
+                    // segments of a chunk have consecutive ids: flush j closes segment d0 + j
+                    const int d0 = nseg > 0 ? seg_s[f] : 0;
+                    for (int pass = 0; pass * 32 < nseg; ++pass) {
+                        const int jlo = pass * 32, jhi = min(nseg, jlo + 32);
+                        float run = 0.f;
+                        int j = 0;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const uint32_t mword = bmask[c];
+#pragma unroll
+                            for (int jj = 0; jj < 32; ++jj) {
+                                run += __uint_as_float(sv[c][jj]);
+                                if (mword >> jj & 1u) {  // warp-uniform branch
+                                    if (j >= jlo && j < jhi)
+                                        part[r * PART_STRIDE + (j - jlo)] = (d0 + j == src) ? 0.f : run;
+                                    ++j;
+                                    run = 0.f;
+                                }
+                            }
+                        }
+                        named_sync_softmax();
+                        // rows per source group -> one fp64 atomic per (src, dst) pair
+                        const int ng = grp[0], nj = jhi - jlo;
+                        for (int e = tid; e < ng * nj; e += 128) {
+                            const int g = e / nj, jj = e % nj;
+                            const int rb = grp[1 + g], re = grp[2 + g];
+                            float acc = 0.f;
+                            for (int rr = rb; rr < re; ++rr) acc += part[rr * PART_STRIDE + jj];
+                            if (acc != 0.f) {
+                                const int gsrc = a.row_seg[a.rows[i0 + rb]];
+                                const int dst = d0 + jlo + jj;
+                                double* tgt = gsrc < 0 ? a.qts_raw + dst : a.sts_raw + int64_t(gsrc) * a.S + dst;
+                                atomicAdd(tgt, double(acc) * double(a.inv_heads));
+                            }
+                        }
+                        named_sync_softmax();
+                    }
+                }
+            }
+        }
+        // ---------------------------------------------------------- outputs
+        if (MODE == MODE_STATS && rvalid) {
+            const int64_t o = (int64_t(sp) * a.n + row) * a.H + head;
+            a.m_part[o] = m_run;
+            a.l_part[o] = l_run;
+        } else if (MODE == MODE_CTX) {
+            if (niter > 0) {
+                mbar_wait(o_full, 0);
+                fence_after();
+            }
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                uint32_t ov[32];
+                if (niter > 0) {
+                    tmem_ld32(tm_o + lane_base + uint32_t(c * 32), ov);
+                } else {
+                    for (int e = 0; e < 32; ++e) ov[e] = 0u;
+                }
+                if (!rvalid) continue;
+                if (a.nsplit == 1) {
+                    uint4* dst = reinterpret_cast<uint4*>(a.ctx + int64_t(row) * a.d + head * DH + c * 32);
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+                        dst[g] = make_uint4(pack_bf16(__uint_as_float(ov[g * 8 + 0]), __uint_as_float(ov[g * 8 + 1])),
+                                            pack_bf16(__uint_as_float(ov[g * 8 + 2]), __uint_as_float(ov[g * 8 + 3])),
+                                            pack_bf16(__uint_as_float(ov[g * 8 + 4]), __uint_as_float(ov[g * 8 + 5])),
+                                            pack_bf16(__uint_as_float(ov[g * 8 + 6]), __uint_as_float(ov[g * 8 + 7])));
+                } else {
+                    float4* dst =
+                        reinterpret_cast<float4*>(a.o_part + (int64_t(sp) * a.n + row) * a.d + head * DH + c * 32);
+#pragma unroll
+                    for (int g = 0; g < 8; ++g)
+                        dst[g] = make_float4(__uint_as_float(ov[4 * g]), __uint_as_float(ov[4 * g + 1]),
+                                             __uint_as_float(ov[4 * g + 2]), __uint_as_float(ov[4 * g + 3]));
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        tmem_dealloc(tmem, LY::TMEM_COLS);
+    }
+}
+
+// m = max_s m_s, l = sum_s l_s 2^(m_s - m)  (split order fixed); inv_l = 1/l
+__global__ void tc_stats_combine(const float* __restrict__ mp, const float* __restrict__ lp, int nsplit,
+                                 int64_t nh, float* __restrict__ m_fin, float* __restrict__ inv_l) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nh; e += int64_t(gridDim.x) * blockDim.x) {
+        float m = -FLT_MAX;
+        for (int s = 0; s < nsplit; ++s) m = fmaxf(m, mp[s * nh + e]);
+        float l = 0.f;
+        for (int s = 0; s < nsplit; ++s) {
+            const float ms = mp[s * nh + e];
+            if (ms > -FLT_MAX) l += lp[s * nh + e] * exp2f(ms - m);
+        }
+        m_fin[e] = m;
+        inv_l[e] = l > 0.f ? 1.f / l : 0.f;
+    }
+}
+
+__global__ void tc_ctx_combine(const float* __restrict__ op, int nsplit, int64_t nd, __nv_bfloat16* __restrict__ ctx) {
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nd; e += int64_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+        for (int s = 0; s < nsplit; ++s) acc += op[s * nd + e];
+        ctx[e] = __float2bfloat16_rn(acc);
+    }
+}
+
+// raw summary -> AttentionSummary: qts/qlen, sts[i][j]/seg_len[i] for j < i
+// (prefill.hpp:306-315)
+__global__ void summary_normalize(const double* __restrict__ qraw, const double* __restrict__ sraw, int S,
+                                  const int32_t* __restrict__ seg_len, int qlen, double* __restrict__ summ) {
+    const int i = int(blockIdx.y) - 1;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < S; j += gridDim.x * blockDim.x) {
+        if (i < 0) summ[j] = qlen > 0 ? qraw[j] / double(qlen) : 0.0;
+        else summ[S + int64_t(i) * S + j] = j < i ? sraw[int64_t(i) * S + j] / double(seg_len[i]) : 0.0;
+    }
+}
+
+// V [T x d] -> V^T [d x ldt] (bf16), 64x64 tiles through shared memory;
+// padding keys [T, ldt) are written as zero.
+__global__ void transpose_bf16(const __nv_bfloat16* __restrict__ v, int T, int d, int64_t ldt,
+                               __nv_bfloat16* __restrict__ vt) {
+    __shared__ __nv_bfloat16 tile[64][66];
+    const int t0 = blockIdx.x * 64, c0 = blockIdx.y * 64;
+    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+        const int r = e / 64, c = e % 64;
+        tile[r][c] = (t0 + r < T) ? v[int64_t(t0 + r) * d + c0 + c] : __float2bfloat16_rn(0.f);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+        const int r = e / 64, c = e % 64;  // out row c0+r, col t0+c
+        vt[int64_t(c0 + r) * ldt + t0 + c] = tile[c][r];
+    }
+}
+
+template <int MODE>
+void launch_mode(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const TcArgs& a, dim3 grid,
+                 cudaStream_t st) {
+    using LY = Layout<MODE>;
+    static bool attr = false;
+    if (!attr) {
+        KEEP_CUDA(cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LY::SMEM)));
+        attr = true;
+    }
+    attn_tc_kernel<MODE><<<grid, NTHR, LY::SMEM, st>>>(q, k, vt, a);
+    KEEP_LAUNCH_CHECK();
+}
+
+static_assert(Layout<MODE_CTX>::SMEM <= 232448, "CTX smem");
+
+}  // namespace
+
+// Host driver of the two passes (see file comment).
+void launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
+    const int n = L.n, T = L.T, H = L.H, d = L.d;
+    if (n == 0) return;
+    const int tiles = int(ceil_div(n, TM));
+    // V^T for the P.V operand (K-major over keys); inner extent padded to a
+    // multiple of 64 keys so TMA boxes never straddle a ragged edge
+    const int64_t ldt = ceil_div(T, 64) * 64;
+    {
+        dim3 g(unsigned(ceil_div(T, 64)), unsigned(d / 64));
+        transpose_bf16<<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(L.v), T, d, ldt, L.vt);
+        KEEP_LAUNCH_CHECK();
+    }
+    const CUtensorMap mq = make_map_bf16(L.q, n, d, d, 128);
+    const CUtensorMap mk = make_map_bf16(L.k, T, d, d, 128);
+    const CUtensorMap mv = make_map_bf16(L.vt, d, ldt, ldt, 128);
+
+    TcArgs a{};
+    a.n = n;
+    a.T = T;
+    a.H = H;
+    a.d = d;
+    a.S = L.S;
+    a.rows = L.rows;
+    a.row_seg = L.row_seg;
+    a.key_lo = L.key_lo;
+    a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(DH)));
+    a.inv_heads = float(1.0 / H);
+    a.m_part = L.m_part;
+    a.l_part = L.l_part;
+    a.m_fin = L.m_fin;
+    a.inv_l = L.inv_l;
+    a.o_part = L.o_part;
+    a.ctx = L.ctx;
+    a.nsplit = L.nsplit_a;
+    a.split_lo = L.split_lo_a;
+    a.split_hi = L.split_hi_a;
+    a.qts_raw = L.with_bins ? L.summ_raw : nullptr;
+    a.sts_raw = L.with_bins ? L.summ_raw + L.S : nullptr;
+    if (L.with_bins)
+        KEEP_CUDA(cudaMemsetAsync(L.summ_raw, 0, sizeof(double) * (size_t(L.S) + size_t(L.S) * L.S), st));
+
+    launch_mode<MODE_STATS>(mq, mk, mv, a, dim3(tiles, H, a.nsplit), st);
+    const int64_t nh = int64_t(n) * H;
+    tc_stats_combine<<<unsigned(std::min<int64_t>(ceil_div(nh, 256), kNumSMs * 8)), 256, 0, st>>>(
+        L.m_part, L.l_part, a.nsplit, nh, L.m_fin, L.inv_l);
+    KEEP_LAUNCH_CHECK();
+    launch_mode<MODE_CTX>(mq, mk, mv, a, dim3(tiles, H, a.nsplit), st);
+    if (a.nsplit > 1) {
+        const int64_t nd = int64_t(n) * d;
+        tc_ctx_combine<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(L.o_part, a.nsplit,
+                                                                                                   nd, L.ctx);
+        KEEP_LAUNCH_CHECK();
+    }
+    if (L.with_bins) {
+        dim3 g(unsigned(ceil_div(L.S, 256)), unsigned(L.S + 1));
+        summary_normalize<<<g, 256, 0, st>>>(L.summ_raw, L.summ_raw + L.S, L.S, L.seg_len, L.qlen, L.summ);
+        KEEP_LAUNCH_CHECK();
+    }
+}
+
+}  // namespace keep_b200

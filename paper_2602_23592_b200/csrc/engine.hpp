@@ -15,6 +15,33 @@ namespace keep_b200 {
 void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb,
                       int M, int N, int K, const EpiArgs& epi, cudaStream_t st, int max_ctas = kNumSMs);
 
+// FAST attention on tcgen05 (head_dim 128): stats / context / bins passes.
+struct AttnTcLaunch {
+    int n, T, H, d, S;
+    const void* q;            // [n x d] bf16 compact queries
+    const void* k;            // [T x d] bf16 merged keys
+    const void* v;            // [T x d] bf16 merged values
+    __nv_bfloat16* vt;        // scratch [d x roundup(T, 64)]
+    const int32_t* rows;
+    const int32_t* row_seg;
+    const int32_t* key_lo;    // nullable
+    bool with_bins;
+    int nsplit_a;             // stats / context splits (any cut)
+    const int32_t* split_lo_a;
+    const int32_t* split_hi_a;
+    float* m_part;            // [nsplit_a x n x H]
+    float* l_part;
+    float* m_fin;             // [n x H]
+    float* inv_l;
+    float* o_part;            // [nsplit_a x n x d]
+    __nv_bfloat16* ctx;       // [n x d]
+    double* summ_raw;         // scratch [S + S*S] (raw qts, sts)
+    double* summ;             // out [S + S*S] normalised summary
+    const int32_t* seg_len;   // [S]
+    int qlen;
+};
+void launch_attention_tc(const AttnTcLaunch& a, cudaStream_t st);
+
 // Per-phase CUDA-event timing (keep_profile_*).
 struct Profiler {
     bool on = false;
@@ -100,7 +127,9 @@ struct Pass {
     // attention scratch
     DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi;
     int split_count = 1;
-    DevBuf seg_cbeg, seg_cend, summ;
+    DevBuf vt, split_lo_a, split_hi_a;  // FAST tensor-core attention
+    int split_count_a = 1;
+    DevBuf seg_cbeg, seg_cend, summ, summ_raw;
     // merged KV destination per layer (device)
     std::vector<void*> kdst, vdst;
     std::vector<uint8_t> prev, dropped;
@@ -123,6 +152,7 @@ struct Context {
     keep_memory_stats stats{};
     // cursor
     std::unique_ptr<Pass> pf;
+    std::unique_ptr<Pass> refresh;  // canonical-KV refresh workspace
     DevBuf kv;  // merged KV of the cursor [L][2][T][d]
     std::vector<void*> seg_ksrc_h, seg_vsrc_h;
     DevBuf d_ksrc, d_vsrc, d_cdst, d_cn;

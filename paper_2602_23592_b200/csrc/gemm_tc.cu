@@ -17,102 +17,51 @@
 // add with a bf16 mirror for the next GEMM, ReLU to bf16, plain fp32 store.
 // Tiles are rasterised in bands of GM m-blocks so a band of A and a window of
 // weight columns stay L2-resident (126 MB) while 148 CTAs sweep them.
-#include <cuda.h>
-
 #include "engine.hpp"
+#include "tc_common.cuh"
 
 namespace keep_b200 {
+
+namespace tc {
+// ------------------------------------------------------------ tensor maps --
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
+            raise(KEEP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeFn>(p);
+    }();
+    return fn;
+}
+
+// 2-D bf16 tensor [rows x cols] (row stride ld elements), box BK x box_rows,
+// 128-byte swizzle; out-of-bounds rows read as zero.
+CUtensorMap make_map_bf16(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    CUtensorMap tm;
+    const cuuint64_t gdim[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    const cuuint64_t gstride[1] = {cuuint64_t(ld * 2)};
+    const cuuint32_t box[2] = {cuuint32_t(64), cuuint32_t(box_rows)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box,
+                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(KEEP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return tm;
+}
+
+}  // namespace tc
 
 namespace {
 
 constexpr int BM = 128, BK = 64, UMMA_K = 16, GM = 16;
 constexpr int kThreads = 256;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t ok = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    } while (!ok);
-}
-
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int x, int y) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-            smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(x), "r"(y)
-        : "memory");
-}
-
-__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-// UMMA shared-memory descriptor: K-major operand staged by TMA with 128B
-// swizzle (8-row x 128-byte atoms, atoms 1024 B apart along M/N).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= uint64_t((saddr >> 4) & 0x3FFF);          // start address
-    d |= uint64_t(1) << 16;                         // leading byte offset (unused for SW128 K-major)
-    d |= uint64_t(1024 >> 4) << 32;                 // stride byte offset: 8 rows * 128 B
-    d |= uint64_t(1) << 46;                         // descriptor version (sm_100)
-    d |= uint64_t(2) << 61;                         // layout: SWIZZLE_128B
-    return d;
-}
-
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, both K-major.
-__host__ __device__ constexpr uint32_t instr_desc(int M, int N) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
-        : "memory");
-}
-
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-}
+using namespace tc;
 
 // Store 32 consecutive values of one row starting at column n.
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
@@ -315,37 +264,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
 }
 
-// ------------------------------------------------------------ tensor maps --
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn encode_fn() {
-    static EncodeFn fn = [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p)
-            raise(KEEP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        return reinterpret_cast<EncodeFn>(p);
-    }();
-    return fn;
-}
-
-// 2-D bf16 tensor [rows x cols] (row stride ld elements), box BK x box_rows,
-// 128-byte swizzle; out-of-bounds rows read as zero.
-CUtensorMap make_map(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
-    CUtensorMap tm;
-    const cuuint64_t gdim[2] = {cuuint64_t(cols), cuuint64_t(rows)};
-    const cuuint64_t gstride[1] = {cuuint64_t(ld * 2)};
-    const cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(box_rows)};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), gdim, gstride, box,
-                                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) raise(KEEP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
-    return tm;
-}
-
 template <int BN>
 void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
                const EpiArgs& epi, cudaStream_t st, int max_ctas = kNumSMs) {
@@ -355,8 +273,8 @@ void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int
         KEEP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM)));
         attr = true;
     }
-    const CUtensorMap ta = make_map(A, M, K, lda, BM);
-    const CUtensorMap tb = make_map(Bt, N, K, ldb, BN);
+    const CUtensorMap ta = make_map_bf16(A, M, K, lda, BM);
+    const CUtensorMap tb = make_map_bf16(Bt, N, K, ldb, BN);
     const int ntiles = int(ceil_div(M, BM) * ceil_div(N, BN));
     const int grid = std::min(ntiles, std::max(1, std::min(max_ctas, kNumSMs)));
     gemm_tc_kernel<BN><<<grid, kThreads, CF::SMEM, st>>>(ta, tb, M, N, K, epi);

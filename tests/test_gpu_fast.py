@@ -20,12 +20,14 @@ def rel(a, b):
 
 
 CASES = [(s, 8, 4, 4, 64, 128, 256) for s in range(2, 12)] + [(40, 24, 6, 2, 128, 256, 300), (41, 12, 3, 8, 256, 512, 500)]
+# head_dim 128: the tcgen05 attention path (multiple 128-row tiles / 128-key chunks / splits)
+CASES_TC = [(50, 20, 4, 2, 256, 512, 512), (51, 40, 3, 4, 512, 1024, 700), (52, 100, 2, 2, 256, 256, 512),
+            (53, 300, 2, 1, 128, 128, 256)]
 
 
-@pytest.fixture(scope="module")
-def results(ko):
+def _run(ko, cases):
     out = []
-    for seed, S, L, H, d, mlp, V in CASES:
+    for seed, S, L, H, d, mlp, V in cases:
         p = ko.make_instance(seed, S, L, H, d, mlp, V)
         w = ko.model_init(L, H, d, mlp, V, seed)
         sched = ko.ratio_schedule(L, 0.5)
@@ -38,6 +40,24 @@ def results(ko):
             sel = ctx.selective_prefill(lay, p.query, ref["plan"])  # same plan -> compare numerics
         out.append((p, w, ref, got, sel))
     return out
+
+
+@pytest.fixture(scope="module")
+def results(ko):
+    return _run(ko, CASES)
+
+
+@pytest.fixture(scope="module")
+def results_tc(ko):
+    return _run(ko, CASES_TC)
+
+
+def test_tc_attention_numerics(results_tc):
+    for p, w, ref, got, sel in results_tc:
+        assert rel(sel["final_hidden"], ref["final_hidden"]) <= RTOL_FAST
+        assert rel(sel["kv"], ref["kv"]) <= RTOL_FAST
+        assert np.max(np.abs(sel["qts"] - ref["qts"])) <= 2e-2
+        assert np.max(np.abs(sel["sts"] - ref["sts"])) <= 2e-2
 
 
 def test_fast_selection_agreement(results):
