@@ -452,6 +452,7 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
             }
             t.seg_len = p.d_seg_len.as<int32_t>();
             t.qlen = p.qlen;
+            t.chunk_tab = p.chunk_tab.p;
             launch_attention_tc(t, st);
         } else {
             ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, 5);
@@ -581,6 +582,10 @@ void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const i
     upload(p.d_tokens, toks, st);
     upload(p.d_row_seg, p.row_seg, st);
     upload(p.d_seg_len, p.seg_len, st);
+    if (use_tc_attention(c)) {
+        p.chunk_tab.ensure(32 * size_t(std::max<int64_t>(1, ceil_div(p.T, 128))));
+        launch_chunk_table(p.d_row_seg.as<int32_t>(), p.T, p.chunk_tab.p, st);
+    }
     std::vector<int32_t> all(p.T);
     std::iota(all.begin(), all.end(), 0);
     p.x.ensure(sizeof(float) * size_t(std::max(p.T, 1)) * c.d);

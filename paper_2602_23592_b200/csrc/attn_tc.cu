@@ -40,7 +40,8 @@ constexpr int NTHR = 256;
 constexpr uint32_t TILE_BYTES = TM * DH * 2;  // 32 KB: [128 x 128] bf16 as 2 boxes of 64 columns
 constexpr uint32_t BOX_BYTES = TILE_BYTES / 2;
 constexpr uint32_t IDESC = instr_desc(128, 128);
-constexpr int PART_STRIDE = 33;               // partial bins: 32 segments per pass (+1 pad)
+constexpr int PART_SEGS = 24;                 // destination segments per binning pass
+constexpr int PART_STRIDE = PART_SEGS + 1;    // floats per row: slot PART_SEGS is a trash slot
 
 enum { MODE_STATS = 0, MODE_CTX = 1 };
 
@@ -62,6 +63,7 @@ struct TcArgs {
     __nv_bfloat16* ctx;     // [n][d]
     double* qts_raw;        // [S]      (nullptr: no summary)
     double* sts_raw;        // [S x S]
+    const int4* chunk_tab;  // [ceil(T/128) x 2] per 128-key chunk: {d0, nseg, -, -}, {mask0..3}
 };
 
 template <int MODE>
@@ -71,10 +73,10 @@ struct Layout {
     static constexpr uint32_t Q_OFF = 0;
     static constexpr uint32_t STAGE_OFF = TILE_BYTES;
     static constexpr uint32_t P_OFF = STAGE_OFF + ST * STAGE;             // CTX: one P tile
-    static constexpr uint32_t PART_OFF = P_OFF + TILE_BYTES;              // CTX: partial bins [128][33] f32
-    static constexpr uint32_t SEG_OFF = PART_OFF + TM * PART_STRIDE * 4;  // CTX: chunk segments [128] i32
-    static constexpr uint32_t GRP_OFF = SEG_OFF + TK * 4;                 // CTX: row groups [130] i32
-    static constexpr uint32_t MSK_OFF = GRP_OFF + (TM + 2) * 4;           // CTX: boundary mask [4] u32
+    static constexpr uint32_t PART_OFF = P_OFF + TILE_BYTES;              // CTX: 2 x partial bins [128][17] f32
+    static constexpr uint32_t SEG_OFF = PART_OFF + 2 * TM * PART_STRIDE * 4;  // (unused)
+    static constexpr uint32_t GRP_OFF = SEG_OFF;                          // CTX: row groups [130] + sources [129]
+    static constexpr uint32_t MSK_OFF = GRP_OFF + (2 * TM + 4) * 4;       // CTX: row-group ballots [4] u32
     static constexpr uint32_t BAR_OFF = MODE == MODE_CTX ? ((MSK_OFF + 16 + 7) & ~7u) : P_OFF;
     static constexpr size_t SMEM = size_t(BAR_OFF) + 256 + 1024;
     static constexpr uint32_t TMEM_COLS = MODE == MODE_CTX ? 512 : 256;
@@ -94,6 +96,13 @@ __device__ __forceinline__ uint64_t desc_k(uint32_t tile, int ks) {
 }
 
 __device__ __forceinline__ void named_sync_softmax() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// one MUFU.EX2 (flush-to-zero; inputs are <= 0 after max subtraction)
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(NTHR, 1)
@@ -216,13 +225,15 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
         const int t = rvalid ? a.rows[row] : -1;
         const int klo = max(lo, rvalid && a.key_lo ? a.key_lo[t] : 0);  // first visible key
         const uint32_t lane_base = uint32_t(q * 32) << 16;
+        const float scale = a.scale_log2;
         float m_run = -FLT_MAX, l_run = 0.f;  // STATS
         float m_row = 0.f, il_row = 0.f;      // CTX
         const bool summary = MODE == MODE_CTX && a.sts_raw != nullptr;
-        float* part = reinterpret_cast<float*>(sm + LY::PART_OFF);
-        int32_t* seg_s = reinterpret_cast<int32_t*>(sm + LY::SEG_OFF);
+        float* part0 = reinterpret_cast<float*>(sm + LY::PART_OFF);
         int32_t* grp = reinterpret_cast<int32_t*>(sm + LY::GRP_OFF);  // [0]=count, then group row starts
+        int32_t* gsrc_s = grp + TM + 2;                                 // source segment of each group
         uint32_t* bmask = reinterpret_cast<uint32_t*>(sm + LY::MSK_OFF);
+        int pbuf = 0;
         int src = -1;  // this row's source segment (-1: query row)
         if (MODE == MODE_CTX) {
             if (rvalid) {
@@ -245,6 +256,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                     grp[0] = ng;
                 }
                 named_sync_softmax();
+                for (int g = tid; g < grp[0]; g += 128) gsrc_s[g] = a.row_seg[a.rows[i0 + grp[1 + g]]];
+                named_sync_softmax();
             }
         }
         for (int it = 0; it < niter; ++it) {
@@ -260,39 +273,61 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             if (lane == 0) mbar_arrive(&s_empty[b]);
             // keys of this chunk visible to this row: [kv0, kv1)
             const int kv0 = klo - k0, kv1 = min(hi, t + 1) - k0;
+            // fully visible chunk for every row of the warp: no per-key masks
+            const bool full_chunk = __all_sync(0xffffffffu, kv0 <= 0 && kv1 >= TK);
             if (MODE == MODE_STATS) {
                 float cm = -FLT_MAX;
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int k = c * 32 + j;
-                        const float v = (k >= kv0 && k < kv1) ? __uint_as_float(sv[c][j]) * a.scale_log2 : -FLT_MAX;
-                        sv[c][j] = __float_as_uint(v);
-                        cm = fmaxf(cm, v);
-                    }
-                if (cm > -FLT_MAX) {
-                    const float mn = fmaxf(m_run, cm);
-                    float part_sum = 0.f;
+                if (full_chunk) {
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) part_sum += exp2f(__uint_as_float(sv[c][j]) - mn);
-                    l_run = (m_run > -FLT_MAX ? l_run * exp2f(m_run - mn) : 0.f) + part_sum;
+                        for (int j = 0; j < 32; ++j) {
+                            const float v = __uint_as_float(sv[c][j]) * scale;
+                            sv[c][j] = __float_as_uint(v);
+                            cm = fmaxf(cm, v);
+                        }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const bool ok = unsigned(c * 32 + j - kv0) < unsigned(kv1 - kv0);
+                            const float v = ok ? __uint_as_float(sv[c][j]) * scale : -FLT_MAX;
+                            sv[c][j] = __float_as_uint(v);
+                            cm = fmaxf(cm, v);
+                        }
+                }
+                if (cm > -FLT_MAX) {
+                    const float mn = fmaxf(m_run, cm);
+                    float ps0 = 0.f, ps1 = 0.f;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int j = 0; j < 32; j += 2) {
+                            ps0 += ex2(__uint_as_float(sv[c][j]) - mn);
+                            ps1 += ex2(__uint_as_float(sv[c][j + 1]) - mn);
+                        }
+                    l_run = (m_run > -FLT_MAX ? l_run * ex2(m_run - mn) : 0.f) + (ps0 + ps1);
                     m_run = mn;
                 }
             } else {
                 // normalised probabilities (fp32, kept in sv for the summary)
+                if (full_chunk) {
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
+                    for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int k = c * 32 + j;
-                        const float p = (k >= kv0 && k < kv1)
-                                            ? exp2f(fmaf(__uint_as_float(sv[c][j]), a.scale_log2, -m_row)) * il_row
-                                            : 0.f;
-                        sv[c][j] = __float_as_uint(p);
-                    }
+                        for (int j = 0; j < 32; ++j)
+                            sv[c][j] = __float_as_uint(ex2(fmaf(__uint_as_float(sv[c][j]), scale, -m_row)) * il_row);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const bool ok = unsigned(c * 32 + j - kv0) < unsigned(kv1 - kv0);
+                            const float p = ex2(fmaf(__uint_as_float(sv[c][j]), scale, -m_row)) * il_row;
+                            sv[c][j] = __float_as_uint(ok ? p : 0.f);
+                        }
+                }
                 mbar_wait(p_empty, (it & 1) ^ 1);
                 uint8_t* pt = sm + LY::P_OFF;
 #pragma unroll
@@ -311,46 +346,40 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                 if (lane == 0) mbar_arrive(p_full);
 
                 if (summary) {
-                    // destination segment of each key; boundary bit k = key k closes a
-                    // memory segment inside this chunk
-                    named_sync_softmax();  // previous chunk's reduction is done with seg_s / part
-                    const int keyk = k0 + tid;
-                    const int sk = (keyk < hi && keyk >= lo) ? a.row_seg[keyk] : -1;
-                    seg_s[tid] = sk;
-                    named_sync_softmax();
-                    const int sn = tid + 1 < TK ? seg_s[tid + 1] : -2;
-                    const uint32_t bb = __ballot_sync(0xffffffffu, sk >= 0 && sn != sk);
-                    if (lane == 0) bmask[q] = bb;
-                    named_sync_softmax();
-                    int nseg = 0, f = -1;
-#pragma unroll
-                    for (int w = 0; w < 4; ++w) {
-                        const uint32_t m = bmask[w];
-                        nseg += __popc(m);
-                        if (f < 0 && m) f = w * 32 + __ffs(m) - 1;
-                    }
-                    // segments of a chunk have consecutive ids: flush j closes segment d0 + j
-                    const int d0 = nseg > 0 ? seg_s[f] : 0;
-                    for (int pass = 0; pass * 32 < nseg; ++pass) {
-                        const int jlo = pass * 32, jhi = min(nseg, jlo + 32);
+                    // per-chunk segment table (prefill constant): flush j of the
+                    // boundary bits closes destination segment d0 + j
+                    const int4 hdr = a.chunk_tab[2 * (k0 / TK)];
+                    const int4 msk = a.chunk_tab[2 * (k0 / TK) + 1];
+                    const int d0 = hdr.x, nseg = hdr.y;
+                    const uint32_t mw[4] = {uint32_t(msk.x), uint32_t(msk.y), uint32_t(msk.z), uint32_t(msk.w)};
+                    for (int pass = 0; pass * PART_SEGS < nseg; ++pass) {
+                        const int jlo = pass * PART_SEGS, jhi = min(nseg, jlo + PART_SEGS);
+                        float* part = part0 + pbuf * (TM * PART_STRIDE);
+                        float* prow = part + r * PART_STRIDE;
+                        // own segment (dropped) as a local flush index: stored to the trash slot
+                        const int own = src - d0 - jlo;
                         float run = 0.f;
-                        int j = 0;
+                        int j = -jlo;  // local index of the next flush
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
-                            const uint32_t mword = bmask[c];
+                            const uint32_t mword = mw[c];
 #pragma unroll
                             for (int jj = 0; jj < 32; ++jj) {
                                 run += __uint_as_float(sv[c][jj]);
-                                if (mword >> jj & 1u) {  // warp-uniform branch
-                                    if (j >= jlo && j < jhi)
-                                        part[r * PART_STRIDE + (j - jlo)] = (d0 + j == src) ? 0.f : run;
-                                    ++j;
-                                    run = 0.f;
-                                }
+                                const uint32_t bit = (mword >> jj) & 1u;
+                                // branch-free: predicated store, index clamped to the trash slot
+                                const unsigned idx = (unsigned(j) < unsigned(PART_SEGS) && j != own) ? unsigned(j)
+                                                                                                       : unsigned(PART_SEGS);
+                                if (bit) prow[idx] = run;
+                                run = bit ? 0.f : run;
+                                j += int(bit);
                             }
                         }
+                        // segments closed in this pass that were the row's own: write 0
+                        if (unsigned(own) < unsigned(PART_SEGS) && own < jhi - jlo) prow[own] = 0.f;
+                        // one barrier per pass: the other buffer's reduction (previous
+                        // pass) finished before anyone got here
                         named_sync_softmax();
-                        // rows per source group -> one fp64 atomic per (src, dst) pair
                         const int ng = grp[0], nj = jhi - jlo;
                         for (int e = tid; e < ng * nj; e += 128) {
                             const int g = e / nj, jj = e % nj;
@@ -358,13 +387,13 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
                             float acc = 0.f;
                             for (int rr = rb; rr < re; ++rr) acc += part[rr * PART_STRIDE + jj];
                             if (acc != 0.f) {
-                                const int gsrc = a.row_seg[a.rows[i0 + rb]];
+                                const int gs = gsrc_s[g];
                                 const int dst = d0 + jlo + jj;
-                                double* tgt = gsrc < 0 ? a.qts_raw + dst : a.sts_raw + int64_t(gsrc) * a.S + dst;
+                                double* tgt = gs < 0 ? a.qts_raw + dst : a.sts_raw + int64_t(gs) * a.S + dst;
                                 atomicAdd(tgt, double(acc) * double(a.inv_heads));
                             }
                         }
-                        named_sync_softmax();
+                        pbuf ^= 1;
                     }
                 }
             }
@@ -439,6 +468,28 @@ __global__ void tc_ctx_combine(const float* __restrict__ op, int nsplit, int64_t
     }
 }
 
+// Per 128-key chunk c: the destination segments whose last key (or the chunk
+// end) falls inside the chunk, as a boundary bit mask, plus the first such
+// segment.  Depends only on the layout, so it is built once per prefill.
+__global__ void chunk_table_kernel(const int32_t* __restrict__ row_seg, int T, int nchunks, int4* __restrict__ tab) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nchunks) return;
+    uint32_t m[4] = {0, 0, 0, 0};
+    int d0 = -1, nseg = 0;
+    for (int k = 0; k < TK; ++k) {
+        const int key = c * TK + k;
+        const int sk = key < T ? row_seg[key] : -1;
+        const int sn = (k + 1 < TK && key + 1 < T) ? row_seg[key + 1] : -2;
+        if (sk >= 0 && sn != sk) {
+            m[k >> 5] |= 1u << (k & 31);
+            if (d0 < 0) d0 = sk;
+            ++nseg;
+        }
+    }
+    tab[2 * c] = make_int4(d0 < 0 ? 0 : d0, nseg, 0, 0);
+    tab[2 * c + 1] = make_int4(int(m[0]), int(m[1]), int(m[2]), int(m[3]));
+}
+
 // raw summary -> AttentionSummary: qts/qlen, sts[i][j]/seg_len[i] for j < i
 // (prefill.hpp:306-315)
 __global__ void summary_normalize(const double* __restrict__ qraw, const double* __restrict__ sraw, int S,
@@ -484,6 +535,12 @@ static_assert(Layout<MODE_CTX>::SMEM <= 232448, "CTX smem");
 
 }  // namespace
 
+void launch_chunk_table(const int32_t* row_seg, int T, void* tab, cudaStream_t st) {
+    const int nchunks = int(ceil_div(T, TK));
+    chunk_table_kernel<<<unsigned(ceil_div(nchunks, 128)), 128, 0, st>>>(row_seg, T, nchunks, static_cast<int4*>(tab));
+    KEEP_LAUNCH_CHECK();
+}
+
 // Host driver of the two passes (see file comment).
 void launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
     const int n = L.n, T = L.T, H = L.H, d = L.d;
@@ -523,6 +580,7 @@ void launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
     a.split_hi = L.split_hi_a;
     a.qts_raw = L.with_bins ? L.summ_raw : nullptr;
     a.sts_raw = L.with_bins ? L.summ_raw + L.S : nullptr;
+    a.chunk_tab = reinterpret_cast<const int4*>(L.chunk_tab);
     if (L.with_bins)
         KEEP_CUDA(cudaMemsetAsync(L.summ_raw, 0, sizeof(double) * (size_t(L.S) + size_t(L.S) * L.S), st));
 

@@ -39,8 +39,11 @@ struct AttnTcLaunch {
     double* summ;             // out [S + S*S] normalised summary
     const int32_t* seg_len;   // [S]
     int qlen;
+    const void* chunk_tab;    // launch_chunk_table output (summary only)
 };
 void launch_attention_tc(const AttnTcLaunch& a, cudaStream_t st);
+// per-128-key-chunk destination-segment table (32 B per chunk)
+void launch_chunk_table(const int32_t* row_seg, int T, void* tab, cudaStream_t st);
 
 // Per-phase CUDA-event timing (keep_profile_*).
 struct Profiler {
@@ -127,7 +130,7 @@ struct Pass {
     // attention scratch
     DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi;
     int split_count = 1;
-    DevBuf vt, split_lo_a, split_hi_a;  // FAST tensor-core attention
+    DevBuf vt, split_lo_a, split_hi_a, chunk_tab;  // FAST tensor-core attention
     int split_count_a = 1;
     DevBuf seg_cbeg, seg_cend, summ, summ_raw;
     // merged KV destination per layer (device)
