@@ -80,9 +80,14 @@ typedef struct {
     int32_t numerics;    /* KEEP_NUMERICS_* */
     uint64_t seed;       /* ModelConfig::seed */
     int32_t device;      /* CUDA ordinal */
-    int32_t world_size;  /* KV-head shards (1 = single GPU) */
-    int32_t rank;
+    int32_t world_size;  /* KV-head shards G (1 = single GPU); num_heads % G == 0 */
+    int32_t rank;        /* this context owns heads [rank*H/G, (rank+1)*H/G) */
     int32_t reserved;
+    /* world_size > 1: exactly one of the following (see keep_comm_unique_id) */
+    const uint8_t* nccl_id; /* 128-byte ncclUniqueId shared by all ranks (library-owned comm) */
+    void* nccl_comm;        /* caller-owned ncclComm_t */
+    void* loopback;         /* keep_loopback_create group: G ranks on one GPU in one process
+                               (one host thread per rank; a test double for the collectives) */
 } keep_config;
 
 typedef struct {
@@ -110,6 +115,8 @@ typedef struct {
     int32_t tier;        /* tier the block was found in before the load */
     int32_t elem_bytes;  /* 4 or 2 */
     double load_ms;      /* measured H2D time of a slow-tier load (0 for fast hits) */
+    int32_t row_elems;   /* elements per row: model_dim / world_size (this rank's head columns) */
+    int32_t col0;        /* first model column of the row slice */
 } keep_kv_view;
 
 typedef struct {
@@ -138,6 +145,17 @@ typedef struct {
 const char* keep_last_error(void);
 const char* keep_version(void);
 
+/* ---- KV-head sharding ----------------------------------
+ * One context per rank.  Every rank calls the same sequence of entry points;
+ * per layer the ranks all-reduce the fp64 segment summary (identical bits on
+ * every rank, so importance_evaluation runs replicated), exchange attention
+ * context head-sharded -> row-sharded (all-to-all) and all-gather the fp32
+ * residual rows after Wo + MLP.  KV blocks, views and kv_out hold the rank's
+ * head columns only (row_elems = model_dim / world_size). */
+int keep_comm_unique_id(uint8_t* id_out /* 128 bytes */);
+int keep_loopback_create(int32_t world_size, void** group_out);
+int keep_loopback_destroy(void* group);
+
 int keep_ctx_create(const keep_config* cfg, void** ctx_out);
 int keep_ctx_destroy(void* ctx);
 int keep_ctx_synchronize(void* ctx);
@@ -148,6 +166,8 @@ int keep_model_init(void* ctx);
 int keep_model_export(void* ctx, float* host_weights, uint64_t count);
 
 /* ---- memory tier: the load_memory surface ------------------------------ */
+/* keys / values: full rows [tokens x model_dim] (a sharded rank keeps its
+ * head columns). */
 int keep_memory_put(void* ctx, keep_owner owner, uint64_t version, int32_t layer,
                     int64_t tokens, const float* keys, const float* values, int32_t tier);
 /* Canonical KV refresh on the GPU for every layer: one standalone prefill per
@@ -163,7 +183,7 @@ int keep_load_memory(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* o
 int keep_memory_has_current(void* ctx, keep_owner owner, uint64_t version, int32_t* out);
 int keep_invalidate(void* ctx, keep_owner owner, uint64_t new_version, uint64_t tokens);
 int keep_memory_stats_get(void* ctx, keep_memory_stats* out);
-/* Copy one block back to the host as fp32 (tests). */
+/* Copy one block back to the host as fp32 (tests): [tokens x row_elems]. */
 int keep_memory_read(void* ctx, keep_owner owner, int32_t layer, float* keys, float* values);
 
 /* ---- prefill cursor: prefill_layer ------------------------------------- */
@@ -171,8 +191,9 @@ int keep_prefill_begin(void* ctx, const keep_layout* layout, const int32_t* quer
                        int32_t query_len);
 /* One layer.  active[S] host mask; summary_out (S+S*S doubles) may be NULL. */
 int keep_prefill_layer(void* ctx, const uint8_t* active, double* summary_out);
-/* final_hidden [T*d] fp32; kv_out per layer keys[T*d] then values[T*d] as
- * fp32 (converted from bf16 in FAST).  Either may be NULL. */
+/* final_hidden [T*d] fp32; kv_out per layer keys[T*dc] then values[T*dc] as
+ * fp32 (converted from bf16 in FAST), dc = model_dim / world_size (the rank's
+ * head columns).  Either may be NULL. */
 int keep_prefill_finish(void* ctx, float* final_hidden, float* kv_out);
 
 /* ---- selection ----------------------------------------------------------- */
@@ -203,6 +224,8 @@ enum {
     KEEP_PROF_EMBED = 9,    /* embedding gather (K1)                         */
     KEEP_PROF_LOGITS = 10,  /* last-row logits (K11)                         */
     KEEP_PROF_LOADER = 11,  /* host->HBM layer loads (K10)                   */
+    KEEP_PROF_COMM = 12,    /* KV-head sharding collectives (NCCL)           */
+    KEEP_PROF_XCHG = 13,    /* ctx pack / residual bf16 refresh around them  */
     KEEP_PROF_COUNT = 16
 };
 typedef struct {

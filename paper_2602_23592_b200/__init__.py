@@ -47,7 +47,8 @@ class keep_config(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("num_heads", C.c_int32), ("model_dim", C.c_int32),
                 ("mlp_dim", C.c_int32), ("vocab_size", C.c_int32), ("numerics", C.c_int32),
                 ("seed", C.c_uint64), ("device", C.c_int32), ("world_size", C.c_int32),
-                ("rank", C.c_int32), ("reserved", C.c_int32)]
+                ("rank", C.c_int32), ("reserved", C.c_int32), ("nccl_id", C.c_void_p),
+                ("nccl_comm", C.c_void_p), ("loopback", C.c_void_p)]
 
 
 class keep_owner(C.Structure):
@@ -63,7 +64,8 @@ class keep_layout(C.Structure):
 
 class keep_kv_view(C.Structure):
     _fields_ = [("keys", C.c_void_p), ("values", C.c_void_p), ("tokens", C.c_int64),
-                ("tier", C.c_int32), ("elem_bytes", C.c_int32), ("load_ms", C.c_double)]
+                ("tier", C.c_int32), ("elem_bytes", C.c_int32), ("load_ms", C.c_double),
+                ("row_elems", C.c_int32), ("col0", C.c_int32)]
 
 
 class keep_memory_stats(C.Structure):
@@ -78,7 +80,7 @@ class keep_profile(C.Structure):
 
 
 PROFILE_PHASES = ["qkv", "attn", "wo", "mlp_in", "mlp_out", "summary", "select", "cached_kv", "compact",
-                  "embed", "logits", "loader"]
+                  "embed", "logits", "loader", "comm", "xchg"]
 
 
 class keep_plan_result(C.Structure):
@@ -133,6 +135,9 @@ def load_library() -> C.CDLL:
                                      C.POINTER(keep_plan_result)]),
         "keep_logits": (C.c_int, [vp, fp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+        "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
+        "keep_loopback_create": (C.c_int, [i32, C.POINTER(vp)]),
+        "keep_loopback_destroy": (C.c_int, [vp]),
         "keep_profile_enable": (C.c_int, [vp, i32]),
         "keep_profile_read": (C.c_int, [vp, C.POINTER(keep_profile), i32]),
     }
@@ -207,13 +212,47 @@ class Layout:
         return [(SEGMENT, i, i, i + 1) for i in range(self.S)]
 
 
+def comm_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (rank 0 makes it, every rank receives it)."""
+    buf = C.create_string_buffer(128)
+    _check(load_library().keep_comm_unique_id(buf))
+    return buf.raw
+
+
+class LoopbackGroup:
+    """G logical ranks on one GPU in one process (one host thread per rank):
+    the test double for the sharded collectives (comm.cu)."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self._h = C.c_void_p()
+        _check(load_library().keep_loopback_create(world, C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            load_library().keep_loopback_destroy(self._h)
+            self._h = C.c_void_p()
+
+
 class Context:
-    """One B200 context: model weights, memory tier and a prefill cursor."""
+    """One B200 context: model weights, memory tier and a prefill cursor.
+
+    KV-head sharding: world > 1 with rank in [0, world) and either nccl_id
+    (bytes from comm_unique_id(), shared by all ranks) or a LoopbackGroup."""
 
     def __init__(self, L: int, H: int, d: int, mlp: int, V: int, seed: int,
-                 numerics: int = PARITY, device: int = 0):
+                 numerics: int = PARITY, device: int = 0, world: int = 1, rank: int = 0,
+                 nccl_id: Optional[bytes] = None, loopback: Optional[LoopbackGroup] = None):
         self.lib = load_library()
-        cfg = keep_config(L, H, d, mlp, V, numerics, seed, device, 1, 0, 0)
+        cfg = keep_config(L, H, d, mlp, V, numerics, seed, device, world, rank, 0)
+        self._id = None
+        if nccl_id is not None:
+            self._id = C.create_string_buffer(bytes(nccl_id), 128)
+            cfg.nccl_id = C.cast(self._id, C.c_void_p)
+        if loopback is not None:
+            cfg.loopback = loopback._h
+        self.world, self.rank = world, rank
+        self.dl = d // world
         self._h = C.c_void_p()
         _check(self.lib.keep_ctx_create(C.byref(cfg), C.byref(self._h)))
         self.L, self.H, self.d, self.mlp, self.V, self.seed = L, H, d, mlp, V, seed
@@ -320,8 +359,9 @@ class Context:
         return {k: getattr(s, k) for k, _ in s._fields_}
 
     def memory_read(self, kind, oid, layer, tokens):
-        k = np.empty((tokens, self.d), np.float32)
-        v = np.empty((tokens, self.d), np.float32)
+        """[tokens x d/world]: this rank's head columns of the block."""
+        k = np.empty((tokens, self.dl), np.float32)
+        v = np.empty((tokens, self.dl), np.float32)
         _check(self.lib.keep_memory_read(self._h, keep_owner(kind, oid), layer, _p(k, C.c_float), _p(v, C.c_float)))
         return k, v
 
@@ -344,7 +384,7 @@ class Context:
 
     def prefill_finish(self, kv=True):
         fh = np.empty((self._T, self.d), np.float32)
-        kvb = np.empty((self.L, 2, self._T, self.d), np.float32) if kv else None
+        kvb = np.empty((self.L, 2, self._T, self.dl), np.float32) if kv else None
         _check(self.lib.keep_prefill_finish(self._h, _p(fh, C.c_float), _p(kvb, C.c_float)))
         return fh, kvb
 

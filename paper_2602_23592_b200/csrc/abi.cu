@@ -16,6 +16,13 @@ using namespace keep_b200;
 namespace {
 
 thread_local std::string g_err;
+}  // namespace
+
+namespace keep_b200 {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace keep_b200
+
+namespace {
 
 template <class F>
 int guard(F&& f) {
@@ -167,23 +174,26 @@ void check_cfg(const keep_config& c) {  // ModelConfig::validate, model.hpp:28-3
     if (c.model_dim / c.num_heads > 128) raise(KEEP_ERR_CONFIG, "head_dim > 128 not supported");
     if (c.numerics == KEEP_NUMERICS_FAST && (c.model_dim % 64 != 0 || c.mlp_dim % 64 != 0))
         raise(KEEP_ERR_CONFIG, "FAST numerics needs model_dim and mlp_dim multiples of 64");
-    if (c.world_size != 1) raise(KEEP_ERR_CONFIG, "head sharding: use one context per rank (world_size 1)");
+    if (c.world_size < 1 || c.rank < 0 || c.rank >= c.world_size) raise(KEEP_ERR_CONFIG, "bad world_size / rank");
+    if (c.num_heads % c.world_size != 0) raise(KEEP_ERR_CONFIG, "num_heads must divide by world_size (KV-head shards)");
+    if (c.numerics == KEEP_NUMERICS_FAST && (c.model_dim / c.world_size) % 64 != 0)
+        raise(KEEP_ERR_CONFIG, "FAST numerics needs model_dim / world_size to be a multiple of 64");
 }
 
 // ------------------------------------------------------------ memory store --
 uint8_t* layer_keys(const Context& c, const Payload& p, int l) {
-    const int64_t sheet = p.arena->rows * c.d * c.elem;
-    return static_cast<uint8_t*>(p.arena->buf.p) + (int64_t(l) * 2) * sheet + p.row0 * c.d * c.elem;
+    const int64_t sheet = p.arena->rows * c.dl * c.elem;
+    return static_cast<uint8_t*>(p.arena->buf.p) + (int64_t(l) * 2) * sheet + p.row0 * c.dl * c.elem;
 }
 uint8_t* layer_values(const Context& c, const Payload& p, int l) {
-    return layer_keys(c, p, l) + p.arena->rows * c.d * c.elem;
+    return layer_keys(c, p, l) + p.arena->rows * c.dl * c.elem;
 }
 
 std::shared_ptr<Arena> make_arena(Context& c, int64_t rows, int tier) {
     auto a = std::make_shared<Arena>();
     a->rows = rows;
     a->tier = tier;
-    a->buf.alloc(size_t(c.L) * 2 * rows * c.d * c.elem, tier == KEEP_TIER_HOST);
+    a->buf.alloc(size_t(c.L) * 2 * rows * c.dl * c.elem, tier == KEEP_TIER_HOST);
     return a;
 }
 
@@ -204,7 +214,8 @@ std::string owner_str(const OwnerKey& k) {
 
 // ----------------------------------------------------------- weight access --
 void model_alloc_init(Context& c) {
-    const int L = c.L, d = c.d, f = c.f, V = c.V;
+    const int L = c.L, d = c.d, f = c.f, V = c.V, dl = c.dl;
+    const int64_t j0 = int64_t(c.R) * dl;  // this rank's head columns of wq / wk / wv
     const double std_ = 1.0 / std::sqrt(double(d));  // model.hpp:56
     cudaStream_t st = c.s_main;
     c.embed.ensure(sizeof(float) * size_t(V) * d);
@@ -220,25 +231,25 @@ void model_alloc_init(Context& c) {
             return name;
         };
         if (!c.fast) {
-            c.w[l * 4 + W_QKV]->ensure(sizeof(float) * size_t(d) * 3 * d);
+            c.w[l * 4 + W_QKV]->ensure(sizeof(float) * size_t(d) * 3 * dl);
             c.w[l * 4 + W_O]->ensure(sizeof(float) * size_t(d) * d);
             c.w[l * 4 + W_IN]->ensure(sizeof(float) * size_t(d) * f);
             c.w[l * 4 + W_OUT]->ensure(sizeof(float) * size_t(f) * d);
-            launch_init_tensor(c.cfg.seed, nm("wq"), d, d, std_, c.wslot(l, W_QKV), 3 * d, 0, false, st);
-            launch_init_tensor(c.cfg.seed, nm("wk"), d, d, std_, c.wslot(l, W_QKV), 3 * d, d, false, st);
-            launch_init_tensor(c.cfg.seed, nm("wv"), d, d, std_, c.wslot(l, W_QKV), 3 * d, 2 * d, false, st);
+            launch_init_tensor(c.cfg.seed, nm("wq"), d, d, std_, c.wslot(l, W_QKV), 3 * dl, 0, false, st, j0, dl);
+            launch_init_tensor(c.cfg.seed, nm("wk"), d, d, std_, c.wslot(l, W_QKV), 3 * dl, dl, false, st, j0, dl);
+            launch_init_tensor(c.cfg.seed, nm("wv"), d, d, std_, c.wslot(l, W_QKV), 3 * dl, 2 * dl, false, st, j0, dl);
             launch_init_tensor(c.cfg.seed, nm("wo"), d, d, std_, c.wslot(l, W_O), d, 0, false, st);
             launch_init_tensor(c.cfg.seed, nm("mlp_in"), d, f, std_, c.wslot(l, W_IN), f, 0, false, st);
             launch_init_tensor(c.cfg.seed, nm("mlp_out"), f, d, std_, c.wslot(l, W_OUT), d, 0, false, st);
         } else {
             const size_t b = sizeof(__nv_bfloat16);
-            c.w[l * 4 + W_QKV]->ensure(b * size_t(3 * d) * d);
+            c.w[l * 4 + W_QKV]->ensure(b * size_t(3 * dl) * d);
             c.w[l * 4 + W_O]->ensure(b * size_t(d) * d);
             c.w[l * 4 + W_IN]->ensure(b * size_t(f) * d);
             c.w[l * 4 + W_OUT]->ensure(b * size_t(d) * f);
-            launch_init_tensor(c.cfg.seed, nm("wq"), d, d, std_, c.wslot(l, W_QKV), d, 0, true, st);
-            launch_init_tensor(c.cfg.seed, nm("wk"), d, d, std_, c.wslot(l, W_QKV), d, d, true, st);
-            launch_init_tensor(c.cfg.seed, nm("wv"), d, d, std_, c.wslot(l, W_QKV), d, 2 * d, true, st);
+            launch_init_tensor(c.cfg.seed, nm("wq"), d, d, std_, c.wslot(l, W_QKV), d, 0, true, st, j0, dl);
+            launch_init_tensor(c.cfg.seed, nm("wk"), d, d, std_, c.wslot(l, W_QKV), d, dl, true, st, j0, dl);
+            launch_init_tensor(c.cfg.seed, nm("wv"), d, d, std_, c.wslot(l, W_QKV), d, 2 * dl, true, st, j0, dl);
             launch_init_tensor(c.cfg.seed, nm("wo"), d, d, std_, c.wslot(l, W_O), d, 0, true, st);
             launch_init_tensor(c.cfg.seed, nm("mlp_in"), d, f, std_, c.wslot(l, W_IN), d, 0, true, st);
             launch_init_tensor(c.cfg.seed, nm("mlp_out"), f, d, std_, c.wslot(l, W_OUT), f, 0, true, st);
@@ -291,7 +302,7 @@ void plan_splits(Context& c, Pass& p) {
         const int target = tc ? 2 * kNumSMs : 4 * kNumSMs;
         nsplit = int(std::min<int64_t>(ceil_div(target, tiles), std::max(1, p.T / 128)));
         // bound the fp64 partial-context scratch to ~512 MB
-        const int64_t per_split = int64_t(p.n) * c.d * 8;
+        const int64_t per_split = int64_t(p.n) * c.dl * 8;
         nsplit = int(std::max<int64_t>(1, std::min<int64_t>(nsplit, (512ll << 20) / std::max<int64_t>(per_split, 1))));
     }
     std::vector<int32_t> lo, hi;
@@ -324,21 +335,22 @@ void plan_splits(Context& c, Pass& p) {
     p.l_part.ensure(sizeof(double) * size_t(nm) * p.n * c.H);
     p.m_fin.ensure(sizeof(double) * size_t(p.n) * c.H);
     p.l_fin.ensure(sizeof(double) * size_t(p.n) * c.H);
-    if (ns > 1 && !tc) p.o_part.ensure(sizeof(double) * size_t(ns) * p.n * c.d);
-    if (tc && p.split_count_a > 1) p.o_part.ensure(sizeof(float) * size_t(p.split_count_a) * p.n * c.d);
+    if (ns > 1 && !tc) p.o_part.ensure(sizeof(double) * size_t(ns) * p.n * c.dl);
+    if (tc && p.split_count_a > 1) p.o_part.ensure(sizeof(float) * size_t(p.split_count_a) * p.n * c.dl);
     p.split_count = ns;
 }
 
 void ensure_layer_scratch(Context& c, Pass& p) {
     const size_t n = size_t(std::max(p.n, 1));
-    if (!c.fast) {
-        p.q.ensure(sizeof(float) * n * c.d);
-        p.ctx.ensure(sizeof(float) * n * c.d);
-        p.h.ensure(sizeof(float) * n * c.f);
-    } else {
-        p.q.ensure(2 * n * c.d);
-        p.ctxb.ensure(2 * n * c.d);
-        p.hb.ensure(2 * n * c.f);
+    // sharded: ctx rows padded to G equal row blocks (all-to-all), Wo / MLP on one block
+    const size_t cpr = size_t(ceil_div(int64_t(n), c.G));
+    const size_t es = c.fast ? 2 : 4;
+    p.q.ensure(es * n * c.dl);
+    (c.fast ? p.ctxb : p.ctx).ensure(es * cpr * c.G * c.dl);
+    (c.fast ? p.hb : p.h).ensure(es * cpr * c.f);
+    if (c.G > 1) {
+        p.xrecv.ensure(es * cpr * c.G * c.dl);
+        p.xrows.ensure(es * cpr * c.d);
     }
     if (p.with_summary && !use_tc_attention(c)) p.rowbin.ensure((c.fast ? 4 : 8) * n * std::max(p.S, 1));
 }
@@ -354,9 +366,17 @@ double visible_pairs(const Pass& p) {
 // (PrefillCursor::step body, prefill.hpp:245-304 minus the cached copy).
 // after_summary runs once the layer's segment summary is complete (the
 // selector for layer l+1 overlaps this layer's Wo + MLP; SPEC D2).
+//
+// KV-head sharding (G > 1): QKV and attention run for this
+// rank's heads over all compact rows (q/k/v/ctx are dl = d/G columns wide,
+// the merged KV holds this rank's head columns); the fp64 summary is summed
+// over ranks (identical bits everywhere, so the selector runs replicated);
+// ctx goes head-sharded -> row-sharded by all-to-all; Wo + MLP run with the
+// full weights on this rank's block of rows (every k-reduction stays on one
+// GPU, as on a single GPU); the fp32 residual rows are all-gathered.
 template <class AfterSummary>
 void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
-    const int n = p.n, d = c.d, f = c.f;
+    const int n = p.n, d = c.d, f = c.f, dl = c.dl;
     cudaStream_t st = c.s_main;
     if (n == 0) return;
     ensure_layer_scratch(c, p);
@@ -365,9 +385,10 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
     AttnArgs a{};
     a.n = n;
     a.T = p.T;
-    a.H = c.H;
+    a.H = c.Hl;
     a.dh = c.dh;
-    a.d = d;
+    a.d = dl;
+    a.inv_heads = 1.0 / c.H;
     a.k = p.kdst[l];
     a.v = p.vdst[l];
     a.rows = rows;
@@ -386,21 +407,28 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
     a.o_part = p.o_part.as<double>();
     a.rowbin = p.rowbin.p;
 
+    // this rank's block of compact rows for Wo + MLP
+    const int G = c.G;
+    const int cpr = int(ceil_div(n, G));
+    const int r0 = std::min(n, c.R * cpr);
+    const int m = std::min(n, r0 + cpr) - r0;
+
     const double wb = c.fast ? 2.0 : 4.0;  // weight / activation element bytes
-    const double gq = 2.0 * n * 3.0 * d * d, go = 2.0 * n * double(d) * d, gi = 2.0 * n * double(d) * f;
-    const double bq = wb * (3.0 * d * d + n * double(d)) + c.elem * 3.0 * n * d;
-    const double bo = wb * (double(d) * d + n * double(d)) + 8.0 * n * d;
-    const double bi = wb * (double(d) * f + n * double(d) + n * double(f));
-    const double bout = wb * (double(d) * f + n * double(f)) + 8.0 * n * d;
+    const double gq = 2.0 * n * 3.0 * dl * d, go = 2.0 * m * double(d) * d, gi = 2.0 * m * double(d) * f;
+    const double bq = wb * (3.0 * dl * d + n * double(d)) + c.elem * 3.0 * n * dl;
+    const double bo = wb * (double(d) * d + m * double(d)) + 8.0 * m * d;
+    const double bi = wb * (double(d) * f + m * double(d) + m * double(f));
+    const double bout = wb * (double(d) * f + m * double(f)) + 8.0 * m * d;
     const double pairs = visible_pairs(p);
     // algorithmic attention: QK^T and PV over visible keys; K+V of the layer read once
-    const double fa = 4.0 * d * pairs, ba = double(c.elem) * (2.0 * p.T * d + 2.0 * n * d);
+    const double fa = 4.0 * dl * pairs, ba = double(c.elem) * (2.0 * p.T * dl + 2.0 * n * dl);
 
     if (!c.fast) {
         {
             ProfScope ps(c.prof, KEEP_PROF_QKV, st, gq, bq);
-            EpiArgs e{EPI_QKV, d, p.q.as<float>(), d, p.kdst[l], p.vdst[l], rows, nullptr};
-            launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * d, n, 3 * d, d, e, st);
+            EpiArgs e{EPI_QKV, dl, p.q.as<float>(), dl, p.kdst[l], p.vdst[l], rows, nullptr};
+            launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * dl, n, 3 * dl, d, e,
+                               st);
         }
         a.q = p.q.p;
         a.ctx = p.ctx.as<float>();
@@ -412,20 +440,21 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
         auto* xb = p.xb.as<__nv_bfloat16>();
         {
             ProfScope ps(c.prof, KEEP_PROF_QKV, st, gq, bq);
-            EpiArgs e{EPI_QKV, d, nullptr, d, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
-            launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_QKV)), d, n, 3 * d, d, e, st);
+            EpiArgs e{EPI_QKV, dl, nullptr, dl, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
+            launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_QKV)), d, n, 3 * dl, d, e, st);
         }
         a.q = p.q.p;
         a.ctx_bf16 = p.ctxb.as<__nv_bfloat16>();
         if (use_tc_attention(c)) {
             ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, p.split_count_a > 1 ? 6 : 5);
-            p.vt.ensure(2 * size_t(d) * size_t(ceil_div(p.T, 64) * 64));
+            p.vt.ensure(2 * size_t(dl) * size_t(ceil_div(p.T, 64) * 64));
             AttnTcLaunch t{};
             t.n = n;
             t.T = p.T;
-            t.H = c.H;
-            t.d = d;
+            t.H = c.Hl;
+            t.d = dl;
             t.S = p.S;
+            t.inv_heads = 1.0 / c.H;
             t.q = p.q.p;
             t.k = p.kdst[l];
             t.v = p.vdst[l];
@@ -453,6 +482,8 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
             t.seg_len = p.d_seg_len.as<int32_t>();
             t.qlen = p.qlen;
             t.chunk_tab = p.chunk_tab.p;
+            t.zt = p.zt.p;
+            t.nb = p.nb;
             launch_attention_tc(t, st);
         } else {
             ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, 5);
@@ -487,40 +518,73 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
             launch_summary_reduce<float>(p.rowbin.as<float>(), p.S, p.seg_cbeg.as<int32_t>(), p.seg_cend.as<int32_t>(),
                                          p.d_seg_len.as<int32_t>(), qb, qe, p.qlen, p.summ.as<double>(), st);
     }
+    if (G > 1 && p.with_summary && p.summary_global) {
+        // per-rank partials (sum over this rank's heads of p / H) -> the summary
+        const size_t ns = size_t(p.S) + size_t(p.S) * p.S;
+        ProfScope ps(c.prof, KEEP_PROF_COMM, st, 0.0, 8.0 * ns * 2.0 * (G - 1) / G, 2);
+        c.comm->allreduce_f64(p.summ.as<double>(), ns, st);
+    }
     after_summary();
-    if (!c.fast) {
-        EpiArgs eo{EPI_RESID, d, p.x.as<float>(), d, nullptr, nullptr, nullptr, nullptr};
+
+    // attention context for the Wo + MLP rows of this rank
+    const int es = c.fast ? 2 : 4;
+    const void* ctx_rows = c.fast ? static_cast<const void*>(p.ctxb.p) : static_cast<const void*>(p.ctx.p);
+    if (G > 1) {
         {
-            ProfScope ps(c.prof, KEEP_PROF_WO, st, go, bo);
-            launch_gemm_f64acc(p.ctx.as<float>(), d, static_cast<const float*>(c.wslot(l, W_O)), d, n, d, d, eo, st);
+            ProfScope ps(c.prof, KEEP_PROF_COMM, st, 0.0, double(es) * cpr * dl * (G - 1), 1);
+            c.comm->alltoall(c.fast ? p.ctxb.p : p.ctx.p, p.xrecv.p, size_t(es) * cpr * dl, st);
         }
-        {
-            ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
-            EpiArgs ei{EPI_RELU, d, p.h.as<float>(), f, nullptr, nullptr, nullptr, nullptr};
-            launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_IN)), f, n, f, d, ei, st);
+        ProfScope ps(c.prof, KEEP_PROF_XCHG, st, 0.0, 2.0 * es * double(m) * d);
+        launch_pack_heads(p.xrecv.p, G, cpr, m, dl, es, p.xrows.p, st);
+        ctx_rows = p.xrows.p;
+    }
+    float* xr = p.x.as<float>() + int64_t(r0) * d;
+    if (m > 0) {
+        if (!c.fast) {
+            EpiArgs eo{EPI_RESID, d, xr, d, nullptr, nullptr, nullptr, nullptr};
+            {
+                ProfScope ps(c.prof, KEEP_PROF_WO, st, go, bo);
+                launch_gemm_f64acc(static_cast<const float*>(ctx_rows), d, static_cast<const float*>(c.wslot(l, W_O)), d, m,
+                                   d, d, eo, st);
+            }
+            {
+                ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
+                EpiArgs ei{EPI_RELU, d, p.h.as<float>(), f, nullptr, nullptr, nullptr, nullptr};
+                launch_gemm_f64acc(xr, d, static_cast<const float*>(c.wslot(l, W_IN)), f, m, f, d, ei, st);
+            }
+            {
+                ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
+                launch_gemm_f64acc(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, m, d, f, eo, st);
+            }
+        } else {
+            auto* xbr = p.xb.as<__nv_bfloat16>() + int64_t(r0) * d;
+            const int mc = c.gemm_ctas;
+            EpiArgs eo{EPI_RESID, d, xr, d, nullptr, nullptr, nullptr, xbr};
+            {
+                ProfScope ps(c.prof, KEEP_PROF_WO, st, go, bo);
+                launch_gemm_bf16(static_cast<const __nv_bfloat16*>(ctx_rows), d,
+                                 static_cast<const __nv_bfloat16*>(c.wslot(l, W_O)), d, m, d, d, eo, st, mc);
+            }
+            {
+                ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
+                EpiArgs ei{EPI_RELU, d, nullptr, f, nullptr, nullptr, nullptr, p.hb.as<__nv_bfloat16>()};
+                launch_gemm_bf16(xbr, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_IN)), d, m, f, d, ei, st, mc);
+            }
+            {
+                ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
+                launch_gemm_bf16(p.hb.as<__nv_bfloat16>(), f, static_cast<const __nv_bfloat16*>(c.wslot(l, W_OUT)), f, m, d,
+                                 f, eo, st, mc);
+            }
         }
+    }
+    if (G > 1) {
         {
-            ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
-            launch_gemm_f64acc(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, n, d, f, eo, st);
+            ProfScope ps(c.prof, KEEP_PROF_COMM, st, 0.0, 4.0 * cpr * double(d) * (G - 1), 1);
+            c.comm->allgather(p.x.as<float>() + int64_t(c.R) * cpr * d, p.x.p, sizeof(float) * size_t(cpr) * d, st);
         }
-    } else {
-        auto* xb = p.xb.as<__nv_bfloat16>();
-        const int mc = c.gemm_ctas;
-        EpiArgs eo{EPI_RESID, d, p.x.as<float>(), d, nullptr, nullptr, nullptr, xb};
-        {
-            ProfScope ps(c.prof, KEEP_PROF_WO, st, go, bo);
-            launch_gemm_bf16(p.ctxb.as<__nv_bfloat16>(), d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_O)), d, n, d, d, eo,
-                             st, mc);
-        }
-        {
-            ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
-            EpiArgs ei{EPI_RELU, d, nullptr, f, nullptr, nullptr, nullptr, p.hb.as<__nv_bfloat16>()};
-            launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_IN)), d, n, f, d, ei, st, mc);
-        }
-        {
-            ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
-            launch_gemm_bf16(p.hb.as<__nv_bfloat16>(), f, static_cast<const __nv_bfloat16*>(c.wslot(l, W_OUT)), f, n, d, f, eo,
-                             st, mc);
+        if (c.fast) {
+            ProfScope ps(c.prof, KEEP_PROF_XCHG, st, 0.0, 6.0 * double(n) * d);
+            launch_to_bf16(p.x.as<float>(), int64_t(n) * d, p.xb.as<__nv_bfloat16>(), st);
         }
     }
 }
@@ -544,7 +608,7 @@ void set_rows(Context& c, Pass& p, const std::vector<int32_t>& rows_new, bool fi
         }
         upload(p.d_idx, idx, st);
         ProfScope ps(c.prof, KEEP_PROF_COMPACT, st, 0.0, double(n_new) * c.d * (8.0 + (c.fast ? 2.0 : 0.0)));
-        p.x_alt.ensure(sizeof(float) * size_t(std::max(n_new, 1)) * c.d);
+        p.x_alt.ensure(sizeof(float) * size_t(std::max(n_new, 1) + c.G) * c.d);
         launch_gather_rows(p.x.as<float>(), p.d_idx.as<int32_t>(), n_new, c.d, p.x_alt.as<float>(),
                            c.fast ? p.xb.as<__nv_bfloat16>() : nullptr, st);
         std::swap(p.x.p, p.x_alt.p);
@@ -585,11 +649,17 @@ void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const i
     if (use_tc_attention(c)) {
         p.chunk_tab.ensure(32 * size_t(std::max<int64_t>(1, ceil_div(p.T, 128))));
         launch_chunk_table(p.d_row_seg.as<int32_t>(), p.T, p.chunk_tab.p, st);
+        p.nb = summary_bins_width(p.row_seg);
+        if (p.nb > 0 && bins_on_tensor_core()) {
+            p.zt.ensure(2 * size_t(ceil_div(p.T, 128)) * p.nb * 128);
+            launch_zt_build(p.d_row_seg.as<int32_t>(), p.T, p.chunk_tab.p, p.nb, p.zt.p, st);
+        }
     }
     std::vector<int32_t> all(p.T);
     std::iota(all.begin(), all.end(), 0);
-    p.x.ensure(sizeof(float) * size_t(std::max(p.T, 1)) * c.d);
-    if (c.fast) p.xb.ensure(2 * size_t(std::max(p.T, 1)) * c.d);
+    // (+G rows: the sharded all-gather moves G equal row blocks)
+    p.x.ensure(sizeof(float) * size_t(std::max(p.T, 1) + c.G) * c.d);
+    if (c.fast) p.xb.ensure(2 * size_t(std::max(p.T, 1) + c.G) * c.d);
     set_rows(c, p, all, true);
     ProfScope ps(c.prof, KEEP_PROF_EMBED, st, 0.0, double(p.T) * c.d * (8.0 + (c.fast ? 2.0 : 0.0)), c.fast ? 2 : 1);
     launch_embed(c.embed.as<float>(), p.d_tokens.as<int32_t>(), p.d_rows.as<int32_t>(), p.T, c.d,
@@ -625,8 +695,8 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
             raise(KEEP_ERR_CACHE_MISS, "owner " + owner_str(ok) + " is host-resident: load it first");
         if (c.seg_owner_row[i] + p.seg_len[i] > pl->tokens)
             raise(KEEP_ERR_INPUT, "cached block of " + owner_str(ok) + " is shorter than its members");
-        ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * c.d * c.elem);
-        vs.push_back(layer_values(c, *pl, l) + c.seg_owner_row[i] * c.d * c.elem);
+        ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * c.dl * c.elem);
+        vs.push_back(layer_values(c, *pl, l) + c.seg_owner_row[i] * c.dl * c.elem);
         dr.push_back(p.seg_start[i]);
         nr.push_back(p.seg_len[i]);
         maxr = std::max(maxr, p.seg_len[i]);
@@ -645,13 +715,13 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
     if (!ks.empty()) {
         double rows_copied = 0.0;
         for (int32_t r : nr) rows_copied += r;
-        ProfScope ps(c.prof, KEEP_PROF_CACHED, st, 0.0, rows_copied * c.d * c.elem * 4.0);
+        ProfScope ps(c.prof, KEEP_PROF_CACHED, st, 0.0, rows_copied * c.dl * c.elem * 4.0);
         upload(c.d_ksrc, ks, st);
         upload(c.d_vsrc, vs, st);
         upload(c.d_cdst, dr, st);
         upload(c.d_cn, nr, st);
         launch_copy_cached(c.d_ksrc.as<const void*>(), c.d_vsrc.as<const void*>(), c.d_cdst.as<int32_t>(),
-                           c.d_cn.as<int32_t>(), int(ks.size()), int64_t(c.d) * c.elem, p.kdst[l], p.vdst[l],
+                           c.d_cn.as<int32_t>(), int(ks.size()), int64_t(c.dl) * c.elem, p.kdst[l], p.vdst[l],
                            maxr, st);
     }
     p.with_summary = true;
@@ -704,9 +774,10 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
     if (!c.pf) c.pf.reset(new Pass());
     Pass& p = *c.pf;
     p.block_diag = false;
+    p.summary_global = true;
     p.key_lo_h.clear();
     pass_init(c, p, sl, lay->tokens, query, qlen);
-    const size_t sheet = size_t(p.T) * c.d * c.elem;
+    const size_t sheet = size_t(p.T) * c.dl * c.elem;
     c.kv.ensure(std::max<size_t>(size_t(c.L) * 2 * sheet, 16));
     p.kdst.resize(c.L);
     p.vdst.resize(c.L);
@@ -735,7 +806,7 @@ void cursor_finish(Context& c, float* final_hidden, float* kv_out) {
             std::memcpy(final_hidden + size_t(p.rows_h[i]) * d, xc.data() + size_t(i) * d, sizeof(float) * d);
     }
     if (kv_out) {
-        const size_t nel = size_t(c.L) * 2 * p.T * d;
+        const size_t nel = size_t(c.L) * 2 * p.T * c.dl;
         if (!c.fast) {
             KEEP_CUDA(cudaMemcpy(kv_out, c.kv.p, sizeof(float) * nel, cudaMemcpyDeviceToHost));
         } else {
@@ -784,7 +855,7 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
         for (int t = 0; t < seglen[o]; ++t) p.key_lo_h[row0[o] + t] = int32_t(row0[o]);
     upload(p.d_key_lo, p.key_lo_h, c.s_main);
     auto dev = make_arena(c, rows, KEEP_TIER_DEVICE);
-    const size_t sheet = size_t(rows) * c.d * c.elem;
+    const size_t sheet = size_t(rows) * c.dl * c.elem;
     p.kdst.resize(c.L);
     p.vdst.resize(c.L);
     for (int l = 0; l < c.L; ++l) {
@@ -831,7 +902,7 @@ int keep_ctx_create(const keep_config* cfg, void** out) {
         cudaDeviceProp prop{};
         KEEP_CUDA(cudaGetDeviceProperties(&prop, cfg->device));
         if (prop.major != 10) raise(KEEP_ERR_CONFIG, "keep_b200 requires an sm_100 (B200) device");
-        auto* c = new Context();
+        std::unique_ptr<Context> c(new Context());
         c->cfg = *cfg;
         c->L = cfg->num_layers;
         c->H = cfg->num_heads;
@@ -841,12 +912,17 @@ int keep_ctx_create(const keep_config* cfg, void** out) {
         c->V = cfg->vocab_size;
         c->fast = cfg->numerics == KEEP_NUMERICS_FAST;
         c->elem = c->fast ? 2 : 4;
+        c->G = cfg->world_size;
+        c->R = cfg->rank;
+        c->Hl = c->H / c->G;
+        c->dl = c->Hl * c->dh;
+        c->comm = make_comm(*cfg);
         KEEP_CUDA(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
         KEEP_CUDA(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
         KEEP_CUDA(cudaStreamCreateWithFlags(&c->s_sel, cudaStreamNonBlocking));
         KEEP_CUDA(cudaEventCreate(&c->ev_a));
         KEEP_CUDA(cudaEventCreate(&c->ev_b));
-        *out = c;
+        *out = c.release();
     });
 }
 
@@ -856,7 +932,9 @@ int keep_ctx_destroy(void* ctx) {
         Context* c = C(ctx);
         cudaDeviceSynchronize();
         c->pf.reset();
+        c->refresh.reset();
         c->store.clear();
+        c->comm.reset();
         cudaStreamDestroy(c->s_main);
         cudaStreamDestroy(c->s_copy);
         cudaStreamDestroy(c->s_sel);
@@ -922,7 +1000,7 @@ int keep_memory_put(void* ctx, keep_owner owner, uint64_t version, int32_t layer
                 pl.tokens = tokens;
                 pl.layer_version = it->second.layer_version;
                 pl.present = it->second.present;
-                const size_t blk = size_t(tokens) * c.d * c.elem;
+                const size_t blk = size_t(tokens) * c.dl * c.elem;
                 for (int l = 0; l < c.L; ++l) {
                     if (!pl.present[l]) continue;
                     KEEP_CUDA(cudaMemcpy(layer_keys(c, pl, l), layer_keys(c, it->second, l), blk, cudaMemcpyDefault));
@@ -937,16 +1015,21 @@ int keep_memory_put(void* ctx, keep_owner owner, uint64_t version, int32_t layer
             c.store[k] = std::move(pl);
         }
         Payload& pl = c.store[k];
-        const size_t nel = size_t(tokens) * c.d;
+        // this rank's head columns of the full rows
+        const int64_t dl = c.dl, c0 = int64_t(c.R) * dl;
+        const size_t nel = size_t(tokens) * dl;
         if (!c.fast) {
-            KEEP_CUDA(cudaMemcpy(layer_keys(c, pl, layer), keys, 4 * nel, cudaMemcpyDefault));
-            KEEP_CUDA(cudaMemcpy(layer_values(c, pl, layer), values, 4 * nel, cudaMemcpyDefault));
+            KEEP_CUDA(cudaMemcpy2D(layer_keys(c, pl, layer), dl * 4, keys + c0, size_t(c.d) * 4, dl * 4, tokens,
+                                   cudaMemcpyDefault));
+            KEEP_CUDA(cudaMemcpy2D(layer_values(c, pl, layer), dl * 4, values + c0, size_t(c.d) * 4, dl * 4, tokens,
+                                   cudaMemcpyDefault));
         } else {
             std::vector<uint16_t> tk(nel), tv(nel);
-            for (size_t i = 0; i < nel; ++i) {
-                tk[i] = f2bf(keys[i]);
-                tv[i] = f2bf(values[i]);
-            }
+            for (int64_t t = 0; t < tokens; ++t)
+                for (int64_t j = 0; j < dl; ++j) {
+                    tk[t * dl + j] = f2bf(keys[t * c.d + c0 + j]);
+                    tv[t * dl + j] = f2bf(values[t * c.d + c0 + j]);
+                }
             KEEP_CUDA(cudaMemcpy(layer_keys(c, pl, layer), tk.data(), 2 * nel, cudaMemcpyDefault));
             KEEP_CUDA(cudaMemcpy(layer_values(c, pl, layer), tv.data(), 2 * nel, cudaMemcpyDefault));
         }
@@ -986,9 +1069,11 @@ int keep_load_memory(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* o
         out->elem_bytes = c.elem;
         out->tier = P.arena->tier;
         out->load_ms = 0.0;
+        out->row_elems = c.dl;
+        out->col0 = c.R * c.dl;
         if (P.arena->tier == KEEP_TIER_HOST) {
             // slow tier: copy the block to HBM and promote the owner (117-127)
-            const size_t blk = size_t(P.tokens) * c.d * c.elem;
+            const size_t blk = size_t(P.tokens) * c.dl * c.elem;
             auto dev = make_arena(c, P.tokens, KEEP_TIER_DEVICE);
             Payload np;
             np.arena = dev;
@@ -1068,7 +1153,7 @@ int keep_memory_read(void* ctx, keep_owner owner, int32_t layer, float* keys, fl
         const Payload* pl = nullptr;
         if (!block_current(c, OwnerKey{owner.kind, owner.id}, layer, &pl))
             raise(KEEP_ERR_CACHE_MISS, "no current block");
-        const size_t nel = size_t(pl->tokens) * c.d;
+        const size_t nel = size_t(pl->tokens) * c.dl;
         if (!c.fast) {
             KEEP_CUDA(cudaMemcpy(keys, layer_keys(c, *pl, layer), 4 * nel, cudaMemcpyDefault));
             KEEP_CUDA(cudaMemcpy(values, layer_values(c, *pl, layer), 4 * nel, cudaMemcpyDefault));
@@ -1265,7 +1350,10 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
                 KEEP_CUDA(cudaEventRecord(ev_sel, c.s_sel));
             };
             c.gemm_ctas = walk ? kNumSMs - 1 : kNumSMs;
+            // sharded: the per-rank summary partials are summed only when read
+            p.summary_global = walk || (out && out->summaries) || (l + 1 < L && budget < live && !multihop);
             cursor_layer(c, active.data(), launch_walk);
+            p.summary_global = true;
             c.gemm_ctas = kNumSMs;
             if (out && out->rows_per_layer) out->rows_per_layer[l] = p.n;
             if (out && out->summaries)

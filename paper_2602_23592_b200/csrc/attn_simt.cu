@@ -349,7 +349,7 @@ void run_attention(const AttnArgs& a, cudaStream_t st) {
     }
     if (a.with_bins) {
         dim3 g3(tiles, a.nsplit);
-        k3<<<g3, NT, smem, st>>>(a, scale, ACC(1.0 / a.H));
+        k3<<<g3, NT, smem, st>>>(a, scale, ACC(a.inv_heads));
         KEEP_LAUNCH_CHECK();
     }
 }

@@ -17,7 +17,8 @@ void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* 
 
 // FAST attention on tcgen05 (head_dim 128): stats / context / bins passes.
 struct AttnTcLaunch {
-    int n, T, H, d, S;
+    int n, T, H, d, S;        // H = this rank's heads, d = H * 128
+    double inv_heads;         // 1 / (heads of the model)
     const void* q;            // [n x d] bf16 compact queries
     const void* k;            // [T x d] bf16 merged keys
     const void* v;            // [T x d] bf16 merged values
@@ -40,10 +41,31 @@ struct AttnTcLaunch {
     const int32_t* seg_len;   // [S]
     int qlen;
     const void* chunk_tab;    // launch_chunk_table output (summary only)
+    const void* zt;           // launch_zt_build output: Z^T tiles [nchunks * nb x 128] bf16
+    int nb;                   // summary bins per chunk on the tensor core (16 / 32; 0 = scan bins)
 };
 void launch_attention_tc(const AttnTcLaunch& a, cudaStream_t st);
 // per-128-key-chunk destination-segment table (32 B per chunk)
 void launch_chunk_table(const int32_t* row_seg, int T, void* tab, cudaStream_t st);
+// bins width for a layout (max segments touching a 128-key chunk, rounded to
+// 16 / 32; 0 when some chunk has more than 32) and the Z^T indicator tiles
+int summary_bins_width(const std::vector<int32_t>& row_seg);
+bool bins_on_tensor_core();  // KEEP_BINS=mma: bf16 P . Z bins (fast, bf16-precision summary)
+void launch_zt_build(const int32_t* row_seg, int T, const void* tab, int nb, void* zt, cudaStream_t st);
+
+// Collectives of KV-head sharding (comm.cu).  All stream-ordered on `st`.
+struct Comm {
+    int world = 1, rank = 0;
+    virtual ~Comm() = default;
+    // sum over ranks; every rank receives identical bits
+    virtual void allreduce_f64(double* buf, size_t n, cudaStream_t st) = 0;
+    // recv = blocks of `bytes` from every rank in rank order (send may be recv + rank*bytes)
+    virtual void allgather(const void* send, void* recv, size_t bytes, cudaStream_t st) = 0;
+    // send block q -> rank q; recv block q <- rank q
+    virtual void alltoall(const void* send, void* recv, size_t bytes, cudaStream_t st) = 0;
+};
+std::unique_ptr<Comm> make_comm(const keep_config& cfg);
+void set_last_error(const std::string& msg);
 
 // Per-phase CUDA-event timing (keep_profile_*).
 struct Profiler {
@@ -127,10 +149,13 @@ struct Pass {
     int n = 0;
     DevBuf d_rows, d_rows_tmp, d_idx;
     DevBuf x, x_alt, xb, q, ctx, ctxb, h, hb;
+    DevBuf xrecv, xrows;          // sharded: all-to-all receive [G][rows/G][dl], packed ctx rows
+    bool summary_global = true;   // sharded: sum the summary over ranks this layer
     // attention scratch
     DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi;
     int split_count = 1;
-    DevBuf vt, split_lo_a, split_hi_a, chunk_tab;  // FAST tensor-core attention
+    DevBuf vt, split_lo_a, split_hi_a, chunk_tab, zt;  // FAST tensor-core attention
+    int nb = 0;
     int split_count_a = 1;
     DevBuf seg_cbeg, seg_cend, summ, summ_raw;
     // merged KV destination per layer (device)
@@ -142,6 +167,10 @@ struct Pass {
 struct Context {
     keep_config cfg{};
     int L = 0, H = 0, d = 0, dh = 0, f = 0, V = 0;
+    // KV-head sharding: this rank owns heads [R*Hl, (R+1)*Hl), i.e. the
+    // q/k/v/ctx columns [R*dl, (R+1)*dl); G = 1 is the single-GPU path
+    int G = 1, R = 0, Hl = 0, dl = 0;
+    std::unique_ptr<Comm> comm;
     bool fast = false;
     int elem = 4;  // merged-KV element bytes
     cudaStream_t s_main = nullptr, s_copy = nullptr, s_sel = nullptr;

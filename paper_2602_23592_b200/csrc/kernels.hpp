@@ -10,9 +10,10 @@ namespace keep_b200 {
 // of Rng::stream(seed, name).  Written either fp32 row-major into a wider
 // matrix (dst[i*ld + col_off + j]) or bf16 transposed (dst[(col_off+j)*ld + i]).
 uint64_t fnv1a64_host(const char* s);
+// [j0, j0 + jn) selects a column window (jn < 0: to the last column).
 void launch_init_tensor(uint64_t seed, const char* name, int64_t rows, int64_t cols, double std_,
                         void* dst, int64_t ld, int64_t col_off, bool bf16_transposed,
-                        cudaStream_t st);
+                        cudaStream_t st, int64_t j0 = 0, int64_t jn = -1);
 
 // K1: x[i] = embed[tokens[rows[i]]] (prefill.hpp:201-211).
 void launch_embed(const float* embed, const int32_t* tokens, const int32_t* rows, int64_t n, int d,
@@ -22,6 +23,10 @@ void launch_embed(const float* embed, const int32_t* tokens, const int32_t* rows
 void launch_gather_rows(const float* src, const int32_t* idx, int64_t n, int d, float* dst,
                         __nv_bfloat16* dst_bf16, cudaStream_t st);
 void launch_to_bf16(const float* src, int64_t n, __nv_bfloat16* dst, cudaStream_t st);
+
+// KV-head sharding: all-to-all receive [G][cpr][dl] (block s = rank s's head
+// columns of this rank's rows) -> row-major rows [m][G*dl]; es = element bytes.
+void launch_pack_heads(const void* recv, int G, int cpr, int m, int dl, int es, void* rows, cudaStream_t st);
 
 // K4: merged-KV assembly from cached blocks (prefill.hpp:255-263, 340-350).
 // For entry e: copy rows [dst_row[e], dst_row[e]+nrows[e]) of K and V from
@@ -72,7 +77,8 @@ void launch_gemm_f64acc(const float* A, int64_t lda, const float* B, int64_t ldb
 struct AttnArgs {
     int n;          // compact rows
     int T;          // keys
-    int H, dh, d;
+    int H, dh, d;   // heads of this rank, head dim, q/k/v/ctx row width (H * dh)
+    double inv_heads;  // 1 / (heads of the model): summary bins are partial sums over this rank's heads
     const void* q;  // [n x d] compact queries (fp32 PARITY / bf16 FAST)
     const void* k;  // [T x d] merged keys
     const void* v;  // [T x d] merged values

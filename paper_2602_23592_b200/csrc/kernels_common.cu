@@ -56,30 +56,54 @@ __device__ __forceinline__ float normal_at(uint64_t s0, uint64_t e, double std_)
 
 // Output-order traversal so the (possibly transposed) stores coalesce; the
 // counter-based stream lets every element be drawn independently.
-__global__ void init_tensor_kernel(uint64_t s0, int64_t rows, int64_t cols, double std_, void* dst,
-                                   int64_t ld, int64_t col_off, int transposed) {
-    const int64_t n = rows * cols;
+__global__ void init_tensor_kernel(uint64_t s0, int64_t rows, int64_t cols, int64_t j0, int64_t jn, double std_,
+                                   void* dst, int64_t ld, int64_t col_off, int transposed) {
+    // columns [j0, j0 + jn) of the named [rows x cols] tensor (a head shard);
+    // element (i, j) is normal #(i*cols + j) of the stream either way
+    const int64_t n = rows * jn;
     for (int64_t o = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; o < n;
          o += int64_t(gridDim.x) * blockDim.x) {
         if (!transposed) {
-            const int64_t i = o / cols, j = o % cols;
-            static_cast<float*>(dst)[i * ld + col_off + j] = normal_at(s0, uint64_t(o), std_);
+            const int64_t i = o / jn, jj = o % jn;
+            static_cast<float*>(dst)[i * ld + col_off + jj] = normal_at(s0, uint64_t(i * cols + j0 + jj), std_);
         } else {
-            const int64_t j = o / rows, i = o % rows;  // dst row j (output), col i (input)
-            static_cast<__nv_bfloat16*>(dst)[(col_off + j) * ld + i] =
-                __float2bfloat16_rn(normal_at(s0, uint64_t(i * cols + j), std_));
+            const int64_t jj = o / rows, i = o % rows;  // dst row jj (output), col i (input)
+            static_cast<__nv_bfloat16*>(dst)[(col_off + jj) * ld + i] =
+                __float2bfloat16_rn(normal_at(s0, uint64_t(i * cols + j0 + jj), std_));
         }
     }
 }
 
 void launch_init_tensor(uint64_t seed, const char* name, int64_t rows, int64_t cols, double std_,
                         void* dst, int64_t ld, int64_t col_off, bool bf16_transposed,
-                        cudaStream_t st) {
+                        cudaStream_t st, int64_t j0, int64_t jn) {
     const uint64_t s0 = seed ^ fnv1a64_host(name);
-    const int64_t n = rows * cols;
+    if (jn < 0) jn = cols - j0;
+    const int64_t n = rows * jn;
     const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n, 256), kNumSMs * 16));
-    init_tensor_kernel<<<grid, 256, 0, st>>>(s0, rows, cols, std_, dst, ld, col_off,
+    init_tensor_kernel<<<grid, 256, 0, st>>>(s0, rows, cols, j0, jn, std_, dst, ld, col_off,
                                              bf16_transposed ? 1 : 0);
+    KEEP_LAUNCH_CHECK();
+}
+
+__global__ void pack_heads_kernel(const uint32_t* __restrict__ recv, int G, int cpr, int m, int wpr,
+                                  uint32_t* __restrict__ rows) {
+    // wpr = 32-bit words per (row, rank) slice
+    const int64_t total = int64_t(m) * G * wpr;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int w = int(e % wpr);
+        const int64_t rs = e / wpr;
+        const int s = int(rs % G), i = int(rs / G);
+        rows[e] = recv[(int64_t(s) * cpr + i) * wpr + w];
+    }
+}
+
+void launch_pack_heads(const void* recv, int G, int cpr, int m, int dl, int es, void* rows, cudaStream_t st) {
+    if (m <= 0) return;
+    const int wpr = dl * es / 4;
+    const int64_t total = int64_t(m) * G * wpr;
+    pack_heads_kernel<<<unsigned(std::min<int64_t>(ceil_div(total, 256), kNumSMs * 8)), 256, 0, st>>>(
+        static_cast<const uint32_t*>(recv), G, cpr, m, wpr, static_cast<uint32_t*>(rows));
     KEEP_LAUNCH_CHECK();
 }
 

@@ -52,12 +52,24 @@ def results_tc(ko):
     return _run(ko, CASES_TC)
 
 
+# summaries relative to their max entry: the tensor-core bins see bf16 P
+# (2^-9 per probability) on top of the bf16 Q.K^T logits
+RTOL_SUMMARY = 1e-2
+
+
 def test_tc_attention_numerics(results_tc):
     for p, w, ref, got, sel in results_tc:
         assert rel(sel["final_hidden"], ref["final_hidden"]) <= RTOL_FAST
         assert rel(sel["kv"], ref["kv"]) <= RTOL_FAST
-        assert np.max(np.abs(sel["qts"] - ref["qts"])) <= 2e-2
-        assert np.max(np.abs(sel["sts"] - ref["sts"])) <= 2e-2
+        assert rel(sel["qts"], ref["qts"]) <= RTOL_SUMMARY
+        assert rel(sel["sts"], ref["sts"]) <= RTOL_SUMMARY
+        # strictly-lower (source, destination) pairs carry mass as in the reference
+        # (fp32 exp2 may flush a few far-tail probabilities to zero)
+        S = len(p.seg_len)
+        lt = np.tril_indices(S, -1)
+        z_got = np.count_nonzero(sel["sts"][:, lt[0], lt[1]] == 0)
+        z_ref = np.count_nonzero(ref["sts"][:, lt[0], lt[1]] == 0)
+        assert z_got <= z_ref + 0.01 * sel["sts"].shape[0] * len(lt[0]), (z_got, z_ref)
 
 
 def test_fast_selection_agreement(results):
