@@ -445,37 +445,46 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 }
 
 // ===================================================================== v2 ==
-// 384 threads: warp 0 TMA, warp 1 MMA, warp 2 TMEM allocator, warp 3 idle,
-// warps 4-7 (half 0) and 8-11 (half 1) softmax.  A row lives in one TMEM
-// lane; half h owns keys [64h, 64h+64) of every chunk -- exactly one 64-wide
-// swizzle box of the P tile -- so two warps share each SM sub-partition and
-// the exp2 / pack work per thread halves.
+// 640 threads: warp 0 TMA, warp 1 MMA, warp 2 TMEM allocator, warp 3 idle,
+// warps 4..19 softmax in NG = 4 key groups: group g (warps 4+4g..7+4g) owns
+// keys [32g, 32g+32) of every 128-key chunk; a row lives in one TMEM lane,
+// so four warps share each SM sub-partition and hide each other's latency.
 //
-// CTX segment summary on the tensor core: per chunk, BINS[128 x NB] =
-// P[128 x 128] . Z[128 x NB] with Z the one-hot key -> destination-segment
-// indicator of the chunk (prefill constant, built once per prefill by
-// zt_build_kernel, TMA-staged with K and V^T).  The query keys have no
-// column (their mass is dropped, prefill.hpp:283).  The softmax warps read
-// the finished bins of the previous chunk from TMEM (double buffered), zero
-// the row's own segment (prefill.hpp:284), reduce rows per source segment
-// through shared memory and add one fp64 atomic per (source, destination).
-// Half h reduces bins columns [h*NB/2, (h+1)*NB/2).
-constexpr int NTHR2 = 384;
+// CTX: p = exp2(s*scale - m) / l (fp32) is split into hi = bf16(p) and
+// lo = bf16(p - hi) and written back into the TMEM columns of the S buffer
+// it came from; tcgen05.mma reads them as the A operand (TS form):
+//   O    += hi . V                (P.V, bf16 P as in flash attention)
+//   BINS  = hi . Z + lo . Z       (segment summary, 16 bits of p: the
+//                                  precision the reference's near-tied
+//                                  selections need)
+// Z is the one-hot key -> destination-segment indicator of the chunk
+// (prefill constant, zt_build_kernel, TMA-staged with K and V^T); query keys
+// have no column (their mass is dropped, prefill.hpp:283).  The softmax warps
+// read the finished bins of the previous chunk from TMEM (double buffered),
+// zero the row's own segment (prefill.hpp:284), reduce rows per source
+// segment through shared memory and add one fp64 atomic per pair; group g
+// reduces bins columns [g*NB/4, (g+1)*NB/4).
+constexpr int NG = 4;             // softmax key groups
+constexpr int KW = TK / NG;       // keys per group per chunk
+constexpr int NTHR2 = 128 + NG * 128;
 constexpr uint32_t BINS_COL = 384;  // TMEM: S 0..255, O 256..383, bins 384..
 
-// NB > 0: bins on the tensor core (bf16 P . Z, NB columns); NB == 0: fp32
-// bins on the CUDA cores (segmented scan of the fp32 probabilities in key
-// order -- the precision the reference's near-tied selections need).
+// Two TMA rings: K (STATS: 4 stages; CTX: ST) freed after Q.K^T, and (CTX)
+// V^T + Z (2 stages) freed after P.V -- so K runs ahead of the softmax
+// instead of waiting behind V for the previous P.V.
 template <int MODE, int NB>
 struct Layout2 {
-    static constexpr int ST = MODE == MODE_STATS ? 4 : 2;
+    static constexpr int ST = MODE == MODE_STATS ? 4 : (NB <= 16 ? 3 : 2);  // K stages
+    static constexpr int NH = NB / NG;  // bins columns per key group
     static constexpr uint32_t ZB = NB * 128 * 2;  // Z^T tile [NB x 128] bf16 (2 boxes of NB x 64)
-    static constexpr uint32_t STAGE = MODE == MODE_STATS ? TILE_BYTES : 2 * TILE_BYTES + ZB;
+    static constexpr uint32_t STAGE = TILE_BYTES;  // K ring stage
+    static constexpr uint32_t VSTAGE = TILE_BYTES + ZB;  // V^T (+ Z) ring stage
     static constexpr uint32_t Q_OFF = 0;
     static constexpr uint32_t STAGE_OFF = TILE_BYTES;
-    static constexpr uint32_t P_OFF = STAGE_OFF + ST * STAGE;
-    static constexpr uint32_t PART_OFF = MODE == MODE_STATS ? P_OFF : P_OFF + TILE_BYTES;
-    static constexpr uint32_t PART_BYTES = MODE == MODE_STATS ? TM * 2 * 4 : (NB == 0 ? 2 * 32 * TM * 4 : 2 * TM * 16 * 4);
+    static constexpr uint32_t VSTAGE_OFF = STAGE_OFF + ST * STAGE;
+    static constexpr uint32_t PART_OFF = VSTAGE_OFF + (MODE == MODE_CTX ? 2 * VSTAGE : 0);
+    // STATS: (m, l) of groups 1..NG-1; CTX: bins partials [2 buf][NG][128][NH]
+    static constexpr uint32_t PART_BYTES = MODE == MODE_STATS ? (NG - 1) * TM * 2 * 4 : 2 * NG * TM * NH * 4;
     static constexpr uint32_t GRP_OFF = PART_OFF + PART_BYTES;  // CTX: groups [130] + sources [130]
     static constexpr uint32_t MSK_OFF = GRP_OFF + (2 * TM + 4) * 4;
     static constexpr uint32_t BAR_OFF = (MSK_OFF + 16 + 7) & ~7u;
@@ -483,7 +492,6 @@ struct Layout2 {
     static constexpr uint32_t TMEM_COLS = MODE == MODE_CTX ? 512 : 256;
 };
 static_assert(Layout2<MODE_CTX, 32>::SMEM <= 232448, "CTX v2 smem");
-static_assert(Layout2<MODE_CTX, 0>::SMEM <= 232448, "CTX v2 scan smem");
 static_assert(Layout2<MODE_STATS, 16>::SMEM <= 232448, "STATS v2 smem");
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -493,19 +501,22 @@ __global__ void __launch_bounds__(NTHR2, 1)
 attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmVt, const __grid_constant__ CUtensorMap tmZ, TcArgs a) {
     using LY = Layout2<MODE, NB>;
-    constexpr uint32_t IDESC_B = instr_desc(128, NB > 0 ? NB : 16);
+    constexpr uint32_t IDESC_B = instr_desc(128, NB);
+    constexpr int NH = LY::NH;  // bins columns reduced per group
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared space
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + LY::BAR_OFF);
     uint64_t* full = bar;          // [ST]
     uint64_t* empty = bar + 4;     // [ST]
     uint64_t* s_full = bar + 8;    // [2]
-    uint64_t* s_empty = bar + 10;  // [2]
-    uint64_t* p_full = bar + 12;
-    uint64_t* p_empty = bar + 13;
+    uint64_t* s_empty = bar + 10;  // [2] (STATS)
+    uint64_t* p_full = bar + 12;   // (CTX)
     uint64_t* q_full = bar + 14;
     uint64_t* o_full = bar + 15;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+    uint64_t* bins_full = bar + 16;  // [2]
+    uint64_t* vfull = bar + 18;      // [2] V ring (CTX)
+    uint64_t* vempty = bar + 20;     // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 22);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = blockIdx.x * TM;
@@ -523,17 +534,19 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         prefetch_map(&tmQ);
         prefetch_map(&tmK);
         if (MODE == MODE_CTX) prefetch_map(&tmVt);
-        if (NB > 0 && bins) prefetch_map(&tmZ);
+        if (bins) prefetch_map(&tmZ);
         for (int s = 0; s < LY::ST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&s_full[b], 1);
-            mbar_init(&s_empty[b], 8);
+            mbar_init(&s_empty[b], NG * 4);
+            mbar_init(&bins_full[b], 1);
+            mbar_init(&vfull[b], 1);
+            mbar_init(&vempty[b], 1);
         }
-        mbar_init(p_full, 8);
-        mbar_init(p_empty, 1);
+        mbar_init(p_full, NG * 4);
         mbar_init(q_full, 1);
         mbar_init(o_full, 1);
         fence_barrier_init();
@@ -546,7 +559,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     const uint32_t tm_s0 = tmem, tm_o = tmem + 256, tm_b = tmem + BINS_COL;
 
     if (warp == 0) {
-        // ------------------------------------------------------------ TMA
+        // ------------------------------------------------------- TMA: Q, K
         if (lane == 0 && niter > 0) {
             mbar_expect_tx(q_full, TILE_BYTES);
             tma_load_2d(sm + LY::Q_OFF, &tmQ, q_full, head * DH, i0);
@@ -556,17 +569,26 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 mbar_wait(&empty[s], ((it / LY::ST) & 1) ^ 1);
                 uint8_t* st = sm + LY::STAGE_OFF + s * LY::STAGE;
                 const int k0 = kbase + it * TK;
-                mbar_expect_tx(&full[s], (NB > 0 && bins) ? LY::STAGE : (MODE == MODE_CTX ? 2 * TILE_BYTES : TILE_BYTES));
+                mbar_expect_tx(&full[s], TILE_BYTES);
                 tma_load_2d(st, &tmK, &full[s], head * DH, k0);
                 tma_load_2d(st + BOX_BYTES, &tmK, &full[s], head * DH + 64, k0);
-                if (MODE == MODE_CTX) {
-                    tma_load_2d(st + TILE_BYTES, &tmVt, &full[s], k0, head * DH);
-                    tma_load_2d(st + TILE_BYTES + BOX_BYTES, &tmVt, &full[s], k0 + 64, head * DH);
-                    if (NB > 0 && bins) {
-                        const int zrow = (k0 / TK) * NB;
-                        tma_load_2d(st + 2 * TILE_BYTES, &tmZ, &full[s], 0, zrow);
-                        tma_load_2d(st + 2 * TILE_BYTES + LY::ZB / 2, &tmZ, &full[s], 64, zrow);
-                    }
+            }
+        }
+    } else if (warp == 3) {
+        // --------------------------------------------------- TMA: V^T, Z (CTX)
+        if (MODE == MODE_CTX && lane == 0 && niter > 0) {
+            for (int it = 0; it < niter; ++it) {
+                const int s = it & 1;
+                mbar_wait(&vempty[s], ((it >> 1) & 1) ^ 1);
+                uint8_t* st = sm + LY::VSTAGE_OFF + s * LY::VSTAGE;
+                const int k0 = kbase + it * TK;
+                mbar_expect_tx(&vfull[s], bins ? LY::VSTAGE : TILE_BYTES);
+                tma_load_2d(st, &tmVt, &vfull[s], k0, head * DH);
+                tma_load_2d(st + BOX_BYTES, &tmVt, &vfull[s], k0 + 64, head * DH);
+                if (bins) {
+                    const int zrow = (k0 / TK) * NB;
+                    tma_load_2d(st + TILE_BYTES, &tmZ, &vfull[s], 0, zrow);
+                    tma_load_2d(st + TILE_BYTES + LY::ZB / 2, &tmZ, &vfull[s], 64, zrow);
                 }
             }
         }
@@ -574,38 +596,46 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         // ------------------------------------------------------------ MMA
         if (lane == 0 && niter > 0) {
             mbar_wait(q_full, 0);
-            auto pv = [&](int j) {  // O += P_j . V_j ; BINS[j&1] = P_j . Z_j  (CTX only)
+            // CTX: O += hi_j . V_j ; BINS[j&1] = hi_j . Z_j + lo_j . Z_j, with
+            // P(j) in S[j&1]: group g's hi at columns 32g..32g+15, lo at +16
+            auto pv = [&](int j) {
                 mbar_wait(p_full, j & 1);
+                mbar_wait(&vfull[j & 1], (j >> 1) & 1);
                 fence_after();
-                const uint32_t pt = smem_u32(sm + LY::P_OFF);
-                const uint32_t stg = smem_u32(sm + LY::STAGE_OFF + (j % LY::ST) * LY::STAGE);
-                const uint32_t vt = stg + TILE_BYTES;
+                const uint32_t pb = tm_s0 + uint32_t((j & 1) * TK);
+                const uint32_t stg = smem_u32(sm + LY::VSTAGE_OFF + (j & 1) * LY::VSTAGE);
+                const uint32_t vt = stg;
 #pragma unroll
                 for (int ks = 0; ks < TK / 16; ++ks)
-                    umma(tm_o, desc_k(pt, ks), desc_k(vt, ks), IDESC, (j | ks) ? 1u : 0u);
-                if (NB > 0 && bins) {
-                    const uint32_t zt = stg + 2 * TILE_BYTES;
+                    umma_ts(tm_o, pb + uint32_t(32 * (ks >> 1) + 8 * (ks & 1)), desc_k(vt, ks), IDESC,
+                            (j | ks) ? 1u : 0u);
+                if (bins) {
+                    const uint32_t zt = stg + TILE_BYTES;
+                    const uint32_t tb = tm_b + uint32_t((j & 1) * NB);
 #pragma unroll
-                    for (int ks = 0; ks < TK / 16; ++ks)
-                        umma(tm_b + uint32_t((j & 1) * NB), desc_k(pt, ks),
-                             smem_desc(zt + uint32_t(ks >> 2) * (LY::ZB / 2) + uint32_t(ks & 3) * 32u), IDESC_B,
-                             ks ? 1u : 0u);
+                    for (int plo = 0; plo < 2; ++plo)
+#pragma unroll
+                        for (int ks = 0; ks < TK / 16; ++ks)
+                            umma_ts(tb, pb + uint32_t(32 * (ks >> 1) + 16 * plo + 8 * (ks & 1)),
+                                    smem_desc(zt + uint32_t(ks >> 2) * (LY::ZB / 2) + uint32_t(ks & 3) * 32u), IDESC_B,
+                                    (plo | ks) ? 1u : 0u);
+                    umma_commit(&bins_full[j & 1]);
                 }
-                umma_commit(p_empty);
-                umma_commit(&empty[j % LY::ST]);
+                umma_commit(&vempty[j & 1]);
             };
             const uint32_t qt = smem_u32(sm + LY::Q_OFF);
             for (int it = 0; it < niter; ++it) {
                 const int s = it % LY::ST, b = it & 1;
                 mbar_wait(&full[s], (it / LY::ST) & 1);
-                mbar_wait(&s_empty[b], ((it >> 1) & 1) ^ 1);
+                // CTX: S[b] held P(it-2), consumed by MMAs issued earlier (issue order)
+                if (MODE == MODE_STATS) mbar_wait(&s_empty[b], ((it >> 1) & 1) ^ 1);
                 fence_after();
                 const uint32_t kt = smem_u32(sm + LY::STAGE_OFF + s * LY::STAGE);
 #pragma unroll
                 for (int ks = 0; ks < DH / 16; ++ks)
                     umma(tm_s0 + uint32_t(b * TK), desc_k(qt, ks), desc_k(kt, ks), IDESC, ks ? 1u : 0u);
                 umma_commit(&s_full[b]);
-                if (MODE == MODE_STATS) umma_commit(&empty[s]);
+                umma_commit(&empty[s]);
                 if (MODE == MODE_CTX && it > 0) pv(it - 1);
             }
             if (MODE == MODE_CTX) {
@@ -616,19 +646,19 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     } else if (warp >= 4) {
         // ------------------------------------------ softmax / summary / epilogue
         const int q = warp & 3;
-        const int half = (warp - 4) >> 2;       // key half of every chunk
-        const int tid = threadIdx.x - 128;      // 0..255 over both halves
-        const int htid = tid & 127;             // within the half
-        const int r = q * 32 + lane;            // tile row == TMEM lane
+        const int kg = (warp - 4) >> 2;       // key group
+        const int tid = threadIdx.x - 128;    // 0 .. NG*128-1
+        const int gtid = tid & 127;           // within the group
+        const int r = q * 32 + lane;          // tile row == TMEM lane
         const bool rvalid = r < nrows;
         const int row = i0 + r;
         const int t = rvalid ? a.rows[row] : -1;
         const int klo = max(lo, rvalid && a.key_lo ? a.key_lo[t] : 0);
         const uint32_t lane_base = uint32_t(q * 32) << 16;
         const float scale = a.scale_log2;
-        const int c0 = half * 64;               // first key column of this half
-        float m_run = -FLT_MAX, l_run = 0.f;    // STATS
-        float m_row = 0.f, il_row = 0.f;        // CTX
+        const int c0 = kg * KW;               // first key column of this group
+        float m_run = -FLT_MAX, l_run = 0.f;  // STATS
+        float m_row = 0.f, il_row = 0.f;      // CTX: p = exp2(s*scale - m_row) * il_row
         float* part = reinterpret_cast<float*>(sm + LY::PART_OFF);
         int32_t* grp = reinterpret_cast<int32_t*>(sm + LY::GRP_OFF);
         int32_t* gsrc_s = grp + TM + 2;
@@ -644,8 +674,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const int prev = (r > 0 && rvalid) ? a.row_seg[a.rows[row - 1]] : INT32_MIN;
                 const bool start = rvalid && (r == 0 || prev != src);
                 const uint32_t bal = __ballot_sync(0xffffffffu, start);
-                if (half == 0 && lane == 0) bmask[q] = bal;
-                named_sync(1, 256);
+                if (kg == 0 && lane == 0) bmask[q] = bal;
+                named_sync(1, NG * 128);
                 if (tid == 0) {
                     int ng = 0;
                     for (int w = 0; w < 4; ++w)
@@ -653,37 +683,38 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     grp[1 + ng] = nrows;
                     grp[0] = ng;
                 }
-                named_sync(1, 256);
-                for (int g = tid; g < grp[0]; g += 256) gsrc_s[g] = a.row_seg[a.rows[i0 + grp[1 + g]]];
-                named_sync(1, 256);
+                named_sync(1, NG * 128);
+                for (int g = tid; g < grp[0]; g += NG * 128) gsrc_s[g] = a.row_seg[a.rows[i0 + grp[1 + g]]];
+                named_sync(1, NG * 128);
             }
         }
         // bins of chunk j (complete in TMEM buffer j&1): own segment zeroed,
         // rows reduced per source segment, one fp64 atomic per pair
-        float* hpart = part + half * (TM * 16);
         auto flush_bins = [&](int j) {
-          if constexpr (NB > 0) {
             const int k0 = kbase + j * TK;
             const int4 hdr = __ldg(&a.chunk_tab[2 * (k0 / TK)]);
             const int d0 = hdr.x, nseg = hdr.y;
-            constexpr int NH = NB / 2;
-            const int jb = half * NH;  // first bins column of this half
-            const int nj = min(NH, nseg - jb);
-            if (nj <= 0) return;       // (uniform across the half)
-            uint32_t bv[NH];
-            if constexpr (NH == 16) tmem_ld16(tm_b + lane_base + uint32_t((j & 1) * NB + jb), bv);
-            else tmem_ld8(tm_b + lane_base + uint32_t((j & 1) * NB + jb), bv);
-            const int own = src - d0 - jb;
+            const int jb = kg * NH;  // first bins column of this group
+            const int nj = min(NH, nseg - jb);  // (uniform across the group)
+            float* gp = part + ((j & 1) * NG + kg) * (TM * NH);
+            if (nj > 0) {
+                uint32_t bv[NH];
+                if constexpr (NH == 8) tmem_ld8(tm_b + lane_base + uint32_t((j & 1) * NB + jb), bv);
+                else tmem_ld4(tm_b + lane_base + uint32_t((j & 1) * NB + jb), bv);
+                const int own = src - d0 - jb;
 #pragma unroll
-            for (int c = 0; c < NH; ++c)
-                hpart[r * 16 + (c ^ (r & 15))] = (c == own) ? 0.f : __uint_as_float(bv[c]);
-            named_sync(2 + half, 128);
+                for (int c = 0; c < NH; ++c) gp[r * NH + (c ^ (r & (NH - 1)))] = (c == own) ? 0.f : __uint_as_float(bv[c]);
+            }
+            // every flush passes this barrier: buffer j&1 is rewritten two
+            // flushes later, after all threads left this flush's reduction
+            named_sync(2 + kg, 128);
+            if (nj <= 0) return;
             const int ng = grp[0];
-            for (int e = htid; e < ng * nj; e += 128) {
+            for (int e = gtid; e < ng * nj; e += 128) {
                 const int g = e / nj, c = e - g * nj;
                 const int rb = grp[1 + g], re = grp[2 + g];
                 float acc = 0.f;
-                for (int rr = rb; rr < re; ++rr) acc += hpart[rr * 16 + (c ^ (rr & 15))];
+                for (int rr = rb; rr < re; ++rr) acc += gp[rr * NH + (c ^ (rr & (NH - 1)))];
                 if (acc != 0.f) {
                     const int gs = gsrc_s[g];
                     const int dst = d0 + jb + c;
@@ -691,178 +722,100 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     atomicAdd(tgt, double(acc) * double(a.inv_heads));
                 }
             }
-            fence_before();
-            named_sync(2 + half, 128);
-          }
-        };
-        // fp32 bins of chunk it on the CUDA cores (NB == 0): each half scans
-        // its 64 keys in order; a flush at every destination-segment boundary
-        // (warp-uniform bits of the chunk table) stores the running sum to
-        // slot j (slot-major [32][128] per half: conflict-free).  Half 0 also
-        // stores its trailing partial to slot j1, the segment that continues
-        // into half 1; the reducer adds the two halves there.
-        auto scan_bins = [&](const int4& hdr, const int4& msk, const uint32_t (&pv)[2][32]) {
-            const int d0 = hdr.x, nseg = hdr.y;
-            const int j1 = __popc(uint32_t(msk.x)) + __popc(uint32_t(msk.y));
-            const uint32_t mw[2] = {uint32_t(half ? msk.z : msk.x), uint32_t(half ? msk.w : msk.y)};
-            float* slots = part + half * (32 * TM) + r;
-            float run = 0.f;
-            // running slot address: +TM floats per flush (slot-major)
-            uint32_t saddr = smem_u32(slots) + uint32_t(half ? j1 : 0) * (TM * 4);
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) {
-                    run += __uint_as_float(pv[c][jj]);
-                    // flush at a boundary: store, advance, restart (predicated, branch-free)
-                    asm volatile(
-                        "{\n\t.reg .pred q;\n\t"
-                        "setp.ne.b32 q, %2, 0;\n\t"
-                        "@q st.shared.f32 [%0], %1;\n\t"
-                        "@q add.u32 %0, %0, %3;\n\t"
-                        "@q mov.b32 %1, 0;\n\t}"
-                        : "+r"(saddr), "+f"(run)
-                        : "r"(mw[c] & (1u << jj)), "n"(TM * 4)
-                        : "memory");
-                }
-            if (half == 0 && j1 < 32) slots[j1 * TM] = run;
-            named_sync(1, 256);
-            const int ng = grp[0];
-            const float* p0 = part;
-            const float* p1 = part + 32 * TM;
-            for (int e = tid; e < ng * nseg; e += 256) {
-                // consecutive threads take consecutive groups (rows) of one slot:
-                // slot-major reads stay on distinct banks
-                const int jj = e / ng, g = e - jj * ng;
-                const int gs = gsrc_s[g];
-                const int dst = d0 + jj;
-                if (dst == gs) continue;  // own segment (prefill.hpp:284)
-                const int rb = grp[1 + g], re = grp[2 + g];
-                float acc = 0.f;
-                if (jj <= j1)
-                    for (int rr = rb; rr < re; ++rr) acc += p0[jj * TM + rr];
-                if (jj >= j1)
-                    for (int rr = rb; rr < re; ++rr) acc += p1[jj * TM + rr];
-                if (acc != 0.f) {
-                    double* tgt = gs < 0 ? a.qts_raw + dst : a.sts_raw + int64_t(gs) * a.S + dst;
-                    atomicAdd(tgt, double(acc) * double(a.inv_heads));
-                }
-            }
-            named_sync(1, 256);
+            // (the buffer is rewritten two chunks later, after the next flush's barrier)
         };
         for (int it = 0; it < niter; ++it) {
             const int b = it & 1;
             const int k0 = kbase + it * TK;
-            // chunk table of this chunk (scan bins): issued early, used after the softmax
-            int4 c_hdr = make_int4(0, 0, 0, 0), c_msk = make_int4(0, 0, 0, 0);
-            if (NB == 0 && bins) {
-                c_hdr = __ldg(&a.chunk_tab[2 * (k0 / TK)]);
-                c_msk = __ldg(&a.chunk_tab[2 * (k0 / TK) + 1]);
-            }
             mbar_wait(&s_full[b], (it >> 1) & 1);
             fence_after();
-            uint32_t sv[2][32];
-            tmem_ld32x2(tm_s0 + lane_base + uint32_t(b * TK + c0), sv[0], sv[1]);
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[b]);
-            const int kv0 = klo - k0 - c0, kv1 = min(hi, t + 1) - k0 - c0;  // visible keys of this half
-            const bool full_half = __all_sync(0xffffffffu, kv0 <= 0 && kv1 >= 64);
+            uint32_t sv[32];
+            tmem_ld32(tm_s0 + lane_base + uint32_t(b * TK + c0), sv);
+            if (MODE == MODE_STATS) {
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_empty[b]);
+            }
+            const int kv0 = klo - k0 - c0, kv1 = min(hi, t + 1) - k0 - c0;  // visible keys of this group
+            const bool full_grp = __all_sync(0xffffffffu, kv0 <= 0 && kv1 >= KW);
             if (MODE == MODE_STATS) {
                 float cm = -FLT_MAX;
-                if (full_half) {
+                if (full_grp) {
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
-#pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) {
-                            const float v = __uint_as_float(sv[c][jj]) * scale;
-                            sv[c][jj] = __float_as_uint(v);
-                            cm = fmaxf(cm, v);
-                        }
+                    for (int jj = 0; jj < KW; ++jj) {
+                        const float v = __uint_as_float(sv[jj]) * scale;
+                        sv[jj] = __float_as_uint(v);
+                        cm = fmaxf(cm, v);
+                    }
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
-#pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) {
-                            const bool ok = unsigned(c * 32 + jj - kv0) < unsigned(kv1 - kv0);
-                            const float v = ok ? __uint_as_float(sv[c][jj]) * scale : -FLT_MAX;
-                            sv[c][jj] = __float_as_uint(v);
-                            cm = fmaxf(cm, v);
-                        }
+                    for (int jj = 0; jj < KW; ++jj) {
+                        const bool ok = unsigned(jj - kv0) < unsigned(kv1 - kv0);
+                        const float v = ok ? __uint_as_float(sv[jj]) * scale : -FLT_MAX;
+                        sv[jj] = __float_as_uint(v);
+                        cm = fmaxf(cm, v);
+                    }
                 }
                 if (cm > -FLT_MAX) {
                     const float mn = fmaxf(m_run, cm);
                     float ps0 = 0.f, ps1 = 0.f, ps2 = 0.f, ps3 = 0.f;
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
-#pragma unroll
-                        for (int jj = 0; jj < 32; jj += 4) {
-                            ps0 += ex2(__uint_as_float(sv[c][jj]) - mn);
-                            ps1 += ex2(__uint_as_float(sv[c][jj + 1]) - mn);
-                            ps2 += ex2(__uint_as_float(sv[c][jj + 2]) - mn);
-                            ps3 += ex2(__uint_as_float(sv[c][jj + 3]) - mn);
-                        }
+                    for (int jj = 0; jj < KW; jj += 4) {
+                        ps0 += ex2(__uint_as_float(sv[jj]) - mn);
+                        ps1 += ex2(__uint_as_float(sv[jj + 1]) - mn);
+                        ps2 += ex2(__uint_as_float(sv[jj + 2]) - mn);
+                        ps3 += ex2(__uint_as_float(sv[jj + 3]) - mn);
+                    }
                     l_run = (m_run > -FLT_MAX ? l_run * ex2(m_run - mn) : 0.f) + ((ps0 + ps1) + (ps2 + ps3));
                     m_run = mn;
                 }
             } else {
-                if (full_half) {
+                // p, then P = hi + lo back into S[b] (this group's 32 columns)
+                uint32_t hv[KW / 2], lv[KW / 2];
 #pragma unroll
-                    for (int c = 0; c < 2; ++c)
-#pragma unroll
-                        for (int jj = 0; jj < 32; ++jj)
-                            sv[c][jj] = __float_as_uint(ex2(fmaf(__uint_as_float(sv[c][jj]), scale, -m_row)) * il_row);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 2; ++c)
-#pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) {
-                            const bool ok = unsigned(c * 32 + jj - kv0) < unsigned(kv1 - kv0);
-                            const float p = ex2(fmaf(__uint_as_float(sv[c][jj]), scale, -m_row)) * il_row;
-                            sv[c][jj] = __float_as_uint(ok ? p : 0.f);
-                        }
-                }
-                mbar_wait(p_empty, (it & 1) ^ 1);  // P.V and bins of chunk it-1 are done
-                uint8_t* pt = sm + LY::P_OFF;
-#pragma unroll
-                for (int c = 0; c < 2; ++c)
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        const uint32_t* v = &sv[c][g * 8];
-                        const uint4 w4 = make_uint4(pack_bf16(__uint_as_float(v[0]), __uint_as_float(v[1])),
-                                                    pack_bf16(__uint_as_float(v[2]), __uint_as_float(v[3])),
-                                                    pack_bf16(__uint_as_float(v[4]), __uint_as_float(v[5])),
-                                                    pack_bf16(__uint_as_float(v[6]), __uint_as_float(v[7])));
-                        *reinterpret_cast<uint4*>(pt + p_chunk_off(r, half * 8 + c * 4 + g)) = w4;
+                for (int i = 0; i < KW / 2; ++i) {
+                    float p0 = ex2(fmaf(__uint_as_float(sv[2 * i]), scale, -m_row)) * il_row;
+                    float p1 = ex2(fmaf(__uint_as_float(sv[2 * i + 1]), scale, -m_row)) * il_row;
+                    if (!full_grp) {
+                        p0 = unsigned(2 * i - kv0) < unsigned(kv1 - kv0) ? p0 : 0.f;
+                        p1 = unsigned(2 * i + 1 - kv0) < unsigned(kv1 - kv0) ? p1 : 0.f;
                     }
-                fence_async_smem();
+                    const uint32_t h = pack_bf16(p0, p1);
+                    hv[i] = h;
+                    lv[i] = pack_bf16(p0 - __uint_as_float(h << 16), p1 - __uint_as_float(h & 0xffff0000u));
+                }
+                const uint32_t tp = tm_s0 + lane_base + uint32_t(b * TK + c0);
+                tmem_st16(tp, hv);
+                tmem_st16(tp + 16u, lv);
+                tmem_wait_st();
+                fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full);
-                if constexpr (NB == 0) {
-                    if (bins) scan_bins(c_hdr, c_msk, sv);
-                } else {
-                    if (bins && it > 0) {
-                        fence_after();
-                        flush_bins(it - 1);
-                    }
+                if (bins && it > 0) {
+                    mbar_wait(&bins_full[(it - 1) & 1], ((it - 1) >> 1) & 1);
+                    fence_after();
+                    flush_bins(it - 1);
+                    fence_before();
                 }
             }
         }
         // ---------------------------------------------------------- outputs
         if (MODE == MODE_STATS) {
-            // combine the two key halves: half 1 publishes, half 0 merges
+            // combine the key groups: groups 1.. publish, group 0 merges in order
             float* ml = part;
-            if (half == 1) {
-                ml[2 * r] = m_run;
-                ml[2 * r + 1] = l_run;
+            if (kg > 0) {
+                ml[((kg - 1) * TM + r) * 2] = m_run;
+                ml[((kg - 1) * TM + r) * 2 + 1] = l_run;
             }
-            named_sync(1, 256);
-            if (half == 0 && rvalid) {
-                const float m1 = ml[2 * r], l1 = ml[2 * r + 1];
-                const float m = fmaxf(m_run, m1);
-                float l = 0.f;
-                if (m_run > -FLT_MAX) l += l_run * ex2(m_run - m);
-                if (m1 > -FLT_MAX) l += l1 * ex2(m1 - m);
+            named_sync(1, NG * 128);
+            if (kg == 0 && rvalid) {
+                float m = m_run;
+                for (int g = 1; g < NG; ++g) m = fmaxf(m, ml[((g - 1) * TM + r) * 2]);
+                float l = m_run > -FLT_MAX ? l_run * ex2(m_run - m) : 0.f;
+                for (int g = 1; g < NG; ++g) {
+                    const float mg = ml[((g - 1) * TM + r) * 2], lg = ml[((g - 1) * TM + r) * 2 + 1];
+                    if (mg > -FLT_MAX) l += lg * ex2(mg - m);
+                }
                 const int64_t o = (int64_t(sp) * a.n + row) * a.H + head;
                 a.m_part[o] = m;
                 a.l_part[o] = l;
@@ -871,37 +824,32 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             if (niter > 0) {
                 mbar_wait(o_full, 0);
                 fence_after();
-                if (NB > 0 && bins) flush_bins(niter - 1);
+                if (bins) flush_bins(niter - 1);
             }
-            uint32_t ov[2][32];
+            // O columns [32 kg, 32 kg + 32) of the head
+            uint32_t ov[32];
             if (niter > 0) {
-                tmem_ld32x2(tm_o + lane_base + uint32_t(c0), ov[0], ov[1]);
+                tmem_ld32(tm_o + lane_base + uint32_t(c0), ov);
             } else {
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) ov[c][e] = 0u;
+                for (int e = 0; e < 32; ++e) ov[e] = 0u;
             }
             if (rvalid) {
+                const int col = head * DH + c0;
+                if (a.nsplit == 1) {
+                    uint4* dst = reinterpret_cast<uint4*>(a.ctx + int64_t(row) * a.d + col);
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int col = head * DH + c0 + c * 32;
-                    if (a.nsplit == 1) {
-                        uint4* dst = reinterpret_cast<uint4*>(a.ctx + int64_t(row) * a.d + col);
+                    for (int g = 0; g < 4; ++g)
+                        dst[g] = make_uint4(pack_bf16(__uint_as_float(ov[g * 8 + 0]), __uint_as_float(ov[g * 8 + 1])),
+                                            pack_bf16(__uint_as_float(ov[g * 8 + 2]), __uint_as_float(ov[g * 8 + 3])),
+                                            pack_bf16(__uint_as_float(ov[g * 8 + 4]), __uint_as_float(ov[g * 8 + 5])),
+                                            pack_bf16(__uint_as_float(ov[g * 8 + 6]), __uint_as_float(ov[g * 8 + 7])));
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(a.o_part + (int64_t(sp) * a.n + row) * a.d + col);
 #pragma unroll
-                        for (int g = 0; g < 4; ++g)
-                            dst[g] = make_uint4(
-                                pack_bf16(__uint_as_float(ov[c][g * 8 + 0]), __uint_as_float(ov[c][g * 8 + 1])),
-                                pack_bf16(__uint_as_float(ov[c][g * 8 + 2]), __uint_as_float(ov[c][g * 8 + 3])),
-                                pack_bf16(__uint_as_float(ov[c][g * 8 + 4]), __uint_as_float(ov[c][g * 8 + 5])),
-                                pack_bf16(__uint_as_float(ov[c][g * 8 + 6]), __uint_as_float(ov[c][g * 8 + 7])));
-                    } else {
-                        float4* dst = reinterpret_cast<float4*>(a.o_part + (int64_t(sp) * a.n + row) * a.d + col);
-#pragma unroll
-                        for (int g = 0; g < 8; ++g)
-                            dst[g] = make_float4(__uint_as_float(ov[c][4 * g]), __uint_as_float(ov[c][4 * g + 1]),
-                                                 __uint_as_float(ov[c][4 * g + 2]), __uint_as_float(ov[c][4 * g + 3]));
-                    }
+                    for (int g = 0; g < 8; ++g)
+                        dst[g] = make_float4(__uint_as_float(ov[4 * g]), __uint_as_float(ov[4 * g + 1]),
+                                             __uint_as_float(ov[4 * g + 2]), __uint_as_float(ov[4 * g + 3]));
                 }
             }
         }
@@ -1050,10 +998,12 @@ void launch_chunk_table(const int32_t* row_seg, int T, void* tab, cudaStream_t s
     KEEP_LAUNCH_CHECK();
 }
 
+// Summary bins on the tensor core (default) or, with KEEP_BINS=scan, the
+// CUDA-core scan (A/B reference for the tensor-core path).
 bool bins_on_tensor_core() {
     static const bool v = [] {
         const char* e = std::getenv("KEEP_BINS");
-        return e && std::string(e) == "mma";
+        return !(e && std::string(e) == "scan");
     }();
     return v;
 }
@@ -1127,7 +1077,7 @@ void launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
 
     // v2 (384 threads, summary bins on the tensor core) unless the layout has
     // more than 32 segments in some 128-key chunk (then the v1 scan bins)
-    const bool v2 = !force_v1() && (!L.with_bins || L.nb > 0);
+    const bool v2 = !force_v1() && (!L.with_bins || (L.nb > 0 && bins_on_tensor_core()));
     const dim3 grid(tiles, H, a.nsplit);
     if (v2) launch_mode2<MODE_STATS, 16>(mq, mk, mv, mq, a, grid, st);
     else launch_mode<MODE_STATS>(mq, mk, mv, a, grid, st);
@@ -1138,9 +1088,7 @@ void launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
     if (v2) {
         if (L.with_bins) {
             const int nchunks = int(ceil_div(T, TK));
-            if (!bins_on_tensor_core()) {
-                launch_mode2<MODE_CTX, 0>(mq, mk, mv, mq, a, grid, st);
-            } else {
+            {
             const CUtensorMap mz = make_map_bf16(L.zt, int64_t(nchunks) * L.nb, TK, TK, L.nb);
             if (L.nb == 16) launch_mode2<MODE_CTX, 16>(mq, mk, mv, mz, a, grid, st);
             else launch_mode2<MODE_CTX, 32>(mq, mk, mv, mz, a, grid, st);

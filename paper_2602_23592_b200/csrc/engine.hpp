@@ -50,7 +50,7 @@ void launch_chunk_table(const int32_t* row_seg, int T, void* tab, cudaStream_t s
 // bins width for a layout (max segments touching a 128-key chunk, rounded to
 // 16 / 32; 0 when some chunk has more than 32) and the Z^T indicator tiles
 int summary_bins_width(const std::vector<int32_t>& row_seg);
-bool bins_on_tensor_core();  // KEEP_BINS=mma: bf16 P . Z bins (fast, bf16-precision summary)
+bool bins_on_tensor_core();  // P . Z bins with P = bf16 hi + bf16 lo (default; KEEP_BINS=scan: CUDA-core scan)
 void launch_zt_build(const int32_t* row_seg, int T, const void* tab, int nb, void* zt, cudaStream_t st);
 
 // Collectives of KV-head sharding (comm.cu).  All stream-ordered on `st`.
