@@ -26,6 +26,7 @@
 #include "tc_common.cuh"
 
 #include <cfloat>
+#include <type_traits>
 
 namespace keep_b200 {
 
@@ -510,13 +511,18 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     uint64_t* empty = bar + 4;     // [ST]
     uint64_t* s_full = bar + 8;    // [2]
     uint64_t* s_empty = bar + 10;  // [2] (STATS)
-    uint64_t* p_full = bar + 12;   // (CTX)
+    // [2] (CTX): per S buffer, so an early arrival for chunk j+1 can never
+    // complete a second phase before the MMA warp has waited for chunk j
+    uint64_t* p_full = bar + 12;
     uint64_t* q_full = bar + 14;
     uint64_t* o_full = bar + 15;
-    uint64_t* bins_full = bar + 16;  // [2]
-    uint64_t* vfull = bar + 18;      // [2] V ring (CTX)
-    uint64_t* vempty = bar + 20;     // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 22);
+    uint64_t* vfull = bar + 16;      // [2] V ring (CTX)
+    uint64_t* vempty = bar + 18;     // [2]
+    uint64_t* bins_full = bar + 20;  // [NBUF]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 24);
+    // bins of chunk j live in TMEM buffer j % NBUF and are flushed two chunks
+    // later, so the softmax never waits for the bins MMA it just enabled
+    constexpr int NBUF = 3;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = blockIdx.x * TM;
@@ -542,11 +548,12 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         for (int b = 0; b < 2; ++b) {
             mbar_init(&s_full[b], 1);
             mbar_init(&s_empty[b], NG * 4);
-            mbar_init(&bins_full[b], 1);
             mbar_init(&vfull[b], 1);
             mbar_init(&vempty[b], 1);
         }
-        mbar_init(p_full, NG * 4);
+        for (int b = 0; b < NBUF; ++b) mbar_init(&bins_full[b], 1);
+        mbar_init(&p_full[0], NG * 4);
+        mbar_init(&p_full[1], NG * 4);
         mbar_init(q_full, 1);
         mbar_init(o_full, 1);
         fence_barrier_init();
@@ -599,7 +606,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             // CTX: O += hi_j . V_j ; BINS[j&1] = hi_j . Z_j + lo_j . Z_j, with
             // P(j) in S[j&1]: group g's hi at columns 32g..32g+15, lo at +16
             auto pv = [&](int j) {
-                mbar_wait(p_full, j & 1);
+                mbar_wait(&p_full[j & 1], (j >> 1) & 1);
                 mbar_wait(&vfull[j & 1], (j >> 1) & 1);
                 fence_after();
                 const uint32_t pb = tm_s0 + uint32_t((j & 1) * TK);
@@ -611,7 +618,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             (j | ks) ? 1u : 0u);
                 if (bins) {
                     const uint32_t zt = stg + TILE_BYTES;
-                    const uint32_t tb = tm_b + uint32_t((j & 1) * NB);
+                    const uint32_t tb = tm_b + uint32_t((j % NBUF) * NB);
 #pragma unroll
                     for (int plo = 0; plo < 2; ++plo)
 #pragma unroll
@@ -619,7 +626,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             umma_ts(tb, pb + uint32_t(32 * (ks >> 1) + 16 * plo + 8 * (ks & 1)),
                                     smem_desc(zt + uint32_t(ks >> 2) * (LY::ZB / 2) + uint32_t(ks & 3) * 32u), IDESC_B,
                                     (plo | ks) ? 1u : 0u);
-                    umma_commit(&bins_full[j & 1]);
+                    umma_commit(&bins_full[j % NBUF]);
                 }
                 umma_commit(&vempty[j & 1]);
             };
@@ -664,11 +671,13 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         int32_t* gsrc_s = grp + TM + 2;
         uint32_t* bmask = reinterpret_cast<uint32_t*>(sm + LY::MSK_OFF);
         int src = -1;
+        float m_eff = 0.f;  // CTX: m_row + log2(l): p = exp2(s*scale - m_eff)
         if (MODE == MODE_CTX) {
             if (rvalid) {
                 m_row = a.m_fin[int64_t(row) * a.H + head];
                 il_row = a.inv_l[int64_t(row) * a.H + head];
                 src = a.row_seg[t];
+                m_eff = il_row > 0.f ? m_row - __log2f(il_row) : INFINITY;
             }
             if (bins) {
                 const int prev = (r > 0 && rvalid) ? a.row_seg[a.rows[row - 1]] : INT32_MIN;
@@ -688,9 +697,12 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 named_sync(1, NG * 128);
             }
         }
-        // bins of chunk j (complete in TMEM buffer j&1): own segment zeroed,
-        // rows reduced per source segment, one fp64 atomic per pair
+        // bins of chunk j (complete in TMEM buffer j % NBUF): own segment
+        // zeroed, rows reduced per source segment, one fp64 atomic per pair
+        const int ngrp = bins ? grp[0] : 0;
         auto flush_bins = [&](int j) {
+            mbar_wait(&bins_full[j % NBUF], (j / NBUF) & 1);
+            fence_after();
             const int k0 = kbase + j * TK;
             const int4 hdr = __ldg(&a.chunk_tab[2 * (k0 / TK)]);
             const int d0 = hdr.x, nseg = hdr.y;
@@ -699,8 +711,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             float* gp = part + ((j & 1) * NG + kg) * (TM * NH);
             if (nj > 0) {
                 uint32_t bv[NH];
-                if constexpr (NH == 8) tmem_ld8(tm_b + lane_base + uint32_t((j & 1) * NB + jb), bv);
-                else tmem_ld4(tm_b + lane_base + uint32_t((j & 1) * NB + jb), bv);
+                if constexpr (NH == 8) tmem_ld8(tm_b + lane_base + uint32_t((j % NBUF) * NB + jb), bv);
+                else tmem_ld4(tm_b + lane_base + uint32_t((j % NBUF) * NB + jb), bv);
                 const int own = src - d0 - jb;
 #pragma unroll
                 for (int c = 0; c < NH; ++c) gp[r * NH + (c ^ (r & (NH - 1)))] = (c == own) ? 0.f : __uint_as_float(bv[c]);
@@ -709,9 +721,10 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             // flushes later, after all threads left this flush's reduction
             named_sync(2 + kg, 128);
             if (nj <= 0) return;
-            const int ng = grp[0];
-            for (int e = gtid; e < ng * nj; e += 128) {
-                const int g = e / nj, c = e - g * nj;
+            constexpr int LNH = NH == 8 ? 3 : 2;
+            for (int e = gtid; e < (ngrp << LNH); e += 128) {
+                const int g = e >> LNH, c = e & (NH - 1);
+                if (c >= nj) continue;
                 const int rb = grp[1 + g], re = grp[2 + g];
                 float acc = 0.f;
                 for (int rr = rb; rr < re; ++rr) acc += gp[rr * NH + (c ^ (rr & (NH - 1)))];
@@ -739,62 +752,62 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             const int kv0 = klo - k0 - c0, kv1 = min(hi, t + 1) - k0 - c0;  // visible keys of this group
             const bool full_grp = __all_sync(0xffffffffu, kv0 <= 0 && kv1 >= KW);
             if (MODE == MODE_STATS) {
-                float cm = -FLT_MAX;
-                if (full_grp) {
+                // max on the raw scores (scale > 0), then exp2(s*scale - m):
+                // FMNMX + FFMA + MUFU + FADD per score.  Masked chunks take a
+                // separate instantiation so full chunks carry no predicated work.
+                auto stats = [&](auto masked) {
+                    float cmr = -INFINITY;
 #pragma unroll
                     for (int jj = 0; jj < KW; ++jj) {
-                        const float v = __uint_as_float(sv[jj]) * scale;
-                        sv[jj] = __float_as_uint(v);
-                        cm = fmaxf(cm, v);
+                        if constexpr (decltype(masked)::value)
+                            if (unsigned(jj - kv0) >= unsigned(kv1 - kv0)) sv[jj] = __float_as_uint(-INFINITY);
+                        cmr = fmaxf(cmr, __uint_as_float(sv[jj]));
                     }
-                } else {
+                    if (cmr > -INFINITY) {
+                        const float mn = fmaxf(m_run, cmr * scale);
+                        float ps0 = 0.f, ps1 = 0.f, ps2 = 0.f, ps3 = 0.f;
 #pragma unroll
-                    for (int jj = 0; jj < KW; ++jj) {
-                        const bool ok = unsigned(jj - kv0) < unsigned(kv1 - kv0);
-                        const float v = ok ? __uint_as_float(sv[jj]) * scale : -FLT_MAX;
-                        sv[jj] = __float_as_uint(v);
-                        cm = fmaxf(cm, v);
+                        for (int jj = 0; jj < KW; jj += 4) {
+                            ps0 += ex2(fmaf(__uint_as_float(sv[jj]), scale, -mn));
+                            ps1 += ex2(fmaf(__uint_as_float(sv[jj + 1]), scale, -mn));
+                            ps2 += ex2(fmaf(__uint_as_float(sv[jj + 2]), scale, -mn));
+                            ps3 += ex2(fmaf(__uint_as_float(sv[jj + 3]), scale, -mn));
+                        }
+                        l_run = (m_run > -FLT_MAX ? l_run * ex2(m_run - mn) : 0.f) + ((ps0 + ps1) + (ps2 + ps3));
+                        m_run = mn;
                     }
-                }
-                if (cm > -FLT_MAX) {
-                    const float mn = fmaxf(m_run, cm);
-                    float ps0 = 0.f, ps1 = 0.f, ps2 = 0.f, ps3 = 0.f;
-#pragma unroll
-                    for (int jj = 0; jj < KW; jj += 4) {
-                        ps0 += ex2(__uint_as_float(sv[jj]) - mn);
-                        ps1 += ex2(__uint_as_float(sv[jj + 1]) - mn);
-                        ps2 += ex2(__uint_as_float(sv[jj + 2]) - mn);
-                        ps3 += ex2(__uint_as_float(sv[jj + 3]) - mn);
-                    }
-                    l_run = (m_run > -FLT_MAX ? l_run * ex2(m_run - mn) : 0.f) + ((ps0 + ps1) + (ps2 + ps3));
-                    m_run = mn;
-                }
+                };
+                if (full_grp) stats(std::false_type{});
+                else stats(std::true_type{});
             } else {
-                // p, then P = hi + lo back into S[b] (this group's 32 columns)
+                // p = exp2(s*scale - m - log2 l), then P = hi + lo back into S[b]
+                // (this group's 32 columns); masked chunks: separate instantiation
                 uint32_t hv[KW / 2], lv[KW / 2];
+                auto make_p = [&](auto masked) {
 #pragma unroll
-                for (int i = 0; i < KW / 2; ++i) {
-                    float p0 = ex2(fmaf(__uint_as_float(sv[2 * i]), scale, -m_row)) * il_row;
-                    float p1 = ex2(fmaf(__uint_as_float(sv[2 * i + 1]), scale, -m_row)) * il_row;
-                    if (!full_grp) {
-                        p0 = unsigned(2 * i - kv0) < unsigned(kv1 - kv0) ? p0 : 0.f;
-                        p1 = unsigned(2 * i + 1 - kv0) < unsigned(kv1 - kv0) ? p1 : 0.f;
+                    for (int i = 0; i < KW / 2; ++i) {
+                        float p0 = ex2(fmaf(__uint_as_float(sv[2 * i]), scale, -m_eff));
+                        float p1 = ex2(fmaf(__uint_as_float(sv[2 * i + 1]), scale, -m_eff));
+                        if constexpr (decltype(masked)::value) {
+                            p0 = unsigned(2 * i - kv0) < unsigned(kv1 - kv0) ? p0 : 0.f;
+                            p1 = unsigned(2 * i + 1 - kv0) < unsigned(kv1 - kv0) ? p1 : 0.f;
+                        }
+                        const uint32_t h = pack_bf16(p0, p1);
+                        hv[i] = h;
+                        lv[i] = pack_bf16(p0 - __uint_as_float(h << 16), p1 - __uint_as_float(h & 0xffff0000u));
                     }
-                    const uint32_t h = pack_bf16(p0, p1);
-                    hv[i] = h;
-                    lv[i] = pack_bf16(p0 - __uint_as_float(h << 16), p1 - __uint_as_float(h & 0xffff0000u));
-                }
+                };
+                if (full_grp) make_p(std::false_type{});
+                else make_p(std::true_type{});
                 const uint32_t tp = tm_s0 + lane_base + uint32_t(b * TK + c0);
                 tmem_st16(tp, hv);
                 tmem_st16(tp + 16u, lv);
                 tmem_wait_st();
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(p_full);
-                if (bins && it > 0) {
-                    mbar_wait(&bins_full[(it - 1) & 1], ((it - 1) >> 1) & 1);
-                    fence_after();
-                    flush_bins(it - 1);
+                if (lane == 0) mbar_arrive(&p_full[b]);
+                if (bins && it >= 2) {
+                    flush_bins(it - 2);
                     fence_before();
                 }
             }
@@ -824,7 +837,10 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             if (niter > 0) {
                 mbar_wait(o_full, 0);
                 fence_after();
-                if (bins) flush_bins(niter - 1);
+                if (bins) {
+                    if (niter >= 2) flush_bins(niter - 2);
+                    flush_bins(niter - 1);
+                }
             }
             // O columns [32 kg, 32 kg + 32) of the head
             uint32_t ov[32];
@@ -1085,8 +1101,13 @@ void launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
     tc_stats_combine<<<unsigned(std::min<int64_t>(ceil_div(nh, 256), kNumSMs * 8)), 256, 0, st>>>(
         L.m_part, L.l_part, a.nsplit, nh, L.m_fin, L.inv_l);
     KEEP_LAUNCH_CHECK();
+    static const bool dbg_no_bins = [] {  // A/B timing aid: KEEP_DEBUG_NO_BINS=1 drops the summary
+        const char* e = std::getenv("KEEP_DEBUG_NO_BINS");
+        return e && *e == '1';
+    }();
+    if (v2 && dbg_no_bins) a.sts_raw = nullptr;
     if (v2) {
-        if (L.with_bins) {
+        if (L.with_bins && !dbg_no_bins) {
             const int nchunks = int(ceil_div(T, TK));
             {
             const CUtensorMap mz = make_map_bf16(L.zt, int64_t(nchunks) * L.nb, TK, TK, L.nb);
