@@ -229,7 +229,13 @@ def run_ours(args, cfg, rank, world, dist):
     layout, query = workload(cfg, args.seed)
     r = kb.ratio_schedule(L, cfg["r_avg"])
     t0 = time.perf_counter()
-    ctx = kb.Context(L, H, d, mlp, V, args.seed + rank * 0, numerics, device=dev)
+    if world > 1:
+        # KV-head sharding: one context per rank over the library's own NCCL
+        # communicator (torch.distributed only carries its unique id)
+        from paper_2602_23592_b200.dist import sharded_context
+        ctx = sharded_context(L, H, d, mlp, V, args.seed, numerics, device=dev)
+    else:
+        ctx = kb.Context(L, H, d, mlp, V, args.seed, numerics, device=dev)
     ctx.model_init()
     t_init = time.perf_counter() - t0
     t0 = time.perf_counter()
@@ -260,7 +266,8 @@ def run_ours(args, cfg, rank, world, dist):
         t = torch.tensor([total_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    value = world * tokens * args.steps / (total_ms / 1e3)
+    # one prefill per step for the whole job (heads split across the ranks)
+    value = tokens * args.steps / (total_ms / 1e3)
 
     # e2e: the C-ABI call with host buffers, host wall clock
     e2e_s = []
@@ -269,7 +276,12 @@ def run_ours(args, cfg, rank, world, dist):
         t0 = time.perf_counter()
         res = ctx.plan_keep(layout, query, r, final_hidden=False)
         e2e_s.append(time.perf_counter() - t0)
-    e2e_val = world * tokens / float(np.mean(e2e_s))
+    e2e_mean = float(np.mean(e2e_s))
+    if dist is not None:
+        t = torch.tensor([e2e_mean], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_mean = float(t.item())
+    e2e_val = tokens / e2e_mean
     h2d = 4 * (len(layout.tokens) + len(query) + layout.S + 3 * len(layout.units) + L)
     d2h = 8 * V + L * layout.S * (1 + 4) + 4 * 2 * L + 8 * 2 * L
 
@@ -296,7 +308,7 @@ def run_ours(args, cfg, rank, world, dist):
     launches = int(sum(v["kernels"] for v in prof.values())) // max(args.steps, 1)
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:
         s = cpu_sample(cfg)
         plan = steps[-1]["plan"]
         ex = cpu_extrapolate(s, cfg, steps[-1]["rows_per_layer"], attention_pairs(layout, len(query), plan))
@@ -308,14 +320,15 @@ def run_ours(args, cfg, rank, world, dist):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16" if numerics == kb.FAST else "f32-store/f64-acc", "data": "synthetic",
             "ttft_ms": float(np.median(ttft)), "ttft_ms_min": float(np.min(ttft)),
             "config": {"workload": args.config, "desc": cfg["desc"], "L": L, "H": H, "d": d, "mlp": mlp, "V": V,
                        "S": layout.S, "T": int(np.sum(layout.seg_len)) + len(query),
                        "units": {"static_groups_of_8": sum(1 for u in layout.units if u[2] == 1),
                                  "dynamic_segments": sum(1 for u in layout.units if u[2] == 0)},
-                       "r_avg": cfg["r_avg"], "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "r_avg": cfg["r_avg"],
+                       "parallelism": f"KV-head sharded x{world} (NCCL)" if world > 1 else "1 GPU",
                        "l2": "inputs larger than L2 (26.8 GB bf16 weights + 16 GB merged KV per step)",
                        "memory_kv": "HBM-resident canonical KV (static groups joint, dynamic per segment)"},
             "recomputed_tokens_per_step": tokens,
@@ -325,7 +338,7 @@ def run_ours(args, cfg, rank, world, dist):
             "phase_ms_per_step": phase_ms,
             "setup_s": {"model_init": t_init, "canonical_kv_refresh": t_mem},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ttft_ms": float(np.mean(e2e_s)) * 1e3},
+                    "ttft_ms": e2e_mean * 1e3},
             "gpu_launches": launches,
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -153,6 +153,13 @@ const char* keep_version(void);
  * residual rows after Wo + MLP.  KV blocks, views and kv_out hold the rank's
  * head columns only (row_elems = model_dim / world_size). */
 int keep_comm_unique_id(uint8_t* id_out /* 128 bytes */);
+/* The partition every rank applies (host functions, no device work):
+ * heads [h0, h0+hn) and model columns [c0, c0+cn) of `rank`; and this
+ * rank's block [r0, r0+m) of n compact rows for Wo + MLP (equal blocks of
+ * ceil(n / world) rows, the all-gather unit). */
+int keep_shard_heads(int32_t num_heads, int32_t model_dim, int32_t world_size, int32_t rank,
+                     int32_t* h0, int32_t* hn, int32_t* c0, int32_t* cn);
+int keep_shard_rows(int64_t n, int32_t world_size, int32_t rank, int64_t* r0, int64_t* m);
 int keep_loopback_create(int32_t world_size, void** group_out);
 int keep_loopback_destroy(void* group);
 

@@ -136,6 +136,8 @@ def load_library() -> C.CDLL:
         "keep_logits": (C.c_int, [vp, fp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
         "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
+        "keep_shard_heads": (C.c_int, [i32, i32, i32, i32, i32p, i32p, i32p, i32p]),
+        "keep_shard_rows": (C.c_int, [i64, i32, i32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "keep_loopback_create": (C.c_int, [i32, C.POINTER(vp)]),
         "keep_loopback_destroy": (C.c_int, [vp]),
         "keep_profile_enable": (C.c_int, [vp, i32]),
@@ -210,6 +212,20 @@ class Layout:
         if self.units:
             return [(int(u[2]), int(u[3]), int(u[0]), int(u[1])) for u in self.units]
         return [(SEGMENT, i, i, i + 1) for i in range(self.S)]
+
+
+def shard_heads(num_heads: int, model_dim: int, world: int, rank: int) -> Tuple[int, int, int, int]:
+    """(h0, hn, c0, cn): the heads and model columns a rank owns (keep_shard_heads)."""
+    v = [C.c_int32() for _ in range(4)]
+    _check(load_library().keep_shard_heads(num_heads, model_dim, world, rank, *[C.byref(x) for x in v]))
+    return tuple(int(x.value) for x in v)
+
+
+def shard_rows(n: int, world: int, rank: int) -> Tuple[int, int]:
+    """(r0, m): a rank's Wo + MLP block of n compact rows (keep_shard_rows)."""
+    r0, m = C.c_int64(), C.c_int64()
+    _check(load_library().keep_shard_rows(n, world, rank, C.byref(r0), C.byref(m)))
+    return int(r0.value), int(m.value)
 
 
 def comm_unique_id() -> bytes:

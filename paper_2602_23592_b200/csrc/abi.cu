@@ -1220,6 +1220,28 @@ int keep_importance_evaluation(void* ctx, int32_t S, const double* qts, const do
     });
 }
 
+int keep_shard_heads(int32_t H, int32_t d, int32_t G, int32_t R, int32_t* h0, int32_t* hn, int32_t* c0,
+                     int32_t* cn) {
+    return guard([&] {
+        if (G < 1 || R < 0 || R >= G || H < 1 || H % G != 0 || d % H != 0)
+            raise(KEEP_ERR_CONFIG, "bad head partition");
+        const int32_t hl = H / G, dh = d / H;
+        *h0 = R * hl;
+        *hn = hl;
+        *c0 = R * hl * dh;
+        *cn = hl * dh;
+    });
+}
+
+int keep_shard_rows(int64_t n, int32_t G, int32_t R, int64_t* r0, int64_t* m) {
+    return guard([&] {
+        if (G < 1 || R < 0 || R >= G || n < 0) raise(KEEP_ERR_CONFIG, "bad row partition");
+        const int64_t cpr = ceil_div(n, G);
+        *r0 = std::min<int64_t>(n, int64_t(R) * cpr);
+        *m = std::min<int64_t>(n, *r0 + cpr) - *r0;
+    });
+}
+
 int keep_ratio_schedule(int32_t L, double r_avg, double* r) {
     return guard([&] {  // recompute.hpp:33-70
         if (L < 1) raise(KEEP_ERR_CONFIG, "num_layers must be >= 1");
