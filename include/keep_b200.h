@@ -217,6 +217,22 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query,
 
 int keep_logits(void* ctx, const float* row, double* out);
 
+/* ---- K10 loader trace: the realised (layer, owner) load schedule of the
+ * last prefill over pinned-host owners, for the reference's timeline rules
+ * (pipeline_sim.hpp:340-428: D1 loads of layer l end before compute(l); P each
+ * workload item loaded once with its block bytes; S pre-loads only of owners
+ * whose members all left the plan).  Times in ms from the prefill start. */
+typedef struct {
+    int32_t layer;        /* the item's layer */
+    int32_t kind;         /* 0 urgent (before compute(layer)), 1 ahead (layer = at_layer + 1), 2 pre-load */
+    int32_t at_layer;     /* issued before compute(at_layer) (urgent) or behind it */
+    keep_owner owner;
+    uint64_t bytes;       /* K + V block bytes of this rank */
+    double batch_start_ms, batch_end_ms;  /* the copy batch that carried it */
+    double compute_start_ms;              /* compute(layer) start on the compute stream */
+} keep_load_record;
+int keep_loader_trace(void* ctx, keep_load_record* out, int32_t cap, int32_t* n_out);
+
 /* ---- per-phase device timing (CUDA events on the launching streams) ----- */
 enum {
     KEEP_PROF_QKV = 0,      /* gathered QKV GEMM + K/V scatter (K3)          */

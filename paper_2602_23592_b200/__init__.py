@@ -79,6 +79,14 @@ class keep_profile(C.Structure):
                 ("launches", C.c_int64 * 16), ("kernels", C.c_int64 * 16)]
 
 
+class keep_load_record(C.Structure):
+    _fields_ = [("layer", C.c_int32), ("kind", C.c_int32), ("at_layer", C.c_int32), ("owner", keep_owner),
+                ("bytes", C.c_uint64), ("batch_start_ms", C.c_double), ("batch_end_ms", C.c_double),
+                ("compute_start_ms", C.c_double)]
+
+
+LOAD_KINDS = {0: "urgent", 1: "ahead", 2: "preload"}
+
 PROFILE_PHASES = ["qkv", "attn", "wo", "mlp_in", "mlp_out", "summary", "select", "cached_kv", "compact",
                   "embed", "logits", "loader", "comm", "xchg"]
 
@@ -136,6 +144,7 @@ def load_library() -> C.CDLL:
         "keep_logits": (C.c_int, [vp, fp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
         "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
+        "keep_loader_trace": (C.c_int, [vp, C.POINTER(keep_load_record), i32, i32p]),
         "keep_shard_heads": (C.c_int, [i32, i32, i32, i32, i32p, i32p, i32p, i32p]),
         "keep_shard_rows": (C.c_int, [i64, i32, i32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "keep_loopback_create": (C.c_int, [i32, C.POINTER(vp)]),
@@ -360,6 +369,16 @@ class Context:
         v = keep_kv_view()
         _check(self.lib.keep_load_memory(self._h, keep_owner(kind, oid), layer, C.byref(v)))
         return v
+
+    def loader_trace(self) -> list:
+        """The K10 load schedule of the last prefill (keep_loader_trace)."""
+        n = C.c_int32()
+        _check(self.lib.keep_loader_trace(self._h, None, 0, C.byref(n)))
+        buf = (keep_load_record * max(n.value, 1))()
+        _check(self.lib.keep_loader_trace(self._h, buf, n.value, C.byref(n)))
+        return [{"layer": r.layer, "kind": LOAD_KINDS[r.kind], "at_layer": r.at_layer,
+                 "owner": (r.owner.kind, r.owner.id), "bytes": int(r.bytes), "start_ms": r.batch_start_ms,
+                 "end_ms": r.batch_end_ms, "compute_start_ms": r.compute_start_ms} for r in buf[: n.value]]
 
     def has_current(self, kind, oid, version) -> bool:
         out = C.c_int32()

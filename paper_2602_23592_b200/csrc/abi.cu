@@ -593,6 +593,17 @@ void run_layer(Context& c, Pass& p, int l) {
     run_layer(c, p, l, [] {});
 }
 
+// Planning estimate of one layer's device time (the K10 pre-load window):
+// recompute GEMMs at ~1.1 PFLOP/s and attention at ~0.35 PFLOP/s per GPU
+// (the measured C3 rates), the analogue of the reference's CostModel.
+double layer_estimate_ms(const Context& c, const Pass& p) {
+    const double n = p.n, d = c.d, f = c.f, dl = c.dl;
+    const double m = std::ceil(n / c.G);
+    const double gemm = 2.0 * n * 3.0 * dl * d + 2.0 * m * (d * d + 2.0 * d * f);
+    const double attn = 4.0 * dl * visible_pairs(p);
+    return (gemm / 1.1e15 + attn / 0.35e15) * 1e3;
+}
+
 // Replace the compact row set (rows only shrink): gather the residual rows.
 void set_rows(Context& c, Pass& p, const std::vector<int32_t>& rows_new, bool first) {
     cudaStream_t st = c.s_main;
@@ -683,7 +694,7 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
     std::vector<int32_t> dr, nr;
     int maxr = 0;
     for (int i = 0; i < S; ++i) {
-        if (active[i]) continue;
+        if (active[i] || loader_covers(c, i)) continue;  // host-tier owners: K10 loader
         const Payload* pl = nullptr;
         const OwnerKey& ok = c.seg_owner[i];
         if (!block_current(c, ok, l, &pl)) {
@@ -691,8 +702,6 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
             raise(KEEP_ERR_CACHE_MISS, "missing cached KV for segment " + std::to_string(i) + " (owner " +
                                            owner_str(ok) + ") layer " + std::to_string(l));
         }
-        if (pl->arena->tier != KEEP_TIER_DEVICE)
-            raise(KEEP_ERR_CACHE_MISS, "owner " + owner_str(ok) + " is host-resident: load it first");
         if (c.seg_owner_row[i] + p.seg_len[i] > pl->tokens)
             raise(KEEP_ERR_INPUT, "cached block of " + owner_str(ok) + " is shorter than its members");
         ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * c.dl * c.elem);
@@ -712,6 +721,7 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
         if (!active[i]) p.dropped[i] = 1;
     set_rows(c, p, rows_new, false);
     cudaStream_t st = c.s_main;
+    loader_before_layer(c, p, l, active);  // pinned-host owners (K10): urgent loads + D1 wait
     if (!ks.empty()) {
         double rows_copied = 0.0;
         for (int32_t r : nr) rows_copied += r;
@@ -732,6 +742,7 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
     } else {
         run_layer(c, p, l, after_summary);
     }
+    loader_after_layer(c, p, l, active, layer_estimate_ms(c, p));
     std::copy(active, active + S, p.prev.begin());
     p.layer++;
 }
@@ -785,6 +796,7 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
         p.kdst[l] = static_cast<uint8_t*>(c.kv.p) + size_t(l) * 2 * sheet;
         p.vdst[l] = static_cast<uint8_t*>(c.kv.p) + (size_t(l) * 2 + 1) * sheet;
     }
+    loader_begin(c, p);
 }
 
 // Row T-1 of the final hidden state (device pointer or nullptr if dropped).

@@ -65,6 +65,14 @@ struct Comm {
     virtual void alltoall(const void* send, void* recv, size_t bytes, cudaStream_t st) = 0;
 };
 std::unique_ptr<Comm> make_comm(const keep_config& cfg);
+
+struct Context;
+struct Pass;
+// loader.cu (K10)
+void loader_begin(Context& c, Pass& p);
+void loader_before_layer(Context& c, Pass& p, int l, const uint8_t* active);
+void loader_after_layer(Context& c, Pass& p, int l, const uint8_t* active, double est_ms);
+bool loader_covers(const Context& c, int seg);  // segment's owner is host-tier (loaded by K10)
 void set_last_error(const std::string& msg);
 
 // Per-phase CUDA-event timing (keep_profile_*).
@@ -164,6 +172,48 @@ struct Pass {
     int layer = 0;
 };
 
+// K10: layer-balanced loading of pinned-host memory KV (loader.cu).
+// Items are (layer, owner) blocks exactly as the reference's workload
+// (pipeline_sim.hpp:103-154); the schedule follows simulate_balanced
+// (261-338) online: urgent loads of a layer before its compute, loads for
+// l+1 of owners already out at l issued behind compute(l), and pre-loads of
+// owners whose members all left the plan for layers >= l+2 filling the
+// estimated compute window.  Copies are cudaMemcpyBatchAsync on a side
+// stream (copy engines, no SMs); compute(l) waits on an event (D1).
+struct Loader {
+    struct Unit {
+        OwnerKey key;
+        int b = 0, e = 0;       // member segment positions [b, e)
+        int64_t dst_row = 0;    // first merged-KV row
+        int64_t tokens = 0;     // block rows
+        const struct Payload* pl = nullptr;
+    };
+    struct Batch {
+        cudaEvent_t a = nullptr, b = nullptr;
+        int kind = 0, at_layer = 0;
+        uint64_t bytes = 0;
+    };
+    struct Rec {
+        int layer, unit, batch;
+        uint64_t bytes;
+    };
+    bool on = false;
+    int L = 0;
+    std::vector<Unit> units;
+    std::vector<uint8_t> loaded;      // [L][units]
+    std::vector<int> out_from;        // per unit: first layer all members are out (INT32_MAX: not yet)
+    std::vector<uint8_t> seg_host;    // per layout segment: owner is host-tier (loaded here)
+    std::vector<int> last_batch;      // per layer: last batch that carried one of its items (-1: none)
+    std::vector<Batch> batches;
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> comp_start;  // per layer, on the compute stream after the load wait
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t t0 = nullptr;
+    double bw_gbs = 50.0;             // H2D estimate (updated from finished batches)
+    size_t bw_seen = 0;
+    ~Loader();
+};
+
 struct Context {
     keep_config cfg{};
     int L = 0, H = 0, d = 0, dh = 0, f = 0, V = 0;
@@ -194,6 +244,7 @@ struct Context {
     DevBuf sel_order, sel_n, sel_cand;
     DevBuf logits;
     Profiler prof;
+    Loader loader;
     int gemm_ctas = kNumSMs;  // 147 while the selector overlaps the MLP
 
     void* wslot(int l, int slot) const { return w[l * 4 + slot]->p; }

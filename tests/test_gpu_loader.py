@@ -1,0 +1,99 @@
+"""K10: memory KV resident in pinned host DRAM, loaded layer by layer into the
+merged KV (loader.cu).  The prefill must be identical to the HBM-resident
+run (PARITY: bit-exact plans, walk orders, hops and hidden states), and the
+realised load schedule must satisfy the reference's timeline rules
+(pipeline_sim.hpp:340-428):
+  P   every workload item (layer l, owner with a member outside plan[l]) is
+      loaded exactly once, with its whole block (derive_workload, 103-154);
+  D1  the batch carrying an item of layer l completes before compute(l);
+  S   a pre-load (item of layer >= l+2 issued behind compute(l)) only touches
+      owners whose members all left the plan by layer l."""
+import numpy as np
+import pytest
+
+import paper_2602_23592_b200 as kb
+
+pytestmark = pytest.mark.gpu
+
+EPS_MS = 1e-3
+
+
+def problem(ko, c):
+    p = ko.make_instance(c["seed"], c["S"], c["L"], c["H"], c["d"], c["mlp"], c["V"], c["lo"], c["hi"], c["qlen"])
+    p.units = [tuple(u) for u in c["units"]]
+    return p
+
+
+def layout_of(p):
+    units = []
+    for u, (b, e, g) in enumerate(p.units):
+        if g:
+            units.append((b, e, kb.GROUP, u))
+        else:
+            units += [(i, i + 1, kb.SEGMENT, i) for i in range(b, e)]
+    return kb.Layout(p.seg_len, p.tokens, units)
+
+
+def check_schedule(trace, plan, lay, d, elem):
+    L, S = plan.shape
+    owners = lay.owners()
+    tokens = {(k, o): int(np.sum(lay.seg_len[b:e])) for k, o, b, e in owners}
+    members = {(k, o): list(range(b, e)) for k, o, b, e in owners}
+    want = {(l, own) for l in range(L) for own, ms in members.items() if any(not plan[l, m] for m in ms)}
+    got = [(r["layer"], r["owner"]) for r in trace]
+    assert len(got) == len(set(got)), "an item was loaded twice"
+    assert set(got) == want, (sorted(want - set(got))[:5], sorted(set(got) - want)[:5])  # P
+    for r in trace:
+        own = r["owner"]
+        assert r["bytes"] == 2 * tokens[own] * d * elem  # whole block, K + V
+        assert r["end_ms"] <= r["compute_start_ms"] + EPS_MS, r  # D1
+        if r["kind"] == "preload":  # S
+            assert r["layer"] >= r["at_layer"] + 2
+            assert all(not plan[r["at_layer"], m] for m in members[own]), r
+
+
+@pytest.mark.parametrize("idx", [0, 7, 21, 40, 56])
+def test_host_memory_parity(ko, golden, idx):
+    if idx >= len(golden["instances"]):
+        pytest.skip("fewer golden instances")
+    c = golden["instances"][idx]
+    p = problem(ko, c)
+    lay = layout_of(p)
+    sched = np.array(c["sched"])
+    w = ko.model_init(c["L"], c["H"], c["d"], c["mlp"], c["V"], c["seed"])
+    ref = ko.plan_keep(p, w, sched)
+    with kb.Context(c["L"], c["H"], c["d"], c["mlp"], c["V"], c["seed"]) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay, version=1, tier=kb.TIER_DEVICE)
+        dev = ctx.plan_keep(lay, p.query, sched)
+        ctx.memory_compute_layout(lay, version=2, tier=kb.TIER_HOST)
+        st0 = ctx.memory_stats()
+        host = ctx.plan_keep(lay, p.query, sched)
+        trace = ctx.loader_trace()
+        st1 = ctx.memory_stats()
+    assert np.array_equal(host["plan"], ref["plan"]) and host["orders"] == ref["orders"]
+    assert np.array_equal(host["hops"], ref["hops"])
+    assert np.array_equal(host["final_hidden"], dev["final_hidden"])  # same arithmetic, other tier
+    assert np.array_equal(host["last_logits"], dev["last_logits"])
+    check_schedule(trace, host["plan"], lay, c["d"], 4)
+    assert st1["bytes_loaded_slow"] - st0["bytes_loaded_slow"] == sum(r["bytes"] for r in trace)
+
+
+def test_host_memory_fast_tc():
+    # head_dim 128, tensor-core attention; preloads exercised by a deep plan
+    seed, S, L, H, d, mlp, V = 71, 60, 6, 2, 256, 512, 512
+    from paper_2602_23592_b200.synth import group_units, make_instance_layout
+    inst = make_instance_layout(seed, S, V)
+    lay = kb.Layout(inst.seg_len, inst.tokens, group_units(S, 4, 0.5))
+    sched = kb.ratio_schedule(L, 0.3)
+    with kb.Context(L, H, d, mlp, V, seed, kb.FAST) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay, version=1)
+        dev = ctx.plan_keep(lay, inst.query, sched)
+        ctx.memory_compute_layout(lay, version=2, tier=kb.TIER_HOST)
+        host = ctx.plan_keep(lay, inst.query, sched)
+        trace = ctx.loader_trace()
+    assert np.array_equal(host["plan"], dev["plan"])
+    assert np.max(np.abs(host["final_hidden"] - dev["final_hidden"])) <= 1e-3 * np.max(np.abs(dev["final_hidden"]))
+    check_schedule(trace, host["plan"], lay, d, 2)
+    assert len(trace) > 0
