@@ -92,6 +92,28 @@ void issue(Context& c, Pass& p, const std::vector<std::pair<int, int>>& items, i
         bt.bytes += 2 * blk;
         c.stats.bytes_loaded_slow += 2 * blk;
     }
+    // coalesce blocks that are adjacent in both the host arena and the merged
+    // KV (consecutive owners of one refresh batch): fewer, larger DMA copies
+    {
+        std::vector<size_t> ord(dsts.size());
+        for (size_t k = 0; k < ord.size(); ++k) ord[k] = k;
+        std::sort(ord.begin(), ord.end(), [&](size_t x, size_t y) { return dsts[x] < dsts[y]; });
+        std::vector<void*> d2, s2;
+        std::vector<size_t> z2;
+        for (size_t k : ord) {
+            if (!d2.empty() && static_cast<uint8_t*>(d2.back()) + z2.back() == dsts[k] &&
+                static_cast<uint8_t*>(s2.back()) + z2.back() == srcs[k]) {
+                z2.back() += sizes[k];
+                continue;
+            }
+            d2.push_back(dsts[k]);
+            s2.push_back(srcs[k]);
+            z2.push_back(sizes[k]);
+        }
+        dsts.swap(d2);
+        srcs.swap(s2);
+        sizes.swap(z2);
+    }
     bt.a = take_event(ld);
     bt.b = take_event(ld);
     KEEP_CUDA(cudaEventRecord(bt.a, c.s_copy));
