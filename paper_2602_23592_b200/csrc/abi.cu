@@ -484,7 +484,7 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
             t.chunk_tab = p.chunk_tab.p;
             t.zt = p.zt.p;
             t.nb = p.nb;
-            launch_attention_tc(t, st);
+            ps.kernels = launch_attention_tc(t, st);
         } else {
             ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, 5);
             launch_attention_fast(a, st);

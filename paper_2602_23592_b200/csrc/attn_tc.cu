@@ -497,6 +497,20 @@ static_assert(Layout2<MODE_STATS, 16>::SMEM <= 232448, "STATS v2 smem");
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
+// MN-major 128B-swizzled B operand (V as [keys x dh], dh contiguous): 64-wide
+// dh chunks 16 KB apart (LBO), 8-key row groups 1024 B apart (SBO); a K=16
+// step starts 2 row groups (2048 B) further.
+__device__ __forceinline__ uint64_t desc_mn(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t(BOX_BYTES >> 4) << 16;  // leading byte offset: next 64 dh columns
+    d |= uint64_t(1024 >> 4) << 32;       // stride byte offset: next 8 keys
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(2) << 61;
+    return d;
+}
+constexpr uint32_t IDESC_VMN = instr_desc(128, 128) | (1u << 16);  // B MN-major
+
 template <int MODE, int NB>
 __global__ void __launch_bounds__(NTHR2, 1)
 attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -590,8 +604,10 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 uint8_t* st = sm + LY::VSTAGE_OFF + s * LY::VSTAGE;
                 const int k0 = kbase + it * TK;
                 mbar_expect_tx(&vfull[s], bins ? LY::VSTAGE : TILE_BYTES);
-                tma_load_2d(st, &tmVt, &vfull[s], k0, head * DH);
-                tma_load_2d(st + BOX_BYTES, &tmVt, &vfull[s], k0 + 64, head * DH);
+                // V rows straight from the merged KV ([keys x dh] tile, dh
+                // contiguous): the MN-major B operand of P.V, no transpose
+                tma_load_2d(st, &tmVt, &vfull[s], head * DH, k0);
+                tma_load_2d(st + BOX_BYTES, &tmVt, &vfull[s], head * DH + 64, k0);
                 if (bins) {
                     const int zrow = (k0 / TK) * NB;
                     tma_load_2d(st + TILE_BYTES, &tmZ, &vfull[s], 0, zrow);
@@ -614,8 +630,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const uint32_t vt = stg;
 #pragma unroll
                 for (int ks = 0; ks < TK / 16; ++ks)
-                    umma_ts(tm_o, pb + uint32_t(32 * (ks >> 1) + 8 * (ks & 1)), desc_k(vt, ks), IDESC,
-                            (j | ks) ? 1u : 0u);
+                    umma_ts(tm_o, pb + uint32_t(32 * (ks >> 1) + 8 * (ks & 1)), desc_mn(vt + uint32_t(ks) * 2048u),
+                            IDESC_VMN, (j | ks) ? 1u : 0u);
                 if (bins) {
                     const uint32_t zt = stg + TILE_BYTES;
                     const uint32_t tb = tm_b + uint32_t((j % NBUF) * NB);
@@ -1049,21 +1065,27 @@ void launch_zt_build(const int32_t* row_seg, int T, const void* tab, int nb, voi
 }
 
 // Host driver of the two passes (see file comment).
-void launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
+int launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
     const int n = L.n, T = L.T, H = L.H, d = L.d;
-    if (n == 0) return;
+    if (n == 0) return 0;
+    int launched = 0;
     const int tiles = int(ceil_div(n, TM));
-    // V^T for the P.V operand (K-major over keys); inner extent padded to a
-    // multiple of 64 keys so TMA boxes never straddle a ragged edge
-    const int64_t ldt = ceil_div(T, 64) * 64;
-    {
+    const bool v2 = !force_v1() && (!L.with_bins || (L.nb > 0 && bins_on_tensor_core()));
+    const CUtensorMap mq = make_map_bf16(L.q, n, d, d, 128);
+    const CUtensorMap mk = make_map_bf16(L.k, T, d, d, 128);
+    CUtensorMap mv;
+    if (v2) {
+        mv = make_map_bf16(L.v, T, d, d, 128);  // V as stored: MN-major B operand
+    } else {
+        // v1: V^T for the P.V operand (K-major over keys); inner extent padded
+        // to a multiple of 64 keys so TMA boxes never straddle a ragged edge
+        const int64_t ldt = ceil_div(T, 64) * 64;
         dim3 g(unsigned(ceil_div(T, 64)), unsigned(d / 64));
         transpose_bf16<<<g, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(L.v), T, d, ldt, L.vt);
         KEEP_LAUNCH_CHECK();
+        ++launched;
+        mv = make_map_bf16(L.vt, d, ldt, ldt, 128);
     }
-    const CUtensorMap mq = make_map_bf16(L.q, n, d, d, 128);
-    const CUtensorMap mk = make_map_bf16(L.k, T, d, d, 128);
-    const CUtensorMap mv = make_map_bf16(L.vt, d, ldt, ldt, 128);
 
     TcArgs a{};
     a.n = n;
@@ -1093,14 +1115,14 @@ void launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
 
     // v2 (384 threads, summary bins on the tensor core) unless the layout has
     // more than 32 segments in some 128-key chunk (then the v1 scan bins)
-    const bool v2 = !force_v1() && (!L.with_bins || (L.nb > 0 && bins_on_tensor_core()));
     const dim3 grid(tiles, H, a.nsplit);
-    if (v2) launch_mode2<MODE_STATS, 16>(mq, mk, mv, mq, a, grid, st);
-    else launch_mode<MODE_STATS>(mq, mk, mv, a, grid, st);
+    if (v2) { launch_mode2<MODE_STATS, 16>(mq, mk, mv, mq, a, grid, st); ++launched; }
+    else { launch_mode<MODE_STATS>(mq, mk, mv, a, grid, st); ++launched; }
     const int64_t nh = int64_t(n) * H;
     tc_stats_combine<<<unsigned(std::min<int64_t>(ceil_div(nh, 256), kNumSMs * 8)), 256, 0, st>>>(
         L.m_part, L.l_part, a.nsplit, nh, L.m_fin, L.inv_l);
     KEEP_LAUNCH_CHECK();
+        ++launched;
     static const bool dbg_no_bins = [] {  // A/B timing aid: KEEP_DEBUG_NO_BINS=1 drops the summary
         const char* e = std::getenv("KEEP_DEBUG_NO_BINS");
         return e && *e == '1';
@@ -1111,26 +1133,30 @@ void launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
             const int nchunks = int(ceil_div(T, TK));
             {
             const CUtensorMap mz = make_map_bf16(L.zt, int64_t(nchunks) * L.nb, TK, TK, L.nb);
-            if (L.nb == 16) launch_mode2<MODE_CTX, 16>(mq, mk, mv, mz, a, grid, st);
-            else launch_mode2<MODE_CTX, 32>(mq, mk, mv, mz, a, grid, st);
+            if (L.nb == 16) { launch_mode2<MODE_CTX, 16>(mq, mk, mv, mz, a, grid, st); ++launched; }
+            else { launch_mode2<MODE_CTX, 32>(mq, mk, mv, mz, a, grid, st); ++launched; }
             }
         } else {
-            launch_mode2<MODE_CTX, 16>(mq, mk, mv, mq, a, grid, st);
+            { launch_mode2<MODE_CTX, 16>(mq, mk, mv, mq, a, grid, st); ++launched; }
         }
     } else {
         launch_mode<MODE_CTX>(mq, mk, mv, a, grid, st);
+        ++launched;
     }
     if (a.nsplit > 1) {
         const int64_t nd = int64_t(n) * d;
         tc_ctx_combine<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(L.o_part, a.nsplit,
                                                                                                    nd, L.ctx);
         KEEP_LAUNCH_CHECK();
+        ++launched;
     }
     if (L.with_bins) {
         dim3 g(unsigned(ceil_div(L.S, 256)), unsigned(L.S + 1));
         summary_normalize<<<g, 256, 0, st>>>(L.summ_raw, L.summ_raw + L.S, L.S, L.seg_len, L.qlen, L.summ);
         KEEP_LAUNCH_CHECK();
+        ++launched;
     }
+    return launched;
 }
 
 }  // namespace keep_b200

@@ -44,7 +44,7 @@ struct AttnTcLaunch {
     const void* zt;           // launch_zt_build output: Z^T tiles [nchunks * nb x 128] bf16
     int nb;                   // summary bins per chunk on the tensor core (16 / 32; 0 = scan bins)
 };
-void launch_attention_tc(const AttnTcLaunch& a, cudaStream_t st);
+int launch_attention_tc(const AttnTcLaunch& a, cudaStream_t st);  // returns kernels launched
 // per-128-key-chunk destination-segment table (32 B per chunk)
 void launch_chunk_table(const int32_t* row_seg, int T, void* tab, cudaStream_t st);
 // bins width for a layout (max segments touching a 128-key chunk, rounded to
