@@ -65,6 +65,7 @@ struct TcArgs {
     double* qts_raw;        // [S]      (nullptr: no summary)
     double* sts_raw;        // [S x S]
     const int4* chunk_tab;  // [ceil(T/128) x 2] per 128-key chunk: {d0, nseg, -, -}, {mask0..3}
+    int dbg;                // A/B timing aid (KEEP_DEBUG_ATTN): 1 = bins from hi only, 2 = no P.V
 };
 
 template <int MODE>
@@ -446,54 +447,60 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
 }
 
 // ===================================================================== v2 ==
-// 640 threads: warp 0 TMA, warp 1 MMA, warp 2 TMEM allocator, warp 3 idle,
-// warps 4..19 softmax in NG = 4 key groups: group g (warps 4+4g..7+4g) owns
-// keys [32g, 32g+32) of every 128-key chunk; a row lives in one TMEM lane,
-// so four warps share each SM sub-partition and hide each other's latency.
+// 608 threads: warp 0 TMA (Q, K), warp 1 MMA issuer, warp 2 TMEM allocator
+// and TMA (V, Z), warps 3..18 softmax in two TEAMS of eight warps.  Team t
+// owns the chunks it = t (mod 2) -- exactly the chunks whose scores land in
+// TMEM buffer S[t] -- so while one team waits for its scores to stream out of
+// TMEM (tcgen05.ld, ~64 B/clk/SM) the other team computes on the chunk it has
+// already read: TMEM reads, MUFU and the tensor pipe overlap across chunks.
+// Within a team, warp w serves TMEM lanes 32(w%4).. (rows) and key half
+// h = ((w-3)/4) & 1 of the chunk (64 keys).
 //
-// CTX: p = exp2(s*scale - m) / l (fp32) is split into hi = bf16(p) and
-// lo = bf16(p - hi) and written back into the TMEM columns of the S buffer
-// it came from; tcgen05.mma reads them as the A operand (TS form):
-//   O    += hi . V                (P.V, bf16 P as in flash attention)
-//   BINS  = hi . Z + lo . Z       (segment summary, 16 bits of p: the
+// CTX: p = exp2(s*scale - m - log2 l) (fp32) is split into hi = bf16(p) and
+// lo = bf16(p - hi), written back into the TMEM columns of S[t] (half h: hi
+// at 64h..64h+31, lo at 64h+32..64h+63) and read by tcgen05.mma as the A
+// operand (TS form):
+//   O    += hi . V                (P.V; V is the MN-major B operand read
+//                                  straight from the merged KV)
+//   BINS  = hi . Z + lo . Z       (segment summary with 16 bits of p: the
 //                                  precision the reference's near-tied
 //                                  selections need)
 // Z is the one-hot key -> destination-segment indicator of the chunk
-// (prefill constant, zt_build_kernel, TMA-staged with K and V^T); query keys
-// have no column (their mass is dropped, prefill.hpp:283).  The softmax warps
-// read the finished bins of the previous chunk from TMEM (double buffered),
-// zero the row's own segment (prefill.hpp:284), reduce rows per source
-// segment through shared memory and add one fp64 atomic per pair; group g
-// reduces bins columns [g*NB/4, (g+1)*NB/4).
-constexpr int NG = 4;             // softmax key groups
-constexpr int KW = TK / NG;       // keys per group per chunk
-constexpr int NTHR2 = 128 + NG * 128;
-constexpr uint32_t BINS_COL = 384;  // TMEM: S 0..255, O 256..383, bins 384..
+// (prefill constant, zt_build_kernel); query keys have no column (their mass
+// is dropped, prefill.hpp:283).  The owning team flushes a chunk's bins two of
+// its chunks later (TMEM buffer 2*(j&1) + ((j>>1)&1)): own segment zeroed
+// (prefill.hpp:284), rows reduced per source segment through shared memory,
+// one fp64 atomic per (source, destination) pair.
+constexpr int NTEAM = 2;
+constexpr int KH = TK / 2;            // keys per warp (key half)
+constexpr int NTHR2 = 96 + NTEAM * 256;
+constexpr uint32_t BINS_COL = 384;    // TMEM: S 0..255, O 256..383, bins 384..
 
-// Two TMA rings: K (STATS: 4 stages; CTX: ST) freed after Q.K^T, and (CTX)
-// V^T + Z (2 stages) freed after P.V -- so K runs ahead of the softmax
-// instead of waiting behind V for the previous P.V.
+// Two TMA rings: K (STATS 4 stages, CTX 3 or 2) freed after Q.K^T, and (CTX)
+// V + Z (2 stages) freed after P.V.
 template <int MODE, int NB>
 struct Layout2 {
     static constexpr int ST = MODE == MODE_STATS ? 4 : (NB <= 16 ? 3 : 2);  // K stages
-    static constexpr int NH = NB / NG;  // bins columns per key group
-    static constexpr uint32_t ZB = NB * 128 * 2;  // Z^T tile [NB x 128] bf16 (2 boxes of NB x 64)
-    static constexpr uint32_t STAGE = TILE_BYTES;  // K ring stage
-    static constexpr uint32_t VSTAGE = TILE_BYTES + ZB;  // V^T (+ Z) ring stage
+    static constexpr int NH = NB / 2;                 // bins columns per key half
+    static constexpr uint32_t ZB = NB * 128 * 2;      // Z^T tile [NB x 128] bf16 (2 boxes of NB x 64)
+    static constexpr uint32_t STAGE = TILE_BYTES;     // K stage
+    static constexpr uint32_t VSTAGE = TILE_BYTES + ZB;
     static constexpr uint32_t Q_OFF = 0;
     static constexpr uint32_t STAGE_OFF = TILE_BYTES;
     static constexpr uint32_t VSTAGE_OFF = STAGE_OFF + ST * STAGE;
     static constexpr uint32_t PART_OFF = VSTAGE_OFF + (MODE == MODE_CTX ? 2 * VSTAGE : 0);
-    // STATS: (m, l) of groups 1..NG-1; CTX: bins partials [2 buf][NG][128][NH]
-    static constexpr uint32_t PART_BYTES = MODE == MODE_STATS ? (NG - 1) * TM * 2 * 4 : 2 * NG * TM * NH * 4;
+    // STATS: (m, l) of the 3 other (team, half) partials; CTX: bins partials [team][half][128][NH]
+    static constexpr uint32_t PART_BYTES = MODE == MODE_STATS ? 3 * TM * 2 * 4 : NTEAM * 2 * TM * NH * 4;
     static constexpr uint32_t GRP_OFF = PART_OFF + PART_BYTES;  // CTX: groups [130] + sources [130]
     static constexpr uint32_t MSK_OFF = GRP_OFF + (2 * TM + 4) * 4;
     static constexpr uint32_t BAR_OFF = (MSK_OFF + 16 + 7) & ~7u;
     static constexpr size_t SMEM = size_t(BAR_OFF) + 256 + 1024;
     static constexpr uint32_t TMEM_COLS = MODE == MODE_CTX ? 512 : 256;
 };
-static_assert(Layout2<MODE_CTX, 32>::SMEM <= 232448, "CTX v2 smem");
+static_assert(Layout2<MODE_CTX, 32>::SMEM <= 232448, "CTX v2 smem (NB 32)");
+static_assert(Layout2<MODE_CTX, 16>::SMEM <= 232448, "CTX v2 smem (NB 16)");
 static_assert(Layout2<MODE_STATS, 16>::SMEM <= 232448, "STATS v2 smem");
+static_assert(BINS_COL + 4 * 32 <= 512, "bins buffers");
 
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -511,32 +518,29 @@ __device__ __forceinline__ uint64_t desc_mn(uint32_t saddr) {
 }
 constexpr uint32_t IDESC_VMN = instr_desc(128, 128) | (1u << 16);  // B MN-major
 
+__device__ __forceinline__ int bins_buf(int j) { return 2 * (j & 1) + ((j >> 1) & 1); }
+
 template <int MODE, int NB>
 __global__ void __launch_bounds__(NTHR2, 1)
 attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                const __grid_constant__ CUtensorMap tmVt, const __grid_constant__ CUtensorMap tmZ, TcArgs a) {
+                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmZ, TcArgs a) {
     using LY = Layout2<MODE, NB>;
     constexpr uint32_t IDESC_B = instr_desc(128, NB);
-    constexpr int NH = LY::NH;  // bins columns reduced per group
+    constexpr int NH = LY::NH;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared space
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + LY::BAR_OFF);
-    uint64_t* full = bar;          // [ST]
-    uint64_t* empty = bar + 4;     // [ST]
-    uint64_t* s_full = bar + 8;    // [2]
-    uint64_t* s_empty = bar + 10;  // [2] (STATS)
-    // [2] (CTX): per S buffer, so an early arrival for chunk j+1 can never
-    // complete a second phase before the MMA warp has waited for chunk j
-    uint64_t* p_full = bar + 12;
+    uint64_t* full = bar;            // [ST] K ring
+    uint64_t* empty = bar + 4;       // [ST]
+    uint64_t* s_full = bar + 8;      // [2] per S buffer (= per team)
+    uint64_t* s_empty = bar + 10;    // [2] (STATS)
+    uint64_t* p_full = bar + 12;     // [2] (CTX)
     uint64_t* q_full = bar + 14;
     uint64_t* o_full = bar + 15;
     uint64_t* vfull = bar + 16;      // [2] V ring (CTX)
     uint64_t* vempty = bar + 18;     // [2]
-    uint64_t* bins_full = bar + 20;  // [NBUF]
+    uint64_t* bins_full = bar + 20;  // [4]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 24);
-    // bins of chunk j live in TMEM buffer j % NBUF and are flushed two chunks
-    // later, so the softmax never waits for the bins MMA it just enabled
-    constexpr int NBUF = 3;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = blockIdx.x * TM;
@@ -553,7 +557,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     if (warp == 0 && lane == 0) {
         prefetch_map(&tmQ);
         prefetch_map(&tmK);
-        if (MODE == MODE_CTX) prefetch_map(&tmVt);
+        if (MODE == MODE_CTX) prefetch_map(&tmV);
         if (bins) prefetch_map(&tmZ);
         for (int s = 0; s < LY::ST; ++s) {
             mbar_init(&full[s], 1);
@@ -561,13 +565,12 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&s_full[b], 1);
-            mbar_init(&s_empty[b], NG * 4);
+            mbar_init(&s_empty[b], 8);
+            mbar_init(&p_full[b], 8);
             mbar_init(&vfull[b], 1);
             mbar_init(&vempty[b], 1);
         }
-        for (int b = 0; b < NBUF; ++b) mbar_init(&bins_full[b], 1);
-        mbar_init(&p_full[0], NG * 4);
-        mbar_init(&p_full[1], NG * 4);
+        for (int b = 0; b < 4; ++b) mbar_init(&bins_full[b], 1);
         mbar_init(q_full, 1);
         mbar_init(o_full, 1);
         fence_barrier_init();
@@ -595,8 +598,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 tma_load_2d(st + BOX_BYTES, &tmK, &full[s], head * DH + 64, k0);
             }
         }
-    } else if (warp == 3) {
-        // --------------------------------------------------- TMA: V^T, Z (CTX)
+    } else if (warp == 2) {
+        // ------------------------------------ TMA: V, Z (CTX; after the alloc)
         if (MODE == MODE_CTX && lane == 0 && niter > 0) {
             for (int it = 0; it < niter; ++it) {
                 const int s = it & 1;
@@ -606,8 +609,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 mbar_expect_tx(&vfull[s], bins ? LY::VSTAGE : TILE_BYTES);
                 // V rows straight from the merged KV ([keys x dh] tile, dh
                 // contiguous): the MN-major B operand of P.V, no transpose
-                tma_load_2d(st, &tmVt, &vfull[s], head * DH, k0);
-                tma_load_2d(st + BOX_BYTES, &tmVt, &vfull[s], head * DH + 64, k0);
+                tma_load_2d(st, &tmV, &vfull[s], head * DH, k0);
+                tma_load_2d(st + BOX_BYTES, &tmV, &vfull[s], head * DH + 64, k0);
                 if (bins) {
                     const int zrow = (k0 / TK) * NB;
                     tma_load_2d(st + TILE_BYTES, &tmZ, &vfull[s], 0, zrow);
@@ -619,30 +622,32 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         // ------------------------------------------------------------ MMA
         if (lane == 0 && niter > 0) {
             mbar_wait(q_full, 0);
-            // CTX: O += hi_j . V_j ; BINS[j&1] = hi_j . Z_j + lo_j . Z_j, with
-            // P(j) in S[j&1]: group g's hi at columns 32g..32g+15, lo at +16
+            // CTX: O += hi_j . V_j ; BINS[bins_buf(j)] = hi_j . Z_j + lo_j . Z_j,
+            // P(j) in S[j&1]: half h's hi at columns 64h..64h+31, lo at +32
             auto pv = [&](int j) {
                 mbar_wait(&p_full[j & 1], (j >> 1) & 1);
                 mbar_wait(&vfull[j & 1], (j >> 1) & 1);
                 fence_after();
                 const uint32_t pb = tm_s0 + uint32_t((j & 1) * TK);
-                const uint32_t stg = smem_u32(sm + LY::VSTAGE_OFF + (j & 1) * LY::VSTAGE);
-                const uint32_t vt = stg;
+                const uint32_t vt = smem_u32(sm + LY::VSTAGE_OFF + (j & 1) * LY::VSTAGE);
+                if (a.dbg != 2)
 #pragma unroll
                 for (int ks = 0; ks < TK / 16; ++ks)
-                    umma_ts(tm_o, pb + uint32_t(32 * (ks >> 1) + 8 * (ks & 1)), desc_mn(vt + uint32_t(ks) * 2048u),
+                    umma_ts(tm_o, pb + uint32_t(64 * (ks >> 2) + 8 * (ks & 3)), desc_mn(vt + uint32_t(ks) * 2048u),
                             IDESC_VMN, (j | ks) ? 1u : 0u);
                 if (bins) {
-                    const uint32_t zt = stg + TILE_BYTES;
-                    const uint32_t tb = tm_b + uint32_t((j % NBUF) * NB);
+                    const uint32_t zt = vt + TILE_BYTES;
+                    const uint32_t tb = tm_b + uint32_t(bins_buf(j) * NB);
+                    const int nplo = a.dbg == 1 ? 1 : 2;
 #pragma unroll
                     for (int plo = 0; plo < 2; ++plo)
+                        if (plo < nplo)
 #pragma unroll
                         for (int ks = 0; ks < TK / 16; ++ks)
-                            umma_ts(tb, pb + uint32_t(32 * (ks >> 1) + 16 * plo + 8 * (ks & 1)),
+                            umma_ts(tb, pb + uint32_t(64 * (ks >> 2) + 32 * plo + 8 * (ks & 3)),
                                     smem_desc(zt + uint32_t(ks >> 2) * (LY::ZB / 2) + uint32_t(ks & 3) * 32u), IDESC_B,
                                     (plo | ks) ? 1u : 0u);
-                    umma_commit(&bins_full[j % NBUF]);
+                    umma_commit(&bins_full[bins_buf(j)]);
                 }
                 umma_commit(&vempty[j & 1]);
             };
@@ -666,12 +671,13 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 umma_commit(o_full);
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp >= 3) {
         // ------------------------------------------ softmax / summary / epilogue
         const int q = warp & 3;
-        const int kg = (warp - 4) >> 2;       // key group
-        const int tid = threadIdx.x - 128;    // 0 .. NG*128-1
-        const int gtid = tid & 127;           // within the group
+        const int team = (warp - 3) >> 3;     // owns chunks it = team (mod 2) and S[team]
+        const int half = ((warp - 3) >> 2) & 1;
+        const int tid = threadIdx.x - 96;     // 0..511
+        const int htid = tid & 127;           // within (team, half)
         const int r = q * 32 + lane;          // tile row == TMEM lane
         const bool rvalid = r < nrows;
         const int row = i0 + r;
@@ -679,19 +685,18 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         const int klo = max(lo, rvalid && a.key_lo ? a.key_lo[t] : 0);
         const uint32_t lane_base = uint32_t(q * 32) << 16;
         const float scale = a.scale_log2;
-        const int c0 = kg * KW;               // first key column of this group
+        const int c0 = half * KH;             // first key column of this warp in a chunk
         float m_run = -FLT_MAX, l_run = 0.f;  // STATS
-        float m_row = 0.f, il_row = 0.f;      // CTX: p = exp2(s*scale - m_row) * il_row
         float* part = reinterpret_cast<float*>(sm + LY::PART_OFF);
         int32_t* grp = reinterpret_cast<int32_t*>(sm + LY::GRP_OFF);
         int32_t* gsrc_s = grp + TM + 2;
         uint32_t* bmask = reinterpret_cast<uint32_t*>(sm + LY::MSK_OFF);
         int src = -1;
-        float m_eff = 0.f;  // CTX: m_row + log2(l): p = exp2(s*scale - m_eff)
+        float m_eff = 0.f;  // CTX: m + log2(l): p = exp2(s*scale - m_eff)
         if (MODE == MODE_CTX) {
             if (rvalid) {
-                m_row = a.m_fin[int64_t(row) * a.H + head];
-                il_row = a.inv_l[int64_t(row) * a.H + head];
+                const float m_row = a.m_fin[int64_t(row) * a.H + head];
+                const float il_row = a.inv_l[int64_t(row) * a.H + head];
                 src = a.row_seg[t];
                 m_eff = il_row > 0.f ? m_row - __log2f(il_row) : INFINITY;
             }
@@ -699,8 +704,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const int prev = (r > 0 && rvalid) ? a.row_seg[a.rows[row - 1]] : INT32_MIN;
                 const bool start = rvalid && (r == 0 || prev != src);
                 const uint32_t bal = __ballot_sync(0xffffffffu, start);
-                if (kg == 0 && lane == 0) bmask[q] = bal;
-                named_sync(1, NG * 128);
+                if (tid < 128 && lane == 0) bmask[q] = bal;  // (warps 3..6 cover q = 3, 0, 1, 2)
+                named_sync(1, NTEAM * 256);
                 if (tid == 0) {
                     int ng = 0;
                     for (int w = 0; w < 4; ++w)
@@ -708,65 +713,67 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     grp[1 + ng] = nrows;
                     grp[0] = ng;
                 }
-                named_sync(1, NG * 128);
-                for (int g = tid; g < grp[0]; g += NG * 128) gsrc_s[g] = a.row_seg[a.rows[i0 + grp[1 + g]]];
-                named_sync(1, NG * 128);
+                named_sync(1, NTEAM * 256);
+                for (int g = tid; g < grp[0]; g += NTEAM * 256) gsrc_s[g] = a.row_seg[a.rows[i0 + grp[1 + g]]];
+                named_sync(1, NTEAM * 256);
             }
         }
-        // bins of chunk j (complete in TMEM buffer j % NBUF): own segment
-        // zeroed, rows reduced per source segment, one fp64 atomic per pair
+        // bins of chunk j (this team's, complete in TMEM buffer bins_buf(j)):
+        // own segment zeroed, rows reduced per source segment, one fp64 atomic
+        // per pair; the (team, half) group reduces bins columns [half*NH, +NH)
         const int ngrp = bins ? grp[0] : 0;
+        const int bar_id = 2 + team * 2 + half;
+        float* gp = part + (team * 2 + half) * (TM * NH);
         auto flush_bins = [&](int j) {
-            mbar_wait(&bins_full[j % NBUF], (j / NBUF) & 1);
+            mbar_wait(&bins_full[bins_buf(j)], (j >> 2) & 1);
             fence_after();
             const int k0 = kbase + j * TK;
             const int4 hdr = __ldg(&a.chunk_tab[2 * (k0 / TK)]);
             const int d0 = hdr.x, nseg = hdr.y;
-            const int jb = kg * NH;  // first bins column of this group
+            const int jb = half * NH;           // first bins column of this group
             const int nj = min(NH, nseg - jb);  // (uniform across the group)
-            float* gp = part + ((j & 1) * NG + kg) * (TM * NH);
             if (nj > 0) {
                 uint32_t bv[NH];
-                if constexpr (NH == 8) tmem_ld8(tm_b + lane_base + uint32_t((j % NBUF) * NB + jb), bv);
-                else tmem_ld4(tm_b + lane_base + uint32_t((j % NBUF) * NB + jb), bv);
+                if constexpr (NH == 16) tmem_ld16(tm_b + lane_base + uint32_t(bins_buf(j) * NB + jb), bv);
+                else tmem_ld8(tm_b + lane_base + uint32_t(bins_buf(j) * NB + jb), bv);
                 const int own = src - d0 - jb;
 #pragma unroll
                 for (int c = 0; c < NH; ++c) gp[r * NH + (c ^ (r & (NH - 1)))] = (c == own) ? 0.f : __uint_as_float(bv[c]);
             }
-            // every flush passes this barrier: buffer j&1 is rewritten two
-            // flushes later, after all threads left this flush's reduction
-            named_sync(2 + kg, 128);
-            if (nj <= 0) return;
-            constexpr int LNH = NH == 8 ? 3 : 2;
-            for (int e = gtid; e < (ngrp << LNH); e += 128) {
-                const int g = e >> LNH, c = e & (NH - 1);
-                if (c >= nj) continue;
-                const int rb = grp[1 + g], re = grp[2 + g];
-                float acc = 0.f;
-                for (int rr = rb; rr < re; ++rr) acc += gp[rr * NH + (c ^ (rr & (NH - 1)))];
-                if (acc != 0.f) {
-                    const int gs = gsrc_s[g];
-                    const int dst = d0 + jb + c;
-                    double* tgt = gs < 0 ? a.qts_raw + dst : a.sts_raw + int64_t(gs) * a.S + dst;
-                    atomicAdd(tgt, double(acc) * double(a.inv_heads));
+            fence_before();
+            named_sync(bar_id, 128);
+            if (nj > 0) {
+                constexpr int LNH = NH == 16 ? 4 : 3;
+                for (int e = htid; e < (ngrp << LNH); e += 128) {
+                    const int g = e >> LNH, c = e & (NH - 1);
+                    if (c >= nj) continue;
+                    const int rb = grp[1 + g], re = grp[2 + g];
+                    float acc = 0.f;
+                    for (int rr = rb; rr < re; ++rr) acc += gp[rr * NH + (c ^ (rr & (NH - 1)))];
+                    if (acc != 0.f) {
+                        const int gs = gsrc_s[g];
+                        const int dst = d0 + jb + c;
+                        double* tgt = gs < 0 ? a.qts_raw + dst : a.sts_raw + int64_t(gs) * a.S + dst;
+                        atomicAdd(tgt, double(acc) * double(a.inv_heads));
+                    }
                 }
             }
-            // (the buffer is rewritten two chunks later, after the next flush's barrier)
+            named_sync(bar_id, 128);  // the partials are rewritten by the next flush
         };
-        for (int it = 0; it < niter; ++it) {
-            const int b = it & 1;
+        const int b = team;
+        for (int it = team; it < niter; it += NTEAM) {
             const int k0 = kbase + it * TK;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             fence_after();
-            uint32_t sv[32];
-            tmem_ld32(tm_s0 + lane_base + uint32_t(b * TK + c0), sv);
+            uint32_t sv[2][32];
+            tmem_ld32x2(tm_s0 + lane_base + uint32_t(b * TK + c0), sv[0], sv[1]);
             if (MODE == MODE_STATS) {
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[b]);
             }
-            const int kv0 = klo - k0 - c0, kv1 = min(hi, t + 1) - k0 - c0;  // visible keys of this group
-            const bool full_grp = __all_sync(0xffffffffu, kv0 <= 0 && kv1 >= KW);
+            const int kv0 = klo - k0 - c0, kv1 = min(hi, t + 1) - k0 - c0;  // visible keys of this half
+            const bool full_half = __all_sync(0xffffffffu, kv0 <= 0 && kv1 >= KH);
             if (MODE == MODE_STATS) {
                 // max on the raw scores (scale > 0), then exp2(s*scale - m):
                 // FMNMX + FFMA + MUFU + FADD per score.  Masked chunks take a
@@ -774,74 +781,83 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 auto stats = [&](auto masked) {
                     float cmr = -INFINITY;
 #pragma unroll
-                    for (int jj = 0; jj < KW; ++jj) {
-                        if constexpr (decltype(masked)::value)
-                            if (unsigned(jj - kv0) >= unsigned(kv1 - kv0)) sv[jj] = __float_as_uint(-INFINITY);
-                        cmr = fmaxf(cmr, __uint_as_float(sv[jj]));
-                    }
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            if constexpr (decltype(masked)::value)
+                                if (unsigned(c * 32 + jj - kv0) >= unsigned(kv1 - kv0))
+                                    sv[c][jj] = __float_as_uint(-INFINITY);
+                            cmr = fmaxf(cmr, __uint_as_float(sv[c][jj]));
+                        }
                     if (cmr > -INFINITY) {
                         const float mn = fmaxf(m_run, cmr * scale);
                         float ps0 = 0.f, ps1 = 0.f, ps2 = 0.f, ps3 = 0.f;
 #pragma unroll
-                        for (int jj = 0; jj < KW; jj += 4) {
-                            ps0 += ex2(fmaf(__uint_as_float(sv[jj]), scale, -mn));
-                            ps1 += ex2(fmaf(__uint_as_float(sv[jj + 1]), scale, -mn));
-                            ps2 += ex2(fmaf(__uint_as_float(sv[jj + 2]), scale, -mn));
-                            ps3 += ex2(fmaf(__uint_as_float(sv[jj + 3]), scale, -mn));
-                        }
+                        for (int c = 0; c < 2; ++c)
+#pragma unroll
+                            for (int jj = 0; jj < 32; jj += 4) {
+                                ps0 += ex2(fmaf(__uint_as_float(sv[c][jj]), scale, -mn));
+                                ps1 += ex2(fmaf(__uint_as_float(sv[c][jj + 1]), scale, -mn));
+                                ps2 += ex2(fmaf(__uint_as_float(sv[c][jj + 2]), scale, -mn));
+                                ps3 += ex2(fmaf(__uint_as_float(sv[c][jj + 3]), scale, -mn));
+                            }
                         l_run = (m_run > -FLT_MAX ? l_run * ex2(m_run - mn) : 0.f) + ((ps0 + ps1) + (ps2 + ps3));
                         m_run = mn;
                     }
                 };
-                if (full_grp) stats(std::false_type{});
+                if (full_half) stats(std::false_type{});
                 else stats(std::true_type{});
             } else {
-                // p = exp2(s*scale - m - log2 l), then P = hi + lo back into S[b]
-                // (this group's 32 columns); masked chunks: separate instantiation
-                uint32_t hv[KW / 2], lv[KW / 2];
-                auto make_p = [&](auto masked) {
+                // p, then P = hi + lo back into S[b] (this half's 64 columns),
+                // 32 keys at a time so the split stays in registers
+                const uint32_t tp = tm_s0 + lane_base + uint32_t(b * TK + half * 64);
+                auto make_p = [&](auto masked, int c) {
+                    uint32_t hv[16], lv[16];
 #pragma unroll
-                    for (int i = 0; i < KW / 2; ++i) {
-                        float p0 = ex2(fmaf(__uint_as_float(sv[2 * i]), scale, -m_eff));
-                        float p1 = ex2(fmaf(__uint_as_float(sv[2 * i + 1]), scale, -m_eff));
+                    for (int i = 0; i < 16; ++i) {
+                        const int kk = 32 * c + 2 * i;
+                        float p0 = ex2(fmaf(__uint_as_float(sv[c][2 * i]), scale, -m_eff));
+                        float p1 = ex2(fmaf(__uint_as_float(sv[c][2 * i + 1]), scale, -m_eff));
                         if constexpr (decltype(masked)::value) {
-                            p0 = unsigned(2 * i - kv0) < unsigned(kv1 - kv0) ? p0 : 0.f;
-                            p1 = unsigned(2 * i + 1 - kv0) < unsigned(kv1 - kv0) ? p1 : 0.f;
+                            p0 = unsigned(kk - kv0) < unsigned(kv1 - kv0) ? p0 : 0.f;
+                            p1 = unsigned(kk + 1 - kv0) < unsigned(kv1 - kv0) ? p1 : 0.f;
                         }
                         const uint32_t h = pack_bf16(p0, p1);
                         hv[i] = h;
                         lv[i] = pack_bf16(p0 - __uint_as_float(h << 16), p1 - __uint_as_float(h & 0xffff0000u));
                     }
+                    tmem_st16(tp + uint32_t(16 * c), hv);
+                    tmem_st16(tp + uint32_t(32 + 16 * c), lv);
                 };
-                if (full_grp) make_p(std::false_type{});
-                else make_p(std::true_type{});
-                const uint32_t tp = tm_s0 + lane_base + uint32_t(b * TK + c0);
-                tmem_st16(tp, hv);
-                tmem_st16(tp + 16u, lv);
+                if (full_half) {
+                    make_p(std::false_type{}, 0);
+                    make_p(std::false_type{}, 1);
+                } else {
+                    make_p(std::true_type{}, 0);
+                    make_p(std::true_type{}, 1);
+                }
                 tmem_wait_st();
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&p_full[b]);
-                if (bins && it >= 2) {
-                    flush_bins(it - 2);
-                    fence_before();
-                }
+                if (bins && it >= 2) flush_bins(it - 2);
             }
         }
         // ---------------------------------------------------------- outputs
         if (MODE == MODE_STATS) {
-            // combine the key groups: groups 1.. publish, group 0 merges in order
+            // combine the 4 (team, half) partials in a fixed order
             float* ml = part;
-            if (kg > 0) {
-                ml[((kg - 1) * TM + r) * 2] = m_run;
-                ml[((kg - 1) * TM + r) * 2 + 1] = l_run;
+            const int gidx = team * 2 + half;
+            if (gidx > 0) {
+                ml[((gidx - 1) * TM + r) * 2] = m_run;
+                ml[((gidx - 1) * TM + r) * 2 + 1] = l_run;
             }
-            named_sync(1, NG * 128);
-            if (kg == 0 && rvalid) {
+            named_sync(1, NTEAM * 256);
+            if (gidx == 0 && rvalid) {
                 float m = m_run;
-                for (int g = 1; g < NG; ++g) m = fmaxf(m, ml[((g - 1) * TM + r) * 2]);
+                for (int g = 1; g < 4; ++g) m = fmaxf(m, ml[((g - 1) * TM + r) * 2]);
                 float l = m_run > -FLT_MAX ? l_run * ex2(m_run - m) : 0.f;
-                for (int g = 1; g < NG; ++g) {
+                for (int g = 1; g < 4; ++g) {
                     const float mg = ml[((g - 1) * TM + r) * 2], lg = ml[((g - 1) * TM + r) * 2 + 1];
                     if (mg > -FLT_MAX) l += lg * ex2(mg - m);
                 }
@@ -853,21 +869,21 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             if (niter > 0) {
                 mbar_wait(o_full, 0);
                 fence_after();
-                if (bins) {
-                    if (niter >= 2) flush_bins(niter - 2);
-                    flush_bins(niter - 1);
-                }
+                // this team's last chunk (its lag-2 flushes covered the rest)
+                const int last = ((niter - 1 - team) >= 0) ? niter - 1 - ((niter - 1 - team) & 1) : -1;
+                if (bins && last >= 0) flush_bins(last);
             }
-            // O columns [32 kg, 32 kg + 32) of the head
+            // O columns [32 g, 32 g + 32), g = 2 team + half
+            const int oc = 32 * (team * 2 + half);
             uint32_t ov[32];
             if (niter > 0) {
-                tmem_ld32(tm_o + lane_base + uint32_t(c0), ov);
+                tmem_ld32(tm_o + lane_base + uint32_t(oc), ov);
             } else {
 #pragma unroll
                 for (int e = 0; e < 32; ++e) ov[e] = 0u;
             }
             if (rvalid) {
-                const int col = head * DH + c0;
+                const int col = head * DH + oc;
                 if (a.nsplit == 1) {
                     uint4* dst = reinterpret_cast<uint4*>(a.ctx + int64_t(row) * a.d + col);
 #pragma unroll
@@ -1128,6 +1144,10 @@ int launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
         return e && *e == '1';
     }();
     if (v2 && dbg_no_bins) a.sts_raw = nullptr;
+    {
+        const char* e = std::getenv("KEEP_DEBUG_ATTN");
+        a.dbg = e ? std::atoi(e) : 0;
+    }
     if (v2) {
         if (L.with_bins && !dbg_no_bins) {
             const int nchunks = int(ceil_div(T, TK));
