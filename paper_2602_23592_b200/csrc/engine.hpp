@@ -192,6 +192,7 @@ struct Loader {
         cudaEvent_t a = nullptr, b = nullptr;
         int kind = 0, at_layer = 0;
         uint64_t bytes = 0;
+        bool host = false;  // carried pinned-host blocks (H2D)
     };
     struct Rec {
         int layer, unit, batch;
@@ -210,6 +211,8 @@ struct Loader {
     std::vector<cudaEvent_t> pool;
     cudaEvent_t t0 = nullptr;
     double bw_gbs = 50.0;             // H2D estimate (updated from finished batches)
+    double bw_d2d_gbs = 1000.0;       // HBM->HBM copy-engine estimate
+    bool any_host = false;
     size_t bw_seen = 0;
     ~Loader();
 };
