@@ -117,14 +117,20 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int m, int n, f
     }
 }
 
-template <int BN>
+// AR = rows of A staged per k-block.  Small-M GEMMs (the deep layers, where
+// only the query rows are recomputed) stage just AR = 32 rows: the M = 128
+// MMA reads the rest of its A window from whatever follows in shared memory
+// (those accumulator rows are never stored), so the weight stream -- the
+// whole cost at small M -- runs through a deep ring of small stages.
+template <int BN, int AR = BM>
 struct Cfg {
-    static constexpr int STAGES = BN == 256 ? 4 : 8;
-    static constexpr uint32_t A_BYTES = BM * BK * 2;
+    static constexpr uint32_t A_BYTES = AR * BK * 2;
     static constexpr uint32_t B_BYTES = BN * BK * 2;
     static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = AR < BM ? int((192u * 1024u) / STAGE_BYTES) : (BN == 256 ? 4 : 8);
     static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    // (+16 KB: the M = 128 window of the last stage's A must stay in bounds)
+    static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + (AR < BM ? BM * BK * 2 : 0) + 1024 + 256;
 };
 
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
@@ -136,14 +142,14 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
     nb = r / gm;
 }
 
-template <int BN>
+template <int BN, int AR>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-               EpiArgs epi) {
-    using CF = Cfg<BN>;
+               EpiArgs epi, int ksplit, float* __restrict__ acc_out) {
+    using CF = Cfg<BN, AR>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared space
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + CF::STAGES * CF::STAGE_BYTES + (AR < BM ? BM * BK * 2 : 0));
     uint64_t* empty = full + CF::STAGES;
     uint64_t* tfull = empty + CF::STAGES;
     uint64_t* tempty = tfull + 2;
@@ -151,7 +157,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tiles_m = int(ceil_div(M, BM)), tiles_n = int(ceil_div(N, BN));
-    const int ntiles = tiles_m * tiles_n, kblocks = K / BK;
+    // split-K (small M): work unit t = (tile, k-slice); the slices' partial
+    // sums meet in acc_out through fp32 reductions, finalised by a separate pass
+    const int ntiles = tiles_m * tiles_n * ksplit, kblocks_all = K / BK;
+    const int kper = int(ceil_div(kblocks_all, ksplit));
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -183,8 +192,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 int mb, nb;
-                tile_coords(t, tiles_m, tiles_n, mb, nb);
-                for (int kb = 0; kb < kblocks; ++kb) {
+                const int ks = t % ksplit;
+                tile_coords(t / ksplit, tiles_m, tiles_n, mb, nb);
+                const int kb0 = ks * kper, kb1 = min(kblocks_all, kb0 + kper);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * CF::STAGE_BYTES;
                     mbar_expect_tx(&full[stage], CF::STAGE_BYTES);
@@ -209,7 +220,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 mbar_wait(&tempty[acc], aphase ^ 1);  // epilogue drained this accumulator
                 fence_after();
                 const uint32_t tmem_d = tmem_base + uint32_t(acc * BN);
-                for (int kb = 0; kb < kblocks; ++kb) {
+                const int ks = t % ksplit;
+                const int kb0 = ks * kper, kb1 = min(kblocks_all, kb0 + kper);
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     fence_after();
                     const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
@@ -217,7 +230,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
                     for (int k = 0; k < BK / UMMA_K; ++k) {
                         // advance 16 bf16 = 32 bytes along K inside the swizzle atom
-                        umma(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb | k) ? 1u : 0u);
+                        umma(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb > kb0 || k) ? 1u : 0u);
                     }
                     umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
                     if (++stage == CF::STAGES) {
@@ -233,7 +246,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int it = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
             int mb, nb;
-            tile_coords(t, tiles_m, tiles_n, mb, nb);
+            tile_coords(t / ksplit, tiles_m, tiles_n, mb, nb);
             const int acc = it & 1;
             mbar_wait(&tfull[acc], (it >> 1) & 1);
             fence_after();
@@ -244,10 +257,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + ch * 32), r);
                 const int n = nb * BN + ch * 32;
                 if (m < M && n < N) {
-                    float v[32];
+                    if (ksplit > 1) {
+                        float* o = acc_out + int64_t(m) * N + n;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                    epilogue_chunk(epi, m, n, v);
+                        for (int j = 0; j < 32; ++j) atomicAdd(o + j, __uint_as_float(r[j]));
+                    } else {
+                        float v[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                        epilogue_chunk(epi, m, n, v);
+                    }
                 }
             }
             fence_before();
@@ -264,21 +283,56 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
 }
 
-template <int BN>
+// split-K finalisation: the fused epilogue over the reduced fp32 tile
+__global__ void splitk_epilogue_kernel(const float* __restrict__ acc, int M, int N, EpiArgs epi) {
+    const int chunks = N / 32;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < M * chunks; e += gridDim.x * blockDim.x) {
+        const int m = e / chunks, n = (e % chunks) * 32;
+        float v[32];
+        const float4* src = reinterpret_cast<const float4*>(acc + int64_t(m) * N + n);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float4 x = src[q];
+            v[4 * q] = x.x;
+            v[4 * q + 1] = x.y;
+            v[4 * q + 2] = x.z;
+            v[4 * q + 3] = x.w;
+        }
+        epilogue_chunk(epi, m, n, v);
+    }
+}
+
+template <int BN, int AR = BM>
 void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
-               const EpiArgs& epi, cudaStream_t st, int max_ctas = kNumSMs) {
-    using CF = Cfg<BN>;
+               const EpiArgs& epi, cudaStream_t st, int max_ctas = kNumSMs, int ksplit = 1) {
+    using CF = Cfg<BN, AR>;
+    static_assert(CF::SMEM <= 232448, "GEMM smem");
     static bool attr = false;
     if (!attr) {
-        KEEP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CF::SMEM)));
+        KEEP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(CF::SMEM)));
         attr = true;
     }
-    const CUtensorMap ta = make_map_bf16(A, M, K, lda, BM);
+    const CUtensorMap ta = make_map_bf16(A, M, K, lda, AR);
     const CUtensorMap tb = make_map_bf16(Bt, N, K, ldb, BN);
-    const int ntiles = int(ceil_div(M, BM) * ceil_div(N, BN));
+    const int ntiles = int(ceil_div(M, BM) * ceil_div(N, BN)) * ksplit;
     const int grid = std::min(ntiles, std::max(1, std::min(max_ctas, kNumSMs)));
-    gemm_tc_kernel<BN><<<grid, kThreads, CF::SMEM, st>>>(ta, tb, M, N, K, epi);
+    float* acc = nullptr;
+    if (ksplit > 1) {
+        // per-thread grow-only fp32 workspace (one context per host thread)
+        thread_local DevBuf ws;
+        ws.ensure(sizeof(float) * size_t(M) * N);
+        acc = ws.as<float>();
+        KEEP_CUDA(cudaMemsetAsync(acc, 0, sizeof(float) * size_t(M) * N, st));
+    }
+    gemm_tc_kernel<BN, AR><<<grid, kThreads, CF::SMEM, st>>>(ta, tb, M, N, K, epi, ksplit, acc);
     KEEP_LAUNCH_CHECK();
+    if (ksplit > 1) {
+        const int work = M * (N / 32);
+        splitk_epilogue_kernel<<<unsigned(std::min<int64_t>(ceil_div(work, 128), kNumSMs * 4)), 128, 0, st>>>(acc, M, N,
+                                                                                                         epi);
+        KEEP_LAUNCH_CHECK();
+    }
 }
 
 }  // namespace
@@ -287,6 +341,14 @@ void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* 
                       const EpiArgs& epi, cudaStream_t st, int max_ctas) {
     if (M == 0 || N == 0) return;
     if (K % BK != 0 || N % 32 != 0) raise(KEEP_ERR_CONFIG, "tcgen05 GEMM needs K % 64 == 0 and N % 32 == 0");
+    // a few rows (deep layers: the query): 32-row A stages and split-K so that
+    // ~4 waves of (tile, k-slice) units stream the weights through every SM
+    if (M <= 32) {
+        const int tiles = int(ceil_div(N, 64)), kb = K / BK;
+        const int ksplit = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(4 * kNumSMs, tiles), kb / 8)));
+        launch_bn<64, 32>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas, ksplit);
+        return;
+    }
     // few row blocks: narrow N tiles so enough CTAs stream the weights
     if (ceil_div(M, BM) * ceil_div(N, 256) >= kNumSMs || N % 256 != 0)
         launch_bn<256>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas);
@@ -305,6 +367,7 @@ extern "C" int keep_debug_gemm_bf16(const void* A, const void* Bt, float* Cout,
         auto b = static_cast<const __nv_bfloat16*>(Bt);
         if (force_bn == 256) keep_b200::launch_bn<256>(a, K, b, K, M, N, K, e, 0);
         else if (force_bn == 64) keep_b200::launch_bn<64>(a, K, b, K, M, N, K, e, 0);
+        else if (force_bn == 32) keep_b200::launch_bn<32, 32>(a, K, b, K, M, N, K, e, 0);
         else keep_b200::launch_gemm_bf16(a, K, b, K, M, N, K, e, 0);
         return cudaDeviceSynchronize() == cudaSuccess ? 0 : KEEP_ERR_CUDA;
     } catch (const keep_b200::KeepError& e) {

@@ -11,6 +11,8 @@ pytestmark = pytest.mark.gpu
     (128, 256, 64, 256), (128, 64, 64, 64), (1, 64, 64, 64), (300, 512, 512, 256), (300, 512, 512, 64),
     (16, 5120, 5120, 0), (1000, 15360, 5120, 0), (17, 13824, 5120, 0), (4100, 5120, 13824, 0),
     (2049, 1024, 1024, 256),
+    # small-M path (deep layers): 32-row A stages, 32-wide N tiles
+    (8, 5120, 5120, 32), (1, 32, 64, 32), (32, 13824, 5120, 32), (8, 5120, 13824, 0), (9, 15360, 5120, 0),
 ])
 def test_gemm_bf16_tcgen05(M, N, K, bn):
     import torch
