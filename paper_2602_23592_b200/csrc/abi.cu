@@ -275,8 +275,20 @@ bool use_tc_attention(const Context& c) {
     return c.fast && c.dh == 128 && !simt;
 }
 
+// Per layer: a 128-row tensor-core tile is mostly padding when only a few
+// rows are recomputed (the deep layers: the query alone); those layers take
+// the CUDA-core path when n <= KEEP_ATTN_SMALL_N (A/B knob).
+int small_n_threshold() {
+    static const int v = [] {
+        const char* e = std::getenv("KEEP_ATTN_SMALL_N");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+bool use_tc_attention(const Context& c, const Pass& p) { return use_tc_attention(c) && p.n > small_n_threshold(); }
+
 void plan_splits(Context& c, Pass& p) {
-    const bool tc = use_tc_attention(c);
+    const bool tc = use_tc_attention(c, p);
     const int tiles = int(ceil_div(p.n, tc ? 128 : 16));
     int nsplit = 1;
     if (tc && !p.block_diag) {
@@ -352,7 +364,7 @@ void ensure_layer_scratch(Context& c, Pass& p) {
         p.xrecv.ensure(es * cpr * c.G * c.dl);
         p.xrows.ensure(es * cpr * c.d);
     }
-    if (p.with_summary && !use_tc_attention(c)) p.rowbin.ensure((c.fast ? 4 : 8) * n * std::max(p.S, 1));
+    if (p.with_summary && !use_tc_attention(c, p)) p.rowbin.ensure((c.fast ? 4 : 8) * n * std::max(p.S, 1));
 }
 
 // Algorithmic attention work of a layer: sum over computed rows of visible keys.
@@ -445,7 +457,7 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
         }
         a.q = p.q.p;
         a.ctx_bf16 = p.ctxb.as<__nv_bfloat16>();
-        if (use_tc_attention(c)) {
+        if (use_tc_attention(c, p)) {
             ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, p.split_count_a > 1 ? 6 : 5);
             p.vt.ensure(2 * size_t(dl) * size_t(ceil_div(p.T, 64) * 64));
             AttnTcLaunch t{};
@@ -490,7 +502,7 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
             launch_attention_fast(a, st);
         }
     }
-    if (p.with_summary && !use_tc_attention(c)) {  // (the tensor-core path bins inside attention)
+    if (p.with_summary && !use_tc_attention(c, p)) {  // (the tensor-core path bins inside attention)
         ProfScope ps(c.prof, KEEP_PROF_SUMMARY, st, 0.0, (c.fast ? 4.0 : 8.0) * n * double(p.S) + 8.0 * p.S * double(p.S));
         // compact row range per segment (rows of a segment are contiguous)
         std::vector<int32_t> cb(p.S, 0), ce(p.S, 0);

@@ -761,10 +761,21 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             named_sync(bar_id, 128);  // the partials are rewritten by the next flush
         };
         const int b = team;
+        // a warp whose 32 rows are all padding (few-row tiles: the deep layers'
+        // query) skips the scores entirely -- its P rows only feed accumulator
+        // rows that are never stored -- and just keeps the barriers moving
+        const bool wvalid = __any_sync(0xffffffffu, rvalid);
         for (int it = team; it < niter; it += NTEAM) {
             const int k0 = kbase + it * TK;
             mbar_wait(&s_full[b], (it >> 1) & 1);
             fence_after();
+            if (!wvalid) {
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(MODE == MODE_STATS ? &s_empty[b] : &p_full[b]);
+                if (MODE == MODE_CTX && bins && it >= 2) flush_bins(it - 2);
+                continue;
+            }
             uint32_t sv[2][32];
             tmem_ld32x2(tm_s0 + lane_base + uint32_t(b * TK + c0), sv[0], sv[1]);
             if (MODE == MODE_STATS) {

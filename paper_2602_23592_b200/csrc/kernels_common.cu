@@ -259,62 +259,72 @@ template void launch_summary_reduce<float>(const float*, int, const int32_t*, co
 // positions that could be the reference's pick, and when that set is not a
 // single clear winner those positions are re-summed in the reference's order
 // and compared with the reference's rule (strict >, lowest position, > 0).
-constexpr int kSelThreads = 1024;
+constexpr int kSelThreads = 512;
+constexpr int kSelWarps = kSelThreads / 32;
+constexpr int kSelMaxS = 28 * kSelThreads;  // positions per thread <= 28 (bitmask)
 
-struct SelRed {
-    double v;
-    int i;
+// One hop's reduction in a single pass: the best lower bound (ties -> lower
+// position) and the two largest upper bounds (with the position of the
+// largest), so a unique winner is recognised without a second pass.
+struct HopRed {
+    double lo;  // best lower bound
+    int i;      // its position (-1: none)
+    double hi1; // largest upper bound
+    int hi1_i;
+    double hi2; // second largest upper bound
 };
 
-__device__ __forceinline__ SelRed sel_better(SelRed a, SelRed b) {
-    // larger value wins; equal values -> lower index
-    if (b.i < 0) return a;
-    if (a.i < 0) return b;
-    if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
-    return a;
+__device__ __forceinline__ HopRed hop_combine(HopRed a, HopRed b) {
+    HopRed r;
+    // best lower bound: larger wins, equal -> lower position
+    if (b.i >= 0 && (a.i < 0 || b.lo > a.lo || (b.lo == a.lo && b.i < a.i))) {
+        r.lo = b.lo;
+        r.i = b.i;
+    } else {
+        r.lo = a.lo;
+        r.i = a.i;
+    }
+    // top-2 upper bounds
+    if (b.hi1 > a.hi1 || (b.hi1 == a.hi1 && b.hi1_i >= 0 && (a.hi1_i < 0 || b.hi1_i < a.hi1_i))) {
+        r.hi1 = b.hi1;
+        r.hi1_i = b.hi1_i;
+        r.hi2 = fmax(a.hi1, b.hi2);
+    } else {
+        r.hi1 = a.hi1;
+        r.hi1_i = a.hi1_i;
+        r.hi2 = fmax(b.hi1, a.hi2);
+    }
+    return r;
 }
 
-__device__ SelRed block_argmax(SelRed x, SelRed* scratch) {
-    for (int o = 16; o > 0; o >>= 1) {
-        SelRed y{__shfl_xor_sync(0xffffffffu, x.v, o), __shfl_xor_sync(0xffffffffu, x.i, o)};
-        x = sel_better(x, y);
-    }
+__device__ __forceinline__ HopRed hop_shfl(HopRed x, int o) {
+    HopRed y;
+    y.lo = __shfl_xor_sync(0xffffffffu, x.lo, o);
+    y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+    y.hi1 = __shfl_xor_sync(0xffffffffu, x.hi1, o);
+    y.hi1_i = __shfl_xor_sync(0xffffffffu, x.hi1_i, o);
+    y.hi2 = __shfl_xor_sync(0xffffffffu, x.hi2, o);
+    return y;
+}
+
+__device__ HopRed block_hop_reduce(HopRed x, HopRed* scratch) {
+    for (int o = 16; o > 0; o >>= 1) x = hop_combine(x, hop_shfl(x, o));
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
     if (l == 0) scratch[w] = x;
     __syncthreads();
     if (w == 0) {
-        x = (l < int(blockDim.x >> 5)) ? scratch[l] : SelRed{0.0, -1};
-        for (int o = 16; o > 0; o >>= 1) {
-            SelRed y{__shfl_xor_sync(0xffffffffu, x.v, o), __shfl_xor_sync(0xffffffffu, x.i, o)};
-            x = sel_better(x, y);
-        }
-        if (l == 0) scratch[32] = x;
+        x = l < kSelWarps ? scratch[l] : HopRed{0.0, -1, -INFINITY, -1, -INFINITY};
+        for (int o = 16; o > 0; o >>= 1) x = hop_combine(x, hop_shfl(x, o));
+        if (l == 0) scratch[kSelWarps] = x;
     }
     __syncthreads();
-    return scratch[32];
+    return scratch[kSelWarps];
 }
 
-__device__ int block_sum_int(int x, int* scratch) {
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    __syncthreads();
-    if (l == 0) scratch[w] = x;
-    __syncthreads();
-    if (w == 0) {
-        x = (l < int(blockDim.x >> 5)) ? scratch[l] : 0;
-        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (l == 0) scratch[32] = x;
-    }
-    __syncthreads();
-    return scratch[32];
-}
-
-// State per position lives in shared memory (colsum fp64, colabs fp32
-// upper bound, ascending relevant list); the allowed set is a per-thread
-// bitmask (position tid + k*1024 -> bit k).
-constexpr int kSelMaxS = 14 * kSelThreads;
-
+// State per position in shared memory: the incremental column sum over the
+// relevant set (fp64), an fp32 upper bound of its absolute terms (the error
+// radius of the sum), and a membership flag; the candidate mask of a thread's
+// positions (tid + k * 512) is a register bitmask.
 __global__ void __launch_bounds__(kSelThreads, 1)
 select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ sts, int64_t budget,
               const uint8_t* __restrict__ cand, int32_t* __restrict__ order, int32_t* n_out,
@@ -322,10 +332,8 @@ select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ 
     extern __shared__ __align__(16) uint8_t sraw[];
     double* colsum = reinterpret_cast<double*>(sraw);               // [S]
     float* colabs = reinterpret_cast<float*>(colsum + S);           // [S]
-    int32_t* sorted_r = reinterpret_cast<int32_t*>(colabs + S);     // [S] ascending relevant set
-    __shared__ SelRed red[33];
-    __shared__ int ired[33];
-    __shared__ int s_win;
+    uint8_t* member = reinterpret_cast<uint8_t*>(colabs + S);       // [S] in the relevant set
+    __shared__ HopRed red[kSelWarps + 1];
 
     const int items = int(ceil_div(S, kSelThreads));
     uint32_t allowed = 0;
@@ -335,13 +343,14 @@ select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ 
         if (i < S) {
             colsum[i] = 0.0;
             colabs[i] = 0.f;
+            member[i] = 0;
         }
     }
     __syncthreads();
     const double u = 0x1.0p-53;
     int n = 0, hop = 0;
-    // score and error radius of position i (scores of the reference: qts
-    // before the first pick, mean over the relevant set afterwards)
+    // score of position i and the radius within which the reference's
+    // ascending re-sum can differ from the incremental one
     auto score_of = [&](int i, double& sc, double& err) {
         if (n == 0) {
             sc = qts[i];
@@ -353,74 +362,54 @@ select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ 
         }
     };
     while (int64_t(n) < budget && hop < S) {
-        SelRed best{0.0, -1};
+        HopRed x{0.0, -1, -INFINITY, -1, -INFINITY};
         for (int k = 0; k < items; ++k) {
             if (!(allowed >> k & 1u)) continue;
             const int i = threadIdx.x + k * kSelThreads;
             double sc, err;
             score_of(i, sc, err);
-            // lower bound of the reference score; only positions that can be > 0
-            if (sc + err > 0.0) best = sel_better(best, SelRed{sc - err, i});
+            const double up = sc + err;
+            if (!(up > 0.0)) continue;  // can never be a strictly positive pick
+            x = hop_combine(x, HopRed{sc - err, i, up, i, -INFINITY});
         }
-        const SelRed lo = block_argmax(best, red);
+        const HopRed r = block_hop_reduce(x, red);
         ++hop;
-        if (lo.i < 0) break;  // nothing can be strictly positive: stalled hop
-        // possible winners: upper bound reaches the best lower bound
-        int mine = 0, first = INT32_MAX;
-        for (int k = 0; k < items; ++k) {
-            if (!(allowed >> k & 1u)) continue;
-            const int i = threadIdx.x + k * kSelThreads;
-            double sc, err;
-            score_of(i, sc, err);
-            if (sc + err > 0.0 && sc + err >= lo.v) {
-                ++mine;
-                first = min(first, i);
-            }
-        }
-        const int cnt = block_sum_int(mine, ired);
-        if (cnt == 1 && lo.v > 0.0) {
-            if (mine) s_win = first;
+        if (r.i < 0) break;  // nothing can be strictly positive: stalled hop (recompute.hpp:124)
+        // unique winner: its lower bound beats every other position's upper bound
+        const double other_hi = r.hi1_i == r.i ? r.hi2 : r.hi1;
+        int win;
+        if (r.lo > 0.0 && r.lo > other_hi) {
+            win = r.i;
         } else {
-            // exact arbitration: the reference's ascending-position sums
-            SelRed ex{0.0, -1};
+            // exact arbitration among the positions that could win: the
+            // reference's ascending-position re-sum and its rule (strict >,
+            // lowest position, > 0)
+            HopRed ex{0.0, -1, -INFINITY, -1, -INFINITY};
             for (int k = 0; k < items; ++k) {
                 if (!(allowed >> k & 1u)) continue;
                 const int i = threadIdx.x + k * kSelThreads;
                 double sc, err;
                 score_of(i, sc, err);
-                if (!(sc + err > 0.0 && sc + err >= lo.v)) continue;
+                if (!(sc + err > 0.0 && sc + err >= r.lo)) continue;
                 double v;
                 if (n == 0) {
                     v = qts[i];
                 } else {
                     double acc = 0.0;
-                    for (int m = 0; m < n; ++m) acc += sts[int64_t(sorted_r[m]) * S + i];
+                    for (int m = 0; m < S; ++m)
+                        if (member[m]) acc += sts[int64_t(m) * S + i];
                     v = acc / double(n);
                 }
-                if (v > 0.0) ex = sel_better(ex, SelRed{v, i});
+                if (v > 0.0) ex = hop_combine(ex, HopRed{v, i, -INFINITY, -1, -INFINITY});
             }
-            const SelRed w = block_argmax(ex, red);
-            if (threadIdx.x == 0) s_win = w.i;
+            const HopRed w = block_hop_reduce(ex, red);
+            win = w.i;
         }
-        __syncthreads();
-        const int win = s_win;
-        __syncthreads();
-        if (win < 0) break;  // the stalled hop still counts (recompute.hpp:124)
-        if (threadIdx.x == 0) order[n] = win;
-        // insert into the ascending list: count smaller entries, shift the tail
-        int cntlt = 0;
-        for (int m = threadIdx.x; m < n; m += kSelThreads) cntlt += sorted_r[m] < win;
-        const int pos = block_sum_int(cntlt, ired);
-        const int tail = n - pos;
-        for (int c = int(ceil_div(tail, kSelThreads)) - 1; c >= 0; --c) {
-            const int off = c * kSelThreads + int(threadIdx.x);
-            const bool ok = off < tail;
-            const int v = ok ? sorted_r[pos + off] : 0;
-            __syncthreads();
-            if (ok) sorted_r[pos + off + 1] = v;
-            __syncthreads();
+        if (win < 0) break;  // the stalled hop still counts
+        if (threadIdx.x == 0) {
+            order[n] = win;
+            member[win] = 1;
         }
-        if (threadIdx.x == 0) sorted_r[pos] = win;
         ++n;
         // fold the new member's row into the column sums (insertion order)
         const double* row = sts + int64_t(win) * S;
@@ -444,7 +433,7 @@ void launch_select(int S, const double* qts, const double* sts, int64_t budget,
                    const uint8_t* candidates, int32_t* order, int32_t* n_out, int32_t* hops_out,
                    cudaStream_t st) {
     if (S > kSelMaxS) raise(KEEP_ERR_CONFIG, "selector supports at most 14336 segments");
-    const size_t smem = size_t(std::max(S, 1)) * (8 + 4 + 4) + 16;
+    const size_t smem = size_t(std::max(S, 1)) * (8 + 4 + 1) + 16;
     if (smem > 48 * 1024)
         KEEP_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     select_kernel<<<1, kSelThreads, smem, st>>>(S, qts, sts, budget, candidates, order, n_out, hops_out);
