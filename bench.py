@@ -272,20 +272,44 @@ def run_ours(args, cfg, rank, world, dist):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # --updates F: before every query a fraction F of the dynamic owners was
+    # updated and must be refreshed (harness.hpp:609-628; "frequent dynamic
+    # updates", test_harness.cpp:266-268); the refresh is part of the TTFT
+    dyn = [i for i, o in enumerate(layout.owners()) if o[0] == kb.SEGMENT]
+    upd_rng = np.random.default_rng(args.seed + 1)
+    version = [1]
+
+    def step():
+        if args.updates > 0:
+            version[0] += 1
+            pick = [u for u in dyn if upd_rng.random() < args.updates]
+            ctx.memory_refresh(layout, pick, version[0], tier=kb.TIER_HOST if host_mem else kb.TIER_DEVICE)
+            # (owners not picked stay current at their old version)
+            step.refreshed_tokens = float(sum(int(np.sum(layout.seg_len[layout.owners()[u][2]:layout.owners()[u][3]]))
+                                              for u in pick))
+        return ctx.plan_keep(layout, query, r, final_hidden=False)
+
+    step.refreshed_tokens = 0.0
     for _ in range(args.warmup):
-        ctx.plan_keep(layout, query, r, final_hidden=False)
+        step()
     ctx.profile_read(reset=True)
     ctx.profile_enable(True)
     barrier()
     steps = []
+    refreshed = []
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
-            steps.append(ctx.plan_keep(layout, query, r, final_hidden=False))
+            steps.append(step())
+            refreshed.append(step.refreshed_tokens)
     barrier()
     ctx.profile_enable(False)
     prof = ctx.profile_read(reset=True)
     ttft = np.array([s["ttft_ms"] for s in steps])
-    tokens = float(np.sum(steps[-1]["rows_per_layer"]))
+    refresh_ms = prof["refresh"]["ms"]  # device time of the in-TTFT refreshes (0 without --updates)
+    if args.updates > 0:
+        ttft = ttft + refresh_ms / max(args.steps, 1)
+    # recomputed tokens: the plan's rows per layer, plus every layer of the refreshed owners
+    tokens = float(np.sum(steps[-1]["rows_per_layer"])) + float(np.mean(refreshed)) * L
     total_ms = float(np.sum(ttft))
     if dist is not None:
         t = torch.tensor([total_ms], device="cuda")
@@ -299,7 +323,7 @@ def run_ours(args, cfg, rank, world, dist):
     for _ in range(max(1, args.steps)):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = ctx.plan_keep(layout, query, r, final_hidden=False)
+        res = step()
         e2e_s.append(time.perf_counter() - t0)
     e2e_mean = float(np.mean(e2e_s))
     if dist is not None:
@@ -373,6 +397,8 @@ def run_ours(args, cfg, rank, world, dist):
                        "memory_kv": ("pinned-host canonical KV, layer-balanced K10 loader" if host_mem else
                                      "HBM-resident canonical KV (static groups joint, dynamic per segment)")},
             "recomputed_tokens_per_step": tokens,
+            "updates": ({"fraction_of_dynamic_owners": args.updates, "refreshed_tokens_per_step": float(np.mean(refreshed)),
+                         "refresh_ms_per_step": refresh_ms / max(args.steps, 1)} if args.updates > 0 else None),
             "plan_segments_per_layer": [int(x) for x in plan.sum(1)],
             "rows_per_layer": [int(x) for x in steps[-1]["rows_per_layer"]],
             "hops_per_layer": [int(x) for x in steps[-1]["hops"]],
@@ -402,6 +428,8 @@ def main():
     ap.add_argument("--r-avg", type=float, default=None)
     ap.add_argument("--seed", type=int, default=20250807)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--updates", type=float, default=0.0,
+                    help="fraction of dynamic owners updated (refreshed inside the TTFT) before every query")
     ap.add_argument("--memory", choices=["hbm", "host"], default="hbm",
                     help="memory KV resident in HBM (C2-C4) or pinned host DRAM with the K10 loader (C5-style)")
     args = ap.parse_args()

@@ -88,7 +88,7 @@ class keep_load_record(C.Structure):
 LOAD_KINDS = {0: "urgent", 1: "ahead", 2: "preload"}
 
 PROFILE_PHASES = ["qkv", "attn", "wo", "mlp_in", "mlp_out", "summary", "select", "cached_kv", "compact",
-                  "embed", "logits", "loader", "comm", "xchg"]
+                  "embed", "logits", "loader", "comm", "xchg", "refresh"]
 
 
 class keep_plan_result(C.Structure):
@@ -364,6 +364,21 @@ class Context:
             members.append([int(x) for x in layout.seg_len[b:e]])
             toks.append(np.asarray(layout.tokens[starts[b]:starts[e]]))
         self.memory_compute_batch(owners, [version] * len(owners), members, np.concatenate(toks), tier)
+
+    def memory_refresh(self, layout: Layout, owner_idx, version, tier=TIER_DEVICE):
+        """compute_and_put for a subset of a layout's owners (indices into
+        layout.owners()): the canonical-KV refresh of updated memory
+        (harness.hpp:609-628), in place when the blocks already exist."""
+        starts = np.concatenate([[0], np.cumsum(layout.seg_len)]).astype(np.int64)
+        allo = layout.owners()
+        owners, members, toks = [], [], []
+        for u in owner_idx:
+            kind, oid, b, e = allo[int(u)]
+            owners.append((kind, oid))
+            members.append([int(x) for x in layout.seg_len[b:e]])
+            toks.append(np.asarray(layout.tokens[starts[b]:starts[e]]))
+        if owners:
+            self.memory_compute_batch(owners, [version] * len(owners), members, np.concatenate(toks), tier)
 
     def load_memory(self, kind, oid, layer) -> keep_kv_view:
         v = keep_kv_view()

@@ -238,6 +238,7 @@ struct Context {
     // cursor
     std::unique_ptr<Pass> pf;
     std::unique_ptr<Pass> refresh;  // canonical-KV refresh workspace
+    DevBuf refresh_ws;               // in-place refresh: merged KV of the refreshed owners
     DevBuf kv;  // merged KV of the cursor [L][2][T][d]
     std::vector<void*> seg_ksrc_h, seg_vsrc_h;
     DevBuf d_ksrc, d_vsrc, d_cdst, d_cn;

@@ -97,3 +97,30 @@ def test_host_memory_fast_tc():
     assert np.max(np.abs(host["final_hidden"] - dev["final_hidden"])) <= 1e-3 * np.max(np.abs(dev["final_hidden"]))
     check_schedule(trace, host["plan"], lay, d, 2)
     assert len(trace) > 0
+
+
+def test_inplace_refresh(ko, golden):
+    """An update refreshes owners in place (no new arena): the blocks, the
+    versions and the prefill stay exactly as a fresh computation's."""
+    c = golden["instances"][11]
+    p = problem(ko, c)
+    lay = layout_of(p)
+    sched = np.array(c["sched"])
+    w = ko.model_init(c["L"], c["H"], c["d"], c["mlp"], c["V"], c["seed"])
+    ref = ko.plan_keep(p, w, sched)
+    owners = lay.owners()
+    pick = list(range(0, len(owners), 2))
+    with kb.Context(c["L"], c["H"], c["d"], c["mlp"], c["V"], c["seed"]) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay, version=1)
+        before = {u: ctx.memory_read(owners[u][0], owners[u][1], 1, int(np.sum(lay.seg_len[owners[u][2]:owners[u][3]])))
+                  for u in range(len(owners))}
+        dev0 = ctx.memory_stats()["device_bytes"]
+        ctx.memory_refresh(lay, pick, version=2)
+        assert ctx.memory_stats()["device_bytes"] == dev0  # refreshed in place
+        for u, (kind, oid, b, e) in enumerate(owners):
+            assert ctx.has_current(kind, oid, 2 if u in pick else 1)
+            k, v = ctx.memory_read(kind, oid, 1, int(np.sum(lay.seg_len[b:e])))
+            assert np.array_equal(k, before[u][0]) and np.array_equal(v, before[u][1])
+        got = ctx.plan_keep(lay, p.query, sched)
+    assert np.array_equal(got["plan"], ref["plan"]) and got["orders"] == ref["orders"]
