@@ -275,7 +275,9 @@ def run_ours(args, cfg, rank, world, dist):
     # --updates F: before every query a fraction F of the dynamic owners was
     # updated and must be refreshed (harness.hpp:609-628; "frequent dynamic
     # updates", test_harness.cpp:266-268); the refresh is part of the TTFT
-    dyn = [i for i, o in enumerate(layout.owners()) if o[0] == kb.SEGMENT]
+    owners_all = layout.owners()
+    dyn = [i for i, o in enumerate(owners_all) if o[0] == kb.SEGMENT]
+    owner_tokens = [int(np.sum(layout.seg_len[o[2]:o[3]])) for o in owners_all]
     upd_rng = np.random.default_rng(args.seed + 1)
     version = [1]
 
@@ -285,8 +287,7 @@ def run_ours(args, cfg, rank, world, dist):
             pick = [u for u in dyn if upd_rng.random() < args.updates]
             ctx.memory_refresh(layout, pick, version[0], tier=kb.TIER_HOST if host_mem else kb.TIER_DEVICE)
             # (owners not picked stay current at their old version)
-            step.refreshed_tokens = float(sum(int(np.sum(layout.seg_len[layout.owners()[u][2]:layout.owners()[u][3]]))
-                                              for u in pick))
+            step.refreshed_tokens = float(sum(owner_tokens[u] for u in pick))
         return ctx.plan_keep(layout, query, r, final_hidden=False)
 
     step.refreshed_tokens = 0.0

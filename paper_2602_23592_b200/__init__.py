@@ -370,7 +370,8 @@ class Context:
         layout.owners()): the canonical-KV refresh of updated memory
         (harness.hpp:609-628), in place when the blocks already exist."""
         starts = np.concatenate([[0], np.cumsum(layout.seg_len)]).astype(np.int64)
-        allo = layout.owners()
+        allo = layout._owners_cache if getattr(layout, "_owners_cache", None) else layout.owners()
+        layout._owners_cache = allo
         owners, members, toks = [], [], []
         for u in owner_idx:
             kind, oid, b, e = allo[int(u)]

@@ -241,7 +241,7 @@ struct Context {
     DevBuf refresh_ws;               // in-place refresh: merged KV of the refreshed owners
     DevBuf kv;  // merged KV of the cursor [L][2][T][d]
     std::vector<void*> seg_ksrc_h, seg_vsrc_h;
-    DevBuf d_ksrc, d_vsrc, d_cdst, d_cn;
+    DevBuf d_ksrc, d_vsrc, d_cdst, d_cn, d_bytes;
     std::vector<OwnerKey> seg_owner;      // owner of each layout segment
     std::vector<int64_t> seg_owner_row;   // row offset of the segment in the owner block
     // selector scratch

@@ -35,6 +35,9 @@ void launch_copy_cached(const void* const* ksrc, const void* const* vsrc, const 
                         const int32_t* nrows, int n_entries, int64_t row_bytes, void* kdst,
                         void* vdst, int max_rows, cudaStream_t st);
 
+// Batched device-to-device copy of n blocks (sizes multiples of 16 bytes).
+void launch_batch_copy(const void* const* src, void* const* dst, const int64_t* bytes, int n, cudaStream_t st);
+
 // K6: rowbins -> summary (prefill.hpp:281-288, 306-315).
 // rowbin[i][j]: probability mass (head mean) of compact row i on segment j.
 // seg_cbeg/seg_cend: compact row range of each segment (empty if inactive);

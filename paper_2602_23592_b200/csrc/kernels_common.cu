@@ -107,6 +107,25 @@ void launch_pack_heads(const void* recv, int G, int cpr, int m, int dl, int es, 
     KEEP_LAUNCH_CHECK();
 }
 
+// Batched device copy: entry e moves bytes[e] (a multiple of 16) from src[e]
+// to dst[e]; one CTA per entry, 16-byte vectors (in-place refresh scatter).
+__global__ void batch_copy_kernel(const int4* const* __restrict__ src, int4* const* __restrict__ dst,
+                                  const int64_t* __restrict__ bytes, int n) {
+    for (int e = blockIdx.x; e < n; e += gridDim.x) {
+        const int4* s = src[e];
+        int4* d = dst[e];
+        const int64_t nv = bytes[e] >> 4;
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) d[i] = s[i];
+    }
+}
+
+void launch_batch_copy(const void* const* src, void* const* dst, const int64_t* bytes, int n, cudaStream_t st) {
+    if (n <= 0) return;
+    batch_copy_kernel<<<unsigned(std::min(n, kNumSMs * 16)), 256, 0, st>>>(
+        reinterpret_cast<const int4* const*>(src), reinterpret_cast<int4* const*>(dst), bytes, n);
+    KEEP_LAUNCH_CHECK();
+}
+
 // ======================================================================= K1 ==
 __global__ void embed_kernel(const float* __restrict__ embed, const int32_t* __restrict__ tokens,
                              const int32_t* __restrict__ rows, int64_t n, int d,
