@@ -746,7 +746,7 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
                            c.d_cn.as<int32_t>(), int(ks.size()), int64_t(c.dl) * c.elem, p.kdst[l], p.vdst[l],
                            maxr, st);
     }
-    p.with_summary = true;
+    p.with_summary = p.summary_wanted;
     if (p.n == 0) {  // no computed rows: the summary is all zero
         p.summ.ensure(sizeof(double) * (size_t(S) + size_t(S) * S));
         KEEP_CUDA(cudaMemsetAsync(p.summ.p, 0, sizeof(double) * (size_t(S) + size_t(S) * S), st));
@@ -798,6 +798,7 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
     Pass& p = *c.pf;
     p.block_diag = false;
     p.summary_global = true;
+    p.summary_wanted = true;
     p.key_lo_h.clear();
     pass_init(c, p, sl, lay->tokens, query, qlen);
     const size_t sheet = size_t(p.T) * c.dl * c.elem;
@@ -1474,10 +1475,15 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
                 KEEP_CUDA(cudaEventRecord(ev_sel, c.s_sel));
             };
             c.gemm_ctas = walk ? kNumSMs - 1 : kNumSMs;
-            // sharded: the per-rank summary partials are summed only when read
-            p.summary_global = walk || (out && out->summaries) || (l + 1 < L && budget < live && !multihop);
+            // The summary is consumed only by a walk (or the single-hop ablation)
+            // and by callers asking for it; plan_keep's plans are unchanged when
+            // the other layers skip it (the reference computes and discards it).
+            // Sharded: the per-rank partials are summed only when read.
+            p.summary_wanted = walk || (out && out->summaries) || (l + 1 < L && budget < live && !multihop);
+            p.summary_global = p.summary_wanted;
             cursor_layer(c, active.data(), launch_walk);
             p.summary_global = true;
+            p.summary_wanted = true;
             c.gemm_ctas = kNumSMs;
             if (out && out->rows_per_layer) out->rows_per_layer[l] = p.n;
             if (out && out->summaries)

@@ -159,6 +159,7 @@ struct Pass {
     DevBuf x, x_alt, xb, q, ctx, ctxb, h, hb;
     DevBuf xrecv, xrows;          // sharded: all-to-all receive [G][rows/G][dl], packed ctx rows
     bool summary_global = true;   // sharded: sum the summary over ranks this layer
+    bool summary_wanted = true;   // plan_keep: only layers whose summary is read compute it
     // attention scratch
     DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi;
     int split_count = 1;
