@@ -66,6 +66,8 @@ struct TcArgs {
     double* sts_raw;        // [S x S]
     const int4* chunk_tab;  // [ceil(T/128) x 2] per 128-key chunk: {d0, nseg, -, -}, {mask0..3}
     int dbg;                // A/B timing aid (KEEP_DEBUG_ATTN): 1 = bins from hi only, 2 = no P.V
+    int norm_end;           // v2 without a summary: STATS finds only the max; CTX sums l and
+                            // normalises O at the end (no exp in STATS)
 };
 
 template <int MODE>
@@ -687,6 +689,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         const float scale = a.scale_log2;
         const int c0 = half * KH;             // first key column of this warp in a chunk
         float m_run = -FLT_MAX, l_run = 0.f;  // STATS
+        float lsum = 0.f;                     // CTX with norm_end: this warp's part of l
         float* part = reinterpret_cast<float*>(sm + LY::PART_OFF);
         int32_t* grp = reinterpret_cast<int32_t*>(sm + LY::GRP_OFF);
         int32_t* gsrc_s = grp + TM + 2;
@@ -698,7 +701,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const float m_row = a.m_fin[int64_t(row) * a.H + head];
                 const float il_row = a.inv_l[int64_t(row) * a.H + head];
                 src = a.row_seg[t];
-                m_eff = il_row > 0.f ? m_row - __log2f(il_row) : INFINITY;
+                m_eff = a.norm_end ? m_row : (il_row > 0.f ? m_row - __log2f(il_row) : INFINITY);
             }
             if (bins) {
                 const int prev = (r > 0 && rvalid) ? a.row_seg[a.rows[row - 1]] : INT32_MIN;
@@ -800,7 +803,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                                     sv[c][jj] = __float_as_uint(-INFINITY);
                             cmr = fmaxf(cmr, __uint_as_float(sv[c][jj]));
                         }
-                    if (cmr > -INFINITY) {
+                    if (cmr > -INFINITY && a.norm_end) {
+                        m_run = fmaxf(m_run, cmr * scale);  // max only: the CTX pass sums l
+                    } else if (cmr > -INFINITY) {
                         const float mn = fmaxf(m_run, cmr * scale);
                         float ps0 = 0.f, ps1 = 0.f, ps2 = 0.f, ps3 = 0.f;
 #pragma unroll
@@ -836,6 +841,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         const uint32_t h = pack_bf16(p0, p1);
                         hv[i] = h;
                         lv[i] = pack_bf16(p0 - __uint_as_float(h << 16), p1 - __uint_as_float(h & 0xffff0000u));
+                        lsum += p0 + p1;
                     }
                     tmem_st16(tp + uint32_t(16 * c), hv);
                     tmem_st16(tp + uint32_t(32 + 16 * c), lv);
@@ -884,6 +890,17 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const int last = ((niter - 1 - team) >= 0) ? niter - 1 - ((niter - 1 - team) & 1) : -1;
                 if (bins && last >= 0) flush_bins(last);
             }
+            // norm_end: l of each row = the 4 (team, half) partials, fixed order
+            float o_scale = 1.f, l_row = 0.f;
+            if (a.norm_end) {
+                float* lp = part;  // [4][128] (the bins partials are unused without a summary)
+                lp[(team * 2 + half) * TM + r] = lsum;
+                named_sync(1, NTEAM * 256);
+                l_row = ((lp[r] + lp[TM + r]) + lp[2 * TM + r]) + lp[3 * TM + r];
+                o_scale = (a.nsplit == 1 && l_row > 0.f) ? 1.f / l_row : 1.f;
+                if (a.nsplit > 1 && rvalid && team == 0 && half == 0)
+                    a.l_part[(int64_t(sp) * a.n + row) * a.H + head] = l_row;
+            }
             // O columns [32 g, 32 g + 32), g = 2 team + half
             const int oc = 32 * (team * 2 + half);
             uint32_t ov[32];
@@ -893,6 +910,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 #pragma unroll
                 for (int e = 0; e < 32; ++e) ov[e] = 0u;
             }
+            if (o_scale != 1.f)
+#pragma unroll
+                for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * o_scale);
             if (rvalid) {
                 const int col = head * DH + oc;
                 if (a.nsplit == 1) {
@@ -954,10 +974,19 @@ __global__ void tc_stats_combine(const float* __restrict__ mp, const float* __re
     }
 }
 
-__global__ void tc_ctx_combine(const float* __restrict__ op, int nsplit, int64_t nd, __nv_bfloat16* __restrict__ ctx) {
+// lp != nullptr (norm_end): the partials are unnormalised with one global max,
+// ctx = sum_s O_s / sum_s l_s
+__global__ void tc_ctx_combine(const float* __restrict__ op, int nsplit, int64_t nd, __nv_bfloat16* __restrict__ ctx,
+                               const float* __restrict__ lp, int d, int H, int64_t nh) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nd; e += int64_t(gridDim.x) * blockDim.x) {
         float acc = 0.f;
         for (int s = 0; s < nsplit; ++s) acc += op[s * nd + e];
+        if (lp) {
+            const int64_t rh = (e / d) * H + (e % d) / DH;
+            float l = 0.f;
+            for (int s = 0; s < nsplit; ++s) l += lp[s * nh + rh];
+            acc = l > 0.f ? acc / l : 0.f;
+        }
         ctx[e] = __float2bfloat16_rn(acc);
     }
 }
@@ -1143,6 +1172,13 @@ int launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
     // v2 (384 threads, summary bins on the tensor core) unless the layout has
     // more than 32 segments in some 128-key chunk (then the v1 scan bins)
     const dim3 grid(tiles, H, a.nsplit);
+    {
+        // without a summary the v2 passes need no normalised p: max-only STATS,
+        // l summed by the CTX pass
+        const char* e = std::getenv("KEEP_DEBUG_NO_BINS");
+        const bool no_bins = !L.with_bins || (e && *e == '1');
+        a.norm_end = (v2 && no_bins) ? 1 : 0;
+    }
     if (v2) { launch_mode2<MODE_STATS, 16>(mq, mk, mv, mq, a, grid, st); ++launched; }
     else { launch_mode<MODE_STATS>(mq, mk, mv, a, grid, st); ++launched; }
     const int64_t nh = int64_t(n) * H;
@@ -1159,6 +1195,7 @@ int launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
         const char* e = std::getenv("KEEP_DEBUG_ATTN");
         a.dbg = e ? std::atoi(e) : 0;
     }
+
     if (v2) {
         if (L.with_bins && !dbg_no_bins) {
             const int nchunks = int(ceil_div(T, TK));
@@ -1176,8 +1213,8 @@ int launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
     }
     if (a.nsplit > 1) {
         const int64_t nd = int64_t(n) * d;
-        tc_ctx_combine<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(L.o_part, a.nsplit,
-                                                                                                   nd, L.ctx);
+        tc_ctx_combine<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(
+            L.o_part, a.nsplit, nd, L.ctx, a.norm_end ? L.l_part : nullptr, d, H, int64_t(n) * H);
         KEEP_LAUNCH_CHECK();
         ++launched;
     }
