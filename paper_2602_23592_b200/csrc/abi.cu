@@ -189,6 +189,8 @@ uint8_t* layer_values(const Context& c, const Payload& p, int l) {
     return layer_keys(c, p, l) + p.arena->rows * c.dl * c.elem;
 }
 
+constexpr int64_t kArenaPad = 128;  // spare rows per arena layer sheet (query rows of aliased layers)
+
 std::shared_ptr<Arena> make_arena(Context& c, int64_t rows, int tier) {
     auto a = std::make_shared<Arena>();
     a->rows = rows;
@@ -701,12 +703,24 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
     if (l >= c.L) raise(KEEP_ERR_PLAN, "stepped past last layer");  // prefill.hpp:227
     for (int i = 0; i < S; ++i)
         if (active[i] && !p.prev[i]) raise(KEEP_ERR_PLAN, "plan is not monotone across layers");
+    // all-reused layer over an in-order arena: run it on the arena sheets
+    // (the cached rows are already in place; only the query rows -- in the
+    // arena's spare rows -- are written), no merged-KV copy
+    bool any_active = false;
+    for (int i = 0; i < S && !any_active; ++i) any_active = active[i] != 0;
+    bool alias_l = c.alias_arena != nullptr && !any_active;
+    for (int i = 0; i < S && alias_l; ++i) alias_l = block_current(c, c.seg_owner[i], l, nullptr);
+    if (alias_l) {
+        const int64_t sheet = c.alias_arena->rows * int64_t(c.dl) * c.elem;
+        p.kdst[l] = static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * sheet;
+        p.vdst[l] = static_cast<uint8_t*>(p.kdst[l]) + sheet;
+    }
     // cached rows of this layer (prefill.hpp:255-263, 340-350): resolve first
     std::vector<void*> ks, vs;
     std::vector<int32_t> dr, nr;
     int maxr = 0;
     for (int i = 0; i < S; ++i) {
-        if (active[i] || loader_covers(c, i)) continue;  // host-tier owners: K10 loader
+        if (active[i] || loader_covers(c, i) || alias_l) continue;  // host-tier owners: K10 loader
         const Payload* pl = nullptr;
         const OwnerKey& ok = c.seg_owner[i];
         if (!block_current(c, ok, l, &pl)) {
@@ -809,6 +823,26 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
         p.kdst[l] = static_cast<uint8_t*>(c.kv.p) + size_t(l) * 2 * sheet;
         p.vdst[l] = static_cast<uint8_t*>(c.kv.p) + (size_t(l) * 2 + 1) * sheet;
     }
+    // is the layout one HBM arena in order (with spare rows for the query)?
+    c.alias_arena = nullptr;
+    c.alias_hold.reset();
+    {
+        const Arena* ar = nullptr;
+        bool ok = true;
+        for (int i = 0; i < S && ok; ++i) {
+            auto it = c.store.find(c.seg_owner[i]);
+            if (it == c.store.end() || it->second.arena->tier != KEEP_TIER_DEVICE) {
+                ok = false;
+                break;
+            }
+            if (!ar) ar = it->second.arena.get();
+            ok = it->second.arena.get() == ar && it->second.row0 + c.seg_owner_row[i] == p.seg_start[i];
+        }
+        if (ok && ar && ar->rows >= p.T) {
+            c.alias_arena = const_cast<Arena*>(ar);
+            c.alias_hold = c.store.find(c.seg_owner[0])->second.arena;  // kept alive for the prefill
+        }
+    }
     loader_begin(c, p);
 }
 
@@ -831,14 +865,20 @@ void cursor_finish(Context& c, float* final_hidden, float* kv_out) {
             std::memcpy(final_hidden + size_t(p.rows_h[i]) * d, xc.data() + size_t(i) * d, sizeof(float) * d);
     }
     if (kv_out) {
-        const size_t nel = size_t(c.L) * 2 * p.T * c.dl;
-        if (!c.fast) {
-            KEEP_CUDA(cudaMemcpy(kv_out, c.kv.p, sizeof(float) * nel, cudaMemcpyDeviceToHost));
-        } else {
-            std::vector<uint16_t> tmp(nel);
-            KEEP_CUDA(cudaMemcpy(tmp.data(), c.kv.p, 2 * nel, cudaMemcpyDeviceToHost));
-            for (size_t i = 0; i < nel; ++i) kv_out[i] = bf2f(tmp[i]);
-        }
+        // per layer and K / V: the merged buffer or an aliased arena sheet
+        const size_t nel = size_t(p.T) * c.dl;
+        std::vector<uint16_t> tmp(c.fast ? nel : 0);
+        for (int l = 0; l < c.L; ++l)
+            for (int kv = 0; kv < 2; ++kv) {
+                const void* src = kv ? p.vdst[l] : p.kdst[l];
+                float* dst = kv_out + (size_t(l) * 2 + kv) * nel;
+                if (!c.fast) {
+                    KEEP_CUDA(cudaMemcpy(dst, src, sizeof(float) * nel, cudaMemcpyDeviceToHost));
+                } else {
+                    KEEP_CUDA(cudaMemcpy(tmp.data(), src, 2 * nel, cudaMemcpyDeviceToHost));
+                    for (size_t i = 0; i < nel; ++i) dst[i] = bf2f(tmp[i]);
+                }
+            }
     }
 }
 
@@ -879,7 +919,6 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
     for (int o = 0; o < n_owners; ++o)
         for (int t = 0; t < seglen[o]; ++t) p.key_lo_h[row0[o] + t] = int32_t(row0[o]);
     upload(p.d_key_lo, p.key_lo_h, c.s_main);
-    const size_t sheet = size_t(rows) * c.dl * c.elem;
     // In place (an update of owners that already have a block of the same
     // size in this tier): compute into the grow-only refresh workspace and
     // copy every block into its slot -- no allocation on the query path
@@ -891,11 +930,16 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
     }
     std::shared_ptr<Arena> dev;
     uint8_t* base = nullptr;
+    // new arenas carry kArenaPad spare rows per layer sheet: a prefill whose
+    // layout is the arena in order can run its all-reused layers directly on
+    // the arena sheets, writing only the query rows into the spare rows
+    const int64_t arows = in_place ? rows : rows + kArenaPad;
+    const size_t sheet = size_t(arows) * c.dl * c.elem;
     if (in_place) {
         c.refresh_ws.ensure(size_t(c.L) * 2 * sheet);
         base = static_cast<uint8_t*>(c.refresh_ws.p);
     } else {
-        dev = make_arena(c, rows, KEEP_TIER_DEVICE);
+        dev = make_arena(c, arows, KEEP_TIER_DEVICE);
         base = static_cast<uint8_t*>(dev->buf.p);
     }
     p.kdst.resize(c.L);
@@ -953,7 +997,7 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
     }
     std::shared_ptr<Arena> arena = dev;
     if (tier == KEEP_TIER_HOST) {
-        arena = make_arena(c, rows, KEEP_TIER_HOST);
+        arena = make_arena(c, arows, KEEP_TIER_HOST);
         KEEP_CUDA(cudaMemcpyAsync(arena->buf.p, dev->buf.p, size_t(c.L) * 2 * sheet, cudaMemcpyDeviceToHost, c.s_main));
     }
     KEEP_CUDA(cudaStreamSynchronize(c.s_main));

@@ -243,6 +243,8 @@ struct Context {
     DevBuf kv;  // merged KV of the cursor [L][2][T][d]
     std::vector<void*> seg_ksrc_h, seg_vsrc_h;
     DevBuf d_ksrc, d_vsrc, d_cdst, d_cn, d_bytes;
+    Arena* alias_arena = nullptr;         // layout == one in-order HBM arena (all-reused layers run on it)
+    std::shared_ptr<Arena> alias_hold;
     std::vector<OwnerKey> seg_owner;      // owner of each layout segment
     std::vector<int64_t> seg_owner_row;   // row offset of the segment in the owner block
     // selector scratch

@@ -146,6 +146,8 @@ def test_selective_prefill_plans(ko, golden, ctx_cache):
         "reuse": np.zeros((L, S), np.uint8),
         "prefix2": np.tile((np.arange(S) < 2).astype(np.uint8), (L, 1)),
         "drop_after_0": np.vstack([np.ones(S, np.uint8)] + [(np.arange(S) < 2).astype(np.uint8)] * (L - 1)),
+        # all memory reused after layer 1: those layers run on the arena sheets (no merged-KV copy)
+        "empty_after_1": np.vstack([np.ones((2, S), np.uint8), np.zeros((L - 2, S), np.uint8)]),
     }
     for name, plan in plans.items():
         got = ctx.selective_prefill(lay, p.query, plan)
