@@ -214,6 +214,30 @@ std::string owner_str(const OwnerKey& k) {
     return (k.kind == KEEP_OWNER_SEGMENT ? "s" : "g") + std::to_string(k.id);
 }
 
+// Resolve each layout segment's owner payload and current version (once per
+// prefill, again only if the memory store changed in between).
+void resolve_segments(Context& c, int S) {
+    c.seg_pl.assign(S, nullptr);
+    c.seg_cur.assign(S, 0);
+    for (int i = 0; i < S; ++i) {
+        auto it = c.store.find(c.seg_owner[i]);
+        auto cv = c.current_version.find(c.seg_owner[i]);
+        if (it != c.store.end() && cv != c.current_version.end()) {
+            c.seg_pl[i] = &it->second;
+            c.seg_cur[i] = cv->second;
+        }
+    }
+    c.seg_gen = c.store_gen;
+}
+
+// The segment's cached block for layer l if current (cache_manager.hpp:104-116),
+// from the per-prefill resolution of cursor_begin (no map lookups per layer).
+const Payload* seg_block_current(const Context& c, int i, int l) {
+    const Payload* pl = c.seg_pl[i];
+    if (!pl || l < 0 || l >= c.L || !pl->present[l] || pl->layer_version[l] != c.seg_cur[i]) return nullptr;
+    return pl;
+}
+
 // ----------------------------------------------------------- weight access --
 void model_alloc_init(Context& c) {
     const int L = c.L, d = c.d, f = c.f, V = c.V, dl = c.dl;
@@ -291,6 +315,11 @@ bool use_tc_attention(const Context& c, const Pass& p) { return use_tc_attention
 
 void plan_splits(Context& c, Pass& p) {
     const bool tc = use_tc_attention(c, p);
+    // the split plan depends only on (n, T, path): layers of equal size reuse
+    // the uploaded arrays (no host->device staging on the deep layers)
+    const int64_t key = (int64_t(p.n) << 32) ^ (int64_t(p.T) << 2) ^ (tc ? 1 : 0) ^ (p.block_diag ? 2 : 0);
+    if (key == p.split_key) return;
+    p.split_key = key;
     const int tiles = int(ceil_div(p.n, tc ? 128 : 16));
     int nsplit = 1;
     if (tc && !p.block_diag) {
@@ -650,6 +679,7 @@ void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const i
                const int32_t* query, int qlen) {
     p.S = int(seg_len.size());
     p.seg_len = seg_len;
+    p.split_key = -1;  // new layout: re-plan the attention splits
     p.seg_start.assign(p.S, 0);
     int pos = 0;
     for (int i = 0; i < p.S; ++i) {
@@ -703,13 +733,14 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
     if (l >= c.L) raise(KEEP_ERR_PLAN, "stepped past last layer");  // prefill.hpp:227
     for (int i = 0; i < S; ++i)
         if (active[i] && !p.prev[i]) raise(KEEP_ERR_PLAN, "plan is not monotone across layers");
+    if (c.seg_gen != c.store_gen) resolve_segments(c, S);  // the store changed mid-prefill
     // all-reused layer over an in-order arena: run it on the arena sheets
     // (the cached rows are already in place; only the query rows -- in the
     // arena's spare rows -- are written), no merged-KV copy
     bool any_active = false;
     for (int i = 0; i < S && !any_active; ++i) any_active = active[i] != 0;
     bool alias_l = c.alias_arena != nullptr && !any_active;
-    for (int i = 0; i < S && alias_l; ++i) alias_l = block_current(c, c.seg_owner[i], l, nullptr);
+    for (int i = 0; i < S && alias_l; ++i) alias_l = seg_block_current(c, i, l) != nullptr;
     if (alias_l) {
         const int64_t sheet = c.alias_arena->rows * int64_t(c.dl) * c.elem;
         p.kdst[l] = static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * sheet;
@@ -721,9 +752,9 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
     int maxr = 0;
     for (int i = 0; i < S; ++i) {
         if (active[i] || loader_covers(c, i) || alias_l) continue;  // host-tier owners: K10 loader
-        const Payload* pl = nullptr;
         const OwnerKey& ok = c.seg_owner[i];
-        if (!block_current(c, ok, l, &pl)) {
+        const Payload* pl = seg_block_current(c, i, l);
+        if (!pl) {
             c.stats.cache_misses++;
             raise(KEEP_ERR_CACHE_MISS, "missing cached KV for segment " + std::to_string(i) + " (owner " +
                                            owner_str(ok) + ") layer " + std::to_string(l));
@@ -823,6 +854,7 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
         p.kdst[l] = static_cast<uint8_t*>(c.kv.p) + size_t(l) * 2 * sheet;
         p.vdst[l] = static_cast<uint8_t*>(c.kv.p) + (size_t(l) * 2 + 1) * sheet;
     }
+    resolve_segments(c, S);
     // is the layout one HBM arena in order (with spare rows for the query)?
     c.alias_arena = nullptr;
     c.alias_hold.reset();
@@ -890,6 +922,7 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
                           const int32_t* owner_members, const int32_t* member_len, const int32_t* tokens,
                           int tier) {
     need_weights(c);
+    ++c.store_gen;
     if (n_owners < 1) return;
     if (tier != KEEP_TIER_DEVICE && tier != KEEP_TIER_HOST) raise(KEEP_ERR_CONFIG, "unknown tier");
     std::vector<int32_t> seglen;  // one "segment" per owner (the owner's rows)
@@ -1116,6 +1149,7 @@ int keep_memory_put(void* ctx, keep_owner owner, uint64_t version, int32_t layer
                     const float* keys, const float* values, int32_t tier) {
     return guard([&] {
         Context& c = *C(ctx);
+        ++c.store_gen;
         if (layer < 0 || layer >= c.L) raise(KEEP_ERR_INPUT, "layer out of range");
         if (tokens < 1) raise(KEEP_ERR_INPUT, "empty block");
         if (tier != KEEP_TIER_DEVICE && tier != KEEP_TIER_HOST) raise(KEEP_ERR_CONFIG, "unknown tier");
@@ -1203,6 +1237,7 @@ int keep_memory_compute_batch(void* ctx, int32_t n_owners, const keep_owner* own
 int keep_load_memory(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* out) {
     return guard([&] {
         Context& c = *C(ctx);
+        ++c.store_gen;
         const OwnerKey k{owner.kind, owner.id};
         const Payload* pl = nullptr;
         if (!block_current(c, k, layer, &pl)) {  // cache_manager.hpp:104-116
@@ -1265,6 +1300,7 @@ int keep_memory_has_current(void* ctx, keep_owner owner, uint64_t version, int32
 int keep_invalidate(void* ctx, keep_owner owner, uint64_t new_version, uint64_t tokens) {
     return guard([&] {  // cache_manager.hpp:163-184
         Context& c = *C(ctx);
+        ++c.store_gen;
         const OwnerKey k{owner.kind, owner.id};
         auto it = c.store.find(k);
         if (it != c.store.end()) {

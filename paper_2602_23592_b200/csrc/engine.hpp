@@ -163,6 +163,7 @@ struct Pass {
     // attention scratch
     DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi;
     int split_count = 1;
+    int64_t split_key = -1;
     DevBuf vt, split_lo_a, split_hi_a, chunk_tab, zt;  // FAST tensor-core attention
     int nb = 0;
     int split_count_a = 1;
@@ -246,6 +247,9 @@ struct Context {
     Arena* alias_arena = nullptr;         // layout == one in-order HBM arena (all-reused layers run on it)
     std::shared_ptr<Arena> alias_hold;
     std::vector<OwnerKey> seg_owner;      // owner of each layout segment
+    std::vector<const Payload*> seg_pl;   // its payload (resolved at prefill begin)
+    std::vector<uint64_t> seg_cur;        // and its current version
+    uint64_t store_gen = 0, seg_gen = 0;  // memory-store mutations / generation resolved
     std::vector<int64_t> seg_owner_row;   // row offset of the segment in the owner block
     // selector scratch
     DevBuf sel_order, sel_n, sel_cand;

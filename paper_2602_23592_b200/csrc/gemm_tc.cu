@@ -17,6 +17,8 @@
 // add with a bf16 mirror for the next GEMM, ReLU to bf16, plain fp32 store.
 // Tiles are rasterised in bands of GM m-blocks so a band of A and a window of
 // weight columns stay L2-resident (126 MB) while 148 CTAs sweep them.
+#include <unordered_map>
+
 #include "engine.hpp"
 #include "tc_common.cuh"
 
@@ -42,6 +44,25 @@ EncodeFn encode_fn() {
 // 2-D bf16 tensor [rows x cols] (row stride ld elements), box BK x box_rows,
 // 128-byte swizzle; out-of-bounds rows read as zero.
 CUtensorMap make_map_bf16(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    // memoised: a map is a pure function of its arguments, and the engine
+    // re-uses the same weight / workspace buffers every layer and every prefill
+    struct Key {
+        const void* p;
+        int64_t r, c, ld;
+        int b;
+        bool operator==(const Key& o) const { return p == o.p && r == o.r && c == o.c && ld == o.ld && b == o.b; }
+    };
+    struct Hash {
+        size_t operator()(const Key& k) const {
+            return std::hash<const void*>()(k.p) ^ (size_t(k.r) * 0x9e3779b97f4a7c15ull) ^ (size_t(k.c) << 17) ^
+                   (size_t(k.ld) << 7) ^ size_t(k.b);
+        }
+    };
+    thread_local std::unordered_map<Key, CUtensorMap, Hash> memo;
+    const Key key{ptr, rows, cols, ld, box_rows};
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+    if (memo.size() > 8192) memo.clear();
     CUtensorMap tm;
     const cuuint64_t gdim[2] = {cuuint64_t(cols), cuuint64_t(rows)};
     const cuuint64_t gstride[1] = {cuuint64_t(ld * 2)};
@@ -51,6 +72,7 @@ CUtensorMap make_map_bf16(const void* ptr, int64_t rows, int64_t cols, int64_t l
                                    estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) raise(KEEP_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    memo.emplace(key, tm);
     return tm;
 }
 
@@ -284,15 +306,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 }
 
 // split-K finalisation: the fused epilogue over the reduced fp32 tile
-__global__ void splitk_epilogue_kernel(const float* __restrict__ acc, int M, int N, EpiArgs epi) {
+// (it leaves the workspace zeroed for the next split-K GEMM)
+__global__ void splitk_epilogue_kernel(float* __restrict__ acc, int M, int N, EpiArgs epi) {
     const int chunks = N / 32;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < M * chunks; e += gridDim.x * blockDim.x) {
         const int m = e / chunks, n = (e % chunks) * 32;
         float v[32];
-        const float4* src = reinterpret_cast<const float4*>(acc + int64_t(m) * N + n);
+        float4* src = reinterpret_cast<float4*>(acc + int64_t(m) * N + n);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const float4 x = src[q];
+            src[q] = make_float4(0.f, 0.f, 0.f, 0.f);
             v[4 * q] = x.x;
             v[4 * q + 1] = x.y;
             v[4 * q + 2] = x.z;
@@ -320,10 +344,14 @@ void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int
     float* acc = nullptr;
     if (ksplit > 1) {
         // per-thread grow-only fp32 workspace (one context per host thread)
+        // (zeroed once when it grows; every finalisation pass re-zeroes what it read)
         thread_local DevBuf ws;
-        ws.ensure(sizeof(float) * size_t(M) * N);
+        const size_t need = sizeof(float) * size_t(M) * N;
+        if (need > ws.bytes || !ws.p) {
+            ws.ensure(need);
+            KEEP_CUDA(cudaMemsetAsync(ws.p, 0, ws.bytes, st));
+        }
         acc = ws.as<float>();
-        KEEP_CUDA(cudaMemsetAsync(acc, 0, sizeof(float) * size_t(M) * N, st));
     }
     gemm_tc_kernel<BN, AR><<<grid, kThreads, CF::SMEM, st>>>(ta, tb, M, N, K, epi, ksplit, acc);
     KEEP_LAUNCH_CHECK();
