@@ -1100,6 +1100,9 @@ int keep_ctx_destroy(void* ctx) {
         c->refresh.reset();
         c->store.clear();
         c->comm.reset();
+        for (auto e : c->pk_evs) cudaEventDestroy(e);
+        if (c->ev_sum) cudaEventDestroy(c->ev_sum);
+        if (c->ev_sel) cudaEventDestroy(c->ev_sel);
         cudaStreamDestroy(c->s_main);
         cudaStreamDestroy(c->s_copy);
         cudaStreamDestroy(c->s_sel);
@@ -1497,14 +1500,14 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
     return guard([&] {
         Context& c = *C(ctx);
         cudaStream_t st = c.s_main;
-        std::vector<cudaEvent_t> evs(c.L + 1);
-        for (auto& e : evs) KEEP_CUDA(cudaEventCreate(&e));
-        struct EvGuard {
-            std::vector<cudaEvent_t>& v;
-            ~EvGuard() {
-                for (auto e : v) cudaEventDestroy(e);
-            }
-        } evg{evs};
+        // per-context events and pinned walk buffer, created once (no
+        // cudaHostAlloc / event churn on the TTFT path)
+        if (c.pk_evs.size() != size_t(c.L + 1)) {
+            for (auto e : c.pk_evs) cudaEventDestroy(e);
+            c.pk_evs.assign(c.L + 1, nullptr);
+            for (auto& e : c.pk_evs) KEEP_CUDA(cudaEventCreate(&e));
+        }
+        std::vector<cudaEvent_t>& evs = c.pk_evs;
         KEEP_CUDA(cudaEventRecord(evs[0], st));
         cursor_begin(c, layout, query, qlen);
         Pass& p = *c.pf;
@@ -1512,22 +1515,15 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
         std::vector<uint8_t> active(S, 1);
         c.sel_order.ensure(sizeof(int32_t) * (S + 2));
         c.sel_cand.ensure(std::max(S, 1));
-        int32_t* hbuf = nullptr;  // pinned: the async D2H of the walk must not stage
-        KEEP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&hbuf), sizeof(int32_t) * (S + 2), cudaHostAllocDefault));
-        struct HostFree {
-            int32_t* p;
-            ~HostFree() { cudaFreeHost(p); }
-        } hf{hbuf};
-        cudaEvent_t ev_sum, ev_sel;
-        KEEP_CUDA(cudaEventCreateWithFlags(&ev_sum, cudaEventDisableTiming));
-        KEEP_CUDA(cudaEventCreateWithFlags(&ev_sel, cudaEventDisableTiming));
-        struct EvFree {
-            cudaEvent_t a, b;
-            ~EvFree() {
-                cudaEventDestroy(a);
-                cudaEventDestroy(b);
-            }
-        } ef{ev_sum, ev_sel};
+        // pinned: the async D2H of the walk must not stage
+        if (c.walk_host.bytes < sizeof(int32_t) * size_t(S + 2) || !c.walk_host.host)
+            c.walk_host.alloc(sizeof(int32_t) * size_t(S + 2), true);
+        int32_t* hbuf = c.walk_host.as<int32_t>();
+        if (!c.ev_sum) {
+            KEEP_CUDA(cudaEventCreateWithFlags(&c.ev_sum, cudaEventDisableTiming));
+            KEEP_CUDA(cudaEventCreateWithFlags(&c.ev_sel, cudaEventDisableTiming));
+        }
+        cudaEvent_t ev_sum = c.ev_sum, ev_sel = c.ev_sel;
         for (int l = 0; l < L; ++l) {
             if (out && out->plan) std::copy(active.begin(), active.end(), out->plan + size_t(l) * S);
             if (out && out->order_len) out->order_len[l] = -1;

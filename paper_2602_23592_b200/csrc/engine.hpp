@@ -254,6 +254,9 @@ struct Context {
     // selector scratch
     DevBuf sel_order, sel_n, sel_cand;
     DevBuf logits;
+    DevBuf walk_host;                     // pinned walk result (plan_keep)
+    std::vector<cudaEvent_t> pk_evs;      // plan_keep layer events
+    cudaEvent_t ev_sum = nullptr, ev_sel = nullptr;
     Profiler prof;
     Loader loader;
     int gemm_ctas = kNumSMs;  // 147 while the selector overlaps the MLP
