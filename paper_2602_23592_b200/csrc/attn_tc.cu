@@ -827,7 +827,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 // p, then P = hi + lo back into S[b] (this half's 64 columns),
                 // 32 keys at a time so the split stays in registers
                 const uint32_t tp = tm_s0 + lane_base + uint32_t(b * TK + half * 64);
-                auto make_p = [&](auto masked, int c) {
+                // (without a summary only hi feeds P.V: lo is neither formed nor stored)
+                auto make_p = [&](auto masked, auto with_lo, int c) {
                     uint32_t hv[16], lv[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -840,18 +841,30 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         }
                         const uint32_t h = pack_bf16(p0, p1);
                         hv[i] = h;
-                        lv[i] = pack_bf16(p0 - __uint_as_float(h << 16), p1 - __uint_as_float(h & 0xffff0000u));
-                        lsum += p0 + p1;
+                        if constexpr (decltype(with_lo)::value)
+                            lv[i] = pack_bf16(p0 - __uint_as_float(h << 16), p1 - __uint_as_float(h & 0xffff0000u));
+                        else
+                            lsum += p0 + p1;
                     }
                     tmem_st16(tp + uint32_t(16 * c), hv);
-                    tmem_st16(tp + uint32_t(32 + 16 * c), lv);
+                    if constexpr (decltype(with_lo)::value) tmem_st16(tp + uint32_t(32 + 16 * c), lv);
                 };
-                if (full_half) {
-                    make_p(std::false_type{}, 0);
-                    make_p(std::false_type{}, 1);
+                if (bins) {
+                    if (full_half) {
+                        make_p(std::false_type{}, std::true_type{}, 0);
+                        make_p(std::false_type{}, std::true_type{}, 1);
+                    } else {
+                        make_p(std::true_type{}, std::true_type{}, 0);
+                        make_p(std::true_type{}, std::true_type{}, 1);
+                    }
                 } else {
-                    make_p(std::true_type{}, 0);
-                    make_p(std::true_type{}, 1);
+                    if (full_half) {
+                        make_p(std::false_type{}, std::false_type{}, 0);
+                        make_p(std::false_type{}, std::false_type{}, 1);
+                    } else {
+                        make_p(std::true_type{}, std::false_type{}, 0);
+                        make_p(std::true_type{}, std::false_type{}, 1);
+                    }
                 }
                 tmem_wait_st();
                 fence_before();
