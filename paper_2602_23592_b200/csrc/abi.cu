@@ -323,9 +323,28 @@ void plan_splits(Context& c, Pass& p) {
     const int tiles = int(ceil_div(p.n, tc ? 128 : 16));
     int nsplit = 1;
     if (tc && !p.block_diag) {
-        // stats / context: unaligned splits, ~2 waves of (tile, head, split) CTAs
-        const int na = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * kNumSMs, int64_t(tiles) * c.H),
-                                                                  ceil_div(p.T, 1024))));
+        // stats / context: unaligned key splits.  One CTA per SM (smem), so
+        // pick the split count minimising (waves of CTAs) x (chunks per CTA):
+        // few-row layers (the query alone) otherwise lose a third of a wave.
+        int na = 1;
+        static const int forced = [] {
+            const char* e = std::getenv("KEEP_ATTN_SPLITS");  // A/B knob
+            return e ? std::atoi(e) : 0;
+        }();
+        if (forced > 0) {
+            na = forced;
+        } else if (int64_t(tiles) * c.H < 2 * kNumSMs) {
+            int64_t best = INT64_MAX;
+            const int64_t nch = ceil_div(p.T, 128);
+            for (int cand = 1; cand <= std::min<int64_t>(32, nch); ++cand) {
+                const int64_t waves = ceil_div(int64_t(tiles) * c.H * cand, kNumSMs);
+                const int64_t cost = waves * (ceil_div(nch, cand) + 2);  // +2: per-CTA prologue / epilogue
+                if (cost < best) {
+                    best = cost;
+                    na = cand;
+                }
+            }
+        }
         std::vector<int32_t> lo, hi;
         const int64_t step = ceil_div(ceil_div(p.T, na), 128) * 128;
         for (int64_t k = 0; k < p.T; k += step) {

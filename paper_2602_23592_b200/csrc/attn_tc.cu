@@ -276,7 +276,9 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ 
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[b]);
             // keys of this chunk visible to this row: [kv0, kv1)
-            const int kv0 = klo - k0, kv1 = min(hi, t + 1) - k0;
+            // (max: a row that ends before this key split sees an empty range,
+            // not a wrapped unsigned one)
+            const int kv0 = klo - k0, kv1 = max(kv0, min(hi, t + 1) - k0);
             // fully visible chunk for every row of the warp: no per-key masks
             const bool full_chunk = __all_sync(0xffffffffu, kv0 <= 0 && kv1 >= TK);
             if (MODE == MODE_STATS) {
@@ -786,7 +788,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s_empty[b]);
             }
-            const int kv0 = klo - k0 - c0, kv1 = min(hi, t + 1) - k0 - c0;  // visible keys of this half
+            // visible keys of this half; a row that ends before this key split
+            // sees an empty range (max), never a wrapped unsigned one
+            const int kv0 = klo - k0 - c0, kv1 = max(kv0, min(hi, t + 1) - k0 - c0);
             const bool full_half = __all_sync(0xffffffffu, kv0 <= 0 && kv1 >= KH);
             if (MODE == MODE_STATS) {
                 // max on the raw scores (scale > 0), then exp2(s*scale - m):
