@@ -372,6 +372,19 @@ def run_ours(args, cfg, rank, world, dist):
                        "items": len(tr), "preloads": sum(1 for r in tr if r["kind"] == "preload"),
                        "urgent": sum(1 for r in tr if r["kind"] == "urgent")}
 
+    # fidelity beside speed: KEEP's last row against a full
+    # recompute of the same prefill (schedule of ones), divergence as in
+    # prefill.hpp:501-531, plus the full recompute's own TTFT
+    quality = None
+    if args.updates == 0 and not args.no_quality:
+        keep_res = ctx.plan_keep(layout, query, r, final_hidden=True)
+        full_res = ctx.plan_keep(layout, query, np.ones(L), final_hidden=True)
+        l2, kl = ctx.divergence(keep_res["final_hidden"][-1], full_res["final_hidden"][-1])
+        quality = {"full_recompute_ttft_ms": full_res["ttft_ms"], "keep_ttft_ms": keep_res["ttft_ms"],
+                   "speedup_vs_full_recompute": full_res["ttft_ms"] / keep_res["ttft_ms"],
+                   "divergence_vs_full": {"l2": l2, "sym_kl": kl},
+                   "full_recomputed_tokens": float(np.sum(full_res["rows_per_layer"]))}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         s = cpu_sample(cfg)
@@ -409,6 +422,7 @@ def run_ours(args, cfg, rank, world, dist):
                     "ttft_ms": e2e_mean * 1e3},
             "gpu_launches": launches,
             "loader": loader_info,
+            "quality": quality,
             "roofline": roof,
             "roofline_kernels": [gemm_roof, attn_roof],
             "cpu_baseline": cpu,
@@ -429,6 +443,7 @@ def main():
     ap.add_argument("--r-avg", type=float, default=None)
     ap.add_argument("--seed", type=int, default=20250807)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-quality", action="store_true", help="skip the full-recompute fidelity comparison")
     ap.add_argument("--updates", type=float, default=0.0,
                     help="fraction of dynamic owners updated (refreshed inside the TTFT) before every query")
     ap.add_argument("--memory", choices=["hbm", "host"], default="hbm",

@@ -26,6 +26,7 @@
  *   keep_ratio_schedule        ratio_schedule               include/keep/recompute.hpp:33-70
  *   keep_layer_budget          layer_budget                 include/keep/recompute.hpp:73-77
  *   keep_logits                Model::logits                include/keep/model.hpp:76-85
+ *   keep_divergence            divergence                   include/keep/prefill.hpp:501-531
  *
  * Threading: a context is single-threaded and stateful like the cursor and
  * the cache manager it replaces; distinct contexts may be
@@ -216,6 +217,9 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query,
                    keep_plan_result* out);
 
 int keep_logits(void* ctx, const float* row, double* out);
+/* divergence (prefill.hpp:501-531): L2 of two final rows and the symmetric
+ * KL of their softmaxed logits (fp64, the reference's formula). */
+int keep_divergence(void* ctx, const float* row_a, const float* row_b, double* l2, double* sym_kl);
 
 /* ---- K10 loader trace: the realised (layer, owner) load schedule of the
  * last prefill over pinned-host owners, for the reference's timeline rules

@@ -142,6 +142,7 @@ def load_library() -> C.CDLL:
         "keep_plan_keep": (C.c_int, [vp, C.POINTER(keep_layout), i32p, i32, dp, i32,
                                      C.POINTER(keep_plan_result)]),
         "keep_logits": (C.c_int, [vp, fp, dp]),
+        "keep_divergence": (C.c_int, [vp, fp, fp, dp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
         "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
         "keep_loader_trace": (C.c_int, [vp, C.POINTER(keep_load_record), i32, i32p]),
@@ -318,6 +319,14 @@ class Context:
         out = np.empty(self.V, np.float64)
         _check(self.lib.keep_logits(self._h, _p(row, C.c_float), _p(out, C.c_double)))
         return out
+
+    def divergence(self, row_a, row_b):
+        """divergence (prefill.hpp:501-531) on the device: (L2, symmetric KL)."""
+        a = np.ascontiguousarray(row_a, np.float32)
+        b = np.ascontiguousarray(row_b, np.float32)
+        l2, kl = C.c_double(), C.c_double()
+        _check(self.lib.keep_divergence(self._h, _p(a, C.c_float), _p(b, C.c_float), C.byref(l2), C.byref(kl)))
+        return l2.value, kl.value
 
     # -- per-phase device timing --------------------------------------------
     def profile_enable(self, on=True):

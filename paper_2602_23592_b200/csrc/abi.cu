@@ -1511,6 +1511,28 @@ int keep_logits(void* ctx, const float* row, double* out) {
     });
 }
 
+int keep_divergence(void* ctx, const float* row_a, const float* row_b, double* l2, double* sym_kl) {
+    return guard([&] {  // prefill.hpp:501-531
+        Context& c = *C(ctx);
+        need_weights(c);
+        DevBuf rows, lg, out;
+        rows.ensure(sizeof(float) * 2 * c.d);
+        lg.ensure(sizeof(double) * 2 * size_t(c.V));
+        out.ensure(sizeof(double) * 2);
+        float* ra = rows.as<float>();
+        KEEP_CUDA(cudaMemcpyAsync(ra, row_a, sizeof(float) * c.d, cudaMemcpyHostToDevice, c.s_main));
+        KEEP_CUDA(cudaMemcpyAsync(ra + c.d, row_b, sizeof(float) * c.d, cudaMemcpyHostToDevice, c.s_main));
+        launch_logits(ra, c.unembed.as<float>(), c.d, c.V, lg.as<double>(), c.s_main);
+        launch_logits(ra + c.d, c.unembed.as<float>(), c.d, c.V, lg.as<double>() + c.V, c.s_main);
+        launch_divergence(ra, ra + c.d, c.d, lg.as<double>(), lg.as<double>() + c.V, c.V, out.as<double>(), c.s_main);
+        double h[2];
+        KEEP_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, c.s_main));
+        KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+        *l2 = h[0];
+        *sym_kl = h[1];
+    });
+}
+
 // plan_keep (recompute.hpp:140-180) with every layer, the selection and the
 // last-row logits on the device.  The host only decides keep-all vs walk from
 // the budget and applies the returned order (one small D2H per layer).

@@ -472,6 +472,73 @@ __global__ void logits_kernel(const float* __restrict__ row, const float* __rest
     out[j] = acc;
 }
 
+// divergence (prefill.hpp:501-531): L2 of the row difference and the
+// symmetric KL of softmax(logits_a) vs softmax(logits_b), fp64 throughout,
+// the reference's formula per element (log of an underflowed p is -inf and
+// propagates exactly as there).  One CTA; block reductions in fixed order.
+__device__ double block_reduce_d(double v, double* sh, bool is_max) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? fmax(v, w) : v + w;
+    }
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        v = lane < int(blockDim.x >> 5) ? sh[lane] : (is_max ? -INFINITY : 0.0);
+        for (int o = 16; o > 0; o >>= 1) {
+            const double w = __shfl_xor_sync(0xffffffffu, v, o);
+            v = is_max ? fmax(v, w) : v + w;
+        }
+        if (lane == 0) sh[32] = v;
+    }
+    __syncthreads();
+    return sh[32];
+}
+
+__global__ void __launch_bounds__(1024) divergence_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                                          int d, const double* __restrict__ la,
+                                                          const double* __restrict__ lb, int V, double* __restrict__ out) {
+    __shared__ double sh[33];
+    double acc = 0.0;
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        const double delta = double(a[j]) - double(b[j]);
+        acc += delta * delta;
+    }
+    const double l2 = sqrt(block_reduce_d(acc, sh, false));
+    double ma = -INFINITY, mb = -INFINITY;
+    for (int j = threadIdx.x; j < V; j += blockDim.x) {
+        ma = fmax(ma, la[j]);
+        mb = fmax(mb, lb[j]);
+    }
+    ma = block_reduce_d(ma, sh, true);
+    mb = block_reduce_d(mb, sh, true);
+    double sa = 0.0, sb = 0.0;
+    for (int j = threadIdx.x; j < V; j += blockDim.x) {
+        sa += exp(la[j] - ma);
+        sb += exp(lb[j] - mb);
+    }
+    sa = block_reduce_d(sa, sh, false);
+    sb = block_reduce_d(sb, sh, false);
+    double kl = 0.0;
+    for (int j = threadIdx.x; j < V; j += blockDim.x) {
+        const double p = exp(la[j] - ma) / sa, q = exp(lb[j] - mb) / sb;
+        kl += (p - q) * (log(p) - log(q));
+    }
+    kl = block_reduce_d(kl, sh, false);
+    if (threadIdx.x == 0) {
+        out[0] = l2;
+        out[1] = kl;
+    }
+}
+
+void launch_divergence(const float* a, const float* b, int d, const double* la, const double* lb, int V, double* out,
+                       cudaStream_t st) {
+    divergence_kernel<<<1, 1024, 0, st>>>(a, b, d, la, lb, V, out);
+    KEEP_LAUNCH_CHECK();
+}
+
 void launch_logits(const float* row, const float* unembed, int d, int V, double* out, cudaStream_t st) {
     logits_kernel<<<static_cast<unsigned>(ceil_div(V, 128)), 128, sizeof(float) * d, st>>>(row, unembed, d, V, out);
     KEEP_LAUNCH_CHECK();

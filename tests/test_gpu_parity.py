@@ -237,3 +237,23 @@ def test_determinism(ko, golden, ctx_cache):
     b = ctx.plan_keep(lay, p.query, np.array(c["sched"]), summaries=True)
     assert np.array_equal(a["final_hidden"], b["final_hidden"])
     assert np.array_equal(a["sts"], b["sts"]) and np.array_equal(a["plan"], b["plan"])
+
+
+def test_divergence_matches_reference(ko, golden, ctx_cache):
+    """divergence (prefill.hpp:501-531) on the device against the reference's
+    values for the golden instances (keep vs full prefill, last row)."""
+    checked = 0
+    for c in golden["instances"][::4]:
+        p = problem(ko, c)
+        w = ko.model_init(c["L"], c["H"], c["d"], c["mlp"], c["V"], c["seed"])
+        res = ko.plan_keep(p, w, np.array(c["sched"]), multihop=c["multihop"])
+        full = ko.full_prefill(p, w, kv=False)
+        ctx = gpu_ctx(ctx_cache, c)
+        l2, kl = ctx.divergence(res["final_hidden"][-1], full["final_hidden"][-1])
+        for got, want in ((l2, c["div_l2"]), (kl, c["div_kl"])):
+            if np.isnan(want):
+                assert np.isnan(got)
+            else:
+                assert abs(got - want) <= 1e-9 * max(1.0, abs(want)), (c["seed"], got, want)
+        checked += 1
+    assert checked >= 10
