@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -43,6 +44,17 @@ CONFIGS = {
 METRIC = "memory-prefill TTFT (ms) and recomputed tokens/s, 16K-token memory, 1/2/4/8 B200"
 UNIT = "recomputed tokens/s"
 
+
+
+def _finite(o):
+    """Strict JSON: non-finite floats become null."""
+    if isinstance(o, float) and not math.isfinite(o):
+        return None
+    if isinstance(o, dict):
+        return {k: _finite(v) for k, v in o.items()}
+    if isinstance(o, (list, tuple)):
+        return [_finite(v) for v in o]
+    return o
 
 def peaks():
     try:
@@ -238,7 +250,7 @@ def run_reference(args, cfg):
                        "T": int(seg_len.sum()) + len(query), "plan_model": "budgets fully realised"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": s["kind"], "sample": s["sample"]},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(_finite(line)), flush=True)
 
 
 # ------------------------------------------------------------------ GPU arm --
@@ -382,7 +394,11 @@ def run_ours(args, cfg, rank, world, dist):
         l2, kl = ctx.divergence(keep_res["final_hidden"][-1], full_res["final_hidden"][-1])
         quality = {"full_recompute_ttft_ms": full_res["ttft_ms"], "keep_ttft_ms": keep_res["ttft_ms"],
                    "speedup_vs_full_recompute": full_res["ttft_ms"] / keep_res["ttft_ms"],
-                   "divergence_vs_full": {"l2": l2, "sym_kl": kl},
+                   "divergence_vs_full": {"l2": l2, "sym_kl": kl, "rel_l2": l2 / max(float(np.linalg.norm(
+                       full_res["final_hidden"][-1].astype(np.float64))), 1e-300)},
+                   # (sym_kl is NaN exactly where prefill.hpp:526-528's is: both
+                   # softmaxes underflow to 0 at the same vocabulary entries)
+                   "top1_agree": bool(np.argmax(keep_res["last_logits"]) == np.argmax(full_res["last_logits"])),
                    "full_recomputed_tokens": float(np.sum(full_res["rows_per_layer"]))}
 
     cpu = None
@@ -428,7 +444,7 @@ def run_ours(args, cfg, rank, world, dist):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
-        print(json.dumps(line), flush=True)
+        print(json.dumps(_finite(line)), flush=True)
     ctx.close()
 
 

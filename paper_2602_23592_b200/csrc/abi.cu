@@ -503,6 +503,7 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
         {
             ProfScope ps(c.prof, KEEP_PROF_QKV, st, gq, bq);
             EpiArgs e{EPI_QKV, dl, nullptr, dl, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
+            if (use_tc_attention(c, p)) e.q_scale = float(1.4426950408889634 / std::sqrt(double(c.dh)));
             launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_QKV)), d, n, 3 * dl, d, e, st);
         }
         a.q = p.q.p;

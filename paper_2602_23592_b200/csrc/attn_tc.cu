@@ -1169,7 +1169,13 @@ int launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
     a.rows = L.rows;
     a.row_seg = L.row_seg;
     a.key_lo = L.key_lo;
-    a.scale_log2 = float(1.4426950408889634 / std::sqrt(double(DH)));
+    // q arrives pre-scaled by log2(e)/sqrt(dh) (QKV epilogue, before its bf16
+    // rounding): the scores are already in the exp2 domain, so both passes
+    // subtract the row max from the SAME fp32 value.  Folding the scale into an
+    // fma here instead would make the max element's exponent the rounding
+    // error of s*scale -- up to ulp(m)/2, i.e. 2^30+ once deep-layer logits
+    // reach 1e9 -- and blow p far above 1.
+    a.scale_log2 = 1.f;
     a.inv_heads = float(L.inv_heads);
     a.m_part = L.m_part;
     a.l_part = L.l_part;

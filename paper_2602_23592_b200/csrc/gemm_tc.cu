@@ -99,6 +99,10 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int m, int n, f
         case EPI_QKV: {
             const int d = e.d;
             if (n < d) {
+                if (e.q_scale != 1.f) {
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) v[q] *= e.q_scale;
+                }
                 store_bf16x32(e.out_bf16 + int64_t(m) * d + n, v);
             } else if (n < 2 * d) {
                 store_bf16x32(static_cast<__nv_bfloat16*>(e.kdst) + int64_t(e.rows[m]) * d + (n - d), v);

@@ -74,6 +74,7 @@ struct EpiArgs {
     void* vdst;
     const int32_t* rows;   // QKV scatter rows
     __nv_bfloat16* out_bf16;  // optional bf16 mirror of the written value (FAST)
+    float q_scale = 1.f;      // QKV (FAST): q is stored as bf16(q * q_scale)
 };
 void launch_gemm_f64acc(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
                         const EpiArgs& epi, cudaStream_t st);

@@ -84,3 +84,28 @@ def test_fast_numerics_on_reference_plan(results):
         # summaries stay close in absolute terms (probabilities in [0, 1])
         assert np.max(np.abs(sel["qts"] - ref["qts"])) <= 2e-2
         assert np.max(np.abs(sel["sts"] - ref["sts"])) <= 2e-2
+
+
+def test_fast_deep_layers_stay_finite():
+    """Activations roughly double per layer, so deep-layer attention logits
+    reach 1e9+.  The tensor-core softmax must subtract the row max from the
+    very value it was taken over (q pre-scaled into the exp2 domain), else
+    the max element's exponent is the rounding error of s*scale (up to
+    ulp(m)/2) and p explodes.  FAST must track PARITY to the same relative
+    error at every depth."""
+    from paper_2602_23592_b200.synth import make_instance_layout
+    L, H, d, mlp, V, seed = 40, 2, 256, 512, 512, 20250807
+    inst = make_instance_layout(7, 12, V)
+    lay = kb.Layout(inst.seg_len, inst.tokens)
+    sched = np.ones((L, lay.S), np.uint8)
+    out = {}
+    for mode in (kb.FAST, kb.PARITY):
+        with kb.Context(L, H, d, mlp, V, seed, mode) as ctx:
+            ctx.model_init()
+            ctx.memory_compute_layout(lay)
+            out[mode] = ctx.selective_prefill(lay, inst.query, sched)["kv"]
+    kf, kp = out[kb.FAST].astype(np.float64), out[kb.PARITY].astype(np.float64)
+    assert np.isfinite(kf).all()
+    for l in range(L):
+        scale = np.max(np.abs(kp[l]))
+        assert np.max(np.abs(kf[l] - kp[l])) <= 0.25 * scale, (l, scale)
