@@ -369,6 +369,16 @@ def run_ours(args, cfg, rank, world, dist):
                  "bound": "tensor", "achieved": a_ach, "peak": tensor_peak, "unit": "TFLOP/s",
                  "frac": a_ach / tensor_peak, "traffic": traffic.get("attn_tc2_kernel"), "peak_source": src,
                  "note": "algorithmic FLOPs 4*d*sum(t+1) (QK^T + PV once); the kernel pair does QK^T twice"}
+    d_ms, d_by, d_n = prof["attn_decode"]["ms"], prof["attn_decode"]["bytes"], prof["attn_decode"]["launches"]
+    hbm_peak = pk["hbm_gbs"]
+    d_ach = d_by / (d_ms / 1e3) / 1e9 if d_ms > 0 else 0.0
+    # the layers after the walk: the query rows alone against the whole merged
+    # KV, HBM-bound (algorithmic bytes = K + V of the visible keys once + q + ctx)
+    decode_roof = {"kernel": "attn_decode_kernel (K5d, split-K flash decoding, TMA stages)", "bound": "hbm",
+                   "achieved": d_ach, "peak": hbm_peak, "unit": "GB/s", "frac": d_ach / hbm_peak,
+                   "traffic": traffic.get("attn_decode_kernel"), "peak_source": src,
+                   "per_launch_ms": d_ms / max(d_n, 1), "algorithmic_bytes_per_launch": d_by / max(d_n, 1),
+                   "launches_per_step": d_n / max(args.steps, 1)}
     roof = gemm_roof if g_ms >= a_ms else attn_roof
     launches = int(sum(v["kernels"] for v in prof.values())) // max(args.steps, 1)
     loader_info = None
@@ -440,7 +450,7 @@ def run_ours(args, cfg, rank, world, dist):
             "loader": loader_info,
             "quality": quality,
             "roofline": roof,
-            "roofline_kernels": [gemm_roof, attn_roof],
+            "roofline_kernels": [gemm_roof, attn_roof] + ([decode_roof] if d_ms > 0 else []),
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }

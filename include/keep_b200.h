@@ -254,6 +254,7 @@ enum {
     KEEP_PROF_COMM = 12,    /* KV-head sharding collectives (NCCL)           */
     KEEP_PROF_XCHG = 13,    /* ctx pack / residual bf16 refresh around them  */
     KEEP_PROF_REFRESH = 14, /* canonical-KV refresh of updated owners (whole call) */
+    KEEP_PROF_DECODE = 15,  /* few-row attention without a summary (K5d, flash decoding) */
     KEEP_PROF_COUNT = 16
 };
 typedef struct {

@@ -88,7 +88,7 @@ class keep_load_record(C.Structure):
 LOAD_KINDS = {0: "urgent", 1: "ahead", 2: "preload"}
 
 PROFILE_PHASES = ["qkv", "attn", "wo", "mlp_in", "mlp_out", "summary", "select", "cached_kv", "compact",
-                  "embed", "logits", "loader", "comm", "xchg", "refresh"]
+                  "embed", "logits", "loader", "comm", "xchg", "refresh", "attn_decode"]
 
 
 class keep_plan_result(C.Structure):

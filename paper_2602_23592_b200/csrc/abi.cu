@@ -313,6 +313,17 @@ int small_n_threshold() {
 }
 bool use_tc_attention(const Context& c, const Pass& p) { return use_tc_attention(c) && p.n > small_n_threshold(); }
 
+// Few computed rows and no summary to bin (the layers after the walk):
+// flash decoding (attn_decode.cu).  KEEP_ATTN_DECODE=0 keeps the two-pass
+// tensor-core kernel (A/B).
+bool use_decode_attention(const Context& c, const Pass& p) {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_ATTN_DECODE");
+        return !(e && *e == '0');
+    }();
+    return on && c.fast && c.dh == 128 && !p.with_summary && !p.block_diag && decode_attention_fits(p.n);
+}
+
 void plan_splits(Context& c, Pass& p) {
     const bool tc = use_tc_attention(c, p);
     // the split plan depends only on (n, T, path): layers of equal size reuse
@@ -508,7 +519,29 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
         }
         a.q = p.q.p;
         a.ctx_bf16 = p.ctxb.as<__nv_bfloat16>();
-        if (use_tc_attention(c, p)) {
+        if (use_tc_attention(c, p) && use_decode_attention(c, p)) {
+            // the query rows alone (walk over): HBM-bound single-pass decoding
+            const int kv_hi = p.rows_h.back() + 1;
+            const int ns = decode_splits(c.Hl, kv_hi);
+            p.m_part.ensure(sizeof(float) * size_t(ns) * n * c.Hl);
+            p.l_part.ensure(sizeof(float) * size_t(ns) * n * c.Hl);
+            p.o_part.ensure(sizeof(float) * size_t(ns) * n * dl);
+            ProfScope ps(c.prof, KEEP_PROF_DECODE, st, fa, double(c.elem) * (2.0 * kv_hi * dl + 2.0 * n * dl), 2);
+            AttnTcLaunch t{};
+            t.n = n;
+            t.T = p.T;
+            t.H = c.Hl;
+            t.d = dl;
+            t.q = p.q.p;
+            t.k = p.kdst[l];
+            t.v = p.vdst[l];
+            t.rows = rows;
+            t.m_part = p.m_part.as<float>();
+            t.l_part = p.l_part.as<float>();
+            t.o_part = p.o_part.as<float>();
+            t.ctx = p.ctxb.as<__nv_bfloat16>();
+            ps.kernels = launch_attention_decode(t, kv_hi, st);
+        } else if (use_tc_attention(c, p)) {
             ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, p.split_count_a > 1 ? 6 : 5);
             p.vt.ensure(2 * size_t(dl) * size_t(ceil_div(p.T, 64) * 64));
             AttnTcLaunch t{};
@@ -1381,6 +1414,7 @@ int keep_prefill_layer(void* ctx, const uint8_t* active, double* summary_out) {
     return guard([&] {
         Context& c = *C(ctx);
         if (!c.pf) raise(KEEP_ERR_PLAN, "no prefill in progress");
+        c.pf->summary_wanted = summary_out != nullptr;  // (nobody reads it otherwise)
         cursor_layer(c, active);
         if (summary_out) {
             const size_t ns = size_t(c.pf->S) + size_t(c.pf->S) * c.pf->S;

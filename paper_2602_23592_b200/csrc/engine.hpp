@@ -45,6 +45,12 @@ struct AttnTcLaunch {
     int nb;                   // summary bins per chunk on the tensor core (16 / 32; 0 = scan bins)
 };
 int launch_attention_tc(const AttnTcLaunch& a, cudaStream_t st);  // returns kernels launched
+// few-row layers without a summary (attn_decode.cu): single-pass split-K
+// flash decoding over keys [0, kv_hi); uses q, k, v, rows, m_part, l_part,
+// o_part (fp32, sized decode_splits x n x {H, d}) and ctx of the launch
+bool decode_attention_fits(int n);
+int decode_splits(int n_heads, int kv_hi);
+int launch_attention_decode(const AttnTcLaunch& a, int kv_hi, cudaStream_t st);
 // per-128-key-chunk destination-segment table (32 B per chunk)
 void launch_chunk_table(const int32_t* row_seg, int T, void* tab, cudaStream_t st);
 // bins width for a layout (max segments touching a 128-key chunk, rounded to

@@ -330,6 +330,138 @@ __global__ void splitk_epilogue_kernel(float* __restrict__ acc, int M, int N, Ep
     }
 }
 
+// ------------------------------------------------------------ skinny GEMM --
+// M <= 16 rows (the layers after the walk compute only the query rows): the
+// GEMM is a weight stream, HBM-bound at 2*N*K bytes.  Persistent CTAs walk a
+// contiguous range of (64-row n-block, 256-wide k-stage) units; a producer warp
+// TMA-loads each stage (B: four 64x64 boxes, A: four 16x64 boxes, 40 KB) into
+// a 4-deep ring and four consumer warps each multiply one 64-wide k slice on
+// mma.sync m16n8k16 (the MMA is never the bound at 16 rows).  Partial sums
+// go to the fp32 split-K workspace with vector reductions whenever a CTA
+// leaves an n-block; splitk_epilogue_kernel applies the fused epilogue.
+constexpr int SK_ST = 4;
+constexpr int SK_BOXB = 64 * 64 * 2;             // B box: 64 n x 64 k
+constexpr int SK_BOXA = 16 * 64 * 2;             // A box: 16 rows x 64 k
+constexpr int SK_STAGE = 4 * SK_BOXB + 4 * SK_BOXA;
+constexpr int SK_SMEM = 1024 + SK_ST * SK_STAGE + 2 * SK_ST * 8;
+constexpr int SK_THREADS = 5 * 32;
+
+__global__ void __launch_bounds__(SK_THREADS, 1)
+gemm_skinny_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int N,
+                   int K, float* __restrict__ acc) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + SK_ST * SK_STAGE);
+    uint64_t* empty = full + SK_ST;
+    const int nb_count = int(ceil_div(N, 64)), ks_count = int(ceil_div(K, 256));
+    const int64_t units = int64_t(nb_count) * ks_count;
+    const int64_t u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < SK_ST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 4);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == 4) {
+        if (lane == 0) {
+            prefetch_map(&ta);
+            prefetch_map(&tb);
+            for (int64_t u = u0; u < u1; ++u) {
+                const int j = int(u - u0), s = j % SK_ST;
+                if (j >= SK_ST) mbar_wait(&empty[s], uint32_t(j / SK_ST - 1) & 1u);
+                mbar_expect_tx(&full[s], SK_STAGE);
+                const int nb = int(u / ks_count), k0 = int(u % ks_count) * 256;
+                uint8_t* st = sm + s * SK_STAGE;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    tma_load_2d(st + q * SK_BOXB, &tb, &full[s], k0 + 64 * q, nb * 64);
+                    tma_load_2d(st + 4 * SK_BOXB + q * SK_BOXA, &ta, &full[s], k0 + 64 * q, 0);
+                }
+            }
+        }
+        return;
+    }
+    const int g = lane >> 2, i4 = lane & 3, mat = lane >> 3;
+    float c[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
+    int cur_nb = -1;
+    auto flush = [&](int nb) {
+        const int r0 = g, r1 = g + 8;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+            const int col = nb * 64 + nt * 8 + 2 * i4;
+            if (col < N) {
+                if (r0 < M) atomicAdd(reinterpret_cast<float2*>(acc + int64_t(r0) * N + col), make_float2(c[nt][0], c[nt][1]));
+                if (r1 < M) atomicAdd(reinterpret_cast<float2*>(acc + int64_t(r1) * N + col), make_float2(c[nt][2], c[nt][3]));
+            }
+            c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
+        }
+    };
+    for (int64_t u = u0; u < u1; ++u) {
+        const int j = int(u - u0), s = j % SK_ST;
+        const int nb = int(u / ks_count);
+        if (nb != cur_nb) {
+            if (cur_nb >= 0) flush(cur_nb);
+            cur_nb = nb;
+        }
+        mbar_wait(&full[s], uint32_t(j / SK_ST) & 1u);
+        const uint32_t sb = smem_u32(sm + s * SK_STAGE);
+        const uint32_t bb = sb + warp * SK_BOXB, ab = sb + 4 * SK_BOXB + warp * SK_BOXA;
+#pragma unroll
+        for (int kp = 0; kp < 2; ++kp) {  // two k-steps of 16 per pass
+            uint32_t a0[4], a1[4];
+            // A (m16 x k16): matrices (rows 0-7, k 0-7), (rows 8-15, k 0-7), (rows 0-7, k 8-15), (rows 8-15, k 8-15)
+            ldsm_x4(ab + swz(((mat & 1) << 3) + (lane & 7), kp * 4 + (mat >> 1)), a0[0], a0[1], a0[2], a0[3]);
+            ldsm_x4(ab + swz(((mat & 1) << 3) + (lane & 7), kp * 4 + 2 + (mat >> 1)), a1[0], a1[1], a1[2], a1[3]);
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4(bb + swz(nt * 8 + (lane & 7), kp * 4 + mat), b0, b1, b2, b3);
+                mma16816(c[nt], a0, b0, b1);
+                mma16816(c[nt], a1, b2, b3);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (cur_nb >= 0) flush(cur_nb);
+}
+
+float* splitk_workspace(int M, int N, cudaStream_t st) {
+    // per-thread grow-only fp32 workspace (one context per host thread)
+    // (zeroed once when it grows; every finalisation pass re-zeroes what it read)
+    thread_local DevBuf ws;
+    const size_t need = sizeof(float) * size_t(M) * N;
+    if (need > ws.bytes || !ws.p) {
+        ws.ensure(need);
+        KEEP_CUDA(cudaMemsetAsync(ws.p, 0, ws.bytes, st));
+    }
+    return ws.as<float>();
+}
+
+void launch_skinny(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
+                   const EpiArgs& epi, cudaStream_t st, int max_ctas) {
+    static bool attr = [] {
+        KEEP_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_SMEM));
+        return true;
+    }();
+    (void)attr;
+    const CUtensorMap ta = make_map_bf16(A, M, K, lda, 16);
+    const CUtensorMap tb = make_map_bf16(Bt, N, K, ldb, 64);
+    const int64_t units = ceil_div(N, 64) * ceil_div(K, 256);
+    const int grid = int(std::min<int64_t>(units, std::max(1, std::min(max_ctas, kNumSMs))));
+    float* acc = splitk_workspace(M, N, st);
+    gemm_skinny_kernel<<<grid, SK_THREADS, SK_SMEM, st>>>(ta, tb, M, N, K, acc);
+    KEEP_LAUNCH_CHECK();
+    const int work = M * (N / 32);
+    splitk_epilogue_kernel<<<unsigned(std::min<int64_t>(ceil_div(work, 128), kNumSMs * 4)), 128, 0, st>>>(acc, M, N, epi);
+    KEEP_LAUNCH_CHECK();
+}
+
 template <int BN, int AR = BM>
 void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
                const EpiArgs& epi, cudaStream_t st, int max_ctas = kNumSMs, int ksplit = 1) {
@@ -345,18 +477,7 @@ void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int
     const CUtensorMap tb = make_map_bf16(Bt, N, K, ldb, BN);
     const int ntiles = int(ceil_div(M, BM) * ceil_div(N, BN)) * ksplit;
     const int grid = std::min(ntiles, std::max(1, std::min(max_ctas, kNumSMs)));
-    float* acc = nullptr;
-    if (ksplit > 1) {
-        // per-thread grow-only fp32 workspace (one context per host thread)
-        // (zeroed once when it grows; every finalisation pass re-zeroes what it read)
-        thread_local DevBuf ws;
-        const size_t need = sizeof(float) * size_t(M) * N;
-        if (need > ws.bytes || !ws.p) {
-            ws.ensure(need);
-            KEEP_CUDA(cudaMemsetAsync(ws.p, 0, ws.bytes, st));
-        }
-        acc = ws.as<float>();
-    }
+    float* acc = ksplit > 1 ? splitk_workspace(M, N, st) : nullptr;
     gemm_tc_kernel<BN, AR><<<grid, kThreads, CF::SMEM, st>>>(ta, tb, M, N, K, epi, ksplit, acc);
     KEEP_LAUNCH_CHECK();
     if (ksplit > 1) {
@@ -369,12 +490,24 @@ void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int
 
 }  // namespace
 
+bool skinny_enabled() {  // KEEP_GEMM_SKINNY=0: the tcgen05 split-K path for M <= 16 too (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_GEMM_SKINNY");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
                       const EpiArgs& epi, cudaStream_t st, int max_ctas) {
     if (M == 0 || N == 0) return;
     if (K % BK != 0 || N % 32 != 0) raise(KEEP_ERR_CONFIG, "tcgen05 GEMM needs K % 64 == 0 and N % 32 == 0");
     // a few rows (deep layers: the query): 32-row A stages and split-K so that
     // ~4 waves of (tile, k-slice) units stream the weights through every SM
+    if (M <= 16 && skinny_enabled()) {
+        launch_skinny(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas);
+        return;
+    }
     if (M <= 32) {
         const int tiles = int(ceil_div(N, 64)), kb = K / BK;
         const int ksplit = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(4 * kNumSMs, tiles), kb / 8)));
@@ -394,13 +527,17 @@ void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* 
 extern "C" int keep_debug_gemm_bf16(const void* A, const void* Bt, float* Cout,
                                                                            int M, int N, int K, int force_bn) {
     try {
+        const bool sync = force_bn < 1000;  // force_bn + 1000: asynchronous (microbenchmarks)
+        force_bn %= 1000;
         keep_b200::EpiArgs e{keep_b200::EPI_STORE, 0, Cout, N, nullptr, nullptr, nullptr, nullptr};
         auto a = static_cast<const __nv_bfloat16*>(A);
         auto b = static_cast<const __nv_bfloat16*>(Bt);
         if (force_bn == 256) keep_b200::launch_bn<256>(a, K, b, K, M, N, K, e, 0);
         else if (force_bn == 64) keep_b200::launch_bn<64>(a, K, b, K, M, N, K, e, 0);
         else if (force_bn == 32) keep_b200::launch_bn<32, 32>(a, K, b, K, M, N, K, e, 0);
+        else if (force_bn == 16) keep_b200::launch_skinny(a, K, b, K, M, N, K, e, 0, keep_b200::kNumSMs);
         else keep_b200::launch_gemm_bf16(a, K, b, K, M, N, K, e, 0);
+        if (!sync) return cudaGetLastError() == cudaSuccess ? 0 : KEEP_ERR_CUDA;
         return cudaDeviceSynchronize() == cudaSuccess ? 0 : KEEP_ERR_CUDA;
     } catch (const keep_b200::KeepError& e) {
         return e.code;

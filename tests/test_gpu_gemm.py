@@ -13,6 +13,9 @@ pytestmark = pytest.mark.gpu
     (2049, 1024, 1024, 256),
     # small-M path (deep layers): 32-row A stages, 32-wide N tiles
     (8, 5120, 5120, 32), (1, 32, 64, 32), (32, 13824, 5120, 32), (8, 5120, 13824, 0), (9, 15360, 5120, 0),
+    # skinny weight-stream path (M <= 16, mma.sync over TMA stages): ragged K stages / n-blocks
+    (8, 5120, 5120, 16), (1, 32, 64, 16), (16, 13824, 5120, 16), (5, 1920, 5120, 16), (3, 96, 320, 16),
+    (16, 5120, 13824, 16),
 ])
 def test_gemm_bf16_tcgen05(M, N, K, bn):
     import torch
