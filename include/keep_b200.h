@@ -216,6 +216,25 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query,
                    int32_t query_len, const double* schedule, int32_t multihop,
                    keep_plan_result* out);
 
+/* ---- batched multi-query prefill ----------------------
+ * B planning queries over one memory layout, each with its own plan and
+ * result exactly as keep_plan_keep(layout, queries[b]) would produce
+ * (PARITY: bit-identical).  Shared work: layer 0's memory rows are computed
+ * once (plan[0] is every segment for every query, and memory rows precede
+ * the query); the projections of all instances run as one GEMM per layer;
+ * all-reused layers of any instance read the in-order arena in place; the
+ * first-token logits of all instances stream the unembedding once.
+ * queries: [B x query_len]; outs: [B] (ttft_ms = the whole batch's device
+ * time; layer_ms per layer of the batch).  One GPU (G = 1), HBM-resident
+ * memory. */
+int keep_plan_keep_batch(void* ctx, const keep_layout* layout, int32_t batch, const int32_t* queries,
+                         int32_t query_len, const double* schedule, int32_t multihop, keep_plan_result* outs);
+/* The same batch with given monotone plans [batch x L x S] (every segment at
+ * layer 0) instead of the walks: selective_prefill (prefill.hpp:478-497) per
+ * query. */
+int keep_selective_prefill_batch(void* ctx, const keep_layout* layout, int32_t batch, const int32_t* queries,
+                                 int32_t query_len, const uint8_t* plans, keep_plan_result* outs);
+
 int keep_logits(void* ctx, const float* row, double* out);
 /* divergence (prefill.hpp:501-531): L2 of two final rows and the symmetric
  * KL of their softmaxed logits (fp64, the reference's formula). */

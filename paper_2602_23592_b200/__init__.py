@@ -141,6 +141,10 @@ def load_library() -> C.CDLL:
         "keep_layer_budget": (i64, [C.c_double, i64]),
         "keep_plan_keep": (C.c_int, [vp, C.POINTER(keep_layout), i32p, i32, dp, i32,
                                      C.POINTER(keep_plan_result)]),
+        "keep_plan_keep_batch": (C.c_int, [vp, C.POINTER(keep_layout), i32, i32p, i32, dp, i32,
+                                           C.POINTER(keep_plan_result)]),
+        "keep_selective_prefill_batch": (C.c_int, [vp, C.POINTER(keep_layout), i32, i32p, i32, u8p,
+                                                   C.POINTER(keep_plan_result)]),
         "keep_logits": (C.c_int, [vp, fp, dp]),
         "keep_divergence": (C.c_int, [vp, fp, fp, dp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
@@ -501,3 +505,46 @@ class Context:
             out["qts"] = summ[:, :S].copy()
             out["sts"] = summ[:, S:].reshape(L, S, S).copy()
         return out
+
+    def plan_keep_batch(self, layout: Layout, queries, sched, multihop=True, final_hidden=False, summaries=False,
+                        plans=None):
+        """keep_plan_keep_batch: B planning queries (rows of `queries`, equal
+        lengths) over one memory layout; one result dict per query, as
+        plan_keep returns it (ttft_ms / layer_ms are the batch's)."""
+        Q = np.ascontiguousarray(np.atleast_2d(queries), np.int32)
+        B, qlen = Q.shape
+        L, S = self.L, layout.S
+        T = int(np.sum(layout.seg_len)) + qlen
+        bufs, res = [], (keep_plan_result * B)()
+        for b in range(B):
+            f = {"plan": np.empty((L, S), np.uint8), "orders": np.full((L, S), -1, np.int32),
+                 "olen": np.empty(L, np.int32), "hops": np.empty(L, np.int32),
+                 "summ": np.empty((L, S + S * S), np.float64) if summaries else None,
+                 "fh": np.empty((T, self.d), np.float32) if final_hidden else None,
+                 "logits": np.empty(self.V, np.float64), "rows": np.empty(L, np.int64), "lms": np.empty(L, np.float64)}
+            bufs.append(f)
+            res[b] = keep_plan_result(_p(f["plan"], C.c_uint8), _p(f["orders"], C.c_int32), _p(f["olen"], C.c_int32),
+                                      _p(f["hops"], C.c_int32), _p(f["summ"], C.c_double), _p(f["fh"], C.c_float),
+                                      _p(f["logits"], C.c_double), _p(f["rows"], C.c_int64), _p(f["lms"], C.c_double),
+                                      0.0)
+        lay = layout.c_struct()
+        if plans is not None:  # keep_selective_prefill_batch
+            pl = np.ascontiguousarray(plans, np.uint8).reshape(B, L, S)
+            _check(self.lib.keep_selective_prefill_batch(self._h, C.byref(lay), B, _p(Q, C.c_int32), qlen,
+                                                         _p(pl, C.c_uint8), res))
+        else:
+            sched = np.ascontiguousarray(sched, np.float64)
+            _check(self.lib.keep_plan_keep_batch(self._h, C.byref(lay), B, _p(Q, C.c_int32), qlen,
+                                                 _p(sched, C.c_double), int(bool(multihop)), res))
+        outs = []
+        for b, f in enumerate(bufs):
+            o = {"plan": f["plan"], "hops": f["hops"],
+                 "orders": [None if f["olen"][l] < 0 else [int(x) for x in f["orders"][l, : f["olen"][l]]]
+                            for l in range(L)],
+                 "final_hidden": f["fh"], "last_logits": f["logits"], "rows_per_layer": f["rows"],
+                 "layer_ms": f["lms"], "ttft_ms": res[b].ttft_ms}
+            if summaries:
+                o["qts"] = f["summ"][:, :S].copy()
+                o["sts"] = f["summ"][:, S:].reshape(L, S, S).copy()
+            outs.append(o)
+        return outs

@@ -425,6 +425,10 @@ void ensure_layer_scratch(Context& c, Pass& p) {
         p.xrecv.ensure(es * cpr * c.G * c.dl);
         p.xrows.ensure(es * cpr * c.d);
     }
+}
+
+void ensure_attn_scratch(Context& c, Pass& p) {
+    const size_t n = size_t(std::max(p.n, 1));
     if (p.with_summary && !use_tc_attention(c, p)) p.rowbin.ensure((c.fast ? 4 : 8) * n * std::max(p.S, 1));
 }
 
@@ -436,9 +440,12 @@ double visible_pairs(const Pass& p) {
 }
 
 // One transformer layer over the compact rows of a pass
-// (PrefillCursor::step body, prefill.hpp:245-304 minus the cached copy).
-// after_summary runs once the layer's segment summary is complete (the
-// selector for layer l+1 overlaps this layer's Wo + MLP; SPEC D2).
+// (PrefillCursor::step body, prefill.hpp:245-304 minus the cached copy), in
+// three phases so that a batch of queries can share the projections and run
+// attention per query: layer_qkv (K3), layer_attention (K5 + K6),
+// layer_dense (K8 + K9, with the sharded exchanges around them).
+// run_layer's after_summary runs once the layer's segment summary is complete
+// (the selector for layer l+1 overlaps this layer's Wo + MLP; SPEC D2).
 //
 // KV-head sharding (G > 1): QKV and attention run for this
 // rank's heads over all compact rows (q/k/v/ctx are dl = d/G columns wide,
@@ -447,12 +454,35 @@ double visible_pairs(const Pass& p) {
 // ctx goes head-sharded -> row-sharded by all-to-all; Wo + MLP run with the
 // full weights on this rank's block of rows (every k-reduction stays on one
 // GPU, as on a single GPU); the fp32 residual rows are all-gathered.
-template <class AfterSummary>
-void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
-    const int n = p.n, d = c.d, f = c.f, dl = c.dl;
+void layer_qkv(Context& c, Pass& p, int l) {
+    const int n = p.n, d = c.d, dl = c.dl;
     cudaStream_t st = c.s_main;
-    if (n == 0) return;
-    ensure_layer_scratch(c, p);
+    const int32_t* rows = p.d_rows.as<int32_t>();
+    const double wb = c.fast ? 2.0 : 4.0;
+    const double gq = 2.0 * n * 3.0 * dl * d;
+    const double bq = wb * (3.0 * dl * d + n * double(d)) + c.elem * 3.0 * n * dl;
+    ProfScope ps(c.prof, KEEP_PROF_QKV, st, gq, bq);
+    if (!c.fast) {
+        EpiArgs e{EPI_QKV, dl, p.q.as<float>(), dl, p.kdst[l], p.vdst[l], rows, nullptr};
+        launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * dl, n, 3 * dl, d, e,
+                           st);
+    } else {
+        EpiArgs e{EPI_QKV, dl, nullptr, dl, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
+        if (use_tc_attention(c, p)) e.q_scale = float(1.4426950408889634 / std::sqrt(double(c.dh)));
+        launch_gemm_bf16(p.xb.as<__nv_bfloat16>(), d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_QKV)), d, n,
+                         3 * dl, d, e, st);
+    }
+}
+
+// Attention of the pass's compact rows against a [p.T x dl] merged KV (k, v;
+// p.rows are positions in it), q / ctx given explicitly: a batch runs one
+// query instance at a time on slices of its shared buffers.  With a summary
+// the normalised AttentionSummary lands in p.summ.
+void layer_attention(Context& c, Pass& p, int l, const void* q, void* ctx, const void* k, const void* v) {
+    const int n = p.n, dl = c.dl;
+    cudaStream_t st = c.s_main;
+    (void)l;
+    ensure_attn_scratch(c, p);
     plan_splits(c, p);
     const int32_t* rows = p.d_rows.as<int32_t>();
     AttnArgs a{};
@@ -462,8 +492,8 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
     a.dh = c.dh;
     a.d = dl;
     a.inv_heads = 1.0 / c.H;
-    a.k = p.kdst[l];
-    a.v = p.vdst[l];
+    a.k = k;
+    a.v = v;
     a.rows = rows;
     a.row_seg = p.d_row_seg.as<int32_t>();
     a.key_lo = p.block_diag ? p.d_key_lo.as<int32_t>() : nullptr;
@@ -480,45 +510,19 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
     a.o_part = p.o_part.as<double>();
     a.rowbin = p.rowbin.p;
 
-    // this rank's block of compact rows for Wo + MLP
-    const int G = c.G;
-    const int cpr = int(ceil_div(n, G));
-    const int r0 = std::min(n, c.R * cpr);
-    const int m = std::min(n, r0 + cpr) - r0;
-
-    const double wb = c.fast ? 2.0 : 4.0;  // weight / activation element bytes
-    const double gq = 2.0 * n * 3.0 * dl * d, go = 2.0 * m * double(d) * d, gi = 2.0 * m * double(d) * f;
-    const double bq = wb * (3.0 * dl * d + n * double(d)) + c.elem * 3.0 * n * dl;
-    const double bo = wb * (double(d) * d + m * double(d)) + 8.0 * m * d;
-    const double bi = wb * (double(d) * f + m * double(d) + m * double(f));
-    const double bout = wb * (double(d) * f + m * double(f)) + 8.0 * m * d;
     const double pairs = visible_pairs(p);
     // algorithmic attention: QK^T and PV over visible keys; K+V of the layer read once
     const double fa = 4.0 * dl * pairs, ba = double(c.elem) * (2.0 * p.T * dl + 2.0 * n * dl);
-
     if (!c.fast) {
-        {
-            ProfScope ps(c.prof, KEEP_PROF_QKV, st, gq, bq);
-            EpiArgs e{EPI_QKV, dl, p.q.as<float>(), dl, p.kdst[l], p.vdst[l], rows, nullptr};
-            launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * dl, n, 3 * dl, d, e,
-                               st);
-        }
-        a.q = p.q.p;
-        a.ctx = p.ctx.as<float>();
+        a.q = q;
+        a.ctx = static_cast<float*>(ctx);
         {
             ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, 5);
             launch_attention_parity(a, st);
         }
     } else {
-        auto* xb = p.xb.as<__nv_bfloat16>();
-        {
-            ProfScope ps(c.prof, KEEP_PROF_QKV, st, gq, bq);
-            EpiArgs e{EPI_QKV, dl, nullptr, dl, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
-            if (use_tc_attention(c, p)) e.q_scale = float(1.4426950408889634 / std::sqrt(double(c.dh)));
-            launch_gemm_bf16(xb, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_QKV)), d, n, 3 * dl, d, e, st);
-        }
-        a.q = p.q.p;
-        a.ctx_bf16 = p.ctxb.as<__nv_bfloat16>();
+        a.q = q;
+        a.ctx_bf16 = static_cast<__nv_bfloat16*>(ctx);
         if (use_tc_attention(c, p) && use_decode_attention(c, p)) {
             // the query rows alone (walk over): HBM-bound single-pass decoding
             const int kv_hi = p.rows_h.back() + 1;
@@ -532,14 +536,14 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
             t.T = p.T;
             t.H = c.Hl;
             t.d = dl;
-            t.q = p.q.p;
-            t.k = p.kdst[l];
-            t.v = p.vdst[l];
+            t.q = q;
+            t.k = k;
+            t.v = v;
             t.rows = rows;
             t.m_part = p.m_part.as<float>();
             t.l_part = p.l_part.as<float>();
             t.o_part = p.o_part.as<float>();
-            t.ctx = p.ctxb.as<__nv_bfloat16>();
+            t.ctx = static_cast<__nv_bfloat16*>(ctx);
             ps.kernels = launch_attention_decode(t, kv_hi, st);
         } else if (use_tc_attention(c, p)) {
             ProfScope ps(c.prof, KEEP_PROF_ATTN, st, fa, ba, p.split_count_a > 1 ? 6 : 5);
@@ -551,9 +555,9 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
             t.d = dl;
             t.S = p.S;
             t.inv_heads = 1.0 / c.H;
-            t.q = p.q.p;
-            t.k = p.kdst[l];
-            t.v = p.vdst[l];
+            t.q = q;
+            t.k = k;
+            t.v = v;
             t.vt = p.vt.as<__nv_bfloat16>();
             t.rows = rows;
             t.row_seg = p.d_row_seg.as<int32_t>();
@@ -567,7 +571,7 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
             t.m_fin = p.m_fin.as<float>();
             t.inv_l = p.l_fin.as<float>();
             t.o_part = p.o_part.as<float>();
-            t.ctx = p.ctxb.as<__nv_bfloat16>();
+            t.ctx = static_cast<__nv_bfloat16*>(ctx);
             if (p.with_summary) {
                 const size_t ns = size_t(p.S) + size_t(p.S) * p.S;
                 p.summ_raw.ensure(sizeof(double) * ns);
@@ -614,14 +618,21 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
             launch_summary_reduce<float>(p.rowbin.as<float>(), p.S, p.seg_cbeg.as<int32_t>(), p.seg_cend.as<int32_t>(),
                                          p.d_seg_len.as<int32_t>(), qb, qe, p.qlen, p.summ.as<double>(), st);
     }
-    if (G > 1 && p.with_summary && p.summary_global) {
-        // per-rank partials (sum over this rank's heads of p / H) -> the summary
-        const size_t ns = size_t(p.S) + size_t(p.S) * p.S;
-        ProfScope ps(c.prof, KEEP_PROF_COMM, st, 0.0, 8.0 * ns * 2.0 * (G - 1) / G, 2);
-        c.comm->allreduce_f64(p.summ.as<double>(), ns, st);
-    }
-    after_summary();
+}
 
+void layer_dense(Context& c, Pass& p, int l) {
+    const int n = p.n, d = c.d, f = c.f, dl = c.dl;
+    cudaStream_t st = c.s_main;
+    const int G = c.G;
+    const int cpr = int(ceil_div(n, G));
+    const int r0 = std::min(n, c.R * cpr);
+    const int m = std::min(n, r0 + cpr) - r0;
+    const double wb = c.fast ? 2.0 : 4.0;  // weight / activation element bytes
+    const double go = 2.0 * m * double(d) * d, gi = 2.0 * m * double(d) * f;
+    const double bo = wb * (double(d) * d + m * double(d)) + 8.0 * m * d;
+    const double bi = wb * (double(d) * f + m * double(d) + m * double(f));
+    const double bout = wb * (double(d) * f + m * double(f)) + 8.0 * m * d;
+    (void)dl;
     // attention context for the Wo + MLP rows of this rank
     const int es = c.fast ? 2 : 4;
     const void* ctx_rows = c.fast ? static_cast<const void*>(p.ctxb.p) : static_cast<const void*>(p.ctx.p);
@@ -685,6 +696,22 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
     }
 }
 
+template <class AfterSummary>
+void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
+    if (p.n == 0) return;
+    ensure_layer_scratch(c, p);
+    layer_qkv(c, p, l);
+    layer_attention(c, p, l, p.q.p, c.fast ? p.ctxb.p : p.ctx.p, p.kdst[l], p.vdst[l]);
+    if (c.G > 1 && p.with_summary && p.summary_global) {
+        // per-rank partials (sum over this rank's heads of p / H) -> the summary
+        const size_t ns = size_t(p.S) + size_t(p.S) * p.S;
+        ProfScope ps(c.prof, KEEP_PROF_COMM, c.s_main, 0.0, 8.0 * ns * 2.0 * (c.G - 1) / c.G, 2);
+        c.comm->allreduce_f64(p.summ.as<double>(), ns, c.s_main);
+    }
+    after_summary();
+    layer_dense(c, p, l);
+}
+
 void run_layer(Context& c, Pass& p, int l) {
     run_layer(c, p, l, [] {});
 }
@@ -726,10 +753,9 @@ void set_rows(Context& c, Pass& p, const std::vector<int32_t>& rows_new, bool fi
     upload(p.d_rows, p.rows_h, st);
 }
 
-// Build a pass over a token sequence.  seg_len partitions the memory rows;
-// query rows follow.
-void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const int32_t* tokens,
-               const int32_t* query, int qlen) {
+// The layout side of a pass: segment offsets, key -> segment map and the
+// attention's per-chunk segment tables (no rows, no hidden states).
+void pass_layout(Context& c, Pass& p, const std::vector<int32_t>& seg_len, int qlen) {
     p.S = int(seg_len.size());
     p.seg_len = seg_len;
     p.split_key = -1;  // new layout: re-plan the attention splits
@@ -745,13 +771,7 @@ void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const i
     p.row_seg.assign(p.T, -1);
     for (int i = 0; i < p.S; ++i)
         for (int t = 0; t < seg_len[i]; ++t) p.row_seg[p.seg_start[i] + t] = i;
-    std::vector<int32_t> toks(p.T);
-    std::copy(tokens, tokens + p.Tm, toks.begin());
-    for (int k = 0; k < qlen; ++k) toks[p.Tm + k] = query[k];
-    for (int32_t t : toks)
-        if (t < 0 || t >= c.V) raise(KEEP_ERR_INPUT, "token " + std::to_string(t) + " out of vocab range");
     cudaStream_t st = c.s_main;
-    upload(p.d_tokens, toks, st);
     upload(p.d_row_seg, p.row_seg, st);
     upload(p.d_seg_len, p.seg_len, st);
     if (use_tc_attention(c)) {
@@ -763,6 +783,24 @@ void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const i
             launch_zt_build(p.d_row_seg.as<int32_t>(), p.T, p.chunk_tab.p, p.nb, p.zt.p, st);
         }
     }
+}
+
+void check_tokens(const Context& c, const int32_t* t, int64_t n) {
+    for (int64_t i = 0; i < n; ++i)
+        if (t[i] < 0 || t[i] >= c.V) raise(KEEP_ERR_INPUT, "token " + std::to_string(t[i]) + " out of vocab range");
+}
+
+// Build a pass over a token sequence.  seg_len partitions the memory rows;
+// query rows follow.
+void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const int32_t* tokens,
+               const int32_t* query, int qlen) {
+    pass_layout(c, p, seg_len, qlen);
+    std::vector<int32_t> toks(p.T);
+    std::copy(tokens, tokens + p.Tm, toks.begin());
+    for (int k = 0; k < qlen; ++k) toks[p.Tm + k] = query[k];
+    check_tokens(c, toks.data(), p.T);
+    cudaStream_t st = c.s_main;
+    upload(p.d_tokens, toks, st);
     std::vector<int32_t> all(p.T);
     std::iota(all.begin(), all.end(), 0);
     // (+G rows: the sharded all-gather moves G equal row blocks)
@@ -861,15 +899,15 @@ void cursor_layer(Context& c, const uint8_t* active) {
     cursor_layer(c, active, [] {});
 }
 
-void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int qlen) {
+// Owners of the cached KV of each layout segment (units = static groups or
+// dynamic segments, prefill.hpp:41-54); returns the segment lengths.
+std::vector<int32_t> bind_owners(Context& c, const keep_layout* lay) {
     need_weights(c);
     if (!lay || lay->num_segments < 1) raise(KEEP_ERR_INPUT, "layout is empty");  // prefill.hpp:177
-    if (qlen < 0) raise(KEEP_ERR_INPUT, "negative query length");
     const int S = lay->num_segments;
     std::vector<int32_t> sl(lay->seg_len, lay->seg_len + S);
     for (int x : sl)
         if (x < 1) raise(KEEP_ERR_INPUT, "empty segment in layout");
-    // owners of the cached KV of each segment (units = static groups or segments)
     c.seg_owner.assign(S, OwnerKey{KEEP_OWNER_SEGMENT, 0});
     c.seg_owner_row.assign(S, 0);
     if (lay->num_units == 0) {
@@ -890,6 +928,35 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
         for (int i = 0; i < S; ++i)
             if (covered[i] != 1) raise(KEEP_ERR_INPUT, "units must partition the layout");
     }
+    resolve_segments(c, S);
+    return sl;
+}
+
+// Is the layout one HBM arena in order, with spare rows for the query?  Then
+// all-reused layers run on the arena sheets (no merged-KV copy).
+void detect_alias(Context& c, const std::vector<int32_t>& seg_start, int T) {
+    c.alias_arena = nullptr;
+    c.alias_hold.reset();
+    const Arena* ar = nullptr;
+    bool ok = true;
+    for (size_t i = 0; i < seg_start.size() && ok; ++i) {
+        auto it = c.store.find(c.seg_owner[i]);
+        if (it == c.store.end() || it->second.arena->tier != KEEP_TIER_DEVICE) {
+            ok = false;
+            break;
+        }
+        if (!ar) ar = it->second.arena.get();
+        ok = it->second.arena.get() == ar && it->second.row0 + c.seg_owner_row[i] == seg_start[i];
+    }
+    if (ok && ar && ar->rows >= T) {
+        c.alias_arena = const_cast<Arena*>(ar);
+        c.alias_hold = c.store.find(c.seg_owner[0])->second.arena;  // kept alive for the prefill
+    }
+}
+
+void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int qlen) {
+    if (qlen < 0) raise(KEEP_ERR_INPUT, "negative query length");
+    const std::vector<int32_t> sl = bind_owners(c, lay);
     // the workspace persists across prefills: buffers only grow (no per-step
     // cudaMalloc / cudaFree on the TTFT path)
     if (!c.pf) c.pf.reset(new Pass());
@@ -907,27 +974,7 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
         p.kdst[l] = static_cast<uint8_t*>(c.kv.p) + size_t(l) * 2 * sheet;
         p.vdst[l] = static_cast<uint8_t*>(c.kv.p) + (size_t(l) * 2 + 1) * sheet;
     }
-    resolve_segments(c, S);
-    // is the layout one HBM arena in order (with spare rows for the query)?
-    c.alias_arena = nullptr;
-    c.alias_hold.reset();
-    {
-        const Arena* ar = nullptr;
-        bool ok = true;
-        for (int i = 0; i < S && ok; ++i) {
-            auto it = c.store.find(c.seg_owner[i]);
-            if (it == c.store.end() || it->second.arena->tier != KEEP_TIER_DEVICE) {
-                ok = false;
-                break;
-            }
-            if (!ar) ar = it->second.arena.get();
-            ok = it->second.arena.get() == ar && it->second.row0 + c.seg_owner_row[i] == p.seg_start[i];
-        }
-        if (ok && ar && ar->rows >= p.T) {
-            c.alias_arena = const_cast<Arena*>(ar);
-            c.alias_hold = c.store.find(c.seg_owner[0])->second.arena;  // kept alive for the prefill
-        }
-    }
+    detect_alias(c, p.seg_start, p.T);
     loader_begin(c, p);
 }
 
@@ -1098,6 +1145,392 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
         pl.layer_version.assign(c.L, versions[o]);
         pl.present.assign(c.L, 1);
         c.store[k] = std::move(pl);
+    }
+}
+
+// ------------------------------------------------ batched multi-query prefill --
+// plan_keep (recompute.hpp:140-180) for B queries over one memory layout
+// (SURVEY.md 8(f2)).  Every instance gets exactly the plan, walk and rows a
+// lone plan_keep would: the rows of instance b are computed with the same
+// arithmetic (row-local projections, attention against the instance's own
+// merged KV), only scheduled together:
+//   - layer 0: every segment is in every plan and memory rows precede the
+//     query, so the memory rows are computed once (instance 0); the other
+//     instances compute their query rows against instance 0's layer-0 keys
+//     and copy its segment-to-segment summary; at layer 1 their memory rows
+//     start from instance 0's hidden states;
+//   - the projections (QKV, Wo, MLP) run once per layer over the rows of all
+//     instances (each weight streamed once for the batch);
+//   - attention runs per instance; an instance with no active segment at a
+//     layer reads the in-order arena in place (its query rows copied into the
+//     arena's spare rows just before), so all-reused layers copy nothing;
+//   - the walks of all instances run on the selector stream behind Wo + MLP;
+//   - the first-token logits of the batch stream the unembedding once.
+// With `plans` ([B][L][S], selective_prefill for each query, prefill.hpp:
+// 478-497) the given monotone plans replace the walks.
+void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* queries, int qlen, const double* sched,
+                     bool multihop, keep_plan_result* outs, const uint8_t* plans = nullptr) {
+    if (B < 1) raise(KEEP_ERR_CONFIG, "batch needs at least one query");
+    if (qlen < 1) raise(KEEP_ERR_INPUT, "batched prefill needs query tokens");
+    if (c.G > 1) raise(KEEP_ERR_CONFIG, "batched prefill runs on one GPU (G = 1)");
+    if (c.fast && small_n_threshold() > 0) raise(KEEP_ERR_CONFIG, "batched prefill needs KEEP_ATTN_SMALL_N=0");
+    cudaStream_t st = c.s_main;
+    const int L = c.L, d = c.d, dl = c.dl;
+    const size_t es = c.fast ? 2 : 4;
+    if (c.pk_evs.size() != size_t(L + 1)) {
+        for (auto e : c.pk_evs) cudaEventDestroy(e);
+        c.pk_evs.assign(L + 1, nullptr);
+        for (auto& e : c.pk_evs) KEEP_CUDA(cudaEventCreate(&e));
+    }
+    if (!c.ev_sum) {
+        KEEP_CUDA(cudaEventCreateWithFlags(&c.ev_sum, cudaEventDisableTiming));
+        KEEP_CUDA(cudaEventCreateWithFlags(&c.ev_sel, cudaEventDisableTiming));
+    }
+    std::vector<cudaEvent_t>& evs = c.pk_evs;
+    KEEP_CUDA(cudaEventRecord(evs[0], st));
+    const std::vector<int32_t> sl = bind_owners(c, lay);
+    const int S = int(sl.size());
+    for (int i = 0; i < S; ++i) {
+        auto it = c.store.find(c.seg_owner[i]);
+        if (it != c.store.end() && it->second.arena->tier != KEEP_TIER_DEVICE)
+            raise(KEEP_ERR_CONFIG, "batched prefill needs HBM-resident memory (" + owner_str(c.seg_owner[i]) + ")");
+    }
+    if (!c.batch) c.batch.reset(new Batch());
+    Batch& bt = *c.batch;
+    if (int(bt.views.size()) < B) bt.views.resize(B);
+    for (int b = 0; b < B; ++b) {
+        if (!bt.views[b]) bt.views[b].reset(new Pass());
+        Pass& v = *bt.views[b];
+        v.block_diag = false;
+        v.key_lo_h.clear();
+        v.rows_h.clear();
+        pass_layout(c, v, sl, qlen);
+    }
+    const Pass& v0 = *bt.views[0];
+    const int Tm = v0.Tm, T = v0.T;
+    const int64_t Tp = ceil_div(T, 128) * 128;
+    if (int64_t(B) * Tp > INT32_MAX / 4) raise(KEEP_ERR_CONFIG, "batch too large");
+    check_tokens(c, lay->tokens, Tm);
+    check_tokens(c, queries, int64_t(B) * qlen);
+    detect_alias(c, v0.seg_start, T);
+    const size_t rowb = size_t(dl) * c.elem;
+    const size_t sheet = size_t(B) * Tp * rowb;
+    bt.kv.ensure(2 * sheet);
+    uint8_t* kvK = static_cast<uint8_t*>(bt.kv.p);
+    uint8_t* kvV = kvK + sheet;
+    Pass& P = bt.all;
+    P.S = S;
+    P.T = int(B * Tp);
+    P.Tm = Tm;
+    P.qlen = qlen;
+    P.block_diag = false;
+    P.with_summary = false;
+    P.kdst.assign(L, kvK);
+    P.vdst.assign(L, kvV);
+
+    // layer 0 rows: instance 0 in full, the query rows of the others
+    std::vector<int32_t> rows, toks;
+    std::vector<int> off(B), nrow(B);
+    for (int b = 0; b < B; ++b) {
+        off[b] = int(rows.size());
+        for (int t = (b == 0 ? 0 : Tm); t < T; ++t) {
+            rows.push_back(int32_t(b * Tp + t));
+            toks.push_back(t < Tm ? lay->tokens[t] : queries[size_t(b) * qlen + (t - Tm)]);
+        }
+        nrow[b] = int(rows.size()) - off[b];
+    }
+    const int n0 = int(rows.size());
+    P.x.ensure(sizeof(float) * size_t(n0) * d);
+    if (c.fast) P.xb.ensure(2 * size_t(n0) * d);
+    upload(bt.tokens, toks, st);
+    {
+        std::vector<int32_t> iota(n0);
+        std::iota(iota.begin(), iota.end(), 0);
+        upload(bt.iota, iota, st);
+    }
+    {
+        ProfScope ps(c.prof, KEEP_PROF_EMBED, st, 0.0, double(n0) * d * (8.0 + (c.fast ? 2.0 : 0.0)), c.fast ? 2 : 1);
+        launch_embed(c.embed.as<float>(), bt.tokens.as<int32_t>(), bt.iota.as<int32_t>(), n0, d, P.x.as<float>(), st);
+        if (c.fast) launch_to_bf16(P.x.as<float>(), int64_t(n0) * d, P.xb.as<__nv_bfloat16>(), st);
+    }
+    P.rows_h = rows;
+    P.n = n0;
+    upload(P.d_rows, P.rows_h, st);
+    auto set_views = [&] {
+        std::vector<int32_t> loc;
+        for (int b = 0; b < B; ++b) {
+            Pass& v = *bt.views[b];
+            loc.resize(nrow[b]);
+            for (int i = 0; i < nrow[b]; ++i) loc[i] = int32_t(P.rows_h[off[b] + i] - b * Tp);
+            v.n = nrow[b];
+            if (loc == v.rows_h) continue;
+            v.rows_h = loc;
+            upload(v.d_rows, v.rows_h, st);
+        }
+    };
+    set_views();
+
+    bt.sel_order.ensure(sizeof(int32_t) * size_t(B) * (S + 2));
+    bt.sel_cand.ensure(size_t(B) * S);
+    if (bt.walk_host.bytes < sizeof(int32_t) * size_t(B) * (S + 2) || !bt.walk_host.host)
+        bt.walk_host.alloc(sizeof(int32_t) * size_t(B) * (S + 2), true);
+    int32_t* hbuf = bt.walk_host.as<int32_t>();
+    std::vector<std::vector<uint8_t>> active(B, std::vector<uint8_t>(S, 1));
+    std::vector<uint8_t> candh(size_t(B) * S, 0);
+    std::vector<int32_t> pos;
+
+    for (int l = 0; l < L; ++l) {
+        int64_t budget = 0;
+        if (plans) {
+            for (int b = 0; b < B; ++b) {
+                const uint8_t* pl = plans + (size_t(b) * L + l) * S;
+                for (int i = 0; i < S; ++i) {
+                    if (pl[i] && !active[b][i]) raise(KEEP_ERR_PLAN, "plan is not monotone across layers");
+                    active[b][i] = pl[i] ? 1 : 0;
+                }
+                if (l == 0 && std::count(active[b].begin(), active[b].end(), 1) != S)
+                    raise(KEEP_ERR_PLAN, "a batched prefill computes every segment at layer 0");
+            }
+        } else if (l + 1 < L) {
+            budget = keep_layer_budget(sched[l + 1], S);
+        }
+        std::vector<int64_t> live(B, 0);
+        std::vector<char> walk(B, 0), wanted(B, 0);
+        bool any_walk = false, any_wanted = false;
+        for (int b = 0; b < B; ++b) {
+            keep_plan_result* o = outs ? &outs[b] : nullptr;
+            if (o && o->plan) std::copy(active[b].begin(), active[b].end(), o->plan + size_t(l) * S);
+            if (o && o->order_len) o->order_len[l] = -1;
+            if (o && o->hops) o->hops[l] = 0;
+            for (uint8_t x : active[b]) live[b] += x;
+            walk[b] = !plans && l + 1 < L && budget < live[b] && multihop;
+            wanted[b] = walk[b] || (o && o->summaries) || (!plans && l + 1 < L && budget < live[b] && !multihop);
+            any_walk = any_walk || walk[b];
+            any_wanted = any_wanted || wanted[b];
+        }
+        if (l == 0) wanted[0] = any_wanted;  // the others take instance 0's segment rows
+        if (l > 0) {
+            // newly dropped rows leave for good (prefill.hpp:233-239); at layer 1
+            // instances b > 0 take their memory rows from instance 0
+            std::vector<int32_t> nr_rows;
+            std::vector<int> noff(B), nn(B);
+            for (int b = 0; b < B; ++b) {
+                noff[b] = int(nr_rows.size());
+                for (int i = 0; i < nrow[b]; ++i) {
+                    const int32_t g = P.rows_h[off[b] + i];
+                    const int t = int(g - b * Tp);
+                    const int sg = v0.row_seg[t];
+                    if (sg < 0 || active[b][sg]) nr_rows.push_back(g);
+                }
+                if (l == 1 && b > 0) {  // + the memory rows computed by instance 0
+                    std::vector<int32_t> mem;
+                    for (int t = 0; t < Tm; ++t)
+                        if (active[b][v0.row_seg[t]]) mem.push_back(int32_t(b * Tp + t));
+                    nr_rows.insert(nr_rows.begin() + noff[b], mem.begin(), mem.end());
+                }
+                nn[b] = int(nr_rows.size()) - noff[b];
+            }
+            if (nr_rows != P.rows_h) {
+                pos.assign(size_t(B) * Tp, -1);
+                for (int i = 0; i < P.n; ++i) pos[P.rows_h[i]] = i;
+                std::vector<int32_t> idx(nr_rows.size());
+                for (size_t i = 0; i < nr_rows.size(); ++i) {
+                    int32_t j = pos[nr_rows[i]];
+                    if (j < 0 && l == 1) j = pos[nr_rows[i] % Tp];  // instance 0's row of the same position
+                    if (j < 0) raise(KEEP_ERR_PLAN, "internal: batched row set grew");
+                    idx[i] = j;
+                }
+                const int n_new = int(nr_rows.size());
+                upload(P.d_idx, idx, st);
+                ProfScope ps(c.prof, KEEP_PROF_COMPACT, st, 0.0, double(n_new) * d * (8.0 + (c.fast ? 2.0 : 0.0)));
+                P.x_alt.ensure(sizeof(float) * size_t(std::max(n_new, 1)) * d);
+                if (c.fast) P.xb.ensure(2 * size_t(std::max(n_new, 1)) * d);
+                launch_gather_rows(P.x.as<float>(), P.d_idx.as<int32_t>(), n_new, d, P.x_alt.as<float>(),
+                                   c.fast ? P.xb.as<__nv_bfloat16>() : nullptr, st);
+                std::swap(P.x.p, P.x_alt.p);
+                std::swap(P.x.bytes, P.x_alt.bytes);
+                P.rows_h = std::move(nr_rows);
+                P.n = n_new;
+                upload(P.d_rows, P.rows_h, st);
+                off = noff;
+                nrow = nn;
+                set_views();
+            }
+        }
+        // cached rows of this layer (prefill.hpp:255-263, 340-350) per
+        // instance -- nothing for an all-reused instance over the arena
+        std::vector<char> alias(B, 0);
+        {
+            std::vector<void*> ks, vs;
+            std::vector<int32_t> dr, nrr;
+            int maxr = 0;
+            for (int b = 0; b < B && l > 0; ++b) {
+                bool any_active = false;
+                for (int i = 0; i < S && !any_active; ++i) any_active = active[b][i] != 0;
+                bool al = c.alias_arena != nullptr && !any_active;
+                for (int i = 0; i < S && al; ++i) al = seg_block_current(c, i, l) != nullptr;
+                alias[b] = al;
+                if (al) continue;
+                for (int i = 0; i < S; ++i) {
+                    if (active[b][i]) continue;
+                    const Payload* pl = seg_block_current(c, i, l);
+                    if (!pl) {
+                        c.stats.cache_misses++;
+                        raise(KEEP_ERR_CACHE_MISS, "missing cached KV for segment " + std::to_string(i) + " (owner " +
+                                                       owner_str(c.seg_owner[i]) + ") layer " + std::to_string(l));
+                    }
+                    if (c.seg_owner_row[i] + sl[i] > pl->tokens)
+                        raise(KEEP_ERR_INPUT, "cached block of " + owner_str(c.seg_owner[i]) + " is shorter than its members");
+                    ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * rowb);
+                    vs.push_back(layer_values(c, *pl, l) + c.seg_owner_row[i] * rowb);
+                    dr.push_back(int32_t(b * Tp + v0.seg_start[i]));
+                    nrr.push_back(sl[i]);
+                    maxr = std::max(maxr, sl[i]);
+                }
+            }
+            if (!ks.empty()) {
+                double rows_copied = 0.0;
+                for (int32_t r : nrr) rows_copied += r;
+                ProfScope ps(c.prof, KEEP_PROF_CACHED, st, 0.0, rows_copied * rowb * 4.0);
+                upload(c.d_ksrc, ks, st);
+                upload(c.d_vsrc, vs, st);
+                upload(c.d_cdst, dr, st);
+                upload(c.d_cn, nrr, st);
+                launch_copy_cached(c.d_ksrc.as<const void*>(), c.d_vsrc.as<const void*>(), c.d_cdst.as<int32_t>(),
+                                   c.d_cn.as<int32_t>(), int(ks.size()), int64_t(rowb), kvK, kvV, maxr, st);
+            }
+        }
+        ensure_layer_scratch(c, P);
+        layer_qkv(c, P, l);
+        const size_t qbytes = size_t(qlen) * rowb;
+        for (int b = 0; b < B; ++b) {
+            Pass& v = *bt.views[b];
+            v.with_summary = wanted[b] != 0;
+            const uint8_t* qb = static_cast<const uint8_t*>(P.q.p) + size_t(off[b]) * dl * es;
+            uint8_t* cb = static_cast<uint8_t*>(c.fast ? P.ctxb.p : P.ctx.p) + size_t(off[b]) * dl * es;
+            const uint8_t* kb = kvK + size_t(b) * Tp * rowb;
+            const uint8_t* vb = kvV + size_t(b) * Tp * rowb;
+            uint8_t* qk = nullptr;  // where this instance's query rows must be for its attention
+            uint8_t* qv = nullptr;
+            if (l == 0 && b > 0) {  // instance 0's layer-0 keys, this query's rows in place
+                qk = kvK + size_t(Tm) * rowb;
+                qv = kvV + size_t(Tm) * rowb;
+                kb = kvK;
+                vb = kvV;
+            } else if (alias[b]) {  // the arena sheets of layer l, query rows in the spare rows
+                const size_t asheet = size_t(c.alias_arena->rows) * rowb;
+                uint8_t* ak = static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * asheet;
+                qk = ak + size_t(Tm) * rowb;
+                qv = ak + asheet + size_t(Tm) * rowb;
+                kb = ak;
+                vb = ak + asheet;
+            }
+            if (qk) {
+                ProfScope ps(c.prof, KEEP_PROF_CACHED, st, 0.0, 4.0 * double(qbytes), 2);
+                KEEP_CUDA(cudaMemcpyAsync(qk, kvK + (size_t(b) * Tp + Tm) * rowb, qbytes, cudaMemcpyDeviceToDevice, st));
+                KEEP_CUDA(cudaMemcpyAsync(qv, kvV + (size_t(b) * Tp + Tm) * rowb, qbytes, cudaMemcpyDeviceToDevice, st));
+            }
+            layer_attention(c, v, l, qb, cb, kb, vb);
+            if (l == 0 && b > 0 && v.with_summary)
+                KEEP_CUDA(cudaMemcpyAsync(v.summ.as<double>() + S, bt.views[0]->summ.as<double>() + S,
+                                          sizeof(double) * size_t(S) * S, cudaMemcpyDeviceToDevice, st));
+        }
+        if (any_walk) {  // the walks for layer l+1 overlap this layer's Wo + MLP
+            for (int b = 0; b < B; ++b)
+                if (walk[b]) std::copy(active[b].begin(), active[b].end(), candh.begin() + size_t(b) * S);
+            KEEP_CUDA(cudaMemcpyAsync(bt.sel_cand.p, candh.data(), size_t(B) * S, cudaMemcpyHostToDevice, c.s_sel));
+            KEEP_CUDA(cudaEventRecord(c.ev_sum, st));
+            KEEP_CUDA(cudaStreamWaitEvent(c.s_sel, c.ev_sum, 0));
+            for (int b = 0; b < B; ++b) {
+                if (!walk[b]) continue;
+                int32_t* o = bt.sel_order.as<int32_t>() + size_t(b) * (S + 2);
+                const double* sm = bt.views[b]->summ.as<double>();
+                ProfScope ps(c.prof, KEEP_PROF_SELECT, c.s_sel, 0.0, 8.0 * double(S) * S);
+                launch_select(S, sm, sm + S, budget, bt.sel_cand.as<uint8_t>() + size_t(b) * S, o + 2, o, o + 1, c.s_sel);
+            }
+            KEEP_CUDA(cudaMemcpyAsync(hbuf, bt.sel_order.p, sizeof(int32_t) * size_t(B) * (S + 2), cudaMemcpyDeviceToHost,
+                                      c.s_sel));
+            KEEP_CUDA(cudaEventRecord(c.ev_sel, c.s_sel));
+        }
+        c.gemm_ctas = any_walk ? kNumSMs - 1 : kNumSMs;
+        layer_dense(c, P, l);
+        c.gemm_ctas = kNumSMs;
+        KEEP_CUDA(cudaEventRecord(evs[l + 1], st));
+        for (int b = 0; b < B; ++b) {
+            keep_plan_result* o = outs ? &outs[b] : nullptr;
+            // N_act of the query's own plan (layer 0: every row, although the
+            // batch computed the memory rows once)
+            if (o && o->rows_per_layer) o->rows_per_layer[l] = l == 0 ? T : nrow[b];
+            if (o && o->summaries)
+                KEEP_CUDA(cudaMemcpyAsync(o->summaries + size_t(l) * (S + size_t(S) * S), bt.views[b]->summ.p,
+                                          sizeof(double) * (S + size_t(S) * S), cudaMemcpyDeviceToHost, st));
+        }
+        if (l + 1 >= L) break;
+        if (any_walk) KEEP_CUDA(cudaEventSynchronize(c.ev_sel));
+        for (int b = 0; b < B && !plans; ++b) {
+            if (budget >= live[b]) continue;  // recompute everything still live
+            keep_plan_result* o = outs ? &outs[b] : nullptr;
+            std::vector<uint8_t> next(S, 0);
+            if (multihop) {
+                const int32_t* h = hbuf + size_t(b) * (S + 2);
+                for (int k = 0; k < h[0]; ++k) next[h[2 + k]] = 1;
+                if (o && o->orders) std::copy(h + 2, h + 2 + h[0], o->orders + size_t(l) * S);
+                if (o && o->order_len) o->order_len[l] = h[0];
+                if (o && o->hops) o->hops[l] = h[1];
+            } else {  // single-hop ablation (recompute.hpp:166-176)
+                std::vector<double> qts(S);
+                KEEP_CUDA(cudaMemcpyAsync(qts.data(), bt.views[b]->summ.p, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+                KEEP_CUDA(cudaStreamSynchronize(st));
+                std::vector<int> ord;
+                for (int i = 0; i < S; ++i)
+                    if (active[b][i]) ord.push_back(i);
+                std::stable_sort(ord.begin(), ord.end(), [&](int a, int z) { return qts[a] > qts[z]; });
+                for (size_t i = 0; i < size_t(budget) && i < ord.size(); ++i) next[ord[i]] = 1;
+            }
+            active[b] = std::move(next);
+        }
+    }
+    // first-token logits of every instance (model.hpp:76-85): the last row of
+    // an instance is its last query row, never dropped
+    std::vector<int32_t> last(B);
+    for (int b = 0; b < B; ++b) last[b] = off[b] + nrow[b] - 1;
+    upload(bt.last_idx, last, st);
+    bt.last_x.ensure(sizeof(float) * size_t(B) * d);
+    bt.logits.ensure(sizeof(double) * size_t(B) * c.V);
+    {
+        ProfScope ps(c.prof, KEEP_PROF_LOGITS, st, 2.0 * B * c.d * double(c.V), 4.0 * c.d * double(c.V));
+        launch_gather_rows(P.x.as<float>(), bt.last_idx.as<int32_t>(), B, d, bt.last_x.as<float>(), nullptr, st);
+        launch_logits_multi(bt.last_x.as<float>(), B, c.unembed.as<float>(), d, c.V, bt.logits.as<double>(), st);
+    }
+    KEEP_CUDA(cudaEventRecord(c.ev_b, st));
+    for (int b = 0; b < B && outs; ++b)
+        if (outs[b].last_logits)
+            KEEP_CUDA(cudaMemcpyAsync(outs[b].last_logits, bt.logits.as<double>() + size_t(b) * c.V,
+                                      sizeof(double) * c.V, cudaMemcpyDeviceToHost, st));
+    KEEP_CUDA(cudaStreamSynchronize(st));
+    if (!outs) return;
+    float ms = 0.f;
+    KEEP_CUDA(cudaEventElapsedTime(&ms, evs[0], c.ev_b));
+    std::vector<double> lms(L, 0.0);
+    for (int l = 0; l < L; ++l) {
+        float m = 0.f;
+        KEEP_CUDA(cudaEventElapsedTime(&m, evs[l], evs[l + 1]));
+        lms[l] = m;
+    }
+    std::vector<float> xc;
+    for (int b = 0; b < B; ++b) {
+        keep_plan_result& o = outs[b];
+        o.ttft_ms = ms;
+        if (o.layer_ms) std::copy(lms.begin(), lms.end(), o.layer_ms);
+        if (o.final_hidden) {  // finish (prefill.hpp:324-337): dropped rows are zero
+            std::memset(o.final_hidden, 0, sizeof(float) * size_t(T) * d);
+            xc.resize(size_t(nrow[b]) * d);
+            KEEP_CUDA(cudaMemcpy(xc.data(), P.x.as<float>() + size_t(off[b]) * d, sizeof(float) * xc.size(),
+                                 cudaMemcpyDeviceToHost));
+            for (int i = 0; i < nrow[b]; ++i)
+                std::memcpy(o.final_hidden + size_t(P.rows_h[off[b] + i] - b * Tp) * d, xc.data() + size_t(i) * d,
+                            sizeof(float) * d);
+        }
     }
 }
 
@@ -1571,6 +2004,19 @@ int keep_divergence(void* ctx, const float* row_a, const float* row_b, double* l
 // plan_keep (recompute.hpp:140-180) with every layer, the selection and the
 // last-row logits on the device.  The host only decides keep-all vs walk from
 // the budget and applies the returned order (one small D2H per layer).
+int keep_plan_keep_batch(void* ctx, const keep_layout* layout, int32_t batch, const int32_t* queries, int32_t qlen,
+                         const double* sched, int32_t multihop, keep_plan_result* outs) {
+    return guard([&] { plan_keep_batch(*C(ctx), layout, batch, queries, qlen, sched, multihop != 0, outs); });
+}
+
+int keep_selective_prefill_batch(void* ctx, const keep_layout* layout, int32_t batch, const int32_t* queries,
+                                 int32_t qlen, const uint8_t* plans, keep_plan_result* outs) {
+    return guard([&] {
+        if (!plans) raise(KEEP_ERR_PLAN, "null plans");
+        plan_keep_batch(*C(ctx), layout, batch, queries, qlen, nullptr, true, outs, plans);
+    });
+}
+
 int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, int32_t qlen,
                    const double* sched, int32_t multihop, keep_plan_result* out) {
     return guard([&] {

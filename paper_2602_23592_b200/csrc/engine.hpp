@@ -225,6 +225,19 @@ struct Loader {
     ~Loader();
 };
 
+// Batched multi-query prefill: B queries over one memory
+// layout.  `all` holds the concatenated compact rows of every instance (the
+// projections stream each weight once per layer for all of them); views[b] is
+// instance b's attention view (layout, instance-local rows, attention scratch,
+// summary).  Instance b's merged KV is rows [b*Tp, b*Tp + T) of `kv`.
+struct Batch {
+    Pass all;
+    std::vector<std::unique_ptr<Pass>> views;
+    DevBuf kv;                        // [2][B*Tp][dl] merged KV of the current layer
+    DevBuf tokens, iota, last_idx, last_x, logits;
+    DevBuf sel_order, sel_cand, walk_host;
+};
+
 struct Context {
     keep_config cfg{};
     int L = 0, H = 0, d = 0, dh = 0, f = 0, V = 0;
@@ -245,6 +258,7 @@ struct Context {
     keep_memory_stats stats{};
     // cursor
     std::unique_ptr<Pass> pf;
+    std::unique_ptr<Batch> batch;   // batched multi-query prefill workspace
     std::unique_ptr<Pass> refresh;  // canonical-KV refresh workspace
     DevBuf refresh_ws;               // in-place refresh: merged KV of the refreshed owners
     DevBuf kv;  // merged KV of the cursor [L][2][T][d]

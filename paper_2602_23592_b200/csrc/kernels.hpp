@@ -56,6 +56,8 @@ void launch_select(int S, const double* qts, const double* sts, int64_t budget,
 // (model.hpp:76-85).
 void launch_logits(const float* row, const float* unembed, int d, int V, double* out,
                    cudaStream_t st);
+// ... for B rows [B x d] -> out [B x V] (same arithmetic per row)
+void launch_logits_multi(const float* rows, int B, const float* unembed, int d, int V, double* out, cudaStream_t st);
 // K11b: divergence (prefill.hpp:501-531) of two rows given their logits;
 // out[0] = L2, out[1] = symmetric KL.
 void launch_divergence(const float* a, const float* b, int d, const double* la, const double* lb, int V, double* out,

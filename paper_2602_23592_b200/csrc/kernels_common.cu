@@ -539,6 +539,35 @@ void launch_divergence(const float* a, const float* b, int d, const double* la, 
     KEEP_LAUNCH_CHECK();
 }
 
+// K11 for a batch of rows: the unembedding streams once for up to 16 rows;
+// each logit is the same fp64 fma chain in ascending i as logits_kernel.
+__global__ void logits_multi_kernel(const float* __restrict__ rows, int B, const float* __restrict__ unembed, int d,
+                                    int V, double* __restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= V) return;
+    double acc[16];
+#pragma unroll
+    for (int b = 0; b < 16; ++b) acc[b] = 0.0;
+    for (int i = 0; i < d; ++i) {
+        const double u = double(unembed[int64_t(i) * V + j]);
+#pragma unroll
+        for (int b = 0; b < 16; ++b)
+            if (b < B) acc[b] = fma(double(__ldg(rows + int64_t(b) * d + i)), u, acc[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < 16; ++b)
+        if (b < B) out[int64_t(b) * V + j] = acc[b];
+}
+
+void launch_logits_multi(const float* rows, int B, const float* unembed, int d, int V, double* out, cudaStream_t st) {
+    for (int b0 = 0; b0 < B; b0 += 16) {
+        const int nb = std::min(16, B - b0);
+        logits_multi_kernel<<<static_cast<unsigned>(ceil_div(V, 128)), 128, 0, st>>>(rows + int64_t(b0) * d, nb, unembed,
+                                                                                     d, V, out + int64_t(b0) * V);
+        KEEP_LAUNCH_CHECK();
+    }
+}
+
 void launch_logits(const float* row, const float* unembed, int d, int V, double* out, cudaStream_t st) {
     logits_kernel<<<static_cast<unsigned>(ceil_div(V, 128)), 128, sizeof(float) * d, st>>>(row, unembed, d, V, out);
     KEEP_LAUNCH_CHECK();

@@ -1,0 +1,128 @@
+"""Batched multi-query prefill (keep_plan_keep_batch): B
+planning queries over one memory layout.  Every query of the batch gets
+exactly what a lone plan_keep gives it -- plans, walk orders, hops, rows per
+layer, summaries and (PARITY) bit-identical final hidden states and logits --
+although layer 0's memory rows are computed once for the whole batch, the
+projections run once per layer over all queries' rows, and all-reused layers
+read the in-order arena in place.  plan_keep itself is pinned to the
+reference oracle by test_gpu_parity.py."""
+import numpy as np
+import pytest
+
+import paper_2602_23592_b200 as kb
+from paper_2602_23592_b200.synth import group_units, make_instance_layout
+
+pytestmark = pytest.mark.gpu
+
+
+def batch_queries(seed, B, qlen, V, first):
+    rng = np.random.default_rng(seed)
+    Q = rng.integers(0, V, size=(B, qlen)).astype(np.int32)
+    Q[0] = first
+    return Q
+
+
+def layout(inst, S, groups):
+    if groups:
+        return kb.Layout(inst.seg_len, inst.tokens, group_units(S, 4, 0.5))
+    return kb.Layout(inst.seg_len, inst.tokens)
+
+
+@pytest.mark.parametrize("seed,S,L,H,d,B,groups,r_avg", [
+    (5, 16, 4, 4, 32, 3, False, 0.5), (6, 40, 5, 2, 64, 5, True, 0.4), (7, 12, 3, 2, 32, 1, False, 0.5),
+    (8, 60, 6, 4, 64, 4, True, 0.3),
+])
+def test_batch_parity_matches_single(seed, S, L, H, d, B, groups, r_avg):
+    mlp, V = 2 * d, 256
+    inst = make_instance_layout(seed, S, V)
+    lay = layout(inst, S, groups)
+    Q = batch_queries(seed, B, len(inst.query), V, inst.query)
+    sched = kb.ratio_schedule(L, r_avg)
+    with kb.Context(L, H, d, mlp, V, seed) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay)
+        batch = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True, summaries=True)
+        singles = [ctx.plan_keep(lay, Q[b], sched, summaries=True) for b in range(B)]
+        again = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True)  # workspace reuse
+    for b, (g, r) in enumerate(zip(batch, singles)):
+        assert np.array_equal(g["plan"], r["plan"]), b
+        assert g["orders"] == r["orders"], b
+        assert np.array_equal(g["hops"], r["hops"]), b
+        assert np.array_equal(g["rows_per_layer"], r["rows_per_layer"]), b
+        assert np.array_equal(g["qts"], r["qts"]) and np.array_equal(g["sts"], r["sts"]), b
+        assert np.array_equal(g["final_hidden"], r["final_hidden"]), b
+        assert np.array_equal(g["last_logits"], r["last_logits"]), b
+        assert np.array_equal(again[b]["final_hidden"], r["final_hidden"]), b
+    assert len({round(g["ttft_ms"], 9) for g in batch}) == 1  # one device time for the batch
+
+
+def test_batch_fast_tc_matches_single():
+    # head_dim 128: tensor-core attention, decode kernel on the query-only layers
+    seed, S, L, H, d, V, B = 31, 50, 6, 2, 256, 512, 4
+    inst = make_instance_layout(seed, S, V)
+    lay = layout(inst, S, True)
+    Q = batch_queries(seed, B, len(inst.query), V, inst.query)
+    sched = kb.ratio_schedule(L, 0.3)
+    with kb.Context(L, H, d, 2 * d, V, seed, kb.FAST) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay)
+        batch = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True)
+        singles = [ctx.plan_keep(lay, Q[b], sched) for b in range(B)]
+    agree = np.mean([np.mean(g["plan"] == r["plan"]) for g, r in zip(batch, singles)])
+    assert agree >= 0.95
+    for g, r in zip(batch, singles):
+        if np.array_equal(g["plan"], r["plan"]):
+            q = slice(-len(inst.query), None)
+            a, e = g["final_hidden"][q].astype(np.float64), r["final_hidden"][q].astype(np.float64)
+            assert np.max(np.abs(a - e)) <= 3e-2 * np.max(np.abs(e))
+
+
+def test_batch_needs_hbm_memory():
+    seed, S, L, H, d, V = 3, 10, 3, 2, 32, 128
+    inst = make_instance_layout(seed, S, V)
+    lay = kb.Layout(inst.seg_len, inst.tokens)
+    with kb.Context(L, H, d, 2 * d, V, seed) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay, tier=kb.TIER_HOST)
+        with pytest.raises(kb.KeepError):
+            ctx.plan_keep_batch(lay, np.array([inst.query]), kb.ratio_schedule(L, 0.5))
+        with pytest.raises(kb.KeepError):
+            ctx.plan_keep_batch(lay, np.zeros((2, 0), np.int32), kb.ratio_schedule(L, 0.5))
+
+
+@pytest.mark.parametrize("mode", [kb.PARITY, kb.FAST])
+def test_batch_selective_prefill_alias_layers(mode):
+    """Given plans (keep_selective_prefill_batch): queries whose later layers
+    reuse all memory run those layers on the in-order arena (their query rows
+    copied into its spare rows one query at a time), the others on their own
+    merged KV; each equals the cursor's selective_prefill of its plan."""
+    seed, S, L, V, B = 12, 24, 5, 256, 4
+    H, d = (4, 32) if mode == kb.PARITY else (2, 256)
+    inst = make_instance_layout(seed, S, V)
+    lay = kb.Layout(inst.seg_len, inst.tokens)
+    Q = batch_queries(seed, B, len(inst.query), V, inst.query)
+    plans = np.zeros((B, L, S), np.uint8)
+    plans[:, 0] = 1
+    plans[0, 1] = 1                  # everything, then nothing
+    plans[1, 1:3, :5] = 1            # a prefix for two layers
+    plans[2] = 1                     # full recompute
+    plans[3, 1, ::3] = 1             # scattered, then nothing
+    with kb.Context(L, H, d, 2 * d, V, seed, mode) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay)
+        batch = ctx.plan_keep_batch(lay, Q, None, final_hidden=True, summaries=True, plans=plans)
+        refs = [ctx.selective_prefill(lay, Q[b], plans[b]) for b in range(B)]
+        with pytest.raises(kb.KeepError):  # not monotone
+            bad = plans.copy()
+            bad[0, 3, 0] = 1
+            ctx.plan_keep_batch(lay, Q, None, plans=bad)
+    for b in range(B):
+        g, r = batch[b], refs[b]
+        assert np.array_equal(g["plan"], plans[b])
+        if mode == kb.PARITY:
+            assert np.array_equal(g["final_hidden"], r["final_hidden"]), b
+            assert np.array_equal(g["qts"], r["qts"]) and np.array_equal(g["sts"], r["sts"]), b
+        else:
+            q = slice(-len(inst.query), None)
+            a, e = g["final_hidden"][q].astype(np.float64), r["final_hidden"][q].astype(np.float64)
+            assert np.max(np.abs(a - e)) <= 3e-2 * np.max(np.abs(e)), b
