@@ -40,6 +40,8 @@ CONFIGS = {
                desc="Qwen2.5-7B dims, 4K-token memory, r_avg 0.15"),
     "c3": dict(L=48, H=40, d=5120, mlp=13824, V=152064, S=1638, r_avg=0.5,
                desc="Qwen2.5-14B dims, 16K-token memory, r_avg 0.5 (reference default, harness.hpp:57)"),
+    "c4": dict(L=64, H=40, d=5120, mlp=27648, V=152064, S=3276, r_avg=0.15,
+               desc="Qwen2.5-32B dims, 32K-token memory, r_avg 0.15 (BASELINE configs[3], here on one GPU)"),
 }
 METRIC = "memory-prefill TTFT (ms) and recomputed tokens/s, 16K-token memory, 1/2/4/8 B200"
 UNIT = "recomputed tokens/s"
@@ -458,6 +460,77 @@ def run_ours(args, cfg, rank, world, dist):
     ctx.close()
 
 
+def run_batch(args, cfg):
+    """--batch B: B concurrent planning queries over one memory layout through
+    keep_plan_keep_batch (BASELINE configs[4]'s batch of 16; here with the
+    memory KV in HBM), against the same B queries one plan_keep at a time."""
+    import torch
+
+    import paper_2602_23592_b200 as kb
+    torch.cuda.set_device(0)
+    numerics = kb.FAST if args.numerics == "fast" else kb.PARITY
+    L, H, d, mlp, V = cfg["L"], cfg["H"], cfg["d"], cfg["mlp"], cfg["V"]
+    layout, query = workload(cfg, args.seed)
+    r = kb.ratio_schedule(L, cfg["r_avg"])
+    B = args.batch
+    rng = np.random.default_rng(args.seed + 17)
+    Q = rng.integers(0, V, size=(B, len(query))).astype(np.int32)
+    Q[0] = query
+    ctx = kb.Context(L, H, d, mlp, V, args.seed, numerics)
+    ctx.model_init()
+    ctx.memory_compute_layout(layout)
+    for _ in range(args.warmup):
+        ctx.plan_keep_batch(layout, Q, r)
+    ctx.profile_read(reset=True)
+    ctx.profile_enable(True)
+    torch.cuda.synchronize()
+    res = []
+    dev = torch.cuda.current_device()
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            res.append(ctx.plan_keep_batch(layout, Q, r))
+    torch.cuda.synchronize()
+    ctx.profile_enable(False)
+    prof = ctx.profile_read(reset=True)
+    batch_ms = np.array([x[0]["ttft_ms"] for x in res])
+    tokens = float(sum(np.sum(o["rows_per_layer"]) for o in res[-1]))
+    value = tokens / (float(np.mean(batch_ms)) / 1e3)
+    # e2e: host query ids in, host plans + logits out, wall clock
+    e2e = []
+    for _ in range(max(1, args.steps)):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.plan_keep_batch(layout, Q, r)
+        e2e.append(time.perf_counter() - t0)
+    # the same queries one at a time
+    for b in range(min(B, 2)):
+        ctx.plan_keep(layout, Q[b], r, final_hidden=False)
+    seq = [ctx.plan_keep(layout, Q[b], r, final_hidden=False) for b in range(B)]
+    seq_ms = float(sum(x["ttft_ms"] for x in seq))
+    same = [bool(np.array_equal(res[-1][b]["plan"], seq[b]["plan"])) for b in range(B)]
+    line = {
+        "metric": METRIC + " -- batched planning queries", "value": value, "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(batch_ms)),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16" if numerics == kb.FAST else "f32-store/f64-acc", "data": "synthetic",
+        "config": {"workload": args.config + f"-batch{B}", "desc": cfg["desc"], "S": layout.S, "batch": B,
+                   "query_len": len(query), "memory": "hbm", "l2": "inputs > L2 (16 GB memory KV)"},
+        "batch": {"batch_ttft_ms": float(np.median(batch_ms)), "sequential_ttft_ms_sum": seq_ms,
+                  "speedup_vs_sequential": seq_ms / float(np.median(batch_ms)),
+                  "plans_equal_to_sequential": same,
+                  "plan_segments_per_layer_q0": [int(x) for x in res[-1][0]["plan"].sum(axis=1)],
+                  "recomputed_tokens_per_batch": tokens},
+        "phase_ms_per_step": {k: round(v["ms"] / args.steps, 3) for k, v in prof.items() if v["ms"] > 0},
+        "e2e": {"value": tokens / float(np.mean(e2e)), "unit": UNIT, "h2d_bytes_per_step": int(4 * Q.size + 8 * L),
+                "d2h_bytes_per_step": int(B * (8 * V + L * layout.S * 5 + 8 * 2 * L)),
+                "ttft_ms": float(np.mean(e2e)) * 1e3},
+        "gpu_launches": int(sum(v["kernels"] for v in prof.values()) / max(args.steps, 1)),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(_finite(line)), flush=True)
+    ctx.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -474,6 +547,8 @@ def main():
                     help="fraction of dynamic owners updated (refreshed inside the TTFT) before every query")
     ap.add_argument("--memory", choices=["hbm", "host"], default="hbm",
                     help="memory KV resident in HBM (C2-C4) or pinned host DRAM with the K10 loader (C5-style)")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="B > 1: B concurrent planning queries through keep_plan_keep_batch (one GPU)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.r_avg is not None:
@@ -484,6 +559,10 @@ def main():
     if args.impl == "reference":
         if rank == 0:
             run_reference(args, cfg)
+        return
+    if args.batch > 1:
+        if rank == 0:
+            run_batch(args, cfg)
         return
     if world > 1:
         import torch.distributed as dist

@@ -1435,24 +1435,32 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                 KEEP_CUDA(cudaMemcpyAsync(v.summ.as<double>() + S, bt.views[0]->summ.as<double>() + S,
                                           sizeof(double) * size_t(S) * S, cudaMemcpyDeviceToDevice, st));
         }
-        if (any_walk) {  // the walks for layer l+1 overlap this layer's Wo + MLP
-            for (int b = 0; b < B; ++b)
+        if (any_walk) {  // the walks for layer l+1 (one CTA each) overlap this layer's Wo + MLP
+            std::vector<uint8_t> run(B, 0);
+            std::vector<const double*> sp(B);
+            for (int b = 0; b < B; ++b) {
+                run[b] = walk[b] ? 1 : 0;
+                sp[b] = bt.views[b]->summ.as<double>();
                 if (walk[b]) std::copy(active[b].begin(), active[b].end(), candh.begin() + size_t(b) * S);
-            KEEP_CUDA(cudaMemcpyAsync(bt.sel_cand.p, candh.data(), size_t(B) * S, cudaMemcpyHostToDevice, c.s_sel));
+            }
+            candh.resize(size_t(B) * S + B);
+            std::copy(run.begin(), run.end(), candh.begin() + size_t(B) * S);
+            bt.sel_cand.ensure(size_t(B) * S + B);
+            KEEP_CUDA(cudaMemcpyAsync(bt.sel_cand.p, candh.data(), size_t(B) * S + B, cudaMemcpyHostToDevice, c.s_sel));
+            upload(bt.sel_ptrs, sp, c.s_sel);
             KEEP_CUDA(cudaEventRecord(c.ev_sum, st));
             KEEP_CUDA(cudaStreamWaitEvent(c.s_sel, c.ev_sum, 0));
-            for (int b = 0; b < B; ++b) {
-                if (!walk[b]) continue;
-                int32_t* o = bt.sel_order.as<int32_t>() + size_t(b) * (S + 2);
-                const double* sm = bt.views[b]->summ.as<double>();
-                ProfScope ps(c.prof, KEEP_PROF_SELECT, c.s_sel, 0.0, 8.0 * double(S) * S);
-                launch_select(S, sm, sm + S, budget, bt.sel_cand.as<uint8_t>() + size_t(b) * S, o + 2, o, o + 1, c.s_sel);
+            {
+                ProfScope ps(c.prof, KEEP_PROF_SELECT, c.s_sel, 0.0, 8.0 * double(S) * S * B);
+                launch_select_batch(S, B, bt.sel_ptrs.as<const double*>(), budget, bt.sel_cand.as<uint8_t>(),
+                                    bt.sel_cand.as<uint8_t>() + size_t(B) * S, bt.sel_order.as<int32_t>(), c.s_sel);
             }
             KEEP_CUDA(cudaMemcpyAsync(hbuf, bt.sel_order.p, sizeof(int32_t) * size_t(B) * (S + 2), cudaMemcpyDeviceToHost,
                                       c.s_sel));
             KEEP_CUDA(cudaEventRecord(c.ev_sel, c.s_sel));
         }
-        c.gemm_ctas = any_walk ? kNumSMs - 1 : kNumSMs;
+        // (one SM per concurrent walk stays free of the GEMMs)
+        c.gemm_ctas = any_walk ? kNumSMs - std::min<int>(int(std::count(walk.begin(), walk.end(), 1)), 32) : kNumSMs;
         layer_dense(c, P, l);
         c.gemm_ctas = kNumSMs;
         KEEP_CUDA(cudaEventRecord(evs[l + 1], st));

@@ -235,7 +235,7 @@ struct Batch {
     std::vector<std::unique_ptr<Pass>> views;
     DevBuf kv;                        // [2][B*Tp][dl] merged KV of the current layer
     DevBuf tokens, iota, last_idx, last_x, logits;
-    DevBuf sel_order, sel_cand, walk_host;
+    DevBuf sel_order, sel_cand, sel_ptrs, walk_host;
 };
 
 struct Context {

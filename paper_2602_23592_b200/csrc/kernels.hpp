@@ -52,6 +52,10 @@ void launch_select(int S, const double* qts, const double* sts, int64_t budget,
                    const uint8_t* candidates, int32_t* order, int32_t* n_out, int32_t* hops_out,
                    cudaStream_t st);
 
+// K7 for a batch of queries: one walk per CTA (see select_batch_kernel).
+void launch_select_batch(int S, int B, const double* const* summ, int64_t budget, const uint8_t* cand,
+                         const uint8_t* run, int32_t* out, cudaStream_t st);
+
 // K11: Model::logits of one fp32 row, fp64 accumulation in ascending i
 // (model.hpp:76-85).
 void launch_logits(const float* row, const float* unembed, int d, int V, double* out,

@@ -344,10 +344,9 @@ __device__ HopRed block_hop_reduce(HopRed x, HopRed* scratch) {
 // relevant set (fp64), an fp32 upper bound of its absolute terms (the error
 // radius of the sum), and a membership flag; the candidate mask of a thread's
 // positions (tid + k * 512) is a register bitmask.
-__global__ void __launch_bounds__(kSelThreads, 1)
-select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ sts, int64_t budget,
-              const uint8_t* __restrict__ cand, int32_t* __restrict__ order, int32_t* n_out,
-              int32_t* hops_out) {
+__device__ __forceinline__ void select_impl(int S, const double* __restrict__ qts, const double* __restrict__ sts,
+                                            int64_t budget, const uint8_t* __restrict__ cand,
+                                            int32_t* __restrict__ order, int32_t* n_out, int32_t* hops_out) {
     extern __shared__ __align__(16) uint8_t sraw[];
     double* colsum = reinterpret_cast<double*>(sraw);               // [S]
     float* colabs = reinterpret_cast<float*>(colsum + S);           // [S]
@@ -446,6 +445,36 @@ select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ 
         *n_out = n;
         *hops_out = hop;
     }
+}
+
+__global__ void __launch_bounds__(kSelThreads, 1)
+select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ sts, int64_t budget,
+              const uint8_t* __restrict__ cand, int32_t* __restrict__ order, int32_t* n_out,
+              int32_t* hops_out) {
+    select_impl(S, qts, sts, budget, cand, order, n_out, hops_out);
+}
+
+// One walk per CTA (batched queries): CTA b reads summ[b] ([S] qts then
+// [S x S] sts), candidates cand + b*S and writes out + b*(S+2) as
+// {n, hops, order...}; CTAs with run[b] == 0 exit.
+__global__ void __launch_bounds__(kSelThreads, 1)
+select_batch_kernel(int S, const double* const* __restrict__ summ, int64_t budget, const uint8_t* __restrict__ cand,
+                    const uint8_t* __restrict__ run, int32_t* __restrict__ out) {
+    const int b = blockIdx.x;
+    if (!run[b]) return;
+    const double* sm = summ[b];
+    int32_t* o = out + int64_t(b) * (S + 2);
+    select_impl(S, sm, sm + S, budget, cand + int64_t(b) * S, o + 2, o, o + 1);
+}
+
+void launch_select_batch(int S, int B, const double* const* summ, int64_t budget, const uint8_t* cand,
+                         const uint8_t* run, int32_t* out, cudaStream_t st) {
+    if (S > kSelMaxS) raise(KEEP_ERR_CONFIG, "selector supports at most 14336 segments");
+    const size_t smem = size_t(std::max(S, 1)) * (8 + 4 + 1) + 16;
+    if (smem > 48 * 1024)
+        KEEP_CUDA(cudaFuncSetAttribute(select_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    select_batch_kernel<<<B, kSelThreads, smem, st>>>(S, summ, budget, cand, run, out);
+    KEEP_LAUNCH_CHECK();
 }
 
 void launch_select(int S, const double* qts, const double* sts, int64_t budget,
