@@ -122,7 +122,7 @@ class ClockSampler:
 
 def ncu_traffic():
     """Per-launch DRAM traffic (read + write bytes) of the kernels captured by
-    the committed `ncu --set full` summary (profiles/, tools/ncu_summary.py),
+    the committed `ncu --set full` summaries (profiles/, tools/ncu_summary.py),
     averaged over the captured launches of each kernel."""
     import csv
     import glob
@@ -132,8 +132,10 @@ def ncu_traffic():
         return out
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     acc = {}
-    with open(files[-1]) as f:
-        for r in csv.DictReader(f):
+    for fn in files:
+        with open(fn) as f:
+            rows = list(csv.DictReader(f))
+        for r in rows:
             name = r["kernel"].split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
             tot = 0.0
             for k, v in r.items():
