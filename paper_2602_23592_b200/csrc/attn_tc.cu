@@ -44,7 +44,7 @@ constexpr uint32_t IDESC = instr_desc(128, 128);
 constexpr int PART_SEGS = 24;                 // destination segments per binning pass
 constexpr int PART_STRIDE = PART_SEGS + 1;    // floats per row: slot PART_SEGS is a trash slot
 
-enum { MODE_STATS = 0, MODE_CTX = 1 };
+enum { MODE_STATS = 0, MODE_CTX = 1, MODE_FLASH = 2 };
 
 struct TcArgs {
     int n, T, H, d, S;
@@ -488,19 +488,22 @@ struct Layout2 {
     static constexpr int NH = NB / 2;                 // bins columns per key half
     static constexpr uint32_t ZB = NB * 128 * 2;      // Z^T tile [NB x 128] bf16 (2 boxes of NB x 64)
     static constexpr uint32_t STAGE = TILE_BYTES;     // K stage
-    static constexpr uint32_t VSTAGE = TILE_BYTES + ZB;
+    static constexpr uint32_t VSTAGE = TILE_BYTES + (MODE == MODE_CTX ? ZB : 0);
     static constexpr uint32_t Q_OFF = 0;
     static constexpr uint32_t STAGE_OFF = TILE_BYTES;
     static constexpr uint32_t VSTAGE_OFF = STAGE_OFF + ST * STAGE;
-    static constexpr uint32_t PART_OFF = VSTAGE_OFF + (MODE == MODE_CTX ? 2 * VSTAGE : 0);
-    // STATS: (m, l) of the 3 other (team, half) partials; CTX: bins partials [team][half][128][NH]
-    static constexpr uint32_t PART_BYTES = MODE == MODE_STATS ? 3 * TM * 2 * 4 : NTEAM * 2 * TM * NH * 4;
+    static constexpr uint32_t PART_OFF = VSTAGE_OFF + (MODE != MODE_STATS ? 2 * VSTAGE : 0);
+    // STATS: (m, l) of the 3 other (team, half) partials; CTX: bins partials [team][half][128][NH];
+    // FLASH: chunk maxima [2][team][half][128] then the epilogue's l [team][half][128] and m [team][128]
+    static constexpr uint32_t PART_BYTES =
+        MODE == MODE_STATS ? 3 * TM * 2 * 4 : (MODE == MODE_CTX ? NTEAM * 2 * TM * NH * 4 : 14 * TM * 4);
     static constexpr uint32_t GRP_OFF = PART_OFF + PART_BYTES;  // CTX: groups [130] + sources [130]
     static constexpr uint32_t MSK_OFF = GRP_OFF + (2 * TM + 4) * 4;
     static constexpr uint32_t BAR_OFF = (MSK_OFF + 16 + 7) & ~7u;
     static constexpr size_t SMEM = size_t(BAR_OFF) + 256 + 1024;
-    static constexpr uint32_t TMEM_COLS = MODE == MODE_CTX ? 512 : 256;
+    static constexpr uint32_t TMEM_COLS = MODE != MODE_STATS ? 512 : 256;
 };
+static_assert(Layout2<MODE_FLASH, 16>::SMEM <= 232448, "FLASH v2 smem");
 static_assert(Layout2<MODE_CTX, 32>::SMEM <= 232448, "CTX v2 smem (NB 32)");
 static_assert(Layout2<MODE_CTX, 16>::SMEM <= 232448, "CTX v2 smem (NB 16)");
 static_assert(Layout2<MODE_STATS, 16>::SMEM <= 232448, "STATS v2 smem");
@@ -561,7 +564,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     if (warp == 0 && lane == 0) {
         prefetch_map(&tmQ);
         prefetch_map(&tmK);
-        if (MODE == MODE_CTX) prefetch_map(&tmV);
+        if (MODE != MODE_STATS) prefetch_map(&tmV);
         if (bins) prefetch_map(&tmZ);
         for (int s = 0; s < LY::ST; ++s) {
             mbar_init(&full[s], 1);
@@ -604,7 +607,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         }
     } else if (warp == 2) {
         // ------------------------------------ TMA: V, Z (CTX; after the alloc)
-        if (MODE == MODE_CTX && lane == 0 && niter > 0) {
+        if (MODE != MODE_STATS && lane == 0 && niter > 0) {
             for (int it = 0; it < niter; ++it) {
                 const int s = it & 1;
                 mbar_wait(&vempty[s], ((it >> 1) & 1) ^ 1);
@@ -634,11 +637,15 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 fence_after();
                 const uint32_t pb = tm_s0 + uint32_t((j & 1) * TK);
                 const uint32_t vt = smem_u32(sm + LY::VSTAGE_OFF + (j & 1) * LY::VSTAGE);
+                // FLASH: one O accumulator per team (columns 256 + 128 team),
+                // each started by the team's first chunk
+                const uint32_t to = MODE == MODE_FLASH ? tm_o + uint32_t((j & 1) * 128) : tm_o;
+                const int jacc = MODE == MODE_FLASH ? (j >> 1) : j;
                 if (a.dbg != 2)
 #pragma unroll
                 for (int ks = 0; ks < TK / 16; ++ks)
-                    umma_ts(tm_o, pb + uint32_t(64 * (ks >> 2) + 8 * (ks & 3)), desc_mn(vt + uint32_t(ks) * 2048u),
-                            IDESC_VMN, (j | ks) ? 1u : 0u);
+                    umma_ts(to, pb + uint32_t(64 * (ks >> 2) + 8 * (ks & 3)), desc_mn(vt + uint32_t(ks) * 2048u),
+                            IDESC_VMN, (jacc | ks) ? 1u : 0u);
                 if (bins) {
                     const uint32_t zt = vt + TILE_BYTES;
                     const uint32_t tb = tm_b + uint32_t(bins_buf(j) * NB);
@@ -668,9 +675,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     umma(tm_s0 + uint32_t(b * TK), desc_k(qt, ks), desc_k(kt, ks), IDESC, ks ? 1u : 0u);
                 umma_commit(&s_full[b]);
                 umma_commit(&empty[s]);
-                if (MODE == MODE_CTX && it > 0) pv(it - 1);
+                if (MODE != MODE_STATS && it > 0) pv(it - 1);
             }
-            if (MODE == MODE_CTX) {
+            if (MODE != MODE_STATS) {
                 pv(niter - 1);
                 umma_commit(o_full);
             }
@@ -691,7 +698,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         const float scale = a.scale_log2;
         const int c0 = half * KH;             // first key column of this warp in a chunk
         float m_run = -FLT_MAX, l_run = 0.f;  // STATS
-        float lsum = 0.f;                     // CTX with norm_end: this warp's part of l
+        float lsum = 0.f;                     // CTX with norm_end / FLASH: this warp's part of l
+        float fm = -INFINITY;                 // FLASH: running max of the team's rows (exp2 domain)
+        bool o_started = false;               // FLASH: this team's O has been written by a P.V
         float* part = reinterpret_cast<float*>(sm + LY::PART_OFF);
         int32_t* grp = reinterpret_cast<int32_t*>(sm + LY::GRP_OFF);
         int32_t* gsrc_s = grp + TM + 2;
@@ -827,6 +836,78 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 };
                 if (full_half) stats(std::false_type{});
                 else stats(std::true_type{});
+            } else if (MODE == MODE_FLASH) {
+                // single pass (no summary): running max per row shared by the
+                // two key halves of the team, lazy rescale of the team's O
+                // (only when the max grows by more than 2^8): P <= 256.  When
+                // S[b] of chunk `it` is full, every MMA issued before Q.K^T(it)
+                // is complete -- P.V(it-2), the last one into O[b] -- and
+                // P.V(it) waits for p_full: O[b] is quiescent here.
+                float cm = -INFINITY;
+                if (full_half) {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) cm = fmaxf(cm, __uint_as_float(sv[c][jj]));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 2; ++c)
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            if (unsigned(c * 32 + jj - kv0) < unsigned(kv1 - kv0)) cm = fmaxf(cm, __uint_as_float(sv[c][jj]));
+                }
+                float* xm = part + ((((it >> 1) & 1) * NTEAM + team) * 2) * TM;  // [parity][team][half][TM]
+                xm[half * TM + r] = cm;
+                named_sync(2 + team * 4 + q, 64);  // the two key halves of rows 32q.. in this team
+                cm = fmaxf(cm, xm[(half ^ 1) * TM + r]);
+                const float m_new = fmaxf(fm, cm);
+                const bool resc = m_new > fm + 8.f;  // (fm = -inf, m_new finite: the first keys)
+                const float al = resc ? ex2(fm - m_new) : 1.f;
+                if (resc) {
+                    fm = m_new;
+                    lsum *= al;
+                }
+                m_eff = fm == -INFINITY ? 0.f : fm;
+                const uint32_t tp = tm_s0 + lane_base + uint32_t(b * TK + half * 64);
+                auto make_p = [&](auto masked, int c) {
+                    uint32_t hv[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int kk = 32 * c + 2 * i;
+                        float p0 = ex2(__uint_as_float(sv[c][2 * i]) - m_eff);
+                        float p1 = ex2(__uint_as_float(sv[c][2 * i + 1]) - m_eff);
+                        if constexpr (decltype(masked)::value) {
+                            p0 = unsigned(kk - kv0) < unsigned(kv1 - kv0) ? p0 : 0.f;
+                            p1 = unsigned(kk + 1 - kv0) < unsigned(kv1 - kv0) ? p1 : 0.f;
+                        }
+                        hv[i] = pack_bf16(p0, p1);
+                        lsum += p0 + p1;
+                    }
+                    tmem_st16(tp + uint32_t(16 * c), hv);
+                };
+                if (full_half) {
+                    make_p(std::false_type{}, 0);
+                    make_p(std::false_type{}, 1);
+                } else {
+                    make_p(std::true_type{}, 0);
+                    make_p(std::true_type{}, 1);
+                }
+                if (o_started && __any_sync(0xffffffffu, resc)) {
+                    const uint32_t to = tm_o + lane_base + uint32_t(b * 128 + half * 64);
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t ov[32];
+                        tmem_ld32(to + uint32_t(32 * c), ov);
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * al);
+                        tmem_st32(to + uint32_t(32 * c), ov);
+                    }
+                }
+                o_started = true;
+                tmem_wait_st();
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[b]);
             } else {
                 // p, then P = hi + lo back into S[b] (this half's 64 columns),
                 // 32 keys at a time so the split stays in registers
@@ -898,6 +979,62 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 const int64_t o = (int64_t(sp) * a.n + row) * a.H + head;
                 a.m_part[o] = m;
                 a.l_part[o] = l;
+            }
+        } else if (MODE == MODE_FLASH) {
+            if (niter > 0) {
+                mbar_wait(o_full, 0);
+                fence_after();
+            }
+            // merge the two teams: O = O0 2^(m0 - M) + O1 2^(m1 - M), l alike
+            float* lp = part + 8 * TM;   // [team][half][TM]
+            float* mp = part + 12 * TM;  // [team][TM]
+            lp[(team * 2 + half) * TM + r] = lsum;
+            if (half == 0) mp[team * TM + r] = fm;
+            named_sync(1, NTEAM * 256);
+            const float m0 = mp[r], m1 = mp[TM + r];
+            const float M = fmaxf(m0, m1);
+            const float f0 = m0 == -INFINITY ? 0.f : ex2(m0 - M), f1 = m1 == -INFINITY ? 0.f : ex2(m1 - M);
+            const float L = (lp[r] + lp[TM + r]) * f0 + (lp[2 * TM + r] + lp[3 * TM + r]) * f1;
+            const int oc = 32 * (team * 2 + half);
+            uint32_t ov[32];
+            if (niter > 0) {
+                uint32_t o1[32];
+                tmem_ld32(tm_o + lane_base + uint32_t(oc), ov);
+                tmem_ld32(tm_o + lane_base + uint32_t(128 + oc), o1);
+                // (a team without chunks, or whose rows saw no key, has f = 0
+                // and an O that was never written)
+#pragma unroll
+                for (int e = 0; e < 32; ++e)
+                    ov[e] = __float_as_uint((f0 != 0.f ? __uint_as_float(ov[e]) * f0 : 0.f) +
+                                            (f1 != 0.f ? __uint_as_float(o1[e]) * f1 : 0.f));
+            } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) ov[e] = 0u;
+            }
+            if (rvalid) {
+                const int col = head * DH + oc;
+                if (a.nsplit == 1) {
+                    const float il = L > 0.f ? 1.f / L : 0.f;
+                    uint4* dst = reinterpret_cast<uint4*>(a.ctx + int64_t(row) * a.d + col);
+#pragma unroll
+                    for (int g = 0; g < 4; ++g)
+                        dst[g] = make_uint4(
+                            pack_bf16(__uint_as_float(ov[g * 8 + 0]) * il, __uint_as_float(ov[g * 8 + 1]) * il),
+                            pack_bf16(__uint_as_float(ov[g * 8 + 2]) * il, __uint_as_float(ov[g * 8 + 3]) * il),
+                            pack_bf16(__uint_as_float(ov[g * 8 + 4]) * il, __uint_as_float(ov[g * 8 + 5]) * il),
+                            pack_bf16(__uint_as_float(ov[g * 8 + 6]) * il, __uint_as_float(ov[g * 8 + 7]) * il));
+                } else {
+                    float4* dst = reinterpret_cast<float4*>(a.o_part + (int64_t(sp) * a.n + row) * a.d + col);
+#pragma unroll
+                    for (int g = 0; g < 8; ++g)
+                        dst[g] = make_float4(__uint_as_float(ov[4 * g]), __uint_as_float(ov[4 * g + 1]),
+                                             __uint_as_float(ov[4 * g + 2]), __uint_as_float(ov[4 * g + 3]));
+                    if (team == 0 && half == 0) {
+                        const int64_t o = (int64_t(sp) * a.n + row) * a.H + head;
+                        a.m_part[o] = M;
+                        a.l_part[o] = L;
+                    }
+                }
             }
         } else {
             if (niter > 0) {
@@ -988,6 +1125,28 @@ __global__ void tc_stats_combine(const float* __restrict__ mp, const float* __re
         }
         m_fin[e] = m;
         inv_l[e] = l > 0.f ? 1.f / l : 0.f;
+    }
+}
+
+// FLASH splits: each split's (m, l, O) relative to its own max
+__global__ void tc_flash_combine(const float* __restrict__ m_part, const float* __restrict__ l_part,
+                                 const float* __restrict__ o_part, int nsplit, int n, int H, int d,
+                                 __nv_bfloat16* __restrict__ ctx) {
+    const int64_t nd = int64_t(n) * d;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nd; e += int64_t(gridDim.x) * blockDim.x) {
+        const int r = int(e / d), c = int(e % d), h = c / DH;
+        float M = -INFINITY;
+        for (int s = 0; s < nsplit; ++s) M = fmaxf(M, m_part[(int64_t(s) * n + r) * H + h]);
+        float L = 0.f, O = 0.f;
+        if (M != -INFINITY)
+            for (int s = 0; s < nsplit; ++s) {
+                const float ms = m_part[(int64_t(s) * n + r) * H + h];
+                if (ms == -INFINITY) continue;
+                const float w = ex2(ms - M);
+                L += l_part[(int64_t(s) * n + r) * H + h] * w;
+                O += o_part[(int64_t(s) * n + r) * d + c] * w;
+            }
+        ctx[e] = __float2bfloat16_rn(L > 0.f ? O / L : 0.f);
     }
 }
 
@@ -1085,6 +1244,14 @@ void launch_mode2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap&
     }
     attn_tc2_kernel<MODE, NB><<<grid, NTHR2, LY::SMEM, st>>>(q, k, vt, z, a);
     KEEP_LAUNCH_CHECK();
+}
+
+bool flash_enabled() {  // KEEP_ATTN_FLASH=0: the two-pass form also without a summary (A/B)
+    static const bool v = [] {
+        const char* e = std::getenv("KEEP_ATTN_FLASH");
+        return !(e && *e == '0');
+    }();
+    return v;
 }
 
 bool force_v1() {
@@ -1201,6 +1368,23 @@ int launch_attention_tc(const AttnTcLaunch& L, cudaStream_t st) {
         const char* e = std::getenv("KEEP_DEBUG_NO_BINS");
         const bool no_bins = !L.with_bins || (e && *e == '1');
         a.norm_end = (v2 && no_bins) ? 1 : 0;
+    }
+    {
+        const char* e = std::getenv("KEEP_DEBUG_ATTN");
+        a.dbg = e ? std::atoi(e) : 0;
+    }
+    if (v2 && a.norm_end && flash_enabled()) {
+        // no summary: single pass with online softmax (no STATS pass, K read once)
+        launch_mode2<MODE_FLASH, 16>(mq, mk, mv, mq, a, grid, st);
+        ++launched;
+        if (a.nsplit > 1) {
+            const int64_t nd = int64_t(n) * d;
+            tc_flash_combine<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(
+                L.m_part, L.l_part, L.o_part, a.nsplit, n, H, d, L.ctx);
+            KEEP_LAUNCH_CHECK();
+            ++launched;
+        }
+        return launched;
     }
     if (v2) { launch_mode2<MODE_STATS, 16>(mq, mk, mv, mq, a, grid, st); ++launched; }
     else { launch_mode<MODE_STATS>(mq, mk, mv, a, grid, st); ++launched; }

@@ -140,3 +140,31 @@ def test_decode_attention_query_rows(seed, S, H, d, qlen):
     assert np.isfinite(out[kb.FAST][0]).all()
     assert rel(out[kb.FAST][0], out[kb.PARITY][0]) <= RTOL_FAST
     assert rel(out[kb.FAST][1], out[kb.PARITY][1]) <= RTOL_FAST
+
+
+@pytest.mark.parametrize("seed,S,H,d,frac", [(70, 120, 2, 256, 1.0), (71, 400, 3, 384, 0.5), (72, 30, 1, 128, 1.0),
+                                             (73, 1500, 4, 512, 0.3)])
+def test_flash_attention_no_summary(seed, S, H, d, frac):
+    """Layers that need no summary run single-pass attention (MODE_FLASH:
+    online softmax with lazy rescale of each team's O accumulator, key
+    splits merged by their own maxima).  Same stated tolerance against PARITY."""
+    from paper_2602_23592_b200.synth import make_instance_layout
+    L, mlp, V = 3, 2 * d, 512
+    inst = make_instance_layout(seed, S, V)
+    lay = kb.Layout(inst.seg_len, inst.tokens)
+    plan = np.ones((L, S), np.uint8)
+    keep = np.arange(S) < max(1, int(frac * S))
+    plan[1:] = keep
+    out = {}
+    for mode in (kb.FAST, kb.PARITY):
+        with kb.Context(L, H, d, mlp, V, seed, mode) as ctx:
+            ctx.model_init()
+            ctx.memory_compute_layout(lay)
+            ctx.prefill_begin(lay, inst.query)
+            for l in range(L):
+                ctx.prefill_layer(plan[l], summary=False)
+            fh, kv = ctx.prefill_finish()
+            out[mode] = (fh, kv)
+    assert np.isfinite(out[kb.FAST][0]).all()
+    assert rel(out[kb.FAST][0], out[kb.PARITY][0]) <= RTOL_FAST
+    assert rel(out[kb.FAST][1], out[kb.PARITY][1]) <= RTOL_FAST
