@@ -480,7 +480,8 @@ def run_batch(args, cfg):
     Q[0] = query
     ctx = kb.Context(L, H, d, mlp, V, args.seed, numerics)
     ctx.model_init()
-    ctx.memory_compute_layout(layout)
+    host_mem = args.memory == "host"
+    ctx.memory_compute_layout(layout, tier=kb.TIER_HOST if host_mem else kb.TIER_DEVICE)
     for _ in range(args.warmup):
         ctx.plan_keep_batch(layout, Q, r)
     ctx.profile_read(reset=True)
@@ -504,6 +505,9 @@ def run_batch(args, cfg):
         t0 = time.perf_counter()
         ctx.plan_keep_batch(layout, Q, r)
         e2e.append(time.perf_counter() - t0)
+    st_b = ctx.memory_stats()["bytes_loaded_slow"]
+    ctx.plan_keep_batch(layout, Q, r)
+    h2d_batch = ctx.memory_stats()["bytes_loaded_slow"] - st_b
     # the same queries one at a time
     for b in range(min(B, 2)):
         ctx.plan_keep(layout, Q[b], r, final_hidden=False)
@@ -515,15 +519,18 @@ def run_batch(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(batch_ms)),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "bf16" if numerics == kb.FAST else "f32-store/f64-acc", "data": "synthetic",
-        "config": {"workload": args.config + f"-batch{B}", "desc": cfg["desc"], "S": layout.S, "batch": B,
-                   "query_len": len(query), "memory": "hbm", "l2": "inputs > L2 (16 GB memory KV)"},
+        "config": {"workload": args.config + f"-batch{B}" + ("-hostmem" if host_mem else ""), "desc": cfg["desc"],
+                   "S": layout.S, "batch": B, "query_len": len(query),
+                   "memory": "pinned host DRAM, one staged layer sheet per layer for the batch" if host_mem else "hbm",
+                   "l2": "inputs > L2 (16 GB memory KV)"},
         "batch": {"batch_ttft_ms": float(np.median(batch_ms)), "sequential_ttft_ms_sum": seq_ms,
                   "speedup_vs_sequential": seq_ms / float(np.median(batch_ms)),
                   "plans_equal_to_sequential": same,
                   "plan_segments_per_layer_q0": [int(x) for x in res[-1][0]["plan"].sum(axis=1)],
-                  "recomputed_tokens_per_batch": tokens},
+                  "recomputed_tokens_per_batch": tokens, "h2d_memory_bytes_per_batch": int(h2d_batch)},
         "phase_ms_per_step": {k: round(v["ms"] / args.steps, 3) for k, v in prof.items() if v["ms"] > 0},
-        "e2e": {"value": tokens / float(np.mean(e2e)), "unit": UNIT, "h2d_bytes_per_step": int(4 * Q.size + 8 * L),
+        "e2e": {"value": tokens / float(np.mean(e2e)), "unit": UNIT,
+                "h2d_bytes_per_step": int(4 * Q.size + 8 * L + h2d_batch),
                 "d2h_bytes_per_step": int(B * (8 * V + L * layout.S * 5 + 8 * 2 * L)),
                 "ttft_ms": float(np.mean(e2e)) * 1e3},
         "gpu_launches": int(sum(v["kernels"] for v in prof.values()) / max(args.steps, 1)),

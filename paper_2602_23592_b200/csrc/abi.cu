@@ -934,22 +934,24 @@ std::vector<int32_t> bind_owners(Context& c, const keep_layout* lay) {
 
 // Is the layout one HBM arena in order, with spare rows for the query?  Then
 // all-reused layers run on the arena sheets (no merged-KV copy).
+// The arena of `tier` that holds every layout segment at its layout row, or null.
+Arena* in_order_arena(Context& c, const std::vector<int32_t>& seg_start, int tier) {
+    Arena* ar = nullptr;
+    for (size_t i = 0; i < seg_start.size(); ++i) {
+        auto it = c.store.find(c.seg_owner[i]);
+        if (it == c.store.end() || it->second.arena->tier != tier) return nullptr;
+        if (!ar) ar = it->second.arena.get();
+        if (it->second.arena.get() != ar || it->second.row0 + c.seg_owner_row[i] != seg_start[i]) return nullptr;
+    }
+    return ar;
+}
+
 void detect_alias(Context& c, const std::vector<int32_t>& seg_start, int T) {
     c.alias_arena = nullptr;
     c.alias_hold.reset();
-    const Arena* ar = nullptr;
-    bool ok = true;
-    for (size_t i = 0; i < seg_start.size() && ok; ++i) {
-        auto it = c.store.find(c.seg_owner[i]);
-        if (it == c.store.end() || it->second.arena->tier != KEEP_TIER_DEVICE) {
-            ok = false;
-            break;
-        }
-        if (!ar) ar = it->second.arena.get();
-        ok = it->second.arena.get() == ar && it->second.row0 + c.seg_owner_row[i] == seg_start[i];
-    }
-    if (ok && ar && ar->rows >= T) {
-        c.alias_arena = const_cast<Arena*>(ar);
+    Arena* ar = in_order_arena(c, seg_start, KEEP_TIER_DEVICE);
+    if (ar && ar->rows >= T) {
+        c.alias_arena = ar;
         c.alias_hold = c.store.find(c.seg_owner[0])->second.arena;  // kept alive for the prefill
     }
 }
@@ -1190,10 +1192,10 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
     KEEP_CUDA(cudaEventRecord(evs[0], st));
     const std::vector<int32_t> sl = bind_owners(c, lay);
     const int S = int(sl.size());
+    bool any_host = false;
     for (int i = 0; i < S; ++i) {
         auto it = c.store.find(c.seg_owner[i]);
-        if (it != c.store.end() && it->second.arena->tier != KEEP_TIER_DEVICE)
-            raise(KEEP_ERR_CONFIG, "batched prefill needs HBM-resident memory (" + owner_str(c.seg_owner[i]) + ")");
+        any_host = any_host || (it != c.store.end() && it->second.arena->tier != KEEP_TIER_DEVICE);
     }
     if (!c.batch) c.batch.reset(new Batch());
     Batch& bt = *c.batch;
@@ -1213,7 +1215,46 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
     check_tokens(c, lay->tokens, Tm);
     check_tokens(c, queries, int64_t(B) * qlen);
     detect_alias(c, v0.seg_start, T);
+    // Memory in pinned host DRAM (BASELINE configs[4]): one in-order arena,
+    // streamed a whole layer sheet at a time into two HBM staging sheets on
+    // the copy stream, one layer ahead of compute -- every query of the batch
+    // reads the same staged sheet, so each byte crosses PCIe once per layer
+    // for the whole batch.  The staged sheet then serves exactly as the
+    // in-order HBM arena does (cached-row source, aliased layers in place).
+    Arena* host_ar = nullptr;
+    if (any_host) {
+        host_ar = in_order_arena(c, v0.seg_start, KEEP_TIER_HOST);
+        if (!host_ar)
+            raise(KEEP_ERR_CONFIG, "batched prefill over host memory needs the layout as one in-order pinned arena");
+        if (qlen > kArenaPad) raise(KEEP_ERR_CONFIG, "query longer than the staging spare rows");
+    }
     const size_t rowb = size_t(dl) * c.elem;
+    const size_t ssheet = size_t(Tm + kArenaPad) * rowb;  // staged sheet: memory rows + spare rows
+    uint8_t* stage[2] = {nullptr, nullptr};
+    if (host_ar) {
+        bt.stage.ensure(4 * ssheet);
+        stage[0] = static_cast<uint8_t*>(bt.stage.p);
+        stage[1] = stage[0] + 2 * ssheet;
+        if (!bt.ev_load[0])
+            for (int k = 0; k < 2; ++k) {
+                KEEP_CUDA(cudaEventCreateWithFlags(&bt.ev_load[k], cudaEventDisableTiming));
+                KEEP_CUDA(cudaEventCreateWithFlags(&bt.ev_used[k], cudaEventDisableTiming));
+            }
+    }
+    auto load_sheet = [&](int l) {  // layer l's canonical K / V of every memory row -> stage[l & 1]
+        uint8_t* dst = stage[l & 1];
+        const size_t asheet = size_t(host_ar->rows) * rowb;
+        const uint8_t* src = static_cast<const uint8_t*>(host_ar->buf.p) + size_t(l) * 2 * asheet;
+        KEEP_CUDA(cudaStreamWaitEvent(c.s_copy, bt.ev_used[l & 1], 0));  // its readers of layer l-2 are done
+        {
+            ProfScope ps(c.prof, KEEP_PROF_LOADER, c.s_copy, 0.0, 2.0 * Tm * rowb, 2);
+            KEEP_CUDA(cudaMemcpyAsync(dst, src, size_t(Tm) * rowb, cudaMemcpyHostToDevice, c.s_copy));
+            KEEP_CUDA(cudaMemcpyAsync(dst + ssheet, src + asheet, size_t(Tm) * rowb, cudaMemcpyHostToDevice, c.s_copy));
+        }
+        KEEP_CUDA(cudaEventRecord(bt.ev_load[l & 1], c.s_copy));
+        c.stats.bytes_loaded_slow += 2ull * Tm * rowb;
+    };
+    if (host_ar && L > 1) load_sheet(1);  // overlaps layer 0 (every segment recomputed there)
     const size_t sheet = size_t(B) * Tp * rowb;
     bt.kv.ensure(2 * sheet);
     uint8_t* kvK = static_cast<uint8_t*>(bt.kv.p);
@@ -1360,6 +1401,7 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
         // cached rows of this layer (prefill.hpp:255-263, 340-350) per
         // instance -- nothing for an all-reused instance over the arena
         std::vector<char> alias(B, 0);
+        if (host_ar && l > 0) KEEP_CUDA(cudaStreamWaitEvent(st, bt.ev_load[l & 1], 0));
         {
             std::vector<void*> ks, vs;
             std::vector<int32_t> dr, nrr;
@@ -1367,7 +1409,7 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
             for (int b = 0; b < B && l > 0; ++b) {
                 bool any_active = false;
                 for (int i = 0; i < S && !any_active; ++i) any_active = active[b][i] != 0;
-                bool al = c.alias_arena != nullptr && !any_active;
+                bool al = (c.alias_arena != nullptr || host_ar != nullptr) && !any_active;
                 for (int i = 0; i < S && al; ++i) al = seg_block_current(c, i, l) != nullptr;
                 alias[b] = al;
                 if (al) continue;
@@ -1381,8 +1423,13 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                     }
                     if (c.seg_owner_row[i] + sl[i] > pl->tokens)
                         raise(KEEP_ERR_INPUT, "cached block of " + owner_str(c.seg_owner[i]) + " is shorter than its members");
-                    ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * rowb);
-                    vs.push_back(layer_values(c, *pl, l) + c.seg_owner_row[i] * rowb);
+                    if (host_ar) {  // the staged sheet, in layout order
+                        ks.push_back(stage[l & 1] + size_t(v0.seg_start[i]) * rowb);
+                        vs.push_back(stage[l & 1] + ssheet + size_t(v0.seg_start[i]) * rowb);
+                    } else {
+                        ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * rowb);
+                        vs.push_back(layer_values(c, *pl, l) + c.seg_owner_row[i] * rowb);
+                    }
                     dr.push_back(int32_t(b * Tp + v0.seg_start[i]));
                     nrr.push_back(sl[i]);
                     maxr = std::max(maxr, sl[i]);
@@ -1418,8 +1465,9 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                 kb = kvK;
                 vb = kvV;
             } else if (alias[b]) {  // the arena sheets of layer l, query rows in the spare rows
-                const size_t asheet = size_t(c.alias_arena->rows) * rowb;
-                uint8_t* ak = static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * asheet;
+                const size_t asheet = host_ar ? ssheet : size_t(c.alias_arena->rows) * rowb;
+                uint8_t* ak = host_ar ? stage[l & 1]
+                                      : static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * asheet;
                 qk = ak + size_t(Tm) * rowb;
                 qv = ak + asheet + size_t(Tm) * rowb;
                 kb = ak;
@@ -1434,6 +1482,10 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
             if (l == 0 && b > 0 && v.with_summary)
                 KEEP_CUDA(cudaMemcpyAsync(v.summ.as<double>() + S, bt.views[0]->summ.as<double>() + S,
                                           sizeof(double) * size_t(S) * S, cudaMemcpyDeviceToDevice, st));
+        }
+        if (host_ar) {  // stage[l & 1] is free once this layer's attention has run
+            KEEP_CUDA(cudaEventRecord(bt.ev_used[l & 1], st));
+            if (l + 2 < L) load_sheet(l + 2);
         }
         if (any_walk) {  // the walks for layer l+1 (one CTA each) overlap this layer's Wo + MLP
             std::vector<uint8_t> run(B, 0);

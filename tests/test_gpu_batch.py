@@ -77,17 +77,39 @@ def test_batch_fast_tc_matches_single():
             assert np.max(np.abs(a - e)) <= 3e-2 * np.max(np.abs(e))
 
 
-def test_batch_needs_hbm_memory():
-    seed, S, L, H, d, V = 3, 10, 3, 2, 32, 128
+def test_batch_host_memory_matches_hbm():
+    """Memory in pinned host DRAM (BASELINE configs[4]): the batch streams one
+    layer sheet per layer over PCIe for all queries (staged one layer ahead)
+    and computes exactly what it computes over HBM-resident memory --
+    walks, and (given plans) all-reused layers on the staged sheet."""
+    seed, S, L, H, d, V, B = 21, 30, 5, 2, 64, 256, 4
     inst = make_instance_layout(seed, S, V)
-    lay = kb.Layout(inst.seg_len, inst.tokens)
+    lay = layout(inst, S, True)
+    Q = batch_queries(seed, B, len(inst.query), V, inst.query)
+    sched = kb.ratio_schedule(L, 0.4)
+    plans = np.zeros((B, L, S), np.uint8)
+    plans[:, 0] = 1
+    plans[1, 1:3, :7] = 1
+    plans[2, 1] = 1
     with kb.Context(L, H, d, 2 * d, V, seed) as ctx:
         ctx.model_init()
-        ctx.memory_compute_layout(lay, tier=kb.TIER_HOST)
+        ctx.memory_compute_layout(lay, version=1)
+        dev = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True)
+        dev_sel = ctx.plan_keep_batch(lay, Q, None, final_hidden=True, plans=plans)
+        ctx.memory_compute_layout(lay, version=2, tier=kb.TIER_HOST)
+        st0 = ctx.memory_stats()
+        host = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True)
+        st1 = ctx.memory_stats()
+        host_sel = ctx.plan_keep_batch(lay, Q, None, final_hidden=True, plans=plans)
         with pytest.raises(kb.KeepError):
-            ctx.plan_keep_batch(lay, np.array([inst.query]), kb.ratio_schedule(L, 0.5))
-        with pytest.raises(kb.KeepError):
-            ctx.plan_keep_batch(lay, np.zeros((2, 0), np.int32), kb.ratio_schedule(L, 0.5))
+            ctx.plan_keep_batch(lay, np.zeros((2, 0), np.int32), sched)
+    for g, r in list(zip(host, dev)) + list(zip(host_sel, dev_sel)):
+        assert np.array_equal(g["plan"], r["plan"]) and g["orders"] == r["orders"]
+        assert np.array_equal(g["final_hidden"], r["final_hidden"])
+        assert np.array_equal(g["last_logits"], r["last_logits"])
+    Tm = int(np.sum(inst.seg_len))
+    # every layer after the first crosses PCIe once for the whole batch
+    assert st1["bytes_loaded_slow"] - st0["bytes_loaded_slow"] == (L - 1) * 2 * Tm * d * 4
 
 
 @pytest.mark.parametrize("mode", [kb.PARITY, kb.FAST])
