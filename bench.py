@@ -437,7 +437,8 @@ def run_ours(args, cfg, rank, world, dist):
                                  "dynamic_segments": sum(1 for u in layout.units if u[2] == 0)},
                        "r_avg": cfg["r_avg"],
                        "parallelism": f"KV-head sharded x{world} (NCCL)" if world > 1 else "1 GPU",
-                       "l2": "inputs larger than L2 (26.8 GB bf16 weights + 16 GB merged KV per step)",
+                       "l2": "inputs larger than L2 ({:.1f} GB bf16 weights + {:.1f} GB memory KV read per step)".format(
+                           2e-9 * L * (4 * d * d + 2 * d * mlp), 4e-9 * L * d * int(np.sum(layout.seg_len))),
                        "memory_kv": ("pinned-host canonical KV, layer-balanced K10 loader" if host_mem else
                                      "HBM-resident canonical KV (static groups joint, dynamic per segment)")},
             "recomputed_tokens_per_step": tokens,
@@ -522,7 +523,7 @@ def run_batch(args, cfg):
         "config": {"workload": args.config + f"-batch{B}" + ("-hostmem" if host_mem else ""), "desc": cfg["desc"],
                    "S": layout.S, "batch": B, "query_len": len(query),
                    "memory": "pinned host DRAM, one staged layer sheet per layer for the batch" if host_mem else "hbm",
-                   "l2": "inputs > L2 (16 GB memory KV)"},
+                   "l2": "inputs > L2 ({:.1f} GB memory KV)".format(4e-9 * L * d * int(np.sum(layout.seg_len)))},
         "batch": {"batch_ttft_ms": float(np.median(batch_ms)), "sequential_ttft_ms_sum": seq_ms,
                   "speedup_vs_sequential": seq_ms / float(np.median(batch_ms)),
                   "plans_equal_to_sequential": same,
