@@ -509,7 +509,8 @@ def run_batch(args, cfg):
     st_b = ctx.memory_stats()["bytes_loaded_slow"]
     ctx.plan_keep_batch(layout, Q, r)
     h2d_batch = ctx.memory_stats()["bytes_loaded_slow"] - st_b
-    # the same queries one at a time
+    # the same queries one at a time (the batch workspace released first)
+    ctx.trim()
     for b in range(min(B, 2)):
         ctx.plan_keep(layout, Q[b], r, final_hidden=False)
     seq = [ctx.plan_keep(layout, Q[b], r, final_hidden=False) for b in range(B)]

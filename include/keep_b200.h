@@ -166,6 +166,9 @@ int keep_loopback_destroy(void* group);
 
 int keep_ctx_create(const keep_config* cfg, void** ctx_out);
 int keep_ctx_destroy(void* ctx);
+/* Release the grow-only prefill / batch / refresh workspaces (memory store and
+ * weights stay); they grow back on the next call. */
+int keep_ctx_trim(void* ctx);
 int keep_ctx_synchronize(void* ctx);
 
 /* Reference-identical counter-based weights generated on the device. */

@@ -145,6 +145,7 @@ def load_library() -> C.CDLL:
                                            C.POINTER(keep_plan_result)]),
         "keep_selective_prefill_batch": (C.c_int, [vp, C.POINTER(keep_layout), i32, i32p, i32, u8p,
                                                    C.POINTER(keep_plan_result)]),
+        "keep_ctx_trim": (C.c_int, [vp]),
         "keep_logits": (C.c_int, [vp, fp, dp]),
         "keep_divergence": (C.c_int, [vp, fp, fp, dp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
@@ -308,6 +309,10 @@ class Context:
             pass
 
     # -- model ------------------------------------------------------------
+    def trim(self):
+        """Release the grow-only workspaces (keep_ctx_trim)."""
+        _check(self.lib.keep_ctx_trim(self._h))
+
     def model_init(self):
         _check(self.lib.keep_model_init(self._h))
         return self

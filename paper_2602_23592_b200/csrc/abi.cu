@@ -158,7 +158,7 @@ namespace {
 template <typename T>
 void upload(DevBuf& b, const std::vector<T>& v, cudaStream_t st) {
     b.ensure(sizeof(T) * std::max<size_t>(v.size(), 1));
-    if (!v.empty()) KEEP_CUDA(cudaMemcpyAsync(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice, st));
+    if (!v.empty()) upload_bytes(b.p, v.data(), sizeof(T) * v.size(), st);
 }
 
 void check_cfg(const keep_config& c) {  // ModelConfig::validate, model.hpp:28-38
@@ -1230,31 +1230,45 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
     }
     const size_t rowb = size_t(dl) * c.elem;
     const size_t ssheet = size_t(Tm + kArenaPad) * rowb;  // staged sheet: memory rows + spare rows
-    uint8_t* stage[2] = {nullptr, nullptr};
+    // A ring of NS staged layers: the copy stream runs up to NS - 1 layers
+    // ahead, so the loads of the cheap all-reused layers at the end overlap the
+    // recompute-heavy layers before them (layer-balanced loading,
+    // pipeline_sim.hpp:261-338, with whole layers as the unit).
+    int NS = 0;
+    std::vector<uint8_t*> stage;
     if (host_ar) {
-        bt.stage.ensure(4 * ssheet);
-        stage[0] = static_cast<uint8_t*>(bt.stage.p);
-        stage[1] = stage[0] + 2 * ssheet;
-        if (!bt.ev_load[0])
-            for (int k = 0; k < 2; ++k) {
-                KEEP_CUDA(cudaEventCreateWithFlags(&bt.ev_load[k], cudaEventDisableTiming));
-                KEEP_CUDA(cudaEventCreateWithFlags(&bt.ev_used[k], cudaEventDisableTiming));
-            }
+        size_t free_b = 0, total_b = 0;
+        KEEP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+        // (at most a third of the free HBM and a sixth of the device: the pass needs the rest)
+        const size_t have = bt.stage.bytes + std::min(free_b / 3, total_b / 6);
+        NS = int(std::max<size_t>(2, std::min<size_t>(size_t(L), have / (2 * ssheet))));
+        bt.stage.ensure(size_t(NS) * 2 * ssheet);
+        for (int k = 0; k < NS; ++k) stage.push_back(static_cast<uint8_t*>(bt.stage.p) + size_t(k) * 2 * ssheet);
+        for (size_t k = bt.ev_load.size(); k < size_t(NS); ++k) {
+            cudaEvent_t a = nullptr, u = nullptr;
+            KEEP_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+            KEEP_CUDA(cudaEventCreateWithFlags(&u, cudaEventDisableTiming));
+            bt.ev_load.push_back(a);
+            bt.ev_used.push_back(u);
+        }
+        for (int k = 0; k < NS; ++k) KEEP_CUDA(cudaEventRecord(bt.ev_used[k], st));  // slots free from here
     }
-    auto load_sheet = [&](int l) {  // layer l's canonical K / V of every memory row -> stage[l & 1]
-        uint8_t* dst = stage[l & 1];
+    auto load_sheet = [&](int l) {  // layer l's canonical K / V of every memory row -> stage[l % NS]
+        const int k = l % NS;
+        uint8_t* dst = stage[k];
         const size_t asheet = size_t(host_ar->rows) * rowb;
         const uint8_t* src = static_cast<const uint8_t*>(host_ar->buf.p) + size_t(l) * 2 * asheet;
-        KEEP_CUDA(cudaStreamWaitEvent(c.s_copy, bt.ev_used[l & 1], 0));  // its readers of layer l-2 are done
+        KEEP_CUDA(cudaStreamWaitEvent(c.s_copy, bt.ev_used[k], 0));  // its readers of layer l - NS are done
         {
             ProfScope ps(c.prof, KEEP_PROF_LOADER, c.s_copy, 0.0, 2.0 * Tm * rowb, 2);
             KEEP_CUDA(cudaMemcpyAsync(dst, src, size_t(Tm) * rowb, cudaMemcpyHostToDevice, c.s_copy));
             KEEP_CUDA(cudaMemcpyAsync(dst + ssheet, src + asheet, size_t(Tm) * rowb, cudaMemcpyHostToDevice, c.s_copy));
         }
-        KEEP_CUDA(cudaEventRecord(bt.ev_load[l & 1], c.s_copy));
+        KEEP_CUDA(cudaEventRecord(bt.ev_load[k], c.s_copy));
         c.stats.bytes_loaded_slow += 2ull * Tm * rowb;
     };
-    if (host_ar && L > 1) load_sheet(1);  // overlaps layer 0 (every segment recomputed there)
+    // layer 0 recomputes every segment: loads start with layer 1
+    for (int l = 1; host_ar && l < std::min(L, NS + 1); ++l) load_sheet(l);
     const size_t sheet = size_t(B) * Tp * rowb;
     bt.kv.ensure(2 * sheet);
     uint8_t* kvK = static_cast<uint8_t*>(bt.kv.p);
@@ -1281,8 +1295,33 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
         nrow[b] = int(rows.size()) - off[b];
     }
     const int n0 = int(rows.size());
-    P.x.ensure(sizeof(float) * size_t(n0) * d);
-    if (c.fast) P.xb.ensure(2 * size_t(n0) * d);
+    // Row buffers sized once for the whole pass (layer 1 is the widest after
+    // layer 0: plans only shrink).  x and x_alt swap at every compaction, so a
+    // grow-on-demand x_alt would reallocate -- and a cudaFree synchronises the
+    // device, i.e. waits behind every layer load queued on the copy engines.
+    int64_t max_rows = n0;
+    {
+        int64_t widest = 0;
+        if (plans) {
+            for (int l = 1; l < L; ++l) {
+                int64_t r = 0;
+                for (int b = 0; b < B; ++b)
+                    for (int i = 0; i < S; ++i) r += plans[(size_t(b) * L + l) * S + i] ? sl[i] : 0;
+                widest = std::max(widest, r + int64_t(B) * qlen);
+            }
+        } else if (L > 1) {
+            const int64_t bud = keep_layer_budget(sched[1], S);
+            std::vector<int32_t> len(sl);
+            std::sort(len.begin(), len.end(), std::greater<int32_t>());
+            int64_t r = 0;
+            for (int64_t i = 0; i < std::min<int64_t>(bud, S); ++i) r += len[i];
+            widest = int64_t(B) * (r + qlen);
+        }
+        max_rows = std::max(max_rows, widest);
+    }
+    P.x.ensure(sizeof(float) * size_t(max_rows) * d);
+    P.x_alt.ensure(sizeof(float) * size_t(max_rows) * d);
+    if (c.fast) P.xb.ensure(2 * size_t(max_rows) * d);
     upload(bt.tokens, toks, st);
     {
         std::vector<int32_t> iota(n0);
@@ -1401,7 +1440,7 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
         // cached rows of this layer (prefill.hpp:255-263, 340-350) per
         // instance -- nothing for an all-reused instance over the arena
         std::vector<char> alias(B, 0);
-        if (host_ar && l > 0) KEEP_CUDA(cudaStreamWaitEvent(st, bt.ev_load[l & 1], 0));
+        if (host_ar && l > 0) KEEP_CUDA(cudaStreamWaitEvent(st, bt.ev_load[l % NS], 0));
         {
             std::vector<void*> ks, vs;
             std::vector<int32_t> dr, nrr;
@@ -1424,8 +1463,8 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                     if (c.seg_owner_row[i] + sl[i] > pl->tokens)
                         raise(KEEP_ERR_INPUT, "cached block of " + owner_str(c.seg_owner[i]) + " is shorter than its members");
                     if (host_ar) {  // the staged sheet, in layout order
-                        ks.push_back(stage[l & 1] + size_t(v0.seg_start[i]) * rowb);
-                        vs.push_back(stage[l & 1] + ssheet + size_t(v0.seg_start[i]) * rowb);
+                        ks.push_back(stage[l % NS] + size_t(v0.seg_start[i]) * rowb);
+                        vs.push_back(stage[l % NS] + ssheet + size_t(v0.seg_start[i]) * rowb);
                     } else {
                         ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * rowb);
                         vs.push_back(layer_values(c, *pl, l) + c.seg_owner_row[i] * rowb);
@@ -1466,7 +1505,7 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                 vb = kvV;
             } else if (alias[b]) {  // the arena sheets of layer l, query rows in the spare rows
                 const size_t asheet = host_ar ? ssheet : size_t(c.alias_arena->rows) * rowb;
-                uint8_t* ak = host_ar ? stage[l & 1]
+                uint8_t* ak = host_ar ? stage[l % NS]
                                       : static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * asheet;
                 qk = ak + size_t(Tm) * rowb;
                 qv = ak + asheet + size_t(Tm) * rowb;
@@ -1474,18 +1513,18 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                 vb = ak + asheet;
             }
             if (qk) {
-                ProfScope ps(c.prof, KEEP_PROF_CACHED, st, 0.0, 4.0 * double(qbytes), 2);
-                KEEP_CUDA(cudaMemcpyAsync(qk, kvK + (size_t(b) * Tp + Tm) * rowb, qbytes, cudaMemcpyDeviceToDevice, st));
-                KEEP_CUDA(cudaMemcpyAsync(qv, kvV + (size_t(b) * Tp + Tm) * rowb, qbytes, cudaMemcpyDeviceToDevice, st));
+                ProfScope ps(c.prof, KEEP_PROF_CACHED, st, 0.0, 4.0 * double(qbytes), 1);
+                launch_copy2(qk, kvK + (size_t(b) * Tp + Tm) * rowb, qv, kvV + (size_t(b) * Tp + Tm) * rowb, int64_t(qbytes),
+                             st);
             }
             layer_attention(c, v, l, qb, cb, kb, vb);
             if (l == 0 && b > 0 && v.with_summary)
                 KEEP_CUDA(cudaMemcpyAsync(v.summ.as<double>() + S, bt.views[0]->summ.as<double>() + S,
                                           sizeof(double) * size_t(S) * S, cudaMemcpyDeviceToDevice, st));
         }
-        if (host_ar) {  // stage[l & 1] is free once this layer's attention has run
-            KEEP_CUDA(cudaEventRecord(bt.ev_used[l & 1], st));
-            if (l + 2 < L) load_sheet(l + 2);
+        if (host_ar && l > 0) {  // this layer's slot is free once its attention has run
+            KEEP_CUDA(cudaEventRecord(bt.ev_used[l % NS], st));
+            if (l + NS < L) load_sheet(l + NS);
         }
         if (any_walk) {  // the walks for layer l+1 (one CTA each) overlap this layer's Wo + MLP
             std::vector<uint8_t> run(B, 0);
@@ -1498,7 +1537,7 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
             candh.resize(size_t(B) * S + B);
             std::copy(run.begin(), run.end(), candh.begin() + size_t(B) * S);
             bt.sel_cand.ensure(size_t(B) * S + B);
-            KEEP_CUDA(cudaMemcpyAsync(bt.sel_cand.p, candh.data(), size_t(B) * S + B, cudaMemcpyHostToDevice, c.s_sel));
+            upload_bytes(bt.sel_cand.p, candh.data(), size_t(B) * S + B, c.s_sel);
             upload(bt.sel_ptrs, sp, c.s_sel);
             KEEP_CUDA(cudaEventRecord(c.ev_sum, st));
             KEEP_CUDA(cudaStreamWaitEvent(c.s_sel, c.ev_sum, 0));
@@ -1655,6 +1694,20 @@ int keep_ctx_destroy(void* ctx) {
         cudaEventDestroy(c->ev_a);
         cudaEventDestroy(c->ev_b);
         delete c;
+    });
+}
+
+int keep_ctx_trim(void* ctx) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        KEEP_CUDA(cudaDeviceSynchronize());
+        c.batch.reset();  // workspaces grow back on demand
+        c.pf.reset();
+        c.refresh.reset();
+        c.refresh_ws.release();
+        c.kv.release();
+        c.alias_arena = nullptr;
+        c.alias_hold.reset();
     });
 }
 
@@ -2120,7 +2173,7 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
             // summary of layer l exists, overlapping this layer's Wo + MLP
             auto launch_walk = [&] {
                 if (!walk) return;
-                KEEP_CUDA(cudaMemcpyAsync(c.sel_cand.p, active.data(), S, cudaMemcpyHostToDevice, c.s_sel));
+                upload_bytes(c.sel_cand.p, active.data(), S, c.s_sel);
                 KEEP_CUDA(cudaEventRecord(ev_sum, st));
                 KEEP_CUDA(cudaStreamWaitEvent(c.s_sel, ev_sum, 0));
                 int32_t* o = c.sel_order.as<int32_t>();

@@ -236,9 +236,9 @@ struct Batch {
     DevBuf kv;                        // [2][B*Tp][dl] merged KV of the current layer
     DevBuf tokens, iota, last_idx, last_x, logits;
     DevBuf sel_order, sel_cand, sel_ptrs, walk_host;
-    DevBuf stage;                                   // host memory: two staged layer sheets [K|V][Tm + pad][dl]
-    cudaEvent_t ev_load[2] = {nullptr, nullptr};    // sheet loaded (copy stream)
-    cudaEvent_t ev_used[2] = {nullptr, nullptr};    // sheet's readers done (compute stream)
+    DevBuf stage;                        // host memory: a ring of staged layer sheets [K|V][Tm + pad][dl]
+    std::vector<cudaEvent_t> ev_load;    // per slot: sheet loaded (copy stream)
+    std::vector<cudaEvent_t> ev_used;    // per slot: the sheet's readers are done (compute stream)
     ~Batch() {
         for (auto e : ev_load) if (e) cudaEventDestroy(e);
         for (auto e : ev_used) if (e) cudaEventDestroy(e);

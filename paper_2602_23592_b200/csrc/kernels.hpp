@@ -35,6 +35,12 @@ void launch_copy_cached(const void* const* ksrc, const void* const* vsrc, const 
                         const int32_t* nrows, int n_entries, int64_t row_bytes, void* kdst,
                         void* vdst, int max_rows, cudaStream_t st);
 
+// Host -> device bytes through kernel parameters (no copy engine, no host sync).
+void upload_bytes(void* dst, const void* src, size_t n, cudaStream_t st);
+
+// d0[0, bytes) = s0, d1[0, bytes) = s1 on the SMs (pointers by value).
+void launch_copy2(void* d0, const void* s0, void* d1, const void* s1, int64_t bytes, cudaStream_t st);
+
 // Batched device-to-device copy of n blocks (sizes multiples of 16 bytes).
 void launch_batch_copy(const void* const* src, void* const* dst, const int64_t* bytes, int n, cudaStream_t st);
 

@@ -1,6 +1,7 @@
 // kernels_common.cu -- K0 init, K1 embed, row gathers, K4 merged-KV assembly,
 // K6 summary reduce, K7 selector, K11 logits.  All HBM- or latency-bound
 // integer/fp64 work: coalesced 16-byte accesses, grids sized in SM multiples.
+#include <cstring>
 #include "kernels.hpp"
 
 #include <cfloat>
@@ -123,6 +124,56 @@ void launch_batch_copy(const void* const* src, void* const* dst, const int64_t* 
     if (n <= 0) return;
     batch_copy_kernel<<<unsigned(std::min(n, kNumSMs * 16)), 256, 0, st>>>(
         reinterpret_cast<const int4* const*>(src), reinterpret_cast<int4* const*>(dst), bytes, n);
+    KEEP_LAUNCH_CHECK();
+}
+
+// Host -> device upload through the kernel's parameter block (<= 31 KB per
+// launch): the bytes travel with the launch, not through a copy engine, so a
+// small upload never queues behind the layer loads streaming on the copy
+// engines, and it never synchronises the host with the stream (pageable
+// cudaMemcpyAsync does both).
+constexpr int kParamWords = 31 * 256;  // 31 KB (the kernel parameter limit is 32,764 bytes)
+struct ParamBlob {
+    uint32_t w[kParamWords];
+};
+__global__ void param_copy_kernel(uint8_t* __restrict__ dst, const __grid_constant__ ParamBlob blob, int n) {
+    const int nw = n >> 2;
+    if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
+        uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+        for (int i = threadIdx.x; i < nw; i += blockDim.x) d[i] = blob.w[i];
+        for (int i = (nw << 2) + threadIdx.x; i < n; i += blockDim.x)
+            dst[i] = reinterpret_cast<const uint8_t*>(blob.w)[i];
+    } else {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = reinterpret_cast<const uint8_t*>(blob.w)[i];
+    }
+}
+
+void upload_bytes(void* dst, const void* src, size_t n, cudaStream_t st) {
+    static thread_local ParamBlob blob;
+    for (size_t off = 0; off < n; off += sizeof(ParamBlob)) {
+        const int m = int(std::min(n - off, sizeof(ParamBlob)));
+        std::memcpy(blob.w, static_cast<const uint8_t*>(src) + off, size_t(m));
+        param_copy_kernel<<<1, 256, 0, st>>>(static_cast<uint8_t*>(dst) + off, blob, m);
+        KEEP_LAUNCH_CHECK();
+    }
+}
+
+// Two contiguous device copies with the pointers passed by value (no upload,
+// no copy engine: small copies issued while the copy engines stream a layer).
+__global__ void copy2_kernel(int4* __restrict__ d0, const int4* __restrict__ s0, int4* __restrict__ d1,
+                             const int4* __restrict__ s1, int64_t nv) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < 2 * nv; i += int64_t(gridDim.x) * blockDim.x) {
+        if (i < nv) d0[i] = s0[i];
+        else d1[i - nv] = s1[i - nv];
+    }
+}
+
+void launch_copy2(void* d0, const void* s0, void* d1, const void* s1, int64_t bytes, cudaStream_t st) {
+    if (bytes <= 0) return;
+    if (bytes % 16) raise(KEEP_ERR_CONFIG, "copy2: size not a multiple of 16 bytes");
+    const int64_t nv = bytes / 16;
+    copy2_kernel<<<unsigned(std::min<int64_t>(ceil_div(2 * nv, 256), kNumSMs * 4)), 256, 0, st>>>(
+        static_cast<int4*>(d0), static_cast<const int4*>(s0), static_cast<int4*>(d1), static_cast<const int4*>(s1), nv);
     KEEP_LAUNCH_CHECK();
 }
 
