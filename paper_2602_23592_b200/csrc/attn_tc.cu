@@ -843,19 +843,27 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 // S[b] of chunk `it` is full, every MMA issued before Q.K^T(it)
                 // is complete -- P.V(it-2), the last one into O[b] -- and
                 // P.V(it) waits for p_full: O[b] is quiescent here.
-                float cm = -INFINITY;
+                // (two interleaved max chains: half the dependent latency)
+                float cm = -INFINITY, cm2 = -INFINITY;
                 if (full_half) {
 #pragma unroll
                     for (int c = 0; c < 2; ++c)
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj) cm = fmaxf(cm, __uint_as_float(sv[c][jj]));
+                        for (int jj = 0; jj < 32; jj += 2) {
+                            cm = fmaxf(cm, __uint_as_float(sv[c][jj]));
+                            cm2 = fmaxf(cm2, __uint_as_float(sv[c][jj + 1]));
+                        }
                 } else {
 #pragma unroll
                     for (int c = 0; c < 2; ++c)
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj)
+                        for (int jj = 0; jj < 32; jj += 2) {
                             if (unsigned(c * 32 + jj - kv0) < unsigned(kv1 - kv0)) cm = fmaxf(cm, __uint_as_float(sv[c][jj]));
+                            if (unsigned(c * 32 + jj + 1 - kv0) < unsigned(kv1 - kv0))
+                                cm2 = fmaxf(cm2, __uint_as_float(sv[c][jj + 1]));
+                        }
                 }
+                cm = fmaxf(cm, cm2);
                 float* xm = part + ((((it >> 1) & 1) * NTEAM + team) * 2) * TM;  // [parity][team][half][TM]
                 xm[half * TM + r] = cm;
                 named_sync(2 + team * 4 + q, 64);  // the two key halves of rows 32q.. in this team
@@ -869,6 +877,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 }
                 m_eff = fm == -INFINITY ? 0.f : fm;
                 const uint32_t tp = tm_s0 + lane_base + uint32_t(b * TK + half * 64);
+                float ls[2] = {0.f, 0.f};  // (one sum chain per 32-key half)
                 auto make_p = [&](auto masked, int c) {
                     uint32_t hv[16];
 #pragma unroll
@@ -881,7 +890,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                             p1 = unsigned(kk + 1 - kv0) < unsigned(kv1 - kv0) ? p1 : 0.f;
                         }
                         hv[i] = pack_bf16(p0, p1);
-                        lsum += p0 + p1;
+                        ls[c] += p0 + p1;
                     }
                     tmem_st16(tp + uint32_t(16 * c), hv);
                 };
@@ -892,6 +901,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     make_p(std::true_type{}, 0);
                     make_p(std::true_type{}, 1);
                 }
+                lsum += ls[0] + ls[1];
                 if (o_started && __any_sync(0xffffffffu, resc)) {
                     const uint32_t to = tm_o + lane_base + uint32_t(b * 128 + half * 64);
 #pragma unroll
