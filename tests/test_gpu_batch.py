@@ -148,3 +148,23 @@ def test_batch_selective_prefill_alias_layers(mode):
             q = slice(-len(inst.query), None)
             a, e = g["final_hidden"][q].astype(np.float64), r["final_hidden"][q].astype(np.float64)
             assert np.max(np.abs(a - e)) <= 3e-2 * np.max(np.abs(e)), b
+
+
+@pytest.mark.parametrize("B,qlen,multihop", [(1, 1, True), (3, 1, False), (20, 5, True)])
+def test_batch_edges(B, qlen, multihop):
+    """One query, one-token queries, the single-hop ablation
+    (recompute.hpp:166-176) and more queries than one logits launch covers."""
+    seed, S, L, H, d, V = 44, 14, 4, 2, 32, 128
+    inst = make_instance_layout(seed, S, V, qlen=qlen)
+    lay = kb.Layout(inst.seg_len, inst.tokens)
+    Q = batch_queries(seed, B, qlen, V, inst.query)
+    sched = kb.ratio_schedule(L, 0.5)
+    with kb.Context(L, H, d, 2 * d, V, seed) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay)
+        batch = ctx.plan_keep_batch(lay, Q, sched, multihop=multihop, final_hidden=True)
+        singles = [ctx.plan_keep(lay, Q[b], sched, multihop=multihop) for b in range(B)]
+    for g, r in zip(batch, singles):
+        assert np.array_equal(g["plan"], r["plan"]) and g["orders"] == r["orders"]
+        assert np.array_equal(g["final_hidden"], r["final_hidden"])
+        assert np.array_equal(g["last_logits"], r["last_logits"])
