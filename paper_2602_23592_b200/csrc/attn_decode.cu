@@ -37,7 +37,7 @@ constexpr int RED_OFF = DST * STAGE_B;  // barriers + per-warp row stats after t
 constexpr int SMEM_B = 1024 + RED_OFF + 2 * DST * 8 + 3 * DWARPS * 16 * 4 + 16 * 4;
 
 struct DecArgs {
-    int n, H, d;            // rows (<= 16), this rank's heads, row stride (= H * 128)
+    int n, H, d;            // rows (<= 64: blocks of 16 on grid z), this rank's heads, row stride (= H * 128)
     int kv_hi;              // keys [0, kv_hi) are visible to some row
     int nsplit, cps;        // key splits, 64-key stages per split
     const __nv_bfloat16* q; // [n x d], pre-scaled by log2(e) / sqrt(128)
@@ -70,6 +70,7 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant
     float* row_L = row_M + 16;                             // [16] merged sum
 
     const int h = blockIdx.x, sp = blockIdx.y;
+    const int r_off = blockIdx.z * 16;  // this CTA's block of (up to) 16 rows
     const int nch_total = int(ceil_div(a.kv_hi, DK));
     const int c0 = sp * a.cps;
     const int nch = max(0, min(nch_total, c0 + a.cps) - c0);
@@ -104,21 +105,23 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant
     }
 
     const int g = lane >> 2, i4 = lane & 3;
-    const int n = a.n;
+    const int n = min(16, a.n - r_off);  // rows of this block
+    const __nv_bfloat16* qblk = a.q + int64_t(r_off) * a.d;
+    const int32_t* rows = a.rows + r_off;
     // Q fragments (A operand, rows g and g + 8; rows >= n are zero)
     uint32_t qa[8][4];
     {
         const int64_t b0 = int64_t(g) * a.d + h * DH + 2 * i4, b1 = int64_t(g + 8) * a.d + h * DH + 2 * i4;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-            qa[ks][0] = ld_q32(a.q, g, n, b0 + ks * 16);
-            qa[ks][1] = ld_q32(a.q, g + 8, n, b1 + ks * 16);
-            qa[ks][2] = ld_q32(a.q, g, n, b0 + ks * 16 + 8);
-            qa[ks][3] = ld_q32(a.q, g + 8, n, b1 + ks * 16 + 8);
+            qa[ks][0] = ld_q32(qblk, g, n, b0 + ks * 16);
+            qa[ks][1] = ld_q32(qblk, g + 8, n, b1 + ks * 16);
+            qa[ks][2] = ld_q32(qblk, g, n, b0 + ks * 16 + 8);
+            qa[ks][3] = ld_q32(qblk, g + 8, n, b1 + ks * 16 + 8);
         }
     }
-    const int t0 = g < n ? a.rows[g] : -1, t1 = g + 8 < n ? a.rows[g + 8] : -1;
-    const int tmin = a.rows[0];
+    const int t0 = g < n ? rows[g] : -1, t1 = g + 8 < n ? rows[g + 8] : -1;
+    const int tmin = rows[0];
     float o[16][4];
 #pragma unroll
     for (int nt = 0; nt < 16; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
@@ -249,14 +252,15 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant
 #pragma unroll
         for (int w = 0; w < DWARPS; ++w) acc += ob[(w * 16 + r) * DH + c];
         const int64_t col = int64_t(h) * DH + c;
+        const int64_t rg = r_off + r;  // row of the launch
         if (a.nsplit == 1) {
             const float L = row_L[r];
-            a.ctx[int64_t(r) * a.d + col] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+            a.ctx[rg * a.d + col] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
         } else {
-            a.o_part[(int64_t(sp) * n + r) * a.d + col] = acc;
+            a.o_part[(int64_t(sp) * a.n + rg) * a.d + col] = acc;
             if (c == 0) {
-                a.m_part[(int64_t(sp) * n + r) * a.H + h] = row_M[r];
-                a.l_part[(int64_t(sp) * n + r) * a.H + h] = row_L[r];
+                a.m_part[(int64_t(sp) * a.n + rg) * a.H + h] = row_M[r];
+                a.l_part[(int64_t(sp) * a.n + rg) * a.H + h] = row_L[r];
             }
         }
     }
@@ -293,12 +297,12 @@ int decode_splits(int n_heads, int kv_hi) {
     return int(ceil_div(nch, cps));
 }
 
-bool decode_attention_fits(int n) { return n >= 1 && n <= 16; }
+bool decode_attention_fits(int n) { return n >= 1 && n <= 64; }
 
 int launch_attention_decode(const AttnTcLaunch& L, int kv_hi, cudaStream_t st) {
     const int n = L.n;
     if (n == 0 || kv_hi <= 0) return 0;
-    if (n > 16) raise(KEEP_ERR_CONFIG, "decode attention takes at most 16 rows");
+    if (n > 64) raise(KEEP_ERR_CONFIG, "decode attention takes at most 64 rows");
     static bool attr = [] {
         KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
         return true;
@@ -319,7 +323,8 @@ int launch_attention_decode(const AttnTcLaunch& L, int kv_hi, cudaStream_t st) {
     a.ctx = L.ctx;
     const CUtensorMap mk = make_map_bf16(L.k, kv_hi, L.d, L.d, DK);
     const CUtensorMap mv = make_map_bf16(L.v, kv_hi, L.d, L.d, DK);
-    attn_decode_kernel<<<dim3(unsigned(L.H), unsigned(a.nsplit)), DTHREADS, SMEM_B, st>>>(mk, mv, a);
+    attn_decode_kernel<<<dim3(unsigned(L.H), unsigned(a.nsplit), unsigned(ceil_div(n, 16))), DTHREADS, SMEM_B, st>>>(
+        mk, mv, a);
     KEEP_LAUNCH_CHECK();
     if (a.nsplit == 1) return 1;
     const int64_t nd = int64_t(n) * L.d;

@@ -340,18 +340,23 @@ __global__ void splitk_epilogue_kernel(float* __restrict__ acc, int M, int N, Ep
 // go to the fp32 split-K workspace with vector reductions whenever a CTA
 // leaves an n-block; splitk_epilogue_kernel applies the fused epilogue.
 constexpr int SK_ST = 4;
-constexpr int SK_BOXB = 64 * 64 * 2;             // B box: 64 n x 64 k
-constexpr int SK_BOXA = 16 * 64 * 2;             // A box: 16 rows x 64 k
-constexpr int SK_STAGE = 4 * SK_BOXB + 4 * SK_BOXA;
-constexpr int SK_SMEM = 1024 + SK_ST * SK_STAGE + 2 * SK_ST * 8;
+constexpr int SK_BOXB = 64 * 64 * 2;  // B box: 64 n x 64 k
 constexpr int SK_THREADS = 5 * 32;
+template <int MT>  // m16 tiles: M <= 16 * MT
+struct SkCfg {
+    static constexpr int BOXA = 16 * MT * 64 * 2;  // A box: 16 MT rows x 64 k
+    static constexpr int STAGE = 4 * SK_BOXB + 4 * BOXA;
+    static constexpr int SMEM = 1024 + SK_ST * STAGE + 2 * SK_ST * 8;
+};
 
+template <int MT>
 __global__ void __launch_bounds__(SK_THREADS, 1)
 gemm_skinny_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int M, int N,
                    int K, float* __restrict__ acc) {
+    using SC = SkCfg<MT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + SK_ST * SK_STAGE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sm + SK_ST * SC::STAGE);
     uint64_t* empty = full + SK_ST;
     const int nb_count = int(ceil_div(N, 64)), ks_count = int(ceil_div(K, 256));
     const int64_t units = int64_t(nb_count) * ks_count;
@@ -372,33 +377,42 @@ gemm_skinny_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant
             for (int64_t u = u0; u < u1; ++u) {
                 const int j = int(u - u0), s = j % SK_ST;
                 if (j >= SK_ST) mbar_wait(&empty[s], uint32_t(j / SK_ST - 1) & 1u);
-                mbar_expect_tx(&full[s], SK_STAGE);
+                mbar_expect_tx(&full[s], SC::STAGE);
                 const int nb = int(u / ks_count), k0 = int(u % ks_count) * 256;
-                uint8_t* st = sm + s * SK_STAGE;
+                uint8_t* st = sm + s * SC::STAGE;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     tma_load_2d(st + q * SK_BOXB, &tb, &full[s], k0 + 64 * q, nb * 64);
-                    tma_load_2d(st + 4 * SK_BOXB + q * SK_BOXA, &ta, &full[s], k0 + 64 * q, 0);
+                    tma_load_2d(st + 4 * SK_BOXB + q * SC::BOXA, &ta, &full[s], k0 + 64 * q, 0);
                 }
             }
         }
         return;
     }
     const int g = lane >> 2, i4 = lane & 3, mat = lane >> 3;
-    float c[8][4];
+    float c[MT][8][4];
 #pragma unroll
-    for (int nt = 0; nt < 8; ++nt) c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) c[mt][nt][0] = c[mt][nt][1] = c[mt][nt][2] = c[mt][nt][3] = 0.f;
     int cur_nb = -1;
     auto flush = [&](int nb) {
-        const int r0 = g, r1 = g + 8;
 #pragma unroll
-        for (int nt = 0; nt < 8; ++nt) {
-            const int col = nb * 64 + nt * 8 + 2 * i4;
-            if (col < N) {
-                if (r0 < M) atomicAdd(reinterpret_cast<float2*>(acc + int64_t(r0) * N + col), make_float2(c[nt][0], c[nt][1]));
-                if (r1 < M) atomicAdd(reinterpret_cast<float2*>(acc + int64_t(r1) * N + col), make_float2(c[nt][2], c[nt][3]));
+        for (int mt = 0; mt < MT; ++mt) {
+            const int r0 = 16 * mt + g, r1 = r0 + 8;
+#pragma unroll
+            for (int nt = 0; nt < 8; ++nt) {
+                const int col = nb * 64 + nt * 8 + 2 * i4;
+                if (col < N) {
+                    if (r0 < M)
+                        atomicAdd(reinterpret_cast<float2*>(acc + int64_t(r0) * N + col),
+                                  make_float2(c[mt][nt][0], c[mt][nt][1]));
+                    if (r1 < M)
+                        atomicAdd(reinterpret_cast<float2*>(acc + int64_t(r1) * N + col),
+                                  make_float2(c[mt][nt][2], c[mt][nt][3]));
+                }
+                c[mt][nt][0] = c[mt][nt][1] = c[mt][nt][2] = c[mt][nt][3] = 0.f;
             }
-            c[nt][0] = c[nt][1] = c[nt][2] = c[nt][3] = 0.f;
         }
     };
     for (int64_t u = u0; u < u1; ++u) {
@@ -409,20 +423,28 @@ gemm_skinny_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant
             cur_nb = nb;
         }
         mbar_wait(&full[s], uint32_t(j / SK_ST) & 1u);
-        const uint32_t sb = smem_u32(sm + s * SK_STAGE);
-        const uint32_t bb = sb + warp * SK_BOXB, ab = sb + 4 * SK_BOXB + warp * SK_BOXA;
+        const uint32_t sb = smem_u32(sm + s * SC::STAGE);
+        const uint32_t bb = sb + warp * SK_BOXB, ab = sb + 4 * SK_BOXB + warp * SC::BOXA;
 #pragma unroll
         for (int kp = 0; kp < 2; ++kp) {  // two k-steps of 16 per pass
-            uint32_t a0[4], a1[4];
-            // A (m16 x k16): matrices (rows 0-7, k 0-7), (rows 8-15, k 0-7), (rows 0-7, k 8-15), (rows 8-15, k 8-15)
-            ldsm_x4(ab + swz(((mat & 1) << 3) + (lane & 7), kp * 4 + (mat >> 1)), a0[0], a0[1], a0[2], a0[3]);
-            ldsm_x4(ab + swz(((mat & 1) << 3) + (lane & 7), kp * 4 + 2 + (mat >> 1)), a1[0], a1[1], a1[2], a1[3]);
+            uint32_t a0[MT][4], a1[MT][4];
+            // A (m16 x k16) of m-tile mt: matrices (rows 0-7, k 0-7), (rows 8-15, k 0-7),
+            // (rows 0-7, k 8-15), (rows 8-15, k 8-15); the 16 MT-row box keeps the swizzle row
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int ar = 16 * mt + ((mat & 1) << 3) + (lane & 7);
+                ldsm_x4(ab + swz(ar, kp * 4 + (mat >> 1)), a0[mt][0], a0[mt][1], a0[mt][2], a0[mt][3]);
+                ldsm_x4(ab + swz(ar, kp * 4 + 2 + (mat >> 1)), a1[mt][0], a1[mt][1], a1[mt][2], a1[mt][3]);
+            }
 #pragma unroll
             for (int nt = 0; nt < 8; ++nt) {
                 uint32_t b0, b1, b2, b3;
                 ldsm_x4(bb + swz(nt * 8 + (lane & 7), kp * 4 + mat), b0, b1, b2, b3);
-                mma16816(c[nt], a0, b0, b1);
-                mma16816(c[nt], a1, b2, b3);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    mma16816(c[mt][nt], a0[mt], b0, b1);
+                    mma16816(c[mt][nt], a1[mt], b2, b3);
+                }
             }
         }
         __syncwarp();
@@ -443,23 +465,31 @@ float* splitk_workspace(int M, int N, cudaStream_t st) {
     return ws.as<float>();
 }
 
-void launch_skinny(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
-                   const EpiArgs& epi, cudaStream_t st, int max_ctas) {
+template <int MT>
+void launch_skinny_mt(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
+                      const EpiArgs& epi, cudaStream_t st, int max_ctas) {
     static bool attr = [] {
-        KEEP_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_SMEM));
+        KEEP_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       SkCfg<MT>::SMEM));
         return true;
     }();
     (void)attr;
-    const CUtensorMap ta = make_map_bf16(A, M, K, lda, 16);
+    const CUtensorMap ta = make_map_bf16(A, M, K, lda, 16 * MT);
     const CUtensorMap tb = make_map_bf16(Bt, N, K, ldb, 64);
     const int64_t units = ceil_div(N, 64) * ceil_div(K, 256);
     const int grid = int(std::min<int64_t>(units, std::max(1, std::min(max_ctas, kNumSMs))));
     float* acc = splitk_workspace(M, N, st);
-    gemm_skinny_kernel<<<grid, SK_THREADS, SK_SMEM, st>>>(ta, tb, M, N, K, acc);
+    gemm_skinny_kernel<MT><<<grid, SK_THREADS, SkCfg<MT>::SMEM, st>>>(ta, tb, M, N, K, acc);
     KEEP_LAUNCH_CHECK();
     const int work = M * (N / 32);
     splitk_epilogue_kernel<<<unsigned(std::min<int64_t>(ceil_div(work, 128), kNumSMs * 4)), 128, 0, st>>>(acc, M, N, epi);
     KEEP_LAUNCH_CHECK();
+}
+
+void launch_skinny(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
+                   const EpiArgs& epi, cudaStream_t st, int max_ctas) {
+    if (M <= 16) launch_skinny_mt<1>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas);
+    else launch_skinny_mt<2>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas);
 }
 
 template <int BN, int AR = BM>
@@ -504,7 +534,7 @@ void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* 
     if (K % BK != 0 || N % 32 != 0) raise(KEEP_ERR_CONFIG, "tcgen05 GEMM needs K % 64 == 0 and N % 32 == 0");
     // a few rows (deep layers: the query): 32-row A stages and split-K so that
     // ~4 waves of (tile, k-slice) units stream the weights through every SM
-    if (M <= 16 && skinny_enabled()) {
+    if (M <= 32 && skinny_enabled()) {
         launch_skinny(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas);
         return;
     }

@@ -127,6 +127,7 @@ def test_decode_attention_query_rows(seed, S, H, d, qlen):
     plan = np.zeros((L, S), np.uint8)
     plan[0] = 1
     plan[1, : S // 3] = 1
+    plan[2, : min(3, S // 3)] = 1  # 17..64 rows: the decode kernel's row blocks
     out = {}
     for mode in (kb.FAST, kb.PARITY):
         with kb.Context(L, H, d, mlp, V, seed, mode) as ctx:
