@@ -544,9 +544,19 @@ void launch_gemm_bf16(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* 
         launch_bn<64, 32>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas, ksplit);
         return;
     }
-    // few row blocks: narrow N tiles so enough CTAs stream the weights
-    if (ceil_div(M, BM) * ceil_div(N, 256) >= kNumSMs || N % 256 != 0)
+    // 128x256 tiles whenever they fill most of a wave: 64-wide tiles feed the
+    // tensor core at well under half the rate (the A tile is re-staged per 64
+    // columns).  Fewer tiles: split K across the idle SMs (fp32 reduction plus
+    // the fused-epilogue pass), else fall back to narrow tiles.
+    const int64_t t256 = ceil_div(M, BM) * ceil_div(N, 256);
+    const int ctas = std::max(1, std::min(max_ctas, kNumSMs));
+    if (t256 * 10 >= int64_t(ctas) * 7 || N % 256 != 0) {
         launch_bn<256>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas);
+        return;
+    }
+    const int ks = int(std::min<int64_t>(ctas / t256, (K / BK) / 8));
+    if (ks >= 2)
+        launch_bn<256>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas, ks);
     else
         launch_bn<64>(A, lda, Bt, ldb, M, N, K, epi, st, max_ctas);
 }

@@ -16,6 +16,8 @@ pytestmark = pytest.mark.gpu
     # skinny weight-stream path (M <= 16, mma.sync over TMA stages): ragged K stages / n-blocks
     (8, 5120, 5120, 16), (1, 32, 64, 16), (16, 13824, 5120, 16), (5, 1920, 5120, 16), (3, 96, 320, 16),
     (16, 5120, 13824, 16),
+    # few 128x256 tiles: one wave, or split along K
+    (1108, 3584, 18944, 0), (300, 5120, 5120, 0), (200, 3584, 13824, 0),
     # two m16 tiles (17..32 rows)
     (24, 5120, 5120, 16), (32, 13824, 5120, 16), (17, 96, 320, 16),
 ])
