@@ -727,6 +727,25 @@ double layer_estimate_ms(const Context& c, const Pass& p) {
     return (gemm / 1.1e15 + attn / 0.35e15) * 1e3;
 }
 
+// The four K4 argument arrays in one device buffer and one upload:
+// [ksrc ptrs][vsrc ptrs][dst rows][row counts].
+void upload_copy_args(Context& c, const std::vector<void*>& ks, const std::vector<void*>& vs,
+                      const std::vector<int32_t>& dr, const std::vector<int32_t>& nr, cudaStream_t st,
+                      const void* const** kp, const void* const** vp, const int32_t** dp, const int32_t** np) {
+    const size_t n = ks.size();
+    std::vector<uint8_t> blob(n * (2 * sizeof(void*) + 2 * sizeof(int32_t)));
+    std::memcpy(blob.data(), ks.data(), n * sizeof(void*));
+    std::memcpy(blob.data() + n * sizeof(void*), vs.data(), n * sizeof(void*));
+    std::memcpy(blob.data() + 2 * n * sizeof(void*), dr.data(), n * sizeof(int32_t));
+    std::memcpy(blob.data() + 2 * n * sizeof(void*) + n * sizeof(int32_t), nr.data(), n * sizeof(int32_t));
+    upload(c.d_ksrc, blob, st);
+    const uint8_t* b = c.d_ksrc.as<const uint8_t>();
+    *kp = reinterpret_cast<const void* const*>(b);
+    *vp = reinterpret_cast<const void* const*>(b + n * sizeof(void*));
+    *dp = reinterpret_cast<const int32_t*>(b + 2 * n * sizeof(void*));
+    *np = reinterpret_cast<const int32_t*>(b + 2 * n * sizeof(void*) + n * sizeof(int32_t));
+}
+
 // Replace the compact row set (rows only shrink): gather the residual rows.
 void set_rows(Context& c, Pass& p, const std::vector<int32_t>& rows_new, bool first) {
     cudaStream_t st = c.s_main;
@@ -874,13 +893,11 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
         double rows_copied = 0.0;
         for (int32_t r : nr) rows_copied += r;
         ProfScope ps(c.prof, KEEP_PROF_CACHED, st, 0.0, rows_copied * c.dl * c.elem * 4.0);
-        upload(c.d_ksrc, ks, st);
-        upload(c.d_vsrc, vs, st);
-        upload(c.d_cdst, dr, st);
-        upload(c.d_cn, nr, st);
-        launch_copy_cached(c.d_ksrc.as<const void*>(), c.d_vsrc.as<const void*>(), c.d_cdst.as<int32_t>(),
-                           c.d_cn.as<int32_t>(), int(ks.size()), int64_t(c.dl) * c.elem, p.kdst[l], p.vdst[l],
-                           maxr, st);
+        const void* const* kp;
+        const void* const* vp;
+        const int32_t *dp, *np;
+        upload_copy_args(c, ks, vs, dr, nr, st, &kp, &vp, &dp, &np);
+        launch_copy_cached(kp, vp, dp, np, int(ks.size()), int64_t(c.dl) * c.elem, p.kdst[l], p.vdst[l], maxr, st);
     }
     p.with_summary = p.summary_wanted;
     if (p.n == 0) {  // no computed rows: the summary is all zero
@@ -1478,12 +1495,11 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                 double rows_copied = 0.0;
                 for (int32_t r : nrr) rows_copied += r;
                 ProfScope ps(c.prof, KEEP_PROF_CACHED, st, 0.0, rows_copied * rowb * 4.0);
-                upload(c.d_ksrc, ks, st);
-                upload(c.d_vsrc, vs, st);
-                upload(c.d_cdst, dr, st);
-                upload(c.d_cn, nrr, st);
-                launch_copy_cached(c.d_ksrc.as<const void*>(), c.d_vsrc.as<const void*>(), c.d_cdst.as<int32_t>(),
-                                   c.d_cn.as<int32_t>(), int(ks.size()), int64_t(rowb), kvK, kvV, maxr, st);
+                const void* const* kp;
+                const void* const* vp;
+                const int32_t *dp, *np;
+                upload_copy_args(c, ks, vs, dr, nrr, st, &kp, &vp, &dp, &np);
+                launch_copy_cached(kp, vp, dp, np, int(ks.size()), int64_t(rowb), kvK, kvV, maxr, st);
             }
         }
         ensure_layer_scratch(c, P);

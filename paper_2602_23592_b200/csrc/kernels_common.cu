@@ -132,11 +132,12 @@ void launch_batch_copy(const void* const* src, void* const* dst, const int64_t* 
 // small upload never queues behind the layer loads streaming on the copy
 // engines, and it never synchronises the host with the stream (pageable
 // cudaMemcpyAsync does both).
-constexpr int kParamWords = 31 * 256;  // 31 KB (the kernel parameter limit is 32,764 bytes)
+template <int W>  // 32-bit words carried by one launch
 struct ParamBlob {
-    uint32_t w[kParamWords];
+    uint32_t w[W];
 };
-__global__ void param_copy_kernel(uint8_t* __restrict__ dst, const __grid_constant__ ParamBlob blob, int n) {
+template <int W>
+__global__ void param_copy_kernel(uint8_t* __restrict__ dst, const __grid_constant__ ParamBlob<W> blob, int n) {
     const int nw = n >> 2;
     if ((reinterpret_cast<uintptr_t>(dst) & 3) == 0) {
         uint32_t* d = reinterpret_cast<uint32_t*>(dst);
@@ -148,13 +149,24 @@ __global__ void param_copy_kernel(uint8_t* __restrict__ dst, const __grid_consta
     }
 }
 
+template <int W>
+void param_upload(uint8_t* dst, const uint8_t* src, int m, cudaStream_t st) {
+    static thread_local ParamBlob<W> blob;
+    std::memcpy(blob.w, src, size_t(m));
+    param_copy_kernel<W><<<1, 256, 0, st>>>(dst, blob, m);
+    KEEP_LAUNCH_CHECK();
+}
+
 void upload_bytes(void* dst, const void* src, size_t n, cudaStream_t st) {
-    static thread_local ParamBlob blob;
-    for (size_t off = 0; off < n; off += sizeof(ParamBlob)) {
-        const int m = int(std::min(n - off, sizeof(ParamBlob)));
-        std::memcpy(blob.w, static_cast<const uint8_t*>(src) + off, size_t(m));
-        param_copy_kernel<<<1, 256, 0, st>>>(static_cast<uint8_t*>(dst) + off, blob, m);
-        KEEP_LAUNCH_CHECK();
+    constexpr size_t kMax = 31 * 1024;  // the kernel parameter limit is 32,764 bytes
+    for (size_t off = 0; off < n; off += kMax) {
+        const int m = int(std::min(n - off, kMax));
+        uint8_t* d = static_cast<uint8_t*>(dst) + off;
+        const uint8_t* h = static_cast<const uint8_t*>(src) + off;
+        // (the launch carries the whole parameter block: size it to the data)
+        if (m <= 256) param_upload<64>(d, h, m, st);
+        else if (m <= 4096) param_upload<1024>(d, h, m, st);
+        else param_upload<int(kMax / 4)>(d, h, m, st);
     }
 }
 
@@ -258,7 +270,24 @@ __global__ void copy_cached_kernel(const void* const* __restrict__ ksrc,
     uint4* kd = reinterpret_cast<uint4*>(kdst + int64_t(dst_row[e]) * row_bytes);
     uint4* vd = reinterpret_cast<uint4*>(vdst + int64_t(dst_row[e]) * row_bytes);
     const int64_t total = int64_t(r1 - r0) * vec, base = int64_t(r0) * vec;
-    for (int64_t i = threadIdx.x; i < total; i += blockDim.x) {
+    // four 16-byte loads of K and four of V in flight per thread before the
+    // stores (the copy is latency-bound otherwise: ~10 rows per CTA)
+    constexpr int U = 4;
+    int64_t i = threadIdx.x;
+    for (; i + (U - 1) * int64_t(blockDim.x) < total; i += U * int64_t(blockDim.x)) {
+        uint4 k[U], v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            k[u] = __ldg(ks + base + i + u * blockDim.x);
+            v[u] = __ldg(vs + base + i + u * blockDim.x);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            kd[base + i + u * blockDim.x] = k[u];
+            vd[base + i + u * blockDim.x] = v[u];
+        }
+    }
+    for (; i < total; i += blockDim.x) {
         kd[base + i] = ks[base + i];
         vd[base + i] = vs[base + i];
     }
