@@ -627,8 +627,16 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA
-        if (lane == 0 && niter > 0) {
+        // The whole warp walks the schedule (waits, descriptors: warp-uniform
+        // values in uniform registers) and one elected lane issues each group
+        // of tcgen05.mma / commits -- no per-instruction divergence loop.
+        if (niter > 0) {
             mbar_wait(q_full, 0);
+            const uint32_t qt = smem_u32(sm + LY::Q_OFF);
+            const uint64_t qd = smem_desc(qt);
+            // k-step ks of 16 elements across the two 64-wide boxes of a tile:
+            // + ((ks >> 2) * BOX_BYTES + (ks & 3) * 32) in the 16-byte address field
+            auto koff = [](int ks) { return uint64_t(((ks >> 2) * BOX_BYTES + (ks & 3) * 32) >> 4); };
             // CTX: O += hi_j . V_j ; BINS[bins_buf(j)] = hi_j . Z_j + lo_j . Z_j,
             // P(j) in S[j&1]: half h's hi at columns 64h..64h+31, lo at +32
             auto pv = [&](int j) {
@@ -637,49 +645,57 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 fence_after();
                 const uint32_t pb = tm_s0 + uint32_t((j & 1) * TK);
                 const uint32_t vt = smem_u32(sm + LY::VSTAGE_OFF + (j & 1) * LY::VSTAGE);
+                const uint64_t vd = desc_mn(vt);
                 // FLASH: one O accumulator per team (columns 256 + 128 team),
                 // each started by the team's first chunk
                 const uint32_t to = MODE == MODE_FLASH ? tm_o + uint32_t((j & 1) * 128) : tm_o;
                 const int jacc = MODE == MODE_FLASH ? (j >> 1) : j;
-                if (a.dbg != 2)
-#pragma unroll
-                for (int ks = 0; ks < TK / 16; ++ks)
-                    umma_ts(to, pb + uint32_t(64 * (ks >> 2) + 8 * (ks & 3)), desc_mn(vt + uint32_t(ks) * 2048u),
-                            IDESC_VMN, (jacc | ks) ? 1u : 0u);
-                if (bins) {
-                    const uint32_t zt = vt + TILE_BYTES;
-                    const uint32_t tb = tm_b + uint32_t(bins_buf(j) * NB);
-                    const int nplo = a.dbg == 1 ? 1 : 2;
-#pragma unroll
-                    for (int plo = 0; plo < 2; ++plo)
-                        if (plo < nplo)
+                if (elect_one()) {
+                    if (a.dbg != 2)
 #pragma unroll
                         for (int ks = 0; ks < TK / 16; ++ks)
-                            umma_ts(tb, pb + uint32_t(64 * (ks >> 2) + 32 * plo + 8 * (ks & 3)),
-                                    smem_desc(zt + uint32_t(ks >> 2) * (LY::ZB / 2) + uint32_t(ks & 3) * 32u), IDESC_B,
-                                    (plo | ks) ? 1u : 0u);
-                    umma_commit(&bins_full[bins_buf(j)]);
+                            umma_ts(to, pb + uint32_t(64 * (ks >> 2) + 8 * (ks & 3)), vd + uint64_t(ks) * 128u,
+                                    IDESC_VMN, (jacc | ks) ? 1u : 0u);
+                    if (bins) {
+                        const uint32_t zt = vt + TILE_BYTES;
+                        const uint64_t zd = smem_desc(zt);
+                        const uint32_t tb = tm_b + uint32_t(bins_buf(j) * NB);
+                        const int nplo = a.dbg == 1 ? 1 : 2;
+#pragma unroll
+                        for (int plo = 0; plo < 2; ++plo)
+                            if (plo < nplo)
+#pragma unroll
+                                for (int ks = 0; ks < TK / 16; ++ks)
+                                    umma_ts(tb, pb + uint32_t(64 * (ks >> 2) + 32 * plo + 8 * (ks & 3)),
+                                            zd + uint64_t(((ks >> 2) * (LY::ZB / 2) + (ks & 3) * 32) >> 4), IDESC_B,
+                                            (plo | ks) ? 1u : 0u);
+                        umma_commit(&bins_full[bins_buf(j)]);
+                    }
+                    umma_commit(&vempty[j & 1]);
                 }
-                umma_commit(&vempty[j & 1]);
+                __syncwarp();
             };
-            const uint32_t qt = smem_u32(sm + LY::Q_OFF);
             for (int it = 0; it < niter; ++it) {
                 const int s = it % LY::ST, b = it & 1;
                 mbar_wait(&full[s], (it / LY::ST) & 1);
                 // CTX: S[b] held P(it-2), consumed by MMAs issued earlier (issue order)
                 if (MODE == MODE_STATS) mbar_wait(&s_empty[b], ((it >> 1) & 1) ^ 1);
                 fence_after();
-                const uint32_t kt = smem_u32(sm + LY::STAGE_OFF + s * LY::STAGE);
+                const uint64_t kd = smem_desc(smem_u32(sm + LY::STAGE_OFF + s * LY::STAGE));
+                if (elect_one()) {
 #pragma unroll
-                for (int ks = 0; ks < DH / 16; ++ks)
-                    umma(tm_s0 + uint32_t(b * TK), desc_k(qt, ks), desc_k(kt, ks), IDESC, ks ? 1u : 0u);
-                umma_commit(&s_full[b]);
-                umma_commit(&empty[s]);
+                    for (int ks = 0; ks < DH / 16; ++ks)
+                        umma(tm_s0 + uint32_t(b * TK), qd + koff(ks), kd + koff(ks), IDESC, ks ? 1u : 0u);
+                    umma_commit(&s_full[b]);
+                    umma_commit(&empty[s]);
+                }
+                __syncwarp();
                 if (MODE != MODE_STATS && it > 0) pv(it - 1);
             }
             if (MODE != MODE_STATS) {
                 pv(niter - 1);
-                umma_commit(o_full);
+                if (elect_one()) umma_commit(o_full);
+                __syncwarp();
             }
         }
     } else if (warp >= 3) {
