@@ -235,7 +235,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
+        {  // ---------------- MMA issuer: the warp walks the schedule, one elected lane issues
             constexpr uint32_t idesc = instr_desc(BM, BN);
             int stage = 0;
             uint32_t phase = 0;
@@ -253,18 +253,22 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                     fence_after();
                     const uint32_t sa = smem_u32(smem + stage * CF::STAGE_BYTES);
                     const uint64_t ad = smem_desc(sa), bd = smem_desc(sa + CF::A_BYTES);
+                    if (elect_one()) {
 #pragma unroll
-                    for (int k = 0; k < BK / UMMA_K; ++k) {
-                        // advance 16 bf16 = 32 bytes along K inside the swizzle atom
-                        umma(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb > kb0 || k) ? 1u : 0u);
+                        for (int k = 0; k < BK / UMMA_K; ++k) {
+                            // advance 16 bf16 = 32 bytes along K inside the swizzle atom
+                            umma(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc, (kb > kb0 || k) ? 1u : 0u);
+                        }
+                        umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
                     }
-                    umma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+                    __syncwarp();
                     if (++stage == CF::STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                if (elect_one()) umma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                __syncwarp();
             }
         }
     } else if (warp >= 4) {  // ---------------- epilogue warps
