@@ -893,20 +893,24 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                 }
                 m_eff = fm == -INFINITY ? 0.f : fm;
                 const uint32_t tp = tm_s0 + lane_base + uint32_t(b * TK + half * 64);
-                float ls[2] = {0.f, 0.f};  // (one sum chain per 32-key half)
+                // packed fp32x2 arithmetic (FADD2): half the subtract / sum instructions
+                float2 ls2 = make_float2(0.f, 0.f);
+                const float2 negm = make_float2(-m_eff, -m_eff);
                 auto make_p = [&](auto masked, int c) {
                     uint32_t hv[16];
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
                         const int kk = 32 * c + 2 * i;
-                        float p0 = ex2(__uint_as_float(sv[c][2 * i]) - m_eff);
-                        float p1 = ex2(__uint_as_float(sv[c][2 * i + 1]) - m_eff);
+                        const float2 x = __fadd2_rn(make_float2(__uint_as_float(sv[c][2 * i]),
+                                                                __uint_as_float(sv[c][2 * i + 1])), negm);
+                        float p0 = ex2(x.x);
+                        float p1 = ex2(x.y);
                         if constexpr (decltype(masked)::value) {
                             p0 = unsigned(kk - kv0) < unsigned(kv1 - kv0) ? p0 : 0.f;
                             p1 = unsigned(kk + 1 - kv0) < unsigned(kv1 - kv0) ? p1 : 0.f;
                         }
                         hv[i] = pack_bf16(p0, p1);
-                        ls[c] += p0 + p1;
+                        ls2 = __fadd2_rn(ls2, make_float2(p0, p1));
                     }
                     tmem_st16(tp + uint32_t(16 * c), hv);
                 };
@@ -917,7 +921,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                     make_p(std::true_type{}, 0);
                     make_p(std::true_type{}, 1);
                 }
-                lsum += ls[0] + ls[1];
+                lsum += ls2.x + ls2.y;
                 if (o_started && __any_sync(0xffffffffu, resc)) {
                     const uint32_t to = tm_o + lane_base + uint32_t(b * 128 + half * 64);
 #pragma unroll
