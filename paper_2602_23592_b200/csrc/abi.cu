@@ -313,6 +313,14 @@ int small_n_threshold() {
 }
 bool use_tc_attention(const Context& c, const Pass& p) { return use_tc_attention(c) && p.n > small_n_threshold(); }
 
+bool batch_multi_decode() {  // KEEP_BATCH_MULTI=0: per-query decode in batches (A/B)
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_BATCH_MULTI");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 // Few computed rows and no summary to bin (the layers after the walk):
 // flash decoding (attn_decode.cu).  KEEP_ATTN_DECODE=0 keeps the two-pass
 // tensor-core kernel (A/B).
@@ -1505,7 +1513,21 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
         ensure_layer_scratch(c, P);
         layer_qkv(c, P, l);
         const size_t qbytes = size_t(qlen) * rowb;
+        // all-reused queries (FAST, no summary read): one multi-query decode over
+        // the shared sheet instead of one attention each (the sheet is read
+        // once through L2 for all of them, and their query rows stay put)
+        std::vector<char> multi(B, 0);
+        int n_multi = 0;
+        if (l > 0 && c.fast && c.dh == 128 && qlen <= 16 && batch_multi_decode()) {
+            for (int b = 0; b < B; ++b)
+                if (alias[b] && !wanted[b]) {
+                    multi[b] = 1;
+                    ++n_multi;
+                }
+            if (n_multi < 2) std::fill(multi.begin(), multi.end(), 0), n_multi = 0;
+        }
         for (int b = 0; b < B; ++b) {
+            if (multi[b]) continue;
             Pass& v = *bt.views[b];
             v.with_summary = wanted[b] != 0;
             const uint8_t* qb = static_cast<const uint8_t*>(P.q.p) + size_t(off[b]) * dl * es;
@@ -1537,6 +1559,34 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
             if (l == 0 && b > 0 && v.with_summary)
                 KEEP_CUDA(cudaMemcpyAsync(v.summ.as<double>() + S, bt.views[0]->summ.as<double>() + S,
                                           sizeof(double) * size_t(S) * S, cudaMemcpyDeviceToDevice, st));
+        }
+        if (n_multi > 0) {
+            const size_t asheet = host_ar ? ssheet : size_t(c.alias_arena->rows) * rowb;
+            uint8_t* ak = host_ar ? stage[l % NS] : static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * asheet;
+            DecodeMulti dm;
+            dm.H = c.Hl;
+            dm.d = dl;
+            dm.qlen = qlen;
+            dm.kv_mem = Tm;
+            dm.own_rows = int(B * Tp);
+            dm.k_mem = ak;
+            dm.v_mem = ak + asheet;
+            dm.k_own = kvK;
+            dm.v_own = kvV;
+            dm.q = P.q.p;
+            dm.ctx = P.ctxb.as<__nv_bfloat16>();
+            int first = -1;
+            for (int b = 0; b < B; ++b) {
+                if (!multi[b]) continue;
+                if (first < 0) first = b;
+                bt.views[b]->with_summary = false;
+                dm.qrow0.push_back(int(b * Tp + Tm));
+                dm.qoff.push_back(off[b]);
+            }
+            dm.rows = bt.views[first]->d_rows.as<int32_t>();  // positions Tm.. (the same for every query)
+            const double pairs = double(n_multi) * qlen * (Tm + (qlen + 1) / 2.0);
+            ProfScope ps(c.prof, KEEP_PROF_DECODE, st, 4.0 * dl * pairs, 2.0 * rowb * (Tm + double(n_multi) * qlen), 1);
+            ps.kernels = launch_attention_decode_multi(dm, st);
         }
         if (host_ar && l > 0) {  // this layer's slot is free once its attention has run
             KEEP_CUDA(cudaEventRecord(bt.ev_used[l % NS], st));

@@ -36,6 +36,8 @@ constexpr int STAGE_B = 4 * BOX_B;      // K dh 0-63, K dh 64-127, V dh 0-63, V 
 constexpr int RED_OFF = DST * STAGE_B;  // barriers + per-warp row stats after the stages
 constexpr int SMEM_B = 1024 + RED_OFF + 2 * DST * 8 + 3 * DWARPS * 16 * 4 + 16 * 4;
 
+constexpr int kMaxMulti = 64;  // queries per multi-instance launch
+
 struct DecArgs {
     int n, H, d;            // rows (<= 64: blocks of 16 on grid z), this rank's heads, row stride (= H * 128)
     int kv_hi;              // keys [0, kv_hi) are visible to some row
@@ -46,6 +48,13 @@ struct DecArgs {
     float* l_part;
     float* o_part;          // [nsplit x n x d]
     __nv_bfloat16* ctx;     // [n x d]
+    // MULTI (a batch's all-reused queries, one per grid x): keys [0, kv_mem)
+    // come from the shared memory sheet (mk, mv), keys [kv_mem, kv_hi) -- the
+    // query's own rows -- from (mk2, mv2) at row qrow0[z] + key - kv_mem; the
+    // query's q / ctx rows start at qoff[z]
+    int kv_mem;
+    int qrow0[kMaxMulti];
+    int qoff[kMaxMulti];
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -58,8 +67,11 @@ __device__ __forceinline__ uint32_t ld_q32(const __nv_bfloat16* q, int r, int n,
     return r < n ? *reinterpret_cast<const uint32_t*>(q + off) : 0u;
 }
 
+template <bool MULTI>
 __global__ void __launch_bounds__(DTHREADS, 2)
-attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv, DecArgs a) {
+attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv,
+                   const __grid_constant__ CUtensorMap mk2, const __grid_constant__ CUtensorMap mv2,
+                   const __grid_constant__ DecArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + RED_OFF);
@@ -69,11 +81,15 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant
     float* row_M = red_l + DWARPS * 16;                    // [16] merged max
     float* row_L = row_M + 16;                             // [16] merged sum
 
-    const int h = blockIdx.x, sp = blockIdx.y;
-    const int r_off = blockIdx.z * 16;  // this CTA's block of (up to) 16 rows
-    const int nch_total = int(ceil_div(a.kv_hi, DK));
+    // single: grid (head, split, 16-row block); MULTI: grid (query, head), one split
+    const int h = MULTI ? blockIdx.y : blockIdx.x, sp = MULTI ? 0 : blockIdx.y;
+    const int z = MULTI ? blockIdx.x : 0;
+    const int r_off = MULTI ? 0 : blockIdx.z * 16;  // this CTA's block of (up to) 16 rows
+    const int kv_mem = MULTI ? a.kv_mem : a.kv_hi;   // keys served by (mk, mv)
+    const int nch_total = int(ceil_div(kv_mem, DK));
     const int c0 = sp * a.cps;
-    const int nch = max(0, min(nch_total, c0 + a.cps) - c0);
+    const int nch_mem = MULTI ? nch_total : max(0, min(nch_total, c0 + a.cps) - c0);
+    const int nch = nch_mem + (MULTI ? int(ceil_div(a.kv_hi - kv_mem, DK)) : 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -94,11 +110,14 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant
                 if (j >= DST) mbar_wait(&empty[s], uint32_t((j / DST) - 1) & 1u);
                 mbar_expect_tx(&full[s], STAGE_B);
                 uint8_t* st = sm + s * STAGE_B;
-                const int key = (c0 + j) * DK;
-                tma_load_2d(st, &mk, &full[s], h * DH, key);
-                tma_load_2d(st + BOX_B, &mk, &full[s], h * DH + 64, key);
-                tma_load_2d(st + 2 * BOX_B, &mv, &full[s], h * DH, key);
-                tma_load_2d(st + 3 * BOX_B, &mv, &full[s], h * DH + 64, key);
+                const bool own = MULTI && j >= nch_mem;  // the query's own key rows
+                const CUtensorMap* k_map = own ? &mk2 : &mk;
+                const CUtensorMap* v_map = own ? &mv2 : &mv;
+                const int key = own ? a.qrow0[z] + (j - nch_mem) * DK : (c0 + j) * DK;
+                tma_load_2d(st, k_map, &full[s], h * DH, key);
+                tma_load_2d(st + BOX_B, k_map, &full[s], h * DH + 64, key);
+                tma_load_2d(st + 2 * BOX_B, v_map, &full[s], h * DH, key);
+                tma_load_2d(st + 3 * BOX_B, v_map, &full[s], h * DH + 64, key);
             }
         }
         return;
@@ -106,7 +125,8 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant
 
     const int g = lane >> 2, i4 = lane & 3;
     const int n = min(16, a.n - r_off);  // rows of this block
-    const __nv_bfloat16* qblk = a.q + int64_t(r_off) * a.d;
+    const int q_off = MULTI ? a.qoff[z] : r_off;
+    const __nv_bfloat16* qblk = a.q + int64_t(q_off) * a.d;
     const int32_t* rows = a.rows + r_off;
     // Q fragments (A operand, rows g and g + 8; rows >= n are zero)
     uint32_t qa[8][4];
@@ -131,7 +151,10 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant
         const int s = j % DST;
         mbar_wait(&full[s], uint32_t(j / DST) & 1u);
         const uint32_t sb = smem_u32(sm + s * STAGE_B);
-        const int kb = (c0 + j) * DK + warp * 16;  // first key of this warp's 16
+        const bool own = MULTI && j >= nch_mem;
+        // first key of this warp's 16, and the end of the keys its source holds
+        const int kb = (own ? kv_mem + (j - nch_mem) * DK : (c0 + j) * DK) + warp * 16;
+        const int klim = own ? a.kv_hi : kv_mem;
         float sc[2][4];
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
@@ -146,14 +169,14 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant
                 mma16816(sc[nt], qa[2 * kq + 1], b2, b3);
             }
         }
-        if (kb + 15 > tmin) {  // some row stops inside these keys (causal limit)
+        if (kb + 15 > tmin || kb + 15 >= klim) {  // a causal limit or the source's end inside these keys
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int key = kb + nt * 8 + 2 * i4 + e;
-                    if (key > t0) sc[nt][e] = -INFINITY;
-                    if (key > t1) sc[nt][2 + e] = -INFINITY;
+                    if (key > t0 || key >= klim) sc[nt][e] = -INFINITY;
+                    if (key > t1 || key >= klim) sc[nt][2 + e] = -INFINITY;
                 }
         }
         float mx0 = fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1]));
@@ -252,7 +275,7 @@ attn_decode_kernel(const __grid_constant__ CUtensorMap mk, const __grid_constant
 #pragma unroll
         for (int w = 0; w < DWARPS; ++w) acc += ob[(w * 16 + r) * DH + c];
         const int64_t col = int64_t(h) * DH + c;
-        const int64_t rg = r_off + r;  // row of the launch
+        const int64_t rg = q_off + r;  // row of the launch
         if (a.nsplit == 1) {
             const float L = row_L[r];
             a.ctx[rg * a.d + col] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
@@ -304,7 +327,8 @@ int launch_attention_decode(const AttnTcLaunch& L, int kv_hi, cudaStream_t st) {
     if (n == 0 || kv_hi <= 0) return 0;
     if (n > 64) raise(KEEP_ERR_CONFIG, "decode attention takes at most 64 rows");
     static bool attr = [] {
-        KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
+        KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
+        KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
         return true;
     }();
     (void)attr;
@@ -323,8 +347,8 @@ int launch_attention_decode(const AttnTcLaunch& L, int kv_hi, cudaStream_t st) {
     a.ctx = L.ctx;
     const CUtensorMap mk = make_map_bf16(L.k, kv_hi, L.d, L.d, DK);
     const CUtensorMap mv = make_map_bf16(L.v, kv_hi, L.d, L.d, DK);
-    attn_decode_kernel<<<dim3(unsigned(L.H), unsigned(a.nsplit), unsigned(ceil_div(n, 16))), DTHREADS, SMEM_B, st>>>(
-        mk, mv, a);
+    attn_decode_kernel<false><<<dim3(unsigned(L.H), unsigned(a.nsplit), unsigned(ceil_div(n, 16))), DTHREADS, SMEM_B,
+                                st>>>(mk, mv, mk, mv, a);
     KEEP_LAUNCH_CHECK();
     if (a.nsplit == 1) return 1;
     const int64_t nd = int64_t(n) * L.d;
@@ -332,6 +356,46 @@ int launch_attention_decode(const AttnTcLaunch& L, int kv_hi, cudaStream_t st) {
         L.m_part, L.l_part, L.o_part, a.nsplit, n, L.H, L.d, L.ctx);
     KEEP_LAUNCH_CHECK();
     return 2;
+}
+
+int launch_attention_decode_multi(const DecodeMulti& M, cudaStream_t st) {
+    const int nq = int(M.qoff.size());
+    if (nq == 0) return 0;
+    if (M.qlen < 1 || M.qlen > 16) raise(KEEP_ERR_CONFIG, "multi decode takes 1..16 query rows per query");
+    static bool attr = [] {
+        KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
+        KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
+        return true;
+    }();
+    (void)attr;
+    const CUtensorMap mk = make_map_bf16(M.k_mem, M.kv_mem, M.d, M.d, DK);
+    const CUtensorMap mv = make_map_bf16(M.v_mem, M.kv_mem, M.d, M.d, DK);
+    const CUtensorMap mk2 = make_map_bf16(M.k_own, M.own_rows, M.d, M.d, DK);
+    const CUtensorMap mv2 = make_map_bf16(M.v_own, M.own_rows, M.d, M.d, DK);
+    int launched = 0;
+    for (int q0 = 0; q0 < nq; q0 += kMaxMulti) {
+        const int nz = std::min(kMaxMulti, nq - q0);
+        DecArgs a{};
+        a.n = M.qlen;
+        a.H = M.H;
+        a.d = M.d;
+        a.kv_mem = M.kv_mem;
+        a.kv_hi = M.kv_mem + M.qlen;
+        a.nsplit = 1;
+        a.cps = int(ceil_div(M.kv_mem, DK));
+        a.q = static_cast<const __nv_bfloat16*>(M.q);
+        a.rows = M.rows;
+        a.ctx = M.ctx;
+        for (int z = 0; z < nz; ++z) {
+            a.qrow0[z] = M.qrow0[q0 + z];
+            a.qoff[z] = M.qoff[q0 + z];
+        }
+        // queries fastest: the CTAs of one head run together and share its K / V through L2
+        attn_decode_kernel<true><<<dim3(unsigned(nz), unsigned(M.H)), DTHREADS, SMEM_B, st>>>(mk, mv, mk2, mv2, a);
+        KEEP_LAUNCH_CHECK();
+        ++launched;
+    }
+    return launched;
 }
 
 }  // namespace keep_b200

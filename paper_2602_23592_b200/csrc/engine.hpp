@@ -51,6 +51,22 @@ int launch_attention_tc(const AttnTcLaunch& a, cudaStream_t st);  // returns ker
 bool decode_attention_fits(int n);
 int decode_splits(int n_heads, int kv_hi);
 int launch_attention_decode(const AttnTcLaunch& a, int kv_hi, cudaStream_t st);
+// Several queries of a batch at an all-reused layer, one launch: each query's
+// rows attend the shared memory sheet (rows [0, kv_mem) of k_mem / v_mem,
+// read once through L2 for all of them) and then their own qlen key rows
+// (rows qrow0[i] .. of k_own / v_own, own_rows rows in total).
+struct DecodeMulti {
+    int H = 0, d = 0, qlen = 0, kv_mem = 0, own_rows = 0;
+    const void* k_mem = nullptr;
+    const void* v_mem = nullptr;
+    const void* k_own = nullptr;
+    const void* v_own = nullptr;
+    const void* q = nullptr;            // [rows x d] (pre-scaled)
+    const int32_t* rows = nullptr;      // [qlen] positions kv_mem .. (the same for every query)
+    __nv_bfloat16* ctx = nullptr;
+    std::vector<int> qrow0, qoff;       // per query: own key row base, first q / ctx row
+};
+int launch_attention_decode_multi(const DecodeMulti& m, cudaStream_t st);
 // per-128-key-chunk destination-segment table (32 B per chunk)
 void launch_chunk_table(const int32_t* row_seg, int T, void* tab, cudaStream_t st);
 // bins width for a layout (max segments touching a 128-key chunk, rounded to
