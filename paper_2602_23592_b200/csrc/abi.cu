@@ -77,7 +77,7 @@ void DevBuf::release() {
 
 void DevBuf::ensure(size_t nbytes) {
     if (nbytes <= bytes && p && !host) return;
-    release();
+    release();  // (cudaFree synchronises the device: growth must stay rare)
     if (nbytes == 0) nbytes = 16;
     if (cudaMalloc(&p, nbytes) != cudaSuccess) {
         cudaGetLastError();
@@ -100,6 +100,14 @@ void DevBuf::alloc(size_t nbytes, bool pinned_host) {
     }
     bytes = nbytes;
     host = pinned_host;
+}
+
+// Grow-only with 25% headroom: per-call sizes that drift (a refresh batch of
+// a random subset of owners) settle after a few calls instead of reallocating
+// -- and synchronising the device -- whenever a call is a little larger.
+void ensure_headroom(DevBuf& b, size_t nbytes) {
+    if (nbytes <= b.bytes && b.p && !b.host) return;
+    b.ensure(nbytes + nbytes / 4);
 }
 
 cudaEvent_t Profiler::get() {
@@ -426,9 +434,9 @@ void ensure_layer_scratch(Context& c, Pass& p) {
     // sharded: ctx rows padded to G equal row blocks (all-to-all), Wo / MLP on one block
     const size_t cpr = size_t(ceil_div(int64_t(n), c.G));
     const size_t es = c.fast ? 2 : 4;
-    p.q.ensure(es * n * c.dl);
-    (c.fast ? p.ctxb : p.ctx).ensure(es * cpr * c.G * c.dl);
-    (c.fast ? p.hb : p.h).ensure(es * cpr * c.f);
+    ensure_headroom(p.q, es * n * c.dl);
+    ensure_headroom(c.fast ? p.ctxb : p.ctx, es * cpr * c.G * c.dl);
+    ensure_headroom(c.fast ? p.hb : p.h, es * cpr * c.f);
     if (c.G > 1) {
         p.xrecv.ensure(es * cpr * c.G * c.dl);
         p.xrows.ensure(es * cpr * c.d);
@@ -769,7 +777,7 @@ void set_rows(Context& c, Pass& p, const std::vector<int32_t>& rows_new, bool fi
         }
         upload(p.d_idx, idx, st);
         ProfScope ps(c.prof, KEEP_PROF_COMPACT, st, 0.0, double(n_new) * c.d * (8.0 + (c.fast ? 2.0 : 0.0)));
-        p.x_alt.ensure(sizeof(float) * size_t(std::max(n_new, 1) + c.G) * c.d);
+        ensure_headroom(p.x_alt, sizeof(float) * size_t(std::max(n_new, 1) + c.G) * c.d);
         launch_gather_rows(p.x.as<float>(), p.d_idx.as<int32_t>(), n_new, c.d, p.x_alt.as<float>(),
                            c.fast ? p.xb.as<__nv_bfloat16>() : nullptr, st);
         std::swap(p.x.p, p.x_alt.p);
@@ -831,8 +839,10 @@ void pass_init(Context& c, Pass& p, const std::vector<int32_t>& seg_len, const i
     std::vector<int32_t> all(p.T);
     std::iota(all.begin(), all.end(), 0);
     // (+G rows: the sharded all-gather moves G equal row blocks)
-    p.x.ensure(sizeof(float) * size_t(std::max(p.T, 1) + c.G) * c.d);
-    if (c.fast) p.xb.ensure(2 * size_t(std::max(p.T, 1) + c.G) * c.d);
+    // (x and x_alt swap at every compaction: both sized for every row)
+    ensure_headroom(p.x, sizeof(float) * size_t(std::max(p.T, 1) + c.G) * c.d);
+    ensure_headroom(p.x_alt, sizeof(float) * size_t(std::max(p.T, 1) + c.G) * c.d);
+    if (c.fast) ensure_headroom(p.xb, 2 * size_t(std::max(p.T, 1) + c.G) * c.d);
     set_rows(c, p, all, true);
     ProfScope ps(c.prof, KEEP_PROF_EMBED, st, 0.0, double(p.T) * c.d * (8.0 + (c.fast ? 2.0 : 0.0)), c.fast ? 2 : 1);
     launch_embed(c.embed.as<float>(), p.d_tokens.as<int32_t>(), p.d_rows.as<int32_t>(), p.T, c.d,
@@ -1096,7 +1106,7 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
     const int64_t arows = in_place ? rows : rows + kArenaPad;
     const size_t sheet = size_t(arows) * c.dl * c.elem;
     if (in_place) {
-        c.refresh_ws.ensure(size_t(c.L) * 2 * sheet);
+        ensure_headroom(c.refresh_ws, size_t(c.L) * 2 * sheet);
         base = static_cast<uint8_t*>(c.refresh_ws.p);
     } else {
         dev = make_arena(c, arows, KEEP_TIER_DEVICE);
