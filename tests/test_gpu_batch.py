@@ -168,3 +168,26 @@ def test_batch_edges(B, qlen, multihop):
         assert np.array_equal(g["plan"], r["plan"]) and g["orders"] == r["orders"]
         assert np.array_equal(g["final_hidden"], r["final_hidden"])
         assert np.array_equal(g["last_logits"], r["last_logits"])
+
+
+def test_trim_releases_and_regrows_workspaces():
+    """keep_ctx_trim frees the prefill / batch / refresh workspaces; the next
+    calls regrow them and compute the same results."""
+    seed, S, L, H, d, V, B = 9, 18, 4, 2, 64, 256, 3
+    inst = make_instance_layout(seed, S, V)
+    lay = kb.Layout(inst.seg_len, inst.tokens)
+    Q = batch_queries(seed, B, len(inst.query), V, inst.query)
+    sched = kb.ratio_schedule(L, 0.5)
+    with kb.Context(L, H, d, 2 * d, V, seed) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay)
+        a = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True)
+        s1 = ctx.plan_keep(lay, Q[1], sched)
+        ctx.trim()
+        with pytest.raises(kb.KeepError):  # no prefill in progress after a trim
+            ctx.prefill_layer(np.ones(S, np.uint8))
+        b = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True)
+        s2 = ctx.plan_keep(lay, Q[1], sched)
+    for x, y in zip(a, b):
+        assert np.array_equal(x["plan"], y["plan"]) and np.array_equal(x["final_hidden"], y["final_hidden"])
+    assert np.array_equal(s1["final_hidden"], s2["final_hidden"])
