@@ -293,6 +293,10 @@ int keep_profile_read(void* ctx, keep_profile* out, int32_t reset);
  * C[M x N] (fp32, device) = A[M x K] . Bt[N x K]^T with bf16 device operands
  * on the tcgen05 GEMM; force_bn 0 = automatic tile, 64 or 256 = forced. */
 int keep_debug_gemm_bf16(const void* A, const void* Bt, float* C, int M, int N, int K, int force_bn);
+/* C[M x N] (fp32, device) = A[M x K] . B[K x N] with fp32 device operands on
+ * the PARITY GEMM: mode 0 automatic, 1 the Ozaki int8 tensor-core GEMM,
+ * 2 the DFMA (vec_mat bit-exact) kernel. */
+int keep_debug_gemm_parity(const float* A, const float* B, float* C, int M, int N, int K, int mode);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

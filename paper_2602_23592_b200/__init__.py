@@ -149,6 +149,7 @@ def load_library() -> C.CDLL:
         "keep_logits": (C.c_int, [vp, fp, dp]),
         "keep_divergence": (C.c_int, [vp, fp, fp, dp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+        "keep_debug_gemm_parity": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
         "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
         "keep_loader_trace": (C.c_int, [vp, C.POINTER(keep_load_record), i32, i32p]),
         "keep_shard_heads": (C.c_int, [i32, i32, i32, i32, i32p, i32p, i32p, i32p]),
@@ -482,6 +483,14 @@ class Context:
                                                    C.byref(hops)))
         return [int(x) for x in order[: n.value]], hops.value
 
+    def _schedule(self, sched) -> np.ndarray:
+        # plan_keep reads sched[l + 1] for every layer (recompute.hpp:144:
+        # ConfigError "schedule length != num_layers")
+        sched = np.ascontiguousarray(sched, np.float64).ravel()
+        if len(sched) != self.L:
+            raise KeepError(1, f"schedule length {len(sched)} != num_layers {self.L}")
+        return sched
+
     def plan_keep(self, layout: Layout, query, sched, multihop=True, summaries=False, final_hidden=True):
         L, S = self.L, layout.S
         T = int(np.sum(layout.seg_len)) + len(query)
@@ -498,7 +507,7 @@ class Context:
                                _p(hops, C.c_int32), _p(summ, C.c_double), _p(fh, C.c_float),
                                _p(logits, C.c_double), _p(rows, C.c_int64), _p(lms, C.c_double), 0.0)
         q = np.ascontiguousarray(query if len(query) else np.zeros(1), np.int32)
-        sched = np.ascontiguousarray(sched, np.float64)
+        sched = self._schedule(sched)
         lay = layout.c_struct()
         _check(self.lib.keep_plan_keep(self._h, C.byref(lay), _p(q, C.c_int32), len(query),
                                        _p(sched, C.c_double), int(bool(multihop)), C.byref(res)))
@@ -538,7 +547,7 @@ class Context:
             _check(self.lib.keep_selective_prefill_batch(self._h, C.byref(lay), B, _p(Q, C.c_int32), qlen,
                                                          _p(pl, C.c_uint8), res))
         else:
-            sched = np.ascontiguousarray(sched, np.float64)
+            sched = self._schedule(sched)
             _check(self.lib.keep_plan_keep_batch(self._h, C.byref(lay), B, _p(Q, C.c_int32), qlen,
                                                  _p(sched, C.c_double), int(bool(multihop)), res))
         outs = []

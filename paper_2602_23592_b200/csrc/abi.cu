@@ -202,6 +202,7 @@ constexpr int64_t kArenaPad = 128;  // spare rows per arena layer sheet (query r
 std::shared_ptr<Arena> make_arena(Context& c, int64_t rows, int tier) {
     auto a = std::make_shared<Arena>();
     a->rows = rows;
+    a->used = rows;
     a->tier = tier;
     a->buf.alloc(size_t(c.L) * 2 * rows * c.dl * c.elem, tier == KEEP_TIER_HOST);
     return a;
@@ -480,8 +481,8 @@ void layer_qkv(Context& c, Pass& p, int l) {
     ProfScope ps(c.prof, KEEP_PROF_QKV, st, gq, bq);
     if (!c.fast) {
         EpiArgs e{EPI_QKV, dl, p.q.as<float>(), dl, p.kdst[l], p.vdst[l], rows, nullptr};
-        launch_gemm_f64acc(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * dl, n, 3 * dl, d, e,
-                           st);
+        launch_gemm_parity(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * dl, n, 3 * dl, d, e,
+                           st, c.oz);
     } else {
         EpiArgs e{EPI_QKV, dl, nullptr, dl, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
         if (use_tc_attention(c, p)) e.q_scale = float(1.4426950408889634 / std::sqrt(double(c.dh)));
@@ -667,17 +668,17 @@ void layer_dense(Context& c, Pass& p, int l) {
             EpiArgs eo{EPI_RESID, d, xr, d, nullptr, nullptr, nullptr, nullptr};
             {
                 ProfScope ps(c.prof, KEEP_PROF_WO, st, go, bo);
-                launch_gemm_f64acc(static_cast<const float*>(ctx_rows), d, static_cast<const float*>(c.wslot(l, W_O)), d, m,
-                                   d, d, eo, st);
+                launch_gemm_parity(static_cast<const float*>(ctx_rows), d, static_cast<const float*>(c.wslot(l, W_O)), d, m,
+                                   d, d, eo, st, c.oz);
             }
             {
                 ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
                 EpiArgs ei{EPI_RELU, d, p.h.as<float>(), f, nullptr, nullptr, nullptr, nullptr};
-                launch_gemm_f64acc(xr, d, static_cast<const float*>(c.wslot(l, W_IN)), f, m, f, d, ei, st);
+                launch_gemm_parity(xr, d, static_cast<const float*>(c.wslot(l, W_IN)), f, m, f, d, ei, st, c.oz);
             }
             {
                 ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
-                launch_gemm_f64acc(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, m, d, f, eo, st);
+                launch_gemm_parity(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, m, d, f, eo, st, c.oz);
             }
         } else {
             auto* xbr = p.xb.as<__nv_bfloat16>() + int64_t(r0) * d;
@@ -981,11 +982,14 @@ Arena* in_order_arena(Context& c, const std::vector<int32_t>& seg_start, int tie
     return ar;
 }
 
-void detect_alias(Context& c, const std::vector<int32_t>& seg_start, int T) {
+// Aliasing writes the query's K/V into arena rows [Tm, T): only safe when the
+// layout covers the arena's whole payload extent (Tm == used), so those rows
+// are the spare pad and no other owner's cached KV lives there.
+void detect_alias(Context& c, const std::vector<int32_t>& seg_start, int Tm, int T) {
     c.alias_arena = nullptr;
     c.alias_hold.reset();
     Arena* ar = in_order_arena(c, seg_start, KEEP_TIER_DEVICE);
-    if (ar && ar->rows >= T) {
+    if (ar && ar->used == Tm && ar->rows >= T) {
         c.alias_arena = ar;
         c.alias_hold = c.store.find(c.seg_owner[0])->second.arena;  // kept alive for the prefill
     }
@@ -1011,7 +1015,7 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
         p.kdst[l] = static_cast<uint8_t*>(c.kv.p) + size_t(l) * 2 * sheet;
         p.vdst[l] = static_cast<uint8_t*>(c.kv.p) + (size_t(l) * 2 + 1) * sheet;
     }
-    detect_alias(c, p.seg_start, p.T);
+    detect_alias(c, p.seg_start, p.Tm, p.T);
     loader_begin(c, p);
 }
 
@@ -1110,6 +1114,7 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
         base = static_cast<uint8_t*>(c.refresh_ws.p);
     } else {
         dev = make_arena(c, arows, KEEP_TIER_DEVICE);
+        dev->used = rows;
         base = static_cast<uint8_t*>(dev->buf.p);
     }
     p.kdst.resize(c.L);
@@ -1168,6 +1173,7 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
     std::shared_ptr<Arena> arena = dev;
     if (tier == KEEP_TIER_HOST) {
         arena = make_arena(c, arows, KEEP_TIER_HOST);
+        arena->used = rows;
         KEEP_CUDA(cudaMemcpyAsync(arena->buf.p, dev->buf.p, size_t(c.L) * 2 * sheet, cudaMemcpyDeviceToHost, c.s_main));
     }
     KEEP_CUDA(cudaStreamSynchronize(c.s_main));
@@ -1249,7 +1255,7 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
     if (int64_t(B) * Tp > INT32_MAX / 4) raise(KEEP_ERR_CONFIG, "batch too large");
     check_tokens(c, lay->tokens, Tm);
     check_tokens(c, queries, int64_t(B) * qlen);
-    detect_alias(c, v0.seg_start, T);
+    detect_alias(c, v0.seg_start, Tm, T);
     // Memory in pinned host DRAM (BASELINE configs[4]): one in-order arena,
     // streamed a whole layer sheet at a time into two HBM staging sheets on
     // the copy stream, one layer ahead of compute -- every query of the batch
@@ -1851,6 +1857,19 @@ int keep_memory_put(void* ctx, keep_owner owner, uint64_t version, int32_t layer
                     KEEP_CUDA(cudaMemcpy(layer_values(c, pl, l), layer_values(c, it->second, l), blk, cudaMemcpyDefault));
                 }
             } else {
+                // A block of another size or tier.  The reference keys blocks by
+                // (owner, layer) (cache_manager.hpp:69-99), so a put never
+                // discards the owner's other layers; here an owner's layers share
+                // one row block.  Stale layers may go (a load of them misses
+                // either way); still-current ones of the old shape are an error
+                // instead of a silent drop.
+                if (it != c.store.end())
+                    for (int l = 0; l < c.L; ++l)
+                        if (l != layer && it->second.present[l] && it->second.layer_version[l] >= cur)
+                            raise(KEEP_ERR_INPUT, "put of " + std::to_string(tokens) + " tokens for " + owner_str(k) +
+                                                      " would drop its current layer " + std::to_string(l) + " of " +
+                                                      std::to_string(it->second.tokens) +
+                                                      " tokens (different size or tier); invalidate the owner first");
                 pl.arena = make_arena(c, tokens, tier);
                 pl.tokens = tokens;
                 pl.layer_version.assign(c.L, 0);

@@ -326,12 +326,8 @@ int launch_attention_decode(const AttnTcLaunch& L, int kv_hi, cudaStream_t st) {
     const int n = L.n;
     if (n == 0 || kv_hi <= 0) return 0;
     if (n > 64) raise(KEEP_ERR_CONFIG, "decode attention takes at most 64 rows");
-    static bool attr = [] {
-        KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
-        KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
-        return true;
-    }();
-    (void)attr;
+    smem_attr(attn_decode_kernel<false>, SMEM_B);
+    smem_attr(attn_decode_kernel<true>, SMEM_B);
     DecArgs a{};
     a.n = n;
     a.H = L.H;
@@ -362,12 +358,8 @@ int launch_attention_decode_multi(const DecodeMulti& M, cudaStream_t st) {
     const int nq = int(M.qoff.size());
     if (nq == 0) return 0;
     if (M.qlen < 1 || M.qlen > 16) raise(KEEP_ERR_CONFIG, "multi decode takes 1..16 query rows per query");
-    static bool attr = [] {
-        KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
-        KEEP_CUDA(cudaFuncSetAttribute(attn_decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_B));
-        return true;
-    }();
-    (void)attr;
+    smem_attr(attn_decode_kernel<false>, SMEM_B);
+    smem_attr(attn_decode_kernel<true>, SMEM_B);
     const CUtensorMap mk = make_map_bf16(M.k_mem, M.kv_mem, M.d, M.d, DK);
     const CUtensorMap mv = make_map_bf16(M.v_mem, M.kv_mem, M.d, M.d, DK);
     const CUtensorMap mk2 = make_map_bf16(M.k_own, M.own_rows, M.d, M.d, DK);

@@ -1251,11 +1251,7 @@ template <int MODE>
 void launch_mode(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const TcArgs& a, dim3 grid,
                  cudaStream_t st) {
     using LY = Layout<MODE>;
-    static bool attr = false;
-    if (!attr) {
-        KEEP_CUDA(cudaFuncSetAttribute(attn_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(LY::SMEM)));
-        attr = true;
-    }
+    smem_attr(attn_tc_kernel<MODE>, int(LY::SMEM));
     attn_tc_kernel<MODE><<<grid, NTHR, LY::SMEM, st>>>(q, k, vt, a);
     KEEP_LAUNCH_CHECK();
 }
@@ -1266,12 +1262,7 @@ template <int MODE, int NB>
 void launch_mode2(const CUtensorMap& q, const CUtensorMap& k, const CUtensorMap& vt, const CUtensorMap& z,
                   const TcArgs& a, dim3 grid, cudaStream_t st) {
     using LY = Layout2<MODE, NB>;
-    static bool attr = false;
-    if (!attr) {
-        KEEP_CUDA(cudaFuncSetAttribute(attn_tc2_kernel<MODE, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(LY::SMEM)));
-        attr = true;
-    }
+    smem_attr(attn_tc2_kernel<MODE, NB>, int(LY::SMEM));
     attn_tc2_kernel<MODE, NB><<<grid, NTHR2, LY::SMEM, st>>>(q, k, vt, z, a);
     KEEP_LAUNCH_CHECK();
 }

@@ -39,6 +39,12 @@ void trace_launch(const char* file, int line);
 
 constexpr int kNumSMs = 148;
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) applies to the current
+// device only: set it once per (kernel, device), thread-safe.
+void set_smem_attr(const void* fn, int bytes);
+template <typename F>
+inline void smem_attr(F* fn, int bytes) { set_smem_attr(reinterpret_cast<const void*>(fn), bytes); }
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ---------------------------------------------------------------- layouts --

@@ -142,12 +142,27 @@ struct DevBuf {
     template <typename T> T* as() const { return static_cast<T*>(p); }
 };
 
+// PARITY projection GEMMs (gemm_oz.cu): the Ozaki int8 tensor-core GEMM from
+// kOzMinRows rows, DFMA (gemm_f64acc.cu) below.  OzWork = its grow-only
+// scratch (digit planes of A and B, scale exponents, fp64 Horner partials).
+struct OzWork {
+    DevBuf a, b, ea, eb, part;
+};
+constexpr int kOzMinRows = 64;
+int oz_slices();  // KEEP_OZ_SLICES (default 7)
+bool ozaki_eligible(int M, int N, int K);
+void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
+                       const EpiArgs& epi, cudaStream_t st, OzWork& w, int max_ctas = kNumSMs);
+void launch_gemm_parity(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
+                        const EpiArgs& epi, cudaStream_t st, OzWork& w, int max_ctas = kNumSMs);
+
 // A KV arena: per layer, keys [rows x d] then values [rows x d].  Owner
 // payloads are row ranges of an arena (a batch of canonical refreshes writes
 // its merged KV straight into the arena -- no staging copy).
 struct Arena {
     DevBuf buf;
     int64_t rows = 0;
+    int64_t used = 0;  // rows [0, used) hold owner payloads; [used, rows) are spare (query rows of aliased layers)
     int tier = KEEP_TIER_DEVICE;
     int refs = 0;
 };
@@ -302,6 +317,7 @@ struct Context {
     cudaEvent_t ev_sum = nullptr, ev_sel = nullptr;
     Profiler prof;
     Loader loader;
+    OzWork oz;  // PARITY Ozaki GEMM scratch
     int gemm_ctas = kNumSMs;  // 147 while the selector overlaps the MLP
 
     void* wslot(int l, int slot) const { return w[l * 4 + slot]->p; }

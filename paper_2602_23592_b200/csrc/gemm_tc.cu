@@ -17,6 +17,8 @@
 // add with a bf16 mirror for the next GEMM, ReLU to bf16, plain fp32 store.
 // Tiles are rasterised in bands of GM m-blocks so a band of A and a window of
 // weight columns stay L2-resident (126 MB) while 148 CTAs sweep them.
+#include <map>
+#include <mutex>
 #include <unordered_map>
 
 #include "engine.hpp"
@@ -26,10 +28,6 @@ namespace keep_b200 {
 
 namespace tc {
 // ------------------------------------------------------------ tensor maps --
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
 EncodeFn encode_fn() {
     static EncodeFn fn = [] {
         void* p = nullptr;
@@ -458,26 +456,32 @@ gemm_skinny_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant
 }
 
 float* splitk_workspace(int M, int N, cudaStream_t st) {
-    // per-thread grow-only fp32 workspace (one context per host thread)
-    // (zeroed once when it grows; every finalisation pass re-zeroes what it read)
-    thread_local DevBuf ws;
-    const size_t need = sizeof(float) * size_t(M) * N;
-    if (need > ws.bytes || !ws.p) {
-        ws.ensure(need);
-        KEEP_CUDA(cudaMemsetAsync(ws.p, 0, ws.bytes, st));
+    // grow-only fp32 workspace per (device, stream): GEMMs in flight on
+    // different streams (or contexts on different GPUs) never share one.
+    // Zeroed once when it grows; every finalisation pass re-zeroes what it read.
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, std::unique_ptr<DevBuf>> pool;
+    int dev = 0;
+    KEEP_CUDA(cudaGetDevice(&dev));
+    DevBuf* ws;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto& slot = pool[{dev, st}];
+        if (!slot) slot.reset(new DevBuf());
+        ws = slot.get();
     }
-    return ws.as<float>();
+    const size_t need = sizeof(float) * size_t(M) * N;
+    if (need > ws->bytes || !ws->p) {
+        ws->ensure(need);
+        KEEP_CUDA(cudaMemsetAsync(ws->p, 0, ws->bytes, st));
+    }
+    return ws->as<float>();
 }
 
 template <int MT>
 void launch_skinny_mt(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int64_t ldb, int M, int N, int K,
                       const EpiArgs& epi, cudaStream_t st, int max_ctas) {
-    static bool attr = [] {
-        KEEP_CUDA(cudaFuncSetAttribute(gemm_skinny_kernel<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       SkCfg<MT>::SMEM));
-        return true;
-    }();
-    (void)attr;
+    smem_attr(gemm_skinny_kernel<MT>, SkCfg<MT>::SMEM);
     const CUtensorMap ta = make_map_bf16(A, M, K, lda, 16 * MT);
     const CUtensorMap tb = make_map_bf16(Bt, N, K, ldb, 64);
     const int64_t units = ceil_div(N, 64) * ceil_div(K, 256);
@@ -501,12 +505,7 @@ void launch_bn(const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bt, int
                const EpiArgs& epi, cudaStream_t st, int max_ctas = kNumSMs, int ksplit = 1) {
     using CF = Cfg<BN, AR>;
     static_assert(CF::SMEM <= 232448, "GEMM smem");
-    static bool attr = false;
-    if (!attr) {
-        KEEP_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, AR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(CF::SMEM)));
-        attr = true;
-    }
+    smem_attr(gemm_tc_kernel<BN, AR>, int(CF::SMEM));
     const CUtensorMap ta = make_map_bf16(A, M, K, lda, AR);
     const CUtensorMap tb = make_map_bf16(Bt, N, K, ldb, BN);
     const int ntiles = int(ceil_div(M, BM) * ceil_div(N, BN)) * ksplit;

@@ -2,11 +2,24 @@
 // K6 summary reduce, K7 selector, K11 logits.  All HBM- or latency-bound
 // integer/fp64 work: coalesced 16-byte accesses, grids sized in SM multiples.
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <tuple>
 #include "kernels.hpp"
 
 #include <cfloat>
 
 namespace keep_b200 {
+
+void set_smem_attr(const void* fn, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, int>> done;
+    int dev = 0;
+    KEEP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(mu);
+    if (!done.insert({fn, dev, bytes}).second) return;
+    KEEP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
 
 bool sync_debug() {
     static const bool on = [] {

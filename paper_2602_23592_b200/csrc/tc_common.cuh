@@ -228,6 +228,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Host: the driver's cuTensorMapEncodeTiled (resolved once).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode_fn();
+
 // Host: 2-D bf16 tensor map [rows x cols] (row stride ld elements), box
 // 64 x box_rows, 128-byte swizzle, out-of-bounds elements read as zero.
 CUtensorMap make_map_bf16(const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows);

@@ -1,0 +1,68 @@
+"""PARITY projection GEMM on the int8 tensor cores (gemm_oz.cu, Ozaki scheme)
+against the reference's arithmetic: fp32 operands, fp64 accumulation, one
+rounding to fp32 (vec_mat, tensor.hpp:31-41).
+
+The exact product (fp64 here, computed by torch on the GPU in float64) is the
+oracle; the DFMA kernel (gemm_f64acc.cu, bit-exact with vec_mat) is the
+baseline.  The Ozaki result must stay within its stated error bound of the
+exact value, and its fp32 outputs must equal the DFMA kernel's except for a
+tiny fraction of 1-ulp rounding-boundary cases.
+"""
+import numpy as np
+import pytest
+
+import paper_2602_23592_b200 as kb
+
+pytestmark = pytest.mark.gpu
+
+
+def run(A, B, mode):
+    import torch
+    M, K = A.shape
+    N = B.shape[1]
+    C = torch.full((M, N), float("nan"), device="cuda", dtype=torch.float32)
+    lib = kb.load_library()
+    rc = lib.keep_debug_gemm_parity(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, mode)
+    assert rc == 0, lib.keep_last_error()
+    return C
+
+
+@pytest.mark.parametrize("M,N,K", [
+    (128, 256, 128), (300, 512, 512), (64, 96, 64), (1000, 15360, 5120), (777, 5120, 13824),
+    (2049, 1024, 1024), (130, 288, 4096), (256, 5120, 27648),
+])
+def test_ozaki_matches_fp64_accumulation(M, N, K):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 31 + N + K)
+    A = torch.randn(M, K, device="cuda", generator=g, dtype=torch.float32)
+    A[:, ::7] *= 1e-3  # a wide dynamic range inside rows
+    A = torch.relu(A) if K % 2 else A
+    B = torch.randn(K, N, device="cuda", generator=g, dtype=torch.float32) / np.sqrt(K)
+    oz = run(A, B, 1)
+    df = run(A, B, 2)
+    exact = A.double() @ B.double()
+    assert not torch.isnan(oz).any()
+    # error bound: per product 2^-(8s-10) max|a_row| max|b_col| (s = 7 digits) plus the fp32 rounding
+    amax = A.abs().amax(dim=1, keepdim=True).double()
+    bmax = B.abs().amax(dim=0, keepdim=True).double()
+    bound = K * 2.0 ** (-(8 * 7 - 10)) * amax * bmax + exact.abs() * 2.0 ** -24
+    assert bool(((oz.double() - exact).abs() <= bound).all())
+    # fp32 outputs equal the DFMA (vec_mat) ones except rounding-boundary ties
+    diff = (oz != df).double().mean().item()
+    assert diff <= 1e-4, diff
+    ulps = ((oz - df).abs() / torch.clamp(df.abs(), min=1e-30)).max().item()
+    assert ulps <= 2.0 ** -22, ulps
+
+
+def test_ozaki_zero_rows_and_tiny_values():
+    import torch
+    M, N, K = 256, 512, 256
+    A = torch.zeros(M, K, device="cuda")
+    A[1] = 1e-30
+    A[2, 5] = 3.0e30
+    A[3] = torch.arange(K, device="cuda", dtype=torch.float32) - 100
+    B = torch.randn(K, N, device="cuda")
+    oz = run(A, B, 1)
+    exact = (A.double() @ B.double()).float()
+    assert torch.equal(oz[0], torch.zeros_like(oz[0]))
+    assert torch.allclose(oz, exact, rtol=1e-6, atol=0)
