@@ -348,7 +348,8 @@ void plan_splits(Context& c, Pass& p) {
     const int64_t key = (int64_t(p.n) << 32) ^ (int64_t(p.T) << 2) ^ (tc ? 1 : 0) ^ (p.block_diag ? 2 : 0);
     if (key == p.split_key) return;
     p.split_key = key;
-    const int tiles = int(ceil_div(p.n, tc ? 128 : 16));
+    const bool dmma = !c.fast && parity_attention_dmma(c.dh);
+    const int tiles = int(ceil_div(p.n, tc ? 128 : (dmma ? attention_dmma_rows_per_tile() : 16)));
     int nsplit = 1;
     if (tc && !p.block_diag) {
         // stats / context: unaligned key splits.  One CTA per SM (smem), so
@@ -390,24 +391,31 @@ void plan_splits(Context& c, Pass& p) {
     }
     if (!p.block_diag) {
         const int target = tc ? 2 * kNumSMs : 4 * kNumSMs;
-        nsplit = int(std::min<int64_t>(ceil_div(target, tiles), std::max(1, p.T / 128)));
+        // (the DMMA kernels run one 256-thread CTA per (row tile, head, split) and SM)
+        const int64_t ctas = dmma ? int64_t(tiles) * c.Hl : tiles;
+        nsplit = int(std::min<int64_t>(ceil_div(dmma ? 2 * kNumSMs : target, ctas), std::max(1, p.T / 128)));
         // bound the fp64 partial-context scratch to ~512 MB
         const int64_t per_split = int64_t(p.n) * c.dl * 8;
         nsplit = int(std::max<int64_t>(1, std::min<int64_t>(nsplit, (512ll << 20) / std::max<int64_t>(per_split, 1))));
     }
-    std::vector<int32_t> lo, hi;
-    if (nsplit == 1) {
-        lo.push_back(0);
-        hi.push_back(p.T);
-    } else {
+    // segment-aligned key splits (a segment's keys never straddle two splits:
+    // every rowbin (row, segment) entry is written by exactly one CTA)
+    auto seg_splits = [&](int ns_want, std::vector<int32_t>& lo, std::vector<int32_t>& hi) {
+        lo.clear();
+        hi.clear();
+        if (ns_want <= 1) {
+            lo.push_back(0);
+            hi.push_back(p.T);
+            return;
+        }
         // candidate cut points: segment starts and the query start
         std::vector<int32_t> cuts;
         for (int i = 0; i < p.S; ++i) cuts.push_back(p.seg_start[i]);
         cuts.push_back(p.Tm);
         int32_t prev = 0;
         lo.push_back(0);
-        for (int k = 1; k < nsplit; ++k) {
-            const int64_t want = int64_t(k) * p.T / nsplit;
+        for (int k = 1; k < ns_want; ++k) {
+            const int64_t want = int64_t(k) * p.T / ns_want;
             auto it = std::lower_bound(cuts.begin(), cuts.end(), int32_t(want));
             if (it == cuts.end()) break;
             if (*it <= prev) continue;
@@ -416,9 +424,24 @@ void plan_splits(Context& c, Pass& p) {
             prev = *it;
         }
         hi.push_back(p.T);
-    }
+    };
+    std::vector<int32_t> lo, hi;
+    seg_splits(nsplit, lo, hi);
     upload(p.split_lo, lo, c.s_main);
     upload(p.split_hi, hi, c.s_main);
+    if (dmma && !p.block_diag) {
+        // the DMMA bins pass loops the heads inside one CTA per (row tile,
+        // split): it needs its own, finer split plan to fill the machine
+        std::vector<int32_t> blo, bhi;
+        seg_splits(int(std::min<int64_t>(ceil_div(8 * kNumSMs, tiles), std::max(1, p.T / 256))), blo, bhi);
+        upload(p.split_lo_b, blo, c.s_main);
+        upload(p.split_hi_b, bhi, c.s_main);
+        p.split_count_b = int(blo.size());
+    } else {
+        upload(p.split_lo_b, lo, c.s_main);
+        upload(p.split_hi_b, hi, c.s_main);
+        p.split_count_b = int(lo.size());
+    }
     const int ns = int(lo.size());
     const int nm = std::max(ns, p.split_count_a);
     p.m_part.ensure(sizeof(double) * size_t(nm) * p.n * c.H);
@@ -519,6 +542,9 @@ void layer_attention(Context& c, Pass& p, int l, const void* q, void* ctx, const
     a.nsplit = p.split_count;
     a.split_lo = p.split_lo.as<int32_t>();
     a.split_hi = p.split_hi.as<int32_t>();
+    a.nsplit_b = p.split_count_b;
+    a.split_lo_b = p.split_lo_b.as<int32_t>();
+    a.split_hi_b = p.split_hi_b.as<int32_t>();
     a.rows_per_tile = 16;
     a.m_part = p.m_part.as<double>();
     a.l_part = p.l_part.as<double>();

@@ -1,0 +1,453 @@
+// attn_dmma.cu -- PARITY K5 attention on the fp64 tensor cores (DMMA).
+//
+// The reference's attention_row (prefill.hpp:124-159) is fp64 throughout: the
+// score dot(q_h, k_h) * (1/sqrt(dh)), the softmax and ctx = sum p v.  The
+// first PARITY kernels (attn_simt.cu) did it with scalar DFMA and three
+// recomputations of Q.K^T; this file runs both matrix products on the
+// B200's fp64 tensor cores, mma.sync.m8n8k4.f64 (37 TFLOP/s measured here,
+// tools/micro/fp64_peak.cu, against 34 for DFMA), with the fp32 q/K/V
+// widened to fp64 on the way in (exact) -- so every product is exact and only
+// the fp64 accumulation order differs from the reference.
+//
+// CTA = 64 compact rows (8 warps x 8 rows) x one head x one key split; keys
+// stream in 64-key fp32 chunks by cp.async (the next chunk lands while this
+// one is multiplied) and are widened to fp64 in shared memory once per chunk.
+// Per warp: Q fragments stay in registers; S (8 rows x 64 keys) is 8 m8n8
+// accumulators; O (8 rows x dh) is dh/8 accumulators.  P.V uses the S
+// accumulators directly as A fragments: thread (g, t) holds keys 8j + 2t and
+// 8j + 2t + 1 of its row, so the k-step j,h reads V rows 8j + 2t + h --
+// a permutation of the summation order, no register shuffles.
+//
+// Modes (the summary needs NORMALISED probabilities):
+//   STATS  running max / sum of exp per (row, head, split)
+//   CTX    p = exp(s - m) * (1/l) with the final statistics, O = P.V
+//   FLASH  one pass, online max (layers without a summary)
+//   BINS   per (row tile, split), heads looped in order: prob_mean[key] +=
+//          p / H exactly as attention_row (prefill.hpp:150-153), then per
+//          row sums over the keys of each destination segment
+//          (prefill.hpp:281-288) -> rowbin, reduced by K6.
+#include <cfloat>
+
+#include "kernels.hpp"
+
+namespace keep_b200 {
+
+namespace {
+
+constexpr int AW = 8;              // warps per CTA
+constexpr int ART = AW * 8;        // compact rows per CTA
+constexpr int AKC = 64;            // keys per chunk
+constexpr int ANT = AW * 32;
+enum { M_STATS = 0, M_CTX = 1, M_FLASH = 2 };
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    const int sz = ok ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Shared memory per CTA: the fp32 chunks land by cp.async in a double-buffered
+// staging ring and are widened to fp64 ONCE per chunk (the fp32 -> fp64
+// conversion runs on the quarter-rate XU pipe: converting per fragment load,
+// 8 warps x every use, made it the bound).  Strides are padded so the m8n8k4
+// fragment loads (8 keys x 4 dims for K, 4 keys x 8 dims for V) hit every
+// bank once per 128-byte wavefront.
+template <int DH>
+struct Geo {
+    static constexpr int P32 = DH + 4;                 // fp32 staging row stride (floats)
+    static constexpr int P64 = DH + 4;                 // fp64 row stride (doubles)
+    static constexpr int S32 = AKC * P32;              // floats per staged K (or V) chunk
+    static constexpr int S64 = AKC * P64;              // doubles per converted chunk
+    static constexpr int NT = DH / 8;                  // n-tiles of P.V
+    // bytes: staging [K|V] fp32 (the next chunk) + converted [K|V] fp64 (this chunk)
+    static constexpr int smem(bool with_v) { return (with_v ? 2 : 1) * (S32 * 4 + S64 * 8); }
+};
+
+// keys [k0, k0 + AKC) of head columns [off, off + DH) of src (row stride d) -> fp32 staging
+template <int DH>
+__device__ __forceinline__ void stage_chunk(float* dst, const float* src, int k0, int hi, int d, int off) {
+    constexpr int V4 = DH / 4;  // 16-byte vectors per key
+    for (int e = threadIdx.x; e < AKC * V4; e += ANT) {
+        const int r = e / V4, c = e % V4;
+        const bool ok = k0 + r < hi;
+        const float* s = src + int64_t(ok ? k0 + r : k0) * d + off + 4 * c;
+        cp_async16(dst + r * Geo<DH>::P32 + 4 * c, s, ok);
+    }
+}
+
+// fp32 staging -> fp64 chunk (exact)
+template <int DH>
+__device__ __forceinline__ void widen_chunk(double* dst, const float* src) {
+    constexpr int V4 = DH / 4;
+    for (int e = threadIdx.x; e < AKC * V4; e += ANT) {
+        const int r = e / V4, c = e % V4;
+        const float4 x = *reinterpret_cast<const float4*>(src + r * Geo<DH>::P32 + 4 * c);
+        double2* o = reinterpret_cast<double2*>(dst + r * Geo<DH>::P64 + 4 * c);
+        o[0] = make_double2(double(x.x), double(x.y));
+        o[1] = make_double2(double(x.z), double(x.w));
+    }
+}
+
+struct RowInfo {
+    int t;    // global row (-1: padding row)
+    int klo;  // first visible key
+};
+
+__device__ __forceinline__ RowInfo row_info(const AttnArgs& a, int i) {
+    RowInfo r;
+    if (i < a.n) {
+        r.t = a.rows[i];
+        r.klo = a.key_lo ? a.key_lo[r.t] : 0;
+    } else {
+        r.t = -1;
+        r.klo = 0x7fffffff;
+    }
+    return r;
+}
+
+constexpr int NJ = AKC / 8;  // key n-tiles per chunk
+
+// S = Q.K^T (scaled) for this warp's 8 rows x the chunk's AKC keys
+template <int DH>
+__device__ __forceinline__ void scores(const double (&qa)[DH / 4], const double* ks, int g, int t, double scale,
+                                       double (&s)[NJ][2]) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) s[j][0] = s[j][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < DH / 4; ++i) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma(s[j], qa[i], ks[(8 * j + g) * Geo<DH>::P64 + 4 * i + t]);
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+        s[j][0] *= scale;
+        s[j][1] *= scale;
+    }
+}
+
+template <int DH, int MODE>
+__global__ void __launch_bounds__(ANT, 1) attn_dmma_kernel(AttnArgs a, double scale) {
+    using G = Geo<DH>;
+    constexpr bool WV = MODE != M_STATS;
+    constexpr int NM = WV ? 2 : 1;  // matrices streamed (K, V)
+    extern __shared__ __align__(16) double smd[];
+    double* kd = smd;                                            // [S64] fp64 K chunk
+    double* vd = smd + G::S64;                                   // [S64] fp64 V chunk (WV)
+    float* stg = reinterpret_cast<float*>(smd + NM * G::S64);    // [2][NM][S32]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int i0 = blockIdx.x * ART;
+    const int h = blockIdx.y, sp = blockIdx.z;
+    const int off = h * DH;
+    // the tile's key range: rows ascending, key_lo non-decreasing in the row
+    const int nrows = min(ART, a.n - i0);
+    const int tmax = a.rows[i0 + nrows - 1];
+    const int klo0 = a.key_lo ? a.key_lo[a.rows[i0]] : 0;
+    const int lo = max(a.split_lo[sp], klo0), hi = min(a.split_hi[sp], tmax + 1);
+    const int row = i0 + warp * 8 + g;
+    const RowInfo ri = row_info(a, row);
+    // Q fragments (A of m8n8k4: row g, k = 4i + t), fp32 -> fp64 exactly
+    double qa[DH / 4];
+    {
+        const float* q = static_cast<const float*>(a.q) + int64_t(min(row, a.n - 1)) * a.d + off;
+#pragma unroll
+        for (int i = 0; i < DH / 4; ++i) qa[i] = ri.t >= 0 ? double(q[4 * i + t]) : 0.0;
+    }
+    double m = -DBL_MAX, l = 0.0, inv = 0.0;
+    if (MODE == M_CTX && ri.t >= 0) {
+        const int64_t o = int64_t(row) * a.H + h;
+        m = a.m_fin[o];
+        inv = 1.0 / a.l_fin[o];  // p = e * (1/sum), prefill.hpp:148-151
+    }
+    double o_acc[G::NT][2];
+#pragma unroll
+    for (int n = 0; n < G::NT; ++n) o_acc[n][0] = o_acc[n][1] = 0.0;
+
+    const float* kg = static_cast<const float*>(a.k);
+    const float* vg = static_cast<const float*>(a.v);
+    const int nchunks = lo < hi ? int(ceil_div(hi - lo, AKC)) : 0;
+    auto issue = [&](int c) {
+        stage_chunk<DH>(stg, kg, lo + c * AKC, hi, a.d, off);
+        if (WV) stage_chunk<DH>(stg + G::S32, vg, lo + c * AKC, hi, a.d, off);
+        cp_commit();
+    };
+    if (nchunks > 0) issue(0);
+    for (int c = 0; c < nchunks; ++c) {
+        const int k0 = lo + c * AKC;
+        cp_wait_all();
+        __syncthreads();  // chunk c staged; everyone done with the previous fp64 chunk
+        widen_chunk<DH>(kd, stg);
+        if (WV) widen_chunk<DH>(vd, stg + G::S32);
+        __syncthreads();
+        if (c + 1 < nchunks) issue(c + 1);  // the next chunk streams in behind this one's math
+        double s[NJ][2];
+        scores<DH>(qa, kd, g, t, scale, s);
+        // visibility of key k0 + 8j + 2t + e for this thread's row
+        bool vis[NJ][2];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int key = k0 + 8 * j + 2 * t + e;
+                vis[j][e] = key < hi && key <= ri.t && key >= ri.klo;
+            }
+        if (MODE == M_STATS || MODE == M_FLASH) {
+            double cm = -DBL_MAX;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (vis[j][e]) cm = fmax(cm, s[j][e]);
+            cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+            cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+            const bool any = cm != -DBL_MAX;
+            const double mn = fmax(m, cm);
+            double part = 0.0;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double p = (any && vis[j][e]) ? exp(s[j][e] - mn) : 0.0;
+                    s[j][e] = p;
+                    part += p;
+                }
+            part += __shfl_xor_sync(0xffffffffu, part, 1);
+            part += __shfl_xor_sync(0xffffffffu, part, 2);
+            if (any) {
+                const double alpha = m == -DBL_MAX ? 0.0 : exp(m - mn);
+                l = l * alpha + part;
+                m = mn;
+                if (MODE == M_FLASH && alpha != 1.0) {
+#pragma unroll
+                    for (int n = 0; n < G::NT; ++n) {
+                        o_acc[n][0] *= alpha;
+                        o_acc[n][1] *= alpha;
+                    }
+                }
+            }
+        } else {  // CTX: normalised probabilities with the final statistics
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) s[j][e] = vis[j][e] ? exp(s[j][e] - m) * inv : 0.0;
+        }
+        if (WV) {  // O += P.V
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double* vr = vd + (8 * j + 2 * t + e) * G::P64 + g;
+#pragma unroll
+                    for (int n = 0; n < G::NT; ++n) dmma(o_acc[n], s[j][e], vr[8 * n]);
+                }
+        }
+    }
+    if (ri.t < 0) return;
+    if (MODE == M_STATS) {
+        if (t == 0) {
+            const int64_t o = (int64_t(sp) * a.n + row) * a.H + h;
+            a.m_part[o] = m;
+            a.l_part[o] = l;
+        }
+        return;
+    }
+    // O fragment: row g, columns 8n + 2t + {0, 1}
+    if (MODE == M_FLASH && a.nsplit == 1) {
+        const double il = l > 0.0 ? 1.0 / l : 0.0;
+#pragma unroll
+        for (int n = 0; n < G::NT; ++n) {
+            const int64_t col = off + 8 * n + 2 * t;
+            *reinterpret_cast<float2*>(a.ctx + int64_t(row) * a.d + col) =
+                make_float2(float(o_acc[n][0] * il), float(o_acc[n][1] * il));
+        }
+        return;
+    }
+    if (MODE == M_FLASH && t == 0) {
+        const int64_t o = (int64_t(sp) * a.n + row) * a.H + h;
+        a.m_part[o] = m;
+        a.l_part[o] = l;
+    }
+    if (a.nsplit == 1) {  // CTX
+#pragma unroll
+        for (int n = 0; n < G::NT; ++n) {
+            const int64_t col = off + 8 * n + 2 * t;
+            *reinterpret_cast<float2*>(a.ctx + int64_t(row) * a.d + col) =
+                make_float2(float(o_acc[n][0]), float(o_acc[n][1]));
+        }
+    } else {
+#pragma unroll
+        for (int n = 0; n < G::NT; ++n) {
+            const int64_t col = off + 8 * n + 2 * t;
+            *reinterpret_cast<double2*>(a.o_part + (int64_t(sp) * a.n + row) * a.d + col) =
+                make_double2(o_acc[n][0], o_acc[n][1]);
+        }
+    }
+}
+
+// flash splits: ctx = sum_s o_s e^(m_s - M) / sum_s l_s e^(m_s - M)
+__global__ void flash_combine_f64_kernel(AttnArgs a, int dh) {
+    const int64_t nd = int64_t(a.n) * a.d;
+    const int64_t nh = int64_t(a.n) * a.H;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nd; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t row = e / a.d;
+        const int h = int(e % a.d) / dh;
+        const int64_t o = row * a.H + h;
+        double M = -DBL_MAX;
+        for (int s = 0; s < a.nsplit; ++s) M = fmax(M, a.m_part[int64_t(s) * nh + o]);
+        double num = 0.0, den = 0.0;
+        for (int s = 0; s < a.nsplit; ++s) {
+            const double ms = a.m_part[int64_t(s) * nh + o];
+            if (ms == -DBL_MAX) continue;
+            const double w = exp(ms - M);
+            num += a.o_part[int64_t(s) * nd + e] * w;
+            den += a.l_part[int64_t(s) * nh + o] * w;
+        }
+        a.ctx[e] = den > 0.0 ? float(num / den) : 0.f;
+    }
+}
+
+// BINS: per (row tile, split), heads in order; pm[row][key] += p / H
+template <int DH>
+__global__ void __launch_bounds__(ANT, 1) attn_dmma_bins_kernel(AttnArgs a, double scale, double inv_heads) {
+    using G = Geo<DH>;
+    extern __shared__ __align__(16) double smd[];
+    double* kd = smd;                                          // [S64] fp64 K chunk of head h
+    double* pm = smd + G::S64;                                 // [ART][AKC + 1]
+    float* stg = reinterpret_cast<float*>(pm + ART * (AKC + 1));  // [S32]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int i0 = blockIdx.x * ART, sp = blockIdx.y;
+    const int nrows = min(ART, a.n - i0);
+    const int tmax = a.rows[i0 + nrows - 1];
+    const int klo0 = a.key_lo ? a.key_lo[a.rows[i0]] : 0;
+    const int lo = max(a.split_lo_b[sp], klo0), hi = min(a.split_hi_b[sp], tmax + 1);
+    if (lo >= hi) return;
+    const int lr = warp * 8 + g;  // local row of this thread's fragments
+    const int row = i0 + lr;
+    const RowInfo ri = row_info(a, row);
+    double* rowbin = static_cast<double*>(a.rowbin);
+    // the binning thread (one per local row) keeps its running bin across chunks
+    int cur = -1;
+    double run = 0.0;
+    const RowInfo rb = threadIdx.x < ART ? row_info(a, i0 + threadIdx.x) : RowInfo{-1, 0};
+    const float* kg = static_cast<const float*>(a.k);
+    const int nchunks = int(ceil_div(hi - lo, AKC));
+    const int nsteps = nchunks * a.H;  // (chunk, head) in order
+    auto issue = [&](int st) {
+        const int c = st / a.H, h = st % a.H;
+        stage_chunk<DH>(stg, kg, lo + c * AKC, hi, a.d, h * DH);
+        cp_commit();
+    };
+    issue(0);
+    for (int st = 0; st < nsteps; ++st) {
+        const int c = st / a.H, h = st % a.H;
+        const int k0 = lo + c * AKC;
+        cp_wait_all();
+        __syncthreads();  // (also: the previous chunk's binning has read pm)
+        widen_chunk<DH>(kd, stg);
+        if (h == 0)
+            for (int e = threadIdx.x; e < ART * (AKC + 1); e += ANT) pm[e] = 0.0;
+        __syncthreads();
+        if (st + 1 < nsteps) issue(st + 1);
+        double qa[DH / 4];
+        const float* q = static_cast<const float*>(a.q) + int64_t(min(row, a.n - 1)) * a.d + h * DH;
+#pragma unroll
+        for (int i = 0; i < DH / 4; ++i) qa[i] = ri.t >= 0 ? double(q[4 * i + t]) : 0.0;
+        double s[NJ][2];
+        scores<DH>(qa, kd, g, t, scale, s);
+        if (ri.t >= 0) {
+            const int64_t o = int64_t(row) * a.H + h;
+            const double mrow = a.m_fin[o];
+            const double inv = 1.0 / a.l_fin[o];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int kk = 8 * j + 2 * t + e, key = k0 + kk;
+                    if (key < hi && key <= ri.t && key >= ri.klo)
+                        pm[lr * (AKC + 1) + kk] += (exp(s[j][e] - mrow) * inv) * inv_heads;
+                }
+        }
+        if (h == a.H - 1) {  // every head added: bin this chunk per row in key order
+            __syncthreads();
+            if (threadIdx.x < nrows) {
+                const int rr = threadIdx.x;
+                const int64_t rowoff = int64_t(i0 + rr) * a.S;
+                for (int kk = 0; kk < AKC; ++kk) {
+                    const int key = k0 + kk;
+                    if (key >= hi || key > rb.t) break;
+                    if (key < rb.klo) continue;
+                    const int dst = a.row_seg[key];
+                    if (dst < 0) continue;  // mass on query tokens is not summarised (prefill.hpp:283)
+                    if (dst != cur) {
+                        if (cur >= 0) rowbin[rowoff + cur] = run;
+                        cur = dst;
+                        run = 0.0;
+                    }
+                    run += pm[rr * (AKC + 1) + kk];
+                }
+            }
+        }
+    }
+    if (threadIdx.x < nrows && cur >= 0) rowbin[int64_t(i0 + threadIdx.x) * a.S + cur] = run;
+}
+
+template <int DH, int MODE>
+void launch_mode_dmma(const AttnArgs& a, dim3 grid, double scale, cudaStream_t st) {
+    const int smem = Geo<DH>::smem(MODE != M_STATS);
+    smem_attr(attn_dmma_kernel<DH, MODE>, smem);
+    attn_dmma_kernel<DH, MODE><<<grid, ANT, smem, st>>>(a, scale);
+    KEEP_LAUNCH_CHECK();
+}
+
+template <int DH>
+void run_dmma(const AttnArgs& a, cudaStream_t st) {
+    const int tiles = int(ceil_div(a.n, ART));
+    const double scale = 1.0 / std::sqrt(double(DH));  // prefill.hpp:129
+    const dim3 grid(unsigned(tiles), unsigned(a.H), unsigned(a.nsplit));
+    const int64_t nh = int64_t(a.n) * a.H;
+    if (!a.with_bins) {
+        launch_mode_dmma<DH, M_FLASH>(a, grid, scale, st);
+        if (a.nsplit > 1) {
+            const int64_t nd = int64_t(a.n) * a.d;
+            flash_combine_f64_kernel<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(a, DH);
+            KEEP_LAUNCH_CHECK();
+        }
+        return;
+    }
+    launch_mode_dmma<DH, M_STATS>(a, grid, scale, st);
+    launch_stats_combine(a, st);
+    launch_mode_dmma<DH, M_CTX>(a, grid, scale, st);
+    if (a.nsplit > 1) launch_ctx_combine(a, st);
+    (void)nh;
+    const int smem = Geo<DH>::S64 * 8 + ART * (AKC + 1) * 8 + Geo<DH>::S32 * 4;
+    smem_attr(attn_dmma_bins_kernel<DH>, smem);
+    attn_dmma_bins_kernel<DH><<<dim3(unsigned(tiles), unsigned(a.nsplit_b)), ANT, smem, st>>>(a, scale, a.inv_heads);
+    KEEP_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+bool attention_dmma_fits(int dh) { return dh == 8 || dh == 16 || dh == 32 || dh == 64 || dh == 128; }
+
+int attention_dmma_rows_per_tile() { return ART; }
+
+void launch_attention_parity_dmma(const AttnArgs& a, cudaStream_t st) {
+    if (a.n == 0) return;
+    switch (a.dh) {
+        case 8: run_dmma<8>(a, st); break;
+        case 16: run_dmma<16>(a, st); break;
+        case 32: run_dmma<32>(a, st); break;
+        case 64: run_dmma<64>(a, st); break;
+        case 128: run_dmma<128>(a, st); break;
+        default: raise(KEEP_ERR_CONFIG, "DMMA attention: head_dim must be 8, 16, 32, 64 or 128");
+    }
+}
+
+}  // namespace keep_b200

@@ -16,6 +16,8 @@
 // FAST instantiation (interim, CUDA cores): bf16 q/K/V, fp32 math, fp32 bins.
 #include "kernels.hpp"
 
+#include <cstring>
+
 #include <cfloat>
 
 namespace keep_b200 {
@@ -356,8 +358,30 @@ void run_attention(const AttnArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+void launch_stats_combine(const AttnArgs& a, cudaStream_t st) {
+    const int64_t nh = int64_t(a.n) * a.H;
+    stats_combine_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(nh, 256), kNumSMs * 8)), 256, 0, st>>>(a);
+    KEEP_LAUNCH_CHECK();
+}
+
+void launch_ctx_combine(const AttnArgs& a, cudaStream_t st) {
+    const int64_t nd = int64_t(a.n) * a.d;
+    ctx_combine_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(a);
+    KEEP_LAUNCH_CHECK();
+}
+
+// KEEP_PARITY_ATTN=simt: the scalar-DFMA kernels above (A/B reference)
+bool parity_attention_dmma(int dh) {
+    static const bool simt = [] {
+        const char* e = std::getenv("KEEP_PARITY_ATTN");
+        return e && !std::strcmp(e, "simt");
+    }();
+    return !simt && attention_dmma_fits(dh);
+}
+
 void launch_attention_parity(const AttnArgs& a, cudaStream_t st) {
-    run_attention<float, float, double, double>(a, st);
+    if (parity_attention_dmma(a.dh)) launch_attention_parity_dmma(a, st);
+    else run_attention<float, float, double, double>(a, st);
 }
 
 void launch_attention_fast(const AttnArgs& a, cudaStream_t st) {

@@ -200,6 +200,8 @@ struct Pass {
     // attention scratch
     DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi;
     int split_count = 1;
+    DevBuf split_lo_b, split_hi_b;  // PARITY DMMA bins pass: its own segment-aligned splits
+    int split_count_b = 1;
     int64_t split_key = -1;
     DevBuf vt, split_lo_a, split_hi_a, chunk_tab, zt;  // FAST tensor-core attention
     int nb = 0;

@@ -7,13 +7,43 @@
 // with vec_mat for any tiling in M/N (no split-K, k never reordered).
 // Fused epilogues: QKV split + scatter of K/V rows into the merged cache,
 // fp32 residual add (prefill.hpp:289-291, 302-303), ReLU (299-300).
+#include <cstdlib>
+
 #include "kernels.hpp"
 
 namespace keep_b200 {
 
 namespace {
 constexpr int BM = 64, BN = 64, BK = 16, TR = 4, TC = 4;
+
+__device__ __forceinline__ void epi_store1(const EpiArgs& epi, int m, int n, float v) {
+    switch (epi.kind) {
+        case EPI_QKV: {
+            const int d = epi.d;
+            if (n < d) {
+                epi.out[int64_t(m) * epi.ldo + n] = v;
+            } else if (n < 2 * d) {
+                static_cast<float*>(epi.kdst)[int64_t(epi.rows[m]) * d + (n - d)] = v;
+            } else {
+                static_cast<float*>(epi.vdst)[int64_t(epi.rows[m]) * d + (n - 2 * d)] = v;
+            }
+            break;
+        }
+        case EPI_RESID: {
+            float* o = epi.out + int64_t(m) * epi.ldo + n;
+            const float x = *o + v;
+            *o = x;
+            if (epi.out_bf16) epi.out_bf16[int64_t(m) * epi.ldo + n] = __float2bfloat16_rn(x);
+            break;
+        }
+        case EPI_RELU:
+            epi.out[int64_t(m) * epi.ldo + n] = (v < 0.0f) ? 0.0f : v;
+            break;
+        default:
+            epi.out[int64_t(m) * epi.ldo + n] = v;
+    }
 }
+}  // namespace
 
 __global__ void __launch_bounds__(256)
 gemm_f64acc_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B, int64_t ldb,
@@ -70,39 +100,106 @@ gemm_f64acc_kernel(const float* __restrict__ A, int64_t lda, const float* __rest
         for (int c = 0; c < TC; ++c) {
             const int n = n0 + tx + 16 * c;
             if (n >= N) continue;
-            const float v = static_cast<float>(acc[r][c]);
-            switch (epi.kind) {
-                case EPI_QKV: {
-                    const int d = epi.d;
-                    if (n < d) {
-                        epi.out[int64_t(m) * epi.ldo + n] = v;
-                    } else if (n < 2 * d) {
-                        static_cast<float*>(epi.kdst)[int64_t(epi.rows[m]) * d + (n - d)] = v;
-                    } else {
-                        static_cast<float*>(epi.vdst)[int64_t(epi.rows[m]) * d + (n - 2 * d)] = v;
-                    }
-                    break;
-                }
-                case EPI_RESID: {
-                    float* o = epi.out + int64_t(m) * epi.ldo + n;
-                    const float x = *o + v;
-                    *o = x;
-                    if (epi.out_bf16) epi.out_bf16[int64_t(m) * epi.ldo + n] = __float2bfloat16_rn(x);
-                    break;
-                }
-                case EPI_RELU:
-                    epi.out[int64_t(m) * epi.ldo + n] = (v < 0.0f) ? 0.0f : v;
-                    break;
-                default:
-                    epi.out[int64_t(m) * epi.ldo + n] = v;
-            }
+            epi_store1(epi, m, n, static_cast<float>(acc[r][c]));
         }
     }
 }
 
+namespace {
+// ------------------------------------------------------------ skinny GEMM --
+// M <= 32 rows (the layers after the walk recompute only the query): a
+// weight stream, HBM-bound at 4 N K bytes.  CTA = 32 columns x every row x all
+// of K; 256 threads = 8 row slots x 32 columns, RPT rows per thread.  B and A
+// tiles (32 k x 32 columns, M x 32 k) arrive by cp.async in a 4-deep ring (several
+// CTAs per SM keep ~64 KB of the stream in flight) and
+// are widened to fp64 once per stage (not per use: the fp32 -> fp64 convert
+// runs on the quarter-rate XU pipe).  Every output is still one thread's DFMA
+// chain in ascending k: bit-exact with vec_mat, like the tiled kernel.
+constexpr int SK_KB = 32, SK_ST = 4, SK_NC = 32;
+
+__device__ __forceinline__ void cpa16(void* dst, const void* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(256) gemm_f64_skinny_kernel(const float* __restrict__ A, int64_t lda,
+                                                              const float* __restrict__ B, int64_t ldb, int M, int N,
+                                                              int K, EpiArgs epi) {
+    constexpr int MR = 8 * RPT;
+    __shared__ __align__(16) float bst[SK_ST][SK_KB][SK_NC];
+    __shared__ __align__(16) float ast[SK_ST][MR][SK_KB];
+    __shared__ double bd[SK_KB][SK_NC];
+    __shared__ double ad[MR][SK_KB];
+    const int tid = threadIdx.x, col = tid & 31, rs = tid >> 5;
+    const int n0 = blockIdx.x * SK_NC;
+    const int nkb = int(ceil_div(K, SK_KB));
+    auto issue = [&](int kb) {
+        if (kb < nkb) {
+            const int s = kb % SK_ST, k0 = kb * SK_KB;
+            {  // B: 32 k-rows x 128 bytes
+                const int r = tid >> 3, c = tid & 7;
+                const bool ok = k0 + r < K && n0 + 4 * c < N;
+                cpa16(&bst[s][r][4 * c], B + (ok ? int64_t(k0 + r) * ldb + n0 + 4 * c : 0), ok);
+            }
+            for (int e = tid; e < M * 8; e += 256) {  // A: M rows x 128 bytes
+                const int r = e >> 3, c = e & 7;
+                const bool ok = k0 + 4 * c < K;
+                cpa16(&ast[s][r][4 * c], A + (ok ? int64_t(r) * lda + k0 + 4 * c : 0), ok);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int kb = 0; kb < SK_ST - 1; ++kb) issue(kb);
+    double acc[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
+    for (int kb = 0; kb < nkb; ++kb) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(SK_ST - 2) : "memory");
+        __syncthreads();  // stage kb landed; the previous fp64 tile is consumed
+        const int s = kb % SK_ST;
+        for (int e = tid; e < SK_KB * SK_NC; e += 256) bd[e >> 5][e & 31] = double(bst[s][e >> 5][e & 31]);
+        for (int e = tid; e < M * SK_KB; e += 256) ad[e >> 5][e & 31] = double(ast[s][e >> 5][e & 31]);
+        __syncthreads();
+        issue(kb + SK_ST - 1);
+        const int kn = min(SK_KB, K - kb * SK_KB);
+        for (int kk = 0; kk < kn; ++kk) {
+            const double b = bd[kk][col];
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) acc[r] = fma(ad[rs + 8 * r][kk], b, acc[r]);
+        }
+    }
+    const int n = n0 + col;
+    if (n >= N) return;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int m = rs + 8 * r;
+        if (m < M) epi_store1(epi, m, n, static_cast<float>(acc[r]));
+    }
+}
+
+// KEEP_PARITY_SKINNY=0: the tiled kernel for few rows too (A/B)
+bool skinny_f64_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_PARITY_SKINNY");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+}  // namespace
+
 void launch_gemm_f64acc(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
                         const EpiArgs& epi, cudaStream_t st) {
     if (M == 0 || N == 0) return;
+    // few rows: the weight stream (16-byte cp.async needs 16-byte aligned rows)
+    if (M <= 32 && skinny_f64_enabled() && K % 4 == 0 && N % 4 == 0 && lda % 4 == 0 && ldb % 4 == 0) {
+        const unsigned grid = unsigned(ceil_div(N, SK_NC));
+        if (M <= 8) gemm_f64_skinny_kernel<1><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, epi);
+        else if (M <= 16) gemm_f64_skinny_kernel<2><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, epi);
+        else gemm_f64_skinny_kernel<4><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, epi);
+        KEEP_LAUNCH_CHECK();
+        return;
+    }
     dim3 grid(static_cast<unsigned>(ceil_div(N, BN)), static_cast<unsigned>(ceil_div(M, BM)));
     gemm_f64acc_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, epi);
     KEEP_LAUNCH_CHECK();

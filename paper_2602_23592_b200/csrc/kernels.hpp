@@ -112,6 +112,9 @@ struct AttnArgs {
     int nsplit;
     const int32_t* split_lo;  // [nsplit] first key of split
     const int32_t* split_hi;  // [nsplit] one past last key
+    int nsplit_b;             // the DMMA bins pass's own segment-aligned splits
+    const int32_t* split_lo_b;
+    const int32_t* split_hi_b;
     int rows_per_tile;
     // scratch / outputs
     double* m_part;  // [nsplit x n x H]
@@ -124,6 +127,14 @@ struct AttnArgs {
     void* rowbin;    // [n x S] fp64 (PARITY) / fp32 (FAST)
 };
 void launch_attention_parity(const AttnArgs& a, cudaStream_t st);
+// PARITY on the fp64 tensor cores (attn_dmma.cu): head_dim 8 / 16 / 32 / 64 / 128,
+// 64-row tiles; the split plan (split_lo / hi, nsplit) as for the SIMT kernels
+bool attention_dmma_fits(int dh);
+bool parity_attention_dmma(int dh);
+int attention_dmma_rows_per_tile();
+void launch_attention_parity_dmma(const AttnArgs& a, cudaStream_t st);
+void launch_stats_combine(const AttnArgs& a, cudaStream_t st);
+void launch_ctx_combine(const AttnArgs& a, cudaStream_t st);
 void launch_attention_fast(const AttnArgs& a, cudaStream_t st);
 
 }  // namespace keep_b200

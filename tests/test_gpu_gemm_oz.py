@@ -66,3 +66,19 @@ def test_ozaki_zero_rows_and_tiny_values():
     exact = (A.double() @ B.double()).float()
     assert torch.equal(oz[0], torch.zeros_like(oz[0]))
     assert torch.allclose(oz, exact, rtol=1e-6, atol=0)
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 96, 64), (8, 512, 260), (9, 512, 1024), (17, 160, 5120), (32, 2048, 996),
+                                   (8, 5120, 5120)])
+def test_dfma_skinny_is_vec_mat(M, N, K):
+    """Few rows (the deep layers): the DFMA weight-stream kernel keeps vec_mat's
+    exact arithmetic -- fp64 accumulation in ascending k, one rounding."""
+    import torch
+    rng = np.random.default_rng(M + N + K)
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = (rng.standard_normal((K, N)) / np.sqrt(K)).astype(np.float32)
+    acc = np.zeros((M, N), np.float64)
+    for k in range(K):  # tensor.hpp:36-39, k ascending
+        acc += A[:, k:k + 1].astype(np.float64) * B[k].astype(np.float64)
+    got = run(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), 2).cpu().numpy()
+    assert np.array_equal(got, acc.astype(np.float32))

@@ -15,7 +15,22 @@ pytestmark = pytest.mark.gpu
 
 # fp32 outputs: relative tolerance on max-normalised differences
 HIDDEN_RTOL = 2e-6
+# fp64 summaries: the Q.K^T dots run on the fp64 tensor cores (attn_dmma.cu)
+# in their own summation order.  A reordered dot moves a score s by
+# ~gamma_dh * sum|q k| * scale; at depth (no norms) |s|
+# reaches 1e3-1e4 and p moves by the same ~1e-10 relative amount.
 SUMMARY_ATOL = 1e-12
+SUMMARY_RTOL = 1e-9
+
+
+def summary_close(got, ref):
+    """per layer: |got - ref| <= atol + rtol * max|ref of that layer|"""
+    got, ref = np.asarray(got), np.asarray(ref)
+    for l in range(ref.shape[0]):
+        tol = SUMMARY_ATOL + SUMMARY_RTOL * float(np.max(np.abs(ref[l])))
+        if float(np.max(np.abs(got[l] - ref[l]))) > tol:
+            return False
+    return True
 
 
 def problem(ko, c):
@@ -119,8 +134,8 @@ def test_plan_keep_parity(ko, golden, ctx_cache, idx):
     assert got["orders"] == c["orders"], tag
     assert got["hops"].tolist() == c["hops"], tag
     # summaries: fp64, summation order only
-    assert np.max(np.abs(got["qts"] - np.array(c["qts"]))) <= SUMMARY_ATOL, tag
-    assert np.max(np.abs(got["sts"] - np.array(c["sts"]))) <= SUMMARY_ATOL, tag
+    assert summary_close(got["qts"], np.array(c["qts"])), tag
+    assert summary_close(got["sts"], np.array(c["sts"])), tag
     # last row vs the golden, whole final hidden vs the oracle
     assert rel(got["final_hidden"][-1], np.array(c["last_row"], np.float32)) <= HIDDEN_RTOL, tag
     w = ko.model_init(c["L"], c["H"], c["d"], c["mlp"], c["V"], c["seed"])
@@ -154,8 +169,8 @@ def test_selective_prefill_plans(ko, golden, ctx_cache):
         ref = ko.selective_prefill(p, w, plan, cached=cached)
         assert rel(got["final_hidden"], ref["final_hidden"]) <= HIDDEN_RTOL, name
         assert rel(got["kv"], ref["kv"]) <= HIDDEN_RTOL, name
-        assert np.max(np.abs(got["sts"] - ref["sts"])) <= SUMMARY_ATOL, name
-        assert np.max(np.abs(got["qts"] - ref["qts"])) <= SUMMARY_ATOL, name
+        assert summary_close(got["sts"], ref["sts"]), name
+        assert summary_close(got["qts"], ref["qts"]), name
         # merged KV takes the (device) cached rows verbatim (test_prefill.cpp:273-287)
         starts = np.concatenate([[0], np.cumsum(p.seg_len)])
         for l in range(L):
