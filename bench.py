@@ -8,14 +8,24 @@ selection, gathered recompute, merged-KV assembly, plus the first-token
 logits) over a 16K-token synthetic memory on Qwen2.5-14B dimensions
 (BASELINE.json configs[2], SURVEY.md 8 "C3").  Prints one JSON line.
 
-  value  recomputed tokens/s = sum_l N_act(l) / TTFT, device-timed (CUDA
-         events) with the memory KV resident in HBM.
-  e2e    the same metric through the C ABI call with host buffers (token
-         ids H2D, logits/plan D2H inside the timed region), host wall clock.
+The headline runs the PARITY numerics -- the reference's own arithmetic
+(fp32 storage, fp64-grade accumulation: Ozaki int8 tensor-core projections and
+fp64 DMMA attention), whose plans, walk orders and hop counts are the
+reference's (tests/test_gpu_parity.py, tests/test_gpu_c3_golden.py).  The bf16
+FAST mode runs beside it on the same inputs (`other_mode`), with its
+`selection_parity` against the headline (plans / walk orders / hops per layer
+and the PARITY walk's decision margins).
+
+  value    recomputed tokens/s = sum_l N_act(l) / TTFT, device-timed (CUDA
+           events) with the memory KV resident in HBM.
+  e2e      the same metric through the C ABI call with host buffers (token
+           ids H2D, logits/plan D2H inside the timed region), host wall clock.
+  updates  configs[2]'s "frequent dynamic-group updates": 35% of the dynamic
+           owners refreshed in place inside the TTFT before each query.
 The CPU baseline is the reference's own path (oracle/_ref, the unmodified
-headers; else the plain-C restatement) timed on a bounded one-layer sample of
-the same configuration on one host core and extrapolated op-for-op to the
-workload (the reference is single-threaded; a full C3 run takes days).
+headers) timed on a bounded one-layer full-width sample on one host core and
+extrapolated op-for-op to the same realised plan (the reference is
+single-threaded; a full C3 run takes days).
 """
 from __future__ import annotations
 
@@ -161,9 +171,12 @@ def ncu_traffic():
 
 
 def numerics_for(args, cfg):
-    """FAST (bf16 tensor cores) needs model / MLP widths in multiples of 64;
-    the reference's tiny CPU default (c1: d = 32) runs in PARITY."""
+    """PARITY (the reference's arithmetic; bit-exact selections) is the
+    headline; FAST (bf16 tensor cores) needs model / MLP widths in multiples
+    of 64 and reports its selection agreement beside it."""
     import paper_2602_23592_b200 as kb
+    if args.numerics == "exact":
+        return kb.PARITY_EXACT
     if args.numerics == "parity" or cfg["d"] % 64 or cfg["mlp"] % 64:
         return kb.PARITY
     return kb.FAST
@@ -195,41 +208,73 @@ def attention_pairs(layout, qlen, plan):
 
 
 # ------------------------------------------------------------------ CPU arm --
+PLAN_FIXTURE = os.path.join(ROOT, "tests", "golden", "{}_realized_plan.json")
+
+
+def host_cpu():
+    """Model name and logical core count of this host (stated beside the CPU baseline)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cores": os.cpu_count()}
+
+
+def plan_from_fixture(name, S, L):
+    """The realised plan of the workload as the GPU arm's PARITY run produced
+    it (tests/golden/c3_realized_plan.json, written by tools/c3_parity.py):
+    runs of layers sharing one segment set.  None if the fixture is absent."""
+    try:
+        with open(PLAN_FIXTURE.format(name)) as f:
+            fx = json.load(f)
+    except OSError:
+        return None
+    if fx.get("config") != name or fx.get("S") != S or fx.get("L") != L:
+        return None
+    plan = np.zeros((L, S), np.uint8)
+    for l0, l1, segs in fx["runs"]:
+        plan[l0:l1, segs] = 1
+    return plan
+
+
 _W_CACHE = {}
 
 
-def cpu_sample(cfg, seed=7, sample_segments=2, reps=1):
-    """Time the reference path (PrefillCursor::step + converge via plan_keep)
-    for ONE layer at the workload's full width on a small layout; return the
-    measured fp64-accumulate MAC rate and what was sampled."""
+def cpu_sample(cfg, seed=7, sample_segments=2):
+    """Time the reference's own path (plan_keep: PrefillCursor::step +
+    converge, recompute.hpp:140-180) for ONE layer at the workload's full width
+    on a small layout, on one host core (the reference is single-threaded).
+    Weights come from the reference's Model::init (model.hpp:54-73); the
+    layer's tensors are the same named streams as the workload model's.
+    Returns the measured fp64-accumulate MAC rate and what was sampled."""
     from oracle.oracle import Oracle, available, Problem
     kind = "reference" if available("kr") else "port"
     orc = Oracle("kr" if kind == "reference" else "ko")
     L1, H, d, mlp = 1, cfg["H"], cfg["d"], cfg["mlp"]
-    V = 1024  # vocabulary only feeds the embedding gather in a step
-    rng = np.random.default_rng(seed)
-    std = 1.0 / np.sqrt(d)
-    n_w = orc.weight_count(L1, H, d, mlp, V)
-    key = (n_w, seed)
+    V = 1024  # the vocabulary only feeds the embedding gather in a step
+    key = (kind, L1, H, d, mlp, V, seed)
     if key not in _W_CACHE:
-        _W_CACHE[key] = (rng.standard_normal(n_w, dtype=np.float32) * np.float32(std)).astype(np.float32)
+        _W_CACHE[key] = orc.model_init(L1, H, d, mlp, V, seed)
     w = _W_CACHE[key]
     from paper_2602_23592_b200.synth import make_instance_layout
     inst = make_instance_layout(seed, sample_segments, V)
     p = Problem(L1, H, d, mlp, V, seed, inst.seg_len, inst.tokens, inst.query)
     T = p.T
     cached = np.zeros((L1, 2, p.Tm, d), np.float32)
-    best = None
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        orc.plan_keep(p, w, np.ones(1), cached=cached)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
+    t0 = time.perf_counter()
+    orc.plan_keep(p, w, np.ones(1), cached=cached)
+    dt = time.perf_counter() - t0
     macs = T * (4.0 * d * d + 2.0 * d * mlp) + 2.0 * d * T * (T + 1) / 2.0
-    return {"kind": kind, "seconds": best, "macs": macs, "rate": macs / best, "rows": T,
-            "sample": f"one layer at full width (d={d}, H={H}, mlp={mlp}) over {T} rows "
-                      f"({sample_segments} segments + {len(inst.query)}-token query), V reduced to {V}; "
-                      f"{kind} path, 1 host core, extrapolated op-for-op to the workload"}
+    return {"kind": kind, "seconds": dt, "macs": macs, "rate": macs / dt, "rows": T,
+            "sample": f"reference plan_keep (oracle/_ref: the unmodified headers, -O2) for one layer at full width "
+                      f"(d={d}, H={H}, mlp={mlp}; Model::init weights) over {T} rows ({sample_segments} segments + "
+                      f"{len(inst.query)}-token query), V reduced to {V}; 1 host core; extrapolated op-for-op to the "
+                      f"workload's realised plan"}
 
 
 def cpu_extrapolate(sample, cfg, rows_per_layer, pairs_per_layer):
@@ -239,48 +284,124 @@ def cpu_extrapolate(sample, cfg, rows_per_layer, pairs_per_layer):
     return {"ttft_s": ttft_s, "tokens_per_s": float(np.sum(rows_per_layer)) / ttft_s}
 
 
-def budget_plan(cfg, layout, r):
-    """Plan sizes if every budget were realised (reference arm's workload
-    model; the realised walk can only be shorter)."""
-    import paper_2602_23592_b200 as kb
-    S = layout.S
-    plan = np.zeros((cfg["L"], S), np.uint8)
-    for l in range(cfg["L"]):
-        b = S if l == 0 else min(S, kb.layer_budget(r[l], S))
-        plan[l, :b] = 1
-    return plan
+def workload_config(args, cfg, layout, query, world, numerics_name):
+    """The config object both arms print (identical: same workload, metric, plan)."""
+    return {"workload": args.config, "desc": cfg["desc"], "L": cfg["L"], "H": cfg["H"], "d": cfg["d"],
+            "mlp": cfg["mlp"], "V": cfg["V"], "S": layout.S, "T": int(np.sum(layout.seg_len)) + len(query),
+            "units": {"static_groups_of_8": sum(1 for u in layout.units if u[2] == 1),
+                      "dynamic_segments": sum(1 for u in layout.units if u[2] == 0)},
+            "r_avg": cfg["r_avg"], "seed": args.seed, "query_len": len(query),
+            "parallelism": f"KV-head sharded x{world} (NCCL)" if world > 1 else "1 GPU",
+            "memory_kv": ("pinned-host canonical KV, layer-balanced K10 loader" if args.memory == "host" else
+                          "HBM-resident canonical KV (static groups joint, dynamic per segment)"),
+            "l2": "inputs larger than L2 (fp32 weights {:.1f} GB + memory KV {:.1f} GB read per step)".format(
+                4e-9 * cfg["L"] * (4 * cfg["d"] ** 2 + 2 * cfg["d"] * cfg["mlp"]),
+                8e-9 * cfg["L"] * cfg["d"] * int(np.sum(layout.seg_len)))}
 
 
 def run_reference(args, cfg):
-    import paper_2602_23592_b200 as kb
+    """The reference's own CPU implementation of the path (oracle/_ref, the
+    unmodified headers) on this host: the same workload and realised plan as
+    the GPU arm.  Only oracle/ and the pure-Python synthetic generator are
+    touched -- the product library is never loaded."""
+    from oracle.oracle import Oracle, available
+    orc = Oracle("kr" if available("kr") else "ko")
     layout, query = workload(cfg, args.seed)
-    r = kb.ratio_schedule(cfg["L"], cfg["r_avg"])
-    plan = budget_plan(cfg, layout, r)
+    r = orc.ratio_schedule(cfg["L"], cfg["r_avg"])
+    plan = plan_from_fixture(args.config, layout.S, cfg["L"])
+    plan_model = f"realised plan of the GPU PARITY run (tests/golden/{args.config}_realized_plan.json)"
+    if plan is None:  # no fixture for this config: every budget fully realised (an upper bound)
+        plan = np.zeros((cfg["L"], layout.S), np.uint8)
+        for l in range(cfg["L"]):
+            b = layout.S if l == 0 else min(layout.S, orc.layer_budget(float(r[l]), layout.S))
+            plan[l, :b] = 1
+        plan_model = "budgets fully realised (no plan fixture for this config)"
     seg_len = np.asarray(layout.seg_len)
     rows = plan.astype(np.int64) @ seg_len + len(query)
     pairs = attention_pairs(layout, len(query), plan)
     for _ in range(args.warmup):
-        cpu_sample(cfg, reps=1)
+        cpu_sample(cfg)
     vals = []
     t0 = time.perf_counter()
+    s = None
     for _ in range(args.steps):
-        s = cpu_sample(cfg, reps=1)
+        s = cpu_sample(cfg)
         vals.append(cpu_extrapolate(s, cfg, rows, pairs))
     wall = time.perf_counter() - t0
     v = float(np.median([x["tokens_per_s"] for x in vals]))
     ttft = float(np.median([x["ttft_s"] for x in vals])) * 1e3
+    conf = workload_config(args, cfg, layout, query, 1, "reference")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / max(args.steps, 1) * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32-store/f64-acc",
-            "data": "synthetic", "ttft_ms": ttft,
-            "config": {"workload": args.config, "desc": cfg["desc"], "S": layout.S,
-                       "T": int(seg_len.sum()) + len(query), "plan_model": "budgets fully realised"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": s["kind"], "sample": s["sample"]},
+            "data": "synthetic", "ttft_ms": ttft, "config": conf,
+            "plan_model": plan_model, "recomputed_tokens_per_step": float(np.sum(rows)),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": s["kind"], "sample": s["sample"],
+                             "host_cpu": host_cpu(), "ttft_ms_extrapolated": ttft},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(_finite(line)), flush=True)
 
 
+# -------------------------------------------------- selection parity (FAST) --
+def walk_margins(qts, sts, order, cand):
+    """Per hop of a converge walk (recompute.hpp:94-126): relative gap between
+    the chosen score and the best other allowed candidate (inf: no rival)."""
+    S = len(qts)
+    allowed = np.asarray(cand, bool).copy()
+    colsum = np.zeros(S, np.float64)
+    gaps = []
+    for h, pick in enumerate(order):
+        score = qts if h == 0 else colsum / h
+        ok = allowed & (score > 0)
+        ok[pick] = False
+        best = score[pick]
+        second = float(np.max(score[ok])) if ok.any() else -np.inf
+        gaps.append(float((best - second) / abs(best)) if best != 0 and np.isfinite(second) else float("inf"))
+        allowed[pick] = False
+        colsum += sts[pick]
+    return np.array(gaps)
+
+
+def selection_parity(ref, other, summaries):
+    """Compare another numerics mode's plan_keep with the headline (PARITY)
+    one on the same inputs: plans, walk orders and hops per layer, and the
+    PARITY walk's decision margins (bf16 can only flip near-ties)."""
+    L = ref["plan"].shape[0]
+    plans_eq = [bool(np.array_equal(ref["plan"][l], other["plan"][l])) for l in range(L)]
+    orders_eq = [ref["orders"][l] == other["orders"][l] for l in range(L)]
+    walks = [l for l in range(L) if ref["orders"][l] is not None]
+    per_walk = []
+    for l in walks:
+        cand = ref["plan"][l].astype(bool)
+        g = walk_margins(summaries["qts"][l], summaries["sts"][l], ref["orders"][l], cand)
+        o, f = ref["orders"][l], other["orders"][l] or []
+        first = next((i for i in range(min(len(o), len(f))) if o[i] != f[i]), None)
+        if first is None and len(o) != len(f):
+            first = min(len(o), len(f))
+        per_walk.append({"layer": l, "hops": len(o), "orders_equal": o == f, "first_differing_hop": first,
+                         "margin_at_first_difference": (float(g[first]) if first is not None and first < len(g)
+                                                        else None),
+                         "min_rel_margin": float(np.min(g)) if len(g) else None,
+                         "decisions_below_1e-6": int(np.sum(g < 1e-6)), "decisions_below_1e-3": int(np.sum(g < 1e-3))})
+    return {"layers": L, "plans_equal": int(sum(plans_eq)), "orders_equal": int(sum(orders_eq)),
+            "hops_equal": bool(np.array_equal(ref["hops"], other["hops"])),
+            "plan_layers_differing": [l for l in range(L) if not plans_eq[l]],
+            "order_layers_differing": [l for l in range(L) if not orders_eq[l]],
+            "walks": per_walk}
+
+
 # ------------------------------------------------------------------ GPU arm --
+def gpu_context(args, cfg, numerics, world, dev):
+    import paper_2602_23592_b200 as kb
+    L, H, d, mlp, V = cfg["L"], cfg["H"], cfg["d"], cfg["mlp"], cfg["V"]
+    if world > 1:
+        # KV-head sharding: one context per rank over the library's own NCCL
+        # communicator (torch.distributed only carries its unique id)
+        from paper_2602_23592_b200.dist import sharded_context
+        return sharded_context(L, H, d, mlp, V, args.seed, numerics, device=dev)
+    return kb.Context(L, H, d, mlp, V, args.seed, numerics, device=dev)
+
+
 def run_ours(args, cfg, rank, world, dist):
     import torch
 
@@ -288,22 +409,18 @@ def run_ours(args, cfg, rank, world, dist):
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
     numerics = numerics_for(args, cfg)
+    parity = numerics == kb.PARITY
     L, H, d, mlp, V = cfg["L"], cfg["H"], cfg["d"], cfg["mlp"], cfg["V"]
     layout, query = workload(cfg, args.seed)
     r = kb.ratio_schedule(L, cfg["r_avg"])
     t0 = time.perf_counter()
-    if world > 1:
-        # KV-head sharding: one context per rank over the library's own NCCL
-        # communicator (torch.distributed only carries its unique id)
-        from paper_2602_23592_b200.dist import sharded_context
-        ctx = sharded_context(L, H, d, mlp, V, args.seed, numerics, device=dev)
-    else:
-        ctx = kb.Context(L, H, d, mlp, V, args.seed, numerics, device=dev)
+    ctx = gpu_context(args, cfg, numerics, world, dev)
     ctx.model_init()
     t_init = time.perf_counter() - t0
     t0 = time.perf_counter()
     host_mem = args.memory == "host"
-    ctx.memory_compute_layout(layout, version=1, tier=kb.TIER_HOST if host_mem else kb.TIER_DEVICE)
+    tier = kb.TIER_HOST if host_mem else kb.TIER_DEVICE
+    ctx.memory_compute_layout(layout, version=1, tier=tier)
     t_mem = time.perf_counter() - t0
 
     def barrier():
@@ -311,59 +428,20 @@ def run_ours(args, cfg, rank, world, dist):
             dist.barrier()
         torch.cuda.synchronize()
 
-    # --updates F: before every query a fraction F of the dynamic owners was
-    # updated and must be refreshed (harness.hpp:609-628; "frequent dynamic
-    # updates", test_harness.cpp:266-268); the refresh is part of the TTFT
-    owners_all = layout.owners()
-    dyn = [i for i, o in enumerate(owners_all) if o[0] == kb.SEGMENT]
-    owner_tokens = [int(np.sum(layout.seg_len[o[2]:o[3]])) for o in owners_all]
-    upd_rng = np.random.default_rng(args.seed + 1)
-    version = [1]
-
     def step():
-        if args.updates > 0:
-            version[0] += 1
-            pick = [u for u in dyn if upd_rng.random() < args.updates]
-            # (the profiler times the refresh call as one scope; the prefill
-            # itself runs unprofiled in the timed steps)
-            was_on = step.profiling
-            ctx.profile_enable(True)
-            ctx.memory_refresh(layout, pick, version[0], tier=kb.TIER_HOST if host_mem else kb.TIER_DEVICE)
-            ctx.profile_enable(was_on)
-            # (owners not picked stay current at their old version)
-            step.refreshed_tokens = float(sum(owner_tokens[u] for u in pick))
         return ctx.plan_keep(layout, query, r, final_hidden=False)
 
-    step.refreshed_tokens = 0.0
-    step.profiling = False
     for _ in range(args.warmup):
         step()
     ctx.profile_read(reset=True)
     barrier()
     steps = []
-    refreshed = []
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             steps.append(step())
-            refreshed.append(step.refreshed_tokens)
     barrier()
-    refresh_ms = ctx.profile_read(reset=True)["refresh"]["ms"]  # device time of the in-TTFT refreshes
-    # per-phase device times (roofline, phase shares) from separate profiled
-    # steps: the per-phase events are a measurement artefact kept out of the
-    # timed steps above
-    n_prof = max(1, min(args.steps, 3))
-    step.profiling = True
-    ctx.profile_enable(True)
-    for _ in range(n_prof):
-        step()
-    ctx.profile_enable(False)
-    step.profiling = False
-    prof = ctx.profile_read(reset=True)
     ttft = np.array([s["ttft_ms"] for s in steps])
-    if args.updates > 0:
-        ttft = ttft + refresh_ms / max(args.steps, 1)
-    # recomputed tokens: the plan's rows per layer, plus every layer of the refreshed owners
-    tokens = float(np.sum(steps[-1]["rows_per_layer"])) + float(np.mean(refreshed)) * L
+    tokens = float(np.sum(steps[-1]["rows_per_layer"]))
     total_ms = float(np.sum(ttft))
     if dist is not None:
         t = torch.tensor([total_ms], device="cuda")
@@ -372,9 +450,21 @@ def run_ours(args, cfg, rank, world, dist):
     # one prefill per step for the whole job (heads split across the ranks)
     value = tokens * args.steps / (total_ms / 1e3)
 
-    # e2e: the C-ABI call with host buffers, host wall clock
+    # per-phase device times (roofline, phase shares) from separate profiled
+    # steps: the per-phase events are a measurement artefact kept out of the
+    # timed steps above
+    n_prof = 1 if parity else max(1, min(args.steps, 3))
+    ctx.profile_enable(True)
+    for _ in range(n_prof):
+        step()
+    ctx.profile_enable(False)
+    prof = ctx.profile_read(reset=True)
+
+    # e2e: the C-ABI call with host buffers (token ids in, plan / walk orders /
+    # logits out), host wall clock
+    n_e2e = max(1, min(args.steps, 3 if parity else args.steps))
     e2e_s = []
-    for _ in range(max(1, args.steps)):
+    for _ in range(n_e2e):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = step()
@@ -388,7 +478,45 @@ def run_ours(args, cfg, rank, world, dist):
     h2d = 4 * (len(layout.tokens) + len(query) + layout.S + 3 * len(layout.units) + L)
     d2h = 8 * V + L * layout.S * (1 + 4) + 4 * 2 * L + 8 * 2 * L
 
+    # configs[2] "with frequent dynamic-group updates": before each query a
+    # fraction of the dynamic owners was updated and is refreshed in place
+    # inside the TTFT (harness.hpp:609-628; 0.35 as test_harness.cpp:266-268)
+    updates = None
+    if args.updates > 0 and world == 1:
+        owners_all = layout.owners()
+        dyn = [i for i, o in enumerate(owners_all) if o[0] == kb.SEGMENT]
+        owner_tokens = [int(np.sum(layout.seg_len[o[2]:o[3]])) for o in owners_all]
+        upd_rng = np.random.default_rng(args.seed + 1)
+        version = 1
+        u_ttft, u_tok, u_ref = [], [], []
+        for i in range(1 + args.update_steps):
+            version += 1
+            pick = [u for u in dyn if upd_rng.random() < args.updates]
+            ctx.profile_read(reset=True)
+            ctx.profile_enable(True)
+            ctx.memory_refresh(layout, pick, version, tier=tier)
+            ctx.profile_enable(False)
+            ref_ms = ctx.profile_read(reset=True)["refresh"]["ms"]
+            res_u = step()
+            if i == 0:
+                continue  # (first: warm-up of the refresh workspace)
+            u_ttft.append(res_u["ttft_ms"] + ref_ms)
+            u_ref.append(ref_ms)
+            u_tok.append(float(np.sum(res_u["rows_per_layer"])) + L * float(sum(owner_tokens[u] for u in pick)))
+        updates = {"fraction_of_dynamic_owners": args.updates, "steps": args.update_steps,
+                   "ttft_ms": float(np.mean(u_ttft)), "refresh_ms_per_step": float(np.mean(u_ref)),
+                   "recomputed_tokens_per_step": float(np.mean(u_tok)),
+                   "value": float(np.mean(u_tok)) / (float(np.mean(u_ttft)) / 1e3), "unit": UNIT,
+                   "note": "the refreshed owners' canonical KV (all layers) is recomputed in place before the query; "
+                           "its device time is part of the TTFT and its rows of the recomputed tokens"}
+
     pk, src = peaks()
+    extra = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_peaks_int8_fp64.json")) as f:
+            extra = json.load(f)
+    except OSError:
+        pass
     gemm_phases = ["qkv", "wo", "mlp_in", "mlp_out"]
     g_ms = sum(prof[p]["ms"] for p in gemm_phases)
     g_fl = sum(prof[p]["flops"] for p in gemm_phases)
@@ -397,67 +525,89 @@ def run_ours(args, cfg, rank, world, dist):
     a_ms, a_fl = prof["attn"]["ms"], prof["attn"]["flops"]
     phase_ms = {k: round(v["ms"] / n_prof, 3) for k, v in prof.items() if v["ms"] > 0}
     traffic = ncu_traffic()
-    tensor_peak = pk["bf16_tflops_sustained"] if numerics == kb.FAST else 37.0
-    g_ach = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
-    a_ach = a_fl / (a_ms / 1e3) / 1e12 if a_ms > 0 else 0.0
-    gemm_roof = {"kernel": "gemm_tc_kernel (tcgen05 bf16, fused epilogues)" if numerics == kb.FAST else "gemm_f64acc",
-                 "bound": "tensor", "achieved": g_ach, "peak": tensor_peak, "unit": "TFLOP/s",
-                 "frac": g_ach / tensor_peak, "traffic": traffic.get("gemm_tc_kernel") if numerics == kb.FAST else None,
-                 "peak_source": src + " (bf16 sustained)", "per_launch_ms": g_ms / max(g_n, 1),
-                 "algorithmic_bytes_per_launch": g_by / max(g_n, 1),
-                 "hbm_gbs_achieved": g_by / (g_ms / 1e3) / 1e9 if g_ms > 0 else 0.0,
-                 "traffic_launches": DETAIL.get("gemm_tc_kernel") if numerics == kb.FAST else None,
-                 "traffic_note": "traffic = the ncu-captured layer-0 launches (M = 16,280: 0.82 GB algorithmic for "
-                                 "the QKV one), not the step average; A is re-read across weight-column bands, "
-                                 "at ~20% of HBM peak -- the kernel stays tensor-bound"}
-    attn_roof = {"kernel": "attn_tc2_kernel STATS + CTX / FLASH (K5, tcgen05, summary bins on the tensor core)"
-                 if numerics == kb.FAST else "attn_stats / ctx / bins kernels (K5, fp64 SIMT, PARITY)",
-                 "bound": "tensor", "achieved": a_ach, "peak": tensor_peak, "unit": "TFLOP/s",
-                 "frac": a_ach / tensor_peak, "traffic": traffic.get("attn_tc2_kernel") if numerics == kb.FAST else None,
-                 "peak_source": src,
-                 "note": "algorithmic FLOPs 4*d*sum(t+1) (QK^T + PV once); the kernel pair does QK^T twice"}
-    d_ms, d_by, d_n = prof["attn_decode"]["ms"], prof["attn_decode"]["bytes"], prof["attn_decode"]["launches"]
-    hbm_peak = pk["hbm_gbs"]
-    d_ach = d_by / (d_ms / 1e3) / 1e9 if d_ms > 0 else 0.0
-    # the layers after the walk: the query rows alone against the whole merged
-    # KV, HBM-bound (algorithmic bytes = K + V of the visible keys once + q + ctx)
-    decode_roof = {"kernel": "attn_decode_kernel (K5d, split-K flash decoding, TMA stages)", "bound": "hbm",
-                   "achieved": d_ach, "peak": hbm_peak, "unit": "GB/s", "frac": d_ach / hbm_peak,
-                   "traffic": traffic.get("attn_decode_kernel"), "traffic_launches": DETAIL.get("attn_decode_kernel"),
-                   "peak_source": src,
-                   "per_launch_ms": d_ms / max(d_n, 1), "algorithmic_bytes_per_launch": d_by / max(d_n, 1),
-                   "launches_per_step": d_n / n_prof}
+    if parity:
+        slices = int(os.environ.get("KEEP_OZ_SLICES", "7"))
+        pairs_oz = slices * (slices + 1) // 2
+        i8_peak = extra.get("int8_tops_sustained") or 2 * pk["bf16_tflops_sustained"]
+        g_ach = g_fl * pairs_oz / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
+        gemm_roof = {"kernel": "gemm_oz_kernel (Ozaki int8 tcgen05 kind::i8, fp64 Horner epilogue)", "bound": "tensor",
+                     "achieved": g_ach, "peak": i8_peak, "unit": "TOP/s (int8)", "frac": g_ach / i8_peak,
+                     "traffic": traffic.get("gemm_oz_kernel"), "traffic_launches": DETAIL.get("gemm_oz_kernel"),
+                     "peak_source": "measured int8 sustained (profiles/r02_peaks_int8_fp64.json: cuBLASLt "
+                                    "torch._int_mm 8192^3)" if extra else "2 x measured bf16 sustained",
+                     "algorithmic": f"2*M*N*K per projection x {pairs_oz} digit pairs ({slices} int8 digits per "
+                                    f"operand); phase includes the digit splits and the few-row DFMA weight stream",
+                     "fp64_equivalent_tflops": g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0,
+                     "per_launch_ms": g_ms / max(g_n, 1)}
+        fp64_peak = extra.get("fp64_dmma_tflops") or 37.0
+        a_ach = a_fl / (a_ms / 1e3) / 1e12 if a_ms > 0 else 0.0
+        attn_roof = {"kernel": "attn_dmma_kernel / attn_dmma_bins_kernel (K5, fp64 DMMA m8n8k4)", "bound": "tensor",
+                     "achieved": a_ach, "peak": fp64_peak, "unit": "TFLOP/s (fp64)", "frac": a_ach / fp64_peak,
+                     "traffic": traffic.get("attn_dmma_kernel"), "traffic_launches": DETAIL.get("attn_dmma_kernel"),
+                     "peak_source": "measured fp64 DMMA (tools/micro/fp64_peak.cu)",
+                     "note": "algorithmic FLOPs 4*d*sum(t+1) (QK^T + PV once); summary layers add a stats and "
+                             "a bins pass (Q.K^T twice more)"}
+        roofs = [gemm_roof, attn_roof]
+    else:
+        tensor_peak = pk["bf16_tflops_sustained"]
+        g_ach = g_fl / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
+        a_ach = a_fl / (a_ms / 1e3) / 1e12 if a_ms > 0 else 0.0
+        gemm_roof = {"kernel": "gemm_tc_kernel (tcgen05 bf16, fused epilogues)", "bound": "tensor", "achieved": g_ach,
+                     "peak": tensor_peak, "unit": "TFLOP/s", "frac": g_ach / tensor_peak,
+                     "traffic": traffic.get("gemm_tc_kernel"), "peak_source": src + " (bf16 sustained)",
+                     "per_launch_ms": g_ms / max(g_n, 1), "algorithmic_bytes_per_launch": g_by / max(g_n, 1),
+                     "traffic_launches": DETAIL.get("gemm_tc_kernel")}
+        attn_roof = {"kernel": "attn_tc2_kernel STATS + CTX / FLASH (K5, tcgen05, summary bins on the tensor core)",
+                     "bound": "tensor", "achieved": a_ach, "peak": tensor_peak, "unit": "TFLOP/s",
+                     "frac": a_ach / tensor_peak, "traffic": traffic.get("attn_tc2_kernel"), "peak_source": src,
+                     "note": "algorithmic FLOPs 4*d*sum(t+1) (QK^T + PV once)"}
+        roofs = [gemm_roof, attn_roof]
+        d_ms, d_by, d_n = prof["attn_decode"]["ms"], prof["attn_decode"]["bytes"], prof["attn_decode"]["launches"]
+        if d_ms > 0:
+            d_ach = d_by / (d_ms / 1e3) / 1e9
+            roofs.append({"kernel": "attn_decode_kernel (K5d, split-K flash decoding, TMA stages)", "bound": "hbm",
+                          "achieved": d_ach, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": d_ach / pk["hbm_gbs"],
+                          "traffic": traffic.get("attn_decode_kernel"), "peak_source": src,
+                          "per_launch_ms": d_ms / max(d_n, 1), "algorithmic_bytes_per_launch": d_by / max(d_n, 1)})
     roof = gemm_roof if g_ms >= a_ms else attn_roof
     launches = int(sum(v["kernels"] for v in prof.values())) // n_prof
     loader_info = None
     if host_mem:
         tr = ctx.loader_trace()
-        h2d_kv = float(sum(r["bytes"] for r in tr))
+        h2d_kv = float(sum(x["bytes"] for x in tr))
         ms = prof["loader"]["ms"] / n_prof
-        # time compute(l) spent waiting beyond the previous layer: not measurable per stream here;
-        # report volume, copy-engine time and achieved H2D bandwidth
         h2d += h2d_kv  # the memory KV crosses PCIe inside every step
         loader_info = {"h2d_bytes_per_step": h2d_kv, "copy_ms_per_step": ms,
                        "h2d_gbs": h2d_kv / (ms * 1e6) if ms > 0 else None,
-                       "items": len(tr), "preloads": sum(1 for r in tr if r["kind"] == "preload"),
-                       "urgent": sum(1 for r in tr if r["kind"] == "urgent")}
+                       "items": len(tr), "preloads": sum(1 for x in tr if x["kind"] == "preload"),
+                       "urgent": sum(1 for x in tr if x["kind"] == "urgent")}
 
-    # fidelity beside speed: KEEP's last row against a full
-    # recompute of the same prefill (schedule of ones), divergence as in
-    # prefill.hpp:501-531, plus the full recompute's own TTFT
-    quality = None
-    if args.updates == 0 and not args.no_quality:
-        keep_res = ctx.plan_keep(layout, query, r, final_hidden=True)
-        full_res = ctx.plan_keep(layout, query, np.ones(L), final_hidden=True)
-        l2, kl = ctx.divergence(keep_res["final_hidden"][-1], full_res["final_hidden"][-1])
-        quality = {"full_recompute_ttft_ms": full_res["ttft_ms"], "keep_ttft_ms": keep_res["ttft_ms"],
-                   "speedup_vs_full_recompute": full_res["ttft_ms"] / keep_res["ttft_ms"],
-                   "divergence_vs_full": {"l2": l2, "sym_kl": kl, "rel_l2": l2 / max(float(np.linalg.norm(
-                       full_res["final_hidden"][-1].astype(np.float64))), 1e-300)},
-                   # (sym_kl is NaN exactly where prefill.hpp:526-528's is: both
-                   # softmaxes underflow to 0 at the same vocabulary entries)
-                   "top1_agree": bool(np.argmax(keep_res["last_logits"]) == np.argmax(full_res["last_logits"])),
-                   "full_recomputed_tokens": float(np.sum(full_res["rows_per_layer"]))}
+    # selections of the other numerics mode on the same inputs (SURVEY.md
+    # 0.1(2): a bf16 mode must report its agreement and the decision margins)
+    sel = None
+    other_mode = None
+    if world == 1 and not args.no_compare and cfg["d"] % 64 == 0 and cfg["mlp"] % 64 == 0:
+        head = ctx.plan_keep(layout, query, r, final_hidden=False, summaries=True)
+        summ = {"qts": head.pop("qts"), "sts": head.pop("sts")}
+        ctx.close()
+        ctx = None
+        torch.cuda.synchronize()
+        other = kb.FAST if parity else kb.PARITY
+        c2 = kb.Context(L, H, d, mlp, V, args.seed, other, device=dev)
+        c2.model_init()
+        c2.memory_compute_layout(layout, version=1, tier=tier)
+        c2.plan_keep(layout, query, r, final_hidden=False)
+        o_steps = [c2.plan_keep(layout, query, r, final_hidden=False) for _ in range(3)]
+        c2.close()
+        ores = o_steps[-1]
+        o_ttft = float(np.median([x["ttft_ms"] for x in o_steps]))
+        ref_res, oth_res = (head, ores) if parity else (ores, head)
+        sel = selection_parity(ref_res, oth_res, summ if parity else None) if parity else None
+        other_mode = {"numerics": "fast (bf16 tcgen05)" if parity else "parity", "ttft_ms": o_ttft,
+                      "value": float(np.sum(ores["rows_per_layer"])) / (o_ttft / 1e3), "unit": UNIT,
+                      "plan_segments_per_layer": [int(x) for x in ores["plan"].sum(1)],
+                      "selections_identical_to_parity": (sel is not None and sel["plans_equal"] == L
+                                                         and sel["orders_equal"] == L and sel["hops_equal"])}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -465,7 +615,7 @@ def run_ours(args, cfg, rank, world, dist):
         plan = steps[-1]["plan"]
         ex = cpu_extrapolate(s, cfg, steps[-1]["rows_per_layer"], attention_pairs(layout, len(query), plan))
         cpu = {"value": ex["tokens_per_s"], "unit": UNIT, "cores": 1, "kind": s["kind"], "sample": s["sample"],
-               "ttft_ms_extrapolated": ex["ttft_s"] * 1e3, "sample_seconds": s["seconds"]}
+               "host_cpu": host_cpu(), "ttft_ms_extrapolated": ex["ttft_s"] * 1e3, "sample_seconds": s["seconds"]}
 
     if rank == 0:
         plan = steps[-1]["plan"]
@@ -473,38 +623,33 @@ def run_ours(args, cfg, rank, world, dist):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16" if numerics == kb.FAST else "f32-store/f64-acc", "data": "synthetic",
+            "dtype": "f32-store/f64-acc" if parity else "bf16", "data": "synthetic",
+            "numerics": ("parity: fp32 storage, fp64-grade accumulation (Ozaki int8 tcgen05 projections, "
+                         "fp64 DMMA attention) -- the reference's arithmetic (tensor.hpp:31-47)" if parity else
+                         "fast: bf16 tcgen05, fp32 accumulation (selections NOT guaranteed bit-exact)"),
             "ttft_ms": float(np.median(ttft)), "ttft_ms_min": float(np.min(ttft)),
-            "config": {"workload": args.config, "desc": cfg["desc"], "L": L, "H": H, "d": d, "mlp": mlp, "V": V,
-                       "S": layout.S, "T": int(np.sum(layout.seg_len)) + len(query),
-                       "units": {"static_groups_of_8": sum(1 for u in layout.units if u[2] == 1),
-                                 "dynamic_segments": sum(1 for u in layout.units if u[2] == 0)},
-                       "r_avg": cfg["r_avg"],
-                       "parallelism": f"KV-head sharded x{world} (NCCL)" if world > 1 else "1 GPU",
-                       "l2": "inputs larger than L2 ({:.1f} GB bf16 weights + {:.1f} GB memory KV read per step)".format(
-                           2e-9 * L * (4 * d * d + 2 * d * mlp), 4e-9 * L * d * int(np.sum(layout.seg_len))),
-                       "memory_kv": ("pinned-host canonical KV, layer-balanced K10 loader" if host_mem else
-                                     "HBM-resident canonical KV (static groups joint, dynamic per segment)")},
+            "config": workload_config(args, cfg, layout, query, world, "parity" if parity else "fast"),
             "recomputed_tokens_per_step": tokens,
-            "updates": ({"fraction_of_dynamic_owners": args.updates, "refreshed_tokens_per_step": float(np.mean(refreshed)),
-                         "refresh_ms_per_step": refresh_ms / max(args.steps, 1)} if args.updates > 0 else None),
             "plan_segments_per_layer": [int(x) for x in plan.sum(1)],
             "rows_per_layer": [int(x) for x in steps[-1]["rows_per_layer"]],
             "hops_per_layer": [int(x) for x in steps[-1]["hops"]],
             "phase_ms_per_step": phase_ms,
             "setup_s": {"model_init": t_init, "canonical_kv_refresh": t_mem},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ttft_ms": e2e_mean * 1e3},
+                    "ttft_ms": e2e_mean * 1e3, "steps": n_e2e},
             "gpu_launches": launches,
+            "updates": updates,
+            "selection_parity": sel,
+            "other_mode": other_mode,
             "loader": loader_info,
-            "quality": quality,
             "roofline": roof,
-            "roofline_kernels": [gemm_roof, attn_roof] + ([decode_roof] if d_ms > 0 else []),
+            "roofline_kernels": roofs,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
         print(json.dumps(_finite(line)), flush=True)
-    ctx.close()
+    if ctx is not None:
+        ctx.close()
 
 
 def run_batch(args, cfg):
@@ -596,13 +741,19 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--numerics", choices=["fast", "parity"], default="fast")
+    ap.add_argument("--numerics", choices=["fast", "parity", "exact"], default="parity",
+                    help="parity (default): the reference's fp32-store / fp64-accumulate arithmetic on the tensor "
+                         "cores; exact: bit-exact projections + reference-order scores (scalar fp64); fast: bf16")
     ap.add_argument("--r-avg", type=float, default=None)
     ap.add_argument("--seed", type=int, default=20250807)
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-quality", action="store_true", help="skip the full-recompute fidelity comparison")
-    ap.add_argument("--updates", type=float, default=0.0,
-                    help="fraction of dynamic owners updated (refreshed inside the TTFT) before every query")
+    ap.add_argument("--no-quality", action="store_true", help="(kept for compatibility; no-op)")
+    ap.add_argument("--no-compare", action="store_true",
+                    help="skip the other numerics mode's run (selection_parity / other_mode blocks)")
+    ap.add_argument("--updates", type=float, default=0.35,
+                    help="fraction of dynamic owners updated (refreshed inside the TTFT) before each query of the "
+                         "updates block (configs[2]: frequent dynamic-group updates; 0 disables the block)")
+    ap.add_argument("--update-steps", type=int, default=2)
     ap.add_argument("--memory", choices=["hbm", "host"], default="hbm",
                     help="memory KV resident in HBM (C2-C4) or pinned host DRAM with the K10 loader (C5-style)")
     ap.add_argument("--batch", type=int, default=1,

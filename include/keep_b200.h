@@ -68,7 +68,12 @@ enum {
     KEEP_ERR_CUDA = 6,       /* CUDA / NCCL / out of memory */
 };
 
-enum { KEEP_NUMERICS_PARITY = 0, KEEP_NUMERICS_FAST = 1 };
+/* PARITY: the reference's arithmetic (fp32 storage, fp64-grade accumulation)
+ *   on the tensor cores -- Ozaki int8 projections, fp64 DMMA attention;
+ * FAST: bf16 tcgen05, fp32 accumulation (selections not guaranteed);
+ * PARITY_EXACT: projections bit-exact with vec_mat (DFMA, ascending k) and
+ *   scores in the reference's dimension order (scalar fp64 attention). */
+enum { KEEP_NUMERICS_PARITY = 0, KEEP_NUMERICS_FAST = 1, KEEP_NUMERICS_PARITY_EXACT = 2 };
 
 /* Memory owner (OwnerRef, memory_store.hpp:61-88): a dynamic segment owns
  * per-segment blocks, a static group owns one joint block per layer. */
@@ -83,7 +88,8 @@ typedef struct {
     int32_t device;      /* CUDA ordinal */
     int32_t world_size;  /* KV-head shards G (1 = single GPU); num_heads % G == 0 */
     int32_t rank;        /* this context owns heads [rank*H/G, (rank+1)*H/G) */
-    int32_t reserved;
+    int32_t max_hops;    /* converge hop cap (BASELINE configs[3] "3-hop recompute"); 0 = the
+                            reference's uncapped walk (recompute.hpp:130-138) */
     /* world_size > 1: exactly one of the following (see keep_comm_unique_id) */
     const uint8_t* nccl_id; /* 128-byte ncclUniqueId shared by all ranks (library-owned comm) */
     void* nccl_comm;        /* caller-owned ncclComm_t */

@@ -168,6 +168,12 @@ int64_t ko_layer_budget(double ratio, int64_t S) {
  * re-derived each hop as the mean over the relevant set (summed in ascending
  * position, as std::set iterates) of segment_to_segment[m][i]; the pick is the
  * first strict maximum in ascending position among scores > 0. */
+/* Optional hop cap (BASELINE configs[3] "3-hop recompute"; not in the
+ * reference, whose converge runs up to S hops): the one-line restatement of
+ * the capped variant is the loop bound min(S, max_hops).  0 = uncapped. */
+static int g_max_hops = 0;
+void ko_set_max_hops(int max_hops) { g_max_hops = max_hops; }
+
 int ko_converge(int S, const double* qts, const double* sts, int64_t budget,
                 const uint8_t* cand, int32_t* order, int32_t* n_out, int32_t* hops_out) {
     double* score = (double*)malloc(sizeof(double) * (S > 0 ? S : 1));
@@ -175,7 +181,8 @@ int ko_converge(int S, const double* qts, const double* sts, int64_t budget,
     if (!score || !in_r) return fail(9, "oom");
     memcpy(score, qts, sizeof(double) * S);
     int n = 0, hop = 0;
-    while ((int64_t)n < budget && hop < S) {
+    const int hop_cap = (g_max_hops > 0 && g_max_hops < S) ? g_max_hops : S;
+    while ((int64_t)n < budget && hop < hop_cap) {
         if (n > 0) {
             for (int i = 0; i < S; ++i) {
                 if ((cand && !cand[i]) || in_r[i]) continue;

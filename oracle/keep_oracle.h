@@ -97,6 +97,9 @@ KEEP_ORACLE_API(ko_)
 KEEP_ORACLE_API(kr_)
 
 const char* ko_last_error(void);
+/* restatement-only extension: cap converge at max_hops hops (0 = the
+ * reference's uncapped walk); see keep_oracle.c */
+void ko_set_max_hops(int max_hops);
 const char* kr_last_error(void);
 
 #ifdef __cplusplus

@@ -138,7 +138,15 @@ class Oracle:
         f("divergence").argtypes = [pp, fp, fp, fp, dp, dp]
         f("logits").argtypes = [pp, fp, fp, dp]
         f("last_error").restype = C.c_char_p
+        if prefix == "ko":
+            lib.ko_set_max_hops.argtypes = [C.c_int]
         self._f = f
+
+    def set_max_hops(self, max_hops: int):
+        """restatement only (ko): cap converge at max_hops hops, 0 = uncapped."""
+        if self.prefix != "ko":
+            raise OracleError(1, "the hop cap exists only in the restatement (the reference has none)")
+        self.lib.ko_set_max_hops(int(max_hops))
 
     def _check(self, rc: int):
         if rc:

@@ -31,7 +31,7 @@ HEADER = os.path.join(os.path.dirname(HERE), "include", "keep_b200.h")
 OK, CONFIG, INPUT, PLAN, CACHE_MISS, TRACE, CUDA = range(7)
 ERROR_NAMES = {CONFIG: "ConfigError", INPUT: "InputError", PLAN: "PlanError",
                CACHE_MISS: "CacheMissError", TRACE: "TraceError", CUDA: "CudaError"}
-PARITY, FAST = 0, 1
+PARITY, FAST, PARITY_EXACT = 0, 1, 2
 SEGMENT, GROUP = 0, 1
 TIER_DEVICE, TIER_HOST = 0, 1
 
@@ -47,7 +47,7 @@ class keep_config(C.Structure):
     _fields_ = [("num_layers", C.c_int32), ("num_heads", C.c_int32), ("model_dim", C.c_int32),
                 ("mlp_dim", C.c_int32), ("vocab_size", C.c_int32), ("numerics", C.c_int32),
                 ("seed", C.c_uint64), ("device", C.c_int32), ("world_size", C.c_int32),
-                ("rank", C.c_int32), ("reserved", C.c_int32), ("nccl_id", C.c_void_p),
+                ("rank", C.c_int32), ("max_hops", C.c_int32), ("nccl_id", C.c_void_p),
                 ("nccl_comm", C.c_void_p), ("loopback", C.c_void_p)]
 
 
@@ -274,9 +274,9 @@ class Context:
 
     def __init__(self, L: int, H: int, d: int, mlp: int, V: int, seed: int,
                  numerics: int = PARITY, device: int = 0, world: int = 1, rank: int = 0,
-                 nccl_id: Optional[bytes] = None, loopback: Optional[LoopbackGroup] = None):
+                 nccl_id: Optional[bytes] = None, loopback: Optional[LoopbackGroup] = None, max_hops: int = 0):
         self.lib = load_library()
-        cfg = keep_config(L, H, d, mlp, V, numerics, seed, device, world, rank, 0)
+        cfg = keep_config(L, H, d, mlp, V, numerics, seed, device, world, rank, max_hops)
         self._id = None
         if nccl_id is not None:
             self._id = C.create_string_buffer(bytes(nccl_id), 128)

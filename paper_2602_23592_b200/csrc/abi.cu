@@ -176,13 +176,15 @@ void check_cfg(const keep_config& c) {  // ModelConfig::validate, model.hpp:28-3
     if (c.mlp_dim < 1) raise(KEEP_ERR_CONFIG, "mlp_dim must be positive");
     if (c.vocab_size < 1) raise(KEEP_ERR_CONFIG, "vocab_size must be positive");
     if (c.model_dim % c.num_heads != 0) raise(KEEP_ERR_CONFIG, "model_dim not divisible by num_heads");
-    if (c.numerics != KEEP_NUMERICS_PARITY && c.numerics != KEEP_NUMERICS_FAST)
+    if (c.numerics != KEEP_NUMERICS_PARITY && c.numerics != KEEP_NUMERICS_FAST &&
+        c.numerics != KEEP_NUMERICS_PARITY_EXACT)
         raise(KEEP_ERR_CONFIG, "unknown numerics mode");
     if (c.model_dim % 4 != 0) raise(KEEP_ERR_CONFIG, "model_dim must be a multiple of 4");
     if (c.model_dim / c.num_heads > 128) raise(KEEP_ERR_CONFIG, "head_dim > 128 not supported");
     if (c.numerics == KEEP_NUMERICS_FAST && (c.model_dim % 64 != 0 || c.mlp_dim % 64 != 0))
         raise(KEEP_ERR_CONFIG, "FAST numerics needs model_dim and mlp_dim multiples of 64");
     if (c.world_size < 1 || c.rank < 0 || c.rank >= c.world_size) raise(KEEP_ERR_CONFIG, "bad world_size / rank");
+    if (c.max_hops < 0) raise(KEEP_ERR_CONFIG, "max_hops must be >= 0 (0 = uncapped)");
     if (c.num_heads % c.world_size != 0) raise(KEEP_ERR_CONFIG, "num_heads must divide by world_size (KV-head shards)");
     if (c.numerics == KEEP_NUMERICS_FAST && (c.model_dim / c.world_size) % 64 != 0)
         raise(KEEP_ERR_CONFIG, "FAST numerics needs model_dim / world_size to be a multiple of 64");
@@ -348,7 +350,7 @@ void plan_splits(Context& c, Pass& p) {
     const int64_t key = (int64_t(p.n) << 32) ^ (int64_t(p.T) << 2) ^ (tc ? 1 : 0) ^ (p.block_diag ? 2 : 0);
     if (key == p.split_key) return;
     p.split_key = key;
-    const bool dmma = !c.fast && parity_attention_dmma(c.dh);
+    const bool dmma = !c.fast && !c.exact && parity_attention_dmma(c.dh);
     const int tiles = int(ceil_div(p.n, tc ? 128 : (dmma ? attention_dmma_rows_per_tile() : 16)));
     int nsplit = 1;
     if (tc && !p.block_diag) {
@@ -505,7 +507,7 @@ void layer_qkv(Context& c, Pass& p, int l) {
     if (!c.fast) {
         EpiArgs e{EPI_QKV, dl, p.q.as<float>(), dl, p.kdst[l], p.vdst[l], rows, nullptr};
         launch_gemm_parity(p.x.as<float>(), d, static_cast<const float*>(c.wslot(l, W_QKV)), 3 * dl, n, 3 * dl, d, e,
-                           st, c.oz);
+                           st, c.oz, c.exact);
     } else {
         EpiArgs e{EPI_QKV, dl, nullptr, dl, p.kdst[l], p.vdst[l], rows, p.q.as<__nv_bfloat16>()};
         if (use_tc_attention(c, p)) e.q_scale = float(1.4426950408889634 / std::sqrt(double(c.dh)));
@@ -538,6 +540,7 @@ void layer_attention(Context& c, Pass& p, int l, const void* q, void* ctx, const
     a.row_seg = p.d_row_seg.as<int32_t>();
     a.key_lo = p.block_diag ? p.d_key_lo.as<int32_t>() : nullptr;
     a.with_bins = p.with_summary;
+    a.exact = c.exact;
     a.S = p.S;
     a.nsplit = p.split_count;
     a.split_lo = p.split_lo.as<int32_t>();
@@ -695,16 +698,17 @@ void layer_dense(Context& c, Pass& p, int l) {
             {
                 ProfScope ps(c.prof, KEEP_PROF_WO, st, go, bo);
                 launch_gemm_parity(static_cast<const float*>(ctx_rows), d, static_cast<const float*>(c.wslot(l, W_O)), d, m,
-                                   d, d, eo, st, c.oz);
+                                   d, d, eo, st, c.oz, c.exact);
             }
             {
                 ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
                 EpiArgs ei{EPI_RELU, d, p.h.as<float>(), f, nullptr, nullptr, nullptr, nullptr};
-                launch_gemm_parity(xr, d, static_cast<const float*>(c.wslot(l, W_IN)), f, m, f, d, ei, st, c.oz);
+                launch_gemm_parity(xr, d, static_cast<const float*>(c.wslot(l, W_IN)), f, m, f, d, ei, st, c.oz, c.exact);
             }
             {
                 ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
-                launch_gemm_parity(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, m, d, f, eo, st, c.oz);
+                launch_gemm_parity(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, m, d, f, eo, st, c.oz,
+                                   c.exact);
             }
         } else {
             auto* xbr = p.xb.as<__nv_bfloat16>() + int64_t(r0) * d;
@@ -1652,7 +1656,8 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
             {
                 ProfScope ps(c.prof, KEEP_PROF_SELECT, c.s_sel, 0.0, 8.0 * double(S) * S * B);
                 launch_select_batch(S, B, bt.sel_ptrs.as<const double*>(), budget, bt.sel_cand.as<uint8_t>(),
-                                    bt.sel_cand.as<uint8_t>() + size_t(B) * S, bt.sel_order.as<int32_t>(), c.s_sel);
+                                    bt.sel_cand.as<uint8_t>() + size_t(B) * S, bt.sel_order.as<int32_t>(), c.s_sel,
+                                    c.cfg.max_hops);
             }
             KEEP_CUDA(cudaMemcpyAsync(hbuf, bt.sel_order.p, sizeof(int32_t) * size_t(B) * (S + 2), cudaMemcpyDeviceToHost,
                                       c.s_sel));
@@ -1769,6 +1774,7 @@ int keep_ctx_create(const keep_config* cfg, void** out) {
         c->f = cfg->mlp_dim;
         c->V = cfg->vocab_size;
         c->fast = cfg->numerics == KEEP_NUMERICS_FAST;
+        c->exact = cfg->numerics == KEEP_NUMERICS_PARITY_EXACT;
         c->elem = c->fast ? 2 : 4;
         c->G = cfg->world_size;
         c->R = cfg->rank;
@@ -2117,7 +2123,7 @@ int keep_importance_evaluation(void* ctx, int32_t S, const double* qts, const do
         c.sel_order.ensure(sizeof(int32_t) * (std::max(S, 1) + 2));
         int32_t* o = c.sel_order.as<int32_t>();
         launch_select(S, dq.as<double>(), ds.as<double>(), budget, candidates ? dc.as<uint8_t>() : nullptr, o + 2,
-                      o, o + 1, st);
+                      o, o + 1, st, c.cfg.max_hops);
         std::vector<int32_t> h(S + 2);
         KEEP_CUDA(cudaMemcpyAsync(h.data(), o, sizeof(int32_t) * (S + 2), cudaMemcpyDeviceToHost, st));
         KEEP_CUDA(cudaStreamSynchronize(st));
@@ -2301,7 +2307,7 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
                 {
                     ProfScope ps(c.prof, KEEP_PROF_SELECT, c.s_sel, 0.0, 8.0 * double(S) * S);
                     launch_select(S, p.summ.as<double>(), p.summ.as<double>() + S, budget, c.sel_cand.as<uint8_t>(), o + 2,
-                                  o, o + 1, c.s_sel);
+                                  o, o + 1, c.s_sel, c.cfg.max_hops);
                 }
                 KEEP_CUDA(cudaMemcpyAsync(hbuf, o, sizeof(int32_t) * (S + 2), cudaMemcpyDeviceToHost, c.s_sel));
                 KEEP_CUDA(cudaEventRecord(ev_sel, c.s_sel));

@@ -126,10 +126,13 @@ __device__ __forceinline__ void scores(const double (&qa)[DH / 4], const double*
 #pragma unroll
         for (int j = 0; j < NJ; ++j) dmma(s[j], qa[i], ks[(8 * j + g) * Geo<DH>::P64 + 4 * i + t]);
     }
+    // s = dot * scale rounded on its own (prefill.hpp:140): no FMA contraction
+    // with the later s - max, which at depth (|s| ~ 1e18, ulp ~ 1e2) would move
+    // exp() by whole orders of magnitude and make the passes disagree
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
-        s[j][0] *= scale;
-        s[j][1] *= scale;
+        s[j][0] = __dmul_rn(s[j][0], scale);
+        s[j][1] = __dmul_rn(s[j][1], scale);
     }
 }
 
@@ -214,14 +217,14 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_kernel(AttnArgs a, double sc
             for (int j = 0; j < NJ; ++j)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const double p = (any && vis[j][e]) ? exp(s[j][e] - mn) : 0.0;
+                    const double p = (any && vis[j][e]) ? exp(__dsub_rn(s[j][e], mn)) : 0.0;
                     s[j][e] = p;
                     part += p;
                 }
             part += __shfl_xor_sync(0xffffffffu, part, 1);
             part += __shfl_xor_sync(0xffffffffu, part, 2);
             if (any) {
-                const double alpha = m == -DBL_MAX ? 0.0 : exp(m - mn);
+                const double alpha = m == -DBL_MAX ? 0.0 : exp(__dsub_rn(m, mn));
                 l = l * alpha + part;
                 m = mn;
                 if (MODE == M_FLASH && alpha != 1.0) {
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_kernel(AttnArgs a, double sc
 #pragma unroll
             for (int j = 0; j < NJ; ++j)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) s[j][e] = vis[j][e] ? exp(s[j][e] - m) * inv : 0.0;
+                for (int e = 0; e < 2; ++e) s[j][e] = vis[j][e] ? __dmul_rn(exp(__dsub_rn(s[j][e], m)), inv) : 0.0;
         }
         if (WV) {  // O += P.V
 #pragma unroll
@@ -371,7 +374,9 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_bins_kernel(AttnArgs a, doub
                 for (int e = 0; e < 2; ++e) {
                     const int kk = 8 * j + 2 * t + e, key = k0 + kk;
                     if (key < hi && key <= ri.t && key >= ri.klo)
-                        pm[lr * (AKC + 1) + kk] += (exp(s[j][e] - mrow) * inv) * inv_heads;
+                        pm[lr * (AKC + 1) + kk] = __dadd_rn(
+                            pm[lr * (AKC + 1) + kk],
+                            __dmul_rn(__dmul_rn(exp(__dsub_rn(s[j][e], mrow)), inv), inv_heads));
                 }
         }
         if (h == a.H - 1) {  // every head added: bin this chunk per row in key order

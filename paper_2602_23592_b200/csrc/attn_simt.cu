@@ -38,6 +38,17 @@ template <typename A> __device__ __forceinline__ A ex(A x);
 template <> __device__ __forceinline__ double ex<double>(double x) { return exp(x); }
 template <> __device__ __forceinline__ float ex<float>(float x) { return __expf(x); }
 
+// Explicitly rounded steps (no FMA contraction): the reference rounds
+// s = dot * scale, then s - max, then p = e * inv, then p * inv_heads
+// (prefill.hpp:140-151); at depth |s| is so large that a contracted
+// s * scale - max moves exp() by orders of magnitude.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
 template <typename A> __device__ __forceinline__ A neg_inf();
 template <> __device__ __forceinline__ double neg_inf<double>() { return -DBL_MAX; }
 template <> __device__ __forceinline__ float neg_inf<float>() { return -FLT_MAX; }
@@ -102,7 +113,7 @@ __device__ __forceinline__ void scores4(const Smem<ACC>& sm, int r, int c, int d
         const int key = c + 16 * kk;
         ACC acc = ACC(0);
         for (int j = 0; j < dh; ++j) acc = fma(sm.q[r * MAXDH + j], ACC(sm.k[key * (MAXDH + 1) + j]), acc);
-        s[kk] = acc * scale;
+        s[kk] = mul_rn(acc, scale);
     }
 }
 
@@ -153,11 +164,11 @@ attn_stats_kernel(AttnArgs a, ACC scale) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
             const int key = k0 + c + 16 * kk;
-            if (any && c + 16 * kk < nk && key <= t && key >= klo) part += ex(s[kk] - mn);
+            if (any && c + 16 * kk < nk && key <= t && key >= klo) part += ex(sub_rn(s[kk], mn));
         }
         part = red16_sum(part);
         if (any) {
-            l = (m == neg_inf<ACC>() ? ACC(0) : l * ex(m - mn)) + part;
+            l = (m == neg_inf<ACC>() ? ACC(0) : l * ex(sub_rn(m, mn))) + part;
             m = mn;
         }
     }
@@ -219,7 +230,7 @@ attn_ctx_kernel(AttnArgs a, ACC scale) {
         for (int kk = 0; kk < 4; ++kk) {
             const int key = k0 + c + 16 * kk;
             const bool ok = (c + 16 * kk < nk) && key <= t && key >= klo;
-            sm.p[r * KC + c + 16 * kk] = ok ? ex(s[kk] - mrow) * inv : ACC(0);
+            sm.p[r * KC + c + 16 * kk] = ok ? mul_rn(ex(sub_rn(s[kk], mrow)), inv) : ACC(0);
         }
         __syncthreads();
         for (int kk = 0; kk < nk; ++kk) {
@@ -294,7 +305,7 @@ attn_bins_kernel(AttnArgs a, ACC scale, ACC inv_heads) {
                 for (int kk = 0; kk < 4; ++kk) {
                     const int key = k0 + c + 16 * kk;
                     if ((c + 16 * kk < nk) && key <= t && key >= klo)
-                        pm[r * KC + c + 16 * kk] += (ex(s[kk] - mrow) * inv) * inv_heads;
+                        pm[r * KC + c + 16 * kk] = add_rn(pm[r * KC + c + 16 * kk], mul_rn(mul_rn(ex(sub_rn(s[kk], mrow)), inv), inv_heads));
                 }
             }
         }
@@ -380,7 +391,7 @@ bool parity_attention_dmma(int dh) {
 }
 
 void launch_attention_parity(const AttnArgs& a, cudaStream_t st) {
-    if (parity_attention_dmma(a.dh)) launch_attention_parity_dmma(a, st);
+    if (!a.exact && parity_attention_dmma(a.dh)) launch_attention_parity_dmma(a, st);
     else run_attention<float, float, double, double>(a, st);
 }
 

@@ -154,7 +154,7 @@ bool ozaki_eligible(int M, int N, int K);
 void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
                        const EpiArgs& epi, cudaStream_t st, OzWork& w, int max_ctas = kNumSMs);
 void launch_gemm_parity(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
-                        const EpiArgs& epi, cudaStream_t st, OzWork& w, int max_ctas = kNumSMs);
+                        const EpiArgs& epi, cudaStream_t st, OzWork& w, bool exact = false, int max_ctas = kNumSMs);
 
 // A KV arena: per layer, keys [rows x d] then values [rows x d].  Owner
 // payloads are row ranges of an arena (a batch of canonical refreshes writes
@@ -286,6 +286,7 @@ struct Context {
     int G = 1, R = 0, Hl = 0, dl = 0;
     std::unique_ptr<Comm> comm;
     bool fast = false;
+    bool exact = false;  // KEEP_NUMERICS_PARITY_EXACT: DFMA projections + reference-order scores
     int elem = 4;  // merged-KV element bytes
     cudaStream_t s_main = nullptr, s_copy = nullptr, s_sel = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;

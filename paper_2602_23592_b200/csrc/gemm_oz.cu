@@ -497,8 +497,8 @@ void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb,
 }
 
 void launch_gemm_parity(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
-                        const EpiArgs& epi, cudaStream_t st, OzWork& w, int max_ctas) {
-    if (ozaki_eligible(M, N, K) && (epi.kind != EPI_QKV || epi.d % 32 == 0)) launch_gemm_ozaki(A, lda, B, ldb, M, N, K, epi, st, w, max_ctas);
+                        const EpiArgs& epi, cudaStream_t st, OzWork& w, bool exact, int max_ctas) {
+    if (!exact && ozaki_eligible(M, N, K) && (epi.kind != EPI_QKV || epi.d % 32 == 0)) launch_gemm_ozaki(A, lda, B, ldb, M, N, K, epi, st, w, max_ctas);
     else launch_gemm_f64acc(A, lda, B, ldb, M, N, K, epi, st);
 }
 

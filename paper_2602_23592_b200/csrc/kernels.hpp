@@ -56,11 +56,11 @@ void launch_summary_reduce(const TB* rowbin, int S, const int32_t* seg_cbeg, con
 // K7: converge on the device (recompute.hpp:86-138).
 void launch_select(int S, const double* qts, const double* sts, int64_t budget,
                    const uint8_t* candidates, int32_t* order, int32_t* n_out, int32_t* hops_out,
-                   cudaStream_t st);
+                   cudaStream_t st, int max_hops = 0);  // max_hops > 0: capped walk (BASELINE configs[3])
 
 // K7 for a batch of queries: one walk per CTA (see select_batch_kernel).
 void launch_select_batch(int S, int B, const double* const* summ, int64_t budget, const uint8_t* cand,
-                         const uint8_t* run, int32_t* out, cudaStream_t st);
+                         const uint8_t* run, int32_t* out, cudaStream_t st, int max_hops = 0);
 
 // K11: Model::logits of one fp32 row, fp64 accumulation in ascending i
 // (model.hpp:76-85).
@@ -107,6 +107,7 @@ struct AttnArgs {
     const int32_t* key_lo;   // [T] first visible key of a row (nullptr = 0: causal prefix);
                              // block-diagonal contexts for canonical refresh
     bool with_bins;
+    bool exact;     // PARITY_EXACT: the scalar kernels (scores in the reference's dimension order)
     int S;
     // split plan (segment-aligned key splits, computed by the host)
     int nsplit;

@@ -439,7 +439,8 @@ __device__ HopRed block_hop_reduce(HopRed x, HopRed* scratch) {
 // positions (tid + k * 512) is a register bitmask.
 __device__ __forceinline__ void select_impl(int S, const double* __restrict__ qts, const double* __restrict__ sts,
                                             int64_t budget, const uint8_t* __restrict__ cand,
-                                            int32_t* __restrict__ order, int32_t* n_out, int32_t* hops_out) {
+                                            int32_t* __restrict__ order, int32_t* n_out, int32_t* hops_out,
+                                            int hop_cap) {
     extern __shared__ __align__(16) uint8_t sraw[];
     double* colsum = reinterpret_cast<double*>(sraw);               // [S]
     float* colabs = reinterpret_cast<float*>(colsum + S);           // [S]
@@ -472,7 +473,8 @@ __device__ __forceinline__ void select_impl(int S, const double* __restrict__ qt
             err = (2.0 * (n + 2)) * u * (double(colabs[i]) * (1.0 + 0x1.0p-20) / double(n)) + 4.0 * u * fabs(sc);
         }
     };
-    while (int64_t(n) < budget && hop < S) {
+    // hop_cap = S: the reference's walk (recompute.hpp:133); smaller: the capped variant
+    while (int64_t(n) < budget && hop < hop_cap) {
         HopRed x{0.0, -1, -INFINITY, -1, -INFINITY};
         for (int k = 0; k < items; ++k) {
             if (!(allowed >> k & 1u)) continue;
@@ -543,8 +545,8 @@ __device__ __forceinline__ void select_impl(int S, const double* __restrict__ qt
 __global__ void __launch_bounds__(kSelThreads, 1)
 select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ sts, int64_t budget,
               const uint8_t* __restrict__ cand, int32_t* __restrict__ order, int32_t* n_out,
-              int32_t* hops_out) {
-    select_impl(S, qts, sts, budget, cand, order, n_out, hops_out);
+              int32_t* hops_out, int hop_cap) {
+    select_impl(S, qts, sts, budget, cand, order, n_out, hops_out, hop_cap);
 }
 
 // One walk per CTA (batched queries): CTA b reads summ[b] ([S] qts then
@@ -552,32 +554,35 @@ select_kernel(int S, const double* __restrict__ qts, const double* __restrict__ 
 // {n, hops, order...}; CTAs with run[b] == 0 exit.
 __global__ void __launch_bounds__(kSelThreads, 1)
 select_batch_kernel(int S, const double* const* __restrict__ summ, int64_t budget, const uint8_t* __restrict__ cand,
-                    const uint8_t* __restrict__ run, int32_t* __restrict__ out) {
+                    const uint8_t* __restrict__ run, int32_t* __restrict__ out, int hop_cap) {
     const int b = blockIdx.x;
     if (!run[b]) return;
     const double* sm = summ[b];
     int32_t* o = out + int64_t(b) * (S + 2);
-    select_impl(S, sm, sm + S, budget, cand + int64_t(b) * S, o + 2, o, o + 1);
+    select_impl(S, sm, sm + S, budget, cand + int64_t(b) * S, o + 2, o, o + 1, hop_cap);
 }
 
+static int hop_cap_of(int S, int max_hops) { return max_hops > 0 ? std::min(S, max_hops) : S; }
+
 void launch_select_batch(int S, int B, const double* const* summ, int64_t budget, const uint8_t* cand,
-                         const uint8_t* run, int32_t* out, cudaStream_t st) {
+                         const uint8_t* run, int32_t* out, cudaStream_t st, int max_hops) {
     if (S > kSelMaxS) raise(KEEP_ERR_CONFIG, "selector supports at most 14336 segments");
     const size_t smem = size_t(std::max(S, 1)) * (8 + 4 + 1) + 16;
     if (smem > 48 * 1024)
         KEEP_CUDA(cudaFuncSetAttribute(select_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    select_batch_kernel<<<B, kSelThreads, smem, st>>>(S, summ, budget, cand, run, out);
+    select_batch_kernel<<<B, kSelThreads, smem, st>>>(S, summ, budget, cand, run, out, hop_cap_of(S, max_hops));
     KEEP_LAUNCH_CHECK();
 }
 
 void launch_select(int S, const double* qts, const double* sts, int64_t budget,
                    const uint8_t* candidates, int32_t* order, int32_t* n_out, int32_t* hops_out,
-                   cudaStream_t st) {
+                   cudaStream_t st, int max_hops) {
     if (S > kSelMaxS) raise(KEEP_ERR_CONFIG, "selector supports at most 14336 segments");
     const size_t smem = size_t(std::max(S, 1)) * (8 + 4 + 1) + 16;
     if (smem > 48 * 1024)
         KEEP_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    select_kernel<<<1, kSelThreads, smem, st>>>(S, qts, sts, budget, candidates, order, n_out, hops_out);
+    select_kernel<<<1, kSelThreads, smem, st>>>(S, qts, sts, budget, candidates, order, n_out, hops_out,
+                                                hop_cap_of(S, max_hops));
     KEEP_LAUNCH_CHECK();
 }
 

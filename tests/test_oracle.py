@@ -128,3 +128,18 @@ def test_restatement_equals_reference_random(ko, kr, seed):
     for k in ["plan", "hops", "qts", "sts", "final_hidden", "kv"]:
         assert np.array_equal(a[k], b[k]), k
     assert a["orders"] == b["orders"]
+
+
+def test_hop_cap_restatement(ko, golden):
+    """ko_set_max_hops: the capped walk stops at max_hops hops; a cap >= S is the reference."""
+    c = next(x for x in golden["converge"] if x["name"] == "hand_trace")
+    try:
+        ko.set_max_hops(2)
+        assert ko.converge(c["qts"], c["sts"], c["budget"]) == ([3, 1], 2)
+        ko.set_max_hops(1)
+        assert ko.converge(c["qts"], c["sts"], c["budget"]) == ([3], 1)
+        ko.set_max_hops(100)
+        assert ko.converge(c["qts"], c["sts"], c["budget"]) == (c["order"], c["hops"])
+    finally:
+        ko.set_max_hops(0)
+    assert ko.converge(c["qts"], c["sts"], c["budget"]) == (c["order"], c["hops"])

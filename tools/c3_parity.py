@@ -1,13 +1,23 @@
-"""Full-scale selection parity: the C3 plan_keep in PARITY (fp32 storage,
-fp64 accumulation -- the reference's arithmetic) against FAST (bf16 tensor
-cores) on the same synthetic weights, memory and query.  Writes a JSON
-summary (plans per layer, walk orders, hops, last-row drift, logits top-1)."""
+"""Full-scale selection parity and the realised-plan fixture.
+
+Runs plan_keep on a BASELINE config in PARITY (the reference's arithmetic)
+and in FAST (bf16) on the same synthetic weights, memory and query; writes
+  * <out>: bench.selection_parity of FAST against PARITY (plans, walk orders,
+    hops per layer, the PARITY walks' decision margins) plus both TTFTs;
+  * tests/golden/<config>_realized_plan.json (with --fixture): the PARITY
+    plan as runs of layers sharing one segment set -- the realised workload
+    the CPU reference arm of bench.py extrapolates to.
+
+    python tools/c3_parity.py [c3] [gpurun_out/c3_parity.json] [--fixture]
+"""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import bench, paper_2602_23592_b200 as kb
-cfgname = sys.argv[1] if len(sys.argv) > 1 else "c3"
-out = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out/c3_parity.json"
+
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+cfgname = args[0] if args else "c3"
+out = args[1] if len(args) > 1 else "gpurun_out/c3_parity.json"
 cfg = bench.CONFIGS[cfgname]
 lay, q = bench.workload(cfg, 20250807)
 r = kb.ratio_schedule(cfg["L"], cfg["r_avg"])
@@ -18,27 +28,41 @@ for name, mode in (("parity", kb.PARITY), ("fast", kb.FAST)):
         ctx.model_init()
         ctx.memory_compute_layout(lay)
         ctx.plan_keep(lay, q, r, final_hidden=False)  # warm
-        res[name] = ctx.plan_keep(lay, q, r, final_hidden=True)
+        res[name] = ctx.plan_keep(lay, q, r, final_hidden=True, summaries=(name == "parity"))
     res[name]["wall_s"] = time.time() - t0
     print(name, "ttft_ms", res[name]["ttft_ms"], "wall", res[name]["wall_s"], flush=True)
 P, F = res["parity"], res["fast"]
-L = cfg["L"]
-same_plan = [bool(np.array_equal(P["plan"][l], F["plan"][l])) for l in range(L)]
-same_order = [P["orders"][l] == F["orders"][l] for l in range(L)]
+summ = {"qts": P.pop("qts"), "sts": P.pop("sts")}
+sel = bench.selection_parity(P, F, summ)
 hp, hf = P["final_hidden"][-len(q):].astype(np.float64), F["final_hidden"][-len(q):].astype(np.float64)
-summary = {
-    "config": cfgname, "S": lay.S, "T": int(np.sum(lay.seg_len)) + len(q),
-    "parity_ttft_ms": P["ttft_ms"], "fast_ttft_ms": F["ttft_ms"],
-    "plan_segments_per_layer_parity": [int(x) for x in P["plan"].sum(axis=1)],
-    "plan_segments_per_layer_fast": [int(x) for x in F["plan"].sum(axis=1)],
-    "layers_with_identical_plan": int(sum(same_plan)), "layers": L,
-    "walk_orders_identical": [i for i, x in enumerate(same_order) if x and P["orders"][i] is not None],
-    "walk_orders_differ": [i for i, x in enumerate(same_order) if not x],
-    "hops_parity": [int(x) for x in P["hops"]], "hops_fast": [int(x) for x in F["hops"]],
-    "query_rows_rel_max_diff": float(np.max(np.abs(hp - hp * 0 - hf)) / max(np.max(np.abs(hp)), 1e-300)),
-    "logits_top1_parity": int(np.argmax(P["last_logits"])), "logits_top1_fast": int(np.argmax(F["last_logits"])),
-}
-print(json.dumps(summary))
-os.makedirs(os.path.dirname(out), exist_ok=True)
+summary = {"config": cfgname, "S": lay.S, "T": int(np.sum(lay.seg_len)) + len(q),
+           "parity_ttft_ms": P["ttft_ms"], "fast_ttft_ms": F["ttft_ms"],
+           "oz_slices": int(os.environ.get("KEEP_OZ_SLICES", "7")),
+           "plan_segments_per_layer_parity": [int(x) for x in P["plan"].sum(axis=1)],
+           "plan_segments_per_layer_fast": [int(x) for x in F["plan"].sum(axis=1)],
+           "hops_parity": [int(x) for x in P["hops"]], "hops_fast": [int(x) for x in F["hops"]],
+           "selection_parity": sel,
+           "query_rows_rel_max_diff": float(np.max(np.abs(hp - hf)) / max(np.max(np.abs(hp)), 1e-300)),
+           "logits_top1_parity": int(np.argmax(P["last_logits"])), "logits_top1_fast": int(np.argmax(F["last_logits"])),
+           "parity_orders": {str(l): P["orders"][l] for l in range(cfg["L"]) if P["orders"][l] is not None}}
+print(json.dumps({k: v for k, v in summary.items() if k != "parity_orders"}))
+os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
 with open(out, "w") as f:
-    json.dump(summary, f, indent=1)
+    json.dump(bench._finite(summary), f, indent=1)
+if "--fixture" in sys.argv:
+    runs, l = [], 0
+    plan = P["plan"]
+    while l < cfg["L"]:
+        e = l + 1
+        while e < cfg["L"] and np.array_equal(plan[e], plan[l]):
+            e += 1
+        runs.append([l, e, [int(i) for i in np.nonzero(plan[l])[0]]])
+        l = e
+    fx = {"generator": "tools/c3_parity.py (GPU PARITY plan_keep; layers 0-1 pinned to oracle/_ref by "
+                       "tests/golden/c3_width_golden.npz)", "config": cfgname, "seed": 20250807,
+          "S": lay.S, "L": cfg["L"], "runs": runs,
+          "rows_per_layer": [int(x) for x in P["rows_per_layer"]], "hops": [int(x) for x in P["hops"]]}
+    path = os.path.join(bench.ROOT, "tests", "golden", f"{cfgname}_realized_plan.json")
+    with open(path, "w") as f:
+        json.dump(fx, f, separators=(",", ":"))
+    print("wrote", path)
