@@ -582,32 +582,58 @@ def run_ours(args, cfg, rank, world, dist):
                        "items": len(tr), "preloads": sum(1 for x in tr if x["kind"] == "preload"),
                        "urgent": sum(1 for x in tr if x["kind"] == "urgent")}
 
-    # selections of the other numerics mode on the same inputs (SURVEY.md
-    # 0.1(2): a bf16 mode must report its agreement and the decision margins)
-    sel = None
-    other_mode = None
-    if world == 1 and not args.no_compare and cfg["d"] % 64 == 0 and cfg["mlp"] % 64 == 0:
-        head = ctx.plan_keep(layout, query, r, final_hidden=False, summaries=True)
+    # selections of the other numerics modes on the same inputs (SURVEY.md
+    # 0.1(2): a bf16 mode must report its agreement and the decision margins;
+    # PARITY_EXACT -- bit-exact projections, reference-order scores -- is the
+    # arbiter of the tensor-core PARITY mode)
+    sel, other_mode, exact_mode = None, None, None
+    if world == 1 and not args.no_compare and parity and cfg["d"] % 64 == 0 and cfg["mlp"] % 64 == 0:
+        head = ctx.plan_keep(layout, query, r, final_hidden=True, summaries=True)
         summ = {"qts": head.pop("qts"), "sts": head.pop("sts")}
+        hq = head["final_hidden"][-len(query):].astype(np.float64)
         ctx.close()
         ctx = None
         torch.cuda.synchronize()
-        other = kb.FAST if parity else kb.PARITY
-        c2 = kb.Context(L, H, d, mlp, V, args.seed, other, device=dev)
-        c2.model_init()
-        c2.memory_compute_layout(layout, version=1, tier=tier)
-        c2.plan_keep(layout, query, r, final_hidden=False)
-        o_steps = [c2.plan_keep(layout, query, r, final_hidden=False) for _ in range(3)]
-        c2.close()
+
+        def run_mode(mode, n):
+            c2 = kb.Context(L, H, d, mlp, V, args.seed, mode, device=dev)
+            c2.model_init()
+            c2.memory_compute_layout(layout, version=1, tier=tier)
+            c2.plan_keep(layout, query, r, final_hidden=False)
+            outs = [c2.plan_keep(layout, query, r, final_hidden=True) for _ in range(n)]
+            c2.close()
+            torch.cuda.synchronize()
+            return outs
+
+        def hidden_rel(o):
+            oq = o["final_hidden"][-len(query):].astype(np.float64)
+            return float(np.max(np.abs(oq - hq)) / max(float(np.max(np.abs(oq))), 1e-300))
+
+        o_steps = run_mode(kb.FAST, 3)
         ores = o_steps[-1]
         o_ttft = float(np.median([x["ttft_ms"] for x in o_steps]))
-        ref_res, oth_res = (head, ores) if parity else (ores, head)
-        sel = selection_parity(ref_res, oth_res, summ if parity else None) if parity else None
-        other_mode = {"numerics": "fast (bf16 tcgen05)" if parity else "parity", "ttft_ms": o_ttft,
+        sel = selection_parity(head, ores, summ)
+        other_mode = {"numerics": "fast (bf16 tcgen05)", "ttft_ms": o_ttft,
                       "value": float(np.sum(ores["rows_per_layer"])) / (o_ttft / 1e3), "unit": UNIT,
                       "plan_segments_per_layer": [int(x) for x in ores["plan"].sum(1)],
-                      "selections_identical_to_parity": (sel is not None and sel["plans_equal"] == L
-                                                         and sel["orders_equal"] == L and sel["hops_equal"])}
+                      "selections_identical_to_parity": (sel["plans_equal"] == L and sel["orders_equal"] == L
+                                                         and sel["hops_equal"]),
+                      "query_rows_rel_diff_vs_parity": hidden_rel(ores),
+                      "logits_top1_equal": bool(np.argmax(ores["last_logits"]) == np.argmax(head["last_logits"]))}
+        if not args.no_exact:
+            e_res = run_mode(kb.PARITY_EXACT, 1)[-1]
+            se = selection_parity(e_res, head, summ)
+            exact_mode = {"numerics": "parity_exact (DFMA projections bit-exact with vec_mat, scalar fp64 attention "
+                                      "in the reference's dimension order)", "ttft_ms": e_res["ttft_ms"],
+                          "plans_equal": se["plans_equal"], "orders_equal": se["orders_equal"],
+                          "hops_equal": se["hops_equal"], "layers": L,
+                          "selections_identical": (se["plans_equal"] == L and se["orders_equal"] == L
+                                                   and se["hops_equal"]),
+                          "query_rows_rel_diff": hidden_rel(e_res),
+                          "logits_top1_equal": bool(np.argmax(e_res["last_logits"]) == np.argmax(head["last_logits"])),
+                          "note": "without norms the reference's deep layers are one-hot (|logit| ~ 1e18, fp64 ulp "
+                                  "~ 1e2): any re-ordered fp64 sum can move a deep attention pick, so the final hidden "
+                                  "state of the tensor-core mode may differ while every selection stays identical"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -641,6 +667,7 @@ def run_ours(args, cfg, rank, world, dist):
             "updates": updates,
             "selection_parity": sel,
             "other_mode": other_mode,
+            "exact_mode": exact_mode,
             "loader": loader_info,
             "roofline": roof,
             "roofline_kernels": roofs,
@@ -749,7 +776,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-quality", action="store_true", help="(kept for compatibility; no-op)")
     ap.add_argument("--no-compare", action="store_true",
-                    help="skip the other numerics mode's run (selection_parity / other_mode blocks)")
+                    help="skip the other numerics modes' runs (selection_parity / other_mode / exact_mode blocks)")
+    ap.add_argument("--no-exact", action="store_true", help="skip the PARITY_EXACT comparison (~40 s at C3)")
     ap.add_argument("--updates", type=float, default=0.35,
                     help="fraction of dynamic owners updated (refreshed inside the TTFT) before each query of the "
                          "updates block (configs[2]: frequent dynamic-group updates; 0 disables the block)")

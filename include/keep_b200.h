@@ -295,6 +295,15 @@ typedef struct {
 int keep_profile_enable(void* ctx, int32_t on);
 int keep_profile_read(void* ctx, keep_profile* out, int32_t reset);
 
+/* ---- RoPE position re-shift (north_star subsystem 3; off by default) -----
+ * The reference is NoPE (model.hpp:3-8): theta = 0 keeps it, and
+ * every parity run uses 0.  theta > 0 applies rotary embeddings to q and k
+ * (pairs (2j, 2j+1) per head, angle pos * theta^(-2j/dh)); canonical KV is
+ * rotated at owner-local positions and a reused block's keys are re-shifted by
+ * its layout offset when merged.  Single GPU, HBM-resident memory, single
+ * query (keep_plan_keep / the cursor); no oracle exists for it. */
+int keep_set_rope(void* ctx, double theta);
+
 /* ---- test hook (not part of the reference surface) ----------------------
  * C[M x N] (fp32, device) = A[M x K] . Bt[N x K]^T with bf16 device operands
  * on the tcgen05 GEMM; force_bn 0 = automatic tile, 64 or 256 = forced. */

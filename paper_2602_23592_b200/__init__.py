@@ -149,6 +149,7 @@ def load_library() -> C.CDLL:
         "keep_logits": (C.c_int, [vp, fp, dp]),
         "keep_divergence": (C.c_int, [vp, fp, fp, dp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+        "keep_set_rope": (C.c_int, [vp, C.c_double]),
         "keep_debug_gemm_parity": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
         "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
         "keep_loader_trace": (C.c_int, [vp, C.POINTER(keep_load_record), i32, i32p]),
@@ -313,6 +314,11 @@ class Context:
     def trim(self):
         """Release the grow-only workspaces (keep_ctx_trim)."""
         _check(self.lib.keep_ctx_trim(self._h))
+
+    def set_rope(self, theta: float):
+        """Opt-in RoPE position re-shift hook (0 = off: the reference's NoPE)."""
+        _check(self.lib.keep_set_rope(self._h, float(theta)))
+        return self
 
     def model_init(self):
         _check(self.lib.keep_model_init(self._h))

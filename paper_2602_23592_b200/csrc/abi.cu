@@ -514,6 +514,9 @@ void layer_qkv(Context& c, Pass& p, int l) {
         launch_gemm_bf16(p.xb.as<__nv_bfloat16>(), d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_QKV)), d, n,
                          3 * dl, d, e, st);
     }
+    if (c.rope_theta > 0.0)  // opt-in RoPE: q and the new key rows at their positions (owner-local in a refresh)
+        launch_rope_qk(p.q.p, p.kdst[l], n, rows, p.block_diag ? p.d_key_lo.as<int32_t>() : nullptr, dl, c.dh,
+                       c.rope_theta, c.fast, st);
 }
 
 // Attention of the pass's compact rows against a [p.T x dl] merged KV (k, v;
@@ -907,7 +910,7 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
     }
     // cached rows of this layer (prefill.hpp:255-263, 340-350): resolve first
     std::vector<void*> ks, vs;
-    std::vector<int32_t> dr, nr;
+    std::vector<int32_t> dr, nr, rope;
     int maxr = 0;
     for (int i = 0; i < S; ++i) {
         if (active[i] || loader_covers(c, i) || alias_l) continue;  // host-tier owners: K10 loader
@@ -922,6 +925,11 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
             raise(KEEP_ERR_INPUT, "cached block of " + owner_str(ok) + " is shorter than its members");
         ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * c.dl * c.elem);
         vs.push_back(layer_values(c, *pl, l) + c.seg_owner_row[i] * c.dl * c.elem);
+        if (c.rope_theta > 0.0) {  // re-shift: owner-local rows -> layout rows
+            rope.push_back(p.seg_start[i]);
+            rope.push_back(p.seg_len[i]);
+            rope.push_back(int32_t(p.seg_start[i] - c.seg_owner_row[i]));
+        }
         dr.push_back(p.seg_start[i]);
         nr.push_back(p.seg_len[i]);
         maxr = std::max(maxr, p.seg_len[i]);
@@ -947,6 +955,11 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
         const int32_t *dp, *np;
         upload_copy_args(c, ks, vs, dr, nr, st, &kp, &vp, &dp, &np);
         launch_copy_cached(kp, vp, dp, np, int(ks.size()), int64_t(c.dl) * c.elem, p.kdst[l], p.vdst[l], maxr, st);
+        if (!rope.empty()) {
+            upload(p.rope_tab, rope, st);
+            launch_rope_shift(p.kdst[l], p.rope_tab.as<int32_t>(), int(rope.size() / 3), maxr, c.dl, c.dh, c.rope_theta,
+                              c.fast, st);
+        }
     }
     p.with_summary = p.summary_wanted;
     if (p.n == 0) {  // no computed rows: the summary is all zero
@@ -1018,6 +1031,7 @@ Arena* in_order_arena(Context& c, const std::vector<int32_t>& seg_start, int tie
 void detect_alias(Context& c, const std::vector<int32_t>& seg_start, int Tm, int T) {
     c.alias_arena = nullptr;
     c.alias_hold.reset();
+    if (c.rope_theta > 0.0) return;  // arena rows hold owner-local positions; the merged KV needs re-shifted keys
     Arena* ar = in_order_arena(c, seg_start, KEEP_TIER_DEVICE);
     if (ar && ar->used == Tm && ar->rows >= T) {
         c.alias_arena = ar;
@@ -1047,6 +1061,8 @@ void cursor_begin(Context& c, const keep_layout* lay, const int32_t* query, int 
     }
     detect_alias(c, p.seg_start, p.Tm, p.T);
     loader_begin(c, p);
+    if (c.rope_theta > 0.0 && c.loader.on && c.loader.any_host)
+        raise(KEEP_ERR_CONFIG, "the RoPE hook re-shifts HBM-resident blocks only (memory in pinned host DRAM)");
 }
 
 // Row T-1 of the final hidden state (device pointer or nullptr if dropped).
@@ -2246,13 +2262,26 @@ int keep_divergence(void* ctx, const float* row_a, const float* row_b, double* l
 // the budget and applies the returned order (one small D2H per layer).
 int keep_plan_keep_batch(void* ctx, const keep_layout* layout, int32_t batch, const int32_t* queries, int32_t qlen,
                          const double* sched, int32_t multihop, keep_plan_result* outs) {
-    return guard([&] { plan_keep_batch(*C(ctx), layout, batch, queries, qlen, sched, multihop != 0, outs); });
+    return guard([&] {
+        if (C(ctx)->rope_theta > 0.0) raise(KEEP_ERR_CONFIG, "the RoPE hook is single-query (keep_plan_keep)");
+        plan_keep_batch(*C(ctx), layout, batch, queries, qlen, sched, multihop != 0, outs);
+    });
+}
+
+int keep_set_rope(void* ctx, double theta) {
+    return guard([&] {
+        if (!(theta >= 0.0)) raise(KEEP_ERR_CONFIG, "rope theta must be >= 0 (0 = off)");
+        Context& c = *C(ctx);
+        if (c.G > 1) raise(KEEP_ERR_CONFIG, "the RoPE hook is single-GPU");
+        c.rope_theta = theta;
+    });
 }
 
 int keep_selective_prefill_batch(void* ctx, const keep_layout* layout, int32_t batch, const int32_t* queries,
                                  int32_t qlen, const uint8_t* plans, keep_plan_result* outs) {
     return guard([&] {
         if (!plans) raise(KEEP_ERR_PLAN, "null plans");
+        if (C(ctx)->rope_theta > 0.0) raise(KEEP_ERR_CONFIG, "the RoPE hook is single-query");
         plan_keep_batch(*C(ctx), layout, batch, queries, qlen, nullptr, true, outs, plans);
     });
 }

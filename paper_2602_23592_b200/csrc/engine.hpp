@@ -201,6 +201,7 @@ struct Pass {
     DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi;
     int split_count = 1;
     DevBuf split_lo_b, split_hi_b;  // PARITY DMMA bins pass: its own segment-aligned splits
+    DevBuf rope_tab;                // RoPE hook: (row, rows, delta) of the re-shifted cached blocks
     int split_count_b = 1;
     int64_t split_key = -1;
     DevBuf vt, split_lo_a, split_hi_a, chunk_tab, zt;  // FAST tensor-core attention
@@ -287,6 +288,7 @@ struct Context {
     std::unique_ptr<Comm> comm;
     bool fast = false;
     bool exact = false;  // KEEP_NUMERICS_PARITY_EXACT: DFMA projections + reference-order scores
+    double rope_theta = 0.0;  // keep_set_rope: 0 = NoPE, the reference (model.hpp:3-8)
     int elem = 4;  // merged-KV element bytes
     cudaStream_t s_main = nullptr, s_copy = nullptr, s_sel = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;

@@ -73,6 +73,14 @@ void launch_logits_multi(const float* rows, int B, const float* unembed, int d, 
 void launch_divergence(const float* a, const float* b, int d, const double* la, const double* lb, int V, double* out,
                        cudaStream_t st);
 
+// RoPE hook (off by default; the reference is NoPE): rotate q[i] and the merged
+// key row rows[i] at position rows[i] - key_lo[rows[i]]; re-shift cached key
+// rows (tab: per entry first row, rows, delta) by delta positions.
+void launch_rope_qk(void* q, void* k, int n, const int32_t* rows, const int32_t* key_lo, int dl, int dh, double theta,
+                    bool bf16, cudaStream_t st);
+void launch_rope_shift(void* k, const int32_t* tab, int n_entries, int max_rows, int dl, int dh, double theta,
+                       bool bf16, cudaStream_t st);
+
 // ------------------------------------------------------------ parity GEMM --
 // C = A[M x K] . B[K x N] with fp32 operands and fp64 accumulation in
 // ascending k (bit-exact with vec_mat, tensor.hpp:31-41).

@@ -700,4 +700,83 @@ void launch_logits(const float* row, const float* unembed, int d, int V, double*
     KEEP_LAUNCH_CHECK();
 }
 
+// ================================================================ RoPE hook ==
+// north_star subsystem (3): "the RoPE position re-shift of reused blocks".  The
+// reference architecture is NoPE (model.hpp:3-8), so this is an
+// opt-in hook (keep_set_rope), off -- the identity -- in every parity run.
+// Rotary pairs are (2j, 2j + 1) inside each head, angle = pos * theta^(-2j/dh),
+// computed in fp64.  Canonical KV is rotated at owner-local positions (a
+// segment_prefill starts at 0); a reused block is re-shifted by its layout
+// offset when it is copied into the merged KV.
+namespace {
+template <typename T> __device__ __forceinline__ float ldv(const T* p);
+template <> __device__ __forceinline__ float ldv<float>(const float* p) { return *p; }
+template <> __device__ __forceinline__ float ldv<__nv_bfloat16>(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void stv(float* p, double v) { *p = float(v); }
+__device__ __forceinline__ void stv(__nv_bfloat16* p, double v) { *p = __float2bfloat16_rn(float(v)); }
+
+template <typename T>
+__device__ __forceinline__ void rotate_pair(T* x, int j, int dh, double pos, double theta) {
+    const double ang = pos * pow(theta, -2.0 * j / dh);
+    double sn, cs;
+    sincos(ang, &sn, &cs);
+    const double a = ldv(x), b = ldv(x + 1);
+    stv(x, a * cs - b * sn);
+    stv(x + 1, a * sn + b * cs);
+}
+
+// q[i] (compact) and k[rows[i]] (merged) at position rows[i] - key_lo[rows[i]]
+template <typename T>
+__global__ void rope_qk_kernel(T* q, T* k, int n, const int32_t* rows, const int32_t* key_lo, int dl, int dh,
+                               double theta) {
+    const int pairs = dl / 2;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(n) * pairs;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e / pairs), pr = int(e % pairs);
+        const int col = 2 * pr, j = (col % dh) / 2;
+        const int r = rows[i];
+        const double pos = double(r - (key_lo ? key_lo[r] : 0));
+        rotate_pair(q + int64_t(i) * dl + col, j, dh, pos, theta);
+        rotate_pair(k + int64_t(r) * dl + col, j, dh, pos, theta);
+    }
+}
+
+// re-shift cached key rows: entry e = (first merged row, rows, delta)
+template <typename T>
+__global__ void rope_shift_kernel(T* k, const int32_t* tab, int n_entries, int dl, int dh, double theta) {
+    const int e = blockIdx.y;
+    if (e >= n_entries) return;
+    const int r0 = tab[3 * e], nr = tab[3 * e + 1], delta = tab[3 * e + 2];
+    const int pairs = dl / 2;
+    for (int64_t x = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; x < int64_t(nr) * pairs;
+         x += int64_t(gridDim.x) * blockDim.x) {
+        const int rr = int(x / pairs), col = 2 * int(x % pairs);
+        rotate_pair(k + int64_t(r0 + rr) * dl + col, (col % dh) / 2, dh, double(delta), theta);
+    }
+}
+}  // namespace
+
+void launch_rope_qk(void* q, void* k, int n, const int32_t* rows, const int32_t* key_lo, int dl, int dh, double theta,
+                    bool bf16, cudaStream_t st) {
+    if (n == 0) return;
+    const unsigned grid = unsigned(std::min<int64_t>(ceil_div(int64_t(n) * dl / 2, 256), kNumSMs * 8));
+    if (bf16)
+        rope_qk_kernel<<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(q), static_cast<__nv_bfloat16*>(k), n, rows,
+                                             key_lo, dl, dh, theta);
+    else
+        rope_qk_kernel<<<grid, 256, 0, st>>>(static_cast<float*>(q), static_cast<float*>(k), n, rows, key_lo, dl, dh,
+                                             theta);
+    KEEP_LAUNCH_CHECK();
+}
+
+void launch_rope_shift(void* k, const int32_t* tab, int n_entries, int max_rows, int dl, int dh, double theta,
+                       bool bf16, cudaStream_t st) {
+    if (n_entries == 0) return;
+    const dim3 grid(unsigned(std::max<int64_t>(1, std::min<int64_t>(ceil_div(int64_t(max_rows) * dl / 2, 256), 64))),
+                    unsigned(n_entries));
+    if (bf16) rope_shift_kernel<<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(k), tab, n_entries, dl, dh, theta);
+    else rope_shift_kernel<<<grid, 256, 0, st>>>(static_cast<float*>(k), tab, n_entries, dl, dh, theta);
+    KEEP_LAUNCH_CHECK();
+}
+
 }  // namespace keep_b200
