@@ -265,6 +265,23 @@ typedef struct {
 } keep_load_record;
 int keep_loader_trace(void* ctx, keep_load_record* out, int32_t cap, int32_t* n_out);
 
+/* The realised timeline of the last keep_plan_keep over pinned-host owners as
+ * the reference's Timeline (pipeline_sim.hpp:69-92), for validate_timeline
+ * (340-428: R one event per resource at a time, D1, D2, P, S): kind 0 load
+ * (one (layer, owner) item; a copy batch's interval is shared out to its items
+ * in byte order), 1 compute(layer) on the compute stream, 2 eval(layer) = the
+ * walk on the selector stream.  *attention_fraction = the smallest
+ * (attention + summary done - compute start) / compute span over the walked
+ * layers.  Times in ms from the prefill start. */
+typedef struct {
+    int32_t kind;
+    int32_t layer;
+    keep_owner owner; /* loads */
+    uint64_t bytes;   /* loads */
+    double start_ms, end_ms;
+} keep_timeline_event;
+int keep_timeline_trace(void* ctx, keep_timeline_event* out, int32_t cap, int32_t* n_out, double* attention_fraction);
+
 /* ---- per-phase device timing (CUDA events on the launching streams) ----- */
 enum {
     KEEP_PROF_QKV = 0,      /* gathered QKV GEMM + K/V scatter (K3)          */

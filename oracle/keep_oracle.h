@@ -96,6 +96,22 @@ typedef struct {
 KEEP_ORACLE_API(ko_)
 KEEP_ORACLE_API(kr_)
 
+/* The reference's validate_timeline (pipeline_sim.hpp:340-428) over a realised
+ * timeline; kr_ only (it is the reference's own checker).  kind: 0 load,
+ * 1 compute, 2 eval.  slow_bytes: [n_units x L] bytes of each unit's block in
+ * the slow tier (0 = fast-resident / absent). */
+typedef struct {
+    int32_t kind, layer;
+    int32_t owner_kind; /* 0 segment, 1 group */
+    uint32_t owner_id;
+    uint64_t bytes;
+    double start, end;
+} kr_timeline_event;
+int kr_validate_timeline(int L, int S, const uint8_t* plan, const int32_t* seg_len, int query_tokens, int n_units,
+                         const int32_t* unit_begin, const int32_t* unit_end, const int32_t* unit_is_group,
+                         const uint32_t* unit_owner_id, const uint64_t* slow_bytes, double attention_fraction,
+                         const kr_timeline_event* ev, int n_ev, char* codes_out, int cap);
+
 const char* ko_last_error(void);
 /* restatement-only extension: cap converge at max_hops hops (0 = the
  * reference's uncapped walk); see keep_oracle.c */

@@ -111,6 +111,11 @@ def available(prefix: str) -> bool:
     return os.path.exists(LIB_PATHS[prefix])
 
 
+class kr_timeline_event(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("layer", C.c_int32), ("owner_kind", C.c_int32), ("owner_id", C.c_uint32),
+                ("bytes", C.c_uint64), ("start", C.c_double), ("end", C.c_double)]
+
+
 class Oracle:
     def __init__(self, prefix: str = "ko"):
         path = LIB_PATHS[prefix]
@@ -147,6 +152,36 @@ class Oracle:
         if self.prefix != "ko":
             raise OracleError(1, "the hop cap exists only in the restatement (the reference has none)")
         self.lib.ko_set_max_hops(int(max_hops))
+
+    def validate_timeline(self, plan, seg_len, query_tokens, units, slow_bytes, attention_fraction, events):
+        """The reference's validate_timeline (pipeline_sim.hpp:340-428) over a
+        realised timeline (kr only).  units: [(begin, end, is_group, owner_id)];
+        slow_bytes: [n_units x L]; events: dicts {kind, layer, owner (kind, id),
+        bytes, start, end}.  Returns the violation codes (empty = valid)."""
+        if self.prefix != "kr":
+            raise OracleError(1, "validate_timeline is the reference's own checker (kr)")
+        plan = np.ascontiguousarray(plan, np.uint8)
+        L, S = plan.shape
+        sl = np.ascontiguousarray(seg_len, np.int32)
+        ub = np.array([u[0] for u in units], np.int32)
+        ue = np.array([u[1] for u in units], np.int32)
+        ug = np.array([int(u[2]) for u in units], np.int32)
+        uo = np.array([u[3] for u in units], np.uint32)
+        sb = np.ascontiguousarray(slow_bytes, np.uint64).reshape(len(units), L)
+        ev = (kr_timeline_event * max(len(events), 1))()
+        for i, e in enumerate(events):
+            ev[i] = kr_timeline_event(e["kind"], e["layer"], e.get("owner", (0, 0))[0], e.get("owner", (0, 0))[1],
+                                      e.get("bytes", 0), e["start"], e["end"])
+        buf = C.create_string_buffer(256)
+        f = self.lib.kr_validate_timeline
+        f.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(C.c_int32), C.c_int, C.c_int,
+                      C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_uint32),
+                      C.POINTER(C.c_uint64), C.c_double, C.POINTER(kr_timeline_event), C.c_int, C.c_char_p, C.c_int]
+        self._check(f(L, S, _ptr(plan, C.c_uint8), _ptr(sl, C.c_int32), int(query_tokens), len(units),
+                      _ptr(ub, C.c_int32), _ptr(ue, C.c_int32), _ptr(ug, C.c_int32), _ptr(uo, C.c_uint32),
+                      _ptr(sb, C.c_uint64), float(attention_fraction), ev, len(events), buf, 256))
+        txt = buf.value.decode()
+        return txt.split() if txt else []
 
     def _check(self, rc: int):
         if rc:

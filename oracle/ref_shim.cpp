@@ -420,4 +420,61 @@ int kr_logits(const keep_problem* p, const float* w, const float* row, double* o
     });
 }
 
+// validate_timeline (pipeline_sim.hpp:340-428) on a realised GPU timeline:
+// the workload is the reference's own derive_workload (103-154) over the plan
+// and the load units; the timeline's events are the device's.  codes_out gets
+// the violation codes (D1 D2 R P S), space separated ("" = valid).
+int kr_validate_timeline(int L, int S, const uint8_t* plan, const int32_t* seg_len, int query_tokens, int n_units,
+                         const int32_t* unit_begin, const int32_t* unit_end, const int32_t* unit_is_group,
+                         const uint32_t* unit_owner_id, const uint64_t* slow_bytes, double attention_fraction,
+                         const kr_timeline_event* ev, int n_ev, char* codes_out, int cap) {
+    return guard([&] {
+        RecomputePlan rp;
+        rp.layers.resize(L);
+        for (int l = 0; l < L; ++l)
+            for (int i = 0; i < S; ++i)
+                if (plan[size_t(l) * S + i]) rp.layers[l].insert(SegmentId(i));
+        std::vector<LayoutSegment> segs;
+        for (int i = 0; i < S; ++i) {
+            LayoutSegment sg;
+            sg.id = SegmentId(i);
+            sg.tokens.assign(size_t(seg_len[i]), 0);
+            segs.push_back(std::move(sg));
+        }
+        const Layout layout = Layout::of(std::move(segs));
+        std::vector<LoadUnit> units;
+        for (int u = 0; u < n_units; ++u) {
+            LoadUnit lu;
+            lu.owner = unit_is_group[u] ? OwnerRef::group(unit_owner_id[u]) : OwnerRef::segment(unit_owner_id[u]);
+            for (int i = unit_begin[u]; i < unit_end[u]; ++i) lu.segments.push_back(SegmentId(i));
+            lu.slow_bytes.assign(slow_bytes + size_t(u) * L, slow_bytes + size_t(u + 1) * L);
+            units.push_back(std::move(lu));
+        }
+        CostModel cost;
+        cost.attention_fraction = attention_fraction;
+        const Workload w = derive_workload(rp, layout, units, size_t(query_tokens), cost, 1.0, true);
+        Timeline tl;
+        for (int i = 0; i < n_ev; ++i) {
+            SimEvent e;
+            e.kind = ev[i].kind == 0 ? SimKind::Load : (ev[i].kind == 1 ? SimKind::Compute : SimKind::Eval);
+            e.resource = ev[i].kind == 0 ? SimResource::LoadEngine
+                                         : (ev[i].kind == 1 ? SimResource::ComputeEngine : SimResource::EvalEngine);
+            e.layer = ev[i].layer;
+            e.owner = ev[i].owner_kind ? OwnerRef::group(ev[i].owner_id) : OwnerRef::segment(ev[i].owner_id);
+            e.bytes = ev[i].bytes;
+            e.start = ev[i].start;
+            e.end = ev[i].end;
+            tl.events.push_back(e);
+            tl.makespan = std::max(tl.makespan, e.end);
+        }
+        const auto vio = validate_timeline(tl, rp, w);
+        std::string codes;
+        for (const auto& v : vio) codes += (codes.empty() ? "" : " ") + v.code;
+        if (cap > 0) {
+            std::strncpy(codes_out, codes.c_str(), size_t(cap - 1));
+            codes_out[cap - 1] = 0;
+        }
+    });
+}
+
 }  // extern "C"

@@ -91,6 +91,11 @@ PROFILE_PHASES = ["qkv", "attn", "wo", "mlp_in", "mlp_out", "summary", "select",
                   "embed", "logits", "loader", "comm", "xchg", "refresh", "attn_decode"]
 
 
+class keep_timeline_event(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("layer", C.c_int32), ("owner", keep_owner), ("bytes", C.c_uint64),
+                ("start_ms", C.c_double), ("end_ms", C.c_double)]
+
+
 class keep_plan_result(C.Structure):
     _fields_ = [("plan", C.POINTER(C.c_uint8)), ("orders", C.POINTER(C.c_int32)),
                 ("order_len", C.POINTER(C.c_int32)), ("hops", C.POINTER(C.c_int32)),
@@ -150,6 +155,7 @@ def load_library() -> C.CDLL:
         "keep_divergence": (C.c_int, [vp, fp, fp, dp, dp]),
         "keep_debug_gemm_bf16": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
         "keep_set_rope": (C.c_int, [vp, C.c_double]),
+        "keep_timeline_trace": (C.c_int, [vp, C.POINTER(keep_timeline_event), i32, i32p, dp]),
         "keep_debug_gemm_parity": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
         "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
         "keep_loader_trace": (C.c_int, [vp, C.POINTER(keep_load_record), i32, i32p]),
@@ -420,6 +426,17 @@ class Context:
         return [{"layer": r.layer, "kind": LOAD_KINDS[r.kind], "at_layer": r.at_layer,
                  "owner": (r.owner.kind, r.owner.id), "bytes": int(r.bytes), "start_ms": r.batch_start_ms,
                  "end_ms": r.batch_end_ms, "compute_start_ms": r.compute_start_ms} for r in buf[: n.value]]
+
+    def timeline_trace(self):
+        """keep_timeline_trace: the realised timeline of the last plan_keep over
+        pinned-host memory as reference Timeline events + the D2 attention fraction."""
+        n, frac = C.c_int32(), C.c_double()
+        _check(self.lib.keep_timeline_trace(self._h, None, 0, C.byref(n), C.byref(frac)))
+        buf = (keep_timeline_event * max(n.value, 1))()
+        _check(self.lib.keep_timeline_trace(self._h, buf, n.value, C.byref(n), C.byref(frac)))
+        evs = [{"kind": e.kind, "layer": e.layer, "owner": (e.owner.kind, e.owner.id), "bytes": int(e.bytes),
+                "start": e.start_ms, "end": e.end_ms} for e in buf[: n.value]]
+        return evs, frac.value
 
     def has_current(self, kind, oid, version) -> bool:
         out = C.c_int32()

@@ -2332,12 +2332,19 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
                 upload_bytes(c.sel_cand.p, active.data(), S, c.s_sel);
                 KEEP_CUDA(cudaEventRecord(ev_sum, st));
                 KEEP_CUDA(cudaStreamWaitEvent(c.s_sel, ev_sum, 0));
+                const bool trace = c.loader.on;  // the realised timeline (keep_timeline_trace)
+                if (trace) {
+                    c.loader.has_eval[l] = 1;
+                    KEEP_CUDA(cudaEventRecord(c.loader.attn_end[l], st));
+                    KEEP_CUDA(cudaEventRecord(c.loader.eval_a[l], c.s_sel));
+                }
                 int32_t* o = c.sel_order.as<int32_t>();
                 {
                     ProfScope ps(c.prof, KEEP_PROF_SELECT, c.s_sel, 0.0, 8.0 * double(S) * S);
                     launch_select(S, p.summ.as<double>(), p.summ.as<double>() + S, budget, c.sel_cand.as<uint8_t>(), o + 2,
                                   o, o + 1, c.s_sel, c.cfg.max_hops);
                 }
+                if (trace) KEEP_CUDA(cudaEventRecord(c.loader.eval_b[l], c.s_sel));
                 KEEP_CUDA(cudaMemcpyAsync(hbuf, o, sizeof(int32_t) * (S + 2), cudaMemcpyDeviceToHost, c.s_sel));
                 KEEP_CUDA(cudaEventRecord(ev_sel, c.s_sel));
             };

@@ -250,6 +250,10 @@ struct Loader {
     std::vector<Batch> batches;
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> comp_start;  // per layer, on the compute stream after the load wait
+    // the realised timeline beside the loads (keep_timeline_trace): compute(l)
+    // end, attention + summary done, and the walk (eval) on the selector stream
+    std::vector<cudaEvent_t> comp_end, attn_end, eval_a, eval_b;
+    std::vector<uint8_t> has_eval;
     std::vector<cudaEvent_t> pool;
     cudaEvent_t t0 = nullptr;
     double bw_gbs = 50.0;             // H2D estimate (updated from finished batches)

@@ -183,8 +183,9 @@ Loader::~Loader() {
         if (b.a) cudaEventDestroy(b.a);
         if (b.b) cudaEventDestroy(b.b);
     }
-    for (auto e : comp_start)
-        if (e) cudaEventDestroy(e);
+    for (auto* v : {&comp_start, &comp_end, &attn_end, &eval_a, &eval_b})
+        for (auto e : *v)
+            if (e) cudaEventDestroy(e);
     for (auto e : pool) cudaEventDestroy(e);
     if (t0) cudaEventDestroy(t0);
 }
@@ -240,11 +241,14 @@ void loader_begin(Context& c, Pass& p) {
     ld.out_from.assign(ld.units.size(), INT32_MAX);
     ld.last_batch.assign(c.L, -1);
     if (ld.comp_start.size() != size_t(c.L)) {
-        for (auto e : ld.comp_start)
-            if (e) cudaEventDestroy(e);
-        ld.comp_start.assign(c.L, nullptr);
-        for (auto& e : ld.comp_start) KEEP_CUDA(cudaEventCreate(&e));
+        for (auto* v : {&ld.comp_start, &ld.comp_end, &ld.attn_end, &ld.eval_a, &ld.eval_b}) {
+            for (auto e : *v)
+                if (e) cudaEventDestroy(e);
+            v->assign(c.L, nullptr);
+            for (auto& e : *v) KEEP_CUDA(cudaEventCreate(&e));
+        }
     }
+    ld.has_eval.assign(c.L, 0);
     if (!ld.t0) KEEP_CUDA(cudaEventCreate(&ld.t0));
     KEEP_CUDA(cudaEventRecord(ld.t0, c.s_main));
     // the copy stream starts after the prefill begins (timeline origin)
@@ -269,7 +273,9 @@ void loader_before_layer(Context& c, Pass& p, int l, const uint8_t* active) {
 
 void loader_after_layer(Context& c, Pass& p, int l, const uint8_t* active, double est_ms) {
     Loader& ld = c.loader;
-    if (!ld.on || l + 1 >= c.L) return;
+    if (!ld.on) return;
+    KEEP_CUDA(cudaEventRecord(ld.comp_end[l], c.s_main));
+    if (l + 1 >= c.L) return;
     const size_t U = ld.units.size();
     update_bw(ld);
     std::vector<std::pair<int, int>> items;
@@ -287,6 +293,12 @@ void loader_after_layer(Context& c, Pass& p, int l, const uint8_t* active, doubl
             ahead_bytes += 2ull * u.tokens * c.dl * c.elem;
         }
     }
+    // everything issued here starts with compute(l) at the earliest (the
+    // reference's "loads for l+1 start with compute(l)", pipeline_sim.hpp:
+    // 261-338): the host runs layers ahead of the device, and an early
+    // pre-load would overlap a compute(k < l) whose plan still holds a member
+    // (rule S)
+    KEEP_CUDA(cudaStreamWaitEvent(c.s_copy, ld.comp_start[l], 0));
     // pre-loads into the idle window of compute(l)
     const double window = est_ms * 1e-3 * (ld.any_host ? ld.bw_gbs : ld.bw_d2d_gbs) * 1e9;
     double budget = window - double(ahead_bytes);
@@ -333,6 +345,79 @@ extern "C" int keep_loader_trace(void* ctx, keep_load_record* out, int32_t cap, 
             o.compute_start_ms = ms;
         }
         *n_out = int32_t(ld.recs.size());
+        return KEEP_OK;
+    } catch (const KeepError& e) {
+        set_last_error(e.what());
+        return e.code;
+    }
+}
+
+// The realised timeline of the last prefill over pinned-host owners, in the
+// reference's Timeline vocabulary (pipeline_sim.hpp:69-92): loads (each copy
+// batch's interval shared out to its items in byte proportion -- one copy
+// engine moves them in order), compute(l) on the compute stream, and the walk
+// (eval) of layer l on the selector stream.  attention_fraction out = the
+// smallest (summary done - compute start) / compute span over the walked
+// layers (bounded by the walk's own start), the D2 parameter of validate_timeline.
+extern "C" int keep_timeline_trace(void* ctx, keep_timeline_event* out, int32_t cap, int32_t* n_out,
+                                   double* attention_fraction) {
+    using namespace keep_b200;
+    try {
+        Context& c = *static_cast<Context*>(ctx);
+        KEEP_CUDA(cudaSetDevice(c.cfg.device));
+        Loader& ld = c.loader;
+        KEEP_CUDA(cudaStreamSynchronize(c.s_copy));
+        KEEP_CUDA(cudaStreamSynchronize(c.s_sel));
+        KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+        if (!ld.on) raise(KEEP_ERR_TRACE, "no loader trace: the last prefill had no pinned-host memory");
+        auto at = [&](cudaEvent_t e) {
+            float ms = 0.f;
+            KEEP_CUDA(cudaEventElapsedTime(&ms, ld.t0, e));
+            return double(ms);
+        };
+        std::vector<keep_timeline_event> ev;
+        // loads: items of a batch in issue order, sub-intervals by bytes
+        std::vector<uint64_t> done(ld.batches.size(), 0);
+        for (const auto& r : ld.recs) {
+            const Loader::Batch& b = ld.batches[r.batch];
+            const double a = at(b.a), e = at(b.b);
+            const double span = std::max(0.0, e - a);
+            const double s0 = a + span * double(done[r.batch]) / double(std::max<uint64_t>(b.bytes, 1));
+            done[r.batch] += r.bytes;
+            const double s1 = a + span * double(done[r.batch]) / double(std::max<uint64_t>(b.bytes, 1));
+            keep_timeline_event x{};
+            x.kind = 0;
+            x.layer = r.layer;
+            x.owner = keep_owner{ld.units[r.unit].key.kind, ld.units[r.unit].key.id};
+            x.bytes = r.bytes;
+            x.start_ms = s0;
+            x.end_ms = s1;
+            ev.push_back(x);
+        }
+        double frac = 1.0;
+        for (int l = 0; l < c.L; ++l) {
+            keep_timeline_event x{};
+            x.kind = 1;
+            x.layer = l;
+            x.start_ms = at(ld.comp_start[l]);
+            x.end_ms = at(ld.comp_end[l]);
+            ev.push_back(x);
+            if (ld.has_eval[l]) {
+                keep_timeline_event y{};
+                y.kind = 2;
+                y.layer = l;
+                y.start_ms = at(ld.eval_a[l]);
+                y.end_ms = at(ld.eval_b[l]);
+                ev.push_back(y);
+                const double span = x.end_ms - x.start_ms;
+                // the walk starts once the summary exists (it waits on that
+                // event): the earlier of the two timestamps bounds "attention done"
+                if (span > 0.0) frac = std::min(frac, (std::min(at(ld.attn_end[l]), y.start_ms) - x.start_ms) / span);
+            }
+        }
+        for (int i = 0; i < int(ev.size()) && i < cap; ++i) out[i] = ev[i];
+        *n_out = int32_t(ev.size());
+        if (attention_fraction) *attention_fraction = std::max(0.0, frac);
         return KEEP_OK;
     } catch (const KeepError& e) {
         set_last_error(e.what());

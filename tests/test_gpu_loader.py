@@ -124,3 +124,43 @@ def test_inplace_refresh(ko, golden):
             assert np.array_equal(k, before[u][0]) and np.array_equal(v, before[u][1])
         got = ctx.plan_keep(lay, p.query, sched)
     assert np.array_equal(got["plan"], ref["plan"]) and got["orders"] == ref["orders"]
+
+
+def validate_real_timeline(kr, ctx, lay, plan, qlen, block_bytes):
+    """The reference's own validate_timeline over the device's timeline."""
+    evs, frac = ctx.timeline_trace()
+    L = plan.shape[0]
+    units = [(b, e, int(k == kb.GROUP), o) for k, o, b, e in lay.owners()]
+    slow = np.array([[block_bytes(b, e)] * L for b, e, _, _ in units], np.uint64)
+    return kr.validate_timeline(plan, lay.seg_len, qlen, units, slow, frac, evs), evs, frac, units, slow
+
+
+@pytest.mark.parametrize("numerics", [kb.PARITY, kb.FAST])
+def test_reference_validate_timeline_on_device_trace(kr, numerics):
+    """pipeline_sim.hpp:340-428 (R, D1, D2, P, S) run by the unmodified
+    reference on the realised copy / compute / selector-stream timeline."""
+    seed, S, L, H, d, mlp, V = 71, 60, 6, 2, 256, 512, 512
+    from paper_2602_23592_b200.synth import group_units, make_instance_layout
+    inst = make_instance_layout(seed, S, V)
+    lay = kb.Layout(inst.seg_len, inst.tokens, group_units(S, 4, 0.5))
+    sched = kb.ratio_schedule(L, 0.3)
+    elem = 2 if numerics == kb.FAST else 4
+    with kb.Context(L, H, d, mlp, V, seed, numerics) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay, version=1, tier=kb.TIER_HOST)
+        res = ctx.plan_keep(lay, inst.query, sched)
+        bb = lambda b, e: 2 * int(np.sum(lay.seg_len[b:e])) * d * elem  # noqa: E731
+        codes, evs, frac, units, slow = validate_real_timeline(kr, ctx, lay, res["plan"], len(inst.query), bb)
+    assert codes == [], codes
+    kinds = {e["kind"] for e in evs}
+    assert kinds == {0, 1, 2} and 0.0 < frac <= 1.0
+    # fault injection (test_pipeline.cpp:276-335): the same checker flags broken timelines
+    comp = {e["layer"]: e for e in evs if e["kind"] == 1}
+    load = next(e for e in evs if e["kind"] == 0 and e["layer"] > 0)
+    late = [dict(e) for e in evs]
+    for e in late:
+        if e is not None and e["kind"] == 0 and e["layer"] == load["layer"] and e["owner"] == load["owner"]:
+            e["end"] = comp[load["layer"]]["start"] + 1.0
+    assert "D1" in kr.validate_timeline(res["plan"], lay.seg_len, len(inst.query), units, slow, frac, late)
+    dup = evs + [dict(load)]
+    assert "P" in kr.validate_timeline(res["plan"], lay.seg_len, len(inst.query), units, slow, frac, dup)
