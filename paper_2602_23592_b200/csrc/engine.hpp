@@ -144,12 +144,13 @@ struct DevBuf {
 
 // PARITY projection GEMMs (gemm_oz.cu): the Ozaki int8 tensor-core GEMM from
 // kOzMinRows rows, DFMA (gemm_f64acc.cu) below.  OzWork = its grow-only
-// scratch (digit planes of A and B, scale exponents, fp64 Horner partials).
+// scratch (residue planes of A and B, scale exponents, Garner digits).
 struct OzWork {
     DevBuf a, b, ea, eb, part;
 };
 constexpr int kOzMinRows = 64;
-int oz_slices();  // KEEP_OZ_SLICES (default 7)
+int oz_moduli();       // KEEP_OZ_MODULI (default 14)
+int oz_bits(int K);    // integer bits per operand at contraction length K
 bool ozaki_eligible(int M, int N, int K);
 void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
                        const EpiArgs& epi, cudaStream_t st, OzWork& w, int max_ctas = kNumSMs);

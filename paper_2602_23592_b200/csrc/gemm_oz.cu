@@ -1,4 +1,5 @@
-// gemm_oz.cu -- PARITY projection GEMM on the int8 tensor cores (Ozaki scheme).
+// gemm_oz.cu -- PARITY projection GEMM on the int8 tensor cores (Ozaki scheme
+// II: integer residues and the Chinese remainder theorem).
 //
 //   C[M x N] = A[M x K] . B[K x N]     fp32 operands, fp64-grade accumulation
 //
@@ -8,28 +9,32 @@
 // 5th-generation tensor cores in exact integer arithmetic:
 //
 //  * every row of A is scaled by a power of two 2^ea[m] so its largest
-//    element lies in [32, 64), and split into s signed 8-bit digits
-//        x * 2^ea = d0 + d1 / 256 + ... + d_{s-1} / 256^(s-1) + r,
-//    d0 in [-65, 65], d_p in [-128, 127] (split_digits), |r| <= 2^-(8s-7);
-//    every column of B likewise with 2^eb[n] (oz_split_rows / oz_split_cols);
-//  * x.w = sum_{p,q} d_p e_q 256^-(p+q).  Level k collects the digit pairs
-//    with p + q = k (k < s, the standard triangular truncation); one level
-//    is an int8 GEMM with K' = (k+1) K accumulated EXACTLY in int32 TMEM
-//    (tcgen05.mma kind::i8; |d_p e_q| <= 2^14, so (k+1) K <= 2^17 keeps the
-//    sum below 2^31 -- longer levels are split into several units);
-//  * the levels are combined in fp64 in Horner order from the smallest
-//    (P = D_{s-1}; P = D_k + P / 256; ...), then scaled by 2^-(ea+eb) and
-//    rounded once to fp32 -- the reference's "fp64 accumulate, cast" with an
-//    error of ~2^-(8s-10) of max|x| max|w| per product instead of 2^-53.
+//    element lies in [2^(b-1), 2^b), and rounded to an integer A' (exact for
+//    every element within b - 24 binades of the row maximum, else an error of
+//    at most 2^-b of it); every column of B likewise (2^eb[n], B');
+//  * the integer product X = A'.B' (|X| <= K 2^2b) is computed modulo n
+//    pairwise-coprime moduli m_i <= 256 (kModuli): one int8 GEMM per modulus
+//    on the symmetric residues of A' and B' (|r| <= 128), accumulated EXACTLY
+//    in int32 TMEM (tcgen05.mma kind::i8; K 2^14 < 2^31);
+//  * X is rebuilt from its residues by Garner's algorithm -- mixed-radix
+//    digits v_i in small exact fp32 arithmetic, computed tile by tile as the
+//    residues arrive (v_i needs v_0..v_{i-1}, kept as int8 in a per-CTA
+//    scratch) -- and Horner in fp64 from the top digit
+//    (X = v_0 + m_0 (v_1 + m_1 (...))), then scaled by 2^-(ea+eb) and rounded
+//    once to fp32: the reference's "fp64 accumulate, cast".
 //
-// That is the same grade as the fp64 re-ordering the PARITY attention already
-// has (any fp64 order reproduced every plan); the int8
-// tensor cores do it at ~4.5 POPS against ~40 TFLOP/s of DFMA.
+// b is the largest integer with K 2^2b < M/4 (M = prod m_i), so the symmetric
+// CRT range holds X with margin: with the default 14 moduli (110 bits) b = 47
+// at K <= 16384, an input error of 2^-47 of the row/column maximum per
+// operand -- the grade of the reference's own fp64 accumulation over
+// K ~ 10^4 terms (any fp64 order reproduced every plan).
+// The previous form of this kernel (Ozaki scheme I: 7 int8 digits per
+// operand, 28 digit-pair GEMMs) had the same grade at twice the tensor work.
 //
 // Kernel structure = gemm_tc.cu's (persistent, warp-specialised, TMA ring,
 // double-buffered TMEM accumulators, 128 x 256 tiles), with a work unit =
-// (tile, level unit) and an epilogue that keeps the fp64 Horner partial of
-// its tile in a per-CTA scratch (L2-resident: 256 KB x 148 CTAs).
+// (tile, modulus) and eight epilogue warps doing the Garner steps.
+#include <cmath>
 #include <cstring>
 
 #include "engine.hpp"
@@ -43,11 +48,25 @@ using namespace tc;
 
 constexpr int OBM = 128, OBN = 256, OBK = 128;  // OBK bytes = int8 elements per stage
 constexpr int OSTAGES = 4;
-constexpr int OTHREADS = 256;
+constexpr int OEPI = 8;                         // epilogue warps (2 per TMEM lane quarter)
+constexpr int OTHREADS = (4 + OEPI) * 32;
 constexpr int OGM = 16;
-constexpr int kMaxUnits = 32;
+constexpr int kMaxModuli = 16;
 constexpr uint32_t OA_BYTES = OBM * OBK, OB_BYTES = OBN * OBK, OSTAGE = OA_BYTES + OB_BYTES;
 constexpr size_t OSMEM = size_t(OSTAGES) * OSTAGE + 1024 + 256;
+// pairwise coprime, descending from 256 (greedy)
+constexpr int kModuliAll[kMaxModuli] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193};
+
+// the modulus tables (kernel parameter: constant bank)
+struct OzCrt {
+    int n;                      // moduli used
+    int mi[kMaxModuli];         // m_i
+    float mf[kMaxModuli];       // m_i
+    float rcp[kMaxModuli];      // 1 / m_i (fp32)
+    double md[kMaxModuli];      // m_i
+    double rcpd[kMaxModuli];    // 1 / m_i (fp64)
+    float inv[kMaxModuli][kMaxModuli];  // inv[j][i] = m_j^-1 mod m_i (j < i)
+};
 
 // kind::i8 instruction descriptor: D s32, A / B signed 8-bit, both K-major.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
@@ -63,16 +82,6 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
         : "memory");
 }
 
-// A unit: digit pairs (p, k - p) for p in [pb, pe) of level k, one int32
-// accumulation.  op: 0 P = D; 1 P = D + P/256 (next level); 2 P = P + D (same level).
-struct OzUnit {
-    int8_t k, pb, pe, op;
-};
-struct OzPlan {
-    int nunits;
-    OzUnit u[kMaxUnits];
-};
-
 __device__ __forceinline__ void otile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
     const int band = t / (OGM * tiles_n);
     const int m0 = band * OGM;
@@ -82,7 +91,7 @@ __device__ __forceinline__ void otile_coords(int t, int tiles_m, int tiles_n, in
     nb = r / gm;
 }
 
-__device__ __forceinline__ void epi_store32(const EpiArgs& e, int m, int n, int N, const float (&v)[32]) {
+__device__ __forceinline__ void epi_store32(const EpiArgs& e, int m, int n, const float (&v)[32]) {
     switch (e.kind) {
         case EPI_QKV: {
             const int d = e.d;
@@ -123,13 +132,30 @@ __device__ __forceinline__ void epi_store32(const EpiArgs& e, int m, int n, int 
             for (int q = 0; q < 8; ++q) o[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
     }
-    (void)N;
 }
 
+// Small exact integer arithmetic in fp32 without the conversion pipe:
+// rounding to an integer by the 1.5 * 2^23 magic constant (round to nearest
+// even, exact for |x| < 2^22), digits stored biased by 128 and widened with a
+// byte permute into the mantissa of 2^23.
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+constexpr float kByteBias = 8388736.0f;  // 2^23 + 128
+
+// x - m rint(x / m) for an exactly representable fp32 integer x (|x| < 2^22):
+// the symmetric residue (canonical for odd m; +-m/2 both possible for even m)
+__device__ __forceinline__ float redm(float x, float m, float rc) {
+    const float q = fmaf(x, rc, kMagic) - kMagic;
+    return fmaf(-q, m, x);
+}
+
+// byte b of w (a digit v + 128) -> 2^23 + 128 + v as fp32
+__device__ __forceinline__ float byte_biased(uint32_t w, int b) {
+    return __uint_as_float(__byte_perm(w, 0x4B000000u, uint32_t(b) | 0x7650u));
+}
 __global__ void __launch_bounds__(OTHREADS, 1)
 gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-               int Mp, int Np, const __grid_constant__ OzPlan plan, const int* __restrict__ ea,
-               const int* __restrict__ eb, double* __restrict__ scratch, EpiArgs epi) {
+               int Mp, int Np, const __grid_constant__ OzCrt crt, const int* __restrict__ ea,
+               const int* __restrict__ eb, uint32_t* __restrict__ scratch, EpiArgs epi) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + OSTAGES * OSTAGE);
@@ -142,7 +168,7 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int tiles_m = int(ceil_div(M, OBM)), tiles_n = int(ceil_div(N, OBN));
     const int ntiles = tiles_m * tiles_n;
     const int kblocks = int(ceil_div(K, OBK));
-    const int U = plan.nunits;
+    const int U = crt.n;
 
     if (warp == 0 && lane == 0) {
         prefetch_map(&tmA);
@@ -153,7 +179,7 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], OEPI);
         }
         fence_barrier_init();
     }
@@ -164,73 +190,66 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
+        if (lane == 0) {  // ---------------- TMA producer: residue planes u of A and B
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 int mb, nb;
                 otile_coords(t, tiles_m, tiles_n, mb, nb);
                 for (int u = 0; u < U; ++u) {
-                    const OzUnit un = plan.u[u];
-                    for (int p = un.pb; p < un.pe; ++p) {
-                        const int q = un.k - p;
-                        for (int kb = 0; kb < kblocks; ++kb) {
-                            mbar_wait(&empty[stage], phase ^ 1);
-                            uint8_t* sa = smem + stage * OSTAGE;
-                            mbar_expect_tx(&full[stage], OSTAGE);
-                            tma_load_2d(sa, &tmA, &full[stage], kb * OBK, p * Mp + mb * OBM);
-                            tma_load_2d(sa + OA_BYTES, &tmB, &full[stage], kb * OBK, q * Np + nb * OBN);
-                            if (++stage == OSTAGES) {
-                                stage = 0;
-                                phase ^= 1;
-                            }
-                        }
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {  // ---------------- MMA issuer
-        constexpr uint32_t idesc = idesc_i8(OBM, OBN);
-        int stage = 0;
-        uint32_t phase = 0;
-        int it = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            for (int u = 0; u < U; ++u, ++it) {
-                const OzUnit un = plan.u[u];
-                const int acc = it & 1;
-                mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
-                fence_after();
-                const uint32_t tmem_d = tmem_base + uint32_t(acc * OBN);
-                bool first = true;
-                for (int p = un.pb; p < un.pe; ++p) {
                     for (int kb = 0; kb < kblocks; ++kb) {
-                        mbar_wait(&full[stage], phase);
-                        fence_after();
-                        const uint32_t sa = smem_u32(smem + stage * OSTAGE);
-                        const uint64_t ad = smem_desc(sa), bd = smem_desc(sa + OA_BYTES);
-                        if (elect_one()) {
-#pragma unroll
-                            for (int k = 0; k < OBK / 32; ++k)  // 32 int8 = 32 bytes per MMA
-                                umma_i8(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
-                                        (first && k == 0) ? 0u : 1u);
-                            umma_commit(&empty[stage]);
-                        }
-                        __syncwarp();
-                        first = false;
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* sa = smem + stage * OSTAGE;
+                        mbar_expect_tx(&full[stage], OSTAGE);
+                        tma_load_2d(sa, &tmA, &full[stage], kb * OBK, u * Mp + mb * OBM);
+                        tma_load_2d(sa + OA_BYTES, &tmB, &full[stage], kb * OBK, u * Np + nb * OBN);
                         if (++stage == OSTAGES) {
                             stage = 0;
                             phase ^= 1;
                         }
                     }
                 }
+            }
+        }
+    } else if (warp == 1) {  // ---------------- MMA issuer: one exact int32 GEMM per modulus
+        constexpr uint32_t idesc = idesc_i8(OBM, OBN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int u = 0; u < U; ++u, ++it) {
+                const int acc = it & 1;
+                mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+                fence_after();
+                const uint32_t tmem_d = tmem_base + uint32_t(acc * OBN);
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * OSTAGE);
+                    const uint64_t ad = smem_desc(sa), bd = smem_desc(sa + OA_BYTES);
+                    if (elect_one()) {
+#pragma unroll
+                        for (int k = 0; k < OBK / 32; ++k)  // 32 int8 = 32 bytes per MMA
+                            umma_i8(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
+                                    (kb == 0 && k == 0) ? 0u : 1u);
+                        umma_commit(&empty[stage]);
+                    }
+                    __syncwarp();
+                    if (++stage == OSTAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
                 if (elect_one()) umma_commit(&tfull[acc]);
                 __syncwarp();
             }
         }
-    } else if (warp >= 4) {  // ---------------- epilogue: fp64 Horner over the levels
-        const int q4 = warp & 3;
-        const int r = q4 * 32 + lane;  // tile row = TMEM lane
-        double* P = scratch + size_t(blockIdx.x) * OBM * OBN;  // [col][row]
+    } else if (warp >= 4) {  // ---------------- epilogue: Garner digits, fp64 Horner on the last modulus
+        const int q4 = warp & 3;                 // TMEM lane quarter
+        const int ch0 = ((warp - 4) >> 2) * (OBN / 32 / 2);  // this warp's four 32-column chunks
+        const int r = q4 * 32 + lane;            // tile row = TMEM lane
+        // digits v_j of this CTA's tile: [j][OBN / 4 column quads][OBM rows] x char4
+        uint32_t* vs = scratch + size_t(blockIdx.x) * kMaxModuli * (OBN / 4) * OBM + r;
         int it = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             int mb, nb;
@@ -239,42 +258,103 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             const bool mok = m < M;
             const int eam = mok ? ea[m] : 0;
             for (int u = 0; u < U; ++u, ++it) {
-                const int op = plan.u[u].op;
                 const bool last = u == U - 1;
                 const int acc = it & 1;
+                const float mf = crt.mf[u], rc = crt.rcp[u];
+                const int mi = crt.mi[u];
                 mbar_wait(&tfull[acc], (it >> 1) & 1);
                 fence_after();
 #pragma unroll 1
-                for (int ch = 0; ch < OBN / 32; ++ch) {
+                for (int ch = ch0; ch < ch0 + OBN / 32 / 2; ++ch) {
                     uint32_t d[32];
                     tmem_ld32(tmem_base + (uint32_t(q4 * 32) << 16) + uint32_t(acc * OBN + ch * 32), d);
                     const int n0 = nb * OBN + ch * 32;
                     if (n0 >= N) continue;
-                    double* pc = P + size_t(ch * 32) * OBM + r;
+                    float tv[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        // |acc| <= K 2^14 < 2^28: the fp32 quotient is within one of exact
+                        const int a = int(d[j]);
+                        const int q = __float_as_int(fmaf(float(a), rc, kMagic)) - __float_as_int(kMagic);
+                        const int rr = a - q * mi;  // |rr| < 2m
+                        tv[j] = redm(__int_as_float(0x4B400000 + rr) - kMagic, mf, rc);
+                    }
+                    if (u == 0) {  // m_0 = 256 is even: +128 -> -128
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) tv[j] = tv[j] >= 0.5f * mf ? tv[j] - mf : tv[j];
+                    }
+                    uint32_t* vq = vs + size_t(ch * 8) * OBM;
+                    // Garner: t = (((r_u - v_0) c_0u - v_1) c_1u - ...) mod m_u; odd m_u,
+                    // so every step leaves the canonical symmetric residue.  The
+                    // digit words stream from the (L2-resident) scratch two steps
+                    // ahead of their use.
+                    auto ld8 = [&](uint32_t(&w)[8], int jm) {
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) w[g] = vq[(size_t(jm) * (OBN / 4) + g) * OBM];
+                    };
+                    auto gstep = [&](const uint32_t(&w)[8], int jm) {
+                        const float c = crt.inv[jm][u];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            tv[j] = redm(((tv[j] + kByteBias) - byte_biased(w[j >> 2], j & 3)) * c, mf, rc);
+                    };
+                    uint32_t w0[8], w1[8], w2[8];
+                    if (u > 0) ld8(w0, 0);
+                    if (u > 1) ld8(w1, 1);
+#pragma unroll 1
+                    for (int jm = 0; jm < u; jm += 3) {
+                        if (jm + 2 < u) ld8(w2, jm + 2);
+                        gstep(w0, jm);
+                        if (jm + 1 >= u) break;
+                        if (jm + 3 < u) ld8(w0, jm + 3);
+                        gstep(w1, jm + 1);
+                        if (jm + 2 >= u) break;
+                        if (jm + 4 < u) ld8(w1, jm + 4);
+                        gstep(w2, jm + 2);
+                    }
                     if (!last) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const double dv = double(int(d[j]));
-                            double pv;
-                            if (op == 0) pv = dv;
-                            else if (op == 1) pv = fma(pc[j * OBM], 0.00390625, dv);
-                            else pv = pc[j * OBM] + dv;
-                            pc[j * OBM] = pv;
+                        for (int g = 0; g < 8; ++g) {
+                            uint32_t b[4];
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) b[k] = uint32_t(__float_as_int(tv[4 * g + k] + kByteBias)) & 0xffu;
+                            vq[(size_t(u) * (OBN / 4) + g) * OBM] = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
                         }
                     } else if (mok) {
+                        // X = v_0 + m_0 (v_1 + m_1 (... + m_{U-2} v_{U-1})), exact while |partial| < 2^53
+                        double P[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) P[j] = double(tv[j]);
+                        auto hstep = [&](const uint32_t(&w)[8], int jm) {
+                            const double mdj = crt.md[jm];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                P[j] = fma(P[j], mdj,
+                                           __hiloint2double(0x43300000, __byte_perm(w[j >> 2], 0u, uint32_t(j & 3) | 0x4440u)) -
+                                               4503599627370624.0);  // (2^52 + 128 + v) - (2^52 + 128)
+                        };
+                        // digits u-1 .. 0, two ahead
+                        if (u > 0) ld8(w0, u - 1);
+                        if (u > 1) ld8(w1, u - 2);
+#pragma unroll 1
+                        for (int k = 0; k < u; k += 3) {
+                            if (k + 2 < u) ld8(w2, u - 3 - k);
+                            hstep(w0, u - 1 - k);
+                            if (k + 1 >= u) break;
+                            if (k + 3 < u) ld8(w0, u - 4 - k);
+                            hstep(w1, u - 2 - k);
+                            if (k + 2 >= u) break;
+                            if (k + 4 < u) ld8(w1, u - 5 - k);
+                            hstep(w2, u - 3 - k);
+                        }
                         float v[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            const double dv = double(int(d[j]));
-                            double pv;
-                            if (op == 0) pv = dv;
-                            else if (op == 1) pv = fma(pc[j * OBM], 0.00390625, dv);
-                            else pv = pc[j * OBM] + dv;
                             const int n = n0 + j;
-                            const int e = eam + (n < N ? eb[n] : 0);
-                            v[j] = float(ldexp(pv, -e));
+                            const int e = eam + (n < N ? eb[n] : 0);  // |e| < 1000: 2^-e is a normal double
+                            v[j] = float(P[j] * __longlong_as_double(int64_t(1023 - e) << 52));
                         }
-                        epi_store32(epi, m, n0, N, v);
+                        epi_store32(epi, m, n0, v);
                     }
                 }
                 fence_before();
@@ -292,41 +372,32 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------- splits --
-// x * 2^e with max |x| * 2^e in [32, 64): e = 6 - exponent(max) (frexp).
-__device__ __forceinline__ int scale_exp(float amax) {
+// x 2^e with max |x| 2^e in [2^(b-1), 2^b): e = b - exponent(max) (frexp).
+__device__ __forceinline__ int scale_exp(float amax, int bits) {
     if (!(amax > 0.f)) return 0;
     int ex;
     frexpf(amax, &ex);
-    return 6 - ex;
+    return bits - ex;
 }
 
-// s base-256 digits of v = x 2^e (|v| < 64), most significant first:
-//   d_p = floor(v_p + 1/2),  v_{p+1} = 256 (v_p - d_p)     (exact in fp64)
-// leaves d_p in [-128, 128]; a digit of 128 becomes -128 with a carry of one
-// into the digit above (128 / 256^p = 1 / 256^(p-1) - 128 / 256^p), so every
-// digit fits int8: d_0 in [-65, 65], d_p in [-128, 127].
-__device__ __forceinline__ void split_digits(double v, int s, int (&dd)[8]) {
-#pragma unroll
-    for (int p = 0; p < 8; ++p) {
-        if (p < s) {
-            const double f = floor(v + 0.5);
-            dd[p] = int(f);
-            v = (v - f) * 256.0;
-        } else {
-            dd[p] = 0;
-        }
-    }
-#pragma unroll
-    for (int p = 7; p >= 1; --p)
-        if (dd[p] == 128) {
-            dd[p] = -128;
-            dd[p - 1] += 1;
-        }
+// symmetric residue of the integer-valued fp64 X (|X| <= 2^52) modulo m_i, in
+// fp64 without the conversion pipe: rint(X / m) by the 1.5 * 2^52 magic
+// constant (|X / m| < 2^51; X * (1/m) is within 2^-13 of X / m, which is at
+// least 1/(2m) from a half-integer for odd m, so the residue is canonical; m_0 =
+// 256 is exact and maps +128 to -128), the int8 read from the low word of
+// r + 1.5 * 2^52
+__device__ __forceinline__ int8_t residue(double X, const OzCrt& c, int i) {
+    constexpr double kM52 = 6755399441055744.0;  // 1.5 * 2^52
+    const double q = fma(X, c.rcpd[i], kM52) - kM52;
+    double r = fma(-q, c.md[i], X);
+    if (i == 0) r = r >= 128.0 ? r - 256.0 : r;
+    return int8_t(__double2loint(r + kM52) & 0xff);
 }
 
-// A rows -> out[p][m][0..Kp) int8 digits + ea[m]; one warp per row.
-__global__ void oz_split_rows_kernel(const float* __restrict__ A, int64_t lda, int M, int K, int Kp, int s, int Mp,
-                                     int8_t* __restrict__ out, int* __restrict__ ea) {
+// A rows -> out[i][m][0..Kp) int8 residues of A' = rint(A 2^ea) + ea[m]; one warp per row.
+__global__ void oz_split_rows_kernel(const float* __restrict__ A, int64_t lda, int M, int K, int Kp, int bits,
+                                     int Mp, const __grid_constant__ OzCrt crt, int8_t* __restrict__ out,
+                                     int* __restrict__ ea) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= M) return;
     const float* a = A + int64_t(warp) * lda;
@@ -334,23 +405,22 @@ __global__ void oz_split_rows_kernel(const float* __restrict__ A, int64_t lda, i
     for (int k = lane; k < K; k += 32) mx = fmaxf(mx, fabsf(a[k]));
 #pragma unroll
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const int e = scale_exp(mx);
+    const int e = scale_exp(mx, bits);
     if (lane == 0) ea[warp] = e;
+    const double pw = ldexp(1.0, e);
     const size_t plane = size_t(Mp) * Kp;
     int8_t* o = out + size_t(warp) * Kp;
     for (int k0 = lane * 4; k0 < Kp; k0 += 128) {
-        int dd[4][8];
+        double X[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) split_digits(ldexp(double((k0 + i < K) ? a[k0 + i] : 0.f), e), s, dd[i]);
-#pragma unroll
-        for (int p = 0; p < 8; ++p) {
-            if (p >= s) break;
+        for (int q = 0; q < 4; ++q) X[q] = rint(double((k0 + q < K) ? a[k0 + q] : 0.f) * pw);
+        for (int i = 0; i < crt.n; ++i) {
             char4 dg;
-            dg.x = int8_t(dd[0][p]);
-            dg.y = int8_t(dd[1][p]);
-            dg.z = int8_t(dd[2][p]);
-            dg.w = int8_t(dd[3][p]);
-            *reinterpret_cast<char4*>(o + p * plane + k0) = dg;
+            dg.x = residue(X[0], crt, i);
+            dg.y = residue(X[1], crt, i);
+            dg.z = residue(X[2], crt, i);
+            dg.w = residue(X[3], crt, i);
+            *reinterpret_cast<char4*>(o + i * plane + k0) = dg;
         }
     }
 }
@@ -367,34 +437,42 @@ __global__ void oz_colmax_kernel(const float* __restrict__ B, int64_t ldb, int K
     atomicMax(cmax + n, __float_as_uint(mx));
 }
 
-// B [K x N] row-major -> out[q][n][0..Kp) int8 digits (transposed, K-major) +
-// eb[n].  Tile 128 k x 32 n through shared memory.
+// B [K x N] row-major -> out[i][n][0..Kp) int8 residues of B' = rint(B 2^eb)
+// (transposed, K-major) + eb[n].  Tile 128 k x 32 n through shared memory,
+// eight moduli at a time.
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const float* __restrict__ B, int64_t ldb, int K, int N,
-                                                            int Kp, int s, int Np, const unsigned* __restrict__ cmax,
+                                                            int Kp, int bits, int Np,
+                                                            const __grid_constant__ OzCrt crt,
+                                                            const unsigned* __restrict__ cmax,
                                                             int8_t* __restrict__ out, int* __restrict__ eb) {
     __shared__ int8_t sd[8][32][128 + 16];
     const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 128;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
     const int n = n0 + tx;
-    const int e = n < N ? scale_exp(__uint_as_float(cmax[n])) : 0;
+    const int e = n < N ? scale_exp(__uint_as_float(cmax[n]), bits) : 0;
     if (blockIdx.y == 0 && ty == 0 && n < N) eb[n] = e;
-    for (int kk = ty; kk < 128; kk += 8) {
-        const int k = k0 + kk;
-        const float x = (k < K && n < N) ? B[int64_t(k) * ldb + n] : 0.f;
-        int dd[8];
-        split_digits(ldexp(double(x), e), s, dd);
+    const double pw = ldexp(1.0, e);
+    double X[16];
 #pragma unroll
-        for (int p = 0; p < 8; ++p)
-            if (p < s) sd[p][tx][kk] = int8_t(dd[p]);
+    for (int q = 0; q < 16; ++q) {
+        const int k = k0 + ty + 8 * q;
+        X[q] = rint(double((k < K && n < N) ? B[int64_t(k) * ldb + n] : 0.f) * pw);
     }
-    __syncthreads();
-    // write rows (q, n): 128 contiguous bytes = 8 x 16 B
     const size_t plane = size_t(Np) * Kp;
-    for (int idx = threadIdx.x; idx < s * 32 * 8; idx += 256) {
-        const int q = idx / 256, rem = idx % 256, nn = rem / 8, c = rem % 8;
-        if (n0 + nn >= N || k0 + c * 16 >= Kp) continue;
-        const int4 v = *reinterpret_cast<const int4*>(&sd[q][nn][c * 16]);
-        *reinterpret_cast<int4*>(out + q * plane + size_t(n0 + nn) * Kp + k0 + c * 16) = v;
+    for (int g0 = 0; g0 < crt.n; g0 += 8) {
+        const int gn = min(8, crt.n - g0);
+        for (int i = 0; i < gn; ++i)
+#pragma unroll
+            for (int q = 0; q < 16; ++q) sd[i][tx][ty + 8 * q] = residue(X[q], crt, g0 + i);
+        __syncthreads();
+        // write rows (i, n): 128 contiguous bytes = 8 x 16 B
+        for (int idx = threadIdx.x; idx < gn * 32 * 8; idx += 256) {
+            const int i = idx / 256, rem = idx % 256, nn = rem / 8, c = rem % 8;
+            if (n0 + nn >= N || k0 + c * 16 >= Kp) continue;
+            const int4 v = *reinterpret_cast<const int4*>(&sd[i][nn][c * 16]);
+            *reinterpret_cast<int4*>(out + (g0 + i) * plane + size_t(n0 + nn) * Kp + k0 + c * 16) = v;
+        }
+        __syncthreads();
     }
 }
 
@@ -411,36 +489,48 @@ CUtensorMap make_map_i8(const void* ptr, int64_t rows, int64_t cols, int64_t ld,
     return tm;
 }
 
-OzPlan make_plan(int s, int K) {
-    // int32 safety: a unit sums pairs * K products of magnitude <= 2^14
-    const int max_pairs = std::max(1, int((int64_t(1) << 17) / std::max(K, 1)));
-    if (max_pairs < 1) raise(KEEP_ERR_CONFIG, "Ozaki GEMM: K too large");
-    OzPlan pl{};
-    pl.nunits = 0;
-    for (int k = s - 1; k >= 0; --k) {
-        const int np = k + 1;  // pairs (p, k - p), p = 0..k
-        for (int pb = 0; pb < np; pb += max_pairs) {
-            if (pl.nunits >= kMaxUnits) raise(KEEP_ERR_CONFIG, "Ozaki GEMM: too many level units");
-            OzUnit& u = pl.u[pl.nunits];
-            u.k = int8_t(k);
-            u.pb = int8_t(pb);
-            u.pe = int8_t(std::min(np, pb + max_pairs));
-            u.op = int8_t(pl.nunits == 0 ? 0 : (pb == 0 ? 1 : 2));
-            ++pl.nunits;
+int mod_inverse(int a, int m) {
+    a %= m;
+    for (int x = 1; x < m; ++x)
+        if ((a * x) % m == 1) return x;
+    raise(KEEP_ERR_CONFIG, "Ozaki GEMM: moduli are not coprime");
+    return 0;
+}
+
+const OzCrt& crt_tables() {
+    static const OzCrt c = [] {
+        OzCrt t{};
+        t.n = oz_moduli();
+        for (int i = 0; i < t.n; ++i) {
+            t.mi[i] = kModuliAll[i];
+            t.mf[i] = float(kModuliAll[i]);
+            t.rcp[i] = 1.f / float(kModuliAll[i]);
+            t.md[i] = double(kModuliAll[i]);
+            t.rcpd[i] = 1.0 / double(kModuliAll[i]);
+            for (int j = 0; j < i; ++j) t.inv[j][i] = float(mod_inverse(kModuliAll[j], kModuliAll[i]));
         }
-    }
-    return pl;
+        return t;
+    }();
+    return c;
 }
 
 }  // namespace
 
-int oz_slices() {
+int oz_moduli() {
     static const int s = [] {
-        const char* e = std::getenv("KEEP_OZ_SLICES");
-        const int v = e ? std::atoi(e) : 7;
-        return std::min(8, std::max(2, v));
+        const char* e = std::getenv("KEEP_OZ_MODULI");
+        const int v = e ? std::atoi(e) : 14;
+        return std::min(kMaxModuli, std::max(8, v));
     }();
     return s;
+}
+
+int oz_bits(int K) {
+    double lm = 0.0;
+    for (int i = 0; i < oz_moduli(); ++i) lm += std::log2(double(kModuliAll[i]));
+    // K 2^2b <= M / 4: the symmetric range (-M/2, M/2) holds every product sum
+    // with a margin for the non-canonical top digit
+    return int(std::floor((lm - 2.0 - std::log2(double(std::max(K, 1)))) / 2.0));
 }
 
 // KEEP_PARITY_GEMM=dfma|ozaki|auto (default auto: Ozaki from kOzMinRows rows)
@@ -456,13 +546,17 @@ int parity_gemm_mode() {
 }
 
 bool ozaki_eligible(int M, int N, int K) {
-    return K % 16 == 0 && N % 32 == 0 && (parity_gemm_mode() == 1 || (parity_gemm_mode() == 0 && M >= kOzMinRows));
+    return K % 16 == 0 && N % 32 == 0 && K <= (1 << 17) &&
+           (parity_gemm_mode() == 1 || (parity_gemm_mode() == 0 && M >= kOzMinRows));
 }
 
 void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
                        const EpiArgs& epi, cudaStream_t st, OzWork& w, int max_ctas) {
     if (M == 0 || N == 0) return;
-    const int s = oz_slices();
+    const OzCrt& crt = crt_tables();
+    const int s = crt.n;
+    const int bits = oz_bits(K);
+    if (bits < 30) raise(KEEP_ERR_CONFIG, "Ozaki GEMM: too few moduli for K = " + std::to_string(K));
     const int Mp = int(ceil_div(M, OBM) * OBM), Np = int(ceil_div(N, OBN) * OBN);
     const int Kp = int(ceil_div(K, 16) * 16);
     w.a.ensure(size_t(s) * Mp * Kp);
@@ -471,9 +565,9 @@ void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb,
     w.eb.ensure(sizeof(int) * size_t(Np) + sizeof(unsigned) * size_t(N));
     int* eb = w.eb.as<int>();
     unsigned* cmax = reinterpret_cast<unsigned*>(eb + Np);
-    // digits of A (rows) and B (columns)
-    oz_split_rows_kernel<<<unsigned(ceil_div(M, 8)), 256, 0, st>>>(A, lda, M, K, Kp, s, Mp, w.a.as<int8_t>(),
-                                                                    w.ea.as<int>());
+    // residues of A (rows) and B (columns)
+    oz_split_rows_kernel<<<unsigned(ceil_div(M, 8)), 256, 0, st>>>(A, lda, M, K, Kp, bits, Mp, crt,
+                                                                    w.a.as<int8_t>(), w.ea.as<int>());
     KEEP_LAUNCH_CHECK();
     KEEP_CUDA(cudaMemsetAsync(cmax, 0, sizeof(unsigned) * size_t(N), st));
     const int ksplit = int(std::min<int64_t>(64, ceil_div(K, 64)));
@@ -481,18 +575,17 @@ void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb,
     oz_colmax_kernel<<<dim3(unsigned(ceil_div(N, 256)), unsigned(ksplit)), 256, 0, st>>>(B, ldb, K, N, krows, cmax);
     KEEP_LAUNCH_CHECK();
     oz_split_cols_kernel<<<dim3(unsigned(ceil_div(N, 32)), unsigned(ceil_div(Kp, 128))), 256, 0, st>>>(
-        B, ldb, K, N, Kp, s, Np, cmax, w.b.as<int8_t>(), eb);
+        B, ldb, K, N, Kp, bits, Np, crt, cmax, w.b.as<int8_t>(), eb);
     KEEP_LAUNCH_CHECK();
     // the GEMM
     smem_attr(gemm_oz_kernel, int(OSMEM));
-    const OzPlan plan = make_plan(s, K);
     const CUtensorMap ta = make_map_i8(w.a.p, int64_t(s) * Mp, K, Kp, OBM);
     const CUtensorMap tb = make_map_i8(w.b.p, int64_t(s) * Np, K, Kp, OBN);
     const int ntiles = int(ceil_div(M, OBM) * ceil_div(N, OBN));
     const int grid = std::min(ntiles, std::max(1, std::min(max_ctas, kNumSMs)));
-    w.part.ensure(sizeof(double) * size_t(grid) * OBM * OBN);
-    gemm_oz_kernel<<<grid, OTHREADS, OSMEM, st>>>(ta, tb, M, N, K, Mp, Np, plan, w.ea.as<int>(), eb,
-                                                  w.part.as<double>(), epi);
+    w.part.ensure(sizeof(uint32_t) * size_t(grid) * kMaxModuli * (OBN / 4) * OBM);
+    gemm_oz_kernel<<<grid, OTHREADS, OSMEM, st>>>(ta, tb, M, N, K, Mp, Np, crt, w.ea.as<int>(), eb,
+                                                  w.part.as<uint32_t>(), epi);
     KEEP_LAUNCH_CHECK();
 }
 

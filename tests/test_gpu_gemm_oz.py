@@ -1,4 +1,4 @@
-"""PARITY projection GEMM on the int8 tensor cores (gemm_oz.cu, Ozaki scheme)
+"""PARITY projection GEMM on the int8 tensor cores (gemm_oz.cu, Ozaki scheme II)
 against the reference's arithmetic: fp32 operands, fp64 accumulation, one
 rounding to fp32 (vec_mat, tensor.hpp:31-41).
 
@@ -8,12 +8,25 @@ baseline.  The Ozaki result must stay within its stated error bound of the
 exact value, and its fp32 outputs must equal the DFMA kernel's except for a
 tiny fraction of 1-ulp rounding-boundary cases.
 """
+import math
+import os
+
 import numpy as np
 import pytest
 
 import paper_2602_23592_b200 as kb
 
 pytestmark = pytest.mark.gpu
+
+
+MODULI = [256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193]
+
+
+def oz_bits(K):
+    """gemm_oz.cu oz_bits: integer bits per operand with K 2^2b <= M / 4."""
+    n = int(os.environ.get("KEEP_OZ_MODULI", "14"))
+    lm = sum(math.log2(m) for m in MODULI[:n])
+    return int(math.floor((lm - 2.0 - math.log2(K)) / 2.0))
 
 
 def run(A, B, mode):
@@ -42,10 +55,13 @@ def test_ozaki_matches_fp64_accumulation(M, N, K):
     df = run(A, B, 2)
     exact = A.double() @ B.double()
     assert not torch.isnan(oz).any()
-    # error bound: per product 2^-(8s-10) max|a_row| max|b_col| (s = 7 digits) plus the fp32 rounding
+    # error bound: each operand rounded to b integer bits of its row / column
+    # maximum (|error| <= 2^-b max), the CRT reconstruction exact, the fp64
+    # Horner within a few ulp, plus the final fp32 rounding
+    b = oz_bits(K)
     amax = A.abs().amax(dim=1, keepdim=True).double()
     bmax = B.abs().amax(dim=0, keepdim=True).double()
-    bound = K * 2.0 ** (-(8 * 7 - 10)) * amax * bmax + exact.abs() * 2.0 ** -24
+    bound = K * 2.0 ** (1 - b) * amax * bmax + exact.abs() * 2.0 ** -24
     assert bool(((oz.double() - exact).abs() <= bound).all())
     # fp32 outputs equal the DFMA (vec_mat) ones except rounding-boundary ties
     diff = (oz != df).double().mean().item()
@@ -82,3 +98,19 @@ def test_dfma_skinny_is_vec_mat(M, N, K):
         acc += A[:, k:k + 1].astype(np.float64) * B[k].astype(np.float64)
     got = run(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), 2).cpu().numpy()
     assert np.array_equal(got, acc.astype(np.float32))
+
+
+@pytest.mark.parametrize("K", [64, 5120, 13824])
+def test_ozaki_crt_range_extremes(K):
+    """The largest product sums the CRT range must hold: every operand at its
+    row / column maximum with one sign (|X| = K 2^2b), and alternating signs."""
+    import torch
+    M, N = 128, 256
+    A = torch.ones(M, K, device="cuda")
+    A[1::2] = -1.0
+    A[2] = 0.75
+    B = torch.ones(K, N, device="cuda")
+    B[:, 1::3] = -0.5
+    oz = run(A, B, 1)
+    exact = (A.double() @ B.double()).float()
+    assert torch.equal(oz, exact)

@@ -37,7 +37,7 @@ sel = bench.selection_parity(P, F, summ)
 hp, hf = P["final_hidden"][-len(q):].astype(np.float64), F["final_hidden"][-len(q):].astype(np.float64)
 summary = {"config": cfgname, "S": lay.S, "T": int(np.sum(lay.seg_len)) + len(q),
            "parity_ttft_ms": P["ttft_ms"], "fast_ttft_ms": F["ttft_ms"],
-           "oz_slices": int(os.environ.get("KEEP_OZ_SLICES", "7")),
+           "oz_moduli": int(os.environ.get("KEEP_OZ_MODULI", "14")),
            "plan_segments_per_layer_parity": [int(x) for x in P["plan"].sum(axis=1)],
            "plan_segments_per_layer_fast": [int(x) for x in F["plan"].sum(axis=1)],
            "hops_parity": [int(x) for x in P["hops"]], "hops_fast": [int(x) for x in F["hops"]],
