@@ -347,7 +347,8 @@ void plan_splits(Context& c, Pass& p) {
     const bool tc = use_tc_attention(c, p);
     // the split plan depends only on (n, T, path): layers of equal size reuse
     // the uploaded arrays (no host->device staging on the deep layers)
-    const int64_t key = (int64_t(p.n) << 32) ^ (int64_t(p.T) << 2) ^ (tc ? 1 : 0) ^ (p.block_diag ? 2 : 0);
+    const int64_t key = (int64_t(p.n) << 32) ^ (int64_t(p.T) << 2) ^ (tc ? 1 : 0) ^ (p.block_diag ? 2 : 0) ^
+                        (int64_t(p.with_summary) << 62);
     if (key == p.split_key) return;
     p.split_key = key;
     const bool dmma = !c.fast && !c.exact && parity_attention_dmma(c.dh);
@@ -395,7 +396,10 @@ void plan_splits(Context& c, Pass& p) {
         const int target = tc ? 2 * kNumSMs : 4 * kNumSMs;
         // (the DMMA kernels run one 256-thread CTA per (row tile, head, split) and SM)
         const int64_t ctas = dmma ? int64_t(tiles) * c.Hl : tiles;
-        nsplit = int(std::min<int64_t>(ceil_div(dmma ? 2 * kNumSMs : target, ctas), std::max(1, p.T / 128)));
+        // (the fp64 decode kernel: one CTA per (head, split), two per SM, a few waves)
+        const bool f64dec = dmma && attention_f64_decode(p.n, c.dh, p.with_summary);
+        const int64_t want = f64dec ? 6 * kNumSMs : (dmma ? 2 * kNumSMs : target);
+        nsplit = int(std::min<int64_t>(ceil_div(want, ctas), std::max(1, p.T / 128)));
         // bound the fp64 partial-context scratch to ~512 MB
         const int64_t per_split = int64_t(p.n) * c.dl * 8;
         nsplit = int(std::max<int64_t>(1, std::min<int64_t>(nsplit, (512ll << 20) / std::max<int64_t>(per_split, 1))));

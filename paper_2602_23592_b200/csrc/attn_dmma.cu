@@ -34,9 +34,11 @@ namespace keep_b200 {
 
 namespace {
 
-constexpr int AW = 8;              // warps per CTA
+constexpr int AW = 12;             // warps per CTA (3 per SM sub-partition: one warp alone cannot issue
+                                   // DMMA at the pipe rate, tools/micro/fp64_shapes.cu)
 constexpr int ART = AW * 8;        // compact rows per CTA
-constexpr int AKC = 64;            // keys per chunk
+constexpr int AKC = 64;            // keys per staged chunk (multiplied in two 32-key halves)
+constexpr int AKH = 32;
 constexpr int ANT = AW * 32;
 enum { M_STATS = 0, M_CTX = 1, M_FLASH = 2 };
 
@@ -63,7 +65,10 @@ __device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_grou
 template <int DH>
 struct Geo {
     static constexpr int P32 = DH + 4;                 // fp32 staging row stride (floats)
-    static constexpr int P64 = DH + 4;                 // fp64 row stride (doubles)
+    static constexpr int P64 = DH + 4;                 // fp64 K row stride (doubles): K fragments
+                                                       // (8 keys x 4 dims) hit each bank pair once
+    static constexpr int P64V = DH + 2;                // fp64 V row stride: V fragments (4 keys x 8
+                                                       // dims) -- DH + 4 put keys 2t and 2t + 4 on one bank
     static constexpr int S32 = AKC * P32;              // floats per staged K (or V) chunk
     static constexpr int S64 = AKC * P64;              // doubles per converted chunk
     static constexpr int NT = DH / 8;                  // n-tiles of P.V
@@ -83,14 +88,14 @@ __device__ __forceinline__ void stage_chunk(float* dst, const float* src, int k0
     }
 }
 
-// fp32 staging -> fp64 chunk (exact)
-template <int DH>
+// fp32 staging -> fp64 chunk (exact), row stride P64
+template <int DH, int P64>
 __device__ __forceinline__ void widen_chunk(double* dst, const float* src) {
     constexpr int V4 = DH / 4;
     for (int e = threadIdx.x; e < AKC * V4; e += ANT) {
         const int r = e / V4, c = e % V4;
         const float4 x = *reinterpret_cast<const float4*>(src + r * Geo<DH>::P32 + 4 * c);
-        double2* o = reinterpret_cast<double2*>(dst + r * Geo<DH>::P64 + 4 * c);
+        double2* o = reinterpret_cast<double2*>(dst + r * P64 + 4 * c);
         o[0] = make_double2(double(x.x), double(x.y));
         o[1] = make_double2(double(x.z), double(x.w));
     }
@@ -113,18 +118,21 @@ __device__ __forceinline__ RowInfo row_info(const AttnArgs& a, int i) {
     return r;
 }
 
-constexpr int NJ = AKC / 8;  // key n-tiles per chunk
+constexpr int NJ = AKC / 8;   // key n-tiles per chunk
+constexpr int NJH = AKH / 8;  // key n-tiles per half chunk
 
-// S = Q.K^T (scaled) for this warp's 8 rows x the chunk's AKC keys
-template <int DH>
-__device__ __forceinline__ void scores(const double (&qa)[DH / 4], const double* ks, int g, int t, double scale,
-                                       double (&s)[NJ][2]) {
+// S = Q.K^T (scaled) for this warp's 8 rows x NJ_ * 8 keys (Q fragments kept
+// in fp32 and widened per k-step: exact, and half the registers)
+template <int DH, int NJ_, typename QT>
+__device__ __forceinline__ void scores(const QT (&qa)[DH / 4], const double* ks, int g, int t, double scale,
+                                       double (&s)[NJ_][2]) {
+    constexpr int NJ = NJ_;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) s[j][0] = s[j][1] = 0.0;
 #pragma unroll
     for (int i = 0; i < DH / 4; ++i) {
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma(s[j], qa[i], ks[(8 * j + g) * Geo<DH>::P64 + 4 * i + t]);
+        for (int j = 0; j < NJ; ++j) dmma(s[j], double(qa[i]), ks[(8 * j + g) * Geo<DH>::P64 + 4 * i + t]);
     }
     // s = dot * scale rounded on its own (prefill.hpp:140): no FMA contraction
     // with the later s - max, which at depth (|s| ~ 1e18, ulp ~ 1e2) would move
@@ -156,12 +164,12 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_kernel(AttnArgs a, double sc
     const int lo = max(a.split_lo[sp], klo0), hi = min(a.split_hi[sp], tmax + 1);
     const int row = i0 + warp * 8 + g;
     const RowInfo ri = row_info(a, row);
-    // Q fragments (A of m8n8k4: row g, k = 4i + t), fp32 -> fp64 exactly
-    double qa[DH / 4];
+    // Q fragments (A of m8n8k4: row g, k = 4i + t), fp32, widened per use
+    float qa[DH / 4];
     {
         const float* q = static_cast<const float*>(a.q) + int64_t(min(row, a.n - 1)) * a.d + off;
 #pragma unroll
-        for (int i = 0; i < DH / 4; ++i) qa[i] = ri.t >= 0 ? double(q[4 * i + t]) : 0.0;
+        for (int i = 0; i < DH / 4; ++i) qa[i] = ri.t >= 0 ? q[4 * i + t] : 0.f;
     }
     double m = -DBL_MAX, l = 0.0, inv = 0.0;
     if (MODE == M_CTX && ri.t >= 0) {
@@ -183,73 +191,78 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_kernel(AttnArgs a, double sc
     };
     if (nchunks > 0) issue(0);
     for (int c = 0; c < nchunks; ++c) {
-        const int k0 = lo + c * AKC;
         cp_wait_all();
         __syncthreads();  // chunk c staged; everyone done with the previous fp64 chunk
-        widen_chunk<DH>(kd, stg);
-        if (WV) widen_chunk<DH>(vd, stg + G::S32);
+        widen_chunk<DH, G::P64>(kd, stg);
+        if (WV) widen_chunk<DH, G::P64V>(vd, stg + G::S32);
         __syncthreads();
         if (c + 1 < nchunks) issue(c + 1);  // the next chunk streams in behind this one's math
-        double s[NJ][2];
-        scores<DH>(qa, kd, g, t, scale, s);
-        // visibility of key k0 + 8j + 2t + e for this thread's row
-        bool vis[NJ][2];
+#pragma unroll 1
+        for (int hh = 0; hh < AKC / AKH; ++hh) {  // two 32-key halves: half the score registers
+            const int k0 = lo + c * AKC + hh * AKH;
+            if (k0 >= hi) break;
+            double s[NJH][2];
+            scores<DH, NJH>(qa, kd + hh * AKH * G::P64, g, t, scale, s);
+            // visibility of key k0 + 8j + 2t + e for this thread's row
+            bool vis[NJH][2];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int key = k0 + 8 * j + 2 * t + e;
-                vis[j][e] = key < hi && key <= ri.t && key >= ri.klo;
-            }
-        if (MODE == M_STATS || MODE == M_FLASH) {
-            double cm = -DBL_MAX;
-#pragma unroll
-            for (int j = 0; j < NJ; ++j)
-#pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    if (vis[j][e]) cm = fmax(cm, s[j][e]);
-            cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
-            cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
-            const bool any = cm != -DBL_MAX;
-            const double mn = fmax(m, cm);
-            double part = 0.0;
-#pragma unroll
-            for (int j = 0; j < NJ; ++j)
+            for (int j = 0; j < NJH; ++j)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const double p = (any && vis[j][e]) ? exp(__dsub_rn(s[j][e], mn)) : 0.0;
-                    s[j][e] = p;
-                    part += p;
+                    const int key = k0 + 8 * j + 2 * t + e;
+                    vis[j][e] = key < hi && key <= ri.t && key >= ri.klo;
                 }
-            part += __shfl_xor_sync(0xffffffffu, part, 1);
-            part += __shfl_xor_sync(0xffffffffu, part, 2);
-            if (any) {
-                const double alpha = m == -DBL_MAX ? 0.0 : exp(__dsub_rn(m, mn));
-                l = l * alpha + part;
-                m = mn;
-                if (MODE == M_FLASH && alpha != 1.0) {
+            if (MODE == M_STATS || MODE == M_FLASH) {
+                double cm = -DBL_MAX;
 #pragma unroll
-                    for (int n = 0; n < G::NT; ++n) {
-                        o_acc[n][0] *= alpha;
-                        o_acc[n][1] *= alpha;
+                for (int j = 0; j < NJH; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        if (vis[j][e]) cm = fmax(cm, s[j][e]);
+                cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+                cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+                const bool any = cm != -DBL_MAX;
+                const double mn = fmax(m, cm);
+                double part = 0.0;
+#pragma unroll
+                for (int j = 0; j < NJH; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const double p = (any && vis[j][e]) ? exp(__dsub_rn(s[j][e], mn)) : 0.0;
+                        s[j][e] = p;
+                        part += p;
+                    }
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                if (any) {
+                    const double alpha = m == -DBL_MAX ? 0.0 : exp(__dsub_rn(m, mn));
+                    l = l * alpha + part;
+                    m = mn;
+                    if (MODE == M_FLASH && alpha != 1.0) {
+#pragma unroll
+                        for (int n = 0; n < G::NT; ++n) {
+                            o_acc[n][0] *= alpha;
+                            o_acc[n][1] *= alpha;
+                        }
                     }
                 }
+            } else {  // CTX: normalised probabilities with the final statistics
+#pragma unroll
+                for (int j = 0; j < NJH; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e)
+                        s[j][e] = vis[j][e] ? __dmul_rn(exp(__dsub_rn(s[j][e], m)), inv) : 0.0;
             }
-        } else {  // CTX: normalised probabilities with the final statistics
+            if (WV) {  // O += P.V
 #pragma unroll
-            for (int j = 0; j < NJ; ++j)
+                for (int j = 0; j < NJH; ++j)
 #pragma unroll
-                for (int e = 0; e < 2; ++e) s[j][e] = vis[j][e] ? __dmul_rn(exp(__dsub_rn(s[j][e], m)), inv) : 0.0;
-        }
-        if (WV) {  // O += P.V
+                    for (int e = 0; e < 2; ++e) {
+                        const double* vr = vd + (hh * AKH + 8 * j + 2 * t + e) * G::P64V + g;
 #pragma unroll
-            for (int j = 0; j < NJ; ++j)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const double* vr = vd + (8 * j + 2 * t + e) * G::P64 + g;
-#pragma unroll
-                    for (int n = 0; n < G::NT; ++n) dmma(o_acc[n], s[j][e], vr[8 * n]);
-                }
+                        for (int n = 0; n < G::NT; ++n) dmma(o_acc[n], s[j][e], vr[8 * n]);
+                    }
+            }
         }
     }
     if (ri.t < 0) return;
@@ -353,7 +366,7 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_bins_kernel(AttnArgs a, doub
         const int k0 = lo + c * AKC;
         cp_wait_all();
         __syncthreads();  // (also: the previous chunk's binning has read pm)
-        widen_chunk<DH>(kd, stg);
+        widen_chunk<DH, G::P64>(kd, stg);
         if (h == 0)
             for (int e = threadIdx.x; e < ART * (AKC + 1); e += ANT) pm[e] = 0.0;
         __syncthreads();
@@ -363,7 +376,7 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_bins_kernel(AttnArgs a, doub
 #pragma unroll
         for (int i = 0; i < DH / 4; ++i) qa[i] = ri.t >= 0 ? double(q[4 * i + t]) : 0.0;
         double s[NJ][2];
-        scores<DH>(qa, kd, g, t, scale, s);
+        scores<DH, NJ>(qa, kd, g, t, scale, s);
         if (ri.t >= 0) {
             const int64_t o = int64_t(row) * a.H + h;
             const double mrow = a.m_fin[o];
@@ -403,6 +416,150 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_bins_kernel(AttnArgs a, doub
     if (threadIdx.x < nrows && cur >= 0) rowbin[int64_t(i0 + threadIdx.x) * a.S + cur] = run;
 }
 
+// ------------------------------------------------------------ decode --
+// Few rows (<= 16: the query alone, every layer after the walk) and no
+// summary: a key-split fp64 flash decode.  The DMMA tiles would be ~90%
+// padding rows; here the key stream is the bound.  CTA = one head x one key
+// split, keys in 64-key tiles through shared memory:
+//   scores  thread = (key, row quarter): fp64 dot in ascending dimension
+//   softmax warp r = row r: online max / sum (prefill.hpp:138-146)
+//   P.V     thread = (dimension, row half)
+// Partials (m, l, o) per split are merged by flash_combine_f64_kernel.
+constexpr int DKT = 64;       // keys per tile
+constexpr int DROWS = 16;     // max rows
+template <int DH>
+struct DecGeo {
+    static constexpr int KS = DH + 1;  // fp32 K row stride: lanes = keys hit distinct banks
+    static constexpr size_t smem = sizeof(double) * DROWS * DH + sizeof(float) * DKT * KS + sizeof(float) * DKT * DH +
+                                   sizeof(double) * DROWS * (DKT + 1) + sizeof(double) * DROWS * 3;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(256, 2) attn_f64_decode_kernel(AttnArgs a, double scale) {
+    using G = DecGeo<DH>;
+    extern __shared__ __align__(16) double sm[];
+    double* qs = sm;                                           // [DROWS][DH]
+    double* ps = qs + DROWS * DH;                              // [DROWS][DKT + 1]
+    double* mrow = ps + DROWS * (DKT + 1);                     // [DROWS]
+    double* lrow = mrow + DROWS;
+    double* arow = lrow + DROWS;                               // alpha of this tile
+    float* ks = reinterpret_cast<float*>(arow + DROWS);        // [DKT][KS]
+    float* vs = ks + DKT * G::KS;                              // [DKT][DH]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int h = blockIdx.x, sp = blockIdx.y, off = h * DH;
+    const int n = a.n;
+    const int tmax = a.rows[n - 1];
+    const int lo = a.split_lo[sp], hi = min(a.split_hi[sp], tmax + 1);
+    for (int e = tid; e < n * DH; e += 256) {
+        const int r = e / DH, c = e % DH;
+        qs[e] = double(static_cast<const float*>(a.q)[int64_t(r) * a.d + off + c]);
+    }
+    if (tid < DROWS) {
+        mrow[tid] = -DBL_MAX;
+        lrow[tid] = 0.0;
+    }
+    const int kk = tid & (DKT - 1), rq = tid >> 6;   // scores: key, row quarter
+    const int dd = tid & (DH - 1), rh = tid / DH;     // P.V: dimension, row group
+    constexpr int RG = 256 / DH;                      // row groups of P.V
+    constexpr int OR = DROWS / RG > 0 ? DROWS / RG : 1;  // rows per thread in P.V (DH = 128: 8)
+    double o[OR];
+#pragma unroll
+    for (int i = 0; i < OR; ++i) o[i] = 0.0;
+    const float* kg = static_cast<const float*>(a.k);
+    const float* vg = static_cast<const float*>(a.v);
+    for (int k0 = lo; k0 < hi; k0 += DKT) {
+        __syncthreads();  // previous tile consumed
+        for (int e = tid; e < DKT * (DH / 4); e += 256) {
+            const int r = e / (DH / 4), c = 4 * (e % (DH / 4));
+            const bool ok = k0 + r < hi;
+            const float4 kv = ok ? *reinterpret_cast<const float4*>(kg + int64_t(k0 + r) * a.d + off + c)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 vv = ok ? *reinterpret_cast<const float4*>(vg + int64_t(k0 + r) * a.d + off + c)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+            float* kr = ks + r * G::KS + c;
+            kr[0] = kv.x;
+            kr[1] = kv.y;
+            kr[2] = kv.z;
+            kr[3] = kv.w;
+            *reinterpret_cast<float4*>(vs + r * DH + c) = vv;
+        }
+        __syncthreads();
+        // scores of (row r, key k0 + kk), r = rq, rq + 4, ...
+        for (int r = rq; r < n; r += 4) {
+            const int t = a.rows[r];
+            const int klo = a.key_lo ? a.key_lo[t] : 0;
+            const int key = k0 + kk;
+            double acc = 0.0;
+            const double* q = qs + r * DH;
+            const float* kr = ks + kk * G::KS;
+#pragma unroll 8
+            for (int c = 0; c < DH; ++c) acc = fma(q[c], double(kr[c]), acc);
+            const bool vis = key < hi && key <= t && key >= klo;
+            ps[r * (DKT + 1) + kk] = vis ? __dmul_rn(acc, scale) : -DBL_MAX;
+        }
+        __syncthreads();
+        // online softmax: warp w handles rows w, w + 8
+        for (int r = warp; r < n; r += 8) {
+            double* pr = ps + r * (DKT + 1);
+            const double s0 = pr[lane], s1 = pr[lane + 32];
+            double cm = fmax(s0, s1);
+#pragma unroll
+            for (int o2 = 16; o2; o2 >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o2));
+            const double m = mrow[r];
+            double alpha = 1.0;
+            if (cm != -DBL_MAX) {
+                const double mn = fmax(m, cm);
+                const double p0 = s0 != -DBL_MAX ? exp(__dsub_rn(s0, mn)) : 0.0;
+                const double p1 = s1 != -DBL_MAX ? exp(__dsub_rn(s1, mn)) : 0.0;
+                pr[lane] = p0;
+                pr[lane + 32] = p1;
+                double part = p0 + p1;
+#pragma unroll
+                for (int o2 = 16; o2; o2 >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o2);
+                alpha = m == -DBL_MAX ? 0.0 : exp(__dsub_rn(m, mn));
+                __syncwarp();
+                if (lane == 0) {
+                    lrow[r] = lrow[r] * alpha + part;
+                    mrow[r] = mn;
+                }
+            } else {
+                pr[lane] = 0.0;
+                pr[lane + 32] = 0.0;
+            }
+            if (lane == 0) arow[r] = alpha;
+        }
+        __syncthreads();
+        // O[r][dd] = O alpha + sum_k p[r][k] V[k][dd]
+#pragma unroll
+        for (int i = 0; i < OR; ++i) {
+            const int r = rh + RG * i;
+            if (r >= n) break;
+            const double* pr = ps + r * (DKT + 1);
+            double acc = o[i] * arow[r];
+#pragma unroll 8
+            for (int k = 0; k < DKT; ++k) acc = fma(pr[k], double(vs[k * DH + dd]), acc);
+            o[i] = acc;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < OR; ++i) {
+        const int r = rh + RG * i;
+        if (r >= n) break;
+        if (a.nsplit == 1) {
+            const double l = lrow[r];
+            a.ctx[int64_t(r) * a.d + off + dd] = l > 0.0 ? float(o[i] * (1.0 / l)) : 0.f;
+        } else {
+            a.o_part[(int64_t(sp) * n + r) * a.d + off + dd] = o[i];
+            if (dd == 0) {
+                const int64_t oo = (int64_t(sp) * n + r) * a.H + h;
+                a.m_part[oo] = mrow[r];
+                a.l_part[oo] = lrow[r];
+            }
+        }
+    }
+}
+
 template <int DH, int MODE>
 void launch_mode_dmma(const AttnArgs& a, dim3 grid, double scale, cudaStream_t st) {
     const int smem = Geo<DH>::smem(MODE != M_STATS);
@@ -417,6 +574,18 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
     const double scale = 1.0 / std::sqrt(double(DH));  // prefill.hpp:129
     const dim3 grid(unsigned(tiles), unsigned(a.H), unsigned(a.nsplit));
     const int64_t nh = int64_t(a.n) * a.H;
+    if constexpr (DH == 128) if (!a.with_bins && a.n <= DROWS) {
+        const size_t smem = DecGeo<DH>::smem;
+        smem_attr(attn_f64_decode_kernel<DH>, int(smem));
+        attn_f64_decode_kernel<DH><<<dim3(unsigned(a.H), unsigned(a.nsplit)), 256, smem, st>>>(a, scale);
+        KEEP_LAUNCH_CHECK();
+        if (a.nsplit > 1) {
+            const int64_t nd = int64_t(a.n) * a.d;
+            flash_combine_f64_kernel<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(a, DH);
+            KEEP_LAUNCH_CHECK();
+        }
+        return;
+    }
     if (!a.with_bins) {
         launch_mode_dmma<DH, M_FLASH>(a, grid, scale, st);
         if (a.nsplit > 1) {
@@ -442,6 +611,8 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
 bool attention_dmma_fits(int dh) { return dh == 8 || dh == 16 || dh == 32 || dh == 64 || dh == 128; }
 
 int attention_dmma_rows_per_tile() { return ART; }
+
+bool attention_f64_decode(int n, int dh, bool with_bins) { return !with_bins && dh == 128 && n <= DROWS; }
 
 void launch_attention_parity_dmma(const AttnArgs& a, cudaStream_t st) {
     if (a.n == 0) return;

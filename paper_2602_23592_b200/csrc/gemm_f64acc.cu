@@ -8,8 +8,11 @@
 // Fused epilogues: QKV split + scatter of K/V rows into the merged cache,
 // fp32 residual add (prefill.hpp:289-291, 302-303), ReLU (299-300).
 #include <cstdlib>
+#include <map>
+#include <memory>
+#include <mutex>
 
-#include "kernels.hpp"
+#include "engine.hpp"
 
 namespace keep_b200 {
 
@@ -125,7 +128,8 @@ __device__ __forceinline__ void cpa16(void* dst, const void* src, bool ok) {
 template <int RPT>
 __global__ void __launch_bounds__(256) gemm_f64_skinny_kernel(const float* __restrict__ A, int64_t lda,
                                                               const float* __restrict__ B, int64_t ldb, int M, int N,
-                                                              int K, EpiArgs epi) {
+                                                              int K, int kchunk, double* __restrict__ part,
+                                                              EpiArgs epi) {
     constexpr int MR = 8 * RPT;
     __shared__ __align__(16) float bst[SK_ST][SK_KB][SK_NC];
     __shared__ __align__(16) float ast[SK_ST][MR][SK_KB];
@@ -133,18 +137,20 @@ __global__ void __launch_bounds__(256) gemm_f64_skinny_kernel(const float* __res
     __shared__ double ad[MR][SK_KB];
     const int tid = threadIdx.x, col = tid & 31, rs = tid >> 5;
     const int n0 = blockIdx.x * SK_NC;
-    const int nkb = int(ceil_div(K, SK_KB));
+    // this CTA's k range [kbeg, kend) (split-K: blockIdx.y)
+    const int kbeg = blockIdx.y * kchunk, kend = min(K, kbeg + kchunk);
+    const int nkb = int(ceil_div(kend - kbeg, SK_KB));
     auto issue = [&](int kb) {
         if (kb < nkb) {
-            const int s = kb % SK_ST, k0 = kb * SK_KB;
+            const int s = kb % SK_ST, k0 = kbeg + kb * SK_KB;
             {  // B: 32 k-rows x 128 bytes
                 const int r = tid >> 3, c = tid & 7;
-                const bool ok = k0 + r < K && n0 + 4 * c < N;
+                const bool ok = k0 + r < kend && n0 + 4 * c < N;
                 cpa16(&bst[s][r][4 * c], B + (ok ? int64_t(k0 + r) * ldb + n0 + 4 * c : 0), ok);
             }
             for (int e = tid; e < M * 8; e += 256) {  // A: M rows x 128 bytes
                 const int r = e >> 3, c = e & 7;
-                const bool ok = k0 + 4 * c < K;
+                const bool ok = k0 + 4 * c < kend;
                 cpa16(&ast[s][r][4 * c], A + (ok ? int64_t(r) * lda + k0 + 4 * c : 0), ok);
             }
         }
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__(256) gemm_f64_skinny_kernel(const float* __res
         for (int e = tid; e < M * SK_KB; e += 256) ad[e >> 5][e & 31] = double(ast[s][e >> 5][e & 31]);
         __syncthreads();
         issue(kb + SK_ST - 1);
-        const int kn = min(SK_KB, K - kb * SK_KB);
+        const int kn = min(SK_KB, kend - kbeg - kb * SK_KB);
         for (int kk = 0; kk < kn; ++kk) {
             const double b = bd[kk][col];
 #pragma unroll
@@ -174,7 +180,20 @@ __global__ void __launch_bounds__(256) gemm_f64_skinny_kernel(const float* __res
 #pragma unroll
     for (int r = 0; r < RPT; ++r) {
         const int m = rs + 8 * r;
-        if (m < M) epi_store1(epi, m, n, static_cast<float>(acc[r]));
+        if (m >= M) continue;
+        if (part) part[(int64_t(blockIdx.y) * M + m) * N + n] = acc[r];
+        else epi_store1(epi, m, n, static_cast<float>(acc[r]));
+    }
+}
+
+// split-K finish: the k-range partials summed in ascending split order
+// (deterministic), one rounding to fp32, the fused epilogue
+__global__ void f64_splitk_finish_kernel(const double* __restrict__ part, int ks, int M, int N, EpiArgs epi) {
+    const int64_t MN = int64_t(M) * N;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < MN; e += int64_t(gridDim.x) * blockDim.x) {
+        double acc = part[e];
+        for (int s = 1; s < ks; ++s) acc += part[int64_t(s) * MN + e];
+        epi_store1(epi, int(e / N), int(e % N), static_cast<float>(acc));
     }
 }
 
@@ -188,16 +207,47 @@ bool skinny_f64_enabled() {
 }
 }  // namespace
 
+double* f64_splitk_workspace(size_t bytes, cudaStream_t st) {
+    // grow-only per (device, stream): GEMMs in flight on different streams (or
+    // contexts on different GPUs) never share one
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, std::unique_ptr<DevBuf>> pool;
+    int dev = 0;
+    KEEP_CUDA(cudaGetDevice(&dev));
+    DevBuf* ws;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto& slot = pool[{dev, st}];
+        if (!slot) slot.reset(new DevBuf());
+        ws = slot.get();
+    }
+    ws->ensure(bytes);
+    return ws->as<double>();
+}
+
 void launch_gemm_f64acc(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
-                        const EpiArgs& epi, cudaStream_t st) {
+                        const EpiArgs& epi, cudaStream_t st, bool exact) {
     if (M == 0 || N == 0) return;
     // few rows: the weight stream (16-byte cp.async needs 16-byte aligned rows)
     if (M <= 32 && skinny_f64_enabled() && K % 4 == 0 && N % 4 == 0 && lda % 4 == 0 && ldb % 4 == 0) {
-        const unsigned grid = unsigned(ceil_div(N, SK_NC));
-        if (M <= 8) gemm_f64_skinny_kernel<1><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, epi);
-        else if (M <= 16) gemm_f64_skinny_kernel<2><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, epi);
-        else gemm_f64_skinny_kernel<4><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, epi);
+        const int nct = int(ceil_div(N, SK_NC));
+        // split K over enough CTAs to keep ~4 per SM streaming (a lone 32-column
+        // CTA per SM cannot keep the HBM busy); PARITY_EXACT keeps one k chain
+        // per output (bit-exact with vec_mat)
+        int ks = exact ? 1 : int(std::min<int64_t>(ceil_div(4 * kNumSMs, nct), std::max(1, K / 512)));
+        const int kchunk = int(ceil_div(ceil_div(K, ks), SK_KB) * SK_KB);
+        ks = int(ceil_div(K, kchunk));
+        double* part = ks > 1 ? f64_splitk_workspace(sizeof(double) * size_t(ks) * M * N, st) : nullptr;
+        const dim3 grid{unsigned(nct), unsigned(ks), 1u};
+        if (M <= 8) gemm_f64_skinny_kernel<1><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, kchunk, part, epi);
+        else if (M <= 16) gemm_f64_skinny_kernel<2><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, kchunk, part, epi);
+        else gemm_f64_skinny_kernel<4><<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, kchunk, part, epi);
         KEEP_LAUNCH_CHECK();
+        if (ks > 1) {
+            f64_splitk_finish_kernel<<<unsigned(std::min<int64_t>(ceil_div(int64_t(M) * N, 256), kNumSMs * 4)), 256, 0,
+                                       st>>>(part, ks, M, N, epi);
+            KEEP_LAUNCH_CHECK();
+        }
         return;
     }
     dim3 grid(static_cast<unsigned>(ceil_div(N, BN)), static_cast<unsigned>(ceil_div(M, BM)));

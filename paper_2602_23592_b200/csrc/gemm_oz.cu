@@ -592,13 +592,14 @@ void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb,
 void launch_gemm_parity(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
                         const EpiArgs& epi, cudaStream_t st, OzWork& w, bool exact, int max_ctas) {
     if (!exact && ozaki_eligible(M, N, K) && (epi.kind != EPI_QKV || epi.d % 32 == 0)) launch_gemm_ozaki(A, lda, B, ldb, M, N, K, epi, st, w, max_ctas);
-    else launch_gemm_f64acc(A, lda, B, ldb, M, N, K, epi, st);
+    else launch_gemm_f64acc(A, lda, B, ldb, M, N, K, epi, st, exact);
 }
 
 }  // namespace keep_b200
 
 // Test hook: C = A . B on device pointers (fp32 [M x K] . [K x N] -> fp32),
-// mode 0 auto, 1 Ozaki, 2 DFMA.
+// mode 0 auto, 1 Ozaki, 2 DFMA one k chain per output (PARITY_EXACT: vec_mat's
+// order), 3 DFMA with the few-row split-K (PARITY).
 extern "C" int keep_debug_gemm_parity(const float* A, const float* B, float* Cout, int M, int N, int K, int mode) {
     try {
         keep_b200::EpiArgs e{keep_b200::EPI_STORE, 0, Cout, N, nullptr, nullptr, nullptr, nullptr};
@@ -606,7 +607,7 @@ extern "C" int keep_debug_gemm_parity(const float* A, const float* B, float* Cou
         if (mode == 1 || (mode == 0 && keep_b200::ozaki_eligible(M, N, K)))
             keep_b200::launch_gemm_ozaki(A, K, B, N, M, N, K, e, 0, w, keep_b200::kNumSMs);
         else
-            keep_b200::launch_gemm_f64acc(A, K, B, N, M, N, K, e, 0);
+            keep_b200::launch_gemm_f64acc(A, K, B, N, M, N, K, e, 0, mode == 2);
         return cudaDeviceSynchronize() == cudaSuccess ? 0 : KEEP_ERR_CUDA;
     } catch (const keep_b200::KeepError& e) {
         return e.code;

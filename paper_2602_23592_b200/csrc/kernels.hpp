@@ -97,7 +97,7 @@ struct EpiArgs {
     float q_scale = 1.f;      // QKV (FAST): q is stored as bf16(q * q_scale)
 };
 void launch_gemm_f64acc(const float* A, int64_t lda, const float* B, int64_t ldb, int M, int N, int K,
-                        const EpiArgs& epi, cudaStream_t st);
+                        const EpiArgs& epi, cudaStream_t st, bool exact = false);
 
 // ------------------------------------------------------- attention family --
 // Causal attention of compact rows against the merged KV of one layer, with
@@ -141,6 +141,8 @@ void launch_attention_parity(const AttnArgs& a, cudaStream_t st);
 bool attention_dmma_fits(int dh);
 bool parity_attention_dmma(int dh);
 int attention_dmma_rows_per_tile();
+// few rows without a summary: the key-split fp64 decode kernel (its own split target)
+bool attention_f64_decode(int n, int dh, bool with_bins);
 void launch_attention_parity_dmma(const AttnArgs& a, cudaStream_t st);
 void launch_stats_combine(const AttnArgs& a, cudaStream_t st);
 void launch_ctx_combine(const AttnArgs& a, cudaStream_t st);
