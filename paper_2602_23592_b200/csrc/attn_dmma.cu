@@ -27,8 +27,10 @@
 //          row sums over the keys of each destination segment
 //          (prefill.hpp:281-288) -> rowbin, reduced by K6.
 #include <cfloat>
+#include <cstdlib>
 
 #include "kernels.hpp"
+#include "tc_common.cuh"
 
 namespace keep_b200 {
 
@@ -46,6 +48,29 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                  : "+d"(c[0]), "+d"(c[1])
                  : "d"(a), "d"(b));
+}
+
+// four independent m8n8k4 accumulations in ONE asm statement: the compiler
+// may not reorder them into a dependent chain (left to itself it emitted the
+// 32 k-steps of each score tile back to back into one accumulator, so every
+// DMMA waited for the previous one's result)
+__device__ __forceinline__ void dmma4(double (&c)[4][2], double a, double b0, double b1, double b2, double b3) {
+    asm volatile(
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%8}, {%9}, {%0, %1};\n\t"
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%2, %3}, {%8}, {%10}, {%2, %3};\n\t"
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%4, %5}, {%8}, {%11}, {%4, %5};\n\t"
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%6, %7}, {%8}, {%12}, {%6, %7};"
+        : "+d"(c[0][0]), "+d"(c[0][1]), "+d"(c[1][0]), "+d"(c[1][1]), "+d"(c[2][0]), "+d"(c[2][1]), "+d"(c[3][0]),
+          "+d"(c[3][1])
+        : "d"(a), "d"(b0), "d"(b1), "d"(b2), "d"(b3));
+}
+
+// fp32 -> fp64 at the point of use (volatile: not hoisted out of the key loop,
+// where 32 widened Q fragments would take 64 registers)
+__device__ __forceinline__ double widen_here(float x) {
+    double r;
+    asm volatile("cvt.f64.f32 %0, %1;" : "=d"(r) : "f"(x));
+    return r;
 }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool ok) {
@@ -129,10 +154,16 @@ __device__ __forceinline__ void scores(const QT (&qa)[DH / 4], const double* ks,
     constexpr int NJ = NJ_;
 #pragma unroll
     for (int j = 0; j < NJ; ++j) s[j][0] = s[j][1] = 0.0;
+    static_assert(NJ % 4 == 0, "score tiles in groups of four");
 #pragma unroll
     for (int i = 0; i < DH / 4; ++i) {
+        const double qd = double(qa[i]);
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma(s[j], double(qa[i]), ks[(8 * j + g) * Geo<DH>::P64 + 4 * i + t]);
+        for (int j = 0; j < NJ; j += 4) {
+            const double* kb = ks + (8 * j + g) * Geo<DH>::P64 + 4 * i + t;
+            dmma4(*reinterpret_cast<double(*)[4][2]>(&s[j][0]), qd, kb[0], kb[8 * Geo<DH>::P64],
+                  kb[16 * Geo<DH>::P64], kb[24 * Geo<DH>::P64]);
+        }
     }
     // s = dot * scale rounded on its own (prefill.hpp:140): no FMA contraction
     // with the later s - max, which at depth (|s| ~ 1e18, ulp ~ 1e2) would move
@@ -416,6 +447,271 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_bins_kernel(AttnArgs a, doub
     if (threadIdx.x < nrows && cur >= 0) rowbin[int64_t(i0 + threadIdx.x) * a.S + cur] = run;
 }
 
+// --------------------------------------------------- warp-specialised --
+// The same three modes with the key stream decoupled from the math (the
+// kernel above stalls the DMMA pipe while every warp widens the next chunk
+// between two __syncthreads; ncu: tensor pipe 63-66%).  Four producer warps
+// load fp32 K / V rows with 16-byte loads (issued before they wait for a free
+// slot, so the HBM / L2 latency overlaps), widen them to fp64 and store them
+// into a 3-stage ring of 32-key slots; eight consumer warps (8 rows each) run
+// Q.K^T, the softmax and P.V on DMMA, synchronised only by mbarriers
+// (full: 128 producer arrivals; empty: 8 consumer arrivals), so one warp's
+// softmax overlaps another's MMAs.
+constexpr int WS_CW = 8;                   // consumer warps
+constexpr int WS_PW = 4;                   // producer warps
+constexpr int WS_THREADS = (WS_CW + WS_PW) * 32;
+constexpr int WS_ROWS = WS_CW * 8;         // compact rows per CTA
+constexpr int WS_KC = 32;                  // keys per slot
+constexpr int WS_ST = 3;                   // ring slots
+template <int DH>
+struct WsGeo {
+    static constexpr int PK = DH + 4, PV = DH + 2;  // fp64 row strides (conflict-free fragments)
+    static constexpr int KD = WS_KC * PK, VD = WS_KC * PV;
+    static constexpr size_t slot(bool with_v) { return sizeof(double) * (KD + (with_v ? VD : 0)); }
+    static constexpr size_t smem(bool with_v) { return WS_ST * slot(with_v) + 2 * WS_ST * sizeof(uint64_t) + 16; }
+};
+
+template <int DH, int MODE>
+__global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a, double scale) {
+    using G = WsGeo<DH>;
+    constexpr bool WV = MODE != M_STATS;
+    extern __shared__ __align__(16) double smd[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smd + WS_ST * (G::KD + (WV ? G::VD : 0)));
+    uint64_t* empty = full + WS_ST;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = blockIdx.x * WS_ROWS;
+    const int h = blockIdx.y, sp = blockIdx.z;
+    const int off = h * DH;
+    const int nrows = min(WS_ROWS, a.n - i0);
+    const int tmax = a.rows[i0 + nrows - 1];
+    const int klo0 = a.key_lo ? a.key_lo[a.rows[i0]] : 0;
+    const int lo = max(a.split_lo[sp], klo0), hi = min(a.split_hi[sp], tmax + 1);
+    const int nchunks = lo < hi ? int(ceil_div(hi - lo, WS_KC)) : 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < WS_ST; ++s) {
+            tc::mbar_init(&full[s], WS_PW * 32);
+            tc::mbar_init(&empty[s], WS_CW);
+        }
+        tc::fence_barrier_init();
+    }
+    __syncthreads();
+    auto kslot = [&](int s) { return smd + s * (G::KD + (WV ? G::VD : 0)); };
+
+    if (warp < WS_PW) {  // ---------------- producers: fp32 rows -> fp64 slots
+        constexpr int V4 = DH / 4;                       // float4 per key row
+        constexpr int PER = WS_KC * V4 / (WS_PW * 32);   // float4 of K (and of V) per thread per slot
+        const float* kg = static_cast<const float*>(a.k);
+        const float* vg = static_cast<const float*>(a.v);
+        const int pt = threadIdx.x;
+        for (int c = 0; c < nchunks; ++c) {
+            const int s = c % WS_ST;
+            const int k0 = lo + c * WS_KC;
+            float4 kr[PER], vr[WV ? PER : 1];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = pt + i * WS_PW * 32, r = e / V4, q = e % V4;
+                const bool ok = k0 + r < hi;
+                const int64_t g = int64_t(ok ? k0 + r : lo) * a.d + off + 4 * q;
+                kr[i] = ok ? *reinterpret_cast<const float4*>(kg + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (WV) vr[i] = ok ? *reinterpret_cast<const float4*>(vg + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            tc::mbar_wait(&empty[s], ((c / WS_ST) & 1) ^ 1);
+            double* kd = kslot(s);
+            double* vd = kd + G::KD;
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int e = pt + i * WS_PW * 32, r = e / V4, q = e % V4;
+                double2* ko = reinterpret_cast<double2*>(kd + r * G::PK + 4 * q);
+                ko[0] = make_double2(double(kr[i].x), double(kr[i].y));
+                ko[1] = make_double2(double(kr[i].z), double(kr[i].w));
+                if (WV) {
+                    double2* vo = reinterpret_cast<double2*>(vd + r * G::PV + 4 * q);
+                    vo[0] = make_double2(double(vr[i].x), double(vr[i].y));
+                    vo[1] = make_double2(double(vr[i].z), double(vr[i].w));
+                }
+            }
+            tc::mbar_arrive(&full[s]);  // release: this thread's stores
+        }
+        return;
+    }
+    // ---------------- consumers: 8 rows per warp
+    const int cw = warp - WS_PW, g = lane >> 2, t = lane & 3;
+    const int row = i0 + cw * 8 + g;
+    const RowInfo ri = row_info(a, row);
+    float qa[DH / 4];
+    {
+        const float* q = static_cast<const float*>(a.q) + int64_t(min(row, a.n - 1)) * a.d + off;
+#pragma unroll
+        for (int i = 0; i < DH / 4; ++i) qa[i] = ri.t >= 0 ? q[4 * i + t] : 0.f;
+    }
+    double m = -DBL_MAX, l = 0.0;
+    if (MODE == M_CTX && ri.t >= 0) m = a.m_fin[int64_t(row) * a.H + h];  // the row max of every key
+    constexpr int NT = DH / 8;
+    double o_acc[NT][2];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o_acc[n][0] = o_acc[n][1] = 0.0;
+    constexpr int NJ = WS_KC / 8;
+    for (int c = 0; c < nchunks; ++c) {
+        const int s = c % WS_ST;
+        const int k0 = lo + c * WS_KC;
+        tc::mbar_wait(&full[s], (c / WS_ST) & 1);  // acquire: the producers' stores
+        const double* kd = kslot(s);
+        const double* vd = kd + G::KD;
+        double sc[NJ][2];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) sc[j][0] = sc[j][1] = 0.0;
+#pragma unroll
+        for (int i = 0; i < DH / 4; ++i) {
+            const double* kb = kd + g * G::PK + 4 * i + t;
+            dmma4(sc, widen_here(qa[i]), kb[0], kb[8 * G::PK], kb[16 * G::PK], kb[24 * G::PK]);
+        }
+
+        // s = dot * scale rounded on its own (prefill.hpp:140), as scores()
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            sc[j][0] = __dmul_rn(sc[j][0], scale);
+            sc[j][1] = __dmul_rn(sc[j][1], scale);
+        }
+        bool vis[NJ][2];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int key = k0 + 8 * j + 2 * t + e;
+                vis[j][e] = key < hi && key <= ri.t && key >= ri.klo;
+            }
+        if (MODE == M_STATS) {  // the row max only: CTX sums the exponentials against it
+            double cm = -DBL_MAX;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (vis[j][e]) cm = fmax(cm, sc[j][e]);
+            m = fmax(m, cm);
+        } else if (MODE == M_FLASH) {
+            double cm = -DBL_MAX;
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (vis[j][e]) cm = fmax(cm, sc[j][e]);
+            cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+            cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+            // lazy running max: re-based only when a score exceeds it by 2^8
+            // (e^256 ~ 1e111: no overflow of p, l or O in fp64); O / l is
+            // the same quotient for any base
+            if (cm != -DBL_MAX && (m == -DBL_MAX || cm > m + 256.0)) {
+                const double alpha = m == -DBL_MAX ? 0.0 : exp(__dsub_rn(m, cm));
+                l *= alpha;
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    o_acc[n][0] *= alpha;
+                    o_acc[n][1] *= alpha;
+                }
+                m = cm;
+            }
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    sc[j][e] = vis[j][e] ? exp(__dsub_rn(sc[j][e], m)) : 0.0;
+                    l += sc[j][e];
+                }
+        } else {  // CTX: exponentials against the final row max; l summed here
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    sc[j][e] = vis[j][e] ? exp(__dsub_rn(sc[j][e], m)) : 0.0;
+                    l += sc[j][e];
+                }
+        }
+        if (WV) {
+#pragma unroll
+            for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const double* vrow = vd + (8 * j + 2 * t + e) * G::PV + g;
+#pragma unroll
+                    for (int n = 0; n < NT; ++n) dmma(o_acc[n], sc[j][e], vrow[8 * n]);
+                }
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);
+    }
+    // per-thread partial sums of the row (its keys 2t, 2t + 1 of each tile)
+    if (MODE == M_STATS) {
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    } else {
+        l += __shfl_xor_sync(0xffffffffu, l, 1);
+        l += __shfl_xor_sync(0xffffffffu, l, 2);
+    }
+    if (ri.t < 0) return;
+    const int64_t oh = int64_t(row) * a.H + h;
+    const int64_t op = (int64_t(sp) * a.n + row) * a.H + h;
+    if (MODE == M_STATS) {
+        if (t == 0) a.m_part[op] = m;
+        return;
+    }
+    if (a.nsplit == 1) {
+        const double il = l > 0.0 ? 1.0 / l : 0.0;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            const int64_t col = off + 8 * n + 2 * t;
+            *reinterpret_cast<float2*>(a.ctx + int64_t(row) * a.d + col) =
+                make_float2(float(o_acc[n][0] * il), float(o_acc[n][1] * il));
+        }
+        if (MODE == M_CTX && t == 0) a.l_fin[oh] = l;
+        return;
+    }
+    if (t == 0) {
+        if (MODE == M_FLASH) a.m_part[op] = m;
+        a.l_part[op] = l;
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        const int64_t col = off + 8 * n + 2 * t;
+        *reinterpret_cast<double2*>(a.o_part + (int64_t(sp) * a.n + row) * a.d + col) =
+            make_double2(o_acc[n][0], o_acc[n][1]);
+    }
+}
+
+// max-only STATS splits -> m_fin
+__global__ void max_combine_kernel(AttnArgs a) {
+    const int64_t nh = int64_t(a.n) * a.H;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nh; e += int64_t(gridDim.x) * blockDim.x) {
+        double m = -DBL_MAX;
+        for (int s = 0; s < a.nsplit; ++s) m = fmax(m, a.m_part[int64_t(s) * nh + e]);
+        a.m_fin[e] = m;
+    }
+}
+
+// CTX splits (all against m_fin): l_fin = sum of the split sums, ctx = sum o / l_fin
+__global__ void ctxl_combine_kernel(AttnArgs a, int dh) {
+    const int64_t nd = int64_t(a.n) * a.d, nh = int64_t(a.n) * a.H;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nd; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t row = e / a.d;
+        const int col = int(e % a.d);
+        const int64_t o = row * a.H + col / dh;
+        double l = 0.0, acc = 0.0;
+        for (int s = 0; s < a.nsplit; ++s) {
+            l += a.l_part[int64_t(s) * nh + o];
+            acc += a.o_part[int64_t(s) * nd + e];
+        }
+        a.ctx[e] = l > 0.0 ? float(acc * (1.0 / l)) : 0.f;
+        if (col % dh == 0) a.l_fin[o] = l;
+    }
+}
+
+bool dmma_ws_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_DMMA_WS");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 // ------------------------------------------------------------ decode --
 // Few rows (<= 16: the query alone, every layer after the walk) and no
 // summary: a key-split fp64 flash decode.  The DMMA tiles would be ~90%
@@ -562,6 +858,14 @@ __global__ void __launch_bounds__(256, 2) attn_f64_decode_kernel(AttnArgs a, dou
 
 template <int DH, int MODE>
 void launch_mode_dmma(const AttnArgs& a, dim3 grid, double scale, cudaStream_t st) {
+    if constexpr (DH >= 32) if (dmma_ws_enabled()) {
+        const dim3 g2{unsigned(ceil_div(a.n, WS_ROWS)), grid.y, grid.z};
+        const int smem = int(WsGeo<DH>::smem(MODE != M_STATS));
+        smem_attr(attn_dmma_ws_kernel<DH, MODE>, smem);
+        attn_dmma_ws_kernel<DH, MODE><<<g2, WS_THREADS, smem, st>>>(a, scale);
+        KEEP_LAUNCH_CHECK();
+        return;
+    }
     const int smem = Geo<DH>::smem(MODE != M_STATS);
     smem_attr(attn_dmma_kernel<DH, MODE>, smem);
     attn_dmma_kernel<DH, MODE><<<grid, ANT, smem, st>>>(a, scale);
@@ -595,10 +899,23 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
         }
         return;
     }
-    launch_mode_dmma<DH, M_STATS>(a, grid, scale, st);
-    launch_stats_combine(a, st);
-    launch_mode_dmma<DH, M_CTX>(a, grid, scale, st);
-    if (a.nsplit > 1) launch_ctx_combine(a, st);
+    if (DH >= 32 && dmma_ws_enabled()) {
+        // max-only stats; the context pass sums the exponentials (l_fin)
+        launch_mode_dmma<DH, M_STATS>(a, grid, scale, st);
+        max_combine_kernel<<<unsigned(std::min<int64_t>(ceil_div(nh, 256), kNumSMs * 8)), 256, 0, st>>>(a);
+        KEEP_LAUNCH_CHECK();
+        launch_mode_dmma<DH, M_CTX>(a, grid, scale, st);
+        if (a.nsplit > 1) {
+            const int64_t nd = int64_t(a.n) * a.d;
+            ctxl_combine_kernel<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(a, DH);
+            KEEP_LAUNCH_CHECK();
+        }
+    } else {
+        launch_mode_dmma<DH, M_STATS>(a, grid, scale, st);
+        launch_stats_combine(a, st);
+        launch_mode_dmma<DH, M_CTX>(a, grid, scale, st);
+        if (a.nsplit > 1) launch_ctx_combine(a, st);
+    }
     (void)nh;
     const int smem = Geo<DH>::S64 * 8 + ART * (AKC + 1) * 8 + Geo<DH>::S32 * 4;
     smem_attr(attn_dmma_bins_kernel<DH>, smem);
@@ -610,7 +927,7 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
 
 bool attention_dmma_fits(int dh) { return dh == 8 || dh == 16 || dh == 32 || dh == 64 || dh == 128; }
 
-int attention_dmma_rows_per_tile() { return ART; }
+int attention_dmma_rows_per_tile() { return dmma_ws_enabled() ? WS_ROWS : ART; }
 
 bool attention_f64_decode(int n, int dh, bool with_bins) { return !with_bins && dh == 128 && n <= DROWS; }
 
