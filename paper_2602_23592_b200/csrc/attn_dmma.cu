@@ -458,17 +458,19 @@ __global__ void __launch_bounds__(ANT, 1) attn_dmma_bins_kernel(AttnArgs a, doub
 // (full: 128 producer arrivals; empty: 8 consumer arrivals), so one warp's
 // softmax overlaps another's MMAs.
 constexpr int WS_CW = 8;                   // consumer warps
-constexpr int WS_PW = 4;                   // producer warps
+constexpr int WS_PW = 4;                   // producer warps (one warpgroup)
 constexpr int WS_THREADS = (WS_CW + WS_PW) * 32;
 constexpr int WS_ROWS = WS_CW * 8;         // compact rows per CTA
 constexpr int WS_KC = 32;                  // keys per slot
-constexpr int WS_ST = 3;                   // ring slots
+constexpr int WS_ST = 2;                   // ring slots (a slot is ~8K consumer cycles: one ahead hides the loads)
 template <int DH>
 struct WsGeo {
     static constexpr int PK = DH + 4, PV = DH + 2;  // fp64 row strides (conflict-free fragments)
     static constexpr int KD = WS_KC * PK, VD = WS_KC * PV;
+    static constexpr int QP = DH + 4;               // fp64 Q row stride (A fragments like K's)
     static constexpr size_t slot(bool with_v) { return sizeof(double) * (KD + (with_v ? VD : 0)); }
-    static constexpr size_t smem(bool with_v) { return WS_ST * slot(with_v) + 2 * WS_ST * sizeof(uint64_t) + 16; }
+    static constexpr size_t qbytes = sizeof(double) * WS_ROWS * QP;
+    static constexpr size_t smem(bool with_v) { return WS_ST * slot(with_v) + qbytes + 2 * WS_ST * sizeof(uint64_t) + 16; }
 };
 
 template <int DH, int MODE>
@@ -476,7 +478,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
     using G = WsGeo<DH>;
     constexpr bool WV = MODE != M_STATS;
     extern __shared__ __align__(16) double smd[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smd + WS_ST * (G::KD + (WV ? G::VD : 0)));
+    double* qsm = smd + WS_ST * (G::KD + (WV ? G::VD : 0));  // [WS_ROWS][QP] fp64 Q of the tile
+    uint64_t* full = reinterpret_cast<uint64_t*>(qsm + WS_ROWS * G::QP);
     uint64_t* empty = full + WS_ST;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = blockIdx.x * WS_ROWS;
@@ -538,12 +541,16 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
     const int cw = warp - WS_PW, g = lane >> 2, t = lane & 3;
     const int row = i0 + cw * 8 + g;
     const RowInfo ri = row_info(a, row);
-    float qa[DH / 4];
-    {
-        const float* q = static_cast<const float*>(a.q) + int64_t(min(row, a.n - 1)) * a.d + off;
-#pragma unroll
-        for (int i = 0; i < DH / 4; ++i) qa[i] = ri.t >= 0 ? q[4 * i + t] : 0.f;
+    // Q fragments: widened once into shared memory (fp64 in registers would
+    // take 64 of them; a per-k-step cvt sat in every DMMA group's dependency
+    // chain).  Each warp stages its own 8 rows.
+    double* qw = qsm + cw * 8 * G::QP;
+    for (int e = lane; e < 8 * DH; e += 32) {
+        const int rr = e / DH, c = e % DH;
+        const int gi = i0 + cw * 8 + rr;
+        qw[rr * G::QP + c] = gi < a.n ? double(static_cast<const float*>(a.q)[int64_t(gi) * a.d + off + c]) : 0.0;
     }
+    __syncwarp();
     double m = -DBL_MAX, l = 0.0;
     if (MODE == M_CTX && ri.t >= 0) m = a.m_fin[int64_t(row) * a.H + h];  // the row max of every key
     constexpr int NT = DH / 8;
@@ -563,7 +570,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
 #pragma unroll
         for (int i = 0; i < DH / 4; ++i) {
             const double* kb = kd + g * G::PK + 4 * i + t;
-            dmma4(sc, widen_here(qa[i]), kb[0], kb[8 * G::PK], kb[16 * G::PK], kb[24 * G::PK]);
+            dmma4(sc, qw[g * G::QP + 4 * i + t], kb[0], kb[8 * G::PK], kb[16 * G::PK], kb[24 * G::PK]);
         }
 
         // s = dot * scale rounded on its own (prefill.hpp:140), as scores()
