@@ -1199,15 +1199,9 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
             launch_batch_copy(c.d_ksrc.as<const void*>(), c.d_vsrc.as<void*>(), c.d_bytes.as<int64_t>(), int(dsts.size()),
                               c.s_main);
         } else {
-            cudaMemcpyAttributes attr{};
-            attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-            size_t attr_idx = 0, fail = 0;
-            if (cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1, &fail,
-                                     c.s_main) != cudaSuccess) {
-                cudaGetLastError();
-                for (size_t k = 0; k < dsts.size(); ++k)
-                    KEEP_CUDA(cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyDefault, c.s_main));
-            }
+            // host tier (or rows not 16-byte aligned): one async copy per block
+            for (size_t k = 0; k < dsts.size(); ++k)
+                KEEP_CUDA(cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyDefault, c.s_main));
         }
         KEEP_CUDA(cudaStreamSynchronize(c.s_main));
         for (int o = 0; o < n_owners; ++o) {

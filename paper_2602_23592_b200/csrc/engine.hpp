@@ -221,7 +221,7 @@ struct Pass {
 // (261-338) online: urgent loads of a layer before its compute, loads for
 // l+1 of owners already out at l issued behind compute(l), and pre-loads of
 // owners whose members all left the plan for layers >= l+2 filling the
-// estimated compute window.  Copies are cudaMemcpyBatchAsync on a side
+// estimated compute window.  Copies are cudaMemcpyAsync (adjacent blocks merged) on a side
 // stream (copy engines, no SMs); compute(l) waits on an event (D1).
 struct Loader {
     struct Unit {

@@ -18,8 +18,8 @@
 //                  ascending (layer, owner) order while they fit the
 //                  estimated compute window of layer l (the idle-window fill,
 //                  314-333).
-//   engine     cudaMemcpyBatchAsync on the context's copy stream: copy
-//              engines, no SM time, one call per batch.
+//   engine     cudaMemcpyAsync on the context's copy stream, one call per
+//              run of adjacent blocks (merged below): copy engines, no SM time.
 // Every batch is bracketed by timing events so the realised timeline can be
 // checked against the reference's validate_timeline rules (D1, P, S).
 #include <algorithm>
@@ -140,20 +140,10 @@ void issue(Context& c, Pass& p, const std::vector<std::pair<int, int>>& items, i
     bt.a = take_event(ld);
     bt.b = take_event(ld);
     KEEP_CUDA(cudaEventRecord(bt.a, c.s_copy));
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t attr_idx = 0, fail = 0;
     {
         ProfScope ps(c.prof, KEEP_PROF_LOADER, c.s_copy, 0.0, double(bt.bytes), 0);
-        const cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr,
-                                                   &attr_idx, 1, &fail, c.s_copy);
-        if (e != cudaSuccess) {
-            // drivers without batched copies: one async copy per block
-            cudaGetLastError();
-            for (size_t k = 0; k < dsts.size(); ++k)
-                KEEP_CUDA(cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyHostToDevice, c.s_copy));
-        }
+        for (size_t k = 0; k < dsts.size(); ++k)
+            KEEP_CUDA(cudaMemcpyAsync(dsts[k], srcs[k], sizes[k], cudaMemcpyHostToDevice, c.s_copy));
     }
     KEEP_CUDA(cudaEventRecord(bt.b, c.s_copy));
     ld.batches.push_back(bt);
