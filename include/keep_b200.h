@@ -200,6 +200,11 @@ int keep_load_memory(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* o
 int keep_memory_has_current(void* ctx, keep_owner owner, uint64_t version, int32_t* out);
 int keep_invalidate(void* ctx, keep_owner owner, uint64_t new_version, uint64_t tokens);
 int keep_memory_stats_get(void* ctx, keep_memory_stats* out);
+/* Drop every block, owner version and statistic: a fresh CacheManager
+ * (cache_manager.hpp:62-66; harness.hpp:490-497 builds one per episode). */
+int keep_memory_clear(void* ctx);
+/* dims[7] = {num_layers, num_heads, model_dim, mlp_dim, vocab_size, numerics, world_size} */
+int keep_ctx_dims(void* ctx, int32_t* dims);
 /* Copy one block back to the host as fp32 (tests): [tokens x row_elems]. */
 int keep_memory_read(void* ctx, keep_owner owner, int32_t layer, float* keys, float* values);
 

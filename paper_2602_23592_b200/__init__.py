@@ -175,10 +175,14 @@ def load_library() -> C.CDLL:
 
 
 def exported_symbols() -> List[str]:
-    """Function names declared by include/keep_b200.h."""
+    """Function names declared by the C-ABI headers (include/keep_b200.h,
+    include/keep_episode.h)."""
+    import glob
     import re
-    with open(HEADER) as f:
-        src = f.read()
+    src = ""
+    for h in sorted(glob.glob(os.path.join(os.path.dirname(HEADER), "*.h"))):
+        with open(h) as f:
+            src += f.read()
     return sorted(set(re.findall(r"\b(keep_[a-z_]+)\s*\(", src)))
 
 

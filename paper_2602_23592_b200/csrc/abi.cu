@@ -2055,6 +2055,27 @@ int keep_invalidate(void* ctx, keep_owner owner, uint64_t new_version, uint64_t 
     });
 }
 
+int keep_memory_clear(void* ctx) {
+    return guard([&] {  // a fresh CacheManager (harness.hpp:490-497 builds one per episode)
+        Context& c = *C(ctx);
+        KEEP_CUDA(cudaDeviceSynchronize());
+        ++c.store_gen;
+        c.alias_arena = nullptr;
+        c.alias_hold.reset();
+        c.store.clear();
+        c.current_version.clear();
+        c.stats = keep_memory_stats{};
+    });
+}
+
+int keep_ctx_dims(void* ctx, int32_t* dims) {
+    return guard([&] {
+        const Context& c = *C(ctx);
+        const int32_t v[7] = {c.L, c.H, c.d, c.f, c.V, c.cfg.numerics, c.cfg.world_size};
+        std::copy(v, v + 7, dims);
+    });
+}
+
 int keep_memory_stats_get(void* ctx, keep_memory_stats* out) {
     return guard([&] {
         Context& c = *C(ctx);
