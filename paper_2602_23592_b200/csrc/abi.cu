@@ -562,6 +562,25 @@ void layer_attention(Context& c, Pass& p, int l, const void* q, void* ctx, const
     a.l_fin = p.l_fin.as<double>();
     a.o_part = p.o_part.as<double>();
     a.rowbin = p.rowbin.p;
+    a.ebin = nullptr;
+    a.seg_start = p.d_seg_start.as<int32_t>();
+    a.Tm = p.Tm;
+    if (!c.fast && !c.exact && p.with_summary && !p.block_diag && parity_attention_dmma(c.dh) &&
+        dmma_fused_bins(c.dh)) {
+        // per-head segment sums of the fused bins: fp64 [H x n x S], grown only
+        // while the device keeps 4 GB free (else the separate bins pass)
+        const size_t need = sizeof(double) * size_t(c.Hl) * n * size_t(p.S);
+        bool fits = need <= p.ebin.bytes;
+        if (!fits) {
+            size_t fr = 0, tot = 0;
+            KEEP_CUDA(cudaMemGetInfo(&fr, &tot));
+            fits = need + (size_t(4) << 30) <= fr + p.ebin.bytes;
+        }
+        if (fits) {
+            p.ebin.ensure(need);
+            a.ebin = p.ebin.as<double>();
+        }
+    }
 
     const double pairs = visible_pairs(p);
     // algorithmic attention: QK^T and PV over visible keys; K+V of the layer read once
@@ -847,6 +866,7 @@ void pass_layout(Context& c, Pass& p, const std::vector<int32_t>& seg_len, int q
     cudaStream_t st = c.s_main;
     upload(p.d_row_seg, p.row_seg, st);
     upload(p.d_seg_len, p.seg_len, st);
+    upload(p.d_seg_start, p.seg_start, st);
     if (use_tc_attention(c)) {
         p.chunk_tab.ensure(32 * size_t(std::max<int64_t>(1, ceil_div(p.T, 128))));
         launch_chunk_table(p.d_row_seg.as<int32_t>(), p.T, p.chunk_tab.p, st);

@@ -473,7 +473,7 @@ struct WsGeo {
     static constexpr size_t smem(bool with_v) { return WS_ST * slot(with_v) + qbytes + 2 * WS_ST * sizeof(uint64_t) + 16; }
 };
 
-template <int DH, int MODE>
+template <int DH, int MODE, bool BINS = false>
 __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a, double scale) {
     using G = WsGeo<DH>;
     constexpr bool WV = MODE != M_STATS;
@@ -482,8 +482,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
     uint64_t* full = reinterpret_cast<uint64_t*>(qsm + WS_ROWS * G::QP);
     uint64_t* empty = full + WS_ST;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i0 = blockIdx.x * WS_ROWS;
-    const int h = blockIdx.y, sp = blockIdx.z;
+    // grid (head, row tile, split), row tiles in DESCENDING order: the causal
+    // tiles' work grows with their index, so the longest CTAs start first and
+    // the short ones fill the last wave (longest-processing-time order)
+    const int i0 = (gridDim.y - 1 - blockIdx.y) * WS_ROWS;
+    const int h = blockIdx.x, sp = blockIdx.z;
     const int off = h * DH;
     const int nrows = min(WS_ROWS, a.n - i0);
     const int tmax = a.rows[i0 + nrows - 1];
@@ -643,6 +646,55 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
                     for (int n = 0; n < NT; ++n) dmma(o_acc[n], sc[j][e], vrow[8 * n]);
                 }
         }
+        if constexpr (BINS) {
+            // summary bins of this chunk on the same DMMA: BIN = E . Z with Z
+            // the one-hot key -> destination-segment indicator (B fragment
+            // (k = t, n = g): key 8j + 2t + e belongs to local segment 8nt + g),
+            // so every product is exact and only the fp64 summation order
+            // differs from attention_row's (prefill.hpp:150-153, 281-288).
+            // Keys of one segment are consecutive: <= 32 segments per chunk.
+            const int kmem = min(hi, a.Tm);  // query keys are not summarised (prefill.hpp:283)
+            if (k0 < kmem) {
+                const int dlo = a.row_seg[k0];
+                const int dhi = a.row_seg[min(k0 + WS_KC, kmem) - 1];
+                const int nb = (dhi - dlo) / 8 + 1;
+                int kseg[NJ][2];
+#pragma unroll
+                for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int key = k0 + 8 * j + 2 * t + e;
+                        kseg[j][e] = key < kmem ? a.row_seg[key] - dlo : -1;
+                    }
+                double bacc[WS_KC / 8][2];
+#pragma unroll
+                for (int nt = 0; nt < WS_KC / 8; ++nt) {
+                    bacc[nt][0] = bacc[nt][1] = 0.0;
+                    if (nt < nb) {
+#pragma unroll
+                        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) dmma(bacc[nt], sc[j][e], kseg[j][e] == 8 * nt + g ? 1.0 : 0.0);
+                    }
+                }
+                // row g, local segments 8nt + 2t + {0, 1}: the first chunk that
+                // holds a segment's first key stores, later chunks add (the same
+                // warp, in key order; __syncwarp orders the lanes' accesses)
+                if (ri.t >= 0) {
+                    double* eb = a.ebin + (int64_t(h) * a.n + row) * a.S;
+#pragma unroll
+                    for (int nt = 0; nt < WS_KC / 8; ++nt)
+#pragma unroll
+                        for (int e2 = 0; e2 < 2; ++e2) {
+                            const int dst = dlo + 8 * nt + 2 * t + e2;
+                            if (nt < nb && dst <= dhi) {
+                                if (a.seg_start[dst] >= k0) eb[dst] = bacc[nt][e2];
+                                else eb[dst] += bacc[nt][e2];
+                            }
+                        }
+                }
+            }
+        }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&empty[s]);
     }
@@ -708,6 +760,26 @@ __global__ void ctxl_combine_kernel(AttnArgs a, int dh) {
         }
         a.ctx[e] = l > 0.0 ? float(acc * (1.0 / l)) : 0.f;
         if (col % dh == 0) a.l_fin[o] = l;
+    }
+}
+
+// fused bins -> rowbin: prob_mean summed over the heads in order,
+// rowbin[row][dst] = sum_h ebin[h][row][dst] * (1 / l_h) / H, for the entries
+// the summary reads (dst < the row's own segment; every dst for query rows)
+__global__ void ebin_reduce_kernel(AttnArgs a) {
+    const int64_t nS = int64_t(a.n) * a.S;
+    double* rowbin = static_cast<double*>(a.rowbin);
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nS; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t row = e / a.S;
+        const int dst = int(e % a.S);
+        const int src = a.row_seg[a.rows[row]];
+        if (src >= 0 && dst >= src) continue;
+        double acc = 0.0;
+        for (int h = 0; h < a.H; ++h) {
+            const double l = a.l_fin[row * a.H + h];
+            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(a.ebin[int64_t(h) * nS + e], 1.0 / l), a.inv_heads));
+        }
+        rowbin[e] = acc;
     }
 }
 
@@ -866,7 +938,7 @@ __global__ void __launch_bounds__(256, 2) attn_f64_decode_kernel(AttnArgs a, dou
 template <int DH, int MODE>
 void launch_mode_dmma(const AttnArgs& a, dim3 grid, double scale, cudaStream_t st) {
     if constexpr (DH >= 32) if (dmma_ws_enabled()) {
-        const dim3 g2{unsigned(ceil_div(a.n, WS_ROWS)), grid.y, grid.z};
+        const dim3 g2{grid.y, unsigned(ceil_div(a.n, WS_ROWS)), grid.z};
         const int smem = int(WsGeo<DH>::smem(MODE != M_STATS));
         smem_attr(attn_dmma_ws_kernel<DH, MODE>, smem);
         attn_dmma_ws_kernel<DH, MODE><<<g2, WS_THREADS, smem, st>>>(a, scale);
@@ -911,11 +983,27 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
         launch_mode_dmma<DH, M_STATS>(a, grid, scale, st);
         max_combine_kernel<<<unsigned(std::min<int64_t>(ceil_div(nh, 256), kNumSMs * 8)), 256, 0, st>>>(a);
         KEEP_LAUNCH_CHECK();
-        launch_mode_dmma<DH, M_CTX>(a, grid, scale, st);
+        if (a.ebin) {  // bins fused into the context pass
+            if constexpr (DH >= 32) {
+                const dim3 g2{grid.y, unsigned(ceil_div(a.n, WS_ROWS)), grid.z};
+                const int smem = int(WsGeo<DH>::smem(true));
+                smem_attr(attn_dmma_ws_kernel<DH, M_CTX, true>, smem);
+                attn_dmma_ws_kernel<DH, M_CTX, true><<<g2, WS_THREADS, smem, st>>>(a, scale);
+                KEEP_LAUNCH_CHECK();
+            }
+        } else {
+            launch_mode_dmma<DH, M_CTX>(a, grid, scale, st);
+        }
         if (a.nsplit > 1) {
             const int64_t nd = int64_t(a.n) * a.d;
             ctxl_combine_kernel<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(a, DH);
             KEEP_LAUNCH_CHECK();
+        }
+        if (a.ebin) {
+            const int64_t nS = int64_t(a.n) * a.S;
+            ebin_reduce_kernel<<<unsigned(std::min<int64_t>(ceil_div(nS, 256), kNumSMs * 16)), 256, 0, st>>>(a);
+            KEEP_LAUNCH_CHECK();
+            return;
         }
     } else {
         launch_mode_dmma<DH, M_STATS>(a, grid, scale, st);
@@ -935,6 +1023,14 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
 bool attention_dmma_fits(int dh) { return dh == 8 || dh == 16 || dh == 32 || dh == 64 || dh == 128; }
 
 int attention_dmma_rows_per_tile() { return dmma_ws_enabled() ? WS_ROWS : ART; }
+
+bool dmma_fused_bins(int dh) {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_FUSED_BINS");  // A/B knob: 0 = the separate bins pass
+        return !(e && *e == '0');
+    }();
+    return on && dh >= 32 && dmma_ws_enabled();
+}
 
 bool attention_f64_decode(int n, int dh, bool with_bins) { return !with_bins && dh == 128 && n <= DROWS; }
 

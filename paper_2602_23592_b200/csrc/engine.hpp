@@ -189,7 +189,8 @@ struct Pass {
     bool block_diag = false;
     std::vector<int32_t> seg_start, seg_len, row_seg;  // host copies
     std::vector<int32_t> key_lo_h;
-    DevBuf d_tokens, d_row_seg, d_key_lo, d_seg_len;
+    DevBuf d_tokens, d_row_seg, d_key_lo, d_seg_len, d_seg_start;
+    DevBuf ebin;                  // PARITY fused bins: [H x n x S] fp64 per-head segment sums
     // compact state
     std::vector<int32_t> rows_h;  // compact -> global row, ascending
     int n = 0;

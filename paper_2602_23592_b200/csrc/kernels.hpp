@@ -134,6 +134,12 @@ struct AttnArgs {
     float* ctx;      // [n x d] fp32 output (PARITY)
     __nv_bfloat16* ctx_bf16;  // [n x d] (FAST)
     void* rowbin;    // [n x S] fp64 (PARITY) / fp32 (FAST)
+    // PARITY DMMA, bins fused into the context pass: per head, row and
+    // destination segment the unnormalised sum of e = exp(s - m) over the
+    // segment's keys ([H x n x S] fp64; nullptr: the separate bins pass)
+    double* ebin;
+    const int32_t* seg_start;  // [S] first key of each segment
+    int Tm;                    // first query key (keys >= Tm have row_seg -1)
 };
 void launch_attention_parity(const AttnArgs& a, cudaStream_t st);
 // PARITY on the fp64 tensor cores (attn_dmma.cu): head_dim 8 / 16 / 32 / 64 / 128,
@@ -141,6 +147,8 @@ void launch_attention_parity(const AttnArgs& a, cudaStream_t st);
 bool attention_dmma_fits(int dh);
 bool parity_attention_dmma(int dh);
 int attention_dmma_rows_per_tile();
+// summary bins fused into the warp-specialised context pass (needs AttnArgs::ebin)
+bool dmma_fused_bins(int dh);
 // few rows without a summary: the key-split fp64 decode kernel (its own split target)
 bool attention_f64_decode(int n, int dh, bool with_bins);
 void launch_attention_parity_dmma(const AttnArgs& a, cudaStream_t st);

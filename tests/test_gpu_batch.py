@@ -56,6 +56,38 @@ def test_batch_parity_matches_single(seed, S, L, H, d, B, groups, r_avg):
     assert len({round(g["ttft_ms"], 9) for g in batch}) == 1  # one device time for the batch
 
 
+@pytest.mark.parametrize("seed,S,L,H,d,B,groups,r_avg", [
+    (5, 16, 4, 4, 32, 3, False, 0.5), (8, 60, 6, 4, 64, 4, True, 0.3), (9, 48, 3, 2, 256, 3, True, 0.5),
+    (10, 120, 3, 1, 128, 4, True, 0.4),
+])
+def test_batch_parity_matches_oracle(ko, seed, S, L, H, d, B, groups, r_avg):
+    """Every query of a PARITY batch against the CPU oracle's own plan_keep
+    (recompute.hpp:140-180) on that query: selections bit-exact, summaries
+    within the fp64 summation-order tolerance, hidden states within 2e-6
+    (head_dim 128 rows: the Ozaki / DMMA kernels with the fused bins)."""
+    from oracle.oracle import Problem
+    mlp, V = 2 * d, 256
+    inst = make_instance_layout(seed, S, V)
+    lay = layout(inst, S, groups)
+    units = [(u[0], u[1], 1 if u[2] == kb.GROUP else 0) for u in lay.units] if groups else []
+    Q = batch_queries(seed + 100, B, len(inst.query), V, inst.query)
+    sched = kb.ratio_schedule(L, r_avg)
+    with kb.Context(L, H, d, mlp, V, seed) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay)
+        batch = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True, summaries=True)
+    w = ko.model_init(L, H, d, mlp, V, seed)
+    for b in range(B):
+        ref = ko.plan_keep(Problem(L, H, d, mlp, V, seed, inst.seg_len, inst.tokens, Q[b], units), w, sched)
+        g = batch[b]
+        assert np.array_equal(g["plan"], ref["plan"]), b
+        assert g["orders"] == ref["orders"] and np.array_equal(g["hops"], ref["hops"]), b
+        assert float(np.max(np.abs(g["qts"] - ref["qts"]))) <= 1e-12, b
+        assert float(np.max(np.abs(g["sts"] - ref["sts"]))) <= 1e-12, b
+        scale = float(np.max(np.abs(ref["final_hidden"])))
+        assert float(np.max(np.abs(g["final_hidden"].astype(np.float64) - ref["final_hidden"]))) <= 2e-6 * scale, b
+
+
 def test_batch_fast_tc_matches_single():
     # head_dim 128: tensor-core attention, decode kernel on the query-only layers
     seed, S, L, H, d, V, B = 31, 50, 6, 2, 256, 512, 4
