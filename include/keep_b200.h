@@ -334,6 +334,8 @@ int keep_debug_gemm_bf16(const void* A, const void* Bt, float* C, int M, int N, 
  * the PARITY GEMM: mode 0 automatic, 1 the Ozaki int8 tensor-core GEMM,
  * 2 the DFMA (vec_mat bit-exact) kernel. */
 int keep_debug_gemm_parity(const float* A, const float* B, float* C, int M, int N, int K, int mode);
+/* Test hook: y[i] = the PARITY softmax's fp64 exp (f64_exp.cuh) of x[i], device pointers. */
+int keep_debug_exp_f64(const double* x, double* y, int64_t n);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

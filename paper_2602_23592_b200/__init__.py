@@ -157,6 +157,7 @@ def load_library() -> C.CDLL:
         "keep_set_rope": (C.c_int, [vp, C.c_double]),
         "keep_timeline_trace": (C.c_int, [vp, C.POINTER(keep_timeline_event), i32, i32p, dp]),
         "keep_debug_gemm_parity": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+        "keep_debug_exp_f64": (C.c_int, [vp, vp, i64]),
         "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
         "keep_loader_trace": (C.c_int, [vp, C.POINTER(keep_load_record), i32, i32p]),
         "keep_shard_heads": (C.c_int, [i32, i32, i32, i32, i32p, i32p, i32p, i32p]),

@@ -29,6 +29,7 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include "f64_exp.cuh"
 #include "kernels.hpp"
 #include "tc_common.cuh"
 
@@ -462,6 +463,7 @@ constexpr int WS_PW = 4;                   // producer warps (one warpgroup)
 constexpr int WS_THREADS = (WS_CW + WS_PW) * 32;
 constexpr int WS_ROWS = WS_CW * 8;         // compact rows per CTA
 constexpr int WS_KC = 32;                  // keys per slot
+constexpr bool QK_SPLIT = true;           // Q.K^T over two dimension halves (8 DMMA chains per warp)
 constexpr int WS_ST = 2;                   // ring slots (a slot is ~8K consumer cycles: one ahead hides the loads)
 template <int DH>
 struct WsGeo {
@@ -470,7 +472,9 @@ struct WsGeo {
     static constexpr int QP = DH + 4;               // fp64 Q row stride (A fragments like K's)
     static constexpr size_t slot(bool with_v) { return sizeof(double) * (KD + (with_v ? VD : 0)); }
     static constexpr size_t qbytes = sizeof(double) * WS_ROWS * QP;
-    static constexpr size_t smem(bool with_v) { return WS_ST * slot(with_v) + qbytes + 2 * WS_ST * sizeof(uint64_t) + 16; }
+    static constexpr size_t smem(bool with_v) {
+        return WS_ST * slot(with_v) + qbytes + 64 * sizeof(double) + 2 * WS_ST * sizeof(uint64_t) + 16;
+    }
 };
 
 template <int DH, int MODE, bool BINS = false>
@@ -479,14 +483,17 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
     constexpr bool WV = MODE != M_STATS;
     extern __shared__ __align__(16) double smd[];
     double* qsm = smd + WS_ST * (G::KD + (WV ? G::VD : 0));  // [WS_ROWS][QP] fp64 Q of the tile
-    uint64_t* full = reinterpret_cast<uint64_t*>(qsm + WS_ROWS * G::QP);
+    double* etab = qsm + WS_ROWS * G::QP;                       // [64] 2^(j/64) for exp_f64
+    uint64_t* full = reinterpret_cast<uint64_t*>(etab + 64);
     uint64_t* empty = full + WS_ST;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // grid (head, row tile, split), row tiles in DESCENDING order: the causal
-    // tiles' work grows with their index, so the longest CTAs start first and
-    // the short ones fill the last wave (longest-processing-time order)
-    const int i0 = (gridDim.y - 1 - blockIdx.y) * WS_ROWS;
-    const int h = blockIdx.x, sp = blockIdx.z;
+    // grid (row tile, head, split), row tiles in DESCENDING order within a
+    // head: the causal tiles' work grows with their index, so each head's
+    // longest CTAs start first and its short ones fill in behind them, while
+    // the CTAs in flight still share one or two heads' K / V in L2 (a
+    // head-fastest order ran 10-20% slower from L2 misses)
+    const int i0 = (gridDim.x - 1 - blockIdx.x) * WS_ROWS;
+    const int h = blockIdx.y, sp = blockIdx.z;
     const int off = h * DH;
     const int nrows = min(WS_ROWS, a.n - i0);
     const int tmax = a.rows[i0 + nrows - 1];
@@ -500,6 +507,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
         }
         tc::fence_barrier_init();
     }
+    exp_tab_load(etab);
     __syncthreads();
     auto kslot = [&](int s) { return smd + s * (G::KD + (WV ? G::VD : 0)); };
 
@@ -561,6 +569,8 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
 #pragma unroll
     for (int n = 0; n < NT; ++n) o_acc[n][0] = o_acc[n][1] = 0.0;
     constexpr int NJ = WS_KC / 8;
+    double bin_carry = 0.0;  // BINS: running sum of the segment cut by the last chunk edge
+    int bin_carry_dst = -1;
     for (int c = 0; c < nchunks; ++c) {
         const int s = c % WS_ST;
         const int k0 = lo + c * WS_KC;
@@ -570,10 +580,32 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
         double sc[NJ][2];
 #pragma unroll
         for (int j = 0; j < NJ; ++j) sc[j][0] = sc[j][1] = 0.0;
+        if constexpr (QK_SPLIT && DH >= 16) {
+            // the head dimensions in two halves on separate accumulators: eight
+            // independent DMMA chains per warp instead of four (ncu: the
+            // consumers' dominant stall was the accumulator dependency), summed
+            // at the end -- an fp64 reordering of the dot product only
+            double sb[NJ][2];
 #pragma unroll
-        for (int i = 0; i < DH / 4; ++i) {
-            const double* kb = kd + g * G::PK + 4 * i + t;
-            dmma4(sc, qw[g * G::QP + 4 * i + t], kb[0], kb[8 * G::PK], kb[16 * G::PK], kb[24 * G::PK]);
+            for (int j = 0; j < NJ; ++j) sb[j][0] = sb[j][1] = 0.0;
+#pragma unroll
+            for (int i = 0; i < DH / 8; ++i) {
+                const double* kb = kd + g * G::PK + 4 * i + t;
+                const double* kc = kb + DH / 2;
+                dmma4(sc, qw[g * G::QP + 4 * i + t], kb[0], kb[8 * G::PK], kb[16 * G::PK], kb[24 * G::PK]);
+                dmma4(sb, qw[g * G::QP + DH / 2 + 4 * i + t], kc[0], kc[8 * G::PK], kc[16 * G::PK], kc[24 * G::PK]);
+            }
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                sc[j][0] = __dadd_rn(sc[j][0], sb[j][0]);
+                sc[j][1] = __dadd_rn(sc[j][1], sb[j][1]);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < DH / 4; ++i) {
+                const double* kb = kd + g * G::PK + 4 * i + t;
+                dmma4(sc, qw[g * G::QP + 4 * i + t], kb[0], kb[8 * G::PK], kb[16 * G::PK], kb[24 * G::PK]);
+            }
         }
 
         // s = dot * scale rounded on its own (prefill.hpp:140), as scores()
@@ -611,7 +643,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
             // (e^256 ~ 1e111: no overflow of p, l or O in fp64); O / l is
             // the same quotient for any base
             if (cm != -DBL_MAX && (m == -DBL_MAX || cm > m + 256.0)) {
-                const double alpha = m == -DBL_MAX ? 0.0 : exp(__dsub_rn(m, cm));
+                const double alpha = m == -DBL_MAX ? 0.0 : exp_f64(__dsub_rn(m, cm), etab);
                 l *= alpha;
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
@@ -624,7 +656,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
             for (int j = 0; j < NJ; ++j)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    sc[j][e] = vis[j][e] ? exp(__dsub_rn(sc[j][e], m)) : 0.0;
+                    sc[j][e] = vis[j][e] ? exp_f64(__dsub_rn(sc[j][e], m), etab) : 0.0;
                     l += sc[j][e];
                 }
         } else {  // CTX: exponentials against the final row max; l summed here
@@ -632,7 +664,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
             for (int j = 0; j < NJ; ++j)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    sc[j][e] = vis[j][e] ? exp(__dsub_rn(sc[j][e], m)) : 0.0;
+                    sc[j][e] = vis[j][e] ? exp_f64(__dsub_rn(sc[j][e], m), etab) : 0.0;
                     l += sc[j][e];
                 }
         }
@@ -655,8 +687,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
             // Keys of one segment are consecutive: <= 32 segments per chunk.
             const int kmem = min(hi, a.Tm);  // query keys are not summarised (prefill.hpp:283)
             if (k0 < kmem) {
+                const int kend = min(k0 + WS_KC, kmem);
                 const int dlo = a.row_seg[k0];
-                const int dhi = a.row_seg[min(k0 + WS_KC, kmem) - 1];
+                const int dhi = a.row_seg[kend - 1];
                 const int nb = (dhi - dlo) / 8 + 1;
                 int kseg[NJ][2];
 #pragma unroll
@@ -677,9 +710,25 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
                             for (int e = 0; e < 2; ++e) dmma(bacc[nt], sc[j][e], kseg[j][e] == 8 * nt + g ? 1.0 : 0.0);
                     }
                 }
-                // row g, local segments 8nt + 2t + {0, 1}: the first chunk that
-                // holds a segment's first key stores, later chunks add (the same
-                // warp, in key order; __syncwarp orders the lanes' accesses)
+                // row g holds local segments 8nt + 2t + {0, 1}.  A segment
+                // cut by the chunk edge is carried in registers (its running
+                // sum moves to the quad's t = 0 lane, local segment 0 of the
+                // next chunk); every finished segment is stored once -- no
+                // global read-modify-write in the key loop.
+                if (dlo == bin_carry_dst && t == 0) bacc[0][0] += bin_carry;
+                const int ld = dhi - dlo;
+                // bacc[ld / 8][ld % 2] without a dynamic register index (which
+                // the compiler would route through local memory): one term is 1
+                double mine = 0.0;
+#pragma unroll
+                for (int nt = 0; nt < WS_KC / 8; ++nt)
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2)
+                        mine = fma(8 * nt + e2 == (ld & ~6) ? 1.0 : 0.0, bacc[nt][e2], mine);
+                const double cval = __shfl_sync(0xffffffffu, mine, (lane & ~3) | ((ld & 7) >> 1));
+                const bool cont = kend < kmem && a.row_seg[kend] == dhi;
+                bin_carry = cval;
+                bin_carry_dst = cont ? dhi : -1;
                 if (ri.t >= 0) {
                     double* eb = a.ebin + (int64_t(h) * a.n + row) * a.S;
 #pragma unroll
@@ -687,10 +736,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
 #pragma unroll
                         for (int e2 = 0; e2 < 2; ++e2) {
                             const int dst = dlo + 8 * nt + 2 * t + e2;
-                            if (nt < nb && dst <= dhi) {
-                                if (a.seg_start[dst] >= k0) eb[dst] = bacc[nt][e2];
-                                else eb[dst] += bacc[nt][e2];
-                            }
+                            if (nt < nb && dst <= dhi && !(cont && dst == dhi)) eb[dst] = bacc[nt][e2];
                         }
                 }
             }
@@ -938,7 +984,7 @@ __global__ void __launch_bounds__(256, 2) attn_f64_decode_kernel(AttnArgs a, dou
 template <int DH, int MODE>
 void launch_mode_dmma(const AttnArgs& a, dim3 grid, double scale, cudaStream_t st) {
     if constexpr (DH >= 32) if (dmma_ws_enabled()) {
-        const dim3 g2{grid.y, unsigned(ceil_div(a.n, WS_ROWS)), grid.z};
+        const dim3 g2{unsigned(ceil_div(a.n, WS_ROWS)), grid.y, grid.z};
         const int smem = int(WsGeo<DH>::smem(MODE != M_STATS));
         smem_attr(attn_dmma_ws_kernel<DH, MODE>, smem);
         attn_dmma_ws_kernel<DH, MODE><<<g2, WS_THREADS, smem, st>>>(a, scale);
@@ -985,7 +1031,7 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
         KEEP_LAUNCH_CHECK();
         if (a.ebin) {  // bins fused into the context pass
             if constexpr (DH >= 32) {
-                const dim3 g2{grid.y, unsigned(ceil_div(a.n, WS_ROWS)), grid.z};
+                const dim3 g2{unsigned(ceil_div(a.n, WS_ROWS)), grid.y, grid.z};
                 const int smem = int(WsGeo<DH>::smem(true));
                 smem_attr(attn_dmma_ws_kernel<DH, M_CTX, true>, smem);
                 attn_dmma_ws_kernel<DH, M_CTX, true><<<g2, WS_THREADS, smem, st>>>(a, scale);
@@ -1047,3 +1093,19 @@ void launch_attention_parity_dmma(const AttnArgs& a, cudaStream_t st) {
 }
 
 }  // namespace keep_b200
+
+// Test hook: y[i] = exp_f64(x[i]) on device pointers (tests/test_gpu_exp.py).
+namespace {
+__global__ void exp_f64_probe_kernel(const double* x, double* y, int64_t n) {
+    __shared__ double tab[64];
+    keep_b200::exp_tab_load(tab);
+    __syncthreads();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        y[i] = keep_b200::exp_f64(x[i], tab);
+}
+}  // namespace
+
+extern "C" int keep_debug_exp_f64(const double* x, double* y, int64_t n) {
+    exp_f64_probe_kernel<<<296, 256>>>(x, y, n);
+    return cudaDeviceSynchronize() == cudaSuccess ? 0 : KEEP_ERR_CUDA;
+}
