@@ -571,10 +571,26 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
     constexpr int NJ = WS_KC / 8;
     double bin_carry = 0.0;  // BINS: running sum of the segment cut by the last chunk edge
     int bin_carry_dst = -1;
+    // the warp's visible key window: chunks wholly outside it (keys past its
+    // last row, or below every row's first key) are masked for all its rows,
+    // so the warp only keeps the slot ring in step (a 64-row tile spans up to
+    // ~1K key positions: ~5% of a causal layer's tile work)
+    const int w_tmax = __reduce_max_sync(0xffffffffu, ri.t);
+    const int w_klo = __reduce_min_sync(0xffffffffu, ri.t >= 0 ? ri.klo : 0x7fffffff);
     for (int c = 0; c < nchunks; ++c) {
         const int s = c % WS_ST;
         const int k0 = lo + c * WS_KC;
         tc::mbar_wait(&full[s], (c / WS_ST) & 1);  // acquire: the producers' stores
+        if (k0 > w_tmax || k0 + WS_KC <= w_klo) {
+            if constexpr (BINS) {  // a segment carried into a masked chunk is complete
+                if (bin_carry_dst >= 0 && ri.t >= 0 && t == 0)
+                    a.ebin[(int64_t(h) * a.n + row) * a.S + bin_carry_dst] = bin_carry;
+                bin_carry_dst = -1;
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&empty[s]);
+            continue;
+        }
         const double* kd = kslot(s);
         const double* vd = kd + G::KD;
         double sc[NJ][2];
