@@ -798,6 +798,310 @@ __global__ void __launch_bounds__(WS_THREADS, 1) attn_dmma_ws_kernel(AttnArgs a,
     }
 }
 
+
+// ------------------------------------------------ m16n8k16 flash pass --
+// FLASH (layers without a summary: 18 of C3's 20 recompute layers) on the
+// large fp64 MMA shape, mma.m16n8k16.f64 (4096 flops per instruction against
+// 512 for m8n8k4: 8x fewer issue slots and operand loads per flop, the
+// accumulator latency amortised over 8x the work).  A warp owns 16 rows, so
+// its O accumulator (16 x dh fp64) takes dh/2 doubles per thread; the CTA has
+// 8 consumer warps = 4 row groups x 2 key halves (each warp multiplies its
+// half -- 16 keys -- of every 32-key chunk, keeps its own online (m, l, O),
+// and the two halves merge at the end like two flash splits) and ONE
+// producer warp widening fp32 K / V rows into the 2-slot fp64 ring.
+//
+// Fragments (PTX m16n8k16 .f64, row.col; g = lane / 4, t = lane % 4):
+//   A (16 x 16): a[i] = A[g + 8 (i & 1)][t + 4 (i >> 1)]
+//   B (16 x 8):  b[i] = B[t + 4 i][g]
+//   C (16 x 8):  c[0..1] = C[g][2t + 0..1], c[2..3] = C[g + 8][2t + 0..1]
+// P.V takes the score accumulators directly as A: k-slot t + 4i holds key
+// pi(t + 4i) = {2t, 2t + 1, 8 + 2t, 9 + 2t}[i] of the warp's 16 keys -- the
+// keys this thread's S fragments already hold -- and V's B fragment reads the
+// same permuted keys, a reordering of the summation only.
+constexpr int F16_CW = 8;                  // consumer warps (4 row groups x 2 key halves): warpgroups 1-2
+constexpr int F16_PW = 4;                  // producer warps: warpgroup 0
+constexpr int F16_THREADS = (F16_CW + F16_PW) * 32;
+// registers: 384 threads launch with 168 each; the producer warpgroup gives
+// back to 40 and the consumers take 232 (setmaxnreg) for their 16-row O
+constexpr int F16_PREG = 40, F16_CREG = 232;
+constexpr int F16_ROWS = 64;
+constexpr int F16_KC = 32;                 // keys per ring slot (16 per key half)
+constexpr int F16_ST = 2;
+template <int DH>
+struct F16Geo {
+    static constexpr int PK = DH + 4, PV = DH + 2, QP = DH + 4;
+    static constexpr int KD = F16_KC * PK, VD = F16_KC * PV;
+    static constexpr size_t slot = sizeof(double) * (KD + VD);
+    static constexpr size_t smem = F16_ST * slot + sizeof(double) * (F16_ROWS * QP + 64) + 2 * F16_ST * 8 + 16;
+};
+
+__device__ __forceinline__ void dmma16(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0, %1, %2, %3}, {%4, %5, %6, %7, %8, %9, %10, %11}, "
+        "{%12, %13, %14, %15}, {%0, %1, %2, %3};"
+        : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]),
+          "d"(b[1]), "d"(b[2]), "d"(b[3]));
+}
+
+template <int DH>
+__global__ void __launch_bounds__(F16_THREADS, 1) attn_dmma16_flash_kernel(AttnArgs a, double scale) {
+    using G = F16Geo<DH>;
+    constexpr int NT = DH / 8;  // O n-tiles
+    extern __shared__ __align__(16) double smd[];
+    double* qsm = smd + F16_ST * (G::KD + G::VD);  // [F16_ROWS][QP]
+    double* etab = qsm + F16_ROWS * G::QP;
+    uint64_t* full = reinterpret_cast<uint64_t*>(etab + 64);
+    uint64_t* empty = full + F16_ST;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i0 = (gridDim.x - 1 - blockIdx.x) * F16_ROWS;  // longest tiles of a head first (see ws kernel)
+    const int h = blockIdx.y, sp = blockIdx.z;
+    const int off = h * DH;
+    const int nrows = min(F16_ROWS, a.n - i0);
+    const int tmax = a.rows[i0 + nrows - 1];
+    const int klo0 = a.key_lo ? a.key_lo[a.rows[i0]] : 0;
+    const int lo = max(a.split_lo[sp], klo0), hi = min(a.split_hi[sp], tmax + 1);
+    const int nchunks = lo < hi ? int(ceil_div(hi - lo, F16_KC)) : 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < F16_ST; ++s) {
+            tc::mbar_init(&full[s], F16_PW * 32);
+            tc::mbar_init(&empty[s], F16_CW);
+        }
+        tc::fence_barrier_init();
+    }
+    exp_tab_load(etab);
+    // Q rows of the tile, widened once (each consumer row group stages its 16 rows below)
+    __syncthreads();
+    auto kslot = [&](int s) { return smd + s * (G::KD + G::VD); };
+
+    if (warp < F16_PW) {  // ---------------- producers: fp32 rows -> fp64 slots
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(F16_PREG));
+        constexpr int V4 = DH / 4;
+        constexpr int PER = 2;                                     // float4 of K (and V) per lane per round
+        constexpr int ROUNDS = F16_KC * V4 / (F16_PW * 32 * PER);
+        const float* kg = static_cast<const float*>(a.k);
+        const float* vg = static_cast<const float*>(a.v);
+        const int pt = threadIdx.x;
+        for (int c = 0; c < nchunks; ++c) {
+            const int s = c % F16_ST;
+            const int k0 = lo + c * F16_KC;
+            double* kd = kslot(s);
+            double* vd = kd + G::KD;
+#pragma unroll 1
+            for (int rd = 0; rd < ROUNDS; ++rd) {
+                float4 kr[PER], vr[PER];
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int e = pt + (rd * PER + i) * F16_PW * 32, r = e / V4, q = e % V4;
+                    const bool ok = k0 + r < hi;
+                    const int64_t gi = int64_t(ok ? k0 + r : lo) * a.d + off + 4 * q;
+                    kr[i] = ok ? *reinterpret_cast<const float4*>(kg + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    vr[i] = ok ? *reinterpret_cast<const float4*>(vg + gi) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                if (rd == 0) tc::mbar_wait(&empty[s], ((c / F16_ST) & 1) ^ 1);
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int e = pt + (rd * PER + i) * F16_PW * 32, r = e / V4, q = e % V4;
+                    double2* ko = reinterpret_cast<double2*>(kd + r * G::PK + 4 * q);
+                    ko[0] = make_double2(double(kr[i].x), double(kr[i].y));
+                    ko[1] = make_double2(double(kr[i].z), double(kr[i].w));
+                    double2* vo = reinterpret_cast<double2*>(vd + r * G::PV + 4 * q);
+                    vo[0] = make_double2(double(vr[i].x), double(vr[i].y));
+                    vo[1] = make_double2(double(vr[i].z), double(vr[i].w));
+                }
+            }
+            tc::mbar_arrive(&full[s]);
+        }
+        return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(F16_CREG));
+    // ---------------- consumers: row group rg (16 rows), key half kh (16 keys of each chunk)
+    const int cw = warp - F16_PW;
+    const int rg = cw >> 1, kh = cw & 1, g = lane >> 2, t = lane & 3;
+    const int r0 = i0 + rg * 16;
+    const RowInfo ra = row_info(a, r0 + g), rb = row_info(a, r0 + g + 8);
+    double* qw = qsm + rg * 16 * G::QP;
+    for (int e = kh * 32 + lane; e < 16 * DH; e += 64) {  // the pair stages its 16 rows together
+        const int rr = e / DH, cc = e % DH;
+        const int gi = r0 + rr;
+        qw[rr * G::QP + cc] = gi < a.n ? double(static_cast<const float*>(a.q)[int64_t(gi) * a.d + off + cc]) : 0.0;
+    }
+    // the pair's 64 threads: Q staged before either multiplies
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + rg) : "memory");
+    const int w_tmax = __reduce_max_sync(0xffffffffu, max(ra.t, rb.t));
+    const int w_klo = __reduce_min_sync(0xffffffffu, min(ra.t >= 0 ? ra.klo : 0x7fffffff, rb.t >= 0 ? rb.klo : 0x7fffffff));
+    double ma = -DBL_MAX, mb = -DBL_MAX, la = 0.0, lb = 0.0;
+    double o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+        const int s = c % F16_ST;
+        const int kb0 = lo + c * F16_KC + kh * 16;  // this warp's 16 keys
+        tc::mbar_wait(&full[s], (c / F16_ST) & 1);
+        if (kb0 > w_tmax || kb0 + 16 <= w_klo || kb0 >= hi) {
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&empty[s]);
+            continue;
+        }
+        const double* kd = kslot(s) + kh * 16 * G::PK;
+        const double* vd = kslot(s) + G::KD + kh * 16 * G::PV;
+        // S = Q . K^T: two 8-key n-tiles, DH / 16 k-steps
+        double sc[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < DH / 16; ++ks) {
+            double qa[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) qa[i] = qw[(g + 8 * (i & 1)) * G::QP + ks * 16 + t + 4 * (i >> 1)];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                double kb[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) kb[i] = kd[(8 * j + g) * G::PK + ks * 16 + t + 4 * i];
+                dmma16(sc[j], qa, kb);
+            }
+        }
+        // scale (rounded on its own, prefill.hpp:140), visibility, lazy online max
+        double cma = -DBL_MAX, cmb = -DBL_MAX;
+        bool va[2][2], vb[2][2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int key = kb0 + 8 * j + 2 * t + e;
+                va[j][e] = key < hi && key <= ra.t && key >= ra.klo;
+                vb[j][e] = key < hi && key <= rb.t && key >= rb.klo;
+                sc[j][e] = __dmul_rn(sc[j][e], scale);
+                sc[j][2 + e] = __dmul_rn(sc[j][2 + e], scale);
+                if (va[j][e]) cma = fmax(cma, sc[j][e]);
+                if (vb[j][e]) cmb = fmax(cmb, sc[j][2 + e]);
+            }
+        cma = fmax(cma, __shfl_xor_sync(0xffffffffu, cma, 1));
+        cma = fmax(cma, __shfl_xor_sync(0xffffffffu, cma, 2));
+        cmb = fmax(cmb, __shfl_xor_sync(0xffffffffu, cmb, 1));
+        cmb = fmax(cmb, __shfl_xor_sync(0xffffffffu, cmb, 2));
+        // (re-based only when a score exceeds the running max by 2^8: e^256
+        // ~ 1e111 cannot overflow p, l or O in fp64; O / l is base-invariant)
+        if (cma != -DBL_MAX && (ma == -DBL_MAX || cma > ma + 256.0)) {
+            const double al = ma == -DBL_MAX ? 0.0 : exp_f64(__dsub_rn(ma, cma), etab);
+            la *= al;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                o[n][0] *= al;
+                o[n][1] *= al;
+            }
+            ma = cma;
+        }
+        if (cmb != -DBL_MAX && (mb == -DBL_MAX || cmb > mb + 256.0)) {
+            const double al = mb == -DBL_MAX ? 0.0 : exp_f64(__dsub_rn(mb, cmb), etab);
+            lb *= al;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                o[n][2] *= al;
+                o[n][3] *= al;
+            }
+            mb = cmb;
+        }
+        double pa[8];  // the A fragment of P.V: k-slot t + 4i = key {2t, 2t+1, 8+2t, 9+2t}[i >> 1]
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const double p0 = va[j][e] ? exp_f64(__dsub_rn(sc[j][e], ma), etab) : 0.0;
+                const double p1 = vb[j][e] ? exp_f64(__dsub_rn(sc[j][2 + e], mb), etab) : 0.0;
+                la += p0;
+                lb += p1;
+                pa[2 * (2 * j + e)] = p0;      // row g
+                pa[2 * (2 * j + e) + 1] = p1;  // row g + 8
+            }
+        // O += P . V (V rows in the same key permutation)
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            double vb4[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) vb4[i] = vd[(8 * (i >> 1) + 2 * t + (i & 1)) * G::PV + 8 * n + g];
+            dmma16(o[n], pa, vb4);
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&empty[s]);
+    }
+    la += __shfl_xor_sync(0xffffffffu, la, 1);
+    la += __shfl_xor_sync(0xffffffffu, la, 2);
+    lb += __shfl_xor_sync(0xffffffffu, lb, 1);
+    lb += __shfl_xor_sync(0xffffffffu, lb, 2);
+    // merge the two key halves of the row group (flash combine of two states)
+    // through shared memory: the ring is free once every consumer is done
+    asm volatile("bar.sync 5, %0;" ::"r"(F16_CW * 32) : "memory");
+    double* mg = smd + rg * (16 * DH + 64);  // [16][DH] O, then m[16], l[16]
+    if (kh == 1) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            *reinterpret_cast<double2*>(mg + g * DH + 8 * n + 2 * t) = make_double2(o[n][0], o[n][1]);
+            *reinterpret_cast<double2*>(mg + (g + 8) * DH + 8 * n + 2 * t) = make_double2(o[n][2], o[n][3]);
+        }
+        if (t == 0) {
+            mg[16 * DH + g] = ma;
+            mg[16 * DH + g + 8] = mb;
+            mg[16 * DH + 16 + g] = la;
+            mg[16 * DH + 16 + g + 8] = lb;
+        }
+    }
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + rg) : "memory");
+    if (kh == 1) return;
+    {
+        const double m2a = mg[16 * DH + g], m2b = mg[16 * DH + g + 8];
+        const double l2a = mg[16 * DH + 16 + g], l2b = mg[16 * DH + 16 + g + 8];
+        const double Ma = fmax(ma, m2a), Mb = fmax(mb, m2b);
+        const double wa1 = ma == -DBL_MAX ? 0.0 : exp_f64(__dsub_rn(ma, Ma), etab);
+        const double wa2 = m2a == -DBL_MAX ? 0.0 : exp_f64(__dsub_rn(m2a, Ma), etab);
+        const double wb1 = mb == -DBL_MAX ? 0.0 : exp_f64(__dsub_rn(mb, Mb), etab);
+        const double wb2 = m2b == -DBL_MAX ? 0.0 : exp_f64(__dsub_rn(m2b, Mb), etab);
+        la = la * wa1 + l2a * wa2;
+        lb = lb * wb1 + l2b * wb2;
+        ma = Ma;
+        mb = Mb;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            const double2 xa = *reinterpret_cast<const double2*>(mg + g * DH + 8 * n + 2 * t);
+            const double2 xb = *reinterpret_cast<const double2*>(mg + (g + 8) * DH + 8 * n + 2 * t);
+            o[n][0] = o[n][0] * wa1 + xa.x * wa2;
+            o[n][1] = o[n][1] * wa1 + xa.y * wa2;
+            o[n][2] = o[n][2] * wb1 + xb.x * wb2;
+            o[n][3] = o[n][3] * wb1 + xb.y * wb2;
+        }
+    }
+    // outputs of rows g (a) and g + 8 (b)
+#pragma unroll
+    for (int hr = 0; hr < 2; ++hr) {
+        const RowInfo& ri = hr ? rb : ra;
+        if (ri.t < 0) continue;
+        const int row = r0 + g + 8 * hr;
+        const double m = hr ? mb : ma, l = hr ? lb : la;
+        if (a.nsplit == 1) {
+            const double il = l > 0.0 ? 1.0 / l : 0.0;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                const int64_t col = off + 8 * n + 2 * t;
+                *reinterpret_cast<float2*>(a.ctx + int64_t(row) * a.d + col) =
+                    make_float2(float(o[n][2 * hr] * il), float(o[n][2 * hr + 1] * il));
+            }
+        } else {
+            const int64_t op = (int64_t(sp) * a.n + row) * a.H + h;
+            if (t == 0) {
+                a.m_part[op] = m;
+                a.l_part[op] = l;
+            }
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                const int64_t col = off + 8 * n + 2 * t;
+                *reinterpret_cast<double2*>(a.o_part + (int64_t(sp) * a.n + row) * a.d + col) =
+                    make_double2(o[n][2 * hr], o[n][2 * hr + 1]);
+            }
+        }
+    }
+}
+
 // max-only STATS splits -> m_fin
 __global__ void max_combine_kernel(AttnArgs a) {
     const int64_t nh = int64_t(a.n) * a.H;
@@ -843,6 +1147,14 @@ __global__ void ebin_reduce_kernel(AttnArgs a) {
         }
         rowbin[e] = acc;
     }
+}
+
+bool dmma16_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_DMMA16");  // A/B knob: 0 = the m8n8k4 flash pass
+        return !(e && *e == '0');
+    }();
+    return on;
 }
 
 bool dmma_ws_enabled() {
@@ -1032,6 +1344,18 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
         return;
     }
     if (!a.with_bins) {
+        if constexpr (DH >= 64) if (dmma16_enabled()) {
+            const dim3 g2{unsigned(ceil_div(a.n, F16_ROWS)), grid.y, grid.z};
+            smem_attr(attn_dmma16_flash_kernel<DH>, int(F16Geo<DH>::smem));
+            attn_dmma16_flash_kernel<DH><<<g2, F16_THREADS, F16Geo<DH>::smem, st>>>(a, scale);
+            KEEP_LAUNCH_CHECK();
+            if (a.nsplit > 1) {
+                const int64_t nd = int64_t(a.n) * a.d;
+                flash_combine_f64_kernel<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(a, DH);
+                KEEP_LAUNCH_CHECK();
+            }
+            return;
+        }
         launch_mode_dmma<DH, M_FLASH>(a, grid, scale, st);
         if (a.nsplit > 1) {
             const int64_t nd = int64_t(a.n) * a.d;
