@@ -946,22 +946,34 @@ __global__ void __launch_bounds__(F16_THREADS, 1) attn_dmma16_flash_kernel(AttnA
         const double* kd = kslot(s) + kh * 16 * G::PK;
         const double* vd = kslot(s) + G::KD + kh * 16 * G::PV;
         // S = Q . K^T: two 8-key n-tiles, DH / 16 k-steps
-        double sc[2][4];
+        // (m16n8k16.f64 issues as 16 dependent-in-k DMMA.8x8x4: the head
+        // dimensions go to two accumulator sets, halving the k chains)
+        double sc[2][4], sd[2][4];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.0;
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) {
-            double qa[8];
+            for (int i = 0; i < 4; ++i) sc[j][i] = sd[j][i] = 0.0;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) qa[i] = qw[(g + 8 * (i & 1)) * G::QP + ks * 16 + t + 4 * (i >> 1)];
+        for (int ks = 0; ks < DH / 32; ++ks) {
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                double kb[4];
+            for (int hv = 0; hv < 2; ++hv) {
+                const int kc = (ks + hv * DH / 32) * 16;
+                double qa[8];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) kb[i] = kd[(8 * j + g) * G::PK + ks * 16 + t + 4 * i];
-                dmma16(sc[j], qa, kb);
+                for (int i = 0; i < 8; ++i) qa[i] = qw[(g + 8 * (i & 1)) * G::QP + kc + t + 4 * (i >> 1)];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    double kb[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) kb[i] = kd[(8 * j + g) * G::PK + kc + t + 4 * i];
+                    dmma16(hv ? sd[j] : sc[j], qa, kb);
+                }
             }
         }
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) sc[j][i] = __dadd_rn(sc[j][i], sd[j][i]);
         // scale (rounded on its own, prefill.hpp:140), visibility, lazy online max
         double cma = -DBL_MAX, cmb = -DBL_MAX;
         bool va[2][2], vb[2][2];
