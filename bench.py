@@ -155,6 +155,8 @@ def ncu_traffic():
                 if k.startswith("dram__bytes_read.sum [") or k.startswith("dram__bytes_write.sum ["):
                     if v:
                         tot += float(v) * scale.get(k.split("[")[1].rstrip("]"), 1.0)
+            if not math.isfinite(tot):  # a launch ncu could not measure (replay limits)
+                continue
             acc.setdefault(name, []).append(tot)
             det = detail.setdefault(name, {"launches": 0, "ms": 0.0, "dram_pct": 0.0})
             det["launches"] += 1
@@ -166,8 +168,9 @@ def ncu_traffic():
     for k, det in detail.items():
         n = max(det["launches"], 1)
         DETAIL[k] = {"captured_launches": det["launches"], "mean_ms": det["ms"] / n,
-                     "mean_dram_pct_of_peak": det["dram_pct"] / n, "mean_dram_bytes": sum(acc[k]) / n}
-    return {k: sum(v) / len(v) for k, v in acc.items()}
+                     "mean_dram_pct_of_peak": det["dram_pct"] / n,
+                     "mean_dram_bytes": sum(acc[k]) / len(acc[k]) if acc.get(k) else None}
+    return {k: sum(v) / len(v) for k, v in acc.items() if v}
 
 
 def numerics_for(args, cfg):
@@ -540,12 +543,15 @@ def run_ours(args, cfg, rank, world, dist):
                      "per_launch_ms": g_ms / max(g_n, 1)}
         fp64_peak = extra.get("fp64_dmma_tflops") or 37.0
         a_ach = a_fl / (a_ms / 1e3) / 1e12 if a_ms > 0 else 0.0
-        attn_roof = {"kernel": "attn_dmma_kernel / attn_dmma_bins_kernel (K5, fp64 DMMA m8n8k4)", "bound": "tensor",
+        attn_roof = {"kernel": "attn_dmma16_flash_kernel (K5 flash pass, mma.m16n8k16.f64) + attn_dmma_ws_kernel "
+                               "(summary layers: max pass, context pass with the bins fused as E.Z)", "bound": "tensor",
                      "achieved": a_ach, "peak": fp64_peak, "unit": "TFLOP/s (fp64)", "frac": a_ach / fp64_peak,
-                     "traffic": traffic.get("attn_dmma_kernel"), "traffic_launches": DETAIL.get("attn_dmma_kernel"),
+                     "traffic": traffic.get("attn_dmma16_flash_kernel"),
+                     "traffic_launches": DETAIL.get("attn_dmma16_flash_kernel"),
                      "peak_source": "measured fp64 DMMA (tools/micro/fp64_peak.cu)",
-                     "note": "algorithmic FLOPs 4*d*sum(t+1) (QK^T + PV once); summary layers add a stats and "
-                             "a bins pass (Q.K^T twice more)"}
+                     "note": "algorithmic FLOPs 4*d*sum(t+1) (QK^T + PV once) over the whole attention phase; "
+                             "summary layers add a max pass (Q.K^T once more); traffic = ncu DRAM bytes of one C3 "
+                             "layer-1 flash launch (profiles/r02_ncu_dmma16_full.csv)"}
         roofs = [gemm_roof, attn_roof]
     else:
         tensor_peak = pk["bf16_tflops_sustained"]
