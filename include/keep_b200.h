@@ -34,10 +34,14 @@
  * CUDA streams; calls return after the work they report has completed.
  *
  * Numerics (keep_config.numerics):
- *   KEEP_NUMERICS_PARITY  fp32 storage, fp64 accumulation in ascending k for
- *                         every projection (tensor.hpp:31-41) and fp64
- *                         attention / softmax / summaries: selections are
- *                         bit-exact with the reference.
+ *   KEEP_NUMERICS_PARITY  fp32 storage, fp64-grade accumulation on the tensor
+ *                         cores: Ozaki-II int8 projections (exact integer
+ *                         products of 47-bit scaled operands, one rounding to
+ *                         fp32), fp64 DMMA attention / softmax / summaries.
+ *                         Selections are bit-exact with the reference.
+ *   KEEP_NUMERICS_PARITY_EXACT  projections bit-exact with vec_mat (DFMA in
+ *                         ascending k) and scores in the reference's
+ *                         dimension order: the arbiter of PARITY.
  *   KEEP_NUMERICS_FAST    bf16 operands on the sm_100a tensor cores (tcgen05)
  *                         with fp32 accumulation, fp32 residual stream, bf16
  *                         merged KV, fp32 probabilities with fp64 summary
