@@ -424,6 +424,10 @@ def run_ours(args, cfg, rank, world, dist):
     host_mem = args.memory == "host"
     tier = kb.TIER_HOST if host_mem else kb.TIER_DEVICE
     ctx.memory_compute_layout(layout, version=1, tier=tier)
+    resident = 0
+    if host_mem and args.hbm_budget_gb > 0:
+        # the capacity-bounded fast tier: the deepest layers also in HBM
+        resident = ctx.memory_residency(int(args.hbm_budget_gb * 1e9))
     t_mem = time.perf_counter() - t0
 
     def barrier():
@@ -583,6 +587,7 @@ def run_ours(args, cfg, rank, world, dist):
         ms = prof["loader"]["ms"] / n_prof
         h2d += h2d_kv  # the memory KV crosses PCIe inside every step
         loader_info = {"h2d_bytes_per_step": h2d_kv, "copy_ms_per_step": ms,
+                       "hbm_resident_bytes": resident, "hbm_budget_gb": args.hbm_budget_gb,
                        "h2d_gbs": h2d_kv / (ms * 1e6) if ms > 0 else None,
                        "items": len(tr), "preloads": sum(1 for x in tr if x["kind"] == "preload"),
                        "urgent": sum(1 for x in tr if x["kind"] == "urgent")}
@@ -789,6 +794,9 @@ def main():
     ap.add_argument("--update-steps", type=int, default=2)
     ap.add_argument("--memory", choices=["hbm", "host"], default="hbm",
                     help="memory KV resident in HBM (C2-C4) or pinned host DRAM with the K10 loader (C5-style)")
+    ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
+                    help="--memory host: keep the deepest layers of the memory KV also in HBM up to this budget "
+                         "(the capacity-bounded fast tier; keep_memory_residency)")
     ap.add_argument("--batch", type=int, default=1,
                     help="B > 1: B concurrent planning queries through keep_plan_keep_batch (one GPU)")
     args = ap.parse_args()

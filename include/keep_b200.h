@@ -207,6 +207,13 @@ int keep_memory_stats_get(void* ctx, keep_memory_stats* out);
 /* Drop every block, owner version and statistic: a fresh CacheManager
  * (cache_manager.hpp:62-66; harness.hpp:490-497 builds one per episode). */
 int keep_memory_clear(void* ctx);
+/* Capacity-bounded fast tier (CacheManager's fast_capacity_bytes,
+ * cache_manager.hpp:23-35): keep the deepest layers of every pinned-host arena
+ * also resident in HBM, as many as fit in hbm_budget_bytes (plans only shrink
+ * with depth, so deep layers reuse the most cached KV).  Those layers are
+ * then fast-tier hits and never loaded; a write to an arena drops its copy.
+ * 0 releases them. */
+int keep_memory_residency(void* ctx, uint64_t hbm_budget_bytes, uint64_t* resident_bytes);
 /* dims[7] = {num_layers, num_heads, model_dim, mlp_dim, vocab_size, numerics, world_size} */
 int keep_ctx_dims(void* ctx, int32_t* dims);
 /* Copy one block back to the host as fp32 (tests): [tokens x row_elems]. */

@@ -158,6 +158,7 @@ def load_library() -> C.CDLL:
         "keep_timeline_trace": (C.c_int, [vp, C.POINTER(keep_timeline_event), i32, i32p, dp]),
         "keep_debug_gemm_parity": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
         "keep_debug_exp_f64": (C.c_int, [vp, vp, i64]),
+        "keep_memory_residency": (C.c_int, [vp, u64, C.POINTER(C.c_uint64)]),
         "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
         "keep_loader_trace": (C.c_int, [vp, C.POINTER(keep_load_record), i32, i32p]),
         "keep_shard_heads": (C.c_int, [i32, i32, i32, i32, i32p, i32p, i32p, i32p]),
@@ -416,6 +417,13 @@ class Context:
             toks.append(np.asarray(layout.tokens[starts[b]:starts[e]]))
         if owners:
             self.memory_compute_batch(owners, [version] * len(owners), members, np.concatenate(toks), tier)
+
+    def memory_residency(self, hbm_budget_bytes: int) -> int:
+        """Keep the deepest layers of the pinned-host memory also in HBM (the
+        capacity-bounded fast tier); returns the resident bytes."""
+        out = C.c_uint64()
+        _check(self.lib.keep_memory_residency(self._h, int(hbm_budget_bytes), C.byref(out)))
+        return out.value
 
     def load_memory(self, kind, oid, layer) -> keep_kv_view:
         v = keep_kv_view()

@@ -193,7 +193,18 @@ void check_cfg(const keep_config& c) {  // ModelConfig::validate, model.hpp:28-3
 // ------------------------------------------------------------ memory store --
 uint8_t* layer_keys(const Context& c, const Payload& p, int l) {
     const int64_t sheet = p.arena->rows * c.dl * c.elem;
+    if (l >= p.arena->mirror_from)  // HBM-resident layer of a pinned-host arena
+        return static_cast<uint8_t*>(p.arena->mirror.p) + (int64_t(l - p.arena->mirror_from) * 2) * sheet +
+               p.row0 * c.dl * c.elem;
     return static_cast<uint8_t*>(p.arena->buf.p) + (int64_t(l) * 2) * sheet + p.row0 * c.dl * c.elem;
+}
+
+// a write to an arena invalidates its HBM mirror (the mirror is a read copy)
+void drop_mirror(Arena& a) {
+    if (a.mirror_from >= (1 << 30)) return;
+    KEEP_CUDA(cudaDeviceSynchronize());
+    a.mirror.release();
+    a.mirror_from = 1 << 30;
 }
 uint8_t* layer_values(const Context& c, const Payload& p, int l) {
     return layer_keys(c, p, l) + p.arena->rows * c.dl * c.elem;
@@ -937,7 +948,7 @@ void cursor_layer(Context& c, const uint8_t* active, AfterSummary&& after_summar
     std::vector<int32_t> dr, nr, rope;
     int maxr = 0;
     for (int i = 0; i < S; ++i) {
-        if (active[i] || loader_covers(c, i) || alias_l) continue;  // host-tier owners: K10 loader
+        if (active[i] || loader_covers(c, i, l) || alias_l) continue;  // host-tier owners: K10 loader
         const OwnerKey& ok = c.seg_owner[i];
         const Payload* pl = seg_block_current(c, i, l);
         if (!pl) {
@@ -1199,6 +1210,7 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
         std::vector<size_t> sizes;
         for (int o = 0; o < n_owners; ++o) {
             const Payload& old = c.store[OwnerKey{owners[o].kind, owners[o].id}];
+            drop_mirror(*old.arena);
             const size_t blk = size_t(seglen[o]) * c.dl * c.elem;
             for (int l = 0; l < c.L; ++l) {
                 dsts.push_back(layer_keys(c, old, l));
@@ -1944,6 +1956,7 @@ int keep_memory_put(void* ctx, keep_owner owner, uint64_t version, int32_t layer
             c.store[k] = std::move(pl);
         }
         Payload& pl = c.store[k];
+        drop_mirror(*pl.arena);
         // this rank's head columns of the full rows
         const int64_t dl = c.dl, c0 = int64_t(c.R) * dl;
         const size_t nel = size_t(tokens) * dl;
@@ -2028,9 +2041,9 @@ int keep_load_memory(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* o
             KEEP_CUDA(cudaEventRecord(c.ev_a, c.s_copy));
             for (int l = 0; l < c.L; ++l) {
                 if (!np.present[l]) continue;
-                KEEP_CUDA(cudaMemcpyAsync(layer_keys(c, np, l), layer_keys(c, P, l), blk, cudaMemcpyHostToDevice, c.s_copy));
-                KEEP_CUDA(cudaMemcpyAsync(layer_values(c, np, l), layer_values(c, P, l), blk, cudaMemcpyHostToDevice, c.s_copy));
-                c.stats.bytes_loaded_slow += 2 * blk;
+                KEEP_CUDA(cudaMemcpyAsync(layer_keys(c, np, l), layer_keys(c, P, l), blk, cudaMemcpyDefault, c.s_copy));
+                KEEP_CUDA(cudaMemcpyAsync(layer_values(c, np, l), layer_values(c, P, l), blk, cudaMemcpyDefault, c.s_copy));
+                if (l < P.arena->mirror_from) c.stats.bytes_loaded_slow += 2 * blk;
             }
             KEEP_CUDA(cudaEventRecord(c.ev_b, c.s_copy));
             KEEP_CUDA(cudaEventSynchronize(c.ev_b));
@@ -2088,6 +2101,38 @@ int keep_memory_clear(void* ctx) {
     });
 }
 
+int keep_memory_residency(void* ctx, uint64_t hbm_budget_bytes, uint64_t* resident_bytes) {
+    return guard([&] {  // CacheManager's capacity-bounded fast tier (cache_manager.hpp:23-35, 103-130)
+        Context& c = *C(ctx);
+        KEEP_CUDA(cudaDeviceSynchronize());
+        ++c.store_gen;
+        std::vector<Arena*> host;
+        for (auto& [k, pl] : c.store)
+            if (pl.arena->tier == KEEP_TIER_HOST &&
+                std::find(host.begin(), host.end(), pl.arena.get()) == host.end())
+                host.push_back(pl.arena.get());
+        uint64_t per_layer = 0;
+        for (Arena* a : host) {
+            drop_mirror(*a);
+            per_layer += uint64_t(2) * a->rows * c.dl * c.elem;
+        }
+        // the deepest layers first: plans only shrink with depth (monotone,
+        // prefill.hpp:95-104), so deep layers reuse the most cached KV
+        const int m = per_layer ? int(std::min<uint64_t>(uint64_t(c.L), hbm_budget_bytes / per_layer)) : 0;
+        uint64_t total = 0;
+        for (Arena* a : host) {
+            if (m == 0) break;
+            const size_t sheet2 = size_t(2) * a->rows * c.dl * c.elem;
+            a->mirror.ensure(sheet2 * m);
+            KEEP_CUDA(cudaMemcpy(a->mirror.p, static_cast<uint8_t*>(a->buf.p) + sheet2 * (c.L - m), sheet2 * m,
+                                 cudaMemcpyHostToDevice));
+            a->mirror_from = c.L - m;
+            total += sheet2 * m;
+        }
+        if (resident_bytes) *resident_bytes = total;
+    });
+}
+
 int keep_ctx_dims(void* ctx, int32_t* dims) {
     return guard([&] {
         const Context& c = *C(ctx);
@@ -2109,6 +2154,7 @@ int keep_memory_stats_get(void* ctx, keep_memory_stats* out) {
             if (std::find(seen.begin(), seen.end(), a) != seen.end()) continue;
             seen.push_back(a);
             (a->tier == KEEP_TIER_HOST ? s.host_bytes : s.device_bytes) += a->buf.bytes;
+            if (a->mirror_from < (1 << 30)) s.device_bytes += a->mirror.bytes;
         }
         *out = s;
     });

@@ -94,7 +94,7 @@ struct Pass;
 void loader_begin(Context& c, Pass& p);
 void loader_before_layer(Context& c, Pass& p, int l, const uint8_t* active);
 void loader_after_layer(Context& c, Pass& p, int l, const uint8_t* active, double est_ms);
-bool loader_covers(const Context& c, int seg);  // segment's owner is host-tier (loaded by K10)
+bool loader_covers(const Context& c, int seg, int l);  // segment's owner is host-tier and layer l not HBM-resident (loaded by K10)
 void set_last_error(const std::string& msg);
 
 // Per-phase CUDA-event timing (keep_profile_*).
@@ -166,6 +166,11 @@ struct Arena {
     int64_t used = 0;  // rows [0, used) hold owner payloads; [used, rows) are spare (query rows of aliased layers)
     int tier = KEEP_TIER_DEVICE;
     int refs = 0;
+    // pinned-host arenas: layers [mirror_from, L) also resident in HBM (the
+    // capacity-bounded fast tier, keep_memory_residency); every read of those
+    // layers goes to the mirror, and a write to the arena drops it
+    DevBuf mirror;
+    int mirror_from = 1 << 30;
 };
 
 struct OwnerKey {
@@ -248,6 +253,7 @@ struct Loader {
     std::vector<uint8_t> loaded;      // [L][units]
     std::vector<int> out_from;        // per unit: first layer all members are out (INT32_MAX: not yet)
     std::vector<uint8_t> seg_host;    // per layout segment: owner is host-tier (loaded here)
+    std::vector<int> seg_mirror_from; // per layout segment: first HBM-resident layer of its owner
     std::vector<int> last_batch;      // per layer: last batch that carried one of its items (-1: none)
     std::vector<Batch> batches;
     std::vector<Rec> recs;

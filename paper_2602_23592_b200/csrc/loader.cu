@@ -180,9 +180,9 @@ Loader::~Loader() {
     if (t0) cudaEventDestroy(t0);
 }
 
-bool loader_covers(const Context& c, int seg) {
+bool loader_covers(const Context& c, int seg, int l) {
     const Loader& ld = c.loader;
-    return ld.on && ld.seg_host[seg];
+    return ld.on && ld.seg_host[seg] && l < ld.seg_mirror_from[seg];
 }
 
 void loader_begin(Context& c, Pass& p) {
@@ -222,12 +222,19 @@ void loader_begin(Context& c, Pass& p) {
     ld.any_host = false;
     for (const auto& u : ld.units) ld.any_host |= u.pl->arena->tier == KEEP_TIER_HOST;
     ld.seg_host.assign(p.S, 0);
+    ld.seg_mirror_from.assign(p.S, INT_MAX);
     for (const auto& u : ld.units)
-        for (int k = u.b; k < u.e; ++k) ld.seg_host[k] = 1;
+        for (int k = u.b; k < u.e; ++k) {
+            ld.seg_host[k] = 1;
+            ld.seg_mirror_from[k] = std::min(u.pl->arena->mirror_from, c.L);
+        }
     if (!ld.on) return;
     // (sort by owner so ascending (layer, owner) order = the reference's item order)
     std::sort(ld.units.begin(), ld.units.end(), [](const Loader::Unit& a, const Loader::Unit& b) { return a.key < b.key; });
     ld.loaded.assign(size_t(c.L) * ld.units.size(), 0);
+    for (size_t ui = 0; ui < ld.units.size(); ++ui)  // HBM-resident layers: fast tier, nothing to load
+        for (int l = std::min(ld.units[ui].pl->arena->mirror_from, c.L); l < c.L; ++l)
+            ld.loaded[size_t(l) * ld.units.size() + ui] = 1;
     ld.out_from.assign(ld.units.size(), INT32_MAX);
     ld.last_batch.assign(c.L, -1);
     if (ld.comp_start.size() != size_t(c.L)) {

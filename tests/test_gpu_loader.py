@@ -164,3 +164,41 @@ def test_reference_validate_timeline_on_device_trace(kr, numerics):
     assert "D1" in kr.validate_timeline(res["plan"], lay.seg_len, len(inst.query), units, slow, frac, late)
     dup = evs + [dict(load)]
     assert "P" in kr.validate_timeline(res["plan"], lay.seg_len, len(inst.query), units, slow, frac, dup)
+
+
+@pytest.mark.parametrize("idx,frac", [(7, 0.5), (40, 0.25), (56, 1.0)])
+def test_hbm_residency_budget(ko, golden, idx, frac):
+    """keep_memory_residency: the deepest layers of the pinned-host memory
+    stay in HBM (the capacity-bounded fast tier, cache_manager.hpp:23-35).
+    The prefill is bit-identical, no item of a resident layer is loaded, every
+    other workload item still is (rule P over the slow layers), and a write
+    to the memory drops the HBM copy."""
+    if idx >= len(golden["instances"]):
+        pytest.skip("fewer golden instances")
+    c = golden["instances"][idx]
+    p = problem(ko, c)
+    lay = layout_of(p)
+    sched = np.array(c["sched"])
+    L = c["L"]
+    with kb.Context(L, c["H"], c["d"], c["mlp"], c["V"], c["seed"]) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay, version=1, tier=kb.TIER_HOST)
+        full = ctx.plan_keep(lay, p.query, sched)
+        per_layer = 2 * int(np.sum(lay.seg_len)) * c["d"] * 4 + 2 * 128 * c["d"] * 4  # (arena pad rows)
+        m = int(frac * L)
+        got = ctx.memory_residency(m * per_layer + per_layer // 2)
+        assert got == m * per_layer
+        res = ctx.plan_keep(lay, p.query, sched)
+        trace = ctx.loader_trace()
+        assert np.array_equal(res["final_hidden"], full["final_hidden"])
+        assert np.array_equal(res["plan"], full["plan"]) and res["orders"] == full["orders"]
+        assert all(r["layer"] < L - m for r in trace)
+        owners = lay.owners()
+        members = {(k, o): list(range(b, e)) for k, o, b, e in owners}
+        want = {(l, own) for l in range(L - m) for own, ms in members.items() if any(not res["plan"][l, mm] for mm in ms)}
+        assert {(r["layer"], r["owner"]) for r in trace} == want
+        # a write to the memory drops the HBM copy; results stay identical
+        ctx.memory_compute_layout(lay, version=2, tier=kb.TIER_HOST)
+        again = ctx.plan_keep(lay, p.query, sched)
+        assert np.array_equal(again["final_hidden"], full["final_hidden"])
+        assert ctx.memory_residency(0) == 0
