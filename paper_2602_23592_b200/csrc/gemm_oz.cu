@@ -82,6 +82,64 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_
         : "memory");
 }
 
+// ---- CTA-pair (cta_group::2) primitives: a 256 x 256 tile over two SMs of a
+// TPC.  Each CTA stages its 128 rows of A and 128 of the 256 rows of B; the
+// leader (cluster rank 0) issues one M = 256 MMA over both CTAs' smem, each CTA
+// holding its 128 accumulator rows in its own TMEM.  Per k-step an SM reads
+// 32 KB instead of 48 KB (ncu: the single-CTA kernel's TMA stream was
+// ~15 TB/s across the chip at 63% tensor-pipe activity).
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank0(uint32_t saddr) {  // the leader's copy of a smem address
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(saddr));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// TMA into this CTA's smem, completing bytes on the LEADER's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* tm, uint32_t bar_leader, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_leader), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void umma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// MMA completion -> the mbarrier at this offset in BOTH CTAs of the pair
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot, uint32_t cols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t base, uint32_t cols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(base), "r"(cols) : "memory");
+}
+constexpr int OSTAGES2 = 6;                            // pair: 32 KB stages
+constexpr uint32_t OB2_BYTES = 128 * OBK, OSTAGE2 = OA_BYTES + OB2_BYTES;
+constexpr size_t OSMEM2 = size_t(OSTAGES2) * OSTAGE2 + 1024 + 256;
+
 __device__ __forceinline__ void otile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
     const int band = t / (OGM * tiles_n);
     const int m0 = band * OGM;
@@ -152,20 +210,27 @@ __device__ __forceinline__ float redm(float x, float m, float rc) {
 __device__ __forceinline__ float byte_biased(uint32_t w, int b) {
     return __uint_as_float(__byte_perm(w, 0x4B000000u, uint32_t(b) | 0x7650u));
 }
+template <bool PAIR>
 __global__ void __launch_bounds__(OTHREADS, 1)
 gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
                int Mp, int Np, const __grid_constant__ OzCrt crt, const int* __restrict__ ea,
                const int* __restrict__ eb, uint32_t* __restrict__ scratch, EpiArgs epi) {
+    constexpr int NST = PAIR ? OSTAGES2 : OSTAGES;
+    constexpr uint32_t STAGE = PAIR ? OSTAGE2 : OSTAGE;
+    constexpr int TM = PAIR ? 2 * OBM : OBM;  // tile rows (over the pair)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + OSTAGES * OSTAGE);
-    uint64_t* empty = full + OSTAGES;
-    uint64_t* tfull = empty + OSTAGES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
+    uint64_t* empty = full + NST;
+    uint64_t* tfull = empty + NST;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tiles_m = int(ceil_div(M, OBM)), tiles_n = int(ceil_div(N, OBN));
+    const int rank = PAIR ? int(cluster_rank()) : 0;
+    const int cid = PAIR ? int(blockIdx.x >> 1) : int(blockIdx.x);      // cluster (tile walker) index
+    const int ncl = PAIR ? int(gridDim.x >> 1) : int(gridDim.x);
+    const int tiles_m = int(ceil_div(M, TM)), tiles_n = int(ceil_div(N, OBN));
     const int ntiles = tiles_m * tiles_n;
     const int kblocks = int(ceil_div(K, OBK));
     const int U = crt.n;
@@ -173,17 +238,21 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (warp == 0 && lane == 0) {
         prefetch_map(&tmA);
         prefetch_map(&tmB);
-        for (int s = 0; s < OSTAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], OEPI);
+            mbar_init(&tempty[a], PAIR ? 2 * OEPI : OEPI);  // pair: both CTAs' epilogues free the leader's buffer
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc(tmem_slot, 512);
+    if constexpr (PAIR) cluster_sync_all();  // barriers initialised in both CTAs before any remote use
+    if (warp == 2) {
+        if constexpr (PAIR) tmem_alloc_pair(tmem_slot, 512);
+        else tmem_alloc(tmem_slot, 512);
+    }
     fence_before();
     __syncthreads();
     fence_after();
@@ -193,17 +262,25 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         if (lane == 0) {  // ---------------- TMA producer: residue planes u of A and B
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int t = cid; t < ntiles; t += ncl) {
                 int mb, nb;
                 otile_coords(t, tiles_m, tiles_n, mb, nb);
                 for (int u = 0; u < U; ++u) {
                     for (int kb = 0; kb < kblocks; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
-                        uint8_t* sa = smem + stage * OSTAGE;
-                        mbar_expect_tx(&full[stage], OSTAGE);
-                        tma_load_2d(sa, &tmA, &full[stage], kb * OBK, u * Mp + mb * OBM);
-                        tma_load_2d(sa + OA_BYTES, &tmB, &full[stage], kb * OBK, u * Np + nb * OBN);
-                        if (++stage == OSTAGES) {
+                        uint8_t* sa = smem + stage * STAGE;
+                        if constexpr (PAIR) {
+                            // both CTAs' bytes complete on the leader's barrier
+                            const uint32_t fl = map_to_rank0(smem_u32(&full[stage]));
+                            if (rank == 0) mbar_expect_tx(&full[stage], 2 * STAGE);
+                            tma_load_2d_pair(sa, &tmA, fl, kb * OBK, u * Mp + mb * TM + rank * OBM);
+                            tma_load_2d_pair(sa + OA_BYTES, &tmB, fl, kb * OBK, u * Np + nb * OBN + rank * (OBN / 2));
+                        } else {
+                            mbar_expect_tx(&full[stage], STAGE);
+                            tma_load_2d(sa, &tmA, &full[stage], kb * OBK, u * Mp + mb * OBM);
+                            tma_load_2d(sa + OA_BYTES, &tmB, &full[stage], kb * OBK, u * Np + nb * OBN);
+                        }
+                        if (++stage == NST) {
                             stage = 0;
                             phase ^= 1;
                         }
@@ -212,36 +289,47 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             }
         }
     } else if (warp == 1) {  // ---------------- MMA issuer: one exact int32 GEMM per modulus
-        constexpr uint32_t idesc = idesc_i8(OBM, OBN);
-        int stage = 0;
-        uint32_t phase = 0;
-        int it = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            for (int u = 0; u < U; ++u, ++it) {
-                const int acc = it & 1;
-                mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
-                fence_after();
-                const uint32_t tmem_d = tmem_base + uint32_t(acc * OBN);
-                for (int kb = 0; kb < kblocks; ++kb) {
-                    mbar_wait(&full[stage], phase);
+        if (!PAIR || rank == 0) {
+            constexpr uint32_t idesc = idesc_i8(TM, OBN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int t = cid; t < ntiles; t += ncl) {
+                for (int u = 0; u < U; ++u, ++it) {
+                    const int acc = it & 1;
+                    mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
                     fence_after();
-                    const uint32_t sa = smem_u32(smem + stage * OSTAGE);
-                    const uint64_t ad = smem_desc(sa), bd = smem_desc(sa + OA_BYTES);
-                    if (elect_one()) {
+                    const uint32_t tmem_d = tmem_base + uint32_t(acc * OBN);
+                    for (int kb = 0; kb < kblocks; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        fence_after();
+                        const uint32_t sa = smem_u32(smem + stage * STAGE);
+                        const uint64_t ad = smem_desc(sa), bd = smem_desc(sa + OA_BYTES);
+                        if (elect_one()) {
 #pragma unroll
-                        for (int k = 0; k < OBK / 32; ++k)  // 32 int8 = 32 bytes per MMA
-                            umma_i8(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
-                                    (kb == 0 && k == 0) ? 0u : 1u);
-                        umma_commit(&empty[stage]);
+                            for (int k = 0; k < OBK / 32; ++k) {  // 32 int8 = 32 bytes per MMA
+                                if constexpr (PAIR)
+                                    umma_i8_pair(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
+                                                 (kb == 0 && k == 0) ? 0u : 1u);
+                                else
+                                    umma_i8(tmem_d, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
+                                            (kb == 0 && k == 0) ? 0u : 1u);
+                            }
+                            if constexpr (PAIR) umma_commit_pair(&empty[stage]);
+                            else umma_commit(&empty[stage]);
+                        }
+                        __syncwarp();
+                        if (++stage == NST) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                    if (elect_one()) {
+                        if constexpr (PAIR) umma_commit_pair(&tfull[acc]);
+                        else umma_commit(&tfull[acc]);
                     }
                     __syncwarp();
-                    if (++stage == OSTAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
                 }
-                if (elect_one()) umma_commit(&tfull[acc]);
-                __syncwarp();
             }
         }
     } else if (warp >= 4) {  // ---------------- epilogue: Garner digits, fp64 Horner on the last modulus
@@ -250,11 +338,12 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const int r = q4 * 32 + lane;            // tile row = TMEM lane
         // digits v_j of this CTA's tile: [j][OBN / 4 column quads][OBM rows] x char4
         uint32_t* vs = scratch + size_t(blockIdx.x) * kMaxModuli * (OBN / 4) * OBM + r;
+        const uint32_t tempty_leader0 = PAIR ? map_to_rank0(smem_u32(&tempty[0])) : 0u;
         int it = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        for (int t = cid; t < ntiles; t += ncl) {
             int mb, nb;
             otile_coords(t, tiles_m, tiles_n, mb, nb);
-            const int m = mb * OBM + r;
+            const int m = mb * TM + rank * OBM + r;
             const bool mok = m < M;
             const int eam = mok ? ea[m] : 0;
             for (int u = 0; u < U; ++u, ++it) {
@@ -359,15 +448,20 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 }
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (lane == 0) {
+                    if constexpr (PAIR) mbar_arrive_cluster(tempty_leader0 + uint32_t(acc * sizeof(uint64_t)));
+                    else mbar_arrive(&tempty[acc]);
+                }
             }
         }
     }
     fence_before();
     __syncthreads();
+    if constexpr (PAIR) cluster_sync_all();  // the peer's TMEM is the leader's MMA target until the end
     if (warp == 2) {
         fence_after();
-        tmem_dealloc(tmem_base, 512);
+        if constexpr (PAIR) tmem_dealloc_pair(tmem_base, 512);
+        else tmem_dealloc(tmem_base, 512);
     }
 }
 
@@ -533,6 +627,15 @@ int oz_bits(int K) {
     return int(std::floor((lm - 2.0 - std::log2(double(std::max(K, 1)))) / 2.0));
 }
 
+// KEEP_OZ_PAIR=0: the single-CTA kernel only (A/B knob)
+bool oz_pair_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_OZ_PAIR");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 // KEEP_PARITY_GEMM=dfma|ozaki|auto (default auto: Ozaki from kOzMinRows rows)
 int parity_gemm_mode() {
     static const int m = [] {
@@ -557,7 +660,11 @@ void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb,
     const int s = crt.n;
     const int bits = oz_bits(K);
     if (bits < 30) raise(KEEP_ERR_CONFIG, "Ozaki GEMM: too few moduli for K = " + std::to_string(K));
-    const int Mp = int(ceil_div(M, OBM) * OBM), Np = int(ceil_div(N, OBN) * OBN);
+    // CTA pairs when the 256-row tiles still fill the machine
+    const int ntiles2 = int(ceil_div(M, 2 * OBM) * ceil_div(N, OBN));
+    const int maxc = std::max(1, std::min(max_ctas, kNumSMs));
+    const bool pair = oz_pair_enabled() && maxc >= 2 && 2 * ntiles2 >= maxc;
+    const int Mp = int(ceil_div(M, 2 * OBM) * 2 * OBM), Np = int(ceil_div(N, OBN) * OBN);
     const int Kp = int(ceil_div(K, 16) * 16);
     w.a.ensure(size_t(s) * Mp * Kp);
     w.b.ensure(size_t(s) * Np * Kp);
@@ -578,14 +685,36 @@ void launch_gemm_ozaki(const float* A, int64_t lda, const float* B, int64_t ldb,
         B, ldb, K, N, Kp, bits, Np, crt, cmax, w.b.as<int8_t>(), eb);
     KEEP_LAUNCH_CHECK();
     // the GEMM
-    smem_attr(gemm_oz_kernel, int(OSMEM));
     const CUtensorMap ta = make_map_i8(w.a.p, int64_t(s) * Mp, K, Kp, OBM);
+    if (pair) {
+        const CUtensorMap tb = make_map_i8(w.b.p, int64_t(s) * Np, K, Kp, OBN / 2);
+        const int grid = std::min(2 * ntiles2, maxc & ~1);
+        w.part.ensure(sizeof(uint32_t) * size_t(grid) * kMaxModuli * (OBN / 4) * OBM);
+        smem_attr(gemm_oz_kernel<true>, int(OSMEM2));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(unsigned(grid));
+        cfg.blockDim = dim3(OTHREADS);
+        cfg.dynamicSmemBytes = OSMEM2;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        KEEP_CUDA(cudaLaunchKernelEx(&cfg, gemm_oz_kernel<true>, ta, tb, M, N, K, Mp, Np, crt, w.ea.as<int>(),
+                                     static_cast<const int*>(eb), w.part.as<uint32_t>(), epi));
+        KEEP_LAUNCH_CHECK();
+        return;
+    }
+    smem_attr(gemm_oz_kernel<false>, int(OSMEM));
     const CUtensorMap tb = make_map_i8(w.b.p, int64_t(s) * Np, K, Kp, OBN);
     const int ntiles = int(ceil_div(M, OBM) * ceil_div(N, OBN));
-    const int grid = std::min(ntiles, std::max(1, std::min(max_ctas, kNumSMs)));
+    const int grid = std::min(ntiles, maxc);
     w.part.ensure(sizeof(uint32_t) * size_t(grid) * kMaxModuli * (OBN / 4) * OBM);
-    gemm_oz_kernel<<<grid, OTHREADS, OSMEM, st>>>(ta, tb, M, N, K, Mp, Np, crt, w.ea.as<int>(), eb,
-                                                  w.part.as<uint32_t>(), epi);
+    gemm_oz_kernel<false><<<grid, OTHREADS, OSMEM, st>>>(ta, tb, M, N, K, Mp, Np, crt, w.ea.as<int>(), eb,
+                                                         w.part.as<uint32_t>(), epi);
     KEEP_LAUNCH_CHECK();
 }
 
