@@ -199,9 +199,23 @@ uint8_t* layer_keys(const Context& c, const Payload& p, int l) {
     return static_cast<uint8_t*>(p.arena->buf.p) + (int64_t(l) * 2) * sheet + p.row0 * c.dl * c.elem;
 }
 
+// HBM held by the resident layers of pinned-host arenas
+uint64_t resident_bytes(const Context& c) {
+    std::vector<const Arena*> seen;
+    uint64_t t = 0;
+    for (const auto& [k, pl] : c.store) {
+        const Arena* a = pl.arena.get();
+        if (a->tier != KEEP_TIER_HOST || a->mirror_from >= (1 << 30)) continue;
+        if (std::find(seen.begin(), seen.end(), a) != seen.end()) continue;
+        seen.push_back(a);
+        t += a->mirror.bytes;
+    }
+    return t;
+}
+
 // a write to an arena invalidates its HBM mirror (the mirror is a read copy)
 void drop_mirror(Arena& a) {
-    if (a.mirror_from >= (1 << 30)) return;
+    if (a.mirror_from >= (1 << 30) || a.split) return;  // a split arena's resident layers live only in HBM
     KEEP_CUDA(cudaDeviceSynchronize());
     a.mirror.release();
     a.mirror_from = 1 << 30;
@@ -212,12 +226,25 @@ uint8_t* layer_values(const Context& c, const Payload& p, int l) {
 
 constexpr int64_t kArenaPad = 128;  // spare rows per arena layer sheet (query rows of aliased layers)
 
+uint64_t resident_bytes(const Context& c);
+
 std::shared_ptr<Arena> make_arena(Context& c, int64_t rows, int tier) {
     auto a = std::make_shared<Arena>();
     a->rows = rows;
     a->used = rows;
     a->tier = tier;
-    a->buf.alloc(size_t(c.L) * 2 * rows * c.dl * c.elem, tier == KEEP_TIER_HOST);
+    const size_t per_layer = size_t(2) * rows * c.dl * c.elem;
+    int m = 0;  // pinned-host arena under an HBM budget: its deepest m layers live in HBM only
+    if (tier == KEEP_TIER_HOST && c.hbm_budget > 0) {
+        const uint64_t used = resident_bytes(c);
+        m = c.hbm_budget > used ? int(std::min<uint64_t>(uint64_t(c.L), (c.hbm_budget - used) / per_layer)) : 0;
+    }
+    a->buf.alloc(per_layer * size_t(c.L - m), tier == KEEP_TIER_HOST);
+    if (m > 0) {
+        a->mirror.ensure(per_layer * m);
+        a->mirror_from = c.L - m;
+        a->split = true;
+    }
     return a;
 }
 
@@ -1136,6 +1163,21 @@ void cursor_finish(Context& c, float* final_hidden, float* kv_out) {
     }
 }
 
+// rows [0, n) of every layer sheet of a device arena (src_rows rows per sheet)
+// -> rows [row0, row0 + n) of an arena, host part or its HBM-resident part
+void place_rows(Context& c, Arena& dst, int64_t row0, const uint8_t* src, int64_t src_rows, int64_t n) {
+    const size_t rowb = size_t(c.dl) * c.elem;
+    const size_t ssheet = size_t(src_rows) * rowb, dsheet = size_t(dst.rows) * rowb;
+    for (int l = 0; l < c.L; ++l)
+        for (int kv = 0; kv < 2; ++kv) {
+            uint8_t* d = l >= dst.mirror_from
+                             ? static_cast<uint8_t*>(dst.mirror.p) + (size_t(l - dst.mirror_from) * 2 + kv) * dsheet
+                             : static_cast<uint8_t*>(dst.buf.p) + (size_t(l) * 2 + kv) * dsheet;
+            KEEP_CUDA(cudaMemcpyAsync(d + row0 * rowb, src + (size_t(l) * 2 + kv) * ssheet, size_t(n) * rowb,
+                                      cudaMemcpyDefault, c.s_main));
+        }
+}
+
 // --------------------------------------------------- canonical KV refresh --
 // compute_and_put (harness.hpp:512-532) for a batch of owners: one pass over
 // all their rows with block-diagonal attention (each owner is its own causal
@@ -1163,6 +1205,47 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
         row0[o] = rows;
         rows += tot;
         seglen.push_back(tot);
+    }
+    // A new pinned-host memory larger than a quarter of the free HBM (BASELINE
+    // configs[4]: 128K tokens, 172 GB of bf16 canonical KV) is computed in
+    // owner chunks: each chunk on the device, then placed into one in-order
+    // host arena (its HBM-resident layers, under keep_memory_residency's
+    // budget, go to the arena's HBM part).
+    if (tier == KEEP_TIER_HOST) {
+        bool fresh = true;
+        for (int o = 0; o < n_owners && fresh; ++o) fresh = !c.store.count(OwnerKey{owners[o].kind, owners[o].id});
+        const size_t per_row = size_t(c.L) * 2 * c.dl * c.elem;
+        size_t fr = 0, tot = 0;
+        KEEP_CUDA(cudaMemGetInfo(&fr, &tot));
+        int64_t chunk_rows = int64_t(std::max<size_t>(8192, fr / 4 / per_row));
+        if (const char* e = std::getenv("KEEP_HOST_CHUNK_ROWS")) chunk_rows = std::max(1, std::atoi(e));  // tests
+        if (fresh && rows + kArenaPad > chunk_rows && n_owners > 1) {
+            auto arena = make_arena(c, rows + kArenaPad, KEEP_TIER_HOST);
+            arena->used = rows;
+            std::vector<int64_t> mo(n_owners + 1, 0), to(n_owners + 1, 0);
+            for (int o = 0; o < n_owners; ++o) {
+                mo[o + 1] = mo[o] + owner_members[o];
+                to[o + 1] = to[o] + seglen[o];
+            }
+            for (int o0 = 0; o0 < n_owners;) {
+                int o1 = o0 + 1;
+                while (o1 < n_owners && to[o1 + 1] - to[o0] <= chunk_rows) ++o1;
+                memory_compute_batch(c, o1 - o0, owners + o0, versions + o0, owner_members + o0, member_len + mo[o0],
+                                     tokens + to[o0], KEEP_TIER_DEVICE);
+                const Payload& first = c.store.at(OwnerKey{owners[o0].kind, owners[o0].id});
+                place_rows(c, *arena, to[o0], static_cast<const uint8_t*>(first.arena->buf.p), first.arena->rows,
+                           to[o1] - to[o0]);
+                KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+                for (int o = o0; o < o1; ++o) {
+                    Payload& pl = c.store.at(OwnerKey{owners[o].kind, owners[o].id});
+                    pl.arena = arena;
+                    pl.row0 = to[o];
+                }
+                o0 = o1;
+            }
+            c.refresh_ws.release();
+            return;
+        }
     }
     if (rows > INT32_MAX / 2) raise(KEEP_ERR_CONFIG, "refresh batch too large");
     if (!c.refresh) c.refresh.reset(new Pass());
@@ -1250,7 +1333,7 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
     if (tier == KEEP_TIER_HOST) {
         arena = make_arena(c, arows, KEEP_TIER_HOST);
         arena->used = rows;
-        KEEP_CUDA(cudaMemcpyAsync(arena->buf.p, dev->buf.p, size_t(c.L) * 2 * sheet, cudaMemcpyDeviceToHost, c.s_main));
+        place_rows(c, *arena, 0, static_cast<const uint8_t*>(dev->buf.p), arows, arows);
     }
     KEEP_CUDA(cudaStreamSynchronize(c.s_main));
     for (int o = 0; o < n_owners; ++o) {
@@ -1370,7 +1453,14 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
         }
         for (int k = 0; k < NS; ++k) KEEP_CUDA(cudaEventRecord(bt.ev_used[k], st));  // slots free from here
     }
+    // a layer resident in HBM (keep_memory_residency) is read in place: no load
+    const int res_from = host_ar ? std::min(host_ar->mirror_from, L) : L;
+    auto sheet_of = [&](int l) -> uint8_t* {
+        if (l >= res_from) return static_cast<uint8_t*>(host_ar->mirror.p) + size_t(l - res_from) * 2 * ssheet;
+        return stage[l % NS];
+    };
     auto load_sheet = [&](int l) {  // layer l's canonical K / V of every memory row -> stage[l % NS]
+        if (l >= res_from) return;
         const int k = l % NS;
         uint8_t* dst = stage[k];
         const size_t asheet = size_t(host_ar->rows) * rowb;
@@ -1557,7 +1647,7 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
         // cached rows of this layer (prefill.hpp:255-263, 340-350) per
         // instance -- nothing for an all-reused instance over the arena
         std::vector<char> alias(B, 0);
-        if (host_ar && l > 0) KEEP_CUDA(cudaStreamWaitEvent(st, bt.ev_load[l % NS], 0));
+        if (host_ar && l > 0 && l < res_from) KEEP_CUDA(cudaStreamWaitEvent(st, bt.ev_load[l % NS], 0));
         {
             std::vector<void*> ks, vs;
             std::vector<int32_t> dr, nrr;
@@ -1580,8 +1670,8 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                     if (c.seg_owner_row[i] + sl[i] > pl->tokens)
                         raise(KEEP_ERR_INPUT, "cached block of " + owner_str(c.seg_owner[i]) + " is shorter than its members");
                     if (host_ar) {  // the staged sheet, in layout order
-                        ks.push_back(stage[l % NS] + size_t(v0.seg_start[i]) * rowb);
-                        vs.push_back(stage[l % NS] + ssheet + size_t(v0.seg_start[i]) * rowb);
+                        ks.push_back(sheet_of(l) + size_t(v0.seg_start[i]) * rowb);
+                        vs.push_back(sheet_of(l) + ssheet + size_t(v0.seg_start[i]) * rowb);
                     } else {
                         ks.push_back(layer_keys(c, *pl, l) + c.seg_owner_row[i] * rowb);
                         vs.push_back(layer_values(c, *pl, l) + c.seg_owner_row[i] * rowb);
@@ -1635,7 +1725,7 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                 vb = kvV;
             } else if (alias[b]) {  // the arena sheets of layer l, query rows in the spare rows
                 const size_t asheet = host_ar ? ssheet : size_t(c.alias_arena->rows) * rowb;
-                uint8_t* ak = host_ar ? stage[l % NS]
+                uint8_t* ak = host_ar ? sheet_of(l)
                                       : static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * asheet;
                 qk = ak + size_t(Tm) * rowb;
                 qv = ak + asheet + size_t(Tm) * rowb;
@@ -1654,7 +1744,7 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
         }
         if (n_multi > 0) {
             const size_t asheet = host_ar ? ssheet : size_t(c.alias_arena->rows) * rowb;
-            uint8_t* ak = host_ar ? stage[l % NS] : static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * asheet;
+            uint8_t* ak = host_ar ? sheet_of(l) : static_cast<uint8_t*>(c.alias_arena->buf.p) + size_t(l) * 2 * asheet;
             DecodeMulti dm;
             dm.H = c.Hl;
             dm.d = dl;
@@ -2106,11 +2196,17 @@ int keep_memory_residency(void* ctx, uint64_t hbm_budget_bytes, uint64_t* reside
         Context& c = *C(ctx);
         KEEP_CUDA(cudaDeviceSynchronize());
         ++c.store_gen;
+        // the budget also places the deepest layers of pinned-host arenas
+        // created from here on (canonical KV computed straight into HBM)
+        c.hbm_budget = hbm_budget_bytes;
         std::vector<Arena*> host;
+        uint64_t split_bytes = 0;
         for (auto& [k, pl] : c.store)
             if (pl.arena->tier == KEEP_TIER_HOST &&
-                std::find(host.begin(), host.end(), pl.arena.get()) == host.end())
-                host.push_back(pl.arena.get());
+                std::find(host.begin(), host.end(), pl.arena.get()) == host.end()) {
+                if (pl.arena->split) split_bytes += pl.arena->mirror.bytes;  // (its layers cannot move)
+                else host.push_back(pl.arena.get());
+            }
         uint64_t per_layer = 0;
         for (Arena* a : host) {
             drop_mirror(*a);
@@ -2118,8 +2214,9 @@ int keep_memory_residency(void* ctx, uint64_t hbm_budget_bytes, uint64_t* reside
         }
         // the deepest layers first: plans only shrink with depth (monotone,
         // prefill.hpp:95-104), so deep layers reuse the most cached KV
-        const int m = per_layer ? int(std::min<uint64_t>(uint64_t(c.L), hbm_budget_bytes / per_layer)) : 0;
-        uint64_t total = 0;
+        const uint64_t avail = hbm_budget_bytes > split_bytes ? hbm_budget_bytes - split_bytes : 0;
+        const int m = per_layer ? int(std::min<uint64_t>(uint64_t(c.L), avail / per_layer)) : 0;
+        uint64_t total = split_bytes;
         for (Arena* a : host) {
             if (m == 0) break;
             const size_t sheet2 = size_t(2) * a->rows * c.dl * c.elem;

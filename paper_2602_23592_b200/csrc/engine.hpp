@@ -171,6 +171,7 @@ struct Arena {
     // layers goes to the mirror, and a write to the arena drops it
     DevBuf mirror;
     int mirror_from = 1 << 30;
+    bool split = false;  // created with its resident layers in HBM only (no host copy of them)
 };
 
 struct OwnerKey {
@@ -301,6 +302,7 @@ struct Context {
     bool fast = false;
     bool exact = false;  // KEEP_NUMERICS_PARITY_EXACT: DFMA projections + reference-order scores
     double rope_theta = 0.0;  // keep_set_rope: 0 = NoPE, the reference (model.hpp:3-8)
+    uint64_t hbm_budget = 0;  // keep_memory_residency: HBM capacity for pinned-host memory layers
     int elem = 4;  // merged-KV element bytes
     cudaStream_t s_main = nullptr, s_copy = nullptr, s_sel = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;

@@ -202,3 +202,51 @@ def test_hbm_residency_budget(ko, golden, idx, frac):
         again = ctx.plan_keep(lay, p.query, sched)
         assert np.array_equal(again["final_hidden"], full["final_hidden"])
         assert ctx.memory_residency(0) == 0
+
+
+@pytest.mark.parametrize("numerics", [kb.PARITY, kb.FAST])
+def test_split_host_arena_chunked(ko, numerics, monkeypatch):
+    """A pinned-host memory created under an HBM budget: computed in owner
+    chunks (KEEP_HOST_CHUNK_ROWS forces them at test size) into ONE in-order
+    arena whose deepest layers live in HBM only.  plan_keep and the batched
+    prefill over it equal the HBM-resident runs bit for bit; resident layers
+    are never loaded."""
+    from paper_2602_23592_b200.synth import group_units, make_instance_layout
+    seed, S, L, H, d, V = 23, 40, 6, 2, 256, 512
+    inst = make_instance_layout(seed, S, V)
+    lay = kb.Layout(inst.seg_len, inst.tokens, group_units(S, 4, 0.5))
+    sched = kb.ratio_schedule(L, 0.4)
+    rng = np.random.default_rng(seed)
+    Q = rng.integers(0, V, size=(3, len(inst.query))).astype(np.int32)
+    Q[0] = inst.query
+    elem = 4 if numerics == kb.PARITY else 2
+    per_layer = 2 * (int(np.sum(inst.seg_len)) + 128) * d * elem
+    with kb.Context(L, H, d, 2 * d, V, seed, numerics) as ctx:
+        ctx.model_init()
+        ctx.memory_compute_layout(lay, version=1, tier=kb.TIER_DEVICE)
+        dev = ctx.plan_keep(lay, Q[0], sched)
+        devb = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True)
+    with kb.Context(L, H, d, 2 * d, V, seed, numerics) as ctx:
+        ctx.model_init()
+        assert ctx.memory_residency(2 * per_layer + 10) == 0  # (no host memory yet: the budget is for new arenas)
+        monkeypatch.setenv("KEEP_HOST_CHUNK_ROWS", "97")
+        ctx.memory_compute_layout(lay, version=1, tier=kb.TIER_HOST)
+        monkeypatch.delenv("KEEP_HOST_CHUNK_ROWS")
+        st = ctx.memory_stats()
+        assert st["device_bytes"] >= 2 * per_layer and st["host_bytes"] == (L - 2) * per_layer
+        host = ctx.plan_keep(lay, Q[0], sched)
+        trace = ctx.loader_trace()
+        hostb = ctx.plan_keep_batch(lay, Q, sched, final_hidden=True)
+    assert all(r["layer"] < L - 2 for r in trace)
+    assert np.array_equal(host["plan"], dev["plan"]) and host["orders"] == dev["orders"]
+
+    def same(a, b):
+        if numerics == kb.PARITY:  # the chunks' canonical KV is bit-identical (row-local arithmetic)
+            return np.array_equal(a, b)
+        # FAST: the chunks' bf16 GEMMs tile / split K differently from one pass
+        return float(np.max(np.abs(a - b))) <= 3e-2 * float(np.max(np.abs(b)))
+
+    assert same(host["final_hidden"], dev["final_hidden"])
+    for a, b in zip(hostb, devb):
+        assert np.array_equal(a["plan"], b["plan"])
+        assert same(a["final_hidden"], b["final_hidden"])
