@@ -52,6 +52,9 @@ CONFIGS = {
                desc="Qwen2.5-14B dims, 16K-token memory, r_avg 0.5 (reference default, harness.hpp:57)"),
     "c4": dict(L=64, H=40, d=5120, mlp=27648, V=152064, S=3276, r_avg=0.15,
                desc="Qwen2.5-32B dims, 32K-token memory, r_avg 0.15 (BASELINE configs[3], here on one GPU)"),
+    "c5": dict(L=64, H=40, d=5120, mlp=27648, V=152064, S=13107, r_avg=0.15,
+               desc="Qwen2.5-32B dims, 128K-token memory bank in pinned host DRAM, batch of 16 planning queries "
+                    "(BASELINE configs[4])"),
 }
 METRIC = "memory-prefill TTFT (ms) and recomputed tokens/s, 16K-token memory, 1/2/4/8 B200"
 UNIT = "recomputed tokens/s"
@@ -708,24 +711,48 @@ def run_batch(args, cfg):
     ctx = kb.Context(L, H, d, mlp, V, args.seed, numerics)
     ctx.model_init()
     host_mem = args.memory == "host"
+    resident = 0
+    if host_mem and args.hbm_budget_gb > 0:
+        # the fast tier: the deepest layers of the new pinned-host memory are
+        # computed straight into HBM (they never occupy host DRAM)
+        ctx.memory_residency(int(args.hbm_budget_gb * 1e9))
+    t0 = time.perf_counter()
     ctx.memory_compute_layout(layout, tier=kb.TIER_HOST if host_mem else kb.TIER_DEVICE)
+    t_mem = time.perf_counter() - t0
+    mem_st = ctx.memory_stats()
+    mem_st["hbm_free_after_memory_bytes"] = int(torch.cuda.mem_get_info()[0])
+    print(f"# memory KV: host {mem_st['host_bytes'] / 1e9:.1f} GB, device {mem_st['device_bytes'] / 1e9:.1f} GB, "
+          f"HBM free {mem_st['hbm_free_after_memory_bytes'] / 1e9:.1f} GB, setup {t_mem:.1f} s", file=sys.stderr, flush=True)
+    sb = args.sub_batch if args.sub_batch > 0 else B
+
+    def batch_step():
+        # B queries as ceil(B / sb) sub-batches of one plan_keep_batch each
+        outs, ms = [], 0.0
+        for q0 in range(0, B, sb):
+            o = ctx.plan_keep_batch(layout, Q[q0:q0 + sb], r)
+            ms += o[0]["ttft_ms"]
+            outs += o
+        for o in outs:
+            o["batch_ms"] = ms
+        return outs
+
     for _ in range(args.warmup):
-        ctx.plan_keep_batch(layout, Q, r)
+        batch_step()
     torch.cuda.synchronize()
     res = []
     dev = torch.cuda.current_device()
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
-            res.append(ctx.plan_keep_batch(layout, Q, r))
+            res.append(batch_step())
     torch.cuda.synchronize()
     # per-phase times from one separate profiled batch (kept out of the timed steps)
     ctx.profile_read(reset=True)
     ctx.profile_enable(True)
-    ctx.plan_keep_batch(layout, Q, r)
+    batch_step()
     ctx.profile_enable(False)
     prof = ctx.profile_read(reset=True)
     n_prof = 1
-    batch_ms = np.array([x[0]["ttft_ms"] for x in res])
+    batch_ms = np.array([x[0]["batch_ms"] for x in res])
     tokens = float(sum(np.sum(o["rows_per_layer"]) for o in res[-1]))
     value = tokens / (float(np.mean(batch_ms)) / 1e3)
     # e2e: host query ids in, host plans + logits out, wall clock
@@ -733,18 +760,20 @@ def run_batch(args, cfg):
     for _ in range(max(1, args.steps)):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        ctx.plan_keep_batch(layout, Q, r)
+        batch_step()
         e2e.append(time.perf_counter() - t0)
     st_b = ctx.memory_stats()["bytes_loaded_slow"]
-    ctx.plan_keep_batch(layout, Q, r)
+    batch_step()
     h2d_batch = ctx.memory_stats()["bytes_loaded_slow"] - st_b
     # the same queries one at a time (the batch workspace released first)
-    ctx.trim()
-    for b in range(min(B, 2)):
-        ctx.plan_keep(layout, Q[b], r, final_hidden=False)
-    seq = [ctx.plan_keep(layout, Q[b], r, final_hidden=False) for b in range(B)]
-    seq_ms = float(sum(x["ttft_ms"] for x in seq))
-    same = [bool(np.array_equal(res[-1][b]["plan"], seq[b]["plan"])) for b in range(B)]
+    seq_ms, same = None, None
+    if not args.no_sequential:
+        ctx.trim()
+        for b in range(min(B, 2)):
+            ctx.plan_keep(layout, Q[b], r, final_hidden=False)
+        seq = [ctx.plan_keep(layout, Q[b], r, final_hidden=False) for b in range(B)]
+        seq_ms = float(sum(x["ttft_ms"] for x in seq))
+        same = [bool(np.array_equal(res[-1][b]["plan"], seq[b]["plan"])) for b in range(B)]
     line = {
         "metric": METRIC + " -- batched planning queries", "value": value, "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(np.mean(batch_ms)),
@@ -755,8 +784,11 @@ def run_batch(args, cfg):
                    "memory": "pinned host DRAM, one staged layer sheet per layer for the batch" if host_mem else "hbm",
                    "l2": "inputs > L2 ({:.1f} GB memory KV)".format(4e-9 * L * d * int(np.sum(layout.seg_len)))},
         "batch": {"batch_ttft_ms": float(np.median(batch_ms)), "sequential_ttft_ms_sum": seq_ms,
-                  "speedup_vs_sequential": seq_ms / float(np.median(batch_ms)),
-                  "plans_equal_to_sequential": same,
+                  "speedup_vs_sequential": seq_ms / float(np.median(batch_ms)) if seq_ms else None,
+                  "plans_equal_to_sequential": same, "sub_batch": sb,
+                  "memory": {"host_bytes": mem_st["host_bytes"], "device_bytes": mem_st["device_bytes"],
+                             "hbm_free_after_memory_bytes": mem_st["hbm_free_after_memory_bytes"],
+                             "hbm_budget_gb": args.hbm_budget_gb, "canonical_kv_setup_s": t_mem},
                   "plan_segments_per_layer_q0": [int(x) for x in res[-1][0]["plan"].sum(axis=1)],
                   "recomputed_tokens_per_batch": tokens, "h2d_memory_bytes_per_batch": int(h2d_batch)},
         "phase_ms_per_step": {k: round(v["ms"] / n_prof, 3) for k, v in prof.items() if v["ms"] > 0},
@@ -797,6 +829,10 @@ def main():
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="--memory host: keep the deepest layers of the memory KV also in HBM up to this budget "
                          "(the capacity-bounded fast tier; keep_memory_residency)")
+    ap.add_argument("--sub-batch", type=int, default=0,
+                    help="--batch: run the B queries as sub-batches of this many (HBM for larger memories)")
+    ap.add_argument("--no-sequential", action="store_true",
+                    help="--batch: skip the one-query-at-a-time comparison")
     ap.add_argument("--batch", type=int, default=1,
                     help="B > 1: B concurrent planning queries through keep_plan_keep_batch (one GPU)")
     args = ap.parse_args()

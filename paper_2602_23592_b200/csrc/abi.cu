@@ -9,6 +9,8 @@
 #include <numeric>
 #include <string>
 
+#include <unistd.h>
+
 #include "engine.hpp"
 
 using namespace keep_b200;
@@ -238,6 +240,15 @@ std::shared_ptr<Arena> make_arena(Context& c, int64_t rows, int tier) {
     if (tier == KEEP_TIER_HOST && c.hbm_budget > 0) {
         const uint64_t used = resident_bytes(c);
         m = c.hbm_budget > used ? int(std::min<uint64_t>(uint64_t(c.L), (c.hbm_budget - used) / per_layer)) : 0;
+    }
+    if (tier == KEEP_TIER_HOST) {
+        // pinned pages cannot be swapped: refuse an arena that would leave the
+        // host under 16 GB of available RAM rather than invite the OOM killer
+        const uint64_t avail = uint64_t(sysconf(_SC_AVPHYS_PAGES)) * uint64_t(sysconf(_SC_PAGESIZE));
+        const uint64_t need = uint64_t(per_layer) * uint64_t(c.L - m);
+        if (need + (uint64_t(16) << 30) > avail)
+            raise(KEEP_ERR_CONFIG, "pinned host arena of " + std::to_string(need >> 30) + " GB would leave less than 16 GB of " +
+                                       std::to_string(avail >> 30) + " GB available host RAM (raise the HBM budget)");
     }
     a->buf.alloc(per_layer * size_t(c.L - m), tier == KEEP_TIER_HOST);
     if (m > 0) {
@@ -1244,6 +1255,7 @@ void memory_compute_batch(Context& c, int n_owners, const keep_owner* owners, co
                 o0 = o1;
             }
             c.refresh_ws.release();
+            c.refresh.reset();  // the chunk pass's row buffers: the memory is built, HBM goes back to the queries
             return;
         }
     }
@@ -1439,9 +1451,11 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
     if (host_ar) {
         size_t free_b = 0, total_b = 0;
         KEEP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-        // (at most a third of the free HBM and a sixth of the device: the pass needs the rest)
-        const size_t have = bt.stage.bytes + std::min(free_b / 3, total_b / 6);
-        NS = int(std::max<size_t>(2, std::min<size_t>(size_t(L), have / (2 * ssheet))));
+        // (at most a quarter of the free HBM and a sixth of the device: the pass
+        // needs the rest; no deeper than the layers that live in host DRAM)
+        const size_t have = bt.stage.bytes + std::min(free_b / 4, total_b / 6);
+        const int host_layers = std::max(1, std::min(host_ar->mirror_from, L) - 1);
+        NS = int(std::max<size_t>(2, std::min<size_t>(size_t(host_layers), have / (2 * ssheet))));
         bt.stage.ensure(size_t(NS) * 2 * ssheet);
         for (int k = 0; k < NS; ++k) stage.push_back(static_cast<uint8_t*>(bt.stage.p) + size_t(k) * 2 * ssheet);
         for (size_t k = bt.ev_load.size(); k < size_t(NS); ++k) {
