@@ -227,6 +227,7 @@ uint8_t* layer_values(const Context& c, const Payload& p, int l) {
 }
 
 constexpr int64_t kArenaPad = 128;  // spare rows per arena layer sheet (query rows of aliased layers)
+constexpr int kTpRows = 32;         // sharded layers of at most this many rows split the weights, not the rows
 
 uint64_t resident_bytes(const Context& c);
 
@@ -754,6 +755,48 @@ void layer_dense(Context& c, Pass& p, int l) {
     const double bi = wb * (double(d) * f + m * double(d) + m * double(f));
     const double bout = wb * (double(d) * f + m * double(f)) + 8.0 * m * d;
     (void)dl;
+    if (G > 1 && !c.fast && !c.exact && n <= kTpRows && f % G == 0) {
+        // Few rows (every layer after the walk: the query alone).  Wo + MLP are
+        // a weight stream here, so the ranks split the WEIGHTS instead of the
+        // rows: Wo row-parallel over this rank's head columns of ctx (no
+        // all-to-all), MLP-in column-parallel (relu on this rank's f / G
+        // columns), MLP-out row-parallel; each row-parallel product is an fp64
+        // partial sum all-reduced in a fixed order (identical bits on every
+        // rank), then x += float(sum) as prefill.hpp:289-291 / 302-303 round
+        // it.  Only the order of the fp64 k-sum changes.
+        const int c0 = c.R * dl, fl = f / G, f0 = c.R * fl;
+        p.tp_part.ensure(sizeof(double) * size_t(n) * d);
+        p.tp_h.ensure(sizeof(float) * size_t(n) * fl);
+        double* part = p.tp_part.as<double>();
+        float* x = p.x.as<float>();
+        const EpiArgs ef{EPI_F64, d, reinterpret_cast<float*>(part), d, nullptr, nullptr, nullptr, nullptr};
+        {
+            ProfScope ps(c.prof, KEEP_PROF_WO, st, 2.0 * n * double(dl) * d, 4.0 * double(dl) * d);
+            launch_gemm_f64acc(p.ctx.as<float>(), dl, static_cast<const float*>(c.wslot(l, W_O)) + size_t(c0) * d, d, n,
+                               d, dl, ef, st, false);
+        }
+        {
+            ProfScope ps(c.prof, KEEP_PROF_COMM, st, 0.0, 8.0 * n * double(d) * 2.0 * (G - 1) / G, 2);
+            c.comm->allreduce_f64(part, size_t(n) * d, st);
+        }
+        launch_f64_resid(part, x, n, d, d, st);
+        {
+            ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, 2.0 * n * double(d) * fl, 4.0 * double(d) * fl);
+            const EpiArgs ei{EPI_RELU, d, p.tp_h.as<float>(), fl, nullptr, nullptr, nullptr, nullptr};
+            launch_gemm_f64acc(x, d, static_cast<const float*>(c.wslot(l, W_IN)) + f0, f, n, fl, d, ei, st, false);
+        }
+        {
+            ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, 2.0 * n * double(fl) * d, 4.0 * double(fl) * d);
+            launch_gemm_f64acc(p.tp_h.as<float>(), fl, static_cast<const float*>(c.wslot(l, W_OUT)) + size_t(f0) * d, d, n,
+                               d, fl, ef, st, false);
+        }
+        {
+            ProfScope ps(c.prof, KEEP_PROF_COMM, st, 0.0, 8.0 * n * double(d) * 2.0 * (G - 1) / G, 2);
+            c.comm->allreduce_f64(part, size_t(n) * d, st);
+        }
+        launch_f64_resid(part, x, n, d, d, st);
+        return;
+    }
     // attention context for the Wo + MLP rows of this rank
     const int es = c.fast ? 2 : 4;
     const void* ctx_rows = c.fast ? static_cast<const void*>(p.ctxb.p) : static_cast<const void*>(p.ctx.p);

@@ -149,6 +149,8 @@ struct OzWork {
     DevBuf a, b, ea, eb, part;
 };
 constexpr int kOzMinRows = 64;
+// the residual add of a cross-rank fp64 sum: x[m][n] += float(sum[m][n])
+void launch_f64_resid(const double* sum, float* x, int M, int N, int64_t ldx, cudaStream_t st);
 int oz_moduli();       // KEEP_OZ_MODULI (default 14)
 int oz_bits(int K);    // integer bits per operand at contraction length K
 bool ozaki_eligible(int M, int N, int K);
@@ -197,6 +199,7 @@ struct Pass {
     std::vector<int32_t> key_lo_h;
     DevBuf d_tokens, d_row_seg, d_key_lo, d_seg_len, d_seg_start;
     DevBuf ebin;                  // PARITY fused bins: [H x n x S] fp64 per-head segment sums
+    DevBuf tp_part, tp_h;         // sharded few-row layers: fp64 partial sums [n x d], this rank's MLP slice [n x f/G]
     // compact state
     std::vector<int32_t> rows_h;  // compact -> global row, ascending
     int n = 0;

@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(256) gemm_f64_skinny_kernel(const float* __res
         const int m = rs + 8 * r;
         if (m >= M) continue;
         if (part) part[(int64_t(blockIdx.y) * M + m) * N + n] = acc[r];
+        else if (epi.kind == EPI_F64) reinterpret_cast<double*>(epi.out)[int64_t(m) * epi.ldo + n] = acc[r];
         else epi_store1(epi, m, n, static_cast<float>(acc[r]));
     }
 }
@@ -193,7 +194,8 @@ __global__ void f64_splitk_finish_kernel(const double* __restrict__ part, int ks
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < MN; e += int64_t(gridDim.x) * blockDim.x) {
         double acc = part[e];
         for (int s = 1; s < ks; ++s) acc += part[int64_t(s) * MN + e];
-        epi_store1(epi, int(e / N), int(e % N), static_cast<float>(acc));
+        if (epi.kind == EPI_F64) reinterpret_cast<double*>(epi.out)[(e / N) * epi.ldo + e % N] = acc;
+        else epi_store1(epi, int(e / N), int(e % N), static_cast<float>(acc));
     }
 }
 
@@ -250,8 +252,26 @@ void launch_gemm_f64acc(const float* A, int64_t lda, const float* B, int64_t ldb
         }
         return;
     }
+    if (epi.kind == EPI_F64) raise(KEEP_ERR_CONFIG, "fp64 output: the few-row DFMA path only");
     dim3 grid(static_cast<unsigned>(ceil_div(N, BN)), static_cast<unsigned>(ceil_div(M, BM)));
     gemm_f64acc_kernel<<<grid, 256, 0, st>>>(A, lda, B, ldb, M, N, K, epi);
+    KEEP_LAUNCH_CHECK();
+}
+
+// x[m][n] += float(sum[m][n]) (the residual add of prefill.hpp:289-291 / 302-303
+// on a cross-rank fp64 sum)
+__global__ void f64_resid_kernel(const double* __restrict__ sum, float* __restrict__ x, int M, int N, int64_t ldx) {
+    const int64_t MN = int64_t(M) * N;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < MN; e += int64_t(gridDim.x) * blockDim.x) {
+        float* o = x + (e / N) * ldx + e % N;
+        *o = *o + static_cast<float>(sum[e]);
+    }
+}
+
+void launch_f64_resid(const double* sum, float* x, int M, int N, int64_t ldx, cudaStream_t st) {
+    const int64_t MN = int64_t(M) * N;
+    if (MN == 0) return;
+    f64_resid_kernel<<<unsigned(std::min<int64_t>(ceil_div(MN, 256), kNumSMs * 4)), 256, 0, st>>>(sum, x, M, N, ldx);
     KEEP_LAUNCH_CHECK();
 }
 

@@ -84,7 +84,7 @@ void launch_rope_shift(void* k, const int32_t* tab, int n_entries, int max_rows,
 // ------------------------------------------------------------ parity GEMM --
 // C = A[M x K] . B[K x N] with fp32 operands and fp64 accumulation in
 // ascending k (bit-exact with vec_mat, tensor.hpp:31-41).
-enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_RELU = 2, EPI_STORE = 3 };
+enum EpiKind { EPI_QKV = 0, EPI_RESID = 1, EPI_RELU = 2, EPI_STORE = 3, EPI_F64 = 4 /* out = double*: the fp64 sum itself (DFMA path) */ };
 struct EpiArgs {
     int kind;
     int d;                 // model dim (QKV split)

@@ -4,7 +4,7 @@
 # 16 planning queries (FAST numerics: the fp32 PARITY weights alone are 105 GB).
 mkdir -p gpurun_out
 free -g | head -2
-for a in "--sub-batch 16 --hbm-budget-gb 30" "--sub-batch 8 --hbm-budget-gb 60"; do
+for a in "--sub-batch 2 --hbm-budget-gb 50" "--sub-batch 1 --hbm-budget-gb 60"; do
   tag=$(echo $a | tr -d ' -')
   timeout 1800 python bench.py --config c5 --numerics fast --batch 16 --memory host $a --steps 1 --warmup 1 \
       --no-sequential > gpurun_out/bench_c5_$tag.json 2> gpurun_out/bench_c5_$tag.err
