@@ -122,3 +122,29 @@ def test_sharded_fast_matches_single_gpu(ko, G):
         assert rel(sel["kv"], ref["kv"][..., r * dl:(r + 1) * dl]) <= RTOL_FAST
         assert rel(sel["sts"], single["sts"]) <= 1e-2
         assert np.array_equal(pk["plan"], out[0][1]["plan"])  # replicated selection
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_few_row_layers_split_weights(ko, G):
+    """Layers of <= 32 rows split the Wo / MLP weights across the ranks
+    (row- / column-parallel, fixed-order fp64 all-reduces): a plan that keeps
+    only the query from layer 1 on runs every later layer that way.  Hidden
+    states within the fp64 re-ordering tolerance of the oracle, identical on
+    every rank."""
+    seed, S, L, H, d, mlp, V = 91, 12, 5, 4, 256, 512, 300
+    p = ko.make_instance(seed, S, L, H, d, mlp, V)
+    w = ko.model_init(L, H, d, mlp, V, seed)
+    plan = np.zeros((L, S), np.uint8)
+    plan[0] = 1
+    ref = ko.selective_prefill(p, w, plan)
+    lay = kb.Layout(p.seg_len, p.tokens)
+
+    def body(ctx):
+        ctx.model_init()
+        ctx.memory_compute_layout(lay)
+        return ctx.selective_prefill(lay, p.query, plan)["final_hidden"]
+
+    outs = run_sharded(G, (L, H, d, mlp, V, seed), kb.PARITY, body)
+    for o in outs:
+        assert np.array_equal(o, outs[0])
+        assert rel(o[-len(p.query):], ref["final_hidden"][-len(p.query):]) <= HIDDEN_RTOL
