@@ -829,7 +829,9 @@ constexpr int F16_KC = 32;                 // keys per ring slot (16 per key hal
 constexpr int F16_ST = 2;
 template <int DH>
 struct F16Geo {
-    static constexpr int PK = DH + 4, PV = DH + 2, QP = DH + 4;
+    // PK / QP = DH + 8: the double2 fragment loads (lane (g, t) -> dims 8p + 2t,
+    // +1) of rows g hit distinct 16-byte bank groups in each 8-lane phase
+    static constexpr int PK = DH + 8, PV = DH + 2, QP = DH + 8;
     static constexpr int KD = F16_KC * PK, VD = F16_KC * PV;
     static constexpr size_t slot = sizeof(double) * (KD + VD);
     static constexpr size_t smem = F16_ST * slot + sizeof(double) * (F16_ROWS * QP + 64) + 2 * F16_ST * 8 + 16;
@@ -946,34 +948,48 @@ __global__ void __launch_bounds__(F16_THREADS, 1) attn_dmma16_flash_kernel(AttnA
         const double* kd = kslot(s) + kh * 16 * G::PK;
         const double* vd = kslot(s) + G::KD + kh * 16 * G::PV;
         // S = Q . K^T: two 8-key n-tiles, DH / 16 k-steps
-        // (m16n8k16.f64 issues as 16 dependent-in-k DMMA.8x8x4: the head
-        // dimensions go to two accumulator sets, halving the k chains)
-        double sc[2][4], sd[2][4];
+        // S = Q . K^T on m8n8k4 DMMA, issued in independent groups of eight
+        // (mma.m16n8k16.f64 expands into DMMA.8x8x4 chains that ptxas
+        // interleaves only two at a time).  Dim pair p: lane t carries dims
+        // 8p + 2t (x) and 8p + 2t + 1 (y) as one 16-byte load of Q and of K;
+        // x and y accumulate separately (an fp64 re-ordering of the dot).
+        // acc[s][mh][j]: component s, rows g + 8 mh, keys 8j + 2t + {0, 1}.
+        double acc[2][2][2][2];
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int a0 = 0; a0 < 2; ++a0)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) sc[j][i] = sd[j][i] = 0.0;
+            for (int a1 = 0; a1 < 2; ++a1)
 #pragma unroll
-        for (int ks = 0; ks < DH / 32; ++ks) {
+                for (int a2 = 0; a2 < 2; ++a2) acc[a0][a1][a2][0] = acc[a0][a1][a2][1] = 0.0;
 #pragma unroll
-            for (int hv = 0; hv < 2; ++hv) {
-                const int kc = (ks + hv * DH / 32) * 16;
-                double qa[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) qa[i] = qw[(g + 8 * (i & 1)) * G::QP + kc + t + 4 * (i >> 1)];
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    double kb[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) kb[i] = kd[(8 * j + g) * G::PK + kc + t + 4 * i];
-                    dmma16(hv ? sd[j] : sc[j], qa, kb);
-                }
-            }
+        for (int pp = 0; pp < DH / 8; ++pp) {
+            const double2 q0 = *reinterpret_cast<const double2*>(qw + g * G::QP + 8 * pp + 2 * t);
+            const double2 q1 = *reinterpret_cast<const double2*>(qw + (g + 8) * G::QP + 8 * pp + 2 * t);
+            const double2 k0 = *reinterpret_cast<const double2*>(kd + g * G::PK + 8 * pp + 2 * t);
+            const double2 k1 = *reinterpret_cast<const double2*>(kd + (8 + g) * G::PK + 8 * pp + 2 * t);
+            asm volatile(
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%16}, {%20}, {%0, %1};\n\t"
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%2, %3}, {%16}, {%22}, {%2, %3};\n\t"
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%4, %5}, {%18}, {%20}, {%4, %5};\n\t"
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%6, %7}, {%18}, {%22}, {%6, %7};\n\t"
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%8, %9}, {%17}, {%21}, {%8, %9};\n\t"
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%10, %11}, {%17}, {%23}, {%10, %11};\n\t"
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%12, %13}, {%19}, {%21}, {%12, %13};\n\t"
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%14, %15}, {%19}, {%23}, {%14, %15};"
+                : "+d"(acc[0][0][0][0]), "+d"(acc[0][0][0][1]), "+d"(acc[0][0][1][0]), "+d"(acc[0][0][1][1]),
+                  "+d"(acc[0][1][0][0]), "+d"(acc[0][1][0][1]), "+d"(acc[0][1][1][0]), "+d"(acc[0][1][1][1]),
+                  "+d"(acc[1][0][0][0]), "+d"(acc[1][0][0][1]), "+d"(acc[1][0][1][0]), "+d"(acc[1][0][1][1]),
+                  "+d"(acc[1][1][0][0]), "+d"(acc[1][1][0][1]), "+d"(acc[1][1][1][0]), "+d"(acc[1][1][1][1])
+                : "d"(q0.x), "d"(q0.y), "d"(q1.x), "d"(q1.y), "d"(k0.x), "d"(k0.y), "d"(k1.x), "d"(k1.y));
         }
+        double sc[2][4];  // [j][c]: c = 0, 1 row g; 2, 3 row g + 8 (keys 8j + 2t + c % 2)
 #pragma unroll
         for (int j = 0; j < 2; ++j)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) sc[j][i] = __dadd_rn(sc[j][i], sd[j][i]);
+            for (int e = 0; e < 2; ++e) {
+                sc[j][e] = __dadd_rn(acc[0][0][j][e], acc[1][0][j][e]);
+                sc[j][2 + e] = __dadd_rn(acc[0][1][j][e], acc[1][1][j][e]);
+            }
         // scale (rounded on its own, prefill.hpp:140), visibility, lazy online max
         double cma = -DBL_MAX, cmb = -DBL_MAX;
         bool va[2][2], vb[2][2];
@@ -1027,13 +1043,30 @@ __global__ void __launch_bounds__(F16_THREADS, 1) attn_dmma16_flash_kernel(AttnA
                 pa[2 * (2 * j + e)] = p0;      // row g
                 pa[2 * (2 * j + e) + 1] = p1;  // row g + 8
             }
-        // O += P . V (V rows in the same key permutation)
+        // O += P . V on m8n8k4: k-step (j, e) takes key 8j + 2t + e from lane t's
+        // own probabilities (the S fragment layout), V rows in the same
+        // permutation; each V fragment feeds both row halves
 #pragma unroll
-        for (int n = 0; n < NT; ++n) {
-            double vb4[4];
+        for (int ks = 0; ks < 4; ++ks) {
+            const double* vrow = vd + (8 * (ks >> 1) + 2 * t + (ks & 1)) * G::PV + g;
+            const double a0 = pa[2 * ks], a1 = pa[2 * ks + 1];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) vb4[i] = vd[(8 * (i >> 1) + 2 * t + (i & 1)) * G::PV + 8 * n + g];
-            dmma16(o[n], pa, vb4);
+            for (int n = 0; n < NT; n += 4) {
+                const double b0 = vrow[8 * n], b1 = vrow[8 * (n + 1)], b2 = vrow[8 * (n + 2)], b3 = vrow[8 * (n + 3)];
+                asm volatile(
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%16}, {%18}, {%0, %1};\n\t"
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%2, %3}, {%17}, {%18}, {%2, %3};\n\t"
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%4, %5}, {%16}, {%19}, {%4, %5};\n\t"
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%6, %7}, {%17}, {%19}, {%6, %7};\n\t"
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%8, %9}, {%16}, {%20}, {%8, %9};\n\t"
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%10, %11}, {%17}, {%20}, {%10, %11};\n\t"
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%12, %13}, {%16}, {%21}, {%12, %13};\n\t"
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%14, %15}, {%17}, {%21}, {%14, %15};"
+                    : "+d"(o[n][0]), "+d"(o[n][1]), "+d"(o[n][2]), "+d"(o[n][3]), "+d"(o[n + 1][0]), "+d"(o[n + 1][1]),
+                      "+d"(o[n + 1][2]), "+d"(o[n + 1][3]), "+d"(o[n + 2][0]), "+d"(o[n + 2][1]), "+d"(o[n + 2][2]),
+                      "+d"(o[n + 2][3]), "+d"(o[n + 3][0]), "+d"(o[n + 3][1]), "+d"(o[n + 3][2]), "+d"(o[n + 3][3])
+                    : "d"(a0), "d"(a1), "d"(b0), "d"(b1), "d"(b2), "d"(b3));
+            }
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&empty[s]);
