@@ -201,6 +201,13 @@ int keep_memory_compute_batch(void* ctx, int32_t n_owners, const keep_owner* own
                               const uint64_t* versions, const int32_t* owner_members,
                               const int32_t* member_len, const int32_t* tokens, int32_t tier);
 int keep_load_memory(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* out);
+/* The asynchronous form: the slow-tier copy is enqueued on
+ * the context's copy stream and the view returned at once; *done (a
+ * cudaEvent_t) completes when the block is in HBM -- wait on it
+ * (cudaStreamWaitEvent / keep_load_wait) before reading the view.  The event
+ * is the context's: valid until its next load. */
+int keep_load_memory_async(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* out, void** done);
+int keep_load_wait(void* ctx);
 int keep_memory_has_current(void* ctx, keep_owner owner, uint64_t version, int32_t* out);
 int keep_invalidate(void* ctx, keep_owner owner, uint64_t new_version, uint64_t tokens);
 int keep_memory_stats_get(void* ctx, keep_memory_stats* out);

@@ -159,6 +159,8 @@ def load_library() -> C.CDLL:
         "keep_debug_gemm_parity": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
         "keep_debug_exp_f64": (C.c_int, [vp, vp, i64]),
         "keep_memory_residency": (C.c_int, [vp, u64, C.POINTER(C.c_uint64)]),
+        "keep_load_memory_async": (C.c_int, [vp, keep_owner, i32, C.POINTER(keep_kv_view), C.POINTER(vp)]),
+        "keep_load_wait": (C.c_int, [vp]),
         "keep_comm_unique_id": (C.c_int, [C.c_char_p]),
         "keep_loader_trace": (C.c_int, [vp, C.POINTER(keep_load_record), i32, i32p]),
         "keep_shard_heads": (C.c_int, [i32, i32, i32, i32, i32p, i32p, i32p, i32p]),
@@ -424,6 +426,17 @@ class Context:
         out = C.c_uint64()
         _check(self.lib.keep_memory_residency(self._h, int(hbm_budget_bytes), C.byref(out)))
         return out.value
+
+    def load_memory_async(self, kind, oid, layer):
+        """load_memory without waiting: (view, completion event handle);
+        call load_wait() (or wait on the event) before reading the view."""
+        v = keep_kv_view()
+        ev = C.c_void_p()
+        _check(self.lib.keep_load_memory_async(self._h, keep_owner(kind, oid), layer, C.byref(v), C.byref(ev)))
+        return v, ev.value
+
+    def load_wait(self):
+        _check(self.lib.keep_load_wait(self._h))
 
     def load_memory(self, kind, oid, layer) -> keep_kv_view:
         v = keep_kv_view()

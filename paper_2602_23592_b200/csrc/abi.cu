@@ -1882,15 +1882,13 @@ void plan_keep_batch(Context& c, const keep_layout* lay, int B, const int32_t* q
                 if (o && o->orders) std::copy(h + 2, h + 2 + h[0], o->orders + size_t(l) * S);
                 if (o && o->order_len) o->order_len[l] = h[0];
                 if (o && o->hops) o->hops[l] = h[1];
-            } else {  // single-hop ablation (recompute.hpp:166-176)
-                std::vector<double> qts(S);
-                KEEP_CUDA(cudaMemcpyAsync(qts.data(), bt.views[b]->summ.p, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+            } else {  // single-hop ablation (recompute.hpp:166-176): ranked on the device
+                upload(c.d_live, active[b], st);
+                c.d_next.ensure(size_t(S));
+                launch_single_hop(bt.views[b]->summ.as<double>(), c.d_live.as<uint8_t>(), S, budget,
+                                  c.d_next.as<uint8_t>(), st);
+                KEEP_CUDA(cudaMemcpyAsync(next.data(), c.d_next.p, size_t(S), cudaMemcpyDeviceToHost, st));
                 KEEP_CUDA(cudaStreamSynchronize(st));
-                std::vector<int> ord;
-                for (int i = 0; i < S; ++i)
-                    if (active[b][i]) ord.push_back(i);
-                std::stable_sort(ord.begin(), ord.end(), [&](int a, int z) { return qts[a] > qts[z]; });
-                for (size_t i = 0; i < size_t(budget) && i < ord.size(); ++i) next[ord[i]] = 1;
             }
             active[b] = std::move(next);
         }
@@ -2157,51 +2155,80 @@ int keep_memory_compute_batch(void* ctx, int32_t n_owners, const keep_owner* own
     });
 }
 
+namespace {
+// CacheManager::load (cache_manager.hpp:103-130).  A slow-tier block is copied
+// to HBM on the copy stream and the owner promoted; async: the copies are
+// only enqueued (c.ev_b completes them), the old host arena is held until then.
+void load_memory_impl(Context& c, keep_owner owner, int32_t layer, keep_kv_view* out, bool async) {
+    ++c.store_gen;
+    const OwnerKey k{owner.kind, owner.id};
+    const Payload* pl = nullptr;
+    if (!block_current(c, k, layer, &pl)) {  // cache_manager.hpp:104-116
+        c.stats.cache_misses++;
+        const bool absent = c.store.find(k) == c.store.end();
+        raise(KEEP_ERR_CACHE_MISS, std::string(absent ? "no block for " : "stale block for ") + owner_str(k) +
+                                       " layer " + std::to_string(layer));
+    }
+    Payload& P = c.store[k];
+    out->tokens = P.tokens;
+    out->elem_bytes = c.elem;
+    out->tier = P.arena->tier;
+    out->load_ms = 0.0;
+    out->row_elems = c.dl;
+    out->col0 = c.R * c.dl;
+    if (!async) c.load_hold.clear();
+    KEEP_CUDA(cudaEventRecord(c.ev_a, c.s_copy));
+    if (P.arena->tier == KEEP_TIER_HOST) {
+        // slow tier: copy the block to HBM and promote the owner (117-127)
+        const size_t blk = size_t(P.tokens) * c.dl * c.elem;
+        auto dev = make_arena(c, P.tokens, KEEP_TIER_DEVICE);
+        Payload np;
+        np.arena = dev;
+        np.tokens = P.tokens;
+        np.layer_version = P.layer_version;
+        np.present = P.present;
+        for (int l = 0; l < c.L; ++l) {
+            if (!np.present[l]) continue;
+            KEEP_CUDA(cudaMemcpyAsync(layer_keys(c, np, l), layer_keys(c, P, l), blk, cudaMemcpyDefault, c.s_copy));
+            KEEP_CUDA(cudaMemcpyAsync(layer_values(c, np, l), layer_values(c, P, l), blk, cudaMemcpyDefault, c.s_copy));
+            if (l < P.arena->mirror_from) c.stats.bytes_loaded_slow += 2 * blk;
+        }
+        c.load_hold.push_back(P.arena);  // the source stays alive until the copies complete
+        c.store[k] = std::move(np);
+    }
+    KEEP_CUDA(cudaEventRecord(c.ev_b, c.s_copy));
+    if (async) {
+        out->load_ms = -1.0;  // (measured only by the blocking form)
+    } else {
+        KEEP_CUDA(cudaEventSynchronize(c.ev_b));
+        float ms = 0.f;
+        KEEP_CUDA(cudaEventElapsedTime(&ms, c.ev_a, c.ev_b));
+        out->load_ms = out->tier == KEEP_TIER_HOST ? ms : 0.0;
+        c.load_hold.clear();
+    }
+    const Payload& Q = c.store[k];
+    out->keys = layer_keys(c, Q, layer);
+    out->values = layer_values(c, Q, layer);
+}
+}  // namespace
+
 int keep_load_memory(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* out) {
+    return guard([&] { load_memory_impl(*C(ctx), owner, layer, out, false); });
+}
+
+int keep_load_memory_async(void* ctx, keep_owner owner, int32_t layer, keep_kv_view* out, void** done) {
     return guard([&] {
         Context& c = *C(ctx);
-        ++c.store_gen;
-        const OwnerKey k{owner.kind, owner.id};
-        const Payload* pl = nullptr;
-        if (!block_current(c, k, layer, &pl)) {  // cache_manager.hpp:104-116
-            c.stats.cache_misses++;
-            const bool absent = c.store.find(k) == c.store.end();
-            raise(KEEP_ERR_CACHE_MISS, std::string(absent ? "no block for " : "stale block for ") + owner_str(k) +
-                                           " layer " + std::to_string(layer));
-        }
-        Payload& P = c.store[k];
-        out->tokens = P.tokens;
-        out->elem_bytes = c.elem;
-        out->tier = P.arena->tier;
-        out->load_ms = 0.0;
-        out->row_elems = c.dl;
-        out->col0 = c.R * c.dl;
-        if (P.arena->tier == KEEP_TIER_HOST) {
-            // slow tier: copy the block to HBM and promote the owner (117-127)
-            const size_t blk = size_t(P.tokens) * c.dl * c.elem;
-            auto dev = make_arena(c, P.tokens, KEEP_TIER_DEVICE);
-            Payload np;
-            np.arena = dev;
-            np.tokens = P.tokens;
-            np.layer_version = P.layer_version;
-            np.present = P.present;
-            KEEP_CUDA(cudaEventRecord(c.ev_a, c.s_copy));
-            for (int l = 0; l < c.L; ++l) {
-                if (!np.present[l]) continue;
-                KEEP_CUDA(cudaMemcpyAsync(layer_keys(c, np, l), layer_keys(c, P, l), blk, cudaMemcpyDefault, c.s_copy));
-                KEEP_CUDA(cudaMemcpyAsync(layer_values(c, np, l), layer_values(c, P, l), blk, cudaMemcpyDefault, c.s_copy));
-                if (l < P.arena->mirror_from) c.stats.bytes_loaded_slow += 2 * blk;
-            }
-            KEEP_CUDA(cudaEventRecord(c.ev_b, c.s_copy));
-            KEEP_CUDA(cudaEventSynchronize(c.ev_b));
-            float ms = 0.f;
-            KEEP_CUDA(cudaEventElapsedTime(&ms, c.ev_a, c.ev_b));
-            out->load_ms = ms;
-            c.store[k] = std::move(np);
-        }
-        const Payload& Q = c.store[k];
-        out->keys = layer_keys(c, Q, layer);
-        out->values = layer_values(c, Q, layer);
+        load_memory_impl(c, owner, layer, out, true);
+        if (done) *done = c.ev_b;
+    });
+}
+
+int keep_load_wait(void* ctx) {
+    return guard([&] {
+        Context& c = *C(ctx);
+        KEEP_CUDA(cudaEventSynchronize(c.ev_b));
+        c.load_hold.clear();
     });
 }
 
@@ -2612,15 +2639,12 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
                 if (out && out->orders) std::copy(hbuf + 2, hbuf + 2 + hbuf[0], out->orders + size_t(l) * S);
                 if (out && out->order_len) out->order_len[l] = hbuf[0];
                 if (out && out->hops) out->hops[l] = hbuf[1];
-            } else {  // single-hop ablation (recompute.hpp:166-176)
-                std::vector<double> qts(S);
-                KEEP_CUDA(cudaMemcpyAsync(qts.data(), p.summ.p, sizeof(double) * S, cudaMemcpyDeviceToHost, st));
+            } else {  // single-hop ablation (recompute.hpp:166-176): ranked on the device
+                upload(c.d_live, active, st);
+                c.d_next.ensure(size_t(S));
+                launch_single_hop(p.summ.as<double>(), c.d_live.as<uint8_t>(), S, budget, c.d_next.as<uint8_t>(), st);
+                KEEP_CUDA(cudaMemcpyAsync(next.data(), c.d_next.p, size_t(S), cudaMemcpyDeviceToHost, st));
                 KEEP_CUDA(cudaStreamSynchronize(st));
-                std::vector<int> ord;
-                for (int i = 0; i < S; ++i)
-                    if (active[i]) ord.push_back(i);
-                std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return qts[a] > qts[b]; });
-                for (size_t i = 0; i < size_t(budget) && i < ord.size(); ++i) next[ord[i]] = 1;
             }
             active = std::move(next);
         }

@@ -306,6 +306,8 @@ struct Context {
     bool exact = false;  // KEEP_NUMERICS_PARITY_EXACT: DFMA projections + reference-order scores
     double rope_theta = 0.0;  // keep_set_rope: 0 = NoPE, the reference (model.hpp:3-8)
     uint64_t hbm_budget = 0;  // keep_memory_residency: HBM capacity for pinned-host memory layers
+    std::vector<std::shared_ptr<Arena>> load_hold;  // sources of in-flight asynchronous loads
+    DevBuf d_live, d_next;                          // single-hop ablation: live mask in, kept mask out
     int elem = 4;  // merged-KV element bytes
     cudaStream_t s_main = nullptr, s_copy = nullptr, s_sel = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;

@@ -54,6 +54,8 @@ void launch_summary_reduce(const TB* rowbin, int S, const int32_t* seg_cbeg, con
                            cudaStream_t st);
 
 // K7: converge on the device (recompute.hpp:86-138).
+void launch_single_hop(const double* qts, const uint8_t* live, int S, int64_t budget, uint8_t* next,
+                       cudaStream_t st);
 void launch_select(int S, const double* qts, const double* sts, int64_t budget,
                    const uint8_t* candidates, int32_t* order, int32_t* n_out, int32_t* hops_out,
                    cudaStream_t st, int max_hops = 0);  // max_hops > 0: capped walk (BASELINE configs[3])

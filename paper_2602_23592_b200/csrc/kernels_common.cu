@@ -574,6 +574,30 @@ void launch_select_batch(int S, int B, const double* const* summ, int64_t budget
     KEEP_LAUNCH_CHECK();
 }
 
+// single-hop ablation (recompute.hpp:166-176): the live segments stable-sorted
+// by qts descending, the first `budget` kept -- as a rank per segment:
+// rank(i) = #{live j : qts[j] > qts[i], or qts[j] == qts[i] and j < i}
+__global__ void single_hop_kernel(const double* __restrict__ qts, const uint8_t* __restrict__ live, int S,
+                                  int64_t budget, uint8_t* __restrict__ next) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < S; i += gridDim.x * blockDim.x) {
+        if (!live[i]) {
+            next[i] = 0;
+            continue;
+        }
+        const double q = qts[i];
+        int64_t rank = 0;
+        for (int j = 0; j < S; ++j) rank += live[j] && (qts[j] > q || (qts[j] == q && j < i));
+        next[i] = rank < budget ? 1 : 0;
+    }
+}
+
+void launch_single_hop(const double* qts, const uint8_t* live, int S, int64_t budget, uint8_t* next,
+                       cudaStream_t st) {
+    single_hop_kernel<<<unsigned(std::max(1, std::min(int(ceil_div(S, 128)), kNumSMs * 4))), 128, 0, st>>>(
+        qts, live, S, budget, next);
+    KEEP_LAUNCH_CHECK();
+}
+
 void launch_select(int S, const double* qts, const double* sts, int64_t budget,
                    const uint8_t* candidates, int32_t* order, int32_t* n_out, int32_t* hops_out,
                    cudaStream_t st, int max_hops) {

@@ -242,6 +242,29 @@ def test_host_tier_load(ko, golden, ctx_cache):
     assert rel(k, ref[1, 0, starts[2]:starts[3]]) <= HIDDEN_RTOL
 
 
+def test_host_tier_load_async(ko, golden, ctx_cache):
+    """keep_load_memory_async: the promotion copy is only enqueued; after the
+    completion event the HBM block equals the canonical KV."""
+    c = golden["instances"][1]
+    p = problem(ko, c)
+    ctx = gpu_ctx(ctx_cache, c)
+    lay = layout_of(p)
+    ctx.memory_compute_layout(lay, version=4, tier=kb.TIER_HOST)
+    owner = (kb.SEGMENT, 3) if (kb.SEGMENT, 3) in [(o[0], o[1]) for o in lay.owners()] else lay.owners()[-1][:2]
+    v, ev = ctx.load_memory_async(owner[0], owner[1], 0)
+    assert ev and v.tier == kb.TIER_HOST and v.load_ms < 0
+    ctx.load_wait()
+    assert ctx.load_memory(owner[0], owner[1], 0).tier == kb.TIER_DEVICE  # promoted
+    w = ko.model_init(c["L"], c["H"], c["d"], c["mlp"], c["V"], c["seed"])
+    ref = ko.canonical_kv(p, w)
+    starts = np.concatenate([[0], np.cumsum(p.seg_len)])
+    b, e = [(o[2], o[3]) for o in lay.owners() if (o[0], o[1]) == tuple(owner)][0]
+    n = int(starts[e] - starts[b])
+    k, vv = ctx.memory_read(owner[0], owner[1], 0, n)
+    assert rel(k, ref[0, 0, starts[b]:starts[e]]) <= HIDDEN_RTOL
+    assert rel(vv, ref[0, 1, starts[b]:starts[e]]) <= HIDDEN_RTOL
+
+
 def test_determinism(ko, golden, ctx_cache):
     c = golden["instances"][-3]
     p = problem(ko, c)
