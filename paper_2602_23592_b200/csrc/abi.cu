@@ -509,6 +509,20 @@ void plan_splits(Context& c, Pass& p) {
     p.split_count = ns;
 }
 
+// MLP rows per chunk: the hidden activation [rows x f] is bounded (4 GB), so a
+// batch of queries with ~10^5 active rows each (BASELINE configs[4]) does not
+// need a [rows x f] buffer of tens of GB; chunks of >= 32K rows keep the
+// GEMMs in their full-wave regime
+size_t mlp_chunk_rows(const Context& c) {
+    static const size_t forced = [] {  // tests: small chunks at test sizes
+        const char* e = std::getenv("KEEP_MLP_CHUNK_ROWS");
+        return e ? size_t(std::max(1, std::atoi(e))) : size_t(0);
+    }();
+    if (forced) return forced;
+    const size_t es = c.fast ? 2 : 4;
+    return std::max<size_t>(32768, (size_t(4) << 30) / (es * size_t(c.f)));
+}
+
 void ensure_layer_scratch(Context& c, Pass& p) {
     const size_t n = size_t(std::max(p.n, 1));
     // sharded: ctx rows padded to G equal row blocks (all-to-all), Wo / MLP on one block
@@ -516,7 +530,7 @@ void ensure_layer_scratch(Context& c, Pass& p) {
     const size_t es = c.fast ? 2 : 4;
     ensure_headroom(p.q, es * n * c.dl);
     ensure_headroom(c.fast ? p.ctxb : p.ctx, es * cpr * c.G * c.dl);
-    ensure_headroom(c.fast ? p.hb : p.h, es * cpr * c.f);
+    ensure_headroom(c.fast ? p.hb : p.h, es * std::min<size_t>(cpr, mlp_chunk_rows(c)) * c.f);
     if (c.G > 1) {
         p.xrecv.ensure(es * cpr * c.G * c.dl);
         p.xrows.ensure(es * cpr * c.d);
@@ -818,15 +832,22 @@ void layer_dense(Context& c, Pass& p, int l) {
                 launch_gemm_parity(static_cast<const float*>(ctx_rows), d, static_cast<const float*>(c.wslot(l, W_O)), d, m,
                                    d, d, eo, st, c.oz, c.exact);
             }
-            {
-                ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
-                EpiArgs ei{EPI_RELU, d, p.h.as<float>(), f, nullptr, nullptr, nullptr, nullptr};
-                launch_gemm_parity(xr, d, static_cast<const float*>(c.wslot(l, W_IN)), f, m, f, d, ei, st, c.oz, c.exact);
-            }
-            {
-                ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
-                launch_gemm_parity(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, m, d, f, eo, st, c.oz,
-                                   c.exact);
+            const int mc = int(std::min<size_t>(size_t(m), mlp_chunk_rows(c)));
+            for (int q0 = 0; q0 < m; q0 += mc) {  // row chunks: the hidden buffer stays bounded
+                const int mq = std::min(mc, m - q0);
+                float* xq = xr + int64_t(q0) * d;
+                {
+                    ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi * mq / m, bi);
+                    EpiArgs ei{EPI_RELU, d, p.h.as<float>(), f, nullptr, nullptr, nullptr, nullptr};
+                    launch_gemm_parity(xq, d, static_cast<const float*>(c.wslot(l, W_IN)), f, mq, f, d, ei, st, c.oz,
+                                       c.exact);
+                }
+                {
+                    ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi * mq / m, bout);
+                    EpiArgs eq{EPI_RESID, d, xq, d, nullptr, nullptr, nullptr, nullptr};
+                    launch_gemm_parity(p.h.as<float>(), f, static_cast<const float*>(c.wslot(l, W_OUT)), d, mq, d, f, eq, st,
+                                       c.oz, c.exact);
+                }
             }
         } else {
             auto* xbr = p.xb.as<__nv_bfloat16>() + int64_t(r0) * d;
@@ -837,15 +858,21 @@ void layer_dense(Context& c, Pass& p, int l) {
                 launch_gemm_bf16(static_cast<const __nv_bfloat16*>(ctx_rows), d,
                                  static_cast<const __nv_bfloat16*>(c.wslot(l, W_O)), d, m, d, d, eo, st, mc);
             }
-            {
-                ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi, bi);
-                EpiArgs ei{EPI_RELU, d, nullptr, f, nullptr, nullptr, nullptr, p.hb.as<__nv_bfloat16>()};
-                launch_gemm_bf16(xbr, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_IN)), d, m, f, d, ei, st, mc);
-            }
-            {
-                ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi, bout);
-                launch_gemm_bf16(p.hb.as<__nv_bfloat16>(), f, static_cast<const __nv_bfloat16*>(c.wslot(l, W_OUT)), f, m, d,
-                                 f, eo, st, mc);
+            const int rc = int(std::min<size_t>(size_t(m), mlp_chunk_rows(c)));
+            for (int q0 = 0; q0 < m; q0 += rc) {  // row chunks: the hidden buffer stays bounded
+                const int mq = std::min(rc, m - q0);
+                {
+                    ProfScope ps(c.prof, KEEP_PROF_MLP_IN, st, gi * mq / m, bi);
+                    EpiArgs ei{EPI_RELU, d, nullptr, f, nullptr, nullptr, nullptr, p.hb.as<__nv_bfloat16>()};
+                    launch_gemm_bf16(xbr + int64_t(q0) * d, d, static_cast<const __nv_bfloat16*>(c.wslot(l, W_IN)), d, mq,
+                                     f, d, ei, st, mc);
+                }
+                {
+                    ProfScope ps(c.prof, KEEP_PROF_MLP_OUT, st, gi * mq / m, bout);
+                    EpiArgs eq{EPI_RESID, d, xr + int64_t(q0) * d, d, nullptr, nullptr, nullptr, xbr + int64_t(q0) * d};
+                    launch_gemm_bf16(p.hb.as<__nv_bfloat16>(), f, static_cast<const __nv_bfloat16*>(c.wslot(l, W_OUT)), f,
+                                     mq, d, f, eq, st, mc);
+                }
             }
         }
     }
