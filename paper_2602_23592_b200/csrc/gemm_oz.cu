@@ -17,11 +17,14 @@
 //    on the symmetric residues of A' and B' (|r| <= 128), accumulated EXACTLY
 //    in int32 TMEM (tcgen05.mma kind::i8; K 2^14 < 2^31);
 //  * X is rebuilt from its residues by Garner's algorithm -- mixed-radix
-//    digits v_i in small exact fp32 arithmetic, computed tile by tile as the
-//    residues arrive (v_i needs v_0..v_{i-1}, kept as int8 in a per-CTA
-//    scratch) -- and Horner in fp64 from the top digit
-//    (X = v_0 + m_0 (v_1 + m_1 (...))), then scaled by 2^-(ea+eb) and rounded
-//    once to fp32: the reference's "fp64 accumulate, cast".
+//    digits v_i, computed tile by tile as the residues arrive (v_i needs
+//    v_0..v_{i-1}, kept as int8 in a per-CTA scratch): v_i = (r_i - sum_j v_j
+//    (W_j mod m_i)) (W_i^-1 mod m_i) mod m_i, the sum exact in int32 with
+//    four digits per dp4a, the two reductions in exact fp32 -- and Horner in
+//    fp64 from the top digit (X = v_0 + m_0 (v_1 + m_1 (...))), then scaled
+//    by 2^-(ea+eb) and rounded once to fp32: the reference's "fp64
+//    accumulate, cast".  (The sequential form, u dependent fp32 steps per
+//    digit, left the tensor pipe idle ~25% of the time at 14 moduli.)
 //
 // b is the largest integer with K 2^2b < M/4 (M = prod m_i), so the symmetric
 // CRT range holds X with margin: with the default 14 moduli (110 bits) b = 47
@@ -65,7 +68,9 @@ struct OzCrt {
     float rcp[kMaxModuli];      // 1 / m_i (fp32)
     double md[kMaxModuli];      // m_i
     double rcpd[kMaxModuli];    // 1 / m_i (fp64)
-    float inv[kMaxModuli][kMaxModuli];  // inv[j][i] = m_j^-1 mod m_i (j < i)
+    int dpk[kMaxModuli][kMaxModuli / 4];  // byte k of dpk[u][g] = W_{4g+k} mod m_u, symmetric (0 for 4g+k >= u)
+    int dcorr[kMaxModuli];              // 128 sum_j (W_j mod m_u): the digits' +128 bias through the dot product
+    float winv[kMaxModuli];             // W_u^-1 mod m_u (symmetric), W_u = m_0 ... m_{u-1}
 };
 
 // kind::i8 instruction descriptor: D s32, A / B signed 8-bit, both K-major.
@@ -204,6 +209,13 @@ constexpr float kByteBias = 8388736.0f;  // 2^23 + 128
 __device__ __forceinline__ float redm(float x, float m, float rc) {
     const float q = fmaf(x, rc, kMagic) - kMagic;
     return fmaf(-q, m, x);
+}
+
+// sum of the four products of the unsigned bytes of a and the signed bytes of b, plus c
+__device__ __forceinline__ int dp4a_us(uint32_t a, int b, int c) {
+    int d;
+    asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
 }
 
 // byte b of w (a digit v + 128) -> 2^23 + 128 + v as fp32
@@ -373,34 +385,55 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                         for (int j = 0; j < 32; ++j) tv[j] = tv[j] >= 0.5f * mf ? tv[j] - mf : tv[j];
                     }
                     uint32_t* vq = vs + size_t(ch * 8) * OBM;
-                    // Garner: t = (((r_u - v_0) c_0u - v_1) c_1u - ...) mod m_u; odd m_u,
-                    // so every step leaves the canonical symmetric residue.  The
-                    // digit words stream from the (L2-resident) scratch two steps
-                    // ahead of their use.
                     auto ld8 = [&](uint32_t(&w)[8], int jm) {
 #pragma unroll
                         for (int g = 0; g < 8; ++g) w[g] = vq[(size_t(jm) * (OBN / 4) + g) * OBM];
                     };
-                    auto gstep = [&](const uint32_t(&w)[8], int jm) {
-                        const float c = crt.inv[jm][u];
+                    // Garner as one dot product: with W_j = m_0 ... m_{j-1},
+                    //   v_u = (r_u - sum_{j<u} v_j (W_j mod m_u)) (W_u^-1 mod m_u)  mod m_u,
+                    // the sum exact in int32: four digits per dp4a (the stored digits are v + 128, unsigned;
+                    // the constants W_j mod m_u symmetric, signed; crt.dcorr[u] removes the bias), after a
+                    // 4 x 4 byte transpose of four digit words (digit-major, 4 columns each) into four
+                    // column words (4 digits each).  Two fp32 reductions per element instead of u
+                    // dependent steps.
+                    if (u > 0) {
+                        const int G = (u + 3) >> 2;  // digit groups 4g .. 4g+3 holding v_0 .. v_{u-1}
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            tv[j] = redm(((tv[j] + kByteBias) - byte_biased(w[j >> 2], j & 3)) * c, mf, rc);
-                    };
-                    uint32_t w0[8], w1[8], w2[8];
-                    if (u > 0) ld8(w0, 0);
-                    if (u > 1) ld8(w1, 1);
-#pragma unroll 1
-                    for (int jm = 0; jm < u; jm += 3) {
-                        if (jm + 2 < u) ld8(w2, jm + 2);
-                        gstep(w0, jm);
-                        if (jm + 1 >= u) break;
-                        if (jm + 3 < u) ld8(w0, jm + 3);
-                        gstep(w1, jm + 1);
-                        if (jm + 2 >= u) break;
-                        if (jm + 4 < u) ld8(w1, jm + 4);
-                        gstep(w2, jm + 2);
+                        for (int hf = 0; hf < 2; ++hf) {  // 16 columns = 4 column quads at a time
+                            uint32_t wd[kMaxModuli][4];
+#pragma unroll
+                            for (int j = 0; j < kMaxModuli; ++j)
+#pragma unroll
+                                for (int q = 0; q < 4; ++q)
+                                    wd[j][q] = (j < u) ? vq[(size_t(j) * (OBN / 4) + hf * 4 + q) * OBM] : 0u;
+                            int s[16];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) s[j] = -crt.dcorr[u];
+#pragma unroll
+                            for (int g = 0; g < kMaxModuli / 4; ++g)
+                                if (g < G) {
+                                    const int dk = crt.dpk[u][g];
+#pragma unroll
+                                    for (int q = 0; q < 4; ++q) {
+                                        const uint32_t a = wd[4 * g][q], b = wd[4 * g + 1][q], c = wd[4 * g + 2][q],
+                                                       e = wd[4 * g + 3][q];
+                                        const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+                                        const uint32_t t2 = __byte_perm(c, e, 0x5140), t3 = __byte_perm(c, e, 0x7362);
+                                        s[4 * q] = dp4a_us(__byte_perm(t0, t2, 0x5410), dk, s[4 * q]);
+                                        s[4 * q + 1] = dp4a_us(__byte_perm(t0, t2, 0x7632), dk, s[4 * q + 1]);
+                                        s[4 * q + 2] = dp4a_us(__byte_perm(t1, t3, 0x5410), dk, s[4 * q + 2]);
+                                        s[4 * q + 3] = dp4a_us(__byte_perm(t1, t3, 0x7632), dk, s[4 * q + 3]);
+                                    }
+                                }
+                            const float wi = crt.winv[u];
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                float& x = tv[hf * 16 + j];  // |r_u - s| < 2^19: redm stays canonical (odd m_u)
+                                x = redm(redm(x - float(s[j]), mf, rc) * wi, mf, rc);
+                            }
+                        }
                     }
+                    uint32_t w0[8], w1[8], w2[8];
                     if (!last) {
 #pragma unroll
                         for (int g = 0; g < 8; ++g) {
@@ -601,7 +634,20 @@ const OzCrt& crt_tables() {
             t.rcp[i] = 1.f / float(kModuliAll[i]);
             t.md[i] = double(kModuliAll[i]);
             t.rcpd[i] = 1.0 / double(kModuliAll[i]);
-            for (int j = 0; j < i; ++j) t.inv[j][i] = float(mod_inverse(kModuliAll[j], kModuliAll[i]));
+            // W_j mod m_i (j < i) and W_i^-1 mod m_i, as symmetric residues
+            const int mi = kModuliAll[i];
+            auto sym = [mi](long long a) {
+                const int r = int(((a % mi) + mi) % mi);
+                return r > mi / 2 ? r - mi : r;
+            };
+            long long w = 1;
+            for (int j = 0; j < i; ++j) {
+                const int dj = sym(w);
+                t.dpk[i][j / 4] = int(uint32_t(t.dpk[i][j / 4]) | ((uint32_t(dj) & 0xffu) << (8 * (j % 4))));
+                t.dcorr[i] += 128 * dj;
+                w = (w * kModuliAll[j]) % mi;
+            }
+            t.winv[i] = i == 0 ? 1.f : float(sym(mod_inverse(int(w), mi)));
         }
         return t;
     }();
