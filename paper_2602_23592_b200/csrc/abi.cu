@@ -643,6 +643,8 @@ void layer_attention(Context& c, Pass& p, int l, const void* q, void* ctx, const
         if (fits) {
             p.ebin.ensure(need);
             a.ebin = p.ebin.as<double>();
+            p.attn_flag.ensure(sizeof(int));
+            a.flag = p.attn_flag.as<int>();
         }
     }
 

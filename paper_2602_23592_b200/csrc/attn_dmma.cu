@@ -1157,6 +1157,37 @@ __global__ void max_combine_kernel(AttnArgs a) {
     }
 }
 
+// m_fin = the score of each row's own key (one warp per row and head; the
+// reference of the one-pass fused-bins context pass)
+template <int DH>
+__global__ void ref_score_kernel(AttnArgs a, double scale) {
+    const int64_t nh = int64_t(a.n) * a.H;
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5, nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const float* q = static_cast<const float*>(a.q);
+    const float* k = static_cast<const float*>(a.k);
+    for (int64_t e = w0; e < nh; e += nw) {
+        const int64_t row = e / a.H;
+        const int h = int(e % a.H);
+        const int t = a.rows[row];
+        double acc = 0.0;
+        for (int c = lane; c < DH; c += 32)
+            acc = fma(double(q[row * a.d + h * DH + c]), double(k[int64_t(t) * a.d + h * DH + c]), acc);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) a.m_fin[e] = acc * scale;
+    }
+}
+
+// one-pass check: every row sum finite and below 2^limit (600; KEEP_REF_MAX_LIMIT)
+__global__ void lsum_check_kernel(AttnArgs a, double limit) {
+    const int64_t nh = int64_t(a.n) * a.H;
+    bool bad = false;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nh; e += int64_t(gridDim.x) * blockDim.x)
+        bad |= !(a.l_fin[e] < limit);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1);
+}
+
 // CTX splits (all against m_fin): l_fin = sum of the split sums, ctx = sum o / l_fin
 __global__ void ctxl_combine_kernel(AttnArgs a, int dh) {
     const int64_t nd = int64_t(a.n) * a.d, nh = int64_t(a.n) * a.H;
@@ -1192,6 +1223,24 @@ __global__ void ebin_reduce_kernel(AttnArgs a) {
         }
         rowbin[e] = acc;
     }
+}
+
+bool ref_max_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_REF_MAX");  // A/B knob: 0 = the max pass before the context pass
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
+// log2 of the row-sum bound above which the one-pass layer reruns with the max pass
+// (tests set 0 to exercise the rerun)
+int ref_max_limit() {
+    static const int v = [] {
+        const char* e = std::getenv("KEEP_REF_MAX_LIMIT");
+        return e ? std::max(0, std::min(600, std::atoi(e))) : 600;
+    }();
+    return v;
 }
 
 bool dmma16_enabled() {
@@ -1408,6 +1457,39 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
             KEEP_LAUNCH_CHECK();
         }
         return;
+    }
+    if constexpr (DH >= 32) if (dmma_ws_enabled() && a.ebin && a.flag && ref_max_enabled()) {
+        // One pass: e = exp(s - m_ref) against the row's own (diagonal) key score instead of the
+        // row max, so no max pass.  p = e / sum e is the same up to fp64 rounding for any reference
+        // (e^(m - m_ref) cancels), the diagonal key is visible to its row (m_ref <= max: nothing
+        // underflows that the reference keeps), and the row sums bound every e and bin.  A sum at
+        // or above 2^600 (max - m_ref > ~415; o would risk overflow) reruns the layer below.
+        const int64_t nhw = int64_t(a.n) * a.H;
+        ref_score_kernel<DH><<<unsigned(std::min<int64_t>(ceil_div(nhw, 8), kNumSMs * 32)), 256, 0, st>>>(a, scale);
+        KEEP_LAUNCH_CHECK();
+        const dim3 g2{unsigned(ceil_div(a.n, WS_ROWS)), grid.y, grid.z};
+        const int smem = int(WsGeo<DH>::smem(true));
+        smem_attr(attn_dmma_ws_kernel<DH, M_CTX, true>, smem);
+        attn_dmma_ws_kernel<DH, M_CTX, true><<<g2, WS_THREADS, smem, st>>>(a, scale);
+        KEEP_LAUNCH_CHECK();
+        if (a.nsplit > 1) {
+            const int64_t nd = int64_t(a.n) * a.d;
+            ctxl_combine_kernel<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(a, DH);
+            KEEP_LAUNCH_CHECK();
+        }
+        KEEP_CUDA(cudaMemsetAsync(a.flag, 0, sizeof(int), st));
+        lsum_check_kernel<<<unsigned(std::min<int64_t>(ceil_div(nhw, 256), kNumSMs * 8)), 256, 0, st>>>(
+            a, std::ldexp(1.0, ref_max_limit()));
+        KEEP_LAUNCH_CHECK();
+        int over = 0;
+        KEEP_CUDA(cudaMemcpyAsync(&over, a.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        KEEP_CUDA(cudaStreamSynchronize(st));
+        if (!over) {
+            const int64_t nS = int64_t(a.n) * a.S;
+            ebin_reduce_kernel<<<unsigned(std::min<int64_t>(ceil_div(nS, 256), kNumSMs * 16)), 256, 0, st>>>(a);
+            KEEP_LAUNCH_CHECK();
+            return;
+        }
     }
     if (DH >= 32 && dmma_ws_enabled()) {
         // max-only stats; the context pass sums the exponentials (l_fin)

@@ -209,7 +209,7 @@ struct Pass {
     bool summary_global = true;   // sharded: sum the summary over ranks this layer
     bool summary_wanted = true;   // plan_keep: only layers whose summary is read compute it
     // attention scratch
-    DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi;
+    DevBuf m_part, l_part, m_fin, l_fin, o_part, rowbin, split_lo, split_hi, attn_flag;
     int split_count = 1;
     DevBuf split_lo_b, split_hi_b;  // PARITY DMMA bins pass: its own segment-aligned splits
     DevBuf rope_tab;                // RoPE hook: (row, rows, delta) of the re-shifted cached blocks

@@ -142,6 +142,7 @@ struct AttnArgs {
     double* ebin;
     const int32_t* seg_start;  // [S] first key of each segment
     int Tm;                    // first query key (keys >= Tm have row_seg -1)
+    int* flag;                 // [1] device scratch: the reference-score pass's overflow check
 };
 void launch_attention_parity(const AttnArgs& a, cudaStream_t st);
 // PARITY on the fp64 tensor cores (attn_dmma.cu): head_dim 8 / 16 / 32 / 64 / 128,
