@@ -63,6 +63,7 @@ constexpr int kModuliAll[kMaxModuli] = {256, 255, 253, 251, 247, 241, 239, 233, 
 // the modulus tables (kernel parameter: constant bank)
 struct OzCrt {
     int n;                      // moduli used
+    int gm;                     // tile raster: bands of gm row tiles (KEEP_OZ_GM, default OGM)
     int mi[kMaxModuli];         // m_i
     float mf[kMaxModuli];       // m_i
     float rcp[kMaxModuli];      // 1 / m_i (fp32)
@@ -145,11 +146,11 @@ constexpr int OSTAGES2 = 6;                            // pair: 32 KB stages
 constexpr uint32_t OB2_BYTES = 128 * OBK, OSTAGE2 = OA_BYTES + OB2_BYTES;
 constexpr size_t OSMEM2 = size_t(OSTAGES2) * OSTAGE2 + 1024 + 256;
 
-__device__ __forceinline__ void otile_coords(int t, int tiles_m, int tiles_n, int& mb, int& nb) {
-    const int band = t / (OGM * tiles_n);
-    const int m0 = band * OGM;
-    const int gm = min(OGM, tiles_m - m0);
-    const int r = t - band * OGM * tiles_n;
+__device__ __forceinline__ void otile_coords(int t, int tiles_m, int tiles_n, int ogm, int& mb, int& nb) {
+    const int band = t / (ogm * tiles_n);
+    const int m0 = band * ogm;
+    const int gm = min(ogm, tiles_m - m0);
+    const int r = t - band * ogm * tiles_n;
     mb = m0 + r % gm;
     nb = r / gm;
 }
@@ -276,7 +277,7 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             uint32_t phase = 0;
             for (int t = cid; t < ntiles; t += ncl) {
                 int mb, nb;
-                otile_coords(t, tiles_m, tiles_n, mb, nb);
+                otile_coords(t, tiles_m, tiles_n, crt.gm, mb, nb);
                 for (int u = 0; u < U; ++u) {
                     for (int kb = 0; kb < kblocks; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
@@ -354,7 +355,7 @@ gemm_oz_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         int it = 0;
         for (int t = cid; t < ntiles; t += ncl) {
             int mb, nb;
-            otile_coords(t, tiles_m, tiles_n, mb, nb);
+            otile_coords(t, tiles_m, tiles_n, crt.gm, mb, nb);
             const int m = mb * TM + rank * OBM + r;
             const bool mok = m < M;
             const int eam = mok ? ea[m] : 0;
@@ -507,14 +508,29 @@ __device__ __forceinline__ int scale_exp(float amax, int bits) {
     return bits - ex;
 }
 
-// symmetric residue of the integer-valued fp64 X (|X| <= 2^52) modulo m_i, in
-// fp64 without the conversion pipe: rint(X / m) by the 1.5 * 2^52 magic
-// constant (|X / m| < 2^51; X * (1/m) is within 2^-13 of X / m, which is at
-// least 1/(2m) from a half-integer for odd m, so the residue is canonical; m_0 =
-// 256 is exact and maps +128 to -128), the int8 read from the low word of
-// r + 1.5 * 2^52
+// X = rint(x 2^e) (|X| < 2^51) held as b = 1.5 * 2^52 + X: b - 1.5 * 2^52 is X
+// exactly, and the low word of b is X mod 2^32 (b's mantissa is 2^51 + X)
+struct OzInt {
+    double b;
+};
+constexpr double kM52 = 6755399441055744.0;  // 1.5 * 2^52
+__device__ __forceinline__ OzInt oz_int(float x, double pw) {
+    return {fma(double(x), pw, kM52)};  // x 2^e is exact: one rounding, to nearest even
+}
+
+// symmetric residue of X modulo m_i: q = rint(X / m) from one fma against the
+// 1.5 * 2^52 magic constant (X * (1/m) is within 2^-13 of X / m, which is at
+// least 1/(2m) from a half-integer for odd m, so the residue is canonical),
+// read as q mod 2^32 from its low word; then r = X - q m in wrapping int32
+// arithmetic (|r| < m).  m_0 = 256: the low byte of X (+128 -> -128).
+__device__ __forceinline__ uint32_t residue_word(const OzInt& X, const OzCrt& c, int i) {  // residue in the low byte
+    const int lo = __double2loint(X.b);
+    if (i == 0) return uint32_t(lo);
+    const int q = __double2loint(fma(X.b - kM52, c.rcpd[i], kM52));
+    return uint32_t(lo - q * c.mi[i]);
+}
+// the same residue from X alone, in fp64 (fewer live registers: the column split)
 __device__ __forceinline__ int8_t residue(double X, const OzCrt& c, int i) {
-    constexpr double kM52 = 6755399441055744.0;  // 1.5 * 2^52
     const double q = fma(X, c.rcpd[i], kM52) - kM52;
     double r = fma(-q, c.md[i], X);
     if (i == 0) r = r >= 128.0 ? r - 256.0 : r;
@@ -538,16 +554,13 @@ __global__ void oz_split_rows_kernel(const float* __restrict__ A, int64_t lda, i
     const size_t plane = size_t(Mp) * Kp;
     int8_t* o = out + size_t(warp) * Kp;
     for (int k0 = lane * 4; k0 < Kp; k0 += 128) {
-        double X[4];
+        OzInt X[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) X[q] = rint(double((k0 + q < K) ? a[k0 + q] : 0.f) * pw);
+        for (int q = 0; q < 4; ++q) X[q] = oz_int((k0 + q < K) ? a[k0 + q] : 0.f, pw);
         for (int i = 0; i < crt.n; ++i) {
-            char4 dg;
-            dg.x = residue(X[0], crt, i);
-            dg.y = residue(X[1], crt, i);
-            dg.z = residue(X[2], crt, i);
-            dg.w = residue(X[3], crt, i);
-            *reinterpret_cast<char4*>(o + i * plane + k0) = dg;
+            const uint32_t p01 = __byte_perm(residue_word(X[0], crt, i), residue_word(X[1], crt, i), 0x0040);
+            const uint32_t p23 = __byte_perm(residue_word(X[2], crt, i), residue_word(X[3], crt, i), 0x0040);
+            *reinterpret_cast<uint32_t*>(o + i * plane + k0) = __byte_perm(p01, p23, 0x5410);
         }
     }
 }
@@ -628,6 +641,8 @@ const OzCrt& crt_tables() {
     static const OzCrt c = [] {
         OzCrt t{};
         t.n = oz_moduli();
+        const char* g = std::getenv("KEEP_OZ_GM");
+        t.gm = g ? std::max(1, std::atoi(g)) : OGM;
         for (int i = 0; i < t.n; ++i) {
             t.mi[i] = kModuliAll[i];
             t.mf[i] = float(kModuliAll[i]);
