@@ -643,7 +643,7 @@ void layer_attention(Context& c, Pass& p, int l, const void* q, void* ctx, const
         if (fits) {
             p.ebin.ensure(need);
             a.ebin = p.ebin.as<double>();
-            p.attn_flag.ensure(sizeof(int));
+            p.attn_flag.ensure(16 + sizeof(double) * size_t(c.Hl));  // flag + per-head key-norm max
             a.flag = p.attn_flag.as<int>();
         }
     }

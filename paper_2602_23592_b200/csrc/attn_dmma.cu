@@ -1157,35 +1157,65 @@ __global__ void max_combine_kernel(AttnArgs a) {
     }
 }
 
-// m_fin = the score of each row's own key (one warp per row and head; the
-// reference of the one-pass fused-bins context pass)
+// kmax[h] = max over the layer's keys of |k_h| (fp64; non-negative doubles order
+// like their bit patterns, so an integer atomicMax reduces them)
 template <int DH>
-__global__ void ref_score_kernel(AttnArgs a, double scale) {
+__global__ void key_norm_max_kernel(AttnArgs a, double* kmax) {
+    __shared__ double wm[8];
+    const int h = blockIdx.y, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const float* k = static_cast<const float*>(a.k);
+    double mx = 0.0;
+    const int t0 = blockIdx.x * 256 + w * 32;  // this warp's 32 keys
+    for (int t = t0; t < min(a.T, t0 + 32); ++t) {
+        double acc = 0.0;
+        for (int c = lane; c < DH; c += 32) {
+            const double v = k[int64_t(t) * a.d + h * DH + c];
+            acc = fma(v, v, acc);
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        mx = fmax(mx, acc);
+    }
+    if (lane == 0) wm[w] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int i = 0; i < 8; ++i) m = fmax(m, wm[i]);
+        atomicMax(reinterpret_cast<unsigned long long*>(kmax + h), __double_as_longlong(sqrt(m) * (1.0 + 1e-12)));
+    }
+}
+
+// m_fin = the score of each row's own key (one warp per row and head; the
+// reference of the one-pass fused-bins context pass); flag[0] = 1 when some
+// row's bound |q| kmax / sqrt(dh) exceeds it by more than `limit`
+template <int DH>
+__global__ void ref_score_kernel(AttnArgs a, double scale, const double* kmax, double limit) {
     const int64_t nh = int64_t(a.n) * a.H;
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5, nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
     const float* q = static_cast<const float*>(a.q);
     const float* k = static_cast<const float*>(a.k);
+    bool over = false;
     for (int64_t e = w0; e < nh; e += nw) {
         const int64_t row = e / a.H;
         const int h = int(e % a.H);
         const int t = a.rows[row];
-        double acc = 0.0;
-        for (int c = lane; c < DH; c += 32)
-            acc = fma(double(q[row * a.d + h * DH + c]), double(k[int64_t(t) * a.d + h * DH + c]), acc);
+        double acc = 0.0, qq = 0.0;
+        for (int c = lane; c < DH; c += 32) {
+            const double qv = q[row * a.d + h * DH + c];
+            acc = fma(qv, double(k[int64_t(t) * a.d + h * DH + c]), acc);
+            qq = fma(qv, qv, qq);
+        }
 #pragma unroll
-        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) a.m_fin[e] = acc * scale;
+        for (int o = 16; o; o >>= 1) {
+            acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            qq += __shfl_xor_sync(0xffffffffu, qq, o);
+        }
+        const double m = acc * scale;
+        if (lane == 0) a.m_fin[e] = m;
+        over |= !(sqrt(qq) * kmax[h] * scale * (1.0 + 1e-12) - m <= limit);
     }
-}
-
-// one-pass check: every row sum finite and below 2^limit (600; KEEP_REF_MAX_LIMIT)
-__global__ void lsum_check_kernel(AttnArgs a, double limit) {
-    const int64_t nh = int64_t(a.n) * a.H;
-    bool bad = false;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < nh; e += int64_t(gridDim.x) * blockDim.x)
-        bad |= !(a.l_fin[e] < limit);
-    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.flag, 1);
+    if (over && lane == 0) atomicOr(a.flag, 1);
 }
 
 // CTX splits (all against m_fin): l_fin = sum of the split sums, ctx = sum o / l_fin
@@ -1233,12 +1263,13 @@ bool ref_max_enabled() {
     return on;
 }
 
-// log2 of the row-sum bound above which the one-pass layer reruns with the max pass
-// (tests set 0 to exercise the rerun)
+// the largest score excess over the row's own-key score the one-pass layer admits
+// (natural-log units; default 400; tests set 0 to force the max pass, or a huge value
+// to force the one pass on small-score instances)
 int ref_max_limit() {
     static const int v = [] {
         const char* e = std::getenv("KEEP_REF_MAX_LIMIT");
-        return e ? std::max(0, std::min(600, std::atoi(e))) : 600;
+        return e ? std::max(0, std::atoi(e)) : 400;
     }();
     return v;
 }
@@ -1461,30 +1492,32 @@ void run_dmma(const AttnArgs& a, cudaStream_t st) {
     if constexpr (DH >= 32) if (dmma_ws_enabled() && a.ebin && a.flag && ref_max_enabled()) {
         // One pass: e = exp(s - m_ref) against the row's own (diagonal) key score instead of the
         // row max, so no max pass.  p = e / sum e is the same up to fp64 rounding for any reference
-        // (e^(m - m_ref) cancels), the diagonal key is visible to its row (m_ref <= max: nothing
-        // underflows that the reference keeps), and the row sums bound every e and bin.  A sum at
-        // or above 2^600 (max - m_ref > ~415; o would risk overflow) reruns the layer below.
+        // (e^(m - m_ref) cancels) and the diagonal key is visible to its row (m_ref <= max: nothing
+        // underflows that the reference keeps).  Taken only when no score can exceed m_ref by more
+        // than 400 (Cauchy-Schwarz: s <= |q| max_k |k| / sqrt(dh)), so every e, row sum (< 2^14 e^400
+        // < 2^600) and o stays finite; otherwise (deep layers' scores reach ~1e18) the max pass below.
         const int64_t nhw = int64_t(a.n) * a.H;
-        ref_score_kernel<DH><<<unsigned(std::min<int64_t>(ceil_div(nhw, 8), kNumSMs * 32)), 256, 0, st>>>(a, scale);
+        double* kmax = reinterpret_cast<double*>(a.flag + 4);
+        KEEP_CUDA(cudaMemsetAsync(a.flag, 0, 16 + sizeof(double) * size_t(a.H), st));
+        key_norm_max_kernel<DH><<<dim3(unsigned(ceil_div(a.T, 256)), unsigned(a.H)), 256, 0, st>>>(a, kmax);
         KEEP_LAUNCH_CHECK();
-        const dim3 g2{unsigned(ceil_div(a.n, WS_ROWS)), grid.y, grid.z};
-        const int smem = int(WsGeo<DH>::smem(true));
-        smem_attr(attn_dmma_ws_kernel<DH, M_CTX, true>, smem);
-        attn_dmma_ws_kernel<DH, M_CTX, true><<<g2, WS_THREADS, smem, st>>>(a, scale);
-        KEEP_LAUNCH_CHECK();
-        if (a.nsplit > 1) {
-            const int64_t nd = int64_t(a.n) * a.d;
-            ctxl_combine_kernel<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(a, DH);
-            KEEP_LAUNCH_CHECK();
-        }
-        KEEP_CUDA(cudaMemsetAsync(a.flag, 0, sizeof(int), st));
-        lsum_check_kernel<<<unsigned(std::min<int64_t>(ceil_div(nhw, 256), kNumSMs * 8)), 256, 0, st>>>(
-            a, std::ldexp(1.0, ref_max_limit()));
+        ref_score_kernel<DH><<<unsigned(std::min<int64_t>(ceil_div(nhw, 8), kNumSMs * 32)), 256, 0, st>>>(
+            a, scale, kmax, double(ref_max_limit()));
         KEEP_LAUNCH_CHECK();
         int over = 0;
         KEEP_CUDA(cudaMemcpyAsync(&over, a.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
         KEEP_CUDA(cudaStreamSynchronize(st));
         if (!over) {
+            const dim3 g2{unsigned(ceil_div(a.n, WS_ROWS)), grid.y, grid.z};
+            const int smem = int(WsGeo<DH>::smem(true));
+            smem_attr(attn_dmma_ws_kernel<DH, M_CTX, true>, smem);
+            attn_dmma_ws_kernel<DH, M_CTX, true><<<g2, WS_THREADS, smem, st>>>(a, scale);
+            KEEP_LAUNCH_CHECK();
+            if (a.nsplit > 1) {
+                const int64_t nd = int64_t(a.n) * a.d;
+                ctxl_combine_kernel<<<unsigned(std::min<int64_t>(ceil_div(nd, 256), kNumSMs * 16)), 256, 0, st>>>(a, DH);
+                KEEP_LAUNCH_CHECK();
+            }
             const int64_t nS = int64_t(a.n) * a.S;
             ebin_reduce_kernel<<<unsigned(std::min<int64_t>(ceil_div(nS, 256), kNumSMs * 16)), 256, 0, st>>>(a);
             KEEP_LAUNCH_CHECK();
