@@ -187,6 +187,107 @@ __global__ void __launch_bounds__(256) gemm_f64_skinny_kernel(const float* __res
     }
 }
 
+// ------------------------------------------------------------ weight stream --
+// PARITY (split-K allowed) for M <= 32: a warp owns 32 CPL columns (CPL
+// consecutive floats per lane: 128 CPL contiguous bytes per k-row) and streams
+// its B strip through its own 3-stage cp.async ring in shared memory (8 k-rows
+// per stage; each lane reads back only the bytes it copied, so no barrier);
+// A's MR rows of the CTA's k-range are widened once into shared memory and read
+// as broadcast k-pairs.  MR x CPL independent fp64 chains per lane in
+// ascending k.  CTA = 8 warps; grid (column blocks, k splits, row groups).
+constexpr int WS_UN = 8, WS_ST = 3, WS_KMAX = 512;
+
+template <int CPL>
+__device__ __forceinline__ void cpa_b(void* dst, const void* src, bool ok) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    if constexpr (CPL == 4)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+
+size_t stream_smem(int MR, int CPL, int kchunk) {
+    return sizeof(double) * size_t(MR) * kchunk + sizeof(float) * size_t(8) * WS_ST * WS_UN * 32 * CPL;
+}
+
+template <int MR, int CPL>
+__global__ void __launch_bounds__(256, 2) gemm_f64_stream_kernel(const float* __restrict__ A, int64_t lda,
+                                                              const float* __restrict__ B, int64_t ldb, int M, int N,
+                                                              int K, int kchunk, double* __restrict__ part,
+                                                              EpiArgs epi) {
+    constexpr int WC = 32 * CPL;  // columns per warp
+    extern __shared__ __align__(16) double as[];  // [MR][kchunk], then the warps' B rings
+    const int kbeg = blockIdx.y * kchunk, kn = min(K, kbeg + kchunk) - kbeg;
+    const int m0 = blockIdx.z * MR, mr = min(MR, M - m0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = (blockIdx.x * 8 + warp) * WC + CPL * lane;
+    const bool nok = n < N;
+    float* ring = reinterpret_cast<float*>(as + MR * kchunk) + warp * (WS_ST * WS_UN * WC) + CPL * lane;
+    const float* bp = B + int64_t(kbeg) * ldb + (nok ? n : 0);
+    const int nit = int(ceil_div(kn, WS_UN));
+    auto issue = [&](int it) {  // k-rows 8 it .. 8 it + 7 into stage it % WS_ST
+        if (it < nit) {
+            float* dst = ring + (it % WS_ST) * (WS_UN * WC);
+#pragma unroll
+            for (int u = 0; u < WS_UN; ++u) {
+                const int k = it * WS_UN + u;
+                cpa_b<CPL>(dst + u * WC, bp + int64_t(k < kn ? k : 0) * ldb, nok && k < kn);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    for (int it = 0; it < WS_ST - 1; ++it) issue(it);
+    for (int e = threadIdx.x; e < MR * kchunk; e += 256) {
+        const int r = e / kchunk, k = e - r * kchunk;
+        as[e] = (r < mr && k < kn) ? double(A[int64_t(m0 + r) * lda + kbeg + k]) : 0.0;
+    }
+    __syncthreads();
+    double acc[MR][CPL];
+#pragma unroll
+    for (int r = 0; r < MR; ++r)
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) acc[r][c] = 0.0;
+    for (int it = 0; it < nit; ++it) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(WS_ST - 2) : "memory");
+        const float* src = ring + (it % WS_ST) * (WS_UN * WC);
+        issue(it + WS_ST - 1);  // into the stage read in the previous iteration
+#pragma unroll
+        for (int u = 0; u < WS_UN; u += 2) {  // rows past kn are zero-filled (0 * a adds nothing)
+            const int k = it * WS_UN + u;
+            double b0[CPL], b1[CPL];
+            if constexpr (CPL == 4) {
+                const float4 v0 = *reinterpret_cast<const float4*>(src + u * WC);
+                const float4 v1 = *reinterpret_cast<const float4*>(src + (u + 1) * WC);
+                b0[0] = v0.x, b0[1] = v0.y, b0[2] = v0.z, b0[3] = v0.w;
+                b1[0] = v1.x, b1[1] = v1.y, b1[2] = v1.z, b1[3] = v1.w;
+            } else {
+                const float2 v0 = *reinterpret_cast<const float2*>(src + u * WC);
+                const float2 v1 = *reinterpret_cast<const float2*>(src + (u + 1) * WC);
+                b0[0] = v0.x, b0[1] = v0.y;
+                b1[0] = v1.x, b1[1] = v1.y;
+            }
+#pragma unroll
+            for (int r = 0; r < MR; ++r) {
+                const double2 a = *reinterpret_cast<const double2*>(as + r * kchunk + k);
+#pragma unroll
+                for (int c = 0; c < CPL; ++c) acc[r][c] = fma(a.y, b1[c], fma(a.x, b0[c], acc[r][c]));
+            }
+        }
+    }
+    if (!nok) return;
+#pragma unroll
+    for (int r = 0; r < MR; ++r) {
+        if (r >= mr) break;
+        const int m = m0 + r;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+            if (part) part[(int64_t(blockIdx.y) * M + m) * N + n + c] = acc[r][c];
+            else if (epi.kind == EPI_F64) reinterpret_cast<double*>(epi.out)[int64_t(m) * epi.ldo + n + c] = acc[r][c];
+            else epi_store1(epi, m, n + c, static_cast<float>(acc[r][c]));
+        }
+    }
+}
+
 // split-K finish: the k-range partials summed in ascending split order
 // (deterministic), one rounding to fp32, the fused epilogue
 __global__ void f64_splitk_finish_kernel(const double* __restrict__ part, int ks, int M, int N, EpiArgs epi) {
@@ -197,6 +298,15 @@ __global__ void f64_splitk_finish_kernel(const double* __restrict__ part, int ks
         if (epi.kind == EPI_F64) reinterpret_cast<double*>(epi.out)[(e / N) * epi.ldo + e % N] = acc;
         else epi_store1(epi, int(e / N), int(e % N), static_cast<float>(acc));
     }
+}
+
+// KEEP_PARITY_STREAM=0: the smem-staged skinny kernel for PARITY's few rows too (A/B)
+bool stream_f64_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_PARITY_STREAM");
+        return !(e && *e == '0');
+    }();
+    return on;
 }
 
 // KEEP_PARITY_SKINNY=0: the tiled kernel for few rows too (A/B)
@@ -231,6 +341,34 @@ void launch_gemm_f64acc(const float* A, int64_t lda, const float* B, int64_t ldb
                         const EpiArgs& epi, cudaStream_t st, bool exact) {
     if (M == 0 || N == 0) return;
     // few rows: the weight stream (16-byte cp.async needs 16-byte aligned rows)
+    if (!exact && M <= 32 && stream_f64_enabled() && N % 4 == 0 && ldb % 4 == 0 &&
+        reinterpret_cast<uintptr_t>(B) % 16 == 0) {
+        // PARITY: the weight stream, split K over ~2 resident CTAs per SM; 4 columns
+        // per lane for up to 8 rows, 2 for up to 16 (register budget)
+        const int MR = M <= 8 ? 8 : 16, CPL = MR == 8 ? 4 : 2;
+        const int nct = int(ceil_div(N, 256 * CPL)), ng = int(ceil_div(M, MR));
+        int ks = int(std::max<int64_t>(ceil_div(K, WS_KMAX), std::min<int64_t>(ceil_div(4 * kNumSMs, int64_t(nct) * ng),
+                                                                                   std::max(1, K / 128))));
+        const int kchunk = int(ceil_div(ceil_div(K, ks), WS_UN) * WS_UN);
+        ks = int(ceil_div(K, kchunk));
+        double* part = ks > 1 ? f64_splitk_workspace(sizeof(double) * size_t(ks) * M * N, st) : nullptr;
+        const dim3 grid{unsigned(nct), unsigned(ks), unsigned(ng)};
+        const size_t smem = stream_smem(MR, CPL, kchunk);
+        if (MR == 8) {
+            smem_attr(gemm_f64_stream_kernel<8, 4>, int(smem));
+            gemm_f64_stream_kernel<8, 4><<<grid, 256, smem, st>>>(A, lda, B, ldb, M, N, K, kchunk, part, epi);
+        } else {
+            smem_attr(gemm_f64_stream_kernel<16, 2>, int(smem));
+            gemm_f64_stream_kernel<16, 2><<<grid, 256, smem, st>>>(A, lda, B, ldb, M, N, K, kchunk, part, epi);
+        }
+        KEEP_LAUNCH_CHECK();
+        if (ks > 1) {
+            f64_splitk_finish_kernel<<<unsigned(std::min<int64_t>(ceil_div(int64_t(M) * N, 256), kNumSMs * 4)), 256, 0,
+                                       st>>>(part, ks, M, N, epi);
+            KEEP_LAUNCH_CHECK();
+        }
+        return;
+    }
     if (M <= 32 && skinny_f64_enabled() && K % 4 == 0 && N % 4 == 0 && lda % 4 == 0 && ldb % 4 == 0) {
         const int nct = int(ceil_div(N, SK_NC));
         // split K over enough CTAs to keep ~4 per SM streaming (a lone 32-column

@@ -3,6 +3,7 @@
 // integer/fp64 work: coalesced 16-byte accesses, grids sized in SM multiples.
 #include <cstring>
 #include <mutex>
+#include <map>
 #include <set>
 #include <tuple>
 #include "kernels.hpp"
@@ -12,13 +13,18 @@
 namespace keep_b200 {
 
 void set_smem_attr(const void* fn, int bytes) {
+    // the attribute only grows: a kernel launched with varying dynamic smem keeps
+    // the largest opt-in it has seen on this device (lowering it after a larger
+    // size was cached would fail the next larger launch)
     static std::mutex mu;
-    static std::set<std::tuple<const void*, int, int>> done;
+    static std::map<std::pair<const void*, int>, int> seen;
     int dev = 0;
     KEEP_CUDA(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> g(mu);
-    if (!done.insert({fn, dev, bytes}).second) return;
+    int& cur = seen[{fn, dev}];
+    if (bytes <= cur) return;
     KEEP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    cur = bytes;
 }
 
 bool sync_debug() {
