@@ -1358,18 +1358,29 @@ __global__ void __launch_bounds__(256, 2) attn_f64_decode_kernel(AttnArgs a, dou
             *reinterpret_cast<float4*>(vs + r * DH + c) = vv;
         }
         __syncthreads();
-        // scores of (row r, key k0 + kk), r = rq, rq + 4, ...
-        for (int r = rq; r < n; r += 4) {
-            const int t = a.rows[r];
-            const int klo = a.key_lo ? a.key_lo[t] : 0;
-            const int key = k0 + kk;
-            double acc = 0.0;
-            const double* q = qs + r * DH;
+        // scores of (row r, key k0 + kk), r = rq, rq + 4, ...: two rows per pass
+        // share each widened K element (the fp32 -> fp64 convert runs on the
+        // quarter-rate XU pipe: ncu 63% XU with one convert per use)
+        for (int r = rq; r < n; r += 8) {
+            const int r2 = r + 4 < n ? r + 4 : r;
+            double acc0 = 0.0, acc1 = 0.0;
+            const double* q0 = qs + r * DH;
+            const double* q1 = qs + r2 * DH;
             const float* kr = ks + kk * G::KS;
 #pragma unroll 8
-            for (int c = 0; c < DH; ++c) acc = fma(q[c], double(kr[c]), acc);
-            const bool vis = key < hi && key <= t && key >= klo;
-            ps[r * (DKT + 1) + kk] = vis ? __dmul_rn(acc, scale) : -DBL_MAX;
+            for (int c = 0; c < DH; ++c) {
+                const double kv = kr[c];
+                acc0 = fma(q0[c], kv, acc0);
+                acc1 = fma(q1[c], kv, acc1);
+            }
+            const int key = k0 + kk;
+            for (int j = 0; j < (r2 != r ? 2 : 1); ++j) {
+                const int rr = j ? r2 : r;
+                const int t = a.rows[rr];
+                const int klo = a.key_lo ? a.key_lo[t] : 0;
+                const bool vis = key < hi && key <= t && key >= klo;
+                ps[rr * (DKT + 1) + kk] = vis ? __dmul_rn(j ? acc1 : acc0, scale) : -DBL_MAX;
+            }
         }
         __syncthreads();
         // online softmax: warp w handles rows w, w + 8
@@ -1403,16 +1414,21 @@ __global__ void __launch_bounds__(256, 2) attn_f64_decode_kernel(AttnArgs a, dou
             if (lane == 0) arow[r] = alpha;
         }
         __syncthreads();
-        // O[r][dd] = O alpha + sum_k p[r][k] V[k][dd]
+        // O[r][dd] = O alpha + sum_k p[r][k] V[k][dd]: each widened V element feeds
+        // every row of the thread
 #pragma unroll
         for (int i = 0; i < OR; ++i) {
             const int r = rh + RG * i;
-            if (r >= n) break;
-            const double* pr = ps + r * (DKT + 1);
-            double acc = o[i] * arow[r];
-#pragma unroll 8
-            for (int k = 0; k < DKT; ++k) acc = fma(pr[k], double(vs[k * DH + dd]), acc);
-            o[i] = acc;
+            if (r < n) o[i] *= arow[r];
+        }
+#pragma unroll 4
+        for (int k = 0; k < DKT; ++k) {
+            const double v = vs[k * DH + dd];
+#pragma unroll
+            for (int i = 0; i < OR; ++i) {
+                const int r = rh + RG * i;
+                if (r < n) o[i] = fma(ps[r * (DKT + 1) + k], v, o[i]);
+            }
         }
     }
     __syncthreads();
