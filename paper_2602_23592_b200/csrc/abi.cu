@@ -523,6 +523,15 @@ size_t mlp_chunk_rows(const Context& c) {
     return std::max<size_t>(32768, (size_t(4) << 30) / (es * size_t(c.f)));
 }
 
+// KEEP_LAZY_SUMMARY=0: always compute the summary a walk would read (A/B)
+bool lazy_summary_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KEEP_LAZY_SUMMARY");
+        return !(e && *e == '0');
+    }();
+    return on;
+}
+
 void ensure_layer_scratch(Context& c, Pass& p) {
     const size_t n = size_t(std::max(p.n, 1));
     // sharded: ctx rows padded to G equal row blocks (all-to-all), Wo / MLP on one block
@@ -895,6 +904,23 @@ void run_layer(Context& c, Pass& p, int l, AfterSummary&& after_summary) {
     if (p.n == 0) return;
     ensure_layer_scratch(c, p);
     layer_qkv(c, p, l);
+    if (p.walk_probe && p.with_summary) {
+        // lazy summary: when no candidate segment can receive query probability this
+        // layer, the walk's first hop adds nothing (recompute.hpp:110-121) and the
+        // summary is never read -- the layer runs its plain attention pass
+        p.d_probe.ensure(16 + sizeof(uint64_t) * 17 * size_t(c.Hl));
+        int* flag = p.d_probe.as<int>();
+        launch_walk_probe(p.q.as<float>(), static_cast<const float*>(p.kdst[l]), p.d_rows.as<int32_t>(),
+                          p.d_row_seg.as<int32_t>(), p.d_walk_cand.as<uint8_t>(), p.n, p.qlen, p.Tm, c.Hl, c.dh, c.dl,
+                          reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(p.d_probe.p) + 16), flag, c.s_main);
+        int need = 1;
+        KEEP_CUDA(cudaMemcpyAsync(&need, flag, sizeof(int), cudaMemcpyDeviceToHost, c.s_main));
+        KEEP_CUDA(cudaStreamSynchronize(c.s_main));
+        if (!need) {
+            p.with_summary = false;
+            p.walk_empty = true;
+        }
+    }
     layer_attention(c, p, l, p.q.p, c.fast ? p.ctxb.p : p.ctx.p, p.kdst[l], p.vdst[l]);
     if (c.G > 1 && p.with_summary && p.summary_global) {
         // per-rank partials (sum over this rank's heads of p / H) -> the summary
@@ -2624,6 +2650,12 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
             // summary of layer l exists, overlapping this layer's Wo + MLP
             auto launch_walk = [&] {
                 if (!walk) return;
+                if (p.walk_empty) {  // the probe's proof: the first hop adds nothing
+                    hbuf[0] = 0;
+                    hbuf[1] = 1;
+                    KEEP_CUDA(cudaEventRecord(ev_sel, c.s_sel));
+                    return;
+                }
                 upload_bytes(c.sel_cand.p, active.data(), S, c.s_sel);
                 KEEP_CUDA(cudaEventRecord(ev_sum, st));
                 KEEP_CUDA(cudaStreamWaitEvent(c.s_sel, ev_sum, 0));
@@ -2650,7 +2682,14 @@ int keep_plan_keep(void* ctx, const keep_layout* layout, const int32_t* query, i
             // Sharded: the per-rank partials are summed only when read.
             p.summary_wanted = walk || (out && out->summaries) || (l + 1 < L && budget < live && !multihop);
             p.summary_global = p.summary_wanted;
+            p.walk_probe = walk && !(out && out->summaries) && !c.fast && !c.exact && c.G == 1 && lazy_summary_enabled();
+            if (p.walk_probe) {
+                p.d_walk_cand.ensure(size_t(S));
+                upload_bytes(p.d_walk_cand.p, active.data(), S, st);
+            }
             cursor_layer(c, active.data(), launch_walk);
+            p.walk_probe = false;
+            p.walk_empty = false;
             p.summary_global = true;
             p.summary_wanted = true;
             c.gemm_ctas = kNumSMs;

@@ -1608,6 +1608,127 @@ void launch_attention_parity_dmma(const AttnArgs& a, cudaStream_t st) {
     }
 }
 
+// ------------------------------------------------------------ lazy summary probe --
+namespace {
+// Grid (key blocks of 256, heads), one key per thread, the query rows' q in
+// shared memory.  Max pass: each query row's max score over its visible keys
+// and the heads' max |k|, reduced by atomicMax on order-preserving bits.  Check
+// pass: a key of a candidate segment within 746 + margin of a query row's max
+// sets the flag (its probability may be non-zero, so the walk's first hop may
+// add a segment).  Scores are fp64 dots of the widened fp32 rows; the margin
+// 1e-12 |q| max|k| / sqrt(dh) + 1 covers any fp64 summation order.
+constexpr int PQ = 16;
+__device__ __forceinline__ uint64_t ord_bits(double x) {
+    const uint64_t b = __double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double ord_value(uint64_t o) {
+    return __longlong_as_double((o >> 63) ? (o & 0x7fffffffffffffffull) : ~o);
+}
+template <int DH, bool CHECK>
+__global__ void __launch_bounds__(256) walk_probe_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                                         const int32_t* __restrict__ rows,
+                                                         const int32_t* __restrict__ row_seg,
+                                                         const uint8_t* __restrict__ cand, int n, int qlen, int Tm,
+                                                         int H, int d, uint64_t* __restrict__ scr,
+                                                         int* __restrict__ flag) {
+    __shared__ double qs[PQ][DH];
+    __shared__ int tq[PQ];
+    __shared__ double lim[PQ];
+    __shared__ uint64_t bm[PQ + 1];
+    const int h = blockIdx.y, off = h * DH;
+    const double scale = 1.0 / sqrt(double(DH));
+    for (int e = threadIdx.x; e < qlen * DH; e += 256)
+        qs[e / DH][e % DH] = q[int64_t(n - qlen + e / DH) * d + off + e % DH];
+    if (threadIdx.x < qlen) tq[threadIdx.x] = rows[n - qlen + threadIdx.x];
+    if (!CHECK && threadIdx.x <= PQ) bm[threadIdx.x] = 0;
+    __syncthreads();
+    if (CHECK && threadIdx.x < qlen) {  // the row's threshold: max - 746 - margin
+        const int i = threadIdx.x;
+        double qq = 0.0;
+        for (int c = 0; c < DH; ++c) qq = fma(qs[i][c], qs[i][c], qq);
+        const double kmax = sqrt(ord_value(scr[int64_t(PQ) * H + h]));
+        lim[i] = ord_value(scr[int64_t(h) * PQ + i]) - 747.0 - 1e-12 * sqrt(qq) * kmax * scale;
+    }
+    if (CHECK) __syncthreads();
+    const int key = blockIdx.x * 256 + threadIdx.x;
+    const int T = tq[qlen - 1] + 1;
+    bool live = key < (CHECK ? min(T, Tm) : T);
+    if (CHECK && live) {
+        const int sg = row_seg[key];
+        live = sg >= 0 && cand[sg];
+    }
+    double s[PQ];
+#pragma unroll
+    for (int i = 0; i < PQ; ++i) s[i] = 0.0;
+    double kn = 0.0;
+    if (live) {
+        const float4* kr = reinterpret_cast<const float4*>(k + int64_t(key) * d + off);
+#pragma unroll 4
+        for (int c4 = 0; c4 < DH / 4; ++c4) {
+            const float4 v = kr[c4];
+            const double kv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                kn = fma(kv[j], kv[j], kn);
+#pragma unroll
+                for (int i = 0; i < PQ; ++i)
+                    if (i < qlen) s[i] = fma(qs[i][4 * c4 + j], kv[j], s[i]);
+            }
+        }
+    }
+    if (!CHECK) {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int i = 0; i < PQ; ++i) {
+            if (i >= qlen) break;
+            double m = (live && key <= tq[i]) ? s[i] * scale : -DBL_MAX;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0 && m != -DBL_MAX) atomicMax(reinterpret_cast<unsigned long long*>(&bm[i]), ord_bits(m));
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) kn = fmax(kn, __shfl_xor_sync(0xffffffffu, kn, o));
+        if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&bm[PQ]), ord_bits(kn));
+        __syncthreads();
+        if (threadIdx.x < qlen && bm[threadIdx.x])
+            atomicMax(reinterpret_cast<unsigned long long*>(scr + int64_t(h) * PQ + threadIdx.x), bm[threadIdx.x]);
+        if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(scr + int64_t(PQ) * H + h), bm[PQ]);
+        return;
+    }
+    bool need = false;
+#pragma unroll
+    for (int i = 0; i < PQ; ++i)
+        if (i < qlen && live && key <= tq[i] && !(s[i] * scale < lim[i])) need = true;
+    if (__any_sync(0xffffffffu, need) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+}  // namespace
+
+void launch_walk_probe(const float* q, const float* k, const int32_t* rows, const int32_t* row_seg,
+                       const uint8_t* cand, int n, int qlen, int Tm, int H, int dh, int d, uint64_t* scratch,
+                       int* flag, cudaStream_t st) {
+    if (qlen < 1 || qlen > PQ || n < qlen || (dh != 64 && dh != 128)) {  // no proof: the summary is computed
+        const int one = 1;
+        KEEP_CUDA(cudaMemcpyAsync(flag, &one, sizeof(int), cudaMemcpyHostToDevice, st));
+        KEEP_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    KEEP_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    KEEP_CUDA(cudaMemsetAsync(scratch, 0, sizeof(uint64_t) * size_t(PQ + 1) * H, st));
+    int tmax = 0;  // the last query row's position bounds the keys
+    KEEP_CUDA(cudaMemcpyAsync(&tmax, rows + n - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    KEEP_CUDA(cudaStreamSynchronize(st));
+    const dim3 grid{unsigned(ceil_div(tmax + 1, 256)), unsigned(H)};
+    if (dh == 128) {
+        walk_probe_kernel<128, false><<<grid, 256, 0, st>>>(q, k, rows, row_seg, cand, n, qlen, Tm, H, d, scratch, flag);
+        walk_probe_kernel<128, true><<<grid, 256, 0, st>>>(q, k, rows, row_seg, cand, n, qlen, Tm, H, d, scratch, flag);
+    } else {
+        walk_probe_kernel<64, false><<<grid, 256, 0, st>>>(q, k, rows, row_seg, cand, n, qlen, Tm, H, d, scratch, flag);
+        walk_probe_kernel<64, true><<<grid, 256, 0, st>>>(q, k, rows, row_seg, cand, n, qlen, Tm, H, d, scratch, flag);
+    }
+    KEEP_LAUNCH_CHECK();
+}
+
 }  // namespace keep_b200
 
 // Test hook: y[i] = exp_f64(x[i]) on device pointers (tests/test_gpu_exp.py).

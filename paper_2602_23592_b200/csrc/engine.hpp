@@ -198,6 +198,10 @@ struct Pass {
     std::vector<int32_t> seg_start, seg_len, row_seg;  // host copies
     std::vector<int32_t> key_lo_h;
     DevBuf d_tokens, d_row_seg, d_key_lo, d_seg_len, d_seg_start;
+    // lazy summary (plan_keep, PARITY): the walk's candidates on the device, the
+    // probe's scratch, and whether the probe proved the walk adds nothing this layer
+    DevBuf d_walk_cand, d_probe;
+    bool walk_probe = false, walk_empty = false;
     DevBuf ebin;                  // PARITY fused bins: [H x n x S] fp64 per-head segment sums
     DevBuf tp_part, tp_h;         // sharded few-row layers: fp64 partial sums [n x d], this rank's MLP slice [n x f/G]
     // compact state

@@ -54,6 +54,15 @@ void launch_summary_reduce(const TB* rowbin, int S, const int32_t* seg_cbeg, con
                            cudaStream_t st);
 
 // K7: converge on the device (recompute.hpp:86-138).
+// Lazy summary probe (PARITY): flag[0] = 1 unless every candidate segment's keys
+// provably get probability 0 from every query row in every head (s - max below
+// -746 by more than the fp64 error bound of the scores), i.e. unless the
+// walk's first hop might add a segment (recompute.hpp:110-121).  q: the compact
+// rows [n x d] (the query rows are the last qlen), k: the layer's merged keys;
+// scratch: (qlen + 1) x H uint64.
+void launch_walk_probe(const float* q, const float* k, const int32_t* rows, const int32_t* row_seg,
+                       const uint8_t* cand, int n, int qlen, int Tm, int H, int dh, int d, uint64_t* scratch,
+                       int* flag, cudaStream_t st);
 void launch_single_hop(const double* qts, const uint8_t* live, int S, int64_t budget, uint8_t* next,
                        cudaStream_t st);
 void launch_select(int S, const double* qts, const double* sts, int64_t budget,
