@@ -529,13 +529,6 @@ __device__ __forceinline__ uint32_t residue_word(const OzInt& X, const OzCrt& c,
     const int q = __double2loint(fma(X.b - kM52, c.rcpd[i], kM52));
     return uint32_t(lo - q * c.mi[i]);
 }
-// the same residue from X alone, in fp64 (fewer live registers: the column split)
-__device__ __forceinline__ int8_t residue(double X, const OzCrt& c, int i) {
-    const double q = fma(X, c.rcpd[i], kM52) - kM52;
-    double r = fma(-q, c.md[i], X);
-    if (i == 0) r = r >= 128.0 ? r - 256.0 : r;
-    return int8_t(__double2loint(r + kM52) & 0xff);
-}
 
 // A rows -> out[i][m][0..Kp) int8 residues of A' = rint(A 2^ea) + ea[m]; one warp per row.
 __global__ void oz_split_rows_kernel(const float* __restrict__ A, int64_t lda, int M, int K, int Kp, int bits,
@@ -579,31 +572,43 @@ __global__ void oz_colmax_kernel(const float* __restrict__ B, int64_t ldb, int K
 
 // B [K x N] row-major -> out[i][n][0..Kp) int8 residues of B' = rint(B 2^eb)
 // (transposed, K-major) + eb[n].  Tile 128 k x 32 n through shared memory,
-// eight moduli at a time.
+// eight moduli at a time; a thread holds 4 consecutive k of its column (4
+// groups), so one modulus' residues leave as four 4-byte smem stores.
 __global__ void __launch_bounds__(256) oz_split_cols_kernel(const float* __restrict__ B, int64_t ldb, int K, int N,
                                                             int Kp, int bits, int Np,
                                                             const __grid_constant__ OzCrt crt,
                                                             const unsigned* __restrict__ cmax,
                                                             int8_t* __restrict__ out, int* __restrict__ eb) {
-    __shared__ int8_t sd[8][32][128 + 16];
+    __shared__ __align__(16) int8_t sd[8][32][128 + 16];
     const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 128;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
     const int n = n0 + tx;
     const int e = n < N ? scale_exp(__uint_as_float(cmax[n]), bits) : 0;
     if (blockIdx.y == 0 && ty == 0 && n < N) eb[n] = e;
     const double pw = ldexp(1.0, e);
-    double X[16];
+    OzInt X[16];  // [g][j]: k = k0 + 32 g + 4 ty + j
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-        const int k = k0 + ty + 8 * q;
-        X[q] = rint(double((k < K && n < N) ? B[int64_t(k) * ldb + n] : 0.f) * pw);
+        const int k = k0 + 32 * (q >> 2) + 4 * ty + (q & 3);
+        X[q] = oz_int((k < K && n < N) ? B[int64_t(k) * ldb + n] : 0.f, pw);
     }
     const size_t plane = size_t(Np) * Kp;
     for (int g0 = 0; g0 < crt.n; g0 += 8) {
         const int gn = min(8, crt.n - g0);
-        for (int i = 0; i < gn; ++i)
+        for (int i = 0; i < gn; ++i) {
 #pragma unroll
-            for (int q = 0; q < 16; ++q) sd[i][tx][ty + 8 * q] = residue(X[q], crt, g0 + i);
+            for (int g = 0; g < 4; ++g) {
+                uint32_t w[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    OzInt x = X[4 * g + j];
+                    asm("" : "+d"(x.b));  // recomputed per modulus, not hoisted into more registers
+                    w[j] = residue_word(x, crt, g0 + i);
+                }
+                *reinterpret_cast<uint32_t*>(&sd[i][tx][32 * g + 4 * ty]) =
+                    __byte_perm(__byte_perm(w[0], w[1], 0x0040), __byte_perm(w[2], w[3], 0x0040), 0x5410);
+            }
+        }
         __syncthreads();
         // write rows (i, n): 128 contiguous bytes = 8 x 16 B
         for (int idx = threadIdx.x; idx < gn * 32 * 8; idx += 256) {
