@@ -11,6 +11,7 @@ layer-1 plan.  Both PARITY modes must reproduce the plan, the walk order and
 the hop counts bit-exactly; summaries and hidden states within the fp64
 re-ordering tolerances of tests/test_gpu_parity.py.
 """
+import hashlib
 import json
 import os
 
@@ -29,10 +30,19 @@ def rel(a, b):
     return float(np.max(np.abs(a.astype(np.float64) - b.astype(np.float64)))) / max(float(np.max(np.abs(b))), 1e-300)
 
 
+SHA = GOLD + ".sha256"  # recorded when the generated golden is adopted
+
+
 @pytest.fixture(scope="module")
 def gold():
     if not os.path.exists(GOLD):
         pytest.skip("C3-width golden not generated (tests/golden/make_c3_golden.py)")
+    if not os.path.exists(SHA):
+        pytest.skip("C3-width golden generated but not adopted (no recorded sha256)")
+    with open(GOLD, "rb") as f:
+        digest = hashlib.sha256(f.read()).hexdigest()
+    with open(SHA) as f:
+        assert digest == f.read().split()[0], "c3_width_golden.npz differs from its recorded sha256"
     g = np.load(GOLD)
     return g, json.loads(bytes(g["meta"]).decode())
 
