@@ -551,13 +551,15 @@ def run_ours(args, cfg, rank, world, dist):
         fp64_peak = extra.get("fp64_dmma_tflops") or 37.0
         a_ach = a_fl / (a_ms / 1e3) / 1e12 if a_ms > 0 else 0.0
         attn_roof = {"kernel": "attn_dmma16_flash_kernel (K5 flash pass, mma.m16n8k16.f64) + attn_dmma_ws_kernel "
-                               "(summary layers: max pass, context pass with the bins fused as E.Z)", "bound": "tensor",
+                               "(summary layers: context pass with the bins fused as E.Z, one pass when the "
+                               "Cauchy-Schwarz bound admits it)", "bound": "tensor",
                      "achieved": a_ach, "peak": fp64_peak, "unit": "TFLOP/s (fp64)", "frac": a_ach / fp64_peak,
                      "traffic": traffic.get("attn_dmma16_flash_kernel"),
                      "traffic_launches": DETAIL.get("attn_dmma16_flash_kernel"),
                      "peak_source": "measured fp64 DMMA (tools/micro/fp64_peak.cu)",
                      "note": "algorithmic FLOPs 4*d*sum(t+1) (QK^T + PV once) over the whole attention phase; "
-                             "summary layers add a max pass (Q.K^T once more); traffic = ncu DRAM bytes of one C3 "
+                             "a summary layer outside the one-pass bound adds a max pass (Q.K^T once more); "
+                             "traffic = ncu DRAM bytes of one C3 "
                              "layer-1 flash launch (profiles/r02_ncu_dmma16_full.csv)"}
         roofs = [gemm_roof, attn_roof]
     else:
